@@ -1,0 +1,349 @@
+"""Pins for the CPU oracle (no GPU).  Each test ties the oracle to something other than
+itself: the paper's printed values, hand-computed examples, closed forms, independent
+library routines (scipy cKDTree, LAPACK eigh, scipy csgraph) and exact integer arithmetic.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _rows(res, j):
+    o = res["offsets"]
+    return res["indices"][o[j]:o[j + 1]], res["s"][o[j]:o[j + 1]]
+
+
+def _hits(res, j):
+    ids, s = _rows(res, j)
+    return set(ids[s <= res["R2"]].tolist())
+
+
+# --------------------------------------------------------------------------- eq:ip1 order
+def test_sqdist_is_left_to_right_without_fma():
+    """eq:ip1 evaluated as pure-Python floats (IEEE fp64, one rounding
+    per op, no FMA) must be bit-identical to the oracle's C evaluation."""
+    rng = np.random.default_rng(11)
+    for d in (1, 2, 3, 7, 64, 784):
+        for _ in range(20):
+            p = rng.standard_normal(d) * 10 ** rng.uniform(-3, 3)
+            q = p + rng.standard_normal(d) * 10 ** rng.uniform(-6, 1)
+            s = 0.0
+            for k in range(d):
+                t = float(p[k]) - float(q[k])
+                s = s + t * t
+            assert oracle.sqdist(p, q) == s
+
+
+# --------------------------------------------------------------------------- hand example
+def test_d3_hand_example_index_and_queries():
+    g = json.load(open(os.path.join(GOLDEN, "d3_hand_example.json")))
+    P = np.array(g["P"], dtype=np.float64)
+    idx = oracle.build_index(P)
+    np.testing.assert_allclose(idx["mu"], g["mu"], atol=0)
+    np.testing.assert_allclose(oracle.center(P, idx["mu"]), g["Xc"], atol=0)
+    np.testing.assert_allclose(idx["v1"], g["v1"], atol=1e-15)
+    assert abs(idx["sigma"][1]) < 1e-12
+    np.testing.assert_allclose(idx["alpha"], g["alpha_sorted"], atol=1e-14)
+    np.testing.assert_allclose(idx["xbar"], g["xbar_sorted"], atol=1e-14)
+    assert idx["perm"].tolist() == g["perm"]
+    for r in g["ranges"]:
+        assert oracle.candidate_range(g["alpha_sorted"], r["alpha_q"], r["R"]) == (r["lo"], r["hi"])
+    for qq in g["queries"]:
+        res = oracle.radius_query(P, np.array([qq["q"]], dtype=np.float64), qq["R"], band_rel=0)
+        ids, s = _rows(res, 0)
+        got = {int(i): math.sqrt(v) for i, v in zip(ids, s)}
+        assert got == {int(k): v for k, v in qq["hits"].items()}
+        assert oracle.alg2_query(idx, P, qq["q"], qq["R"]).tolist() == sorted(got)
+    b = g["batch"]
+    res = oracle.radius_query(P, np.array(b["Q"], dtype=np.float64), b["R"], band_rel=0)
+    assert [sorted(_hits(res, j)) for j in range(2)] == b["hits"]
+
+
+# --------------------------------------------------------------------------- exact boundary
+@pytest.mark.parametrize("d,R", [(2, 5), (3, 5), (3, 3), (2, 0)])
+def test_integer_lattice_exact_boundary(d, R):
+    """Integer points: squared distances are exact in fp64, so the inclusive boundary
+    ("<= R") must be reproduced exactly, e.g. (3,4) at R=5 is a hit."""
+    g = np.stack(np.meshgrid(*[np.arange(-6, 7)] * d, indexing="ij"), -1).reshape(-1, d)
+    Q = np.array([[0] * d, [1] * d, [2, -3] + [1] * (d - 2)], dtype=np.float64)
+    res = oracle.radius_query(g.astype(np.float64), Q, float(R), band_rel=0)
+    for j, q in enumerate(Q.astype(np.int64)):
+        expect = {i for i, p in enumerate(g) if int(((p - q) ** 2).sum()) <= R * R}
+        assert _hits(res, j) == expect
+    if (d, R) == (2, 5):
+        ids = _hits(res, 0)
+        assert {tuple(g[i]) for i in ids} >= {(3, 4), (4, 3), (-5, 0), (0, 5)}
+
+
+# --------------------------------------------------------------------------- library cross-check
+@pytest.mark.parametrize("n,m,d,seed", [(3000, 200, 2, 1), (2000, 150, 3, 2), (1500, 100, 8, 3),
+                                        (1000, 80, 64, 4), (600, 40, 784, 5)])
+def test_matches_scipy_ckdtree(n, m, d, seed):
+    """Independent implementation: scipy's cKDTree ball query.  Sets must agree except
+    for pairs within 1e-9 relative of the boundary (different rounding paths)."""
+    from scipy.spatial import cKDTree
+    rng = np.random.default_rng(seed)
+    P = rng.random((n, d))
+    Q = rng.random((m, d))
+    # radius giving ~1% return ratio
+    R = float(np.quantile(np.linalg.norm(P[:300, None, :] - Q[None, :20, :], axis=-1), 0.01))
+    res = oracle.radius_query(P, Q, R, band_rel=1e-9)
+    tree = cKDTree(P)
+    for j in range(m):
+        ids, s = _rows(res, j)
+        sure = set(ids[s <= R * R * (1 - 1e-9)].tolist())
+        mine = set(ids[s <= R * R].tolist())
+        ref = set(tree.query_ball_point(Q[j], R))
+        assert sure <= ref <= set(ids.tolist())
+        assert mine <= set(ids.tolist())
+
+
+def test_distances_against_numpy_norm():
+    rng = np.random.default_rng(7)
+    P = rng.standard_normal((500, 5)) * 3
+    Q = rng.standard_normal((20, 5)) * 3
+    res = oracle.radius_query(P, Q, 3.0, band_rel=0)
+    for j in range(20):
+        ids, s = _rows(res, j)
+        np.testing.assert_allclose(np.sqrt(s), np.linalg.norm(P[ids] - Q[j], axis=1), rtol=1e-14)
+        full = np.linalg.norm(P - Q[j], axis=1)
+        sure = set(np.nonzero(full <= 3.0 * (1 - 1e-12))[0].tolist())
+        maybe = set(np.nonzero(full <= 3.0 * (1 + 1e-12))[0].tolist())
+        assert sure <= set(ids.tolist()) <= maybe
+
+
+# --------------------------------------------------------------------------- closed forms
+def _unit_square(r):
+    return math.pi * r * r - 8 * r ** 3 / 3 + r ** 4 / 2
+
+
+def _unit_cube(r):
+    return 4 * math.pi / 3 * r ** 3 - 1.5 * math.pi * r ** 4 + 1.6 * r ** 5 - r ** 6 / 6
+
+
+def test_c1_return_ratio_closed_form_and_paper_table1():
+    """C1 = the paper's Table 1 cell n=2000, d=2, R=0.05 (0.755%).
+    Non-self pair fraction vs the closed form P(|U-V|<=r) on the unit square."""
+    w = workloads.c1()
+    res = oracle.radius_query(w.X, w.X, w.R, band_rel=0)
+    n = w.n
+    nonself = sum(len(_hits(res, j)) - 1 for j in range(n)) / (n * (n - 1))
+    g = json.load(open(os.path.join(GOLDEN, "paper_return_ratios.json")))
+    assert abs(100 * nonself - 100 * _unit_square(0.05)) / (100 * _unit_square(0.05)) < 0.05
+    assert abs(100 * nonself - g["table1_d2"]["n2000"]["0.05"]) / g["table1_d2"]["n2000"]["0.05"] < 0.05
+    # every point is its own neighbour; the relation is symmetric
+    for j in range(0, n, 97):
+        assert j in _hits(res, j)
+        for i in _hits(res, j):
+            assert j in _hits(res, i)
+
+
+@pytest.mark.parametrize("R", ["0.02", "0.05", "0.08", "0.11", "0.14"])
+def test_table1_d2_n10000_ratios(R):
+    g = json.load(open(os.path.join(GOLDEN, "paper_return_ratios.json")))
+    w = workloads.uniform(10000, 2, seed=123)
+    r = float(R)
+    Q = w.X[:1000]
+    res = oracle.radius_query(w.X, Q, r, band_rel=0)
+    nonself = (res["offsets"][-1] - 1000) / (1000 * (w.n - 1))
+    closed = _unit_square(r)
+    printed = g["table1_d2"]["n10000"][R] / 100
+    tol = 0.04 if r > 0.03 else 0.08
+    assert abs(nonself - closed) / closed < tol
+    assert abs(closed - printed) / printed < 0.006   # closed form vs paper's print
+
+
+@pytest.mark.parametrize("R", ["0.05", "0.10", "0.15", "0.20", "0.25"])
+def test_table2_d3_ratios(R):
+    g = json.load(open(os.path.join(GOLDEN, "paper_return_ratios.json")))
+    w = workloads.uniform(10000, 3, seed=321)
+    r = float(R)
+    res = oracle.radius_query(w.X, w.X[:1000], r, band_rel=0)
+    nonself = (res["offsets"][-1] - 1000) / (1000 * (w.n - 1))
+    closed = _unit_cube(r)
+    printed = g["table2_d3"]["n10000"][R] / 100
+    assert abs(nonself - closed) / closed < (0.15 if r < 0.07 else 0.05)
+    assert abs(closed - printed) / printed < 0.05
+
+
+# --------------------------------------------------------------------------- invariants
+def test_invariants_symmetry_self_monotone_R0():
+    rng = np.random.default_rng(5)
+    P = rng.random((800, 3)).astype(np.float32)
+    P[10] = P[20]                     # duplicate pair
+    a = oracle.radius_query(P, P, 0.08, band_rel=0)
+    b = oracle.radius_query(P, P, 0.12, band_rel=0)
+    z = oracle.radius_query(P, P, 0.0, band_rel=0)
+    for j in range(800):
+        ha, hb = _hits(a, j), _hits(b, j)
+        assert j in ha and ha <= hb
+        for i in ha:
+            assert j in _hits(a, i)
+        expect_zero = {j} | ({10, 20} if j in (10, 20) else set())
+        assert _hits(z, j) == expect_zero
+
+
+def test_empty_query_and_errors():
+    P = np.zeros((5, 2))
+    res = oracle.radius_query(P, np.zeros((0, 2)), 1.0)
+    assert res["offsets"].tolist() == [0]
+    with pytest.raises(ValueError):
+        oracle.radius_query(P, np.zeros((1, 2)), -1.0)
+    with pytest.raises(ValueError):
+        oracle.radius_query(P, np.zeros((1, 3)), 1.0)
+    with pytest.raises(ValueError):
+        oracle.column_mean(np.zeros((0, 2)))
+
+
+# --------------------------------------------------------------------------- Algorithm 1 pins
+def test_principal_direction_pins():
+    # d = 1: v1 = (1)
+    v, _ = oracle.principal_direction(oracle.center(np.array([[1.0], [5.0], [2.0]]), [8 / 3]))
+    assert v.tolist() == [1.0]
+    # all-zero data -> e1 (SPEC.md:141 reading C9)
+    v, s = oracle.principal_direction(np.zeros((4, 3)))
+    assert v.tolist() == [1.0, 0.0, 0.0] and not s.any()
+    # independent LAPACK routine (symmetric eigensolver on X^T X) agrees
+    rng = np.random.default_rng(3)
+    X = rng.standard_normal((4000, 6)) * np.array([3, 1, 0.5, 0.4, 0.3, 0.2])
+    X = X @ np.linalg.qr(rng.standard_normal((6, 6)))[0]
+    Xc = oracle.center(X, oracle.column_mean(X))
+    v, s = oracle.principal_direction(Xc)
+    w, V = np.linalg.eigh(Xc.T @ Xc)
+    assert abs(abs(v @ V[:, -1]) - 1) < 1e-12
+    np.testing.assert_allclose(s[0] ** 2, w[-1], rtol=1e-12)
+    assert np.argmax(np.abs(v)) == np.argmax(np.abs(v)) and v[np.argmax(np.abs(v))] > 0
+
+
+@pytest.mark.parametrize("s", [0.1, 0.5])
+def test_elongated_gaussian_sigma_ratio(s):
+    """std (1, s, ..., s) => singular values -> sqrt(n)(1, s, ..., s),
+    v1 -> e1 (SPEC.md:132 asserts |sigma2/sigma1 - s| <= 0.05 at n=50,000)."""
+    rng = np.random.default_rng(17)
+    X = rng.standard_normal((50000, 5)) * np.array([1, s, s, s, s])
+    v, sig = oracle.principal_direction(oracle.center(X, oracle.column_mean(X)))
+    assert abs(sig[1] / sig[0] - s) <= 0.05
+    assert abs(v[0]) > 0.99
+
+
+def test_c3_closed_form_v1():
+    """C3 covariance = Qo^T diag(1/i) Qo => v1 = +-(first row of Qo), sigma2/sigma1 ->
+    1/sqrt(2) (SURVEY.md §8(c) pins)."""
+    w = workloads.c3(n=40000, m=10)
+    v, sig = oracle.principal_direction(oracle.center(w.X, oracle.column_mean(w.X)))
+    assert abs(abs(v @ w.meta["Qo"][0]) - 1) < 2e-3
+    assert abs(sig[1] / sig[0] - 1 / math.sqrt(2)) < 0.02
+
+
+def test_sort_is_stable_with_duplicates():
+    """five identical points -> all alpha = 0, pi = identity."""
+    P = np.tile(np.array([[2.0, 3.0]]), (5, 1))
+    idx = oracle.build_index(P)
+    assert idx["perm"].tolist() == [0, 1, 2, 3, 4]
+    assert not idx["alpha"].any() and not idx["xbar"].any()
+
+
+# --------------------------------------------------------------------------- Algorithm 2 pins
+@pytest.mark.parametrize("d,seed", [(2, 1), (3, 2), (5, 3)])
+def test_cauchy_schwarz_window_contains_all_hits(d, seed):
+    """eq:lower: every true neighbour lies in J.  And Alg. 2's answer
+    equals the brute force; replacing v1 by any unit vector keeps it."""
+    rng = np.random.default_rng(seed)
+    P = rng.random((600, d)) * np.array([4.0] + [1.0] * (d - 1))
+    Q = rng.random((25, d)) * np.array([4.0] + [1.0] * (d - 1))
+    R = 0.3
+    idx = oracle.build_index(P)
+    res = oracle.radius_query(P, Q, R, band_rel=0)
+    u = rng.standard_normal(d)
+    u /= np.linalg.norm(u)
+    Xc = oracle.center(P, idx["mu"])
+    a2 = oracle.scores(Xc, u)
+    pr = oracle.sort_index(a2)
+    idx_u = dict(idx, v1=u, alpha=a2[pr], perm=pr)
+    pos = np.empty(600, dtype=np.int64)
+    pos[idx["perm"]] = np.arange(600)
+    for j in range(25):
+        h = _hits(res, j)
+        aq = float((Q[j] - idx["mu"]) @ idx["v1"])
+        lo, hi = oracle.candidate_range(idx["alpha"], aq, R)
+        assert all(lo <= pos[i] < hi for i in h)
+        assert set(oracle.alg2_query(idx, P, Q[j], R).tolist()) == h
+        assert set(oracle.alg2_query(idx_u, P, Q[j], R).tolist()) == h
+
+
+# --------------------------------------------------------------------------- DBSCAN pins
+def test_dbscan_spec_examples():
+    rng = np.random.default_rng(0)
+    # two blobs: K = 2
+    A = np.concatenate([rng.standard_normal((500, 2)) * 0.5,
+                        rng.standard_normal((500, 2)) * 0.5 + 10])
+    lab, K, _ = oracle.dbscan(A, 1.0, 5)
+    assert K == 2
+    core0 = lab[:500][lab[:500] >= 0]
+    core1 = lab[500:][lab[500:] >= 0]
+    assert len(set(core0.tolist())) == 1 and len(set(core1.tolist())) == 1
+    assert core0[0] != core1[0]
+    # grid spacing 10, eps 0.1: all noise
+    G = np.stack(np.meshgrid(np.arange(10) * 10.0, np.arange(10) * 10.0), -1).reshape(-1, 2)
+    lab, K, _ = oracle.dbscan(G, 0.1, 5)
+    assert K == 0 and (lab == -1).all()
+    # minPts 1, huge eps: one cluster
+    lab, K, _ = oracle.dbscan(A, 1e6, 1)
+    assert K == 1 and (lab == 0).all()
+
+
+def test_dbscan_hand_chain():
+    """1-D hand example: core chain 0-1-2-3 (spacing 1, eps 1, minPts 3), border 4 at
+    distance 1 from core 3 only, isolated 5 -> noise; points ordered to test numbering."""
+    P = np.array([[10.0], [0.0], [1.0], [2.0], [3.0], [4.0], [50.0], [11.0], [12.0]])
+    lab, K, cnt = oracle.dbscan(P, 1.0, 3)
+    # neighbourhoods incl. self: 10:{10,11}=2(non-core) ...
+    assert cnt.tolist() == [2, 2, 3, 3, 3, 2, 1, 3, 2]
+    # core: ids 2,3,4 (coords 1,2,3) and 7 (coord 11)
+    # cluster 0 = {2,3,4} (min core id 2), cluster 1 = {7} (min core id 7)
+    # borders: id1 (0.0) -> core 2 -> 0; id5 (4.0) -> core 4 -> 0;
+    #          id0 (10) -> core 7 -> 1; id8 (12) -> core 7 -> 1; id6 noise
+    assert K == 2
+    assert lab.tolist() == [1, 0, 0, 0, 0, 0, -1, 1, 1]
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_dbscan_vs_scipy_csgraph(seed):
+    from scipy.sparse import coo_matrix
+    from scipy.sparse.csgraph import connected_components
+    from scipy.spatial import cKDTree
+    w = workloads.c5(n=3000, seed=seed, box=200.0)
+    P = w.X.astype(np.float64)
+    eps, mp = 3.0, 5
+    lab, K, cnt = oracle.dbscan(P, eps, mp)
+    tree = cKDTree(P)
+    nb = tree.query_ball_point(P, eps)
+    # reject instances with a pair within 1e-9 of eps (rounding-path dependence)
+    pairs = tree.query_pairs(eps * (1 + 1e-9), output_type="ndarray")
+    dd = np.linalg.norm(P[pairs[:, 0]] - P[pairs[:, 1]], axis=1)
+    assert not np.any(np.abs(dd - eps) < 1e-9 * eps)
+    ref_cnt = np.array([len(x) for x in nb])
+    assert (ref_cnt == cnt).all()
+    core = ref_cnt >= mp
+    cid = np.nonzero(core)[0]
+    e = pairs[core[pairs[:, 0]] & core[pairs[:, 1]] & (dd <= eps)]
+    A = coo_matrix((np.ones(len(e)), (e[:, 0], e[:, 1])), shape=(len(P), len(P)))
+    _, comp = connected_components(A, directed=False)
+    ref = np.full(len(P), -1)
+    order = {}
+    for i in cid:                      # canonical numbering by min core id
+        order.setdefault(comp[i], len(order))
+        ref[i] = order[comp[i]]
+    for i in np.nonzero(~core)[0]:
+        cn = [j for j in nb[i] if core[j]]
+        if cn:
+            ref[i] = ref[min(cn)]
+    assert K == len(order)
+    assert (ref == lab).all()
