@@ -1,0 +1,352 @@
+"""bench.py -- SNN (arXiv 2212.07679) hot path on B200: index build + batched radius
+queries, BASELINE.json metric "radius queries/s at n=1M; index build ms; % of roofline".
+
+A step = one pass of the whole hot path over one batch: snn_build (Algorithm 1: mean,
+power-iteration v1, keys, radix sort, gather + norms) + snn_query_self (Algorithm 2 for
+all n points: windows, count pass, scan, write pass into CSR) + freeing both, on
+BASELINE.json configs[1] (n = 1,000,000, d = 3, fp32, self-query, R from
+workloads/radii.json).  Inputs are resident in HBM; L2 (126 MB) is flushed by writing a
+256 MB buffer before every timed step.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl snn|reference] [--config c2]
+
+Multi-GPU (torchrun, one rank per GPU): every rank runs an independent replica of the
+workload (weak scaling, no data-path collective); timings are the
+max over ranks.  ``--impl reference`` times the CPU oracle (fp64 brute force) on a bounded
+sample of the same workload, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads  # noqa: E402
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+TRAFFIC_PATH = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+METRIC = "radius queries/s at n=1M (index build + self-queries)"
+
+
+# ----------------------------------------------------------------------------- helpers
+def load_peaks():
+    try:
+        return json.load(open(PEAKS_PATH)), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def fp32_alu_peak_tflops(sm_mhz: float, sms: int = 148) -> float:
+    """FP32 FMA issue peak: SMs x 128 FP32 lanes x 2 flop x clock (B200_PROFILING.md
+    table: 148 SMs, 1965 MHz max; 4 SMSPs x 32 lanes per SM)."""
+    return sms * 128 * 2 * sm_mhz * 1e6 / 1e12
+
+
+class ClockSampler:
+    QUERY = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.p = None
+        self.path = os.path.join("/tmp", f"snn_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.QUERY}",
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self, t0: float, t1: float):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.close()
+        rows = []
+        import datetime
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 10:
+                continue
+            try:
+                ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except ValueError:
+                continue
+            rows.append((ts, parts))
+        inwin = [p for ts, p in rows if t0 - 0.05 <= ts <= t1 + 0.05] or [p for _, p in rows[-3:]]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        sm, smax = [], []
+        for p in inwin:
+            try:
+                sm.append(float(p[2]))
+                smax.append(float(p[3]))
+            except ValueError:
+                pass
+            for k, nm in enumerate(names):
+                if p[6 + k].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(inwin)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def max_over_ranks(x: float, world: int, device=None) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def weak_units(per_rank_units: int, world: int) -> int:
+    """Whole-job units for weak scaling: every rank processes its own replica."""
+    return per_rank_units * world
+
+
+def workload(name: str):
+    w = workloads.CONFIGS[name]()
+    if w.R is None:
+        raise SystemExit(f"radius for {name} missing: run scripts/select_radii.py")
+    return w
+
+
+# ----------------------------------------------------------------------------- oracle
+def oracle_sample_rate(w, target_s: float):
+    """Oracle (fp64 brute force, host cores) on a bounded sample of the workload's
+    queries: returns (queries/s, sample size, seconds, threads)."""
+    import oracle
+    Q = w.queries
+    k = min(64, w.m)
+    t = time.perf_counter()
+    oracle.radius_query(w.X, Q[:k], w.R)
+    dt = time.perf_counter() - t
+    k2 = int(min(w.m, max(k, k * target_s / max(dt, 1e-6))))
+    t = time.perf_counter()
+    oracle.radius_query(w.X, Q[:k2], w.R)
+    dt2 = time.perf_counter() - t
+    return k2 / dt2, k2, dt2, oracle.num_threads()
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle
+    w = workload(args.config)
+    # per-step sample sized so the whole --steps/--warmup run ends in ~1-2 minutes
+    rate, _, _, threads = oracle_sample_rate(w, 2.0)
+    per_step = int(max(8, min(w.m, rate * 60.0 / max(1, args.steps + args.warmup))))
+    Q = w.queries
+    for i in range(args.warmup):
+        oracle.radius_query(w.X, Q[:per_step], w.R)
+    t = time.perf_counter()
+    for i in range(args.steps):
+        s0 = (i * per_step) % max(1, w.m - per_step + 1)
+        oracle.radius_query(w.X, Q[s0:s0 + per_step], w.R)
+    dt = time.perf_counter() - t
+    value = per_step * args.steps / dt
+    sample = (f"{per_step} of {w.m} queries per step against all {w.n} points "
+              f"(fp64 brute force, no index build)")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "queries/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_block(w, args),
+            "cpu_baseline": {"value": value, "unit": "queries/s", "cores": threads,
+                             "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_block(w, args):
+    return {"workload": f"{args.config}: n={w.n}, d={w.d}, "
+                        f"{'self-query' if w.Q is None else f'm={w.m} queries'}, R={w.R:.6g}",
+            "n": w.n, "m": w.m, "d": w.d, "R": w.R, "input_dtype": str(w.X.dtype),
+            "l2": "flushed (256 MB write) before every timed step",
+            "parallelism": f"replicas x{args.gpus} (weak scaling)"}
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def run_gpu(args):
+    import torch
+    world, rank, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+    import paper_2212_07679_b200 as snn
+    snn.load_library()
+    w = workload(args.config)
+    X = torch.from_numpy(w.X).to(dev)
+    Qd = None if w.Q is None else torch.from_numpy(w.Q).to(dev)
+    R = w.R
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+
+    def step():
+        idx = snn.snn_build(X)
+        r = snn.snn_query_self(idx, R) if Qd is None else snn.snn_query_radius(idx, Qd, R)
+        nnz = snn.snn_result_csr(r)["nnz"]
+        snn.snn_result_free(r)
+        snn.snn_free(idx)
+        return nnz
+
+    for _ in range(max(3, args.warmup)):
+        nnz = step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    snn.snn_profile_enable(True)
+    l0 = snn.snn_launch_count()
+    clk = ClockSampler(torch.cuda.current_device() if world == 1 else local)
+    clk.start()
+    time.sleep(0.3)
+    t_host0 = time.time()
+    times = []
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        step()
+        e1.record()
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+    t_host1 = time.time()
+    clocks = clk.stop(t_host0, t_host1)
+    launches = snn.snn_launch_count() - l0
+    prof = {f: snn.snn_profile_read(f) for f in ("build", "window_count", "window_write", "query")}
+    snn.snn_profile_enable(False)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    total_ms = max_over_ranks(sum(times), world, dev)
+    units = weak_units(w.m * args.steps, world)
+    value = units / (total_ms / 1e3)
+
+    # ---- end to end through the C ABI with HOST buffers (copies inside the timed region)
+    Xh = torch.from_numpy(w.X).pin_memory()
+    Qh = None if w.Q is None else torch.from_numpy(w.Q).pin_memory()
+    off_h = torch.empty(w.m + 1, dtype=torch.int64).pin_memory()
+    idx_h = torch.empty(max(nnz, 1), dtype=torch.int32).pin_memory()
+    dist_h = torch.empty(max(nnz, 1), dtype=torch.float32).pin_memory()
+    e2e_times = []
+    for i in range(args.warmup + args.steps):
+        flush.fill_(1.0)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        idx = snn.snn_build(Xh)
+        r = snn.snn_query_self(idx, R) if Qh is None else snn.snn_query_radius(idx, Qh, R)
+        snn.snn_result_copy(r, off_h, idx_h, dist_h)
+        snn.snn_result_free(r)
+        snn.snn_free(idx)
+        e1.record()
+        e1.synchronize()
+        if i >= args.warmup:
+            e2e_times.append(e0.elapsed_time(e1))
+    e2e_ms = max_over_ranks(sum(e2e_times), world, dev)
+    e2e_value = weak_units(w.m * args.steps, world) / (e2e_ms / 1e3)
+    h2d = w.X.nbytes + (0 if w.Q is None else w.Q.nbytes)
+    d2h = (w.m + 1) * 8 + nnz * 8
+
+    # ---- roofline of the dominant kernel (windowed distance passes, K8)
+    peaks, src = load_peaks()
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    peak_alu = fp32_alu_peak_tflops(sm_max, n_sm)
+    kms = prof["window_count"]["ms"] + prof["window_write"]["ms"]
+    klaunch = prof["window_count"]["launches"] + prof["window_write"]["launches"]
+    kunits = prof["window_count"]["units"] + prof["window_write"]["units"]
+    flop_per_pair = 3 * w.d - 1             # eq:ip1 flop count
+    achieved = (flop_per_pair * kunits / klaunch) / (kms / klaunch * 1e-3) / 1e12 if klaunch else 0.0
+    traffic = None
+    try:
+        tr = json.load(open(TRAFFIC_PATH))
+        traffic = tr.get(args.config, {}).get("window_pass_dram_bytes_per_launch")
+    except Exception:
+        pass
+    roofline = {"kernel": "window_lowd (K8 count + write passes)", "bound": "alu",
+                "achieved": achieved, "peak": peak_alu, "unit": "TFLOP/s",
+                "frac": achieved / peak_alu if peak_alu else None, "traffic": traffic,
+                "peak_source": f"FP32 FMA issue peak at {sm_max:.0f} MHz x {n_sm} SMs "
+                               f"(sm_max_mhz from MEASURED_PEAKS.json, {src})",
+                "work": f"{flop_per_pair} flop per evaluated candidate pair (eq:ip1), "
+                        f"{kunits / max(klaunch, 1):.4g} pairs per launch",
+                "share_of_step": kms / sum(times) if times else None}
+
+    line = {"metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64" if w.X.dtype == np.float64 else "f32", "data": "synthetic",
+            "config": config_block(w, args),
+            "build_ms": prof["build"]["ms"] / max(1, prof["build"]["launches"]),
+            "query_ms": prof["query"]["ms"] / max(1, prof["query"]["launches"]),
+            "nnz": nnz,
+            "breakdown_ms_per_step": {k: v["ms"] / args.steps for k, v in prof.items()},
+            "clocks": clocks, "gpu_launches": launches,
+            "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.steps},
+            "roofline": roofline}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, k, dt, threads = oracle_sample_rate(w, args.cpu_seconds)
+        line["cpu_baseline"] = {"value": rate, "unit": "queries/s", "cores": threads,
+                                "kind": "oracle",
+                                "sample": f"first {k} of {w.m} queries vs all {w.n} points, "
+                                          f"fp64 brute force ({dt:.1f} s)"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="snn", choices=["snn", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,166 @@
+/*
+ * snn.h -- C ABI of the B200-native SNN hot path (arXiv 2212.07679, "sorting-based
+ * exact fixed-radius near-neighbour search").  Plain C: no CUDA or torch types.
+ *
+ * Problem (§3, §3.2): given data p_1..p_n in R^d and query
+ * points q (in- or out-of-sample) and a radius R, return every i with ||p_i - q|| <= R
+ * (inclusive), with its Euclidean distance ("can also return the corresponding distances
+ * if needed").  The result is EXACT: it equals fp64 brute force computed as
+ * s = sum_k (p_ik - q_k)^2 left to right without FMA, hit iff s <= R*R (DESIGN.md
+ * readings C1, C3, C5).
+ *
+ * Conventions for every entry point
+ *  - Array arguments are row-major with row stride d (contiguous).  They may be DEVICE
+ *    pointers (current CUDA device) or HOST pointers (pageable or pinned); host inputs
+ *    are staged to the device inside the call (this is the end-to-end path).
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  All
+ *    device work is ordered on it.  Every call is synchronous with respect to its
+ *    results: on return the outputs are valid (a query reads its output size from the
+ *    device once).
+ *  - Errors: a non-OK status is returned and snn_last_error() gives a thread-local
+ *    message.  Output handles are left NULL on error.  Nothing is leaked on error.
+ *  - Index ids are 0-based original row numbers of X; n must be < 2^30.
+ *  - Thread safety: an index is immutable after snn_build; concurrent queries on one
+ *    index (different streams / threads) are allowed; snn_free must not race a query.
+ */
+#ifndef SNN_H
+#define SNN_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum { SNN_F32 = 0, SNN_F64 = 1 } snn_dtype;
+
+typedef enum {
+    SNN_OK = 0,
+    SNN_ERR_INVALID_ARGUMENT = 1, /* NULL pointer, d < 1, m < 0, R < 0 or non-finite, ... */
+    SNN_ERR_EMPTY = 2,            /* n == 0 ("empty dataset", Alg. 1 needs >= 1 point)   */
+    SNN_ERR_NONFINITE = 3,        /* NaN / Inf in X or Q                                 */
+    SNN_ERR_DIM_MISMATCH = 4,     /* query d or dtype differs from the index             */
+    SNN_ERR_OUT_OF_MEMORY = 5,
+    SNN_ERR_CUDA = 6,             /* any other CUDA runtime error                        */
+    SNN_ERR_UNSUPPORTED = 7       /* n >= 2^30, or device is not sm_100                  */
+} snn_status;
+
+typedef struct snn_index_s *snn_index;   /* opaque; immutable after build  */
+typedef struct snn_result_s *snn_result; /* opaque; owns CSR device buffers */
+
+/* CSR view of a query result.  Row j = query j in the caller's query order.  All three
+ * arrays are DEVICE pointers owned by the snn_result.  Within a row, hits are in
+ * ascending order of the index's sort key (deterministic); graded as sets. */
+typedef struct {
+    int64_t m;                 /* number of queries (rows)                        */
+    int64_t nnz;               /* number of (query, point) hits                   */
+    const int64_t *offsets;    /* m + 1, offsets[0] = 0, offsets[m] = nnz         */
+    const int32_t *indices;    /* nnz original row ids of X                       */
+    const float *distances;    /* nnz Euclidean distances, = (float)sqrt(s_fp64)  */
+} snn_csr;
+
+/* Diagnostics of a built index (Algorithm 1 outputs). */
+typedef struct {
+    int64_t n;
+    int32_t d;
+    int32_t dtype;             /* snn_dtype                                        */
+    int32_t ld;                /* padded row stride (elements) of the sorted copy  */
+    int32_t power_iters;       /* power iterations used for v1                     */
+    double sigma1;             /* top singular value of the centered data          */
+    double key_err;            /* rigorous bound E_x on |computed key - exact key|  */
+    double v1_norm;            /* ||v1 as stored in fp32||_2                        */
+    const double *mu;          /* device, d: column mean (fp64)                     */
+    const float *v1;           /* device, d: top principal direction (fp32, unit)   */
+    const float *keys;         /* device, n: sorted projection keys alpha (fp32)    */
+    const int32_t *perm;       /* device, n: pi[sorted position] = original id      */
+    const float *xbar;         /* device, n: half squared norms of centered sorted rows */
+    const void *xs;            /* device, n x ld: original coordinates in key order */
+} snn_index_info_t;
+
+/*
+ * snn_build -- Algorithm 1 "SNN Index":
+ *   mu = mean(p_j) (l.2), X = P - mu (l.3), v1 = top right singular vector of X (l.4,
+ *   eq:svd PAPER.md:94-102; computed by power iteration on X^T X), alpha_i = x_i^T v1
+ *   (l.5), sort by alpha (l.6; stable, ties by original id), xbar_i = x_i^T x_i / 2 (l.7).
+ * X: n x d, dtype dt (SNN_F32 or SNN_F64), host or device.  X may be freed after return
+ * (the index keeps its own sorted copy).  Errors: n == 0 -> SNN_ERR_EMPTY; d < 1, NULL X
+ * or out -> SNN_ERR_INVALID_ARGUMENT; NaN/Inf -> SNN_ERR_NONFINITE; n >= 2^30 ->
+ * SNN_ERR_UNSUPPORTED.
+ */
+snn_status snn_build(const void *X, int64_t n, int32_t d, snn_dtype dt, void *stream,
+                     snn_index *out);
+
+/*
+ * snn_query_radius -- Algorithm 2 "SNN Query" for a batch of m
+ * queries (batched as in PAPER.md:218-219, per block of consecutive key-sorted queries):
+ *   x_q = q - mu (l.2), alpha_q = x_q^T v1 (l.3), candidate range J from the sorted keys
+ *   by binary search (l.4, eq:lower PAPER.md:142-153, padded by rigorous rounding bounds),
+ *   exact radius test over X(J,:) (l.5-6, eq:ip1/eq:ip2 PAPER.md:205-216).
+ * Q: m x d, same dtype as the index (dt), host or device.  m == 0 is valid (offsets =
+ * {0}).  R >= 0 and finite (R == 0 returns exact coincidences).  Errors: d or dt differ
+ * from the index -> SNN_ERR_DIM_MISMATCH; R < 0 / NaN, m < 0, NULL -> INVALID_ARGUMENT;
+ * NaN/Inf in Q -> SNN_ERR_NONFINITE.  *out owns the CSR buffers (snn_result_free).
+ */
+snn_status snn_query_radius(snn_index idx, const void *Q, int64_t m, int32_t d, snn_dtype dt,
+                            double R, void *stream, snn_result *out);
+
+/* Self-query: identical to snn_query_radius(idx, X, n, d, dt, R, ...) with the X the
+ * index was built from (every point is its own neighbour), without re-projecting X. */
+snn_status snn_query_self(snn_index idx, double R, void *stream, snn_result *out);
+
+/* CSR view (device pointers, valid until snn_result_free). */
+snn_status snn_result_csr(snn_result r, snn_csr *view);
+
+/* Copy the CSR to caller-owned buffers, HOST or DEVICE (offsets m+1, indices nnz,
+ * distances nnz; indices / distances may be NULL to skip).  Synchronous. */
+snn_status snn_result_copy(snn_result r, int64_t *offsets, int32_t *indices,
+                           float *distances, void *stream);
+
+void snn_result_free(snn_result r); /* NULL ok */
+
+/*
+ * snn_dbscan -- DBSCAN with SNN as the neighbourhood backend, exact
+ * readings of DESIGN.md C18: eps-neighbourhoods are closed balls incl. the point itself;
+ * core iff |N_eps| >= min_pts; clusters = connected components of core points under
+ * eps-adjacency; a non-core point with a core neighbour takes the cluster of its
+ * smallest-id core neighbour; others are noise (-1); clusters are numbered 0..K-1 by
+ * increasing smallest core id.  labels: n int32, host or device, ORIGINAL order.
+ * *n_clusters (host) receives K.  The neighbour lists are never materialised.
+ */
+snn_status snn_dbscan(snn_index idx, double eps, int32_t min_pts, int32_t *labels,
+                      int32_t *n_clusters, void *stream);
+
+void snn_free(snn_index idx); /* NULL ok */
+
+/* Thread-local message for the last non-OK status of this thread ("" if none). */
+const char *snn_last_error(void);
+
+snn_status snn_index_info(snn_index idx, snn_index_info_t *info);
+
+/* Number of kernels this library has launched in this process (monotone counter). */
+uint64_t snn_launch_count(void);
+
+/* Kernel-time profiling (diagnostics; process-global; off by default).  While enabled,
+ * the library brackets each kernel family with CUDA events on the launching stream and
+ * accumulates device time.  snn_profile_enable(1) also resets the counters.
+ * snn_profile_read synchronises the recorded events and returns, for `family`:
+ *   ms        summed device milliseconds,      launches  number of bracketed launches,
+ *   units     work units processed (window passes: candidate pairs evaluated; build:
+ *             points indexed), summed.
+ * Families: "build", "window_count", "window_write", "query" (whole query call).
+ * Unknown family -> SNN_ERR_INVALID_ARGUMENT. */
+snn_status snn_profile_enable(int on);
+snn_status snn_profile_read(const char *family, double *ms, uint64_t *launches, double *units);
+
+/* Test / tuning hooks (process-global; not thread-safe; 0 restores the default):
+ *   "force_generic"  1 = use the generic-d FFMA tile kernel even for d <= 16
+ *   "query_block"    queries per block for the low-d kernel (32..256, multiple of 32)
+ *   "chunk"          candidates per work item (multiple of 64)
+ *   "power_iters"    cap on power iterations (>= 1)
+ * Returns SNN_ERR_INVALID_ARGUMENT for an unknown key or bad value. */
+snn_status snn_set_option(const char *key, int64_t value);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SNN_H */

@@ -1,0 +1,563 @@
+// api.cu -- the C ABI (include/snn.h) and the host runtime around the kernels: argument
+// validation, device / memory-pool setup, stream-ordered workspaces, the launch
+// sequences of Algorithm 1 (build) and Algorithm 2 (query), and result ownership.
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <atomic>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/snn.h"
+#include "common.cuh"
+#include "internal.h"
+#include "query.h"
+#include "index.h"
+
+namespace snn {
+
+static std::atomic<uint64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+struct Options {
+    int force_generic = 0;
+    int query_block = 256;
+    int chunk = 2048;
+    int power_iters = 1000;
+};
+static Options g_opt;
+
+static thread_local std::string t_err;
+
+// ------------------------------------------------------------------ kernel-time profiler
+enum Fam { F_BUILD = 0, F_COUNT = 1, F_WRITE = 2, F_QUERY = 3, F_N = 4 };
+static const char *kFamNames[F_N] = {"build", "window_count", "window_write", "query"};
+struct ProfRec {
+    int fam;
+    cudaEvent_t a, b;
+    double units;
+};
+struct Profiler {
+    std::mutex mu;
+    bool on = false;
+    std::vector<ProfRec> pending;
+    double ms[F_N] = {}, units[F_N] = {};
+    uint64_t launches[F_N] = {};
+};
+static Profiler g_prof;
+
+static int prof_begin(int fam, cudaStream_t s) {
+    if (!g_prof.on) return -1;
+    ProfRec r{fam, nullptr, nullptr, 0.0};
+    cudaEventCreate(&r.a);
+    cudaEventCreate(&r.b);
+    cudaEventRecord(r.a, s);
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    g_prof.pending.push_back(r);
+    return (int)g_prof.pending.size() - 1;
+}
+static void prof_end(int tok, cudaStream_t s, double units) {
+    if (tok < 0 || !g_prof.on) return;
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    if (tok >= (int)g_prof.pending.size()) return;
+    g_prof.pending[tok].units = units;
+    cudaEventRecord(g_prof.pending[tok].b, s);
+}
+static void prof_drain() {
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    for (auto &r : g_prof.pending) {
+        float ms = 0.f;
+        cudaEventSynchronize(r.b);
+        if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) {
+            g_prof.ms[r.fam] += ms;
+            g_prof.units[r.fam] += r.units;
+            g_prof.launches[r.fam] += 1;
+        }
+        cudaGetLastError();
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    g_prof.pending.clear();
+}
+
+snn_status fail(snn_status st, const std::string &msg) {
+    t_err = msg;
+    return st;
+}
+
+snn_status cuda_fail(cudaError_t e, const char *where) {
+    cudaGetLastError();   // clear sticky-free errors
+    if (e == cudaErrorMemoryAllocation) return fail(SNN_ERR_OUT_OF_MEMORY, std::string(where) + ": out of device memory");
+    return fail(SNN_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(expr, where)                                      \
+    do {                                                     \
+        cudaError_t _e = (expr);                             \
+        if (_e != cudaSuccess) return cuda_fail(_e, where);  \
+    } while (0)
+
+struct DeviceInfo {
+    int ok = -1;   // -1 unknown, 0 unsupported, 1 ok
+    int sm_count = 148;
+};
+static std::mutex g_dev_mu;
+static DeviceInfo g_dev[64];
+
+snn_status device_check(int *sm_count) {
+    int dev = 0;
+    CK(cudaGetDevice(&dev), "cudaGetDevice");
+    if (dev < 0 || dev >= 64) return fail(SNN_ERR_UNSUPPORTED, "device ordinal out of range");
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    DeviceInfo &di = g_dev[dev];
+    if (di.ok < 0) {
+        int major = 0, minor = 0, sms = 0;
+        CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev), "attr");
+        CK(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev), "attr");
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
+        di.ok = (major == 10 && minor == 0) ? 1 : 0;
+        di.sm_count = sms;
+        if (di.ok) {   // keep freed stream-ordered memory in the pool (no per-call cudaMalloc)
+            cudaMemPool_t pool;
+            CK(cudaDeviceGetDefaultMemPool(&pool, dev), "mempool");
+            uint64_t thr = UINT64_MAX;
+            CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr), "mempool");
+        }
+    }
+    if (!di.ok) return fail(SNN_ERR_UNSUPPORTED, "this library is built for sm_100a (B200) only");
+    *sm_count = di.sm_count;
+    return SNN_OK;
+}
+
+bool is_device_ptr(const void *p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+// small pinned host staging for scalar read-backs
+struct Pinned {
+    void *p = nullptr;
+    Pinned() { cudaMallocHost(&p, 4096); }
+    ~Pinned() { if (p) cudaFreeHost(p); }
+};
+static thread_local Pinned t_pinned;
+
+int row_stride(int d) { return d == 1 ? 1 : d == 2 ? 2 : (int)round_up(d, 4); }
+
+}  // namespace snn
+
+using namespace snn;
+
+static void free_index(snn_index idx) {
+    if (!idx) return;
+    for (void *p : idx->owned) cudaFreeAsync(p, 0);
+    delete idx;
+}
+
+extern "C" {
+
+snn_status snn_profile_enable(int on) {
+    prof_drain();
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    g_prof.on = on != 0;
+    for (int f = 0; f < F_N; ++f) { g_prof.ms[f] = 0; g_prof.units[f] = 0; g_prof.launches[f] = 0; }
+    return SNN_OK;
+}
+
+snn_status snn_profile_read(const char *family, double *ms, uint64_t *launches, double *units) {
+    if (!family) return fail(SNN_ERR_INVALID_ARGUMENT, "NULL family");
+    prof_drain();
+    for (int f = 0; f < F_N; ++f) {
+        if (strcmp(family, kFamNames[f]) == 0) {
+            if (ms) *ms = g_prof.ms[f];
+            if (launches) *launches = g_prof.launches[f];
+            if (units) *units = g_prof.units[f];
+            return SNN_OK;
+        }
+    }
+    return fail(SNN_ERR_INVALID_ARGUMENT, std::string("unknown profile family ") + family);
+}
+
+const char *snn_last_error(void) { return t_err.c_str(); }
+uint64_t snn_launch_count(void) { return g_launches.load(); }
+
+snn_status snn_set_option(const char *key, int64_t value) {
+    if (!key) return fail(SNN_ERR_INVALID_ARGUMENT, "NULL option key");
+    std::string k(key);
+    if (k == "force_generic") { g_opt.force_generic = value ? 1 : 0; return SNN_OK; }
+    if (k == "query_block") {
+        if (value == 0) value = 256;
+        if (value < 32 || value > 256 || value % 32) return fail(SNN_ERR_INVALID_ARGUMENT, "query_block must be 32..256, multiple of 32");
+        g_opt.query_block = (int)value;
+        return SNN_OK;
+    }
+    if (k == "chunk") {
+        if (value == 0) value = 2048;
+        if (value < 64 || value > 8192 || value % 64) return fail(SNN_ERR_INVALID_ARGUMENT, "chunk must be 64..8192, multiple of 64");
+        g_opt.chunk = (int)value;
+        return SNN_OK;
+    }
+    if (k == "power_iters") {
+        if (value == 0) value = 1000;
+        if (value < 1 || value > 1000000) return fail(SNN_ERR_INVALID_ARGUMENT, "power_iters must be >= 1");
+        g_opt.power_iters = (int)value;
+        return SNN_OK;
+    }
+    return fail(SNN_ERR_INVALID_ARGUMENT, "unknown option " + k);
+}
+
+snn_status snn_build(const void *X, int64_t n, int32_t d, snn_dtype dt, void *stream, snn_index *out) {
+    if (!out) return fail(SNN_ERR_INVALID_ARGUMENT, "NULL output handle");
+    *out = nullptr;
+    if (n == 0) return fail(SNN_ERR_EMPTY, "empty dataset");
+    if (!X || n < 0 || d < 1 || (dt != SNN_F32 && dt != SNN_F64))
+        return fail(SNN_ERR_INVALID_ARGUMENT, "invalid argument to snn_build");
+    if (n >= (int64_t(1) << 30)) return fail(SNN_ERR_UNSUPPORTED, "n >= 2^30 is not supported");
+    int sms = 0;
+    snn_status st = device_check(&sms);
+    if (st != SNN_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const bool f64 = dt == SNN_F64;
+    const size_t es = f64 ? 8 : 4;
+
+    snn_index idx = new snn_index_s();
+    idx->n = n; idx->d = d; idx->dt = dt; idx->sm_count = sms;
+    idx->ld = row_stride(d);
+    idx->n_pad = round_up(n, 4);
+    Workspace ws(s);
+    auto own = [&](auto **p, size_t count) -> cudaError_t {
+        cudaError_t e = ws.alloc(p, count);
+        if (e == cudaSuccess) { ws.release(*p); idx->owned.push_back(*p); }
+        return e;
+    };
+#define CKI(expr, where)                                                   \
+    do {                                                                   \
+        cudaError_t _e = (expr);                                           \
+        if (_e != cudaSuccess) { free_index(idx); return cuda_fail(_e, where); } \
+    } while (0)
+    uint8_t *xs_bytes = nullptr;
+    CKI(own(&xs_bytes, (size_t)idx->n_pad * idx->ld * es), "alloc Xs");
+    idx->Xs = xs_bytes;
+    CKI(own(&idx->keys, (size_t)n), "alloc keys");
+    CKI(own(&idx->perm, (size_t)n), "alloc perm");
+    CKI(own(&idx->xbar, (size_t)idx->n_pad), "alloc xbar");
+    CKI(own(&idx->mu_d, (size_t)d), "alloc");
+    CKI(own(&idx->mu_f, (size_t)d), "alloc");
+    CKI(own(&idx->v_d, (size_t)d), "alloc");
+    CKI(own(&idx->v_f, (size_t)d), "alloc");
+    CKI(own(&idx->stats, (size_t)ST_COUNT + 2), "alloc");
+
+    const void *Xd = X;
+    if (!is_device_ptr(X)) {   // host input: stage (end-to-end path)
+        uint8_t *tmp = nullptr;
+        CKI(ws.alloc(&tmp, (size_t)n * d * es), "alloc staging");
+        CKI(cudaMemcpyAsync(tmp, X, (size_t)n * d * es, cudaMemcpyHostToDevice, s), "H2D X");
+        Xd = tmp;
+    }
+    double *sums = nullptr, *G = nullptr;
+    uint32_t *maxabs = nullptr;
+    int *flag = nullptr;
+    float *keys_raw = nullptr;
+    uint8_t *sort_tmp = nullptr;
+    CKI(ws.alloc(&sums, (size_t)d), "alloc");
+    CKI(ws.alloc(&maxabs, (size_t)d), "alloc");
+    CKI(ws.alloc(&flag, 1), "alloc");
+    CKI(ws.alloc(&G, (size_t)d * d), "alloc Gram");
+    CKI(ws.alloc(&keys_raw, (size_t)n), "alloc");
+    CKI(ws.alloc(&sort_tmp, radix_sort_temp_bytes(n)), "alloc sort");
+    CKI(cudaMemsetAsync(sums, 0, d * 8, s), "memset");
+    CKI(cudaMemsetAsync(maxabs, 0, d * 4, s), "memset");
+    CKI(cudaMemsetAsync(flag, 0, 4, s), "memset");
+    CKI(cudaMemsetAsync(G, 0, (size_t)d * d * 8, s), "memset");
+    CKI(cudaMemsetAsync(idx->stats, 0, (ST_COUNT + 2) * 8, s), "memset");
+
+    const int ptok = prof_begin(F_BUILD, s);
+    launch_colstats(Xd, f64, n, d, sums, maxabs, flag, s);                        // K1
+    launch_finalize_mean(sums, n, d, idx->mu_d, idx->mu_f, s);
+    launch_gram(Xd, f64, n, d, idx->mu_f, G, s);                                  // K2a
+    launch_power_iteration(G, d, g_opt.power_iters, 1e-7, maxabs, idx->mu_d, idx->mu_f,
+                           idx->v_d, idx->v_f, idx->stats, s);                     // K2b
+    launch_keys(Xd, f64, n, d, idx->mu_d, idx->mu_f, idx->v_d, idx->v_f, keys_raw, s);  // K3
+    radix_sort_pairs(keys_raw, nullptr, idx->keys, reinterpret_cast<uint32_t *>(idx->perm), n,
+                     sort_tmp, s);                                                 // K4
+    launch_gather(Xd, f64, n, d, idx->ld, idx->n_pad, reinterpret_cast<const uint32_t *>(idx->perm),
+                  idx->mu_d, idx->Xs, idx->xbar, s);                               // K5
+    prof_end(ptok, s, (double)n);
+    CKI(cudaGetLastError(), "launch");
+    double *hs = static_cast<double *>(t_pinned.p);
+    CKI(cudaMemcpyAsync(hs, idx->stats, ST_COUNT * 8, cudaMemcpyDeviceToHost, s), "D2H stats");
+    CKI(cudaMemcpyAsync(hs + ST_COUNT, flag, 4, cudaMemcpyDeviceToHost, s), "D2H flag");
+    CKI(cudaStreamSynchronize(s), "build");
+    memcpy(idx->h_stats, hs, sizeof(idx->h_stats));
+    int nonfinite = *reinterpret_cast<int *>(hs + ST_COUNT);
+    if (nonfinite) {
+        free_index(idx);
+        return fail(SNN_ERR_NONFINITE, "X contains NaN or Inf");
+    }
+    *out = idx;
+    return SNN_OK;
+#undef CKI
+}
+
+void snn_free(snn_index idx) { free_index(idx); }
+
+static void thresholds(double R2, int d, float *T_in, float *T_out) {
+    const double u32 = ldexp(1.0, -24), u64 = ldexp(1.0, -53);
+    const double g32 = (d + 2) * u32 / (1.0 - (d + 2) * u32);
+    const double g64 = (d + 2) * u64 / (1.0 - (d + 2) * u64);
+    const double eta = (2.0 * d + 2.0) * ldexp(1.0, -149);
+    const double tin = R2 * (1.0 - g32) / (1.0 + g64) * (1.0 - 1e-12) - eta;
+    const double tout = R2 * (1.0 + g32) / (1.0 - g64) * (1.0 + 1e-12) + eta;
+    float fi = (float)tin;
+    if ((double)fi > tin) fi = nextafterf(fi, -INFINITY);
+    float fo = (float)tout;
+    if ((double)fo < tout) fo = nextafterf(fo, INFINITY);
+    *T_in = fi;
+    *T_out = fo;
+}
+
+static snn_status make_empty_result(int64_t m, cudaStream_t s, snn_result *out) {
+    snn_result r = new snn_result_s();
+    r->m = m;
+    void *p = nullptr;
+    cudaError_t e = cudaMallocAsync(&p, (size_t)(m + 1) * 8, s);
+    if (e != cudaSuccess) { delete r; return cuda_fail(e, "alloc offsets"); }
+    r->offsets = static_cast<int64_t *>(p);
+    cudaMemsetAsync(r->offsets, 0, (size_t)(m + 1) * 8, s);
+    cudaMallocAsync(&p, 16, s); r->indices = static_cast<int32_t *>(p);
+    cudaMallocAsync(&p, 16, s); r->distances = static_cast<float *>(p);
+    e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) { snn_result_free(r); return cuda_fail(e, "query"); }
+    *out = r;
+    return SNN_OK;
+}
+
+static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d, snn_dtype dt,
+                             double R, void *stream, snn_result *out) {
+    if (!out) return fail(SNN_ERR_INVALID_ARGUMENT, "NULL output handle");
+    *out = nullptr;
+    if (!idx) return fail(SNN_ERR_INVALID_ARGUMENT, "NULL index");
+    if (m < 0 || !(R >= 0.0) || !isfinite(R)) return fail(SNN_ERR_INVALID_ARGUMENT, "negative or non-finite radius / m < 0");
+    const bool self = (Q == nullptr);
+    if (!self && (d != idx->d || dt != idx->dt)) return fail(SNN_ERR_DIM_MISMATCH, "query dimension / dtype differs from the index");
+    if (m >= (int64_t(1) << 31)) return fail(SNN_ERR_UNSUPPORTED, "m >= 2^31");
+    int sms = 0;
+    snn_status st = device_check(&sms);
+    if (st != SNN_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (m == 0) return make_empty_result(0, s, out);
+
+    const bool f64 = idx->dt == SNN_F64;
+    const size_t es = f64 ? 8 : 4;
+    const int D = idx->d, ld = idx->ld;
+    const int qtok = prof_begin(F_QUERY, s);
+    Workspace ws(s);
+    const void *Qs = idx->Xs;
+    const float *qkeys = idx->keys;
+    const int32_t *qperm = idx->perm;
+    const double *eq = idx->stats + ST_EX_F;
+    int *qflag = nullptr;
+    unsigned long long *pairs = nullptr;
+    CK(ws.alloc(&qflag, 2), "alloc");
+    CK(ws.alloc(&pairs, 1), "alloc");
+    CK(cudaMemsetAsync(qflag, 0, 8, s), "memset");
+    CK(cudaMemsetAsync(pairs, 0, 8, s), "memset");
+    if (!self) {
+        const void *Qd = Q;
+        if (!is_device_ptr(Q)) {
+            uint8_t *tmp = nullptr;
+            CK(ws.alloc(&tmp, (size_t)m * D * es), "alloc staging");
+            CK(cudaMemcpyAsync(tmp, Q, (size_t)m * D * es, cudaMemcpyHostToDevice, s), "H2D Q");
+            Qd = tmp;
+        }
+        double *qsums = nullptr, *eqd = nullptr;
+        uint32_t *qmax = nullptr;
+        float *qk_raw = nullptr, *qk = nullptr;
+        int32_t *qp = nullptr;
+        uint8_t *qs = nullptr, *sort_tmp = nullptr;
+        CK(ws.alloc(&qsums, (size_t)D), "alloc");
+        CK(ws.alloc(&qmax, (size_t)D), "alloc");
+        CK(ws.alloc(&eqd, 1), "alloc");
+        CK(ws.alloc(&qk_raw, (size_t)m), "alloc");
+        CK(ws.alloc(&qk, (size_t)m), "alloc");
+        CK(ws.alloc(&qp, (size_t)m), "alloc");
+        CK(ws.alloc(&qs, (size_t)m * ld * es), "alloc");
+        CK(ws.alloc(&sort_tmp, radix_sort_temp_bytes(m)), "alloc");
+        CK(cudaMemsetAsync(qsums, 0, D * 8, s), "memset");
+        CK(cudaMemsetAsync(qmax, 0, D * 4, s), "memset");
+        // K6 query prep: finiteness + max |q| (E_q), keys (Alg. 2 l.2-3), sort, gather
+        launch_colstats(Qd, f64, m, D, qsums, qmax, qflag, s);
+        launch_query_key_err(D, f64, qmax, idx->mu_d, idx->mu_f, idx->v_d, idx->v_f, eqd, s);
+        launch_keys(Qd, f64, m, D, idx->mu_d, idx->mu_f, idx->v_d, idx->v_f, qk_raw, s);
+        radix_sort_pairs(qk_raw, nullptr, qk, reinterpret_cast<uint32_t *>(qp), m, sort_tmp, s);
+        launch_gather(Qd, f64, m, D, ld, m, reinterpret_cast<const uint32_t *>(qp), idx->mu_d, qs, nullptr, s);
+        Qs = qs; qkeys = qk; qperm = qp; eq = eqd;
+    }
+    const bool generic = g_opt.force_generic || !lowd_supported(D);
+    const int B = generic ? 64 : g_opt.query_block;
+    const int chunk = generic ? 1024 : g_opt.chunk;
+    const int64_t nblocks = ceil_div(m, B);
+    int64_t *blk_lo = nullptr, *blk_hi = nullptr, *nitems = nullptr, *item_start = nullptr;
+    uint8_t *scan_tmp = nullptr;
+    CK(ws.alloc(&blk_lo, (size_t)nblocks), "alloc");
+    CK(ws.alloc(&blk_hi, (size_t)nblocks), "alloc");
+    CK(ws.alloc(&nitems, (size_t)nblocks), "alloc");
+    CK(ws.alloc(&item_start, (size_t)nblocks + 1), "alloc");
+    CK(ws.alloc(&scan_tmp, scan_temp_bytes(m > nblocks ? m : nblocks)), "alloc");
+    WindowSpec w;
+    w.qkeys = qkeys; w.m = m; w.B = B; w.keys = idx->keys; w.n = idx->n; w.n_pad = idx->n_pad;
+    w.R = R;
+    w.wnorm = idx->stats + (f64 ? ST_WNORM_D : ST_WNORM_F);
+    w.ex = idx->stats + (f64 ? ST_EX_D : ST_EX_F);
+    w.eq = eq;
+    w.chunk = chunk;
+    w.blk_lo = blk_lo; w.blk_hi = blk_hi; w.nitems = nitems; w.pairs = pairs;
+    launch_block_windows(w, s);                                                    // K7
+    exclusive_scan_i64(nitems, item_start, nblocks, scan_tmp, s);
+    int64_t *hp = static_cast<int64_t *>(t_pinned.p);
+    CK(cudaMemcpyAsync(hp, item_start + nblocks, 8, cudaMemcpyDeviceToHost, s), "D2H items");
+    CK(cudaMemcpyAsync(hp + 1, qflag, 4, cudaMemcpyDeviceToHost, s), "D2H flag");
+    CK(cudaMemcpyAsync(hp + 2, pairs, 8, cudaMemcpyDeviceToHost, s), "D2H pairs");
+    CK(cudaStreamSynchronize(s), "query windows");
+    const int64_t total_items = hp[0];
+    const double pairs_eval = (double)*reinterpret_cast<unsigned long long *>(hp + 2);
+    if (*reinterpret_cast<int *>(hp + 1)) return fail(SNN_ERR_NONFINITE, "Q contains NaN or Inf");
+
+    int32_t *cnt = nullptr, *row_count = nullptr;
+    CK(ws.alloc(&cnt, (size_t)total_items * B), "alloc counts");
+    CK(ws.alloc(&row_count, (size_t)m), "alloc");
+    snn_result r = new snn_result_s();
+    r->m = m;
+    auto bail = [&](cudaError_t e, const char *where) { snn_result_free(r); return cuda_fail(e, where); };
+    {
+        void *p = nullptr;
+        cudaError_t e = cudaMallocAsync(&p, (size_t)(m + 1) * 8, s);
+        if (e != cudaSuccess) return bail(e, "alloc offsets");
+        r->offsets = static_cast<int64_t *>(p);
+    }
+    PassArgs a;
+    a.Xs = idx->Xs; a.Qs = Qs; a.ld = ld; a.d = D; a.f64 = f64; a.m = m;
+    a.perm = idx->perm; a.qperm = qperm;
+    a.blk_lo = blk_lo; a.blk_hi = blk_hi; a.item_start = item_start;
+    a.nblocks = nblocks; a.total_items = total_items;
+    a.B = B; a.chunk = chunk; a.generic = generic;
+    a.R2 = R * R;
+    thresholds(a.R2, D, &a.T_in, &a.T_out);
+    a.cnt = cnt; a.offsets = r->offsets; a.out_idx = nullptr; a.out_dist = nullptr;
+    a.sm_count = sms;
+    if (total_items == 0) {
+        cudaMemsetAsync(row_count, 0, (size_t)m * 4, s);
+    } else {
+        const int ctok = prof_begin(F_COUNT, s);
+        launch_window_pass(false, a, s);                                           // K8 count
+        prof_end(ctok, s, pairs_eval);
+        launch_row_totals(cnt, item_start, m, B, qperm, row_count, s);             // K11
+    }
+    exclusive_scan_i32_to_i64(row_count, r->offsets, m, scan_tmp, s);
+    {
+        cudaError_t e = cudaMemcpyAsync(hp, r->offsets + m, 8, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) return bail(e, "query count");
+    }
+    r->nnz = hp[0];
+    {
+        void *p = nullptr;
+        cudaError_t e = cudaMallocAsync(&p, (size_t)(r->nnz > 0 ? r->nnz : 1) * 4, s);
+        if (e != cudaSuccess) return bail(e, "alloc indices");
+        r->indices = static_cast<int32_t *>(p);
+        e = cudaMallocAsync(&p, (size_t)(r->nnz > 0 ? r->nnz : 1) * 4, s);
+        if (e != cudaSuccess) return bail(e, "alloc distances");
+        r->distances = static_cast<float *>(p);
+    }
+    a.out_idx = r->indices; a.out_dist = r->distances;
+    if (r->nnz > 0) {
+        const int wtok = prof_begin(F_WRITE, s);
+        launch_window_pass(true, a, s);                                            // K8 write
+        prof_end(wtok, s, pairs_eval);
+    }
+    prof_end(qtok, s, (double)m);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return bail(e, "launch");
+    e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return bail(e, "query");
+    *out = r;
+    return SNN_OK;
+}
+
+snn_status snn_query_radius(snn_index idx, const void *Q, int64_t m, int32_t d, snn_dtype dt,
+                            double R, void *stream, snn_result *out) {
+    if (!Q && m > 0) return fail(SNN_ERR_INVALID_ARGUMENT, "NULL query pointer");
+    if (!Q) {   // m == 0 with NULL Q: still validate the header
+        if (out) *out = nullptr;
+        if (!idx || !out) return fail(SNN_ERR_INVALID_ARGUMENT, "NULL argument");
+        if (d != idx->d || dt != idx->dt) return fail(SNN_ERR_DIM_MISMATCH, "query dimension / dtype differs from the index");
+        if (m < 0 || !(R >= 0.0) || !isfinite(R)) return fail(SNN_ERR_INVALID_ARGUMENT, "negative or non-finite radius / m < 0");
+        int sms;
+        snn_status st = device_check(&sms);
+        if (st != SNN_OK) return st;
+        return make_empty_result(0, static_cast<cudaStream_t>(stream), out);
+    }
+    return query_impl(idx, Q, m, d, dt, R, stream, out);
+}
+
+snn_status snn_query_self(snn_index idx, double R, void *stream, snn_result *out) {
+    if (!idx) return fail(SNN_ERR_INVALID_ARGUMENT, "NULL index");
+    return query_impl(idx, nullptr, idx->n, idx->d, idx->dt, R, stream, out);
+}
+
+snn_status snn_result_csr(snn_result r, snn_csr *view) {
+    if (!r || !view) return fail(SNN_ERR_INVALID_ARGUMENT, "NULL argument");
+    view->m = r->m; view->nnz = r->nnz;
+    view->offsets = r->offsets; view->indices = r->indices; view->distances = r->distances;
+    return SNN_OK;
+}
+
+snn_status snn_result_copy(snn_result r, int64_t *offsets, int32_t *indices,
+                           float *distances, void *stream) {
+    if (!r || !offsets) return fail(SNN_ERR_INVALID_ARGUMENT, "NULL argument");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    CK(cudaMemcpyAsync(offsets, r->offsets, (size_t)(r->m + 1) * 8, cudaMemcpyDefault, s), "copy offsets");
+    if (indices && r->nnz) CK(cudaMemcpyAsync(indices, r->indices, (size_t)r->nnz * 4, cudaMemcpyDefault, s), "copy indices");
+    if (distances && r->nnz) CK(cudaMemcpyAsync(distances, r->distances, (size_t)r->nnz * 4, cudaMemcpyDefault, s), "copy distances");
+    CK(cudaStreamSynchronize(s), "D2H");
+    return SNN_OK;
+}
+
+void snn_result_free(snn_result r) {
+    if (!r) return;
+    if (r->offsets) cudaFreeAsync(r->offsets, 0);
+    if (r->indices) cudaFreeAsync(r->indices, 0);
+    if (r->distances) cudaFreeAsync(r->distances, 0);
+    delete r;
+}
+
+snn_status snn_index_info(snn_index idx, snn_index_info_t *info) {
+    if (!idx || !info) return fail(SNN_ERR_INVALID_ARGUMENT, "NULL argument");
+    const bool f64 = idx->dt == SNN_F64;
+    info->n = idx->n; info->d = idx->d; info->dtype = idx->dt; info->ld = idx->ld;
+    info->power_iters = (int32_t)idx->h_stats[ST_ITERS];
+    info->sigma1 = idx->h_stats[ST_SIGMA1];
+    info->key_err = idx->h_stats[f64 ? ST_EX_D : ST_EX_F];
+    info->v1_norm = idx->h_stats[f64 ? ST_WNORM_D : ST_WNORM_F];
+    info->mu = idx->mu_d; info->v1 = idx->v_f; info->keys = idx->keys; info->perm = idx->perm;
+    info->xbar = idx->xbar; info->xs = idx->Xs;
+    return SNN_OK;
+}
+
+snn_status snn_dbscan(snn_index idx, double eps, int32_t min_pts, int32_t *labels,
+                      int32_t *n_clusters, void *stream) {
+    if (!idx || !labels || !n_clusters) return fail(SNN_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (!(eps >= 0.0) || !isfinite(eps) || min_pts < 1) return fail(SNN_ERR_INVALID_ARGUMENT, "eps must be finite >= 0, min_pts >= 1");
+    int sms = 0;
+    snn_status st = device_check(&sms);
+    if (st != SNN_OK) return st;
+    return dbscan_impl(idx, eps, min_pts, labels, n_clusters, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

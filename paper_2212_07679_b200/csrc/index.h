@@ -1,0 +1,73 @@
+// index.h -- the opaque handle types of include/snn.h and small runtime helpers shared
+// by api.cu and dbscan.cu.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/snn.h"
+#include "internal.h"
+
+namespace snn {
+snn_status fail(snn_status st, const std::string &msg);
+snn_status cuda_fail(cudaError_t e, const char *where);
+bool is_device_ptr(const void *p);
+
+// Stream-ordered workspace: every allocation is freed on the same stream at scope exit.
+struct Workspace {
+    cudaStream_t s;
+    std::vector<void *> ptrs;
+    explicit Workspace(cudaStream_t st) : s(st) {}
+    ~Workspace() {
+        for (void *p : ptrs) cudaFreeAsync(p, s);
+    }
+    template <typename T>
+    cudaError_t alloc(T **out, size_t count) {
+        void *p = nullptr;
+        size_t bytes = count * sizeof(T);
+        if (bytes == 0) bytes = 16;
+        cudaError_t e = cudaMallocAsync(&p, bytes, s);
+        if (e == cudaSuccess) ptrs.push_back(p);
+        *out = static_cast<T *>(p);
+        return e;
+    }
+    void release(void *p) {   // hand ownership to the caller
+        std::vector<void *> keep;
+        for (void *q : ptrs) if (q != p) keep.push_back(q);
+        ptrs.swap(keep);
+    }
+};
+}  // namespace snn
+
+struct snn_index_s {
+    int64_t n = 0, n_pad = 0;
+    int d = 0, ld = 0;
+    snn_dtype dt = SNN_F32;
+    void *Xs = nullptr;        // n_pad x ld, original coordinates in key order
+    float *keys = nullptr;     // n sorted keys
+    int32_t *perm = nullptr;   // n: sorted position -> original id
+    float *xbar = nullptr;     // n_pad half squared norms (centered)
+    double *mu_d = nullptr;
+    float *mu_f = nullptr;
+    double *v_d = nullptr;
+    float *v_f = nullptr;
+    double *stats = nullptr;   // ST_COUNT doubles
+    double h_stats[snn::ST_COUNT] = {};
+    int sm_count = 148;
+    std::vector<void *> owned;
+};
+
+struct snn_result_s {
+    int64_t m = 0, nnz = 0;
+    int64_t *offsets = nullptr;
+    int32_t *indices = nullptr;
+    float *distances = nullptr;
+};
+
+
+namespace snn {
+snn_status dbscan_impl(snn_index idx, double eps, int32_t min_pts, int32_t *labels,
+                       int32_t *n_clusters, cudaStream_t s);
+}

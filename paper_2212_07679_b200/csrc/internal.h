@@ -1,0 +1,58 @@
+// internal.h -- host-side launchers shared between the .cu translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace snn {
+
+// ----------------------------------------------------------------------- build (build.cu)
+// K1: column sums (fp64), column max |x| (fp32, stored as uint bits), non-finite flag.
+// sums/maxabs_bits/flag must be zeroed by the caller.
+void launch_colstats(const void *X, bool f64, int64_t n, int d, double *sums,
+                     uint32_t *maxabs_bits, int *nonfinite, cudaStream_t s);
+// mu_d = sums/n, mu_f = (float)mu_d.
+void launch_finalize_mean(const double *sums, int64_t n, int d, double *mu_d, float *mu_f,
+                          cudaStream_t s);
+// K2a: G += sum_i (p_i - mu)(p_i - mu)^T (fp32 products, fp64 accumulation), G zeroed.
+void launch_gram(const void *X, bool f64, int64_t n, int d, const float *mu_f, double *G,
+                 cudaStream_t s);
+// K2b: power iteration on G (d x d, fp64).  Writes v_d (fp64 unit), v_f (fp32), and
+// stats[]: see enum Stat.  maxabs_bits/mu feed the key error bound E_x.
+enum Stat {
+    ST_SIGMA1 = 0, ST_ITERS = 1, ST_WNORM_F = 2, ST_WNORM_D = 3, ST_EX_F = 4, ST_EX_D = 5,
+    ST_COUNT = 8
+};
+void launch_power_iteration(const double *G, int d, int max_iters, double tol,
+                            const uint32_t *maxabs_bits, const double *mu_d, const float *mu_f,
+                            double *v_d, float *v_f, double *stats, cudaStream_t s);
+// Key error bound for a query set: eq = 2(d+2)2^-24 sum_k (maxabs_k + |mu_k|)|v_k|.
+void launch_query_key_err(int d, bool f64, const uint32_t *maxabs_bits, const double *mu_d,
+                          const float *mu_f, const double *v_d, const float *v_f, double *eq,
+                          cudaStream_t s);
+// K3: keys_i = sum_k (p_ik - mu_k) v_k (fp32 path: fp32 FMA chain; fp64 path: fp64 then
+// rounded to fp32).
+void launch_keys(const void *X, bool f64, int64_t n, int d, const double *mu_d,
+                 const float *mu_f, const double *v_d, const float *v_f, float *keys,
+                 cudaStream_t s);
+// K5: Xs[i] = X[perm[i]] (stride ld, zero pad columns; rows [n, n_pad) = NaN sentinels) and
+// xbar[i] = 0.5 * ||X[perm[i]] - mu||^2 (fp64 accumulate, stored fp32; nullable).
+void launch_gather(const void *X, bool f64, int64_t n, int d, int ld, int64_t n_pad,
+                   const uint32_t *perm, const double *mu_d, void *Xs, float *xbar,
+                   cudaStream_t s);
+
+// ----------------------------------------------------------------------- sort (radix_sort.cu)
+// Stable ascending sort of fp32 keys (finite) with uint32 payload.  If vals_in == nullptr
+// the payload is the iota 0..n-1.  Outputs in keys_out / vals_out.  temp_bytes() tells
+// the scratch size.
+size_t radix_sort_temp_bytes(int64_t n);
+void radix_sort_pairs(const float *keys_in, const uint32_t *vals_in, float *keys_out,
+                      uint32_t *vals_out, int64_t n, void *temp, cudaStream_t s);
+
+// ----------------------------------------------------------------------- scan (scan.cu)
+size_t scan_temp_bytes(int64_t n);
+// out[0..n] = exclusive prefix sums of in[0..n) (out[n] = total).  int64.
+void exclusive_scan_i64(const int64_t *in, int64_t *out, int64_t n, void *temp, cudaStream_t s);
+void exclusive_scan_i32_to_i64(const int32_t *in, int64_t *out, int64_t n, void *temp,
+                               cudaStream_t s);
+
+}  // namespace snn

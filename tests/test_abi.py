@@ -1,0 +1,85 @@
+"""Host-side checks of the C-ABI library (no GPU needed): it builds for sm_100a, loads,
+and exports every entry point include/snn.h declares; the binding has the same names;
+the product path never imports the oracle."""
+import ast
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def libpath():
+    from paper_2212_07679_b200 import build_lib
+    return build_lib.build()
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "snn.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(snn_[a-z_]+)\s*\(", src)))
+
+
+def test_header_declares_the_boundary():
+    fns = header_functions()
+    for f in ["snn_build", "snn_query_radius", "snn_free"]:   # BASELINE.json north_star
+        assert f in fns
+
+
+def test_library_exports_every_declared_symbol(libpath):
+    lib = ctypes.CDLL(libpath)
+    for f in header_functions():
+        assert hasattr(lib, f), f
+    out = subprocess.check_output(["nm", "-D", "--defined-only", libpath]).decode()
+    exported = set(re.findall(r" T (snn_\w+)", out))
+    assert set(header_functions()) <= exported
+
+
+def test_library_is_sm100a_only(libpath):
+    out = subprocess.check_output(["/usr/local/cuda/bin/cuobjdump", "--list-elf", libpath]).decode()
+    assert "sm_100a" in out
+    assert "sm_90" not in out and "sm_80" not in out
+
+
+def test_sass_uses_bulk_async_copy(libpath):
+    sass = subprocess.check_output(["/usr/local/cuda/bin/cuobjdump", "-sass", libpath]).decode()
+    assert "UBLKCP" in sass     # cp.async.bulk (TMA engine) staging of candidate rows
+
+
+def test_binding_names_match_header():
+    import paper_2212_07679_b200 as p
+    for f in header_functions():
+        assert hasattr(p, f), f
+    assert sorted(p.EXPORTS) == sorted(header_functions())
+
+
+def test_product_path_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_2212_07679_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith(".py"):
+                tree = ast.parse(open(os.path.join(dirpath, f)).read())
+                for node in ast.walk(tree):
+                    if isinstance(node, ast.Import):
+                        assert all(not a.name.startswith("oracle") for a in node.names)
+                    if isinstance(node, ast.ImportFrom):
+                        assert not (node.module or "").startswith("oracle")
+            if f.endswith((".cu", ".cuh", ".h", ".cpp")):
+                for line in open(os.path.join(dirpath, f)):
+                    if line.strip().startswith("#include"):
+                        assert "oracle" not in line.lower()
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    import paper_2212_07679_b200 as p
+    saved = p._lib
+    try:
+        p._lib = None
+        with pytest.raises(RuntimeError, match="CUDA library missing"):
+            p.load_library(str(tmp_path / "nope.so"))
+    finally:
+        p._lib = saved

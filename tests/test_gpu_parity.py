@@ -1,0 +1,279 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle, element by
+element on the same seeded inputs.  All tests need an sm_100 device."""
+import numpy as np
+import pytest
+
+import oracle
+import workloads
+from tests.parity import compare
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def snn():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2212_07679_b200 import build_lib
+    build_lib.build()
+    import paper_2212_07679_b200 as p
+    p.load_library()
+    return p
+
+
+def _dev(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def run(snn, X, Q, R, host=False):
+    idx = snn.Index(X if host else _dev(X))
+    try:
+        if Q is None:
+            return idx.query_self(R)
+        return idx.query(Q if host else _dev(Q), R)
+    finally:
+        idx.free()
+
+
+# --------------------------------------------------------------------------- small random
+CASES = [
+    # (n, m, d, dtype, R-quantile, seed)
+    (1000, 300, 1, np.float32, 0.01, 1),
+    (3001, 517, 2, np.float32, 0.01, 2),
+    (4099, 1000, 3, np.float32, 0.005, 3),
+    (2500, 333, 4, np.float32, 0.02, 4),
+    (1777, 250, 5, np.float32, 0.02, 5),
+    (1500, 200, 8, np.float32, 0.05, 6),
+    (1200, 130, 9, np.float32, 0.05, 7),
+    (1100, 129, 16, np.float32, 0.05, 8),
+    (900, 100, 17, np.float32, 0.05, 9),
+    (700, 77, 64, np.float32, 0.05, 10),
+    (500, 65, 100, np.float32, 0.05, 11),
+    (300, 40, 784, np.float32, 0.05, 12),
+    (2000, 300, 2, np.float64, 0.01, 13),
+    (1500, 200, 3, np.float64, 0.01, 14),
+    (600, 70, 33, np.float64, 0.05, 15),
+]
+
+
+@pytest.mark.parametrize("n,m,d,dt,qr,seed", CASES)
+def test_random_parity(snn, n, m, d, dt, qr, seed):
+    rng = np.random.default_rng(seed)
+    X = (rng.standard_normal((n, d)) * rng.uniform(0.5, 3, d)).astype(dt)
+    Q = (rng.standard_normal((m, d)) * rng.uniform(0.5, 3, d)).astype(dt)
+    R = float(np.quantile(np.linalg.norm(X[:200, None, :].astype(np.float64) - Q[None, :50, :], axis=-1), qr))
+    gpu = run(snn, X, Q, R)
+    ora = oracle.radius_query(X, Q, R)
+    compare(gpu, ora)
+
+
+@pytest.mark.parametrize("d,dt", [(2, np.float32), (3, np.float32), (3, np.float64), (20, np.float32)])
+def test_self_query_parity_and_invariants(snn, d, dt):
+    rng = np.random.default_rng(100 + d)
+    X = (rng.random((5000, d)) * 10).astype(dt)
+    X[17] = X[4000]            # exact duplicate
+    R = 0.9 if d <= 3 else 6.0
+    gpu = run(snn, X, None, R)
+    ora = oracle.radius_query(X, X, R)
+    compare(gpu, ora)
+    off = gpu.offsets
+    for j in range(0, 5000, 37):
+        ids = set(gpu.indices[off[j]:off[j + 1]].tolist())
+        assert j in ids                                   # every point is its own neighbour
+        for i in list(ids)[:10]:
+            assert j in set(gpu.indices[off[i]:off[i + 1]].tolist())   # symmetry
+    assert 4000 in set(gpu.indices[off[17]:off[18]].tolist())
+
+
+def test_host_pointer_inputs_match_device(snn):
+    rng = np.random.default_rng(3)
+    X = rng.random((3000, 3)).astype(np.float32)
+    Q = rng.random((400, 3)).astype(np.float32)
+    a = run(snn, X, Q, 0.07, host=False)
+    b = run(snn, X, Q, 0.07, host=True)
+    assert np.array_equal(a.offsets, b.offsets)
+    assert np.array_equal(a.indices, b.indices)
+    assert np.array_equal(a.distances, b.distances)
+
+
+# --------------------------------------------------------------------------- adversarial
+def test_exact_boundary_integer_lattice(snn):
+    """Pairs at exactly d = R (3-4-5 triangles) are hits; fp32-exact inputs."""
+    g = np.stack(np.meshgrid(np.arange(-8, 9), np.arange(-8, 9), np.arange(-2, 3), indexing="ij"), -1)
+    X = g.reshape(-1, 3).astype(np.float32)
+    for R in (5.0, 3.0, np.sqrt(2.0), 0.0):
+        gpu = run(snn, X, X[::7], float(R))
+        ora = oracle.radius_query(X, X[::7], float(R))
+        compare(gpu, ora)
+
+
+def test_far_from_origin_cancellation(snn):
+    """Coordinates ~1e4 with R ~ 1e-2: large |x|, tiny distances (centering and the
+    expanded form would lose everything; the direct form + recheck stays exact)."""
+    rng = np.random.default_rng(9)
+    X = (1e4 + rng.random((20000, 3)) * 0.5).astype(np.float32)
+    Q = X[rng.integers(0, 20000, 500)] + rng.standard_normal((500, 3)).astype(np.float32) * 1e-3
+    gpu = run(snn, X, Q.astype(np.float32), 0.02)
+    ora = oracle.radius_query(X, Q.astype(np.float32), 0.02)
+    st = compare(gpu, ora)
+    assert st["oracle_hits"] > 0
+
+
+def test_near_boundary_pairs_fp32(snn):
+    """Queries placed at distance R(1 +- k 2^-24) from data points."""
+    rng = np.random.default_rng(21)
+    X = rng.random((4000, 3)).astype(np.float32) * 4
+    R = 0.25
+    u = rng.standard_normal((3000, 3))
+    u /= np.linalg.norm(u, axis=1, keepdims=True)
+    k = rng.integers(-8, 9, 3000)[:, None]
+    base = X[rng.integers(0, 4000, 3000)].astype(np.float64)
+    Q = (base + u * R * (1 + k * 2.0 ** -24)).astype(np.float32)
+    gpu = run(snn, X, Q, R)
+    ora = oracle.radius_query(X, Q, R)
+    compare(gpu, ora)
+
+
+# --------------------------------------------------------------------------- edge cases
+def test_edge_cases(snn):
+    import paper_2212_07679_b200 as p
+    # n = 1
+    X = np.array([[1.0, 2.0]], dtype=np.float32)
+    r = run(snn, X, None, 0.0)
+    assert r.offsets.tolist() == [0, 1] and r.indices.tolist() == [0]
+    # all identical points: every pair at distance 0
+    X = np.ones((300, 4), dtype=np.float32)
+    r = run(snn, X, None, 0.0)
+    assert r.nnz == 300 * 300 and not r.distances.any()
+    # collinear data (sigma2 = 0): every candidate on the line within R is a hit
+    t = np.linspace(0, 10, 2001)
+    X = np.stack([t, 2 * t, -t], 1).astype(np.float32)
+    compare(run(snn, X, None, 0.05), oracle.radius_query(X, X, 0.05))
+    # m = 0
+    idx = p.Index(_dev(np.random.rand(10, 3).astype(np.float32)))
+    r = idx.query(_dev(np.zeros((0, 3), dtype=np.float32)), 1.0)
+    assert r.offsets.tolist() == [0]
+    # errors
+    with pytest.raises(p.SnnError) as e:
+        idx.query(_dev(np.zeros((2, 4), dtype=np.float32)), 1.0)
+    assert e.value.name == "SNN_ERR_DIM_MISMATCH"
+    with pytest.raises(p.SnnError) as e:
+        idx.query(_dev(np.zeros((2, 3), dtype=np.float32)), -1.0)
+    assert e.value.name == "SNN_ERR_INVALID_ARGUMENT"
+    bad = np.zeros((2, 3), dtype=np.float32)
+    bad[1, 2] = np.nan
+    with pytest.raises(p.SnnError) as e:
+        idx.query(_dev(bad), 1.0)
+    assert e.value.name == "SNN_ERR_NONFINITE"
+    idx.free()
+    with pytest.raises(p.SnnError) as e:
+        p.Index(_dev(np.zeros((0, 3), dtype=np.float32)))
+    assert e.value.name == "SNN_ERR_EMPTY"
+    Xb = np.zeros((5, 3), dtype=np.float32)
+    Xb[2, 0] = np.inf
+    with pytest.raises(p.SnnError) as e:
+        p.Index(_dev(Xb))
+    assert e.value.name == "SNN_ERR_NONFINITE"
+
+
+def test_options_do_not_change_results(snn):
+    import paper_2212_07679_b200 as p
+    rng = np.random.default_rng(31)
+    X = rng.random((6000, 3)).astype(np.float32)
+    Q = rng.random((700, 3)).astype(np.float32)
+    ref = run(snn, X, Q, 0.06)
+    ora = oracle.radius_query(X, Q, 0.06)
+    try:
+        for key, val in [("force_generic", 1), ("chunk", 64), ("query_block", 32), ("power_iters", 1)]:
+            p.snn_set_option(key, val)
+            r = run(snn, X, Q, 0.06)
+            compare(r, ora)
+            p.snn_set_option(key, 0)
+    finally:
+        for key in ("force_generic", "chunk", "query_block", "power_iters"):
+            p.snn_set_option(key, 0)
+    assert ref.nnz == r.nnz
+
+
+# --------------------------------------------------------------------------- index build
+def test_index_build_parity(snn):
+    """Alg. 1 outputs: mean, v1, keys within the rigorous bound, stable sort, gather, xbar."""
+    import paper_2212_07679_b200 as p
+    for d, n in ((3, 50000), (2, 7777), (64, 20000), (13, 3000)):
+        w = workloads.c2(n=n) if d == 3 else None
+        X = w.X if w else np.random.default_rng(d).standard_normal((n, d)).astype(np.float32) * \
+            np.linspace(3, 0.5, d).astype(np.float32)
+        idx = p.Index(_dev(X))
+        arr = idx.arrays()
+        info = arr["info"]
+        mu, v1, keys, perm, xbar, xs = (arr[k].cpu().numpy() for k in ("mu", "v1", "keys", "perm", "xbar", "xs"))
+        assert np.array_equal(xs[:, :d], X[perm])        # gather is a bitwise permutation
+        assert not xs[:, d:].any()
+        ref = oracle.build_index(X)
+        np.testing.assert_allclose(mu, ref["mu"], rtol=1e-12, atol=1e-12)
+        assert abs(float(v1.astype(np.float64) @ ref["v1"])) > 1 - 1e-5
+        assert abs(np.linalg.norm(v1.astype(np.float64)) - 1) < 1e-6
+        # sort: the permutation is the stable argsort of the GPU keys
+        assert np.array_equal(np.sort(perm), np.arange(n))
+        assert np.all(np.diff(keys) >= 0)
+        # keys: exact projection with the stored fp32 v1 and mu, within E_x
+        exact = (X[perm].astype(np.float64) - mu.astype(np.float32).astype(np.float64)) @ v1.astype(np.float64)
+        assert np.max(np.abs(exact - keys)) <= info["key_err"]
+        unsorted = np.empty(n, dtype=np.float32)
+        unsorted[perm] = keys
+        assert np.array_equal(np.argsort(unsorted, kind="stable"), perm)
+        Xc = X[perm].astype(np.float64) - ref["mu"]
+        np.testing.assert_allclose(xbar, 0.5 * np.einsum("ij,ij->i", Xc, Xc), rtol=1e-6)
+        idx.free()
+
+
+def test_sort_ties_and_signed_zero(snn):
+    """Many equal keys (incl. -0.0 vs +0.0) must keep ascending original id."""
+    import paper_2212_07679_b200 as p
+    rng = np.random.default_rng(5)
+    n = 20000
+    X = np.zeros((n, 1), dtype=np.float32)
+    X[:, 0] = rng.integers(-3, 4, n).astype(np.float32)
+    idx = p.Index(_dev(X))
+    perm = idx.arrays()["perm"].cpu().numpy()
+    assert np.array_equal(perm, np.argsort(X[:, 0], kind="stable"))
+    r = idx.query_self(0.0)
+    compare(r, oracle.radius_query(X, X, 0.0))
+    idx.free()
+
+
+# --------------------------------------------------------------------------- configs
+def test_c1_full(snn):
+    w = workloads.c1()
+    gpu = run(snn, w.X, None, w.R)
+    st = compare(gpu, oracle.radius_query(w.X, w.X, w.R))
+    assert 15 < st["oracle_hits"] / w.n < 17.5
+
+
+@pytest.mark.parametrize("name,kw", [("c2", dict(n=60000)), ("c3", dict(n=20000, m=2000)),
+                                     ("c4", dict(n=6000, m=300)), ("c5", dict(n=40000))])
+def test_scaled_configs_full_parity(snn, name, kw):
+    """Same recipes at sizes the oracle finishes in seconds (several tiles + ragged tails)."""
+    w = workloads.CONFIGS[name](**kw)
+    R = w.R if w.R is not None else {"c2": 0.5866, "c3": 1.8134, "c4": 5.948}[name]
+    gpu = run(snn, w.X, w.Q, R)
+    compare(gpu, oracle.radius_query(w.X, w.queries, R))
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4"])
+def test_full_size_sampled_parity(snn, name):
+    """BASELINE.json sizes, default launch configuration; oracle on sampled queries."""
+    w = workloads.CONFIGS[name]()
+    gpu = run(snn, w.X, w.Q, w.R)
+    rng = np.random.default_rng(0)
+    k = {"c2": 400, "c3": 300, "c4": 40}[name]
+    rows = np.sort(rng.choice(w.m, k, replace=False))
+    ora = oracle.radius_query(w.X, w.queries[rows], w.R)
+    st = compare(gpu, ora, rows_subset=rows)
+    assert st["oracle_hits"] > 0
+    # whole-result properties at full size
+    assert gpu.offsets[0] == 0 and np.all(np.diff(gpu.offsets) >= 0)
+    if w.Q is None:
+        assert np.all(np.diff(gpu.offsets) >= 1)      # self-membership
