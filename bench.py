@@ -246,6 +246,8 @@ def run_gpu(args):
     clocks = clk.stop(t_host0, t_host1)
     launches = snn.snn_launch_count() - l0
     prof = {f: snn.snn_profile_read(f) for f in ("build", "window_count", "window_write", "query")}
+    overflow = snn.snn_profile_read("overflow")["units"]
+    lost = snn.snn_profile_read("lost")["units"]
     snn.snn_profile_enable(False)
     torch.cuda.synchronize()
     if world > 1:
@@ -285,9 +287,9 @@ def run_gpu(args):
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
     peak_alu = fp32_alu_peak_tflops(sm_max, n_sm)
-    kms = prof["window_count"]["ms"] + prof["window_write"]["ms"]
-    klaunch = prof["window_count"]["launches"] + prof["window_write"]["launches"]
-    kunits = prof["window_count"]["units"] + prof["window_write"]["units"]
+    kms = prof["window_count"]["ms"]
+    klaunch = prof["window_count"]["launches"]
+    kunits = prof["window_count"]["units"]
     flop_per_pair = 3 * w.d - 1             # eq:ip1 flop count
     achieved = (flop_per_pair * kunits / klaunch) / (kms / klaunch * 1e-3) / 1e12 if klaunch else 0.0
     traffic = None
@@ -296,7 +298,7 @@ def run_gpu(args):
         traffic = tr.get(args.config, {}).get("window_pass_dram_bytes_per_launch")
     except Exception:
         pass
-    roofline = {"kernel": "window_lowd (K8 count + write passes)", "bound": "alu",
+    roofline = {"kernel": "window_lowd<float,3,0> (K8 scan pass: count + record hits)", "bound": "alu",
                 "achieved": achieved, "peak": peak_alu, "unit": "TFLOP/s",
                 "frac": achieved / peak_alu if peak_alu else None, "traffic": traffic,
                 "peak_source": f"FP32 FMA issue peak at {sm_max:.0f} MHz x {n_sm} SMs "
@@ -312,7 +314,7 @@ def run_gpu(args):
             "config": config_block(w, args),
             "build_ms": prof["build"]["ms"] / max(1, prof["build"]["launches"]),
             "query_ms": prof["query"]["ms"] / max(1, prof["query"]["launches"]),
-            "nnz": nnz,
+            "nnz": nnz, "overflow_records": overflow, "fix_items": lost,
             "breakdown_ms_per_step": {k: v["ms"] / args.steps for k, v in prof.items()},
             "clocks": clocks, "gpu_launches": launches,
             "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": h2d,

@@ -64,7 +64,8 @@ typedef struct {
     int64_t n;
     int32_t d;
     int32_t dtype;             /* snn_dtype                                        */
-    int32_t ld;                /* padded row stride (elements) of the sorted copy  */
+    int32_t ld;                /* row stride (elements) of the sorted copy; 0 = AoSoA4:
+                                  element (i, k) at xs[(i/4)*4*d + k*4 + i%4] (d <= 8) */
     int32_t power_iters;       /* power iterations used for v1                     */
     double sigma1;             /* top singular value of the centered data          */
     double key_err;            /* rigorous bound E_x on |computed key - exact key|  */
@@ -147,7 +148,11 @@ uint64_t snn_launch_count(void);
  *   ms        summed device milliseconds,      launches  number of bracketed launches,
  *   units     work units processed (window passes: candidate pairs evaluated; build:
  *             points indexed), summed.
- * Families: "build", "window_count", "window_write", "query" (whole query call).
+ * Families: "build"; "window_count" (low d: the scan pass that counts and records hits;
+ * generic d: the count pass); "window_write" (low d: CSR compaction + overflow fix,
+ * units = hits; generic d: the recomputing write pass); "query" (whole query call);
+ * "overflow" (units = hit records that went to the overflow list in the last low-d query);
+ * "lost" (units = work items re-run by the fix pass in the last low-d query).
  * Unknown family -> SNN_ERR_INVALID_ARGUMENT. */
 snn_status snn_profile_enable(int on);
 snn_status snn_profile_read(const char *family, double *ms, uint64_t *launches, double *units);
@@ -157,6 +162,11 @@ snn_status snn_profile_read(const char *family, double *ms, uint64_t *launches, 
  *   "query_block"    queries per block for the low-d kernel (32..256, multiple of 32)
  *   "chunk"          candidates per work item (multiple of 64)
  *   "power_iters"    cap on power iterations (>= 1)
+ *   "cap"            hit-record slots per (work item, query) in the low-d scan pass
+ *                    (1..1024); further records go to a global overflow list
+ *   "ovf_records"    capacity of that overflow list (entries that do not fit are
+ *                    recomputed by a fix pass)
+ * "force_generic" is read by snn_build (it fixes the sorted copy's layout).
  * Returns SNN_ERR_INVALID_ARGUMENT for an unknown key or bad value. */
 snn_status snn_set_option(const char *key, int64_t value);
 

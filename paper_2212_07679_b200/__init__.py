@@ -244,12 +244,17 @@ def index_arrays(index) -> dict:
     info = snn_index_info(index)
     n, d, ld = info["n"], info["d"], info["ld"]
     xs_t = "<f8" if info["dtype"] == SNN_F64 else "<f4"
+    if ld == 0:   # AoSoA4: element (i, k) at xs[(i/4)*4d + k*4 + i%4]
+        n_pad = (n + 3) // 4 * 4
+        xs = device_view(info["xs"], (n_pad // 4, d, 4), xs_t).permute(0, 2, 1).reshape(n_pad, d)[:n]
+    else:
+        xs = device_view(info["xs"], (n, ld), xs_t)
     return {"mu": device_view(info["mu"], (d,), "<f8").clone(),
             "v1": device_view(info["v1"], (d,), "<f4").clone(),
             "keys": device_view(info["keys"], (n,), "<f4").clone(),
             "perm": device_view(info["perm"], (n,), "<i4").clone(),
             "xbar": device_view(info["xbar"], (n,), "<f4").clone(),
-            "xs": device_view(info["xs"], (n, ld), xs_t).clone(),
+            "xs": xs.clone(),
             "info": info}
 
 

@@ -26,7 +26,11 @@ struct Options {
     int query_block = 256;
     int chunk = 2048;
     int power_iters = 1000;
+    int cap = 64;
+    int32_t ovf_rec_cap = 1 << 20;
+    int variant = 1;
 };
+static std::atomic<int64_t> g_last_ovf{0}, g_last_lost{0};
 static Options g_opt;
 
 static thread_local std::string t_err;
@@ -148,7 +152,12 @@ struct Pinned {
 };
 static thread_local Pinned t_pinned;
 
-int row_stride(int d) { return d == 1 ? 1 : d == 2 ? 2 : (int)round_up(d, 4); }
+// row stride of the sorted copy: 0 = AoSoA4 layout (low-d kernels), else padded row-major
+int row_stride(int d) {
+    if (lowd_supported(d) && !g_opt.force_generic) return 0;
+    return d == 1 ? 1 : d == 2 ? 2 : (int)round_up(d, 4);
+}
+int64_t row_elems(int d, int ld) { return ld ? ld : d; }
 
 }  // namespace snn
 
@@ -173,6 +182,18 @@ snn_status snn_profile_enable(int on) {
 snn_status snn_profile_read(const char *family, double *ms, uint64_t *launches, double *units) {
     if (!family) return fail(SNN_ERR_INVALID_ARGUMENT, "NULL family");
     prof_drain();
+    if (strcmp(family, "overflow") == 0) {   // hit-slot overflows of the last low-d query
+        if (ms) *ms = 0.0;
+        if (launches) *launches = 0;
+        if (units) *units = (double)g_last_ovf.load();
+        return SNN_OK;
+    }
+    if (strcmp(family, "lost") == 0) {   // items re-run by the fix pass in the last query
+        if (ms) *ms = 0.0;
+        if (launches) *launches = 0;
+        if (units) *units = (double)g_last_lost.load();
+        return SNN_OK;
+    }
     for (int f = 0; f < F_N; ++f) {
         if (strcmp(family, kFamNames[f]) == 0) {
             if (ms) *ms = g_prof.ms[f];
@@ -201,6 +222,24 @@ snn_status snn_set_option(const char *key, int64_t value) {
         if (value == 0) value = 2048;
         if (value < 64 || value > 8192 || value % 64) return fail(SNN_ERR_INVALID_ARGUMENT, "chunk must be 64..8192, multiple of 64");
         g_opt.chunk = (int)value;
+        return SNN_OK;
+    }
+    if (k == "cap") {
+        if (value == 0) value = 64;
+        if (value < 1 || value > 1024) return fail(SNN_ERR_INVALID_ARGUMENT, "cap must be 1..1024");
+        g_opt.cap = (int)value;
+        return SNN_OK;
+    }
+    if (k == "variant") {
+        if (value == 0) value = 1;
+        if (value < 1 || value > 2) return fail(SNN_ERR_INVALID_ARGUMENT, "variant must be 1 or 2");
+        g_opt.variant = (int)value;
+        return SNN_OK;
+    }
+    if (k == "ovf_records") {
+        if (value == 0) value = 1 << 20;
+        if (value < 1 || value > (int64_t(1) << 30)) return fail(SNN_ERR_INVALID_ARGUMENT, "ovf_records must be 1..2^30");
+        g_opt.ovf_rec_cap = (int32_t)value;
         return SNN_OK;
     }
     if (k == "power_iters") {
@@ -242,7 +281,7 @@ snn_status snn_build(const void *X, int64_t n, int32_t d, snn_dtype dt, void *st
         if (_e != cudaSuccess) { free_index(idx); return cuda_fail(_e, where); } \
     } while (0)
     uint8_t *xs_bytes = nullptr;
-    CKI(own(&xs_bytes, (size_t)idx->n_pad * idx->ld * es), "alloc Xs");
+    CKI(own(&xs_bytes, (size_t)idx->n_pad * row_elems(d, idx->ld) * es), "alloc Xs");
     idx->Xs = xs_bytes;
     CKI(own(&idx->keys, (size_t)n), "alloc keys");
     CKI(own(&idx->perm, (size_t)n), "alloc perm");
@@ -387,7 +426,7 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
         CK(ws.alloc(&qk_raw, (size_t)m), "alloc");
         CK(ws.alloc(&qk, (size_t)m), "alloc");
         CK(ws.alloc(&qp, (size_t)m), "alloc");
-        CK(ws.alloc(&qs, (size_t)m * ld * es), "alloc");
+        CK(ws.alloc(&qs, (size_t)round_up(m, 4) * row_elems(D, ld) * es), "alloc");
         CK(ws.alloc(&sort_tmp, radix_sort_temp_bytes(m)), "alloc");
         CK(cudaMemsetAsync(qsums, 0, D * 8, s), "memset");
         CK(cudaMemsetAsync(qmax, 0, D * 4, s), "memset");
@@ -396,10 +435,10 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
         launch_query_key_err(D, f64, qmax, idx->mu_d, idx->mu_f, idx->v_d, idx->v_f, eqd, s);
         launch_keys(Qd, f64, m, D, idx->mu_d, idx->mu_f, idx->v_d, idx->v_f, qk_raw, s);
         radix_sort_pairs(qk_raw, nullptr, qk, reinterpret_cast<uint32_t *>(qp), m, sort_tmp, s);
-        launch_gather(Qd, f64, m, D, ld, m, reinterpret_cast<const uint32_t *>(qp), idx->mu_d, qs, nullptr, s);
+        launch_gather(Qd, f64, m, D, ld, round_up(m, 4), reinterpret_cast<const uint32_t *>(qp), idx->mu_d, qs, nullptr, s);
         Qs = qs; qkeys = qk; qperm = qp; eq = eqd;
     }
-    const bool generic = g_opt.force_generic || !lowd_supported(D);
+    const bool generic = ld != 0;
     const int B = generic ? 64 : g_opt.query_block;
     const int chunk = generic ? 1024 : g_opt.chunk;
     const int64_t nblocks = ceil_div(m, B);
@@ -429,9 +468,22 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
     const double pairs_eval = (double)*reinterpret_cast<unsigned long long *>(hp + 2);
     if (*reinterpret_cast<int *>(hp + 1)) return fail(SNN_ERR_NONFINITE, "Q contains NaN or Inf");
 
-    int32_t *cnt = nullptr, *row_count = nullptr;
+    int32_t *cnt = nullptr, *pre = nullptr, *row_count = nullptr, *ovf = nullptr;
+    uint16_t *slots = nullptr;
+    OvfRec *ovf_rec = nullptr;
+    const int cap = g_opt.cap;
+    const int32_t ovf_rec_cap = g_opt.ovf_rec_cap;
     CK(ws.alloc(&cnt, (size_t)total_items * B), "alloc counts");
     CK(ws.alloc(&row_count, (size_t)m), "alloc");
+    if (!generic) {
+        CK(ws.alloc(&pre, (size_t)total_items * B), "alloc prefixes");
+        CK(ws.alloc(&slots, (size_t)total_items * B * cap), "alloc hit slots");
+        CK(ws.alloc(&ovf, (size_t)total_items + 2), "alloc");
+        CK(cudaMemsetAsync(ovf + total_items, 0, 8, s), "memset");
+        CK(ws.alloc(&ovf_rec, (size_t)ovf_rec_cap), "alloc overflow records");
+    } else {
+        pre = cnt;   // the generic write pass only needs the prefixes
+    }
     snn_result r = new snn_result_s();
     r->m = m;
     auto bail = [&](cudaError_t e, const char *where) { snn_result_free(r); return cuda_fail(e, where); };
@@ -446,26 +498,36 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
     a.perm = idx->perm; a.qperm = qperm;
     a.blk_lo = blk_lo; a.blk_hi = blk_hi; a.item_start = item_start;
     a.nblocks = nblocks; a.total_items = total_items;
-    a.B = B; a.chunk = chunk; a.generic = generic;
+    a.B = B; a.chunk = chunk;
     a.R2 = R * R;
     thresholds(a.R2, D, &a.T_in, &a.T_out);
-    a.cnt = cnt; a.offsets = r->offsets; a.out_idx = nullptr; a.out_dist = nullptr;
+    a.cnt = cnt; a.pre = pre; a.slots = slots; a.cap = cap;
+    a.ovf_items = ovf; a.ovf_count = ovf ? ovf + total_items : nullptr; a.n_ovf = 0;
+    a.ovf_rec = ovf_rec; a.ovf_rec_count = ovf ? ovf + total_items + 1 : nullptr;
+    a.ovf_rec_cap = ovf_rec_cap; a.n_ovf_rec = 0;
+    a.offsets = r->offsets; a.out_idx = nullptr; a.out_dist = nullptr;
     a.sm_count = sms;
+    a.variant = g_opt.variant;
     if (total_items == 0) {
         cudaMemsetAsync(row_count, 0, (size_t)m * 4, s);
     } else {
         const int ctok = prof_begin(F_COUNT, s);
-        launch_window_pass(false, a, s);                                           // K8 count
+        if (generic) launch_generic_pass(false, a, s);                           // K8 count
+        else launch_lowd_scan(a, s);                                             // K8 scan
         prof_end(ctok, s, pairs_eval);
-        launch_row_totals(cnt, item_start, m, B, qperm, row_count, s);             // K11
+        launch_row_totals(cnt, pre, item_start, m, B, qperm, row_count, s);      // K11
     }
     exclusive_scan_i32_to_i64(row_count, r->offsets, m, scan_tmp, s);
     {
         cudaError_t e = cudaMemcpyAsync(hp, r->offsets + m, 8, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess && a.ovf_count)
+            e = cudaMemcpyAsync(hp + 1, a.ovf_count, 8, cudaMemcpyDeviceToHost, s);
         if (e == cudaSuccess) e = cudaStreamSynchronize(s);
         if (e != cudaSuccess) return bail(e, "query count");
     }
     r->nnz = hp[0];
+    a.n_ovf = a.ovf_count ? reinterpret_cast<int32_t *>(hp + 1)[0] : 0;
+    a.n_ovf_rec = a.ovf_count ? reinterpret_cast<int32_t *>(hp + 1)[1] : 0;
     {
         void *p = nullptr;
         cudaError_t e = cudaMallocAsync(&p, (size_t)(r->nnz > 0 ? r->nnz : 1) * 4, s);
@@ -478,9 +540,16 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
     a.out_idx = r->indices; a.out_dist = r->distances;
     if (r->nnz > 0) {
         const int wtok = prof_begin(F_WRITE, s);
-        launch_window_pass(true, a, s);                                            // K8 write
-        prof_end(wtok, s, pairs_eval);
+        if (generic) {
+            launch_generic_pass(true, a, s);                                     // K8 write
+        } else {
+            launch_lowd_compact(a, s);                                           // K11 compact
+            launch_lowd_fix(a, s);                                               // overflow fix
+        }
+        prof_end(wtok, s, generic ? pairs_eval : (double)r->nnz);
     }
+    g_last_ovf = a.n_ovf_rec;
+    g_last_lost = a.n_ovf;
     prof_end(qtok, s, (double)m);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return bail(e, "launch");

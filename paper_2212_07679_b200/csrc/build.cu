@@ -520,6 +520,38 @@ __global__ void __launch_bounds__(kThreads) gather_small(const T *__restrict__ X
     }
 }
 
+// AoSoA4 layout for the low-d query kernel: rows are grouped by 4; group g stores
+// coordinate k of its 4 rows contiguously: Xs[g*4*D + k*4 + r].  A chunk of candidates
+// starting at a multiple of 4 rows is one contiguous byte range (bulk-copy friendly) and
+// each coordinate of 4 consecutive candidates is one 16-byte shared-memory vector.
+template <typename T, int D>
+__global__ void __launch_bounds__(kThreads) gather_aosoa4(const T *__restrict__ X, int64_t n,
+                                                          int64_t n_pad,
+                                                          const uint32_t *__restrict__ perm,
+                                                          const double *__restrict__ mu_d,
+                                                          T *__restrict__ Xs, float *xbar) {
+    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n_pad;
+         i += (int64_t)gridDim.x * kThreads) {
+        const int64_t g = i >> 2, r = i & 3;
+        double h = 0.0;
+        if (i < n) {
+            const int64_t src = perm[i];
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+                T v = X[src * D + k];
+                Xs[g * 4 * D + k * 4 + r] = v;
+                double t = (double)v - mu_d[k];
+                h = fma(t, t, h);
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < D; ++k) Xs[g * 4 * D + k * 4 + r] = (T)NAN;   // never a hit
+            h = NAN;
+        }
+        if (xbar) xbar[i] = (float)(0.5 * h);
+    }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kThreads) gather_generic(const T *__restrict__ X, int64_t n,
                                                            int d, int ld, int64_t n_pad,
@@ -639,6 +671,15 @@ void launch_gather(const void *X, bool f64, int64_t n, int d, int ld, int64_t n_
                    const uint32_t *perm, const double *mu_d, void *Xs, float *xbar,
                    cudaStream_t s) {
     const int g = grid_for(n_pad);
+    if (ld == 0) {   // AoSoA4 layout (low-d kernels)
+#define CASE(D)                                                                               \
+    case D:                                                                                   \
+        if (f64) SNN_LAUNCH((gather_aosoa4<double, D>), g, kThreads, 0, s, (const double *)X, n, n_pad, perm, mu_d, (double *)Xs, xbar); \
+        else SNN_LAUNCH((gather_aosoa4<float, D>), g, kThreads, 0, s, (const float *)X, n, n_pad, perm, mu_d, (float *)Xs, xbar); \
+        return;
+        switch (d) { SNN_SMALL_D_CASES(CASE) default: return; }
+#undef CASE
+    }
 #define CASE(D, LD)                                                                           \
     if (d == D && ld == LD) {                                                                 \
         if (f64) SNN_LAUNCH((gather_small<double, D, LD>), g, kThreads, 0, s, (const double *)X, n, n_pad, perm, mu_d, (double *)Xs, xbar); \

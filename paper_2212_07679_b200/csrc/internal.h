@@ -34,7 +34,8 @@ void launch_query_key_err(int d, bool f64, const uint32_t *maxabs_bits, const do
 void launch_keys(const void *X, bool f64, int64_t n, int d, const double *mu_d,
                  const float *mu_f, const double *v_d, const float *v_f, float *keys,
                  cudaStream_t s);
-// K5: Xs[i] = X[perm[i]] (stride ld, zero pad columns; rows [n, n_pad) = NaN sentinels) and
+// K5: Xs[i] = X[perm[i]] (stride ld, zero pad columns; rows [n, n_pad) = NaN sentinels;
+// ld == 0 selects the AoSoA4 layout Xs[(i/4)*4d + k*4 + i%4], d <= 8) and
 // xbar[i] = 0.5 * ||X[perm[i]] - mu||^2 (fp64 accumulate, stored fp32; nullable).
 void launch_gather(const void *X, bool f64, int64_t n, int d, int ld, int64_t n_pad,
                    const uint32_t *perm, const double *mu_d, void *Xs, float *xbar,

@@ -14,8 +14,11 @@
 //                          ambiguous pairs are re-evaluated in fp64 with the oracle's exact
 //                          operation sequence (no FMA), so membership is bit-identical;
 //                        - fp64 data: the oracle's fp64 sequence directly.
-//                      Count pass -> per-(item, query) counts; write pass -> CSR entries
-//                      (original id, (float)sqrt(fp64 s)).
+//                      Low d (<= 8, AoSoA4 rows): ONE scan pass counts and records hits
+//                      (chunk-local indices, up to `cap` per (item, query)); a compaction
+//                      kernel writes the CSR (original id, (float)sqrt(fp64 s)); a fix pass
+//                      recomputes only the rare overflowed (item, query) entries.
+//                      Generic d: count pass + recomputing write pass.
 //  Candidate rows of a chunk are contiguous ("memory efficient to access
 //  X(J,:)") and are staged into shared memory by the TMA bulk-copy engine
 //  (cp.async.bulk + mbarrier), double-buffered across the persistent item loop.
@@ -81,34 +84,150 @@ __device__ __forceinline__ void locate(const PassArgs &a, int64_t item, int64_t 
     c1 = min(c0 + a.chunk, a.blk_hi[b]);
 }
 
-template <typename T, int LD>
-__device__ __forceinline__ void load_row(const T *buf, int j, T (&x)[LD]) {
-    if constexpr (sizeof(T) * LD == 16) {
-        int4 v = reinterpret_cast<const int4 *>(buf)[j];
-        *reinterpret_cast<int4 *>(x) = v;
-    } else if constexpr (sizeof(T) * LD == 32) {
-        int4 v0 = reinterpret_cast<const int4 *>(buf)[2 * j];
-        int4 v1 = reinterpret_cast<const int4 *>(buf)[2 * j + 1];
-        reinterpret_cast<int4 *>(x)[0] = v0;
-        reinterpret_cast<int4 *>(x)[1] = v1;
-    } else if constexpr (sizeof(T) * LD == 8) {
-        *reinterpret_cast<int2 *>(x) = reinterpret_cast<const int2 *>(buf)[j];
-    } else {
+// ---------------------------------------------------------------------------- K8 low d
+// One thread per query (registers); candidates in the AoSoA4 layout are broadcast from
+// shared memory 4 at a time: coordinate k of candidates 4g..4g+3 is one float4.  The
+// fp32 direct form is evaluated with packed f32x2 instructions (two candidates per
+// instruction; FADD2 takes the query coordinate as a scalar broadcast operand), then one
+// min-test per 4 candidates sends the rare near/inside pairs to the classification path.
+__device__ __forceinline__ uint64_t f2pack(float x, float y) {
+    float2 v = make_float2(x, y);
+    return *reinterpret_cast<uint64_t *>(&v);
+}
+__device__ __forceinline__ float2 f2unpack(uint64_t u) { return *reinterpret_cast<float2 *>(&u); }
+__device__ __forceinline__ uint64_t f2add(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ uint64_t f2mul(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ uint64_t f2fma(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+
+// Per-4-candidate hit mask -> output.  MODE 0 records (g << 4 | mask) in the entry's
+// slot list, or, once `cap` slots are used, appends (entry, hits-before, record) to the
+// global overflow list; MODE 1 (fix) writes the CSR entries directly.
+__device__ __forceinline__ float lane4(const float4 &v, int i) {   // i is unrolled (static)
+    return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
+}
+
+// Hit masks -> output.  MODE 0 records (g << 4 | mask) in the entry's slot list, or, once
+// `cap` slots are used, appends (entry, hits-before, record) to the global overflow list;
+// MODE 1 (fix) writes the CSR entries directly.
+template <typename T, int D, int MODE>
+struct Emitter {
+    const PassArgs &a;
+    uint16_t *slot;
+    int64_t e, c0, pos;
+    int32_t c = 0, rec = 0;
+    bool lost = false;
+    __device__ __forceinline__ void record(int g, uint32_t mask) {   // MODE 0
+        const uint32_t v = ((uint32_t)g << 4) | mask;
+        if (rec < a.cap) {
+            slot[rec] = (uint16_t)v;
+        } else {
+            const int32_t k = atomicAdd(a.ovf_rec_count, 1);
+            if (k < a.ovf_rec_cap) a.ovf_rec[k] = OvfRec{(int32_t)e, c, v};
+            else lost = true;
+        }
+        ++rec;
+        c += __popc(mask);
+    }
+    __device__ __forceinline__ void write(int64_t j, double s) {      // MODE 1
+        a.out_idx[pos] = a.perm[j];
+        a.out_dist[pos] = (float)sqrt(s);
+        ++pos;
+        ++c;
+    }
+};
+
+// Classify the 4 fp32 d^2 of group g (candidates of xv): sure-in (<= T_in), ambiguous
+// (<= T_out: decided by the oracle-order fp64 sequence), else out.
+template <typename E, int D, int MODE>
+__device__ __forceinline__ void classify4(E &em, int g, const float4 (&xv)[D], float d0, float d1,
+                                          float d2, float d3, float T_in, float T_out, double R2,
+                                          const float (&q)[D]) {
+    const float dv[4] = {d0, d1, d2, d3};
+    uint32_t m_in = 0;
 #pragma unroll
-        for (int k = 0; k < LD; ++k) x[k] = buf[j * LD + k];
+    for (int i = 0; i < 4; ++i) {
+        if (dv[i] <= T_out) {
+            bool hit = dv[i] <= T_in;
+            double s = 0.0;
+            if (MODE == 1 || !hit) {
+                float x[D];
+#pragma unroll
+                for (int k = 0; k < D; ++k) x[k] = lane4(xv[k], i);
+                s = sqdist_exact(x, q, D);
+                if (!hit) hit = s <= R2;
+            }
+            if (hit) {
+                if (MODE == 0) m_in |= 1u << i;
+                else em.write(em.c0 + g * 4 + i, s);
+            }
+        }
+    }
+    if (MODE == 0 && m_in) em.record(g, m_in);
+}
+
+__device__ __forceinline__ uint32_t mask4(float d0, float d1, float d2, float d3, float T) {
+    return (uint32_t)(d0 <= T) | ((uint32_t)(d1 <= T) << 1) | ((uint32_t)(d2 <= T) << 2) |
+           ((uint32_t)(d3 <= T) << 3);
+}
+
+// near-boundary candidates of a group (bits of amb): the oracle-order fp64 sequence decides
+template <int D>
+__device__ __forceinline__ uint32_t resolve4(uint32_t amb, const float4 (&xv)[D], const float (&q)[D],
+                                             double R2) {
+    uint32_t m = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        if (amb & (1u << i)) {
+            float x[D];
+#pragma unroll
+            for (int k = 0; k < D; ++k) x[k] = lane4(xv[k], i);
+            if (sqdist_exact(x, q, D) <= R2) m |= 1u << i;
+        }
+    }
+    return m;
+}
+
+// packed fp32 direct form for the 4 candidates of one group: (lo, hi) = d^2 of (0,1), (2,3)
+template <int D>
+__device__ __forceinline__ void group_d2(const float4 (&xv)[D], const uint64_t (&nq)[D],
+                                         uint64_t &lo, uint64_t &hi) {
+    uint64_t t = f2add(f2pack(xv[0].x, xv[0].y), nq[0]);
+    lo = f2mul(t, t);
+    t = f2add(f2pack(xv[0].z, xv[0].w), nq[0]);
+    hi = f2mul(t, t);
+#pragma unroll
+    for (int k = 1; k < D; ++k) {
+        t = f2add(f2pack(xv[k].x, xv[k].y), nq[k]);
+        lo = f2fma(t, t, lo);
+        t = f2add(f2pack(xv[k].z, xv[k].w), nq[k]);
+        hi = f2fma(t, t, hi);
     }
 }
 
-// ---------------------------------------------------------------------------- K8 low d
-// One thread per query (registers), candidates broadcast from shared memory.
-template <typename T, int D, int LD, bool WRITE>
+// MODE 0 = scan (count + record hits); MODE 1 = fix (recompute entries flagged lost and
+// write them straight into the CSR).
+template <typename T, int D, int MODE, int G>
 __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
-    T *buf[2] = {reinterpret_cast<T *>(smem), reinterpret_cast<T *>(smem) + (size_t)a.chunk * LD};
-    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + (size_t)2 * a.chunk * LD * sizeof(T));
     const int tid = threadIdx.x;
     const T *Xs = static_cast<const T *>(a.Xs);
     const T *Qs = static_cast<const T *>(a.Qs);
+    const size_t buf_bytes = (size_t)a.chunk * D * sizeof(T);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + 2 * buf_bytes);
+    const int64_t n_work = MODE == 0 ? a.total_items : a.n_ovf;
+    auto item_of = [&](int64_t w) -> int64_t { return MODE == 0 ? w : (int64_t)a.ovf_items[w]; };
     if (tid == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
@@ -118,91 +237,201 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
     auto issue = [&](int64_t item, int sidx) {
         int64_t b, c0, c1;
         locate(a, item, b, c0, c1);
-        const uint32_t bytes = (uint32_t)((c1 - c0) * LD * sizeof(T));
+        const uint32_t bytes = (uint32_t)((c1 - c0) * D * sizeof(T));
         fence_proxy_async_smem();
         mbar_arrive_expect_tx(&bar[sidx], bytes);
-        bulk_g2s(buf[sidx], Xs + c0 * LD, bytes, &bar[sidx]);
+        bulk_g2s(smem + sidx * buf_bytes, Xs + c0 * D, bytes, &bar[sidx]);
     };
     uint32_t phase[2] = {0u, 0u};
-    int64_t item = blockIdx.x;
-    if (tid == 0 && item < a.total_items) issue(item, 0);
+    int64_t w = blockIdx.x;
+    if (tid == 0 && w < n_work) issue(item_of(w), 0);
     const float T_in = a.T_in, T_out = a.T_out;
     const double R2 = a.R2;
-    for (int it = 0; item < a.total_items; item += gridDim.x, ++it) {
+    for (int it = 0; w < n_work; w += gridDim.x, ++it) {
         const int sidx = it & 1;
-        const int64_t next = item + gridDim.x;
-        if (tid == 0 && next < a.total_items) issue(next, sidx ^ 1);
+        const int64_t item = item_of(w);
+        const int64_t wn = w + gridDim.x;
+        if (tid == 0 && wn < n_work) issue(item_of(wn), sidx ^ 1);
         int64_t b, c0, c1;
         locate(a, item, b, c0, c1);
         const int64_t sp = b * a.B + tid;
-        const bool active = sp < a.m;
+        bool active = sp < a.m;
+        const int64_t e = item * a.B + tid;
         T q[D];
-        int64_t pos = 0;
-        int32_t qid = 0;
-        if (active) {
-#pragma unroll
-            for (int k = 0; k < D; ++k) q[k] = Qs[sp * LD + k];
-            if (WRITE) {
-                qid = a.qperm[sp];
-                pos = a.offsets[qid] + a.cnt[item * a.B + tid];
-            }
-        } else {
-#pragma unroll
-            for (int k = 0; k < D; ++k) q[k] = (T)0;
+        Emitter<T, D, MODE> em{a, a.slots + (size_t)e * a.cap, e, c0, 0};
+        if (MODE == 1) {
+            active = active && a.cnt[e] < 0;   // lost-entry flag (sign bit)
+            if (active) em.pos = a.offsets[a.qperm[sp]] + a.pre[e];
         }
+#pragma unroll
+        for (int k = 0; k < D; ++k) q[k] = active ? Qs[(sp >> 2) * 4 * D + k * 4 + (sp & 3)] : (T)0;
         mbar_wait(&bar[sidx], phase[sidx]);
         phase[sidx] ^= 1u;
-        int32_t c = 0;
         if (active) {
-            const T *xb = buf[sidx];
-            const int len = (int)(c1 - c0);
-#pragma unroll 4
-            for (int j = 0; j < len; ++j) {
-                T x[LD];
-                load_row<T, LD>(xb, j, x);
-                if constexpr (sizeof(T) == 4) {
-                    float t = x[0] - q[0];
-                    float d2 = t * t;
+            const int ngroups = (int)((c1 - c0) >> 2);
+            if constexpr (sizeof(T) == 4) {
+                const float4 *g4 = reinterpret_cast<const float4 *>(smem + sidx * buf_bytes);
+                uint64_t nq[D];
 #pragma unroll
-                    for (int k = 1; k < D; ++k) { t = x[k] - q[k]; d2 = fmaf(t, t, d2); }
-                    if (d2 <= T_out) {
-                        bool hit = d2 <= T_in;
-                        double s = 0.0;
-                        if (WRITE || !hit) {
-                            s = sqdist_exact(x, q, D);
-                            if (!hit) hit = s <= R2;
-                        }
-                        if (hit) {
-                            if (WRITE) {
-                                a.out_idx[pos] = a.perm[c0 + j];
-                                a.out_dist[pos] = (float)sqrt(s);
-                                ++pos;
-                            } else {
-                                ++c;
-                            }
-                        }
-                    }
-                } else {
-                    double s = 0.0;
-#pragma unroll
-                    for (int k = 0; k < D; ++k) {
-                        double t = __dsub_rn(x[k], q[k]);
-                        s = __dadd_rn(s, __dmul_rn(t, t));
-                    }
-                    if (s <= R2) {
-                        if (WRITE) {
-                            a.out_idx[pos] = a.perm[c0 + j];
-                            a.out_dist[pos] = (float)sqrt(s);
-                            ++pos;
+                for (int k = 0; k < D; ++k) nq[k] = f2pack(-q[k], -q[k]);
+                int g = 0;
+                if (MODE == 0) {
+                    // straight-line hit path (taken by ~1 lane of a warp at a time): 4-bit
+                    // masks, slot pointer precomputed; ambiguous pairs and slot overflow
+                    // are rare out-of-line cases
+                    uint16_t *const slotp = em.slot;
+                    const int cap = a.cap;
+                    auto emit0 = [&](int gg, uint32_t m) {
+                        const uint32_t v = ((uint32_t)gg << 4) | m;
+                        if (em.rec < cap) {
+                            slotp[em.rec] = (uint16_t)v;
                         } else {
-                            ++c;
+                            const int32_t k = atomicAdd(a.ovf_rec_count, 1);
+                            if (k < a.ovf_rec_cap) a.ovf_rec[k] = OvfRec{(int32_t)e, em.c, v};
+                            else em.lost = true;
+                        }
+                        ++em.rec;
+                        em.c += __popc(m);
+                    };
+                    for (; G == 2 && g + 1 < ngroups; g += 2) {
+                        float4 xa[D], xb[D];
+#pragma unroll
+                        for (int k = 0; k < D; ++k) { xa[k] = g4[g * D + k]; xb[k] = g4[(g + 1) * D + k]; }
+                        uint64_t la, ha, lb, hb;
+                        group_d2<D>(xa, nq, la, ha);
+                        group_d2<D>(xb, nq, lb, hb);
+                        const float2 pa = f2unpack(la), qa = f2unpack(ha), pb = f2unpack(lb), qb = f2unpack(hb);
+                        const float mn = fminf(fminf(fminf(pa.x, pa.y), fminf(qa.x, qa.y)),
+                                               fminf(fminf(pb.x, pb.y), fminf(qb.x, qb.y)));
+                        if (mn <= T_out) {
+                            uint32_t ia = mask4(pa.x, pa.y, qa.x, qa.y, T_in);
+                            uint32_t ib = mask4(pb.x, pb.y, qb.x, qb.y, T_in);
+                            const uint32_t oa = mask4(pa.x, pa.y, qa.x, qa.y, T_out);
+                            const uint32_t ob = mask4(pb.x, pb.y, qb.x, qb.y, T_out);
+                            if ((ia ^ oa) | (ib ^ ob)) {
+                                ia |= resolve4<D>(oa & ~ia, xa, q, R2);
+                                ib |= resolve4<D>(ob & ~ib, xb, q, R2);
+                            }
+                            if (ia) emit0(g, ia);
+                            if (ib) emit0(g + 1, ib);
                         }
                     }
+                    for (; g < ngroups; ++g) {
+                        float4 xa[D];
+#pragma unroll
+                        for (int k = 0; k < D; ++k) xa[k] = g4[g * D + k];
+                        uint64_t la, ha;
+                        group_d2<D>(xa, nq, la, ha);
+                        const float2 pa = f2unpack(la), qa = f2unpack(ha);
+                        if (fminf(fminf(pa.x, pa.y), fminf(qa.x, qa.y)) <= T_out) {
+                            uint32_t ia = mask4(pa.x, pa.y, qa.x, qa.y, T_in);
+                            const uint32_t oa = mask4(pa.x, pa.y, qa.x, qa.y, T_out);
+                            if (ia ^ oa) ia |= resolve4<D>(oa & ~ia, xa, q, R2);
+                            if (ia) emit0(g, ia);
+                        }
+                    }
+                } else {   // fix pass: per-candidate classification, direct CSR writes
+                    for (; g < ngroups; ++g) {
+                        float4 xa[D];
+#pragma unroll
+                        for (int k = 0; k < D; ++k) xa[k] = g4[g * D + k];
+                        uint64_t la, ha;
+                        group_d2<D>(xa, nq, la, ha);
+                        const float2 pa = f2unpack(la), qa = f2unpack(ha);
+                        if (fminf(fminf(pa.x, pa.y), fminf(qa.x, qa.y)) <= T_out)
+                            classify4<decltype(em), D, MODE>(em, g, xa, pa.x, pa.y, qa.x, qa.y, T_in, T_out, R2, q);
+                    }
+                }
+            } else {   // fp64 data: the oracle's sequence directly
+                const T *gb = reinterpret_cast<const T *>(smem + sidx * buf_bytes);
+                for (int g = 0; g < ngroups; ++g) {
+                    uint32_t m = 0;
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        double s = 0.0;
+#pragma unroll
+                        for (int k = 0; k < D; ++k) {
+                            double t = __dsub_rn(gb[g * 4 * D + k * 4 + i], q[k]);
+                            s = __dadd_rn(s, __dmul_rn(t, t));
+                        }
+                        if (s <= R2) {
+                            if (MODE == 0) m |= 1u << i;
+                            else em.write(c0 + g * 4 + i, s);
+                        }
+                    }
+                    if (MODE == 0 && m) em.record(g, m);
                 }
             }
         }
-        if (!WRITE) a.cnt[item * a.B + tid] = c;
-        __syncthreads();
+        if (MODE == 0) {
+            const bool lost = active && em.lost;
+            if (tid < a.B) a.cnt[e] = em.c | (lost ? (int32_t)0x80000000 : 0);
+            if (__syncthreads_or(lost) && tid == 0) a.ovf_items[atomicAdd(a.ovf_count, 1)] = (int32_t)item;
+        } else {
+            __syncthreads();
+        }
+    }
+}
+
+// Compaction of the recorded hits into the CSR: original ids via pi and distances as
+// (float)sqrt of the oracle-order fp64 squared distance.  One CTA per item; one thread
+// per (item, query) entry expands its slot records (the first `cap` records).
+template <typename T, int D>
+__device__ __forceinline__ void expand_record(const PassArgs &a, int64_t c0, uint32_t v,
+                                              const T (&q)[D], int64_t &pos) {
+    const T *Xs = static_cast<const T *>(a.Xs);
+    const int64_t g = c0 / 4 + (v >> 4);
+    uint32_t mask = v & 15u;
+    while (mask) {
+        const int i = __ffs(mask) - 1;
+        mask &= mask - 1;
+        T x[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) x[k] = Xs[g * 4 * D + k * 4 + i];
+        a.out_idx[pos] = a.perm[g * 4 + i];
+        a.out_dist[pos] = (float)sqrt(sqdist_exact(x, q, D));
+        ++pos;
+    }
+}
+
+template <typename T, int D>
+__global__ void __launch_bounds__(256) compact_lowd(PassArgs a) {
+    const T *Qs = static_cast<const T *>(a.Qs);
+    for (int64_t item = blockIdx.x; item < a.total_items; item += gridDim.x) {
+        int64_t b, c0, c1;
+        locate(a, item, b, c0, c1);
+        const int64_t sp = b * a.B + threadIdx.x;
+        if (sp >= a.m) continue;
+        const int64_t e = item * a.B + threadIdx.x;
+        const int32_t cv = a.cnt[e];
+        if (cv <= 0) continue;   // no hits, or lost entry (sign bit): the fix pass writes it
+        int64_t pos = a.offsets[a.qperm[sp]] + a.pre[e];
+        const int64_t end = pos + cv;
+        T q[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) q[k] = Qs[(sp >> 2) * 4 * D + k * 4 + (sp & 3)];
+        const uint16_t *slot = a.slots + (size_t)e * a.cap;
+        for (int r = 0; r < a.cap && pos < end; ++r) expand_record<T, D>(a, c0, slot[r], q, pos);
+    }
+}
+
+// Records beyond `cap` (global overflow list): one thread per record.
+template <typename T, int D>
+__global__ void __launch_bounds__(256) compact_overflow(PassArgs a, int64_t n_rec) {
+    const T *Qs = static_cast<const T *>(a.Qs);
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n_rec;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const OvfRec r = a.ovf_rec[k];
+        if (a.cnt[r.e] < 0) continue;   // lost entry: rewritten by the fix pass
+        const int64_t item = r.e / a.B, t = r.e % a.B;
+        int64_t b, c0, c1;
+        locate(a, item, b, c0, c1);
+        const int64_t sp = b * a.B + t;
+        int64_t pos = a.offsets[a.qperm[sp]] + a.pre[r.e] + r.before;
+        T q[D];
+#pragma unroll
+        for (int kk = 0; kk < D; ++kk) q[kk] = Qs[(sp >> 2) * 4 * D + kk * 4 + (sp & 3)];
+        expand_record<T, D>(a, c0, r.v, q, pos);
     }
 }
 
@@ -228,7 +457,7 @@ __global__ void __launch_bounds__(256) window_generic(PassArgs a) {
         if (tid < kGB) {
             s_cnt[tid] = 0;
             if (WRITE && sp0 + tid < a.m)
-                s_base[tid] = a.offsets[a.qperm[sp0 + tid]] + a.cnt[item * kGB + tid];
+                s_base[tid] = a.offsets[a.qperm[sp0 + tid]] + a.pre[item * kGB + tid];
         }
         __syncthreads();
         for (int64_t cb = c0; cb < c1; cb += kGB) {
@@ -327,15 +556,15 @@ __global__ void __launch_bounds__(256) window_generic(PassArgs a) {
     }
 }
 
-__global__ void row_totals(int32_t *cnt, const int64_t *item_start, int64_t m, int B,
-                           const int32_t *qperm, int32_t *row_count) {
+__global__ void row_totals(const int32_t *cnt, int32_t *pre, const int64_t *item_start, int64_t m,
+                           int B, const int32_t *qperm, int32_t *row_count) {
     const int64_t sp = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (sp >= m) return;
     const int64_t b = sp / B, t = sp % B;
     int32_t run = 0;
     for (int64_t item = item_start[b]; item < item_start[b + 1]; ++item) {
-        int32_t c = cnt[item * B + t];
-        cnt[item * B + t] = run;
+        int32_t c = cnt[item * B + t] & 0x7fffffff;   // bit 31 = hit-slot overflow flag
+        pre[item * B + t] = run;
         run += c;
     }
     row_count[qperm[sp]] = run;
@@ -351,20 +580,14 @@ int persistent_grid(K kernel, int threads, size_t smem, int64_t items, int sm_co
     return (int)(g < 1 ? 1 : g);
 }
 
-template <typename T, int D, int LD>
-void run_lowd(bool write, const PassArgs &a, cudaStream_t s) {
-    const size_t smem = (size_t)2 * a.chunk * LD * sizeof(T) + 16;
-    if (write) {
-        auto k = window_lowd<T, D, LD, true>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        int g = persistent_grid(k, a.B, smem, a.total_items, a.sm_count);
-        SNN_LAUNCH(k, g, a.B, smem, s, a);
-    } else {
-        auto k = window_lowd<T, D, LD, false>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        int g = persistent_grid(k, a.B, smem, a.total_items, a.sm_count);
-        SNN_LAUNCH(k, g, a.B, smem, s, a);
-    }
+template <typename T, int D, int MODE>
+void run_lowd(const PassArgs &a, cudaStream_t s) {
+    const size_t smem = (size_t)2 * a.chunk * D * sizeof(T) + 16;
+    auto k = a.variant == 1 ? window_lowd<T, D, MODE, 1> : window_lowd<T, D, MODE, 2>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int64_t work = MODE == 0 ? a.total_items : a.n_ovf;
+    int g = persistent_grid(k, a.B, smem, work, a.sm_count);
+    SNN_LAUNCH(k, g, a.B, smem, s, a);
 }
 
 template <typename T>
@@ -390,27 +613,56 @@ void launch_block_windows(const WindowSpec &w, cudaStream_t s) {
     SNN_LAUNCH(block_windows, (int)ceil_div(nb, 256), 256, 0, s, w);
 }
 
-void launch_window_pass(bool write, const PassArgs &a, cudaStream_t s) {
+#define SNN_LOWD_DISPATCH(FN)                                                          \
+    switch (a.d) {                                                                     \
+        case 1: if (a.f64) FN(double, 1); else FN(float, 1); return;                   \
+        case 2: if (a.f64) FN(double, 2); else FN(float, 2); return;                   \
+        case 3: if (a.f64) FN(double, 3); else FN(float, 3); return;                   \
+        case 4: if (a.f64) FN(double, 4); else FN(float, 4); return;                   \
+        case 5: if (a.f64) FN(double, 5); else FN(float, 5); return;                   \
+        case 6: if (a.f64) FN(double, 6); else FN(float, 6); return;                   \
+        case 7: if (a.f64) FN(double, 7); else FN(float, 7); return;                   \
+        case 8: if (a.f64) FN(double, 8); else FN(float, 8); return;                   \
+        default: return;                                                               \
+    }
+
+void launch_lowd_scan(const PassArgs &a, cudaStream_t s) {
     if (a.total_items == 0) return;
-    if (a.generic) {
-        if (a.f64) run_generic<double>(write, a, s); else run_generic<float>(write, a, s);
-        return;
-    }
-#define CASE(D, LD)                                                                        \
-    case D:                                                                                \
-        if (a.f64) run_lowd<double, D, LD>(write, a, s); else run_lowd<float, D, LD>(write, a, s); \
-        return;
-    switch (a.d) {
-        CASE(1, 1) CASE(2, 2) CASE(3, 4) CASE(4, 4) CASE(5, 8) CASE(6, 8) CASE(7, 8) CASE(8, 8)
-        default: break;
-    }
-#undef CASE
+#define FN(T, D) run_lowd<T, D, 0>(a, s)
+    SNN_LOWD_DISPATCH(FN)
+#undef FN
 }
 
-void launch_row_totals(int32_t *cnt, const int64_t *item_start, int64_t m, int B,
-                       const int32_t *qperm, int32_t *row_count, cudaStream_t s) {
+void launch_lowd_fix(const PassArgs &a, cudaStream_t s) {
+    if (a.n_ovf == 0) return;
+#define FN(T, D) run_lowd<T, D, 1>(a, s)
+    SNN_LOWD_DISPATCH(FN)
+#undef FN
+}
+
+void launch_lowd_compact(const PassArgs &a, cudaStream_t s) {
+    if (a.total_items == 0) return;
+    const int g = (int)(a.total_items < 148 * 32 ? a.total_items : 148 * 32);
+    const int64_t n_rec = a.n_ovf_rec < a.ovf_rec_cap ? a.n_ovf_rec : a.ovf_rec_cap;
+    const int go = (int)(ceil_div(n_rec, 256) < 148 * 8 ? ceil_div(n_rec, 256) : 148 * 8);
+#define FN(T, D)                                                                         \
+    do {                                                                                 \
+        SNN_LAUNCH((compact_lowd<T, D>), g, a.B, 0, s, a);                               \
+        if (n_rec > 0) SNN_LAUNCH((compact_overflow<T, D>), go, 256, 0, s, a, n_rec);    \
+    } while (0)
+    SNN_LOWD_DISPATCH(FN)
+#undef FN
+}
+
+void launch_generic_pass(bool write, const PassArgs &a, cudaStream_t s) {
+    if (a.total_items == 0) return;
+    if (a.f64) run_generic<double>(write, a, s); else run_generic<float>(write, a, s);
+}
+
+void launch_row_totals(const int32_t *cnt, int32_t *pre, const int64_t *item_start, int64_t m,
+                       int B, const int32_t *qperm, int32_t *row_count, cudaStream_t s) {
     if (m == 0) return;
-    SNN_LAUNCH(row_totals, (int)ceil_div(m, 256), 256, 0, s, cnt, item_start, m, B, qperm, row_count);
+    SNN_LAUNCH(row_totals, (int)ceil_div(m, 256), 256, 0, s, cnt, pre, item_start, m, B, qperm, row_count);
 }
 
 }  // namespace snn

@@ -4,6 +4,12 @@
 #include <stdint.h>
 
 namespace snn {
+// A hit record beyond the per-entry slot capacity (low-d scan pass).
+struct OvfRec {
+    int32_t e;        // entry = item * B + thread
+    int32_t before;   // hits of this entry recorded before this record
+    uint32_t v;       // group << 4 | 4-bit hit mask
+};
 
 // K7: per-block union window of B consecutive key-sorted queries (Alg. 2 l.4,
 // PAPER.md:296; eq:lower PAPER.md:142-153; batching PAPER.md:218-219).
@@ -23,11 +29,11 @@ struct WindowSpec {
 };
 void launch_block_windows(const WindowSpec &w, cudaStream_t s);
 
-// K8: windowed exact radius test over the work list (count pass / write pass).
+// K8: windowed exact radius test over the work list.
 struct PassArgs {
-    const void *Xs;         // n_pad x ld sorted index rows (original coordinates)
-    const void *Qs;         // m x ld sorted query rows
-    int ld;
+    const void *Xs;         // sorted index rows (original coordinates); layout below
+    const void *Qs;         // sorted query rows, same layout
+    int ld;                 // row stride (generic path); 0 = AoSoA4 layout (low-d path)
     int d;
     bool f64;
     int64_t m;
@@ -36,22 +42,40 @@ struct PassArgs {
     const int64_t *blk_lo, *blk_hi, *item_start;
     int64_t nblocks, total_items;
     int B, chunk;
-    bool generic;           // generic-d FFMA tile kernel (B must be 64)
     float T_in, T_out;      // fp32 sure-in / sure-out thresholds on the fp32 d^2
     double R2;              // R*R (fp64), the oracle's threshold
-    int32_t *cnt;           // total_items x B: counts (count pass) -> exclusive prefixes
-    const int64_t *offsets; // m+1 CSR offsets (write pass)
+    int32_t *cnt;           // total_items x B hit counts (count / scan pass)
+    int32_t *pre;           // total_items x B exclusive per-row prefixes (after row totals)
+    uint16_t *slots;        // low-d scan pass: total_items x B x cap chunk-local hit indices
+    int cap;
+    OvfRec *ovf_rec;        // low-d: records beyond `cap` (global overflow list)
+    int32_t *ovf_rec_count; // device counter for ovf_rec
+    int32_t ovf_rec_cap;    // capacity of ovf_rec
+    int64_t n_ovf_rec;      // host copy
+    int32_t *ovf_items;     // low-d: ids of items with a lost entry (ovf_rec full)
+    int32_t *ovf_count;     // device counter for ovf_items
+    int64_t n_ovf;          // host copy (fix pass)
+    const int64_t *offsets; // m+1 CSR offsets (write / compaction / fix)
     int32_t *out_idx;
     float *out_dist;
     int sm_count;
+    int variant;            // low-d inner loop: groups of 4 candidates per iteration (1 or 2)
 };
-void launch_window_pass(bool write, const PassArgs &a, cudaStream_t s);
 
-// K11 helper: per-row totals over a block's items; cnt -> exclusive per-item prefixes;
-// row_count[qperm[sp]] = total.
-void launch_row_totals(int32_t *cnt, const int64_t *item_start, int64_t m, int B,
-                       const int32_t *qperm, int32_t *row_count, cudaStream_t s);
+bool lowd_supported(int d);   // d handled by the register-resident low-d kernels
 
-bool lowd_supported(int d);   // d handled by the register-resident low-d kernel
+// Low-d path (AoSoA4, d <= 8): one scan pass records hits, then compaction, then a fix
+// pass that recomputes only (item, query) entries whose hits overflowed `cap`.
+void launch_lowd_scan(const PassArgs &a, cudaStream_t s);
+void launch_lowd_compact(const PassArgs &a, cudaStream_t s);
+void launch_lowd_fix(const PassArgs &a, cudaStream_t s);
+
+// Generic-d path (row-major, any d): count pass + write pass (write recomputes).
+void launch_generic_pass(bool write, const PassArgs &a, cudaStream_t s);
+
+// K11 helper: per-row totals over a block's items; pre = exclusive per-item prefixes
+// (pre may alias cnt); row_count[qperm[sp]] = total.
+void launch_row_totals(const int32_t *cnt, int32_t *pre, const int64_t *item_start, int64_t m,
+                       int B, const int32_t *qperm, int32_t *row_count, cudaStream_t s);
 
 }  // namespace snn

@@ -186,13 +186,18 @@ def test_options_do_not_change_results(snn):
     ref = run(snn, X, Q, 0.06)
     ora = oracle.radius_query(X, Q, 0.06)
     try:
-        for key, val in [("force_generic", 1), ("chunk", 64), ("query_block", 32), ("power_iters", 1)]:
-            p.snn_set_option(key, val)
+        settings = [[("force_generic", 1)], [("chunk", 64)], [("query_block", 32)],
+                    [("power_iters", 1)], [("cap", 1)], [("cap", 3)],
+                    [("cap", 1), ("ovf_records", 5)], [("cap", 2), ("ovf_records", 1), ("chunk", 128)]]
+        for setting in settings:
+            for key, val in setting:
+                p.snn_set_option(key, val)
             r = run(snn, X, Q, 0.06)
             compare(r, ora)
-            p.snn_set_option(key, 0)
+            for key, _ in setting:
+                p.snn_set_option(key, 0)
     finally:
-        for key in ("force_generic", "chunk", "query_block", "power_iters"):
+        for key in ("force_generic", "chunk", "query_block", "power_iters", "cap", "ovf_records"):
             p.snn_set_option(key, 0)
     assert ref.nnz == r.nnz
 
