@@ -1,8 +1,185 @@
-// dbscan.cu -- K12 (placeholder until the GPU DBSCAN lands).
+// dbscan.cu -- K12: DBSCAN with SNN as the neighbourhood backend.
+//
+// Readings (C18): closed eps-balls including the point itself; core iff
+// |N_eps(i)| >= min_pts; clusters = connected components of core points under
+// eps-adjacency; a non-core point with >= 1 core neighbour takes the cluster of its
+// smallest-original-id core neighbour; other points are noise (-1); clusters are numbered
+// 0..K-1 by increasing smallest original core id.  All neighbourhood tests use the exact
+// windowed classification of the radius query (bit-identical to the fp64 oracle).
+//
+// Pipeline on the sorted index (neighbour lists are never materialised):
+//   windows (K7, R = eps) -> M_COUNT pass -> per-point counts -> core flags
+//   -> M_UNION pass (core i, core j > i: lock-free union-find) -> flatten
+//   -> per-root smallest original id -> flag + scan over original ids = canonical ranks
+//   -> core labels -> M_BORDER pass (non-core points) -> labels scattered to original order.
+#include <math.h>
+
+#include "common.cuh"
 #include "index.h"
+#include "query.h"
 
 namespace snn {
-snn_status dbscan_impl(snn_index, double, int32_t, int32_t *, int32_t *, cudaStream_t) {
-    return fail(SNN_ERR_UNSUPPORTED, "snn_dbscan: not implemented yet");
+namespace {
+
+__global__ void init_core(const int32_t *count, int64_t n, int32_t min_pts, uint8_t *core,
+                          int32_t *parent, int32_t *minid, int32_t *best) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        core[i] = count[i] >= min_pts;
+        parent[i] = (int32_t)i;
+        minid[i] = 0x7fffffff;
+        best[i] = 0x7fffffff;
+    }
 }
+
+__device__ __forceinline__ int32_t find_root(const int32_t *p, int32_t x) {
+    int32_t px = p[x];
+    while (px != x) { x = px; px = p[x]; }
+    return x;
+}
+
+// flatten + smallest original id per root
+__global__ void flatten(int32_t *parent, const uint8_t *core, const int32_t *perm, int64_t n,
+                        int32_t *minid) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        if (!core[i]) continue;
+        const int32_t r = find_root(parent, (int32_t)i);
+        parent[i] = r;
+        atomicMin(&minid[r], perm[i]);
+    }
+}
+
+// flag[minid of each root] = 1 (original-id space), for the canonical ranking
+__global__ void flag_roots(const int32_t *parent, const uint8_t *core, const int32_t *minid,
+                           int64_t n, int32_t *flag) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        if (core[i] && parent[i] == i) flag[minid[i]] = 1;
+}
+
+// labels of core points (sorted order) and inverse permutation
+__global__ void core_labels(const int32_t *parent, const uint8_t *core, const int32_t *minid,
+                            const int64_t *rank, const int32_t *perm, int64_t n, int32_t *lab,
+                            int32_t *inv) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        lab[i] = core[i] ? (int32_t)rank[minid[parent[i]]] : -1;
+        inv[perm[i]] = (int32_t)i;
+    }
+}
+
+// border points: cluster of the smallest-id core neighbour; scatter to original order
+__global__ void final_labels(const int32_t *lab, const uint8_t *core, const int32_t *best,
+                             const int32_t *inv, const int32_t *perm, int64_t n, int32_t *out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t l = lab[i];
+        if (!core[i]) l = (best[i] != 0x7fffffff) ? lab[inv[best[i]]] : -1;
+        out[perm[i]] = l;
+    }
+}
+
+int grid_n(int64_t n) {
+    int64_t g = ceil_div(n, 256);
+    return (int)(g < 148 * 16 ? (g < 1 ? 1 : g) : 148 * 16);
+}
+
+}  // namespace
+
+snn_status dbscan_impl(snn_index idx, double eps, int32_t min_pts, int32_t *labels,
+                       int32_t *n_clusters, cudaStream_t s) {
+    if (idx->ld != 0)
+        return fail(SNN_ERR_UNSUPPORTED, "snn_dbscan: only the low-d layout (d <= 8) is supported");
+    const int64_t n = idx->n;
+    const bool f64 = idx->dt == SNN_F64;
+    const int B = 256, chunk = 2048;
+    const int64_t nblocks = ceil_div(n, B);
+    Workspace ws(s);
+#define CKD(expr, where)                                       \
+    do {                                                       \
+        cudaError_t _e = (expr);                               \
+        if (_e != cudaSuccess) return cuda_fail(_e, where);    \
+    } while (0)
+    int64_t *blk_lo, *blk_hi, *nitems, *item_start, *hbuf;
+    unsigned long long *pairs;
+    uint8_t *scan_tmp;
+    CKD(ws.alloc(&blk_lo, (size_t)nblocks), "alloc");
+    CKD(ws.alloc(&blk_hi, (size_t)nblocks), "alloc");
+    CKD(ws.alloc(&nitems, (size_t)nblocks), "alloc");
+    CKD(ws.alloc(&item_start, (size_t)nblocks + 1), "alloc");
+    CKD(ws.alloc(&pairs, 1), "alloc");
+    CKD(ws.alloc(&scan_tmp, scan_temp_bytes(n > nblocks ? n : nblocks)), "alloc");
+    CKD(cudaMallocHost(&hbuf, 16), "pinned");
+    struct HostFree { void *p; ~HostFree() { cudaFreeHost(p); } } hf{hbuf};
+    CKD(cudaMemsetAsync(pairs, 0, 8, s), "memset");
+    WindowSpec w;
+    w.qkeys = idx->keys; w.m = n; w.B = B; w.keys = idx->keys; w.n = n; w.n_pad = idx->n_pad;
+    w.R = eps;
+    w.wnorm = idx->stats + (f64 ? ST_WNORM_D : ST_WNORM_F);
+    w.ex = idx->stats + (f64 ? ST_EX_D : ST_EX_F);
+    w.eq = w.ex;
+    w.chunk = chunk;
+    w.blk_lo = blk_lo; w.blk_hi = blk_hi; w.nitems = nitems; w.pairs = pairs;
+    launch_block_windows(w, s);
+    exclusive_scan_i64(nitems, item_start, nblocks, scan_tmp, s);
+    CKD(cudaMemcpyAsync(hbuf, item_start + nblocks, 8, cudaMemcpyDeviceToHost, s), "D2H");
+    CKD(cudaStreamSynchronize(s), "dbscan windows");
+    const int64_t total_items = hbuf[0];
+
+    int32_t *cnt, *count, *parent, *minid, *best, *flag, *lab, *inv, *out;
+    int64_t *rank;
+    uint8_t *core;
+    CKD(ws.alloc(&cnt, (size_t)total_items * B), "alloc");
+    CKD(ws.alloc(&count, (size_t)n), "alloc");
+    CKD(ws.alloc(&core, (size_t)n), "alloc");
+    CKD(ws.alloc(&parent, (size_t)n), "alloc");
+    CKD(ws.alloc(&minid, (size_t)n), "alloc");
+    CKD(ws.alloc(&best, (size_t)n), "alloc");
+    CKD(ws.alloc(&flag, (size_t)n), "alloc");
+    CKD(ws.alloc(&rank, (size_t)n + 1), "alloc");
+    CKD(ws.alloc(&lab, (size_t)n), "alloc");
+    CKD(ws.alloc(&inv, (size_t)n), "alloc");
+    const bool dev_out = is_device_ptr(labels);
+    if (dev_out) out = labels; else CKD(ws.alloc(&out, (size_t)n), "alloc");
+
+    PassArgs a{};
+    a.Xs = idx->Xs; a.Qs = idx->Xs; a.ld = 0; a.d = idx->d; a.f64 = f64; a.m = n;
+    a.perm = idx->perm; a.qperm = idx->perm;
+    a.blk_lo = blk_lo; a.blk_hi = blk_hi; a.item_start = item_start;
+    a.nblocks = nblocks; a.total_items = total_items;
+    a.B = B; a.chunk = chunk;
+    a.R2 = eps * eps;
+    {   // same rigorous fp32 thresholds as the radius query (api.cu)
+        const int d = idx->d;
+        const double u32 = ldexp(1.0, -24), u64 = ldexp(1.0, -53);
+        const double g32 = (d + 2) * u32 / (1.0 - (d + 2) * u32);
+        const double g64 = (d + 2) * u64 / (1.0 - (d + 2) * u64);
+        const double eta = (2.0 * d + 2.0) * ldexp(1.0, -149);
+        const double tin = a.R2 * (1.0 - g32) / (1.0 + g64) * (1.0 - 1e-12) - eta;
+        const double tout = a.R2 * (1.0 + g32) / (1.0 - g64) * (1.0 + 1e-12) + eta;
+        float fi = (float)tin, fo = (float)tout;
+        if ((double)fi > tin) fi = nextafterf(fi, -INFINITY);
+        if ((double)fo < tout) fo = nextafterf(fo, INFINITY);
+        a.T_in = fi; a.T_out = fo;
+    }
+    a.cnt = cnt; a.pre = cnt; a.cap = 0; a.variant = 1;
+    a.sm_count = idx->sm_count;
+    a.core = core; a.parent = parent; a.best = best;
+
+    launch_lowd_mode(2, a, s);                                              // counts
+    launch_row_totals(cnt, cnt, item_start, n, B, nullptr, count, s);
+    SNN_LAUNCH(init_core, grid_n(n), 256, 0, s, count, n, min_pts, core, parent, minid, best);
+    launch_lowd_mode(3, a, s);                                              // unions
+    SNN_LAUNCH(flatten, grid_n(n), 256, 0, s, parent, core, idx->perm, n, minid);
+    CKD(cudaMemsetAsync(flag, 0, (size_t)n * 4, s), "memset");
+    SNN_LAUNCH(flag_roots, grid_n(n), 256, 0, s, parent, core, minid, n, flag);
+    exclusive_scan_i32_to_i64(flag, rank, n, scan_tmp, s);                  // canonical ranks
+    SNN_LAUNCH(core_labels, grid_n(n), 256, 0, s, parent, core, minid, rank, idx->perm, n, lab, inv);
+    launch_lowd_mode(4, a, s);                                              // border points
+    SNN_LAUNCH(final_labels, grid_n(n), 256, 0, s, lab, core, best, inv, idx->perm, n, out);
+    if (!dev_out) CKD(cudaMemcpyAsync(labels, out, (size_t)n * 4, cudaMemcpyDeviceToHost, s), "D2H labels");
+    CKD(cudaMemcpyAsync(hbuf + 1, rank + n, 8, cudaMemcpyDeviceToHost, s), "D2H K");
+    CKD(cudaGetLastError(), "launch");
+    CKD(cudaStreamSynchronize(s), "dbscan");
+    *n_clusters = (int32_t)hbuf[1];
+    return SNN_OK;
+#undef CKD
+}
+
 }  // namespace snn

@@ -218,6 +218,40 @@ __device__ __forceinline__ void group_d2(const float4 (&xv)[D], const uint64_t (
 
 // MODE 0 = scan (count + record hits); MODE 1 = fix (recompute entries flagged lost and
 // write them straight into the CSR).
+// Kernel modes of the windowed pass (same exact classification in every mode):
+//   M_SCAN   count + record hits (radius query, CSR path)
+//   M_FIX    recompute entries whose records were lost; write CSR directly
+//   M_COUNT  DBSCAN: |N_eps(i)| (self included)
+//   M_UNION  DBSCAN: union core i with every core neighbour j > i (sorted positions)
+//   M_BORDER DBSCAN: for non-core i, the smallest original id among core neighbours
+enum { M_SCAN = 0, M_FIX = 1, M_COUNT = 2, M_UNION = 3, M_BORDER = 4 };
+
+// Lock-free union-find over sorted positions (parent[x] <= x: every link goes from the
+// larger root to the smaller, so chains decrease and path halving is race-benign).
+__device__ __forceinline__ int32_t uf_rep(volatile int32_t *p, int32_t x) {
+    int32_t cur = p[x];
+    if (cur != x) {
+        int32_t next, prev = x;
+        while (cur > (next = p[cur])) {
+            p[prev] = next;
+            prev = cur;
+            cur = next;
+        }
+    }
+    return cur;
+}
+__device__ __forceinline__ void uf_unite(int32_t *p, int32_t a, int32_t b) {
+    volatile int32_t *vp = p;
+    int32_t ra = uf_rep(vp, a), rb = uf_rep(vp, b);
+    while (ra != rb) {
+        if (ra < rb) { const int32_t t = ra; ra = rb; rb = t; }
+        const int32_t old = atomicCAS(&p[ra], ra, rb);
+        if (old == ra) break;
+        ra = uf_rep(vp, old);
+        rb = uf_rep(vp, rb);
+    }
+}
+
 template <typename T, int D, int MODE, int G>
 __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
@@ -226,8 +260,8 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
     const T *Qs = static_cast<const T *>(a.Qs);
     const size_t buf_bytes = (size_t)a.chunk * D * sizeof(T);
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem + 2 * buf_bytes);
-    const int64_t n_work = MODE == 0 ? a.total_items : a.n_ovf;
-    auto item_of = [&](int64_t w) -> int64_t { return MODE == 0 ? w : (int64_t)a.ovf_items[w]; };
+    const int64_t n_work = MODE == M_FIX ? a.n_ovf : a.total_items;
+    auto item_of = [&](int64_t w) -> int64_t { return MODE == M_FIX ? (int64_t)a.ovf_items[w] : w; };
     if (tid == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
@@ -259,10 +293,13 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
         const int64_t e = item * a.B + tid;
         T q[D];
         Emitter<T, D, MODE> em{a, a.slots + (size_t)e * a.cap, e, c0, 0};
-        if (MODE == 1) {
+        if (MODE == M_FIX) {
             active = active && a.cnt[e] < 0;   // lost-entry flag (sign bit)
             if (active) em.pos = a.offsets[a.qperm[sp]] + a.pre[e];
         }
+        if (MODE == M_UNION) active = active && a.core[sp] && c1 - 1 > sp;   // pairs j > i only
+        if (MODE == M_BORDER) active = active && !a.core[sp];
+        int32_t best = 0x7fffffff;   // M_BORDER: smallest original id of a core neighbour
 #pragma unroll
         for (int k = 0; k < D; ++k) q[k] = active ? Qs[(sp >> 2) * 4 * D + k * 4 + (sp & 3)] : (T)0;
         mbar_wait(&bar[sidx], phase[sidx]);
@@ -275,22 +312,38 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
 #pragma unroll
                 for (int k = 0; k < D; ++k) nq[k] = f2pack(-q[k], -q[k]);
                 int g = 0;
-                if (MODE == 0) {
+                if (MODE != M_FIX) {
                     // straight-line hit path (taken by ~1 lane of a warp at a time): 4-bit
                     // masks, slot pointer precomputed; ambiguous pairs and slot overflow
                     // are rare out-of-line cases
                     uint16_t *const slotp = em.slot;
                     const int cap = a.cap;
                     auto emit0 = [&](int gg, uint32_t m) {
-                        const uint32_t v = ((uint32_t)gg << 4) | m;
-                        if (em.rec < cap) {
-                            slotp[em.rec] = (uint16_t)v;
-                        } else {
-                            const int32_t k = atomicAdd(a.ovf_rec_count, 1);
-                            if (k < a.ovf_rec_cap) a.ovf_rec[k] = OvfRec{(int32_t)e, em.c, v};
-                            else em.lost = true;
+                        if (MODE == M_SCAN) {
+                            const uint32_t v = ((uint32_t)gg << 4) | m;
+                            if (em.rec < cap) {
+                                slotp[em.rec] = (uint16_t)v;
+                            } else {
+                                const int32_t k = atomicAdd(a.ovf_rec_count, 1);
+                                if (k < a.ovf_rec_cap) a.ovf_rec[k] = OvfRec{(int32_t)e, em.c, v};
+                                else em.lost = true;
+                            }
+                            ++em.rec;
+                        } else if (MODE == M_UNION) {
+                            while (m) {
+                                const int i = __ffs(m) - 1;
+                                m &= m - 1;
+                                const int64_t j = c0 + gg * 4 + i;
+                                if (j > sp && a.core[j]) uf_unite(a.parent, (int32_t)sp, (int32_t)j);
+                            }
+                        } else if (MODE == M_BORDER) {
+                            while (m) {
+                                const int i = __ffs(m) - 1;
+                                m &= m - 1;
+                                const int64_t j = c0 + gg * 4 + i;
+                                if (a.core[j]) best = min(best, a.perm[j]);
+                            }
                         }
-                        ++em.rec;
                         em.c += __popc(m);
                     };
                     for (; G == 2 && g + 1 < ngroups; g += 2) {
@@ -330,7 +383,7 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
                             if (ia) emit0(g, ia);
                         }
                     }
-                } else {   // fix pass: per-candidate classification, direct CSR writes
+                } else {   // M_FIX: per-candidate classification, direct CSR writes
                     for (; g < ngroups; ++g) {
                         float4 xa[D];
 #pragma unroll
@@ -355,19 +408,35 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
                             s = __dadd_rn(s, __dmul_rn(t, t));
                         }
                         if (s <= R2) {
-                            if (MODE == 0) m |= 1u << i;
-                            else em.write(c0 + g * 4 + i, s);
+                            if (MODE == M_FIX) em.write(c0 + g * 4 + i, s);
+                            else m |= 1u << i;
                         }
                     }
-                    if (MODE == 0 && m) em.record(g, m);
+                    if (MODE != M_FIX && m) {
+                        if (MODE == M_SCAN) {
+                            em.record(g, m);
+                        } else if (MODE == M_COUNT) {
+                            em.c += __popc(m);
+                        } else {
+                            while (m) {
+                                const int i = __ffs(m) - 1;
+                                m &= m - 1;
+                                const int64_t j = c0 + g * 4 + i;
+                                if (MODE == M_UNION && j > sp && a.core[j]) uf_unite(a.parent, (int32_t)sp, (int32_t)j);
+                                if (MODE == M_BORDER && a.core[j]) best = min(best, a.perm[j]);
+                            }
+                        }
+                    }
                 }
             }
         }
-        if (MODE == 0) {
+        if (MODE == M_SCAN) {
             const bool lost = active && em.lost;
             if (tid < a.B) a.cnt[e] = em.c | (lost ? (int32_t)0x80000000 : 0);
             if (__syncthreads_or(lost) && tid == 0) a.ovf_items[atomicAdd(a.ovf_count, 1)] = (int32_t)item;
         } else {
+            if (MODE == M_COUNT) a.cnt[e] = em.c;
+            if (MODE == M_BORDER && active && best != 0x7fffffff) atomicMin(&a.best[sp], best);
             __syncthreads();
         }
     }
@@ -567,7 +636,7 @@ __global__ void row_totals(const int32_t *cnt, int32_t *pre, const int64_t *item
         pre[item * B + t] = run;
         run += c;
     }
-    row_count[qperm[sp]] = run;
+    row_count[qperm ? qperm[sp] : sp] = run;
 }
 
 template <typename K>
@@ -585,7 +654,7 @@ void run_lowd(const PassArgs &a, cudaStream_t s) {
     const size_t smem = (size_t)2 * a.chunk * D * sizeof(T) + 16;
     auto k = a.variant == 1 ? window_lowd<T, D, MODE, 1> : window_lowd<T, D, MODE, 2>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const int64_t work = MODE == 0 ? a.total_items : a.n_ovf;
+    const int64_t work = MODE == M_FIX ? a.n_ovf : a.total_items;
     int g = persistent_grid(k, a.B, smem, work, a.sm_count);
     SNN_LAUNCH(k, g, a.B, smem, s, a);
 }
@@ -638,6 +707,22 @@ void launch_lowd_fix(const PassArgs &a, cudaStream_t s) {
 #define FN(T, D) run_lowd<T, D, 1>(a, s)
     SNN_LOWD_DISPATCH(FN)
 #undef FN
+}
+
+void launch_lowd_mode(int mode, const PassArgs &a, cudaStream_t s) {
+    if (a.total_items == 0) return;
+    switch (mode) {
+#define FN(T, D) run_lowd<T, D, M_COUNT>(a, s)
+        case M_COUNT: SNN_LOWD_DISPATCH(FN) break;
+#undef FN
+#define FN(T, D) run_lowd<T, D, M_UNION>(a, s)
+        case M_UNION: SNN_LOWD_DISPATCH(FN) break;
+#undef FN
+#define FN(T, D) run_lowd<T, D, M_BORDER>(a, s)
+        case M_BORDER: SNN_LOWD_DISPATCH(FN) break;
+#undef FN
+        default: break;
+    }
 }
 
 void launch_lowd_compact(const PassArgs &a, cudaStream_t s) {

@@ -60,6 +60,10 @@ struct PassArgs {
     float *out_dist;
     int sm_count;
     int variant;            // low-d inner loop: groups of 4 candidates per iteration (1 or 2)
+    // DBSCAN modes (sorted positions)
+    const uint8_t *core;    // core flags
+    int32_t *parent;        // union-find parents
+    int32_t *best;          // M_BORDER: smallest original id of a core neighbour (atomicMin)
 };
 
 bool lowd_supported(int d);   // d handled by the register-resident low-d kernels
@@ -69,12 +73,14 @@ bool lowd_supported(int d);   // d handled by the register-resident low-d kernel
 void launch_lowd_scan(const PassArgs &a, cudaStream_t s);
 void launch_lowd_compact(const PassArgs &a, cudaStream_t s);
 void launch_lowd_fix(const PassArgs &a, cudaStream_t s);
+// DBSCAN passes over the self-query work list: mode 2 = count, 3 = union, 4 = border.
+void launch_lowd_mode(int mode, const PassArgs &a, cudaStream_t s);
 
 // Generic-d path (row-major, any d): count pass + write pass (write recomputes).
 void launch_generic_pass(bool write, const PassArgs &a, cudaStream_t s);
 
 // K11 helper: per-row totals over a block's items; pre = exclusive per-item prefixes
-// (pre may alias cnt); row_count[qperm[sp]] = total.
+// (pre may alias cnt); row_count[qperm[sp]] = total (qperm NULL: row_count[sp]).
 void launch_row_totals(const int32_t *cnt, int32_t *pre, const int64_t *item_start, int64_t m,
                        int B, const int32_t *qperm, int32_t *row_count, cudaStream_t s);
 

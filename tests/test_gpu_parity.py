@@ -282,3 +282,67 @@ def test_full_size_sampled_parity(snn, name):
     assert gpu.offsets[0] == 0 and np.all(np.diff(gpu.offsets) >= 0)
     if w.Q is None:
         assert np.all(np.diff(gpu.offsets) >= 1)      # self-membership
+
+
+# --------------------------------------------------------------------------- DBSCAN (a12)
+def _gpu_dbscan(snn, X, eps, mp):
+    idx = snn.Index(_dev(X))
+    try:
+        return idx.dbscan(eps, mp)
+    finally:
+        idx.free()
+
+
+def test_dbscan_spec_examples_gpu(snn):
+    rng = np.random.default_rng(0)
+    A = np.concatenate([rng.standard_normal((500, 2)) * 0.5,
+                        rng.standard_normal((500, 2)) * 0.5 + 10]).astype(np.float32)
+    lab, K = _gpu_dbscan(snn, A, 1.0, 5)
+    ref, Kr, _ = oracle.dbscan(A, 1.0, 5)
+    assert K == Kr == 2 and np.array_equal(lab, ref)
+    G = np.stack(np.meshgrid(np.arange(10) * 10.0, np.arange(10) * 10.0), -1).reshape(-1, 2).astype(np.float32)
+    lab, K = _gpu_dbscan(snn, G, 0.1, 5)
+    assert K == 0 and (lab == -1).all()
+    lab, K = _gpu_dbscan(snn, A, 1e6, 1)
+    assert K == 1 and (lab == 0).all()
+
+
+@pytest.mark.parametrize("n,seed,box,eps,mp,dt", [(20000, 4, 1000.0, 3.0, 5, np.float32),
+                                                  (15000, 7, 300.0, 3.0, 5, np.float32),
+                                                  (8000, 9, 200.0, 2.5, 4, np.float64),
+                                                  (12000, 11, 150.0, 3.0, 10, np.float32)])
+def test_dbscan_full_parity(snn, n, seed, box, eps, mp, dt):
+    """C5 recipe at oracle-sized n: labels equal the oracle's exactly (canonical numbering)."""
+    w = workloads.c5(n=n, seed=seed, box=box)
+    X = w.X.astype(dt)
+    lab, K = _gpu_dbscan(snn, X, eps, mp)
+    ref, Kr, _ = oracle.dbscan(X, eps, mp)
+    assert K == Kr
+    assert np.array_equal(lab, ref)
+
+
+def test_dbscan_c5_full_size_sampled(snn):
+    """BASELINE config 5 at full size (n = 2M): sampled points checked one by one."""
+    w = workloads.c5()
+    lab, K = _gpu_dbscan(snn, w.X, w.R, w.dbscan_min_pts)
+    assert K >= 1 and lab.max() == K - 1 and lab.min() >= -1
+    rng = np.random.default_rng(1)
+    ids = rng.choice(w.n, 24, replace=False)
+    cnt = oracle.neighbour_counts(w.X, w.R, ids)
+    X64 = w.X.astype(np.float64)
+    for i, c in zip(ids, cnt):
+        s = ((X64 - X64[i]) ** 2).sum(axis=1)          # candidates only; membership via oracle
+        nb = np.nonzero(s <= w.R * w.R * 1.001)[0]
+        res = oracle.radius_query(w.X, w.X[i:i + 1], w.R)
+        nb = np.sort(res["indices"][res["s"] <= res["R2"]])
+        assert len(nb) == c
+        sub = nb if len(nb) <= 24 else np.concatenate([[nb.min()], rng.choice(nb, 23, replace=False)])
+        nbc = oracle.neighbour_counts(w.X, w.R, sub) >= w.dbscan_min_pts
+        if c >= w.dbscan_min_pts:           # core: same cluster as its core neighbours
+            assert lab[i] >= 0
+            assert all(lab[j] == lab[i] for j, isc in zip(sub, nbc) if isc)
+        else:
+            allc = oracle.neighbour_counts(w.X, w.R, nb) >= w.dbscan_min_pts
+            core_nb = nb[allc]
+            expect = lab[core_nb.min()] if len(core_nb) else -1
+            assert lab[i] == expect
