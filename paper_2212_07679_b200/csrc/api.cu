@@ -14,6 +14,7 @@
 #include "common.cuh"
 #include "internal.h"
 #include "query.h"
+#include "tc.h"
 #include "index.h"
 
 namespace snn {
@@ -29,6 +30,9 @@ struct Options {
     int cap = 64;
     int32_t ovf_rec_cap = 1 << 20;
     int variant = 1;
+    int tc = 1;          // use the tcgen05 path for d >= tc_min_d
+    int tc_min_d = 32;
+    int tc_tiles = 8;    // 256-candidate tiles per work item on the tensor-core path
 };
 static std::atomic<int64_t> g_last_ovf{0}, g_last_lost{0};
 static Options g_opt;
@@ -230,6 +234,19 @@ snn_status snn_set_option(const char *key, int64_t value) {
         g_opt.cap = (int)value;
         return SNN_OK;
     }
+    if (k == "tc") { g_opt.tc = value == 0 ? 1 : (value > 0 ? 1 : 0); if (value < 0) g_opt.tc = 0; return SNN_OK; }
+    if (k == "tc_min_d") {
+        if (value == 0) value = 32;
+        if (value < 9 || value > 65536) return fail(SNN_ERR_INVALID_ARGUMENT, "tc_min_d must be 9..65536");
+        g_opt.tc_min_d = (int)value;
+        return SNN_OK;
+    }
+    if (k == "tc_tiles") {
+        if (value == 0) value = 8;
+        if (value < 1 || value > 64) return fail(SNN_ERR_INVALID_ARGUMENT, "tc_tiles must be 1..64");
+        g_opt.tc_tiles = (int)value;
+        return SNN_OK;
+    }
     if (k == "variant") {
         if (value == 0) value = 1;
         if (value < 1 || value > 2) return fail(SNN_ERR_INVALID_ARGUMENT, "variant must be 1 or 2");
@@ -327,6 +344,13 @@ snn_status snn_build(const void *X, int64_t n, int32_t d, snn_dtype dt, void *st
                      sort_tmp, s);                                                 // K4
     launch_gather(Xd, f64, n, d, idx->ld, idx->n_pad, reinterpret_cast<const uint32_t *>(idx->perm),
                   idx->mu_d, idx->Xs, idx->xbar, s);                               // K5
+    if (idx->ld != 0 && g_opt.tc && !g_opt.force_generic && d >= g_opt.tc_min_d) {   // K5': TF32 copy
+        idx->tc = 1;
+        idx->kpad = tc_kpad(d);
+        CKI(own(&idx->Xt, (size_t)n * idx->kpad), "alloc TF32 copy");
+        launch_gather_tf32(Xd, f64, n, d, reinterpret_cast<const uint32_t *>(idx->perm), idx->mu_f,
+                           idx->Xt, idx->xbar, s);
+    }
     prof_end(ptok, s, (double)n);
     CKI(cudaGetLastError(), "launch");
     double *hs = static_cast<double *>(t_pinned.p);
@@ -377,6 +401,145 @@ static snn_status make_empty_result(int64_t m, cudaStream_t s, snn_result *out) 
     return SNN_OK;
 }
 
+// Tensor-core query path (d >= tc_min_d): K7 windows (128-query blocks) -> K9 tcgen05
+// candidate filter -> K10 exact fp64 recheck -> hits sorted (index position, then original
+// query id) with two stable radix passes -> CSR.
+static snn_status query_tc(snn_index idx, Workspace &ws, cudaStream_t s, int sms, int64_t m, double R,
+                           const void *Qs, const float *qkeys, const int32_t *qperm, const double *eq,
+                           const float *Qt, const float *qbar, const int *qflag, snn_result *out) {
+    const bool f64 = idx->dt == SNN_F64;
+    const int D = idx->d, TM = tc_tile_rows(), TN = tc_tile_cols();
+    const int chunk = TN * g_opt.tc_tiles;
+    const int64_t nblocks = ceil_div(m, TM);
+    int64_t *blk_lo, *blk_hi, *nitems, *item_start;
+    unsigned long long *pcount, *wpairs;
+    uint8_t *scan_tmp;
+    CK(ws.alloc(&blk_lo, (size_t)nblocks), "alloc");
+    CK(ws.alloc(&blk_hi, (size_t)nblocks), "alloc");
+    CK(ws.alloc(&nitems, (size_t)nblocks), "alloc");
+    CK(ws.alloc(&item_start, (size_t)nblocks + 1), "alloc");
+    CK(ws.alloc(&pcount, 1), "alloc");
+    CK(ws.alloc(&wpairs, 1), "alloc");
+    CK(cudaMemsetAsync(pcount, 0, 8, s), "memset");
+    CK(cudaMemsetAsync(wpairs, 0, 8, s), "memset");
+    WindowSpec w;
+    w.qkeys = qkeys; w.m = m; w.B = TM; w.keys = idx->keys; w.n = idx->n; w.n_pad = idx->n_pad;
+    w.R = R;
+    w.wnorm = idx->stats + (f64 ? ST_WNORM_D : ST_WNORM_F);
+    w.ex = idx->stats + (f64 ? ST_EX_D : ST_EX_F);
+    w.eq = eq;
+    w.chunk = chunk;
+    w.blk_lo = blk_lo; w.blk_hi = blk_hi; w.nitems = nitems; w.pairs = wpairs;
+    launch_block_windows(w, s);                                                    // K7
+    CK(ws.alloc(&scan_tmp, scan_temp_bytes(m > nblocks ? m : nblocks) + 4096), "alloc");
+    exclusive_scan_i64(nitems, item_start, nblocks, scan_tmp, s);
+    int64_t *hp = static_cast<int64_t *>(t_pinned.p);
+    CK(cudaMemcpyAsync(hp, item_start + nblocks, 8, cudaMemcpyDeviceToHost, s), "D2H items");
+    CK(cudaMemcpyAsync(hp + 1, qflag, 4, cudaMemcpyDeviceToHost, s), "D2H flag");
+    CK(cudaMemcpyAsync(hp + 2, wpairs, 8, cudaMemcpyDeviceToHost, s), "D2H pairs");
+    CK(cudaStreamSynchronize(s), "query windows");
+    const int64_t total_items = hp[0];
+    if (*reinterpret_cast<int *>(hp + 1)) return fail(SNN_ERR_NONFINITE, "Q contains NaN or Inf");
+    const double pairs_eval = (double)*reinterpret_cast<unsigned long long *>(hp + 2);
+
+    // separable margin (reading C20): TF32 operands treated as truncated (2^-10)
+    // plus fp32 centring, accumulation bound (d+2) 2^-22, fp32 evaluation slack.
+    const double u = ldexp(1.0, -10) + ldexp(1.0, -24);
+    const double gacc = (D + 2) * ldexp(1.0, -22);
+    const double ga = 2 * u + u * u + gacc * (1 + u) * (1 + u);
+    const double c1 = (2 * ga + ldexp(1.0, -21) + 8 * ldexp(1.0, -24)) * 1.01;
+    const double c0 = 1e-30;
+    TcArgs t{};
+    t.xbar = idx->xbar; t.qbar = qbar; t.n = idx->n; t.m = m;
+    t.kpad = idx->kpad; t.kblocks = idx->kpad / 32;
+    t.blk_lo = blk_lo; t.blk_hi = blk_hi; t.item_start = item_start;
+    t.nblocks = nblocks; t.total_items = total_items; t.chunk = chunk;
+    {
+        const double c1h = 1.0 - c1 / 2;
+        const double r2h = (R * R * (1.0 + 1e-12) * (1.0 + ldexp(1.0, -20)) + c0) / 2;
+        float f1 = (float)c1h;
+        if ((double)f1 > c1h) f1 = nextafterf(f1, -INFINITY);
+        float f2 = (float)r2h;
+        if ((double)f2 < r2h) f2 = nextafterf(f2, INFINITY);
+        t.c1h = f1; t.r2h = f2;
+    }
+    int64_t cap = g_opt.ovf_rec_cap > 0 ? (int64_t)64 * m : 0;
+    if (cap < (int64_t(1) << 22)) cap = int64_t(1) << 22;
+    int32_t *pq = nullptr, *pj = nullptr;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        CK(ws.alloc(&pq, (size_t)cap), "alloc pairs");
+        CK(ws.alloc(&pj, (size_t)cap), "alloc pairs");
+        t.pair_q = pq; t.pair_j = pj; t.pair_count = pcount; t.pair_cap = cap;
+        CK(cudaMemsetAsync(pcount, 0, 8, s), "memset");
+        const int ctok = prof_begin(F_COUNT, s);
+        if (!launch_tc_window(Qt, idx->Xt, t, sms, s)) return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");   // K9
+        prof_end(ctok, s, pairs_eval);
+        CK(cudaMemcpyAsync(hp, pcount, 8, cudaMemcpyDeviceToHost, s), "D2H pair count");
+        CK(cudaStreamSynchronize(s), "tc filter");
+        const int64_t np = (int64_t)*reinterpret_cast<unsigned long long *>(hp);
+        if (np <= cap) { cap = np; break; }
+        cap = np;   // exact capacity, re-run once
+    }
+    const int64_t P = cap;
+    const int wtok = prof_begin(F_WRITE, s);
+    uint32_t *flag, *hq, *hj, *order1, *k2, *order2, *sk;
+    float *dist, *hd;
+    int64_t *pos;
+    int32_t *row_count;
+    uint8_t *sort_tmp;
+    CK(ws.alloc(&flag, (size_t)P), "alloc");
+    CK(ws.alloc(&dist, (size_t)P), "alloc");
+    CK(ws.alloc(&pos, (size_t)P + 1), "alloc");
+    CK(ws.alloc(&row_count, (size_t)m), "alloc");
+    CK(cudaMemsetAsync(row_count, 0, (size_t)m * 4, s), "memset");
+    const int ld = idx->ld;
+    launch_recheck(idx->Xs, Qs, f64, ld, D, pq, pj, P, R * R, flag, dist, s);            // K10
+    uint8_t *scan2;
+    CK(ws.alloc(&scan2, scan_temp_bytes(P > 0 ? P : 1)), "alloc");
+    exclusive_scan_i32_to_i64(reinterpret_cast<const int32_t *>(flag), pos, P, scan2, s);
+    CK(cudaMemcpyAsync(hp, pos + P, 8, cudaMemcpyDeviceToHost, s), "D2H hits");
+    CK(cudaStreamSynchronize(s), "recheck");
+    const int64_t H = hp[0];
+    CK(ws.alloc(&hq, (size_t)H), "alloc");
+    CK(ws.alloc(&hj, (size_t)H), "alloc");
+    CK(ws.alloc(&hd, (size_t)H), "alloc");
+    CK(ws.alloc(&order1, (size_t)H), "alloc");
+    CK(ws.alloc(&k2, (size_t)H), "alloc");
+    CK(ws.alloc(&order2, (size_t)H), "alloc");
+    CK(ws.alloc(&sk, (size_t)H), "alloc");
+    CK(ws.alloc(&sort_tmp, radix_sort_temp_bytes(H > 0 ? H : 1)), "alloc");
+    launch_tc_scatter(flag, pos, pq, pj, dist, qperm, P, hq, hj, hd, row_count, s);
+    // deterministic row order: stable sort by index position, then by original query id
+    radix_sort_u32_pairs(hj, nullptr, sk, order1, H, sort_tmp, s);
+    launch_gather_u32(hq, order1, H, k2, s);
+    radix_sort_u32_pairs(k2, order1, sk, order2, H, sort_tmp, s);
+
+    snn_result r = new snn_result_s();
+    r->m = m;
+    r->nnz = H;
+    auto bail = [&](cudaError_t e, const char *where) { snn_result_free(r); return cuda_fail(e, where); };
+    void *p = nullptr;
+    cudaError_t e = cudaMallocAsync(&p, (size_t)(m + 1) * 8, s);
+    if (e != cudaSuccess) return bail(e, "alloc offsets");
+    r->offsets = static_cast<int64_t *>(p);
+    e = cudaMallocAsync(&p, (size_t)(H > 0 ? H : 1) * 4, s);
+    if (e != cudaSuccess) return bail(e, "alloc indices");
+    r->indices = static_cast<int32_t *>(p);
+    e = cudaMallocAsync(&p, (size_t)(H > 0 ? H : 1) * 4, s);
+    if (e != cudaSuccess) return bail(e, "alloc distances");
+    r->distances = static_cast<float *>(p);
+    exclusive_scan_i32_to_i64(row_count, r->offsets, m, scan_tmp, s);
+    launch_tc_write(order2, hj, hd, idx->perm, H, r->indices, r->distances, s);
+    prof_end(wtok, s, (double)H);
+    g_last_ovf = P - H;   // candidates rejected by the exact recheck
+    g_last_lost = 0;
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return bail(e, "query");
+    *out = r;
+    return SNN_OK;
+}
+
 static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d, snn_dtype dt,
                              double R, void *stream, snn_result *out) {
     if (!out) return fail(SNN_ERR_INVALID_ARGUMENT, "NULL output handle");
@@ -403,6 +566,7 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
     const double *eq = idx->stats + ST_EX_F;
     int *qflag = nullptr;
     unsigned long long *pairs = nullptr;
+    const float *Qt = idx->Xt, *qbar = idx->xbar;
     CK(ws.alloc(&qflag, 2), "alloc");
     CK(ws.alloc(&pairs, 1), "alloc");
     CK(cudaMemsetAsync(qflag, 0, 8, s), "memset");
@@ -437,6 +601,18 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
         radix_sort_pairs(qk_raw, nullptr, qk, reinterpret_cast<uint32_t *>(qp), m, sort_tmp, s);
         launch_gather(Qd, f64, m, D, ld, round_up(m, 4), reinterpret_cast<const uint32_t *>(qp), idx->mu_d, qs, nullptr, s);
         Qs = qs; qkeys = qk; qperm = qp; eq = eqd;
+        if (idx->tc) {   // TF32 centred queries + half norms (tensor-core operand A)
+            float *qt = nullptr, *qb = nullptr;
+            CK(ws.alloc(&qt, (size_t)m * idx->kpad), "alloc");
+            CK(ws.alloc(&qb, (size_t)m), "alloc");
+            launch_gather_tf32(Qd, f64, m, D, reinterpret_cast<const uint32_t *>(qp), idx->mu_f, qt, qb, s);
+            Qt = qt; qbar = qb;
+        }
+    }
+    if (idx->tc) {
+        snn_status r = query_tc(idx, ws, s, sms, m, R, Qs, qkeys, qperm, eq, Qt, qbar, qflag, out);
+        prof_end(qtok, s, (double)m);
+        return r;
     }
     const bool generic = ld != 0;
     const int B = generic ? 64 : g_opt.query_block;

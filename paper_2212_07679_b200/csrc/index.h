@@ -56,6 +56,9 @@ struct snn_index_s {
     double *stats = nullptr;   // ST_COUNT doubles
     double h_stats[snn::ST_COUNT] = {};
     int sm_count = 148;
+    int tc = 0;                // tensor-core (tcgen05 TF32) query path enabled
+    int kpad = 0;              // K padded to 32 for the TF32 copy
+    float *Xt = nullptr;       // n x kpad TF32-rounded centred copy (tensor-core operand)
     std::vector<void *> owned;
 };
 

@@ -48,6 +48,9 @@ void launch_gather(const void *X, bool f64, int64_t n, int d, int ld, int64_t n_
 size_t radix_sort_temp_bytes(int64_t n);
 void radix_sort_pairs(const float *keys_in, const uint32_t *vals_in, float *keys_out,
                       uint32_t *vals_out, int64_t n, void *temp, cudaStream_t s);
+// Same for uint32 keys (stable, ascending).
+void radix_sort_u32_pairs(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t *keys_out,
+                          uint32_t *vals_out, int64_t n, void *temp, cudaStream_t s);
 
 // ----------------------------------------------------------------------- scan (scan.cu)
 size_t scan_temp_bytes(int64_t n);

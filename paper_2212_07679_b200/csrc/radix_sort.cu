@@ -36,13 +36,13 @@ __device__ __forceinline__ uint32_t unflip(uint32_t u) {
 }
 
 __global__ void __launch_bounds__(kThreads) radix_hist(const uint32_t *__restrict__ keys, int64_t n,
-                                                       uint32_t *hist) {
+                                                       uint32_t *hist, bool fl) {
     __shared__ uint32_t sh[kPasses][kRadix];
     for (int i = threadIdx.x; i < kPasses * kRadix; i += kThreads) (&sh[0][0])[i] = 0;
     __syncthreads();
     for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * kThreads) {
-        uint32_t u = flip(keys[i]);
+        uint32_t u = fl ? flip(keys[i]) : keys[i];
 #pragma unroll
         for (int p = 0; p < kPasses; ++p) {
             uint32_t dg = (u >> (p * kBits)) & (kRadix - 1);
@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(kThreads) onesweep(const uint32_t *__restrict_
                                                      uint32_t *__restrict__ keys_out,
                                                      uint32_t *__restrict__ vals_out, int64_t n,
                                                      int shift, const uint32_t *__restrict__ digit_offs,
-                                                     uint32_t *lookback, uint32_t *tile_ctr) {
+                                                     uint32_t *lookback, uint32_t *tile_ctr, bool fl) {
     __shared__ uint32_t s_tile;
     __shared__ uint32_t s_whist[kWarps][kRadix];
     __shared__ uint32_t s_keys[kTile];
@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(kThreads) onesweep(const uint32_t *__restrict_
         int64_t idx = base + w * (kWarp * kItems) + i * kWarp + l;
         if (idx < n) {
             uint32_t k = keys_in[idx];
-            key[i] = FIRST ? flip(k) : k;
+            key[i] = (FIRST && fl) ? flip(k) : k;
             val[i] = vals_in ? vals_in[idx] : (uint32_t)idx;
         } else {
             key[i] = 0xffffffffu;   // sorts after every finite key, and after valid digit-255 keys
@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(kThreads) onesweep(const uint32_t *__restrict_
         uint32_t k = s_keys[j];
         uint32_t dg = (k >> shift) & (kRadix - 1);
         uint32_t out = s_gbase[dg] + (uint32_t)j - s_start[dg];
-        keys_out[out] = LAST ? unflip(k) : k;
+        keys_out[out] = (LAST && fl) ? unflip(k) : k;
         vals_out[out] = s_vals[j];
     }
 }
@@ -203,8 +203,22 @@ size_t radix_sort_temp_bytes(int64_t n) {
                     round_up(n * 4, 256) + round_up(n * 4, 256));
 }
 
+void radix_sort_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t *keys_out,
+                     uint32_t *vals_out, int64_t n, void *temp, cudaStream_t s, bool fl);
+
 void radix_sort_pairs(const float *keys_in, const uint32_t *vals_in, float *keys_out,
                       uint32_t *vals_out, int64_t n, void *temp, cudaStream_t s) {
+    radix_sort_impl(reinterpret_cast<const uint32_t *>(keys_in), vals_in,
+                    reinterpret_cast<uint32_t *>(keys_out), vals_out, n, temp, s, true);
+}
+
+void radix_sort_u32_pairs(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t *keys_out,
+                          uint32_t *vals_out, int64_t n, void *temp, cudaStream_t s) {
+    radix_sort_impl(keys_in, vals_in, keys_out, vals_out, n, temp, s, false);
+}
+
+void radix_sort_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t *keys_out,
+                     uint32_t *vals_out, int64_t n, void *temp, cudaStream_t s, bool fl) {
     if (n <= 0) return;
     SortTemp st = carve(temp, n);
     const int64_t tiles = ceil_div(n, kTile);
@@ -213,19 +227,19 @@ void radix_sort_pairs(const float *keys_in, const uint32_t *vals_in, float *keys
                               (size_t)kPasses * tiles * kRadix * 4;
     cudaMemsetAsync(st.hist, 0, zero_bytes, s);
     const int hg = (int)(ceil_div(n, kThreads) < 148 * 4 ? ceil_div(n, kThreads) : 148 * 4);
-    SNN_LAUNCH(radix_hist, hg, kThreads, 0, s, reinterpret_cast<const uint32_t *>(keys_in), n, st.hist);
+    SNN_LAUNCH(radix_hist, hg, kThreads, 0, s, keys_in, n, st.hist, fl);
     SNN_LAUNCH(radix_hist_scan, kPasses, kRadix, 0, s, st.hist, st.offs);
-    const uint32_t *kin = reinterpret_cast<const uint32_t *>(keys_in);
-    uint32_t *kout = reinterpret_cast<uint32_t *>(keys_out);
+    const uint32_t *kin = keys_in;
+    uint32_t *kout = keys_out;
     // pass 0: in -> alt, 1: alt -> out, 2: out -> alt, 3: alt -> out
     SNN_LAUNCH((onesweep<true, false>), (int)tiles, kThreads, 0, s, kin, vals_in, st.alt_keys, st.alt_vals, n, 0,
-               st.offs + 0 * kRadix, st.lookback + 0 * tiles * kRadix, st.tile_ctr + 0);
+               st.offs + 0 * kRadix, st.lookback + 0 * tiles * kRadix, st.tile_ctr + 0, fl);
     SNN_LAUNCH((onesweep<false, false>), (int)tiles, kThreads, 0, s, st.alt_keys, st.alt_vals, kout, vals_out, n, 8,
-               st.offs + 1 * kRadix, st.lookback + 1 * tiles * kRadix, st.tile_ctr + 1);
+               st.offs + 1 * kRadix, st.lookback + 1 * tiles * kRadix, st.tile_ctr + 1, fl);
     SNN_LAUNCH((onesweep<false, false>), (int)tiles, kThreads, 0, s, kout, vals_out, st.alt_keys, st.alt_vals, n, 16,
-               st.offs + 2 * kRadix, st.lookback + 2 * tiles * kRadix, st.tile_ctr + 2);
+               st.offs + 2 * kRadix, st.lookback + 2 * tiles * kRadix, st.tile_ctr + 2, fl);
     SNN_LAUNCH((onesweep<false, true>), (int)tiles, kThreads, 0, s, st.alt_keys, st.alt_vals, kout, vals_out, n, 24,
-               st.offs + 3 * kRadix, st.lookback + 3 * tiles * kRadix, st.tile_ctr + 3);
+               st.offs + 3 * kRadix, st.lookback + 3 * tiles * kRadix, st.tile_ctr + 3, fl);
 }
 
 }  // namespace snn

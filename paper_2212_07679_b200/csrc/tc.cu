@@ -1,0 +1,444 @@
+// tc.cu -- K9: windowed distance tiles on the 5th-generation tensor cores (tcgen05,
+// kind::tf32) for d >= 32, and K10: the exact fp64 recheck of the emitted pairs.
+//
+// Filter (eq:ip2): with centred operands x_c = x - mu, q_c = q - mu,
+//   d^2 = 2 xbar + 2 qbar - 2 x_c.q_c,   xbar = x_c.x_c / 2 (Alg. 1 l.7).
+// The batched inner products X(J,:) [q_1..q_l] (the "gemm" of PAPER.md:218-219) are one
+// tcgen05.mma tile D[128 queries x 256 candidates] += Q_tile . X_tile^T per 8-wide K step,
+// TF32 operands (pre-rounded, cvt.rna) from shared memory (TMA, 128B swizzle), FP32
+// accumulators in TMEM.  The expanded form is NOT accurate under cancellation (DESIGN.md
+// reading C4), so the epilogue only selects CANDIDATES with a rigorous separable margin
+//   |d^2_tc - d^2| <= c1 (xbar + qbar) + c0            (reading C20)
+// i.e. acc - xbar (1 - c1/2) >= qbar (1 - c1/2) - (R^2 (1+1e-12) + c0)/2,
+// and every candidate pair is re-decided by K10 with the oracle's exact fp64 sequence
+// (eq:ip1 on the original coordinates), which also produces the distance.
+//
+// Kernel structure (one CTA per SM, persistent over (query block, candidate chunk) items):
+//   warp 0    : TMA producer  (cp.async.bulk.tensor.2d, mbarrier full/empty ring, 4 stages)
+//   warp 1    : TMEM allocator + single-thread tcgen05.mma issuer, tcgen05.commit
+//   warps 2-5 : epilogue: tcgen05.ld 32x32b.x32 -> registers, margin test, staged pair
+//               output with one atomic per warp per tile; TMEM double-buffered (2 x 256 cols)
+#include <cuda.h>
+#include <math.h>
+
+#include "common.cuh"
+#include "index.h"
+#include "tc.h"
+
+namespace snn {
+namespace {
+
+constexpr int TM = 128, TN = 256, TK = 32, STAGES = 4;
+constexpr int A_BYTES = TM * TK * 4, B_BYTES = TN * TK * 4, STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int STAGE_CAP = 32;                      // staged hits per epilogue thread per tile
+constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 2 * TN * 4 + 128 * STAGE_CAP * 4 + 256;
+constexpr uint32_t IDESC = (1u << 4)               // D format F32
+                         | (2u << 7) | (2u << 10)  // A, B format TF32
+                         | ((uint32_t)(TN >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);   // N, M
+
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+    uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)1 << 16;            // LBO (unused for swizzled K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;  // SBO: 8 rows x 128 B
+    d |= (uint64_t)1 << 46;            // descriptor version (sm_100)
+    d |= (uint64_t)2 << 61;            // SWIZZLE_128B
+    return d;
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, uint32_t bar,
+                                            int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                 : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t phase) {
+    uint32_t ok = 0;
+    while (!ok) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(bar), "r"(phase)
+            : "memory");
+    }
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+          "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+          "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+__device__ __forceinline__ void tc_locate(const TcArgs &a, int64_t item, int64_t &b, int64_t &c0, int64_t &c1) {
+    int64_t lo = 0, hi = a.nblocks;
+    while (hi - lo > 1) {
+        int64_t mid = (lo + hi) >> 1;
+        if (a.item_start[mid] <= item) lo = mid; else hi = mid;
+    }
+    b = lo;
+    c0 = a.blk_lo[b] + (item - a.item_start[b]) * a.chunk;
+    c1 = min(c0 + a.chunk, a.blk_hi[b]);
+}
+
+__global__ void __launch_bounds__(192, 1)
+tc_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcArgs a) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    uint8_t *gbase = smem_raw + (base - raw);
+    // carve: stages | a_vals[2][TN] | stage hits [128][STAGE_CAP] | barriers | tmem ptr
+    float *a_vals = reinterpret_cast<float *>(gbase + STAGES * STAGE_BYTES);
+    int32_t *s_hits = reinterpret_cast<int32_t *>(gbase + STAGES * STAGE_BYTES + 2 * TN * 4);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(gbase + STAGES * STAGE_BYTES + 2 * TN * 4 + 128 * STAGE_CAP * 4);
+    uint64_t *full = bars, *empty = bars + STAGES, *tfull = bars + 2 * STAGES, *tempty = bars + 2 * STAGES + 2;
+    uint32_t *tmem_ptr = reinterpret_cast<uint32_t *>(bars + 2 * STAGES + 4);
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 128); }
+        fence_mbar_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_ptr)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_ptr;
+
+    if (warp == 0) {
+        // ------------------------------------------------------------ TMA producer
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int64_t item = blockIdx.x; item < a.total_items; item += gridDim.x) {
+                int64_t b, c0, c1;
+                tc_locate(a, item, b, c0, c1);
+                for (int64_t t0 = c0; t0 < c1; t0 += TN) {
+                    for (int kb = 0; kb < a.kblocks; ++kb) {
+                        mbar_wait_u32(smem_u32(&empty[stage]), phase ^ 1);
+                        const uint32_t sa = base + stage * STAGE_BYTES, sb = sa + A_BYTES;
+                        mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+                        tma_load_2d(sa, &tmA, smem_u32(&full[stage]), kb * TK, (int)(b * TM));
+                        tma_load_2d(sb, &tmB, smem_u32(&full[stage]), kb * TK, (int)t0);
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0, acc = 0, aphase = 0;
+            for (int64_t item = blockIdx.x; item < a.total_items; item += gridDim.x) {
+                int64_t b, c0, c1;
+                tc_locate(a, item, b, c0, c1);
+                for (int64_t t0 = c0; t0 < c1; t0 += TN) {
+                    mbar_wait_u32(smem_u32(&tempty[acc]), aphase ^ 1);
+                    tc_fence_after();
+                    const uint32_t dcol = tmem + acc * TN;
+                    for (int kb = 0; kb < a.kblocks; ++kb) {
+                        mbar_wait_u32(smem_u32(&full[stage]), phase);
+                        tc_fence_after();
+                        const uint32_t sa = base + stage * STAGE_BYTES, sb = sa + A_BYTES;
+                        const uint64_t da = sw128_desc(sa), db = sw128_desc(sb);
+#pragma unroll
+                        for (int kk = 0; kk < TK / 8; ++kk)
+                            mma_tf32(dcol, da + 2 * kk, db + 2 * kk, (kb | kk) != 0);
+                        mma_commit(smem_u32(&empty[stage]));
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    }
+                    mma_commit(smem_u32(&tfull[acc]));
+                    acc ^= 1;
+                    if (acc == 0) aphase ^= 1;
+                }
+            }
+        }
+    } else {
+        // ------------------------------------------------------------ epilogue (128 threads)
+        const int et = threadIdx.x - 64;              // 0..127
+        const int quarter = warp & 3;                 // TMEM lane quarter this warp may access
+        const int row = quarter * 32 + lane;          // query row of the tile
+        int32_t *my_hits = s_hits + row * STAGE_CAP;
+        uint32_t acc = 0, aphase = 0;
+        for (int64_t item = blockIdx.x; item < a.total_items; item += gridDim.x) {
+            int64_t b, c0, c1;
+            tc_locate(a, item, b, c0, c1);
+            const int64_t sp = b * TM + row;
+            const float bi = sp < a.m ? fmaf(a.qbar[sp], a.c1h, -a.r2h) : INFINITY;
+            for (int64_t t0 = c0; t0 < c1; t0 += TN) {
+                float *av = a_vals + acc * TN;
+                for (int c = et; c < TN; c += 128) {
+                    const int64_t j = t0 + c;
+                    av[c] = j < c1 ? a.xbar[j] * a.c1h : NAN;
+                }
+                named_bar(1, 128);
+                mbar_wait_u32(smem_u32(&tfull[acc]), aphase);
+                tc_fence_after();
+                int nh = 0;
+                const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + acc * TN;
+#pragma unroll 1
+                for (int cc = 0; cc < TN / 32; ++cc) {
+                    float v[32];
+                    tmem_ld32(taddr + cc * 32, v);
+                    float mx = -INFINITY;
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) { v[c] -= av[cc * 32 + c]; mx = fmaxf(mx, v[c]); }
+                    if (mx >= bi) {
+#pragma unroll
+                        for (int c = 0; c < 32; ++c) {
+                            if (v[c] >= bi) {
+                                const int32_t j = (int32_t)(t0 + cc * 32 + c);
+                                if (nh < STAGE_CAP) {
+                                    my_hits[nh++] = j;
+                                } else {   // rare: direct append
+                                    const unsigned long long k = atomicAdd(a.pair_count, 1ull);
+                                    if (k < (unsigned long long)a.pair_cap) {
+                                        a.pair_q[k] = (int32_t)sp;
+                                        a.pair_j[k] = j;
+                                    }
+                                }
+                            }
+                        }
+                    }
+                }
+                tc_fence_before();
+                mbar_arrive(smem_u32(&tempty[acc]));
+                // one atomic per warp per tile for the staged hits
+                int incl = nh;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                const int total = __shfl_sync(0xffffffffu, incl, 31);
+                unsigned long long wbase = 0;
+                if (lane == 31 && total > 0) wbase = atomicAdd(a.pair_count, (unsigned long long)total);
+                wbase = __shfl_sync(0xffffffffu, wbase, 31);
+                const unsigned long long my0 = wbase + (unsigned long long)(incl - nh);
+                for (int h = 0; h < nh; ++h) {
+                    const unsigned long long k = my0 + h;
+                    if (k < (unsigned long long)a.pair_cap) {
+                        a.pair_q[k] = (int32_t)sp;
+                        a.pair_j[k] = my_hits[h];
+                    }
+                }
+                __syncwarp();
+                acc ^= 1;
+                if (acc == 0) aphase ^= 1;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+// TF32 centred copy: out[i][k] = rna_tf32(fl32(X[perm[i]][k] - mu_f[k])), zero padded
+// to kpad columns; also half norms of the (fp32) centred row, fp64 accumulation.
+template <typename T>
+__global__ void __launch_bounds__(256) gather_tf32(const T *__restrict__ X, int64_t rows, int d, int kpad,
+                                                   const uint32_t *__restrict__ perm,
+                                                   const float *__restrict__ mu_f, float *__restrict__ out,
+                                                   float *half_norm) {
+    const int l = threadIdx.x % 32;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; i < rows;
+         i += (int64_t)gridDim.x * blockDim.x / 32) {
+        const T *x = X + (int64_t)perm[i] * d;
+        double h = 0.0;
+        for (int k = l; k < kpad; k += 32) {
+            float v = 0.f;
+            if (k < d) {
+                const float c = (float)((double)x[k] - (double)mu_f[k]);   // exact for fp32 inputs up to one rounding
+                h += (double)c * (double)c;
+                uint32_t t;
+                asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(t) : "f"(c));
+                v = __uint_as_float(t);
+            }
+            out[i * kpad + k] = v;
+        }
+        h = warp_sum(h);
+        if (l == 0 && half_norm) half_norm[i] = (float)(0.5 * h);
+    }
+}
+
+// K10: exact recheck of candidate pairs (oracle sequence on the original coordinates).
+template <typename T>
+__global__ void __launch_bounds__(256) recheck_pairs(const T *__restrict__ Xs, const T *__restrict__ Qs, int ld, int d,
+                                                     const int32_t *__restrict__ pq, const int32_t *__restrict__ pj,
+                                                     int64_t npairs, double R2, uint32_t *flag, float *dist) {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < npairs; k += (int64_t)gridDim.x * blockDim.x) {
+        const double s = sqdist_exact(Xs + (int64_t)pj[k] * ld, Qs + (int64_t)pq[k] * ld, d);
+        flag[k] = s <= R2;
+        dist[k] = (float)sqrt(s);
+    }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------- host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+static bool make_map(CUtensorMap *m, const float *ptr, int64_t rows, int kpad, int box_rows) {
+    EncodeTiledFn enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)kpad, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)kpad * 4};
+    cuuint32_t box[2] = {(cuuint32_t)TK, (cuuint32_t)box_rows};
+    cuuint32_t es[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(ptr), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int tc_tile_rows() { return TM; }
+int tc_tile_cols() { return TN; }
+int tc_kpad(int d) { return (int)round_up(d, TK); }
+
+void launch_gather_tf32(const void *X, bool f64, int64_t rows, int d, const uint32_t *perm, const float *mu_f,
+                        float *out, float *half_norm, cudaStream_t s) {
+    if (rows == 0) return;
+    const int kpad = tc_kpad(d);
+    int64_t g = ceil_div(rows * 32, 256);
+    if (g > 148 * 16) g = 148 * 16;
+    if (f64) SNN_LAUNCH(gather_tf32<double>, (int)g, 256, 0, s, (const double *)X, rows, d, kpad, perm, mu_f, out, half_norm);
+    else SNN_LAUNCH(gather_tf32<float>, (int)g, 256, 0, s, (const float *)X, rows, d, kpad, perm, mu_f, out, half_norm);
+}
+
+bool launch_tc_window(const float *Qt, const float *Xt, const TcArgs &a, int sm_count, cudaStream_t s) {
+    if (a.total_items == 0) return true;
+    CUtensorMap ma, mb;
+    if (!make_map(&ma, Qt, a.m, a.kpad, TM) || !make_map(&mb, Xt, a.n, a.kpad, TN)) return false;
+    cudaFuncSetAttribute(tc_window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    int g = (int)(a.total_items < sm_count ? a.total_items : sm_count);
+    SNN_LAUNCH(tc_window_kernel, g, 192, SMEM_BYTES, s, ma, mb, a);
+    return true;
+}
+
+void launch_recheck(const void *Xs, const void *Qs, bool f64, int ld, int d, const int32_t *pq, const int32_t *pj,
+                    int64_t npairs, double R2, uint32_t *flag, float *dist, cudaStream_t s) {
+    if (npairs == 0) return;
+    int64_t g = ceil_div(npairs, 256);
+    if (g > 148 * 16) g = 148 * 16;
+    if (f64) SNN_LAUNCH(recheck_pairs<double>, (int)g, 256, 0, s, (const double *)Xs, (const double *)Qs, ld, d, pq, pj, npairs, R2, flag, dist);
+    else SNN_LAUNCH(recheck_pairs<float>, (int)g, 256, 0, s, (const float *)Xs, (const float *)Qs, ld, d, pq, pj, npairs, R2, flag, dist);
+}
+
+}  // namespace snn
+
+// ------------------------------------------------------------------------- CSR assembly
+namespace snn {
+namespace {
+
+__global__ void tc_scatter_hits(const uint32_t *flag, const int64_t *pos, const int32_t *pq, const int32_t *pj,
+                                const float *dist, const int32_t *qperm, int64_t P, uint32_t *hq, uint32_t *hj,
+                                float *hd, int32_t *row_count) {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < P; k += (int64_t)gridDim.x * blockDim.x) {
+        if (!flag[k]) continue;
+        const int64_t p = pos[k];
+        const int32_t q = qperm[pq[k]];
+        hq[p] = (uint32_t)q;
+        hj[p] = (uint32_t)pj[k];
+        hd[p] = dist[k];
+        atomicAdd(&row_count[q], 1);
+    }
+}
+
+__global__ void tc_gather_u32(const uint32_t *src, const uint32_t *idx, int64_t H, uint32_t *dst) {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < H; k += (int64_t)gridDim.x * blockDim.x)
+        dst[k] = src[idx[k]];
+}
+
+__global__ void tc_write_csr(const uint32_t *order, const uint32_t *hj, const float *hd, const int32_t *perm,
+                             int64_t H, int32_t *out_idx, float *out_dist) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < H; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t k = order[i];
+        out_idx[i] = perm[hj[k]];
+        out_dist[i] = hd[k];
+    }
+}
+
+int grid_for_n(int64_t n) {
+    int64_t g = ceil_div(n, 256);
+    return (int)(g < 1 ? 1 : (g > 148 * 16 ? 148 * 16 : g));
+}
+
+}  // namespace
+
+void launch_tc_scatter(const uint32_t *flag, const int64_t *pos, const int32_t *pq, const int32_t *pj,
+                       const float *dist, const int32_t *qperm, int64_t P, uint32_t *hq, uint32_t *hj, float *hd,
+                       int32_t *row_count, cudaStream_t s) {
+    if (P == 0) return;
+    SNN_LAUNCH(tc_scatter_hits, grid_for_n(P), 256, 0, s, flag, pos, pq, pj, dist, qperm, P, hq, hj, hd, row_count);
+}
+
+void launch_gather_u32(const uint32_t *src, const uint32_t *idx, int64_t H, uint32_t *dst, cudaStream_t s) {
+    if (H == 0) return;
+    SNN_LAUNCH(tc_gather_u32, grid_for_n(H), 256, 0, s, src, idx, H, dst);
+}
+
+void launch_tc_write(const uint32_t *order, const uint32_t *hj, const float *hd, const int32_t *perm, int64_t H,
+                     int32_t *out_idx, float *out_dist, cudaStream_t s) {
+    if (H == 0) return;
+    SNN_LAUNCH(tc_write_csr, grid_for_n(H), 256, 0, s, order, hj, hd, perm, H, out_idx, out_dist);
+}
+
+}  // namespace snn

@@ -1,0 +1,47 @@
+// tc.h -- tensor-core (tcgen05, kind::tf32) windowed candidate filter, d >= 32.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace snn {
+
+struct TcArgs {
+    const float *xbar;      // index half norms of the TF32-path centred rows (sorted, n_pad)
+    const float *qbar;      // query half norms (sorted, m)
+    int64_t n, m;
+    int kpad, kblocks;      // K padded to 32; kpad / 32
+    const int64_t *blk_lo, *blk_hi, *item_start;
+    int64_t nblocks, total_items;
+    int chunk;              // candidates per work item (multiple of 256)
+    float c1h;              // 1 - c1/2   (separable margin, reading C20)
+    float r2h;              // (R^2 (1 + 1e-12) + c0) / 2
+    int32_t *pair_q, *pair_j;            // candidate pairs (sorted query pos, sorted index pos)
+    unsigned long long *pair_count;
+    int64_t pair_cap;
+};
+
+int tc_tile_rows();   // queries per tile (128)
+int tc_tile_cols();   // candidates per tile (256)
+int tc_kpad(int d);   // d rounded up to 32
+
+// TF32 centred copy (row-major, kpad columns) + half norms of the centred rows.
+void launch_gather_tf32(const void *X, bool f64, int64_t rows, int d, const uint32_t *perm, const float *mu_f,
+                        float *out, float *half_norm, cudaStream_t s);
+// false if the TMA tensor maps could not be created.
+bool launch_tc_window(const float *Qt, const float *Xt, const TcArgs &a, int sm_count, cudaStream_t s);
+// K10: exact fp64 recheck of pairs on the original (row-major) coordinates.
+void launch_recheck(const void *Xs, const void *Qs, bool f64, int ld, int d, const int32_t *pq, const int32_t *pj,
+                    int64_t npairs, double R2, uint32_t *flag, float *dist, cudaStream_t s);
+
+}  // namespace snn
+
+namespace snn {
+// CSR assembly for the tensor-core path (hits -> rows in original query order, within a
+// row ascending sorted-index position).
+void launch_tc_scatter(const uint32_t *flag, const int64_t *pos, const int32_t *pq, const int32_t *pj,
+                       const float *dist, const int32_t *qperm, int64_t P, uint32_t *hq, uint32_t *hj, float *hd,
+                       int32_t *row_count, cudaStream_t s);
+void launch_gather_u32(const uint32_t *src, const uint32_t *idx, int64_t H, uint32_t *dst, cudaStream_t s);
+void launch_tc_write(const uint32_t *order, const uint32_t *hj, const float *hd, const int32_t *perm, int64_t H,
+                     int32_t *out_idx, float *out_dist, cudaStream_t s);
+}  // namespace snn

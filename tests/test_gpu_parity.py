@@ -346,3 +346,51 @@ def test_dbscan_c5_full_size_sampled(snn):
             core_nb = nb[allc]
             expect = lab[core_nb.min()] if len(core_nb) else -1
             assert lab[i] == expect
+
+
+# --------------------------------------------------------------------------- tensor-core path (a9)
+def test_tc_and_generic_paths_agree_exactly(snn):
+    """Same data through the tcgen05 TF32 filter and the SIMT generic kernel."""
+    import paper_2212_07679_b200 as p
+    rng = np.random.default_rng(77)
+    X = (rng.standard_normal((5000, 40)) * np.linspace(2, 0.2, 40)).astype(np.float32)
+    Q = (rng.standard_normal((900, 40)) * np.linspace(2, 0.2, 40)).astype(np.float32)
+    R = 2.2
+    a = run(snn, X, Q, R)
+    try:
+        p.snn_set_option("tc", -1)
+        b = run(snn, X, Q, R)
+    finally:
+        p.snn_set_option("tc", 0)
+    ora = oracle.radius_query(X, Q, R)
+    compare(a, ora)
+    compare(b, ora)
+    assert np.array_equal(a.offsets, b.offsets)
+
+
+@pytest.mark.parametrize("d", [32, 48, 96])
+def test_tc_clustered_far_from_origin(snn, d):
+    """Tight clusters far from the origin and from each other: |x - mu| >> R, so the
+    expanded form cancels heavily; the margin must keep every true neighbour."""
+    rng = np.random.default_rng(d)
+    centers = rng.standard_normal((6, d)) * 50 + 300
+    lab = rng.integers(0, 6, 6000)
+    X = (centers[lab] + rng.standard_normal((6000, d)) * 0.05).astype(np.float32)
+    R = float(0.05 * np.sqrt(2 * d))           # ~ typical within-cluster distance
+    gpu = run(snn, X, X[:700], R)
+    compare(gpu, oracle.radius_query(X, X[:700], R))
+
+
+def test_tc_tile_edges_and_tiles_option(snn):
+    """m and n not multiples of the 128 x 256 tile; several tiles-per-item settings."""
+    import paper_2212_07679_b200 as p
+    rng = np.random.default_rng(5)
+    X = rng.standard_normal((4097, 64)).astype(np.float32)
+    Q = rng.standard_normal((129, 64)).astype(np.float32)
+    ora = oracle.radius_query(X, Q, 9.5)
+    try:
+        for tiles in (1, 3, 8):
+            p.snn_set_option("tc_tiles", tiles)
+            compare(run(snn, X, Q, 9.5), ora)
+    finally:
+        p.snn_set_option("tc_tiles", 0)
