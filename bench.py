@@ -194,6 +194,51 @@ def config_block(w, args):
             "parallelism": f"replicas x{args.gpus} (weak scaling)"}
 
 
+# ----------------------------------------------------------------------------- roofline
+def roofline_block(args, w, prof, times, dev):
+    """Roofline of the dominant kernel, from CUDA-event times taken by the library on the
+    launching stream (snn_profile_*) during the timed steps.
+
+    d <= 8 : K8 scan pass (window_lowd), FP32-ALU bound: (3d-1) flop per evaluated pair
+             (eq:ip1) vs 148 SMs x 128 lanes x 2 x sm_max_mhz.
+    d >= 32: K9 tcgen05 TF32 filter (tc_window_kernel), tensor bound: 2 kpad flop per pair
+             (the X(J,:)^T x_q contraction) vs TF32 dense peak = measured
+             bf16 burst x 1/2 (B200_PROFILING.md nominal ratio tf32 1.1 : bf16 2.25 PF).
+    """
+    import torch
+    peaks, src = load_peaks()
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    kms = prof["window_count"]["ms"]
+    klaunch = prof["window_count"]["launches"]
+    kunits = prof["window_count"]["units"]
+    traffic = None
+    try:
+        tr = json.load(open(TRAFFIC_PATH))
+        traffic = tr.get(args.config, {}).get("dominant_kernel_dram_bytes_per_launch")
+    except Exception:
+        pass
+    if w.d >= 32:
+        kpad = (w.d + 31) // 32 * 32
+        flop_per_pair = 2 * kpad
+        peak = float(peaks.get("bf16_tflops", 1590.0)) * 0.5
+        kernel, bound = "tc_window_kernel (K9 tcgen05 kind::tf32 filter)", "tensor"
+        peak_src = f"TF32 dense = bf16_tflops {peaks.get('bf16_tflops')} x 0.5 ({src})"
+        work = f"2*kpad = {flop_per_pair} flop per evaluated pair (padded contraction)"
+    else:
+        flop_per_pair = 3 * w.d - 1
+        peak = fp32_alu_peak_tflops(sm_max, n_sm)
+        kernel, bound = f"window_lowd<float,{w.d},scan> (K8 scan pass)", "alu"
+        peak_src = f"FP32 FMA issue peak at {sm_max:.0f} MHz x {n_sm} SMs (sm_max_mhz, {src})"
+        work = f"{flop_per_pair} flop per evaluated candidate pair (eq:ip1)"
+    achieved = (flop_per_pair * kunits / klaunch) / (kms / klaunch * 1e-3) / 1e12 if klaunch else 0.0
+    return {"kernel": kernel, "bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved / peak if peak else None, "traffic": traffic, "peak_source": peak_src,
+            "work": f"{work}; {kunits / max(klaunch, 1):.4g} pairs per launch",
+            "kernel_ms_per_launch": kms / max(klaunch, 1),
+            "share_of_step": kms / sum(times) if times else None}
+
+
 # ----------------------------------------------------------------------------- GPU arm
 def run_gpu(args):
     import torch
@@ -212,8 +257,15 @@ def run_gpu(args):
     R = w.R
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
 
+    dbscan = w.dbscan_min_pts is not None
+    labels_d = torch.empty(w.n, dtype=torch.int32, device=dev) if dbscan else None
+
     def step():
         idx = snn.snn_build(X)
+        if dbscan:   # config 5: build + DBSCAN
+            k = snn.snn_dbscan(idx, R, w.dbscan_min_pts, labels_d)
+            snn.snn_free(idx)
+            return k
         r = snn.snn_query_self(idx, R) if Qd is None else snn.snn_query_radius(idx, Qd, R)
         nnz = snn.snn_result_csr(r)["nnz"]
         snn.snn_result_free(r)
@@ -245,7 +297,7 @@ def run_gpu(args):
     t_host1 = time.time()
     clocks = clk.stop(t_host0, t_host1)
     launches = snn.snn_launch_count() - l0
-    prof = {f: snn.snn_profile_read(f) for f in ("build", "window_count", "window_write", "query")}
+    prof = {f: snn.snn_profile_read(f) for f in ("build", "window_count", "window_write", "query", "dbscan")}
     overflow = snn.snn_profile_read("overflow")["units"]
     lost = snn.snn_profile_read("lost")["units"]
     snn.snn_profile_enable(False)
@@ -260,8 +312,9 @@ def run_gpu(args):
     Xh = torch.from_numpy(w.X).pin_memory()
     Qh = None if w.Q is None else torch.from_numpy(w.Q).pin_memory()
     off_h = torch.empty(w.m + 1, dtype=torch.int64).pin_memory()
-    idx_h = torch.empty(max(nnz, 1), dtype=torch.int32).pin_memory()
-    dist_h = torch.empty(max(nnz, 1), dtype=torch.float32).pin_memory()
+    idx_h = torch.empty(1 if dbscan else max(nnz, 1), dtype=torch.int32).pin_memory()
+    dist_h = torch.empty(1 if dbscan else max(nnz, 1), dtype=torch.float32).pin_memory()
+    labels_h = torch.empty(w.n, dtype=torch.int32).pin_memory() if dbscan else None
     e2e_times = []
     for i in range(args.warmup + args.steps):
         flush.fill_(1.0)
@@ -269,9 +322,12 @@ def run_gpu(args):
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
         idx = snn.snn_build(Xh)
-        r = snn.snn_query_self(idx, R) if Qh is None else snn.snn_query_radius(idx, Qh, R)
-        snn.snn_result_copy(r, off_h, idx_h, dist_h)
-        snn.snn_result_free(r)
+        if dbscan:
+            snn.snn_dbscan(idx, R, w.dbscan_min_pts, labels_h)
+        else:
+            r = snn.snn_query_self(idx, R) if Qh is None else snn.snn_query_radius(idx, Qh, R)
+            snn.snn_result_copy(r, off_h, idx_h, dist_h)
+            snn.snn_result_free(r)
         snn.snn_free(idx)
         e1.record()
         e1.synchronize()
@@ -280,47 +336,26 @@ def run_gpu(args):
     e2e_ms = max_over_ranks(sum(e2e_times), world, dev)
     e2e_value = weak_units(w.m * args.steps, world) / (e2e_ms / 1e3)
     h2d = w.X.nbytes + (0 if w.Q is None else w.Q.nbytes)
-    d2h = (w.m + 1) * 8 + nnz * 8
+    d2h = w.n * 4 if dbscan else (w.m + 1) * 8 + nnz * 8
+    metric = "DBSCAN points/s (index build + DBSCAN, n=2M)" if dbscan else METRIC
+    unit = "points/s" if dbscan else "queries/s"
 
-    # ---- roofline of the dominant kernel (windowed distance passes, K8)
-    peaks, src = load_peaks()
-    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
-    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
-    peak_alu = fp32_alu_peak_tflops(sm_max, n_sm)
-    kms = prof["window_count"]["ms"]
-    klaunch = prof["window_count"]["launches"]
-    kunits = prof["window_count"]["units"]
-    flop_per_pair = 3 * w.d - 1             # eq:ip1 flop count
-    achieved = (flop_per_pair * kunits / klaunch) / (kms / klaunch * 1e-3) / 1e12 if klaunch else 0.0
-    traffic = None
-    try:
-        tr = json.load(open(TRAFFIC_PATH))
-        traffic = tr.get(args.config, {}).get("window_pass_dram_bytes_per_launch")
-    except Exception:
-        pass
-    roofline = {"kernel": "window_lowd<float,3,0> (K8 scan pass: count + record hits)", "bound": "alu",
-                "achieved": achieved, "peak": peak_alu, "unit": "TFLOP/s",
-                "frac": achieved / peak_alu if peak_alu else None, "traffic": traffic,
-                "peak_source": f"FP32 FMA issue peak at {sm_max:.0f} MHz x {n_sm} SMs "
-                               f"(sm_max_mhz from MEASURED_PEAKS.json, {src})",
-                "work": f"{flop_per_pair} flop per evaluated candidate pair (eq:ip1), "
-                        f"{kunits / max(klaunch, 1):.4g} pairs per launch",
-                "share_of_step": kms / sum(times) if times else None}
+    roofline = roofline_block(args, w, prof, times, dev)
 
-    line = {"metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
+    line = {"metric": metric, "value": value, "unit": unit, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64" if w.X.dtype == np.float64 else "f32", "data": "synthetic",
             "config": config_block(w, args),
             "build_ms": prof["build"]["ms"] / max(1, prof["build"]["launches"]),
             "query_ms": prof["query"]["ms"] / max(1, prof["query"]["launches"]),
-            "nnz": nnz, "overflow_records": overflow, "fix_items": lost,
+            ("clusters" if dbscan else "nnz"): nnz, "overflow_records": overflow, "fix_items": lost,
             "breakdown_ms_per_step": {k: v["ms"] / args.steps for k, v in prof.items()},
             "clocks": clocks, "gpu_launches": launches,
-            "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": h2d,
+            "e2e": {"value": e2e_value, "unit": unit, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.steps},
             "roofline": roofline}
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not dbscan:
         rate, k, dt, threads = oracle_sample_rate(w, args.cpu_seconds)
         line["cpu_baseline"] = {"value": rate, "unit": "queries/s", "cores": threads,
                                 "kind": "oracle",
@@ -338,7 +373,7 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="snn", choices=["snn", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -149,8 +149,10 @@ uint64_t snn_launch_count(void);
  *   units     work units processed (window passes: candidate pairs evaluated; build:
  *             points indexed), summed.
  * Families: "build"; "window_count" (low d: the scan pass that counts and records hits;
- * generic d: the count pass); "window_write" (low d: CSR compaction + overflow fix,
+ * generic d: the count pass; tensor-core path: the tcgen05 filter; DBSCAN: the count
+ * pass); "window_write" (low d: CSR compaction + overflow fix,
  * units = hits; generic d: the recomputing write pass); "query" (whole query call);
+ * "dbscan" (whole snn_dbscan call, units = points);
  * "overflow" (units = hit records that went to the overflow list in the last low-d query);
  * "lost" (units = work items re-run by the fix pass in the last low-d query).
  * Unknown family -> SNN_ERR_INVALID_ARGUMENT. */

@@ -40,8 +40,7 @@ static Options g_opt;
 static thread_local std::string t_err;
 
 // ------------------------------------------------------------------ kernel-time profiler
-enum Fam { F_BUILD = 0, F_COUNT = 1, F_WRITE = 2, F_QUERY = 3, F_N = 4 };
-static const char *kFamNames[F_N] = {"build", "window_count", "window_write", "query"};
+static const char *kFamNames[F_N] = {"build", "window_count", "window_write", "query", "dbscan"};
 struct ProfRec {
     int fam;
     cudaEvent_t a, b;
@@ -56,7 +55,7 @@ struct Profiler {
 };
 static Profiler g_prof;
 
-static int prof_begin(int fam, cudaStream_t s) {
+int prof_begin(int fam, cudaStream_t s) {
     if (!g_prof.on) return -1;
     ProfRec r{fam, nullptr, nullptr, 0.0};
     cudaEventCreate(&r.a);
@@ -66,7 +65,7 @@ static int prof_begin(int fam, cudaStream_t s) {
     g_prof.pending.push_back(r);
     return (int)g_prof.pending.size() - 1;
 }
-static void prof_end(int tok, cudaStream_t s, double units) {
+void prof_end(int tok, cudaStream_t s, double units) {
     if (tok < 0 || !g_prof.on) return;
     std::lock_guard<std::mutex> lk(g_prof.mu);
     if (tok >= (int)g_prof.pending.size()) return;
@@ -302,7 +301,7 @@ snn_status snn_build(const void *X, int64_t n, int32_t d, snn_dtype dt, void *st
     idx->Xs = xs_bytes;
     CKI(own(&idx->keys, (size_t)n), "alloc keys");
     CKI(own(&idx->perm, (size_t)n), "alloc perm");
-    CKI(own(&idx->xbar, (size_t)idx->n_pad), "alloc xbar");
+    CKI(own(&idx->xbar, (size_t)idx->n_pad + 256), "alloc xbar");   // +256: tile-wide bulk copies
     CKI(own(&idx->mu_d, (size_t)d), "alloc");
     CKI(own(&idx->mu_f, (size_t)d), "alloc");
     CKI(own(&idx->v_d, (size_t)d), "alloc");
@@ -669,7 +668,7 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
         if (e != cudaSuccess) return bail(e, "alloc offsets");
         r->offsets = static_cast<int64_t *>(p);
     }
-    PassArgs a;
+    PassArgs a{};
     a.Xs = idx->Xs; a.Qs = Qs; a.ld = ld; a.d = D; a.f64 = f64; a.m = m;
     a.perm = idx->perm; a.qperm = qperm;
     a.blk_lo = blk_lo; a.blk_hi = blk_hi; a.item_start = item_start;
@@ -802,7 +801,10 @@ snn_status snn_dbscan(snn_index idx, double eps, int32_t min_pts, int32_t *label
     int sms = 0;
     snn_status st = device_check(&sms);
     if (st != SNN_OK) return st;
-    return dbscan_impl(idx, eps, min_pts, labels, n_clusters, static_cast<cudaStream_t>(stream));
+    const int tok = prof_begin(F_DBSCAN, static_cast<cudaStream_t>(stream));
+    st = dbscan_impl(idx, eps, min_pts, labels, n_clusters, static_cast<cudaStream_t>(stream));
+    prof_end(tok, static_cast<cudaStream_t>(stream), (double)idx->n);
+    return st;
 }
 
 }  // extern "C"

@@ -25,7 +25,7 @@ __global__ void init_core(const int32_t *count, int64_t n, int32_t min_pts, uint
                           int32_t *parent, int32_t *minid, int32_t *best) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         core[i] = count[i] >= min_pts;
-        parent[i] = (int32_t)i;
+        parent[i] = core[i] ? (int32_t)i : -1;   // -1 marks non-core points
         minid[i] = 0x7fffffff;
         best[i] = 0x7fffffff;
     }
@@ -160,9 +160,15 @@ snn_status dbscan_impl(snn_index idx, double eps, int32_t min_pts, int32_t *labe
     }
     a.cnt = cnt; a.pre = cnt; a.cap = 0; a.variant = 1;
     a.sm_count = idx->sm_count;
-    a.core = core; a.parent = parent; a.best = best;
+    a.core = core; a.parent = parent; a.best = best; a.min_pts = min_pts;
 
+    unsigned long long *hp_pairs = reinterpret_cast<unsigned long long *>(hbuf);
+    CKD(cudaMemcpyAsync(hp_pairs, pairs, 8, cudaMemcpyDeviceToHost, s), "D2H");
+    CKD(cudaStreamSynchronize(s), "dbscan pairs");
+    const double pairs_eval = (double)*hp_pairs;
+    const int ctok = prof_begin(F_COUNT, s);
     launch_lowd_mode(2, a, s);                                              // counts
+    prof_end(ctok, s, pairs_eval);
     launch_row_totals(cnt, cnt, item_start, n, B, nullptr, count, s);
     SNN_LAUNCH(init_core, grid_n(n), 256, 0, s, count, n, min_pts, core, parent, minid, best);
     launch_lowd_mode(3, a, s);                                              // unions

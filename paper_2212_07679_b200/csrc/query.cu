@@ -300,6 +300,8 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
         if (MODE == M_UNION) active = active && a.core[sp] && c1 - 1 > sp;   // pairs j > i only
         if (MODE == M_BORDER) active = active && !a.core[sp];
         int32_t best = 0x7fffffff;   // M_BORDER: smallest original id of a core neighbour
+        int32_t uroot = -1;          // M_UNION: cached union-find root of this query
+        if (MODE == M_UNION && active) uroot = uf_rep(a.parent, (int32_t)sp);
 #pragma unroll
         for (int k = 0; k < D; ++k) q[k] = active ? Qs[(sp >> 2) * 4 * D + k * 4 + (sp & 3)] : (T)0;
         mbar_wait(&bar[sidx], phase[sidx]);
@@ -334,7 +336,13 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
                                 const int i = __ffs(m) - 1;
                                 m &= m - 1;
                                 const int64_t j = c0 + gg * 4 + i;
-                                if (j > sp && a.core[j]) uf_unite(a.parent, (int32_t)sp, (int32_t)j);
+                                if (j > sp) {   // parent < 0: not core; == root: already joined
+                                    const int32_t pj = reinterpret_cast<volatile int32_t *>(a.parent)[j];
+                                    if (pj >= 0 && pj != uroot) {
+                                        uf_unite(a.parent, (int32_t)sp, (int32_t)j);
+                                        uroot = uf_rep(a.parent, (int32_t)sp);
+                                    }
+                                }
                             }
                         } else if (MODE == M_BORDER) {
                             while (m) {
@@ -422,7 +430,10 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
                                 const int i = __ffs(m) - 1;
                                 m &= m - 1;
                                 const int64_t j = c0 + g * 4 + i;
-                                if (MODE == M_UNION && j > sp && a.core[j]) uf_unite(a.parent, (int32_t)sp, (int32_t)j);
+                                if (MODE == M_UNION && j > sp && a.parent[j] >= 0 && a.parent[j] != uroot) {
+                                    uf_unite(a.parent, (int32_t)sp, (int32_t)j);
+                                    uroot = uf_rep(a.parent, (int32_t)sp);
+                                }
                                 if (MODE == M_BORDER && a.core[j]) best = min(best, a.perm[j]);
                             }
                         }

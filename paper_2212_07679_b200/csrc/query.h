@@ -64,6 +64,7 @@ struct PassArgs {
     const uint8_t *core;    // core flags
     int32_t *parent;        // union-find parents
     int32_t *best;          // M_BORDER: smallest original id of a core neighbour (atomicMin)
+    int32_t min_pts;        // M_COUNT: counts are only needed up to min_pts (early exit)
 };
 
 bool lowd_supported(int d);   // d handled by the register-resident low-d kernels

@@ -30,8 +30,11 @@ namespace {
 
 constexpr int TM = 128, TN = 256, TK = 32, STAGES = 4;
 constexpr int A_BYTES = TM * TK * 4, B_BYTES = TN * TK * 4, STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int STAGE_CAP = 32;                      // staged hits per epilogue thread per tile
-constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 2 * TN * 4 + 128 * STAGE_CAP * 4 + 256;
+constexpr int STAGE_CAP = 8;                       // staged hits per epilogue thread per tile
+constexpr int EPI = 512;                           // epilogue threads (16 warps)
+constexpr int COLS = TN / (EPI / 128);             // columns per epilogue thread
+constexpr int THREADS = 64 + EPI;
+constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 2 * TN * 4 + EPI * STAGE_CAP * 4 + 512;
 constexpr uint32_t IDESC = (1u << 4)               // D format F32
                          | (2u << 7) | (2u << 10)  // A, B format TF32
                          | ((uint32_t)(TN >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);   // N, M
@@ -117,23 +120,27 @@ __device__ __forceinline__ void tc_locate(const TcArgs &a, int64_t item, int64_t
     c1 = min(c0 + a.chunk, a.blk_hi[b]);
 }
 
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(THREADS, 1)
 tc_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcArgs a) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
     uint8_t *gbase = smem_raw + (base - raw);
-    // carve: stages | a_vals[2][TN] | stage hits [128][STAGE_CAP] | barriers | tmem ptr
+    // carve: stages | a_vals[2][TN] | stage hits [EPI][STAGE_CAP] | barriers | tmem ptr
     float *a_vals = reinterpret_cast<float *>(gbase + STAGES * STAGE_BYTES);
     int32_t *s_hits = reinterpret_cast<int32_t *>(gbase + STAGES * STAGE_BYTES + 2 * TN * 4);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(gbase + STAGES * STAGE_BYTES + 2 * TN * 4 + 128 * STAGE_CAP * 4);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(gbase + STAGES * STAGE_BYTES + 2 * TN * 4 + EPI * STAGE_CAP * 4);
     uint64_t *full = bars, *empty = bars + STAGES, *tfull = bars + 2 * STAGES, *tempty = bars + 2 * STAGES + 2;
-    uint32_t *tmem_ptr = reinterpret_cast<uint32_t *>(bars + 2 * STAGES + 4);
+    uint64_t *afull = bars + 2 * STAGES + 4, *aempty = bars + 2 * STAGES + 6;
+    uint32_t *tmem_ptr = reinterpret_cast<uint32_t *>(bars + 2 * STAGES + 8);
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-        for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 128); }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&tfull[s], 1); mbar_init(&tempty[s], EPI);
+            mbar_init(&afull[s], 1); mbar_init(&aempty[s], EPI);
+        }
         fence_mbar_init();
     }
     if (warp == 1) {
@@ -151,11 +158,17 @@ tc_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
             int stage = 0;
-            uint32_t phase = 0;
+            uint32_t phase = 0, aslot = 0, aph = 0;
             for (int64_t item = blockIdx.x; item < a.total_items; item += gridDim.x) {
                 int64_t b, c0, c1;
                 tc_locate(a, item, b, c0, c1);
                 for (int64_t t0 = c0; t0 < c1; t0 += TN) {
+                    // x-bar slice of this tile -> a-ring slot (read by the epilogue)
+                    mbar_wait_u32(smem_u32(&aempty[aslot]), aph ^ 1);
+                    mbar_arrive_expect_tx(&afull[aslot], TN * 4);
+                    bulk_g2s(a_vals + aslot * TN, a.xbar + t0, TN * 4, &afull[aslot]);
+                    aslot ^= 1;
+                    if (aslot == 0) aph ^= 1;
                     for (int kb = 0; kb < a.kblocks; ++kb) {
                         mbar_wait_u32(smem_u32(&empty[stage]), phase ^ 1);
                         const uint32_t sa = base + stage * STAGE_BYTES, sb = sa + A_BYTES;
@@ -197,40 +210,54 @@ tc_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             }
         }
     } else {
-        // ------------------------------------------------------------ epilogue (128 threads)
-        const int et = threadIdx.x - 64;              // 0..127
-        const int quarter = warp & 3;                 // TMEM lane quarter this warp may access
-        const int row = quarter * 32 + lane;          // query row of the tile
-        int32_t *my_hits = s_hits + row * STAGE_CAP;
+        // ------------------------------------------------------------ epilogue (EPI threads)
+        // 16 warps: warp w may only touch TMEM lane quarter (w % 4); the four warps of a
+        // quarter split the 256 columns into 64-column slices.  One thread = one query row.
+        const int et = threadIdx.x - 64;              // 0..EPI-1
+        const int quarter = warp & 3;
+        const int slice = et >> 7;                    // 0..3
+        const int row = quarter * 32 + lane;
+        int32_t *my_hits = s_hits + et * STAGE_CAP;
+        const float c1h = a.c1h;
         uint32_t acc = 0, aphase = 0;
         for (int64_t item = blockIdx.x; item < a.total_items; item += gridDim.x) {
             int64_t b, c0, c1;
             tc_locate(a, item, b, c0, c1);
             const int64_t sp = b * TM + row;
-            const float bi = sp < a.m ? fmaf(a.qbar[sp], a.c1h, -a.r2h) : INFINITY;
+            const float bi = sp < a.m ? fmaf(a.qbar[sp], c1h, -a.r2h) : INFINITY;
             for (int64_t t0 = c0; t0 < c1; t0 += TN) {
-                float *av = a_vals + acc * TN;
-                for (int c = et; c < TN; c += 128) {
-                    const int64_t j = t0 + c;
-                    av[c] = j < c1 ? a.xbar[j] * a.c1h : NAN;
-                }
-                named_bar(1, 128);
+                const float *av = a_vals + acc * TN + slice * COLS;
+                mbar_wait_u32(smem_u32(&afull[acc]), aphase);
                 mbar_wait_u32(smem_u32(&tfull[acc]), aphase);
                 tc_fence_after();
                 int nh = 0;
-                const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + acc * TN;
+                const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + acc * TN + slice * COLS;
 #pragma unroll 1
-                for (int cc = 0; cc < TN / 32; ++cc) {
+                for (int ch = 0; ch < COLS / 32; ++ch) {
                     float v[32];
-                    tmem_ld32(taddr + cc * 32, v);
-                    float mx = -INFINITY;
+                    tmem_ld32(taddr + ch * 32, v);
+                    const float4 *a4 = reinterpret_cast<const float4 *>(av + ch * 32);
 #pragma unroll
-                    for (int c = 0; c < 32; ++c) { v[c] -= av[cc * 32 + c]; mx = fmaxf(mx, v[c]); }
+                    for (int c4 = 0; c4 < 8; ++c4) {   // v = acc - xbar (1 - c1/2)
+                        const float4 w = a4[c4];
+                        v[4 * c4 + 0] = fmaf(-w.x, c1h, v[4 * c4 + 0]);
+                        v[4 * c4 + 1] = fmaf(-w.y, c1h, v[4 * c4 + 1]);
+                        v[4 * c4 + 2] = fmaf(-w.z, c1h, v[4 * c4 + 2]);
+                        v[4 * c4 + 3] = fmaf(-w.w, c1h, v[4 * c4 + 3]);
+                    }
+                    float m[11];
+#pragma unroll
+                    for (int c = 0; c < 10; ++c) m[c] = fmaxf(fmaxf(v[3 * c], v[3 * c + 1]), v[3 * c + 2]);
+                    m[10] = fmaxf(v[30], v[31]);
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) m[c] = fmaxf(fmaxf(m[3 * c], m[3 * c + 1]), m[3 * c + 2]);
+                    const float mx = fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[9] > m[10] ? m[9] : m[10]));
                     if (mx >= bi) {
 #pragma unroll
                         for (int c = 0; c < 32; ++c) {
-                            if (v[c] >= bi) {
-                                const int32_t j = (int32_t)(t0 + cc * 32 + c);
+                            const int64_t jj = t0 + slice * COLS + ch * 32 + c;
+                            if (v[c] >= bi && jj < c1) {
+                                const int32_t j = (int32_t)jj;
                                 if (nh < STAGE_CAP) {
                                     my_hits[nh++] = j;
                                 } else {   // rare: direct append
@@ -246,26 +273,28 @@ tc_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 }
                 tc_fence_before();
                 mbar_arrive(smem_u32(&tempty[acc]));
+                mbar_arrive(smem_u32(&aempty[acc]));
                 // one atomic per warp per tile for the staged hits
-                int incl = nh;
+                if (__any_sync(0xffffffffu, nh > 0)) {
+                    int incl = nh;
 #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int y = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (lane >= o) incl += y;
-                }
-                const int total = __shfl_sync(0xffffffffu, incl, 31);
-                unsigned long long wbase = 0;
-                if (lane == 31 && total > 0) wbase = atomicAdd(a.pair_count, (unsigned long long)total);
-                wbase = __shfl_sync(0xffffffffu, wbase, 31);
-                const unsigned long long my0 = wbase + (unsigned long long)(incl - nh);
-                for (int h = 0; h < nh; ++h) {
-                    const unsigned long long k = my0 + h;
-                    if (k < (unsigned long long)a.pair_cap) {
-                        a.pair_q[k] = (int32_t)sp;
-                        a.pair_j[k] = my_hits[h];
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                        if (lane >= o) incl += y;
+                    }
+                    const int total = __shfl_sync(0xffffffffu, incl, 31);
+                    unsigned long long wbase = 0;
+                    if (lane == 31) wbase = atomicAdd(a.pair_count, (unsigned long long)total);
+                    wbase = __shfl_sync(0xffffffffu, wbase, 31);
+                    const unsigned long long my0 = wbase + (unsigned long long)(incl - nh);
+                    for (int h = 0; h < nh; ++h) {
+                        const unsigned long long k = my0 + h;
+                        if (k < (unsigned long long)a.pair_cap) {
+                            a.pair_q[k] = (int32_t)sp;
+                            a.pair_j[k] = my_hits[h];
+                        }
                     }
                 }
-                __syncwarp();
                 acc ^= 1;
                 if (acc == 0) aphase ^= 1;
             }
@@ -312,7 +341,26 @@ __global__ void __launch_bounds__(256) recheck_pairs(const T *__restrict__ Xs, c
                                                      const int32_t *__restrict__ pq, const int32_t *__restrict__ pj,
                                                      int64_t npairs, double R2, uint32_t *flag, float *dist) {
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < npairs; k += (int64_t)gridDim.x * blockDim.x) {
-        const double s = sqdist_exact(Xs + (int64_t)pj[k] * ld, Qs + (int64_t)pq[k] * ld, d);
+        const T *x = Xs + (int64_t)pj[k] * ld, *q = Qs + (int64_t)pq[k] * ld;
+        double s = 0.0;
+        if constexpr (sizeof(T) == 4) {   // rows are 16-byte aligned (ld % 4 == 0): vector loads,
+            int kk = 0;                   // same left-to-right operation order as the oracle
+            for (; kk + 4 <= d; kk += 4) {
+                const float4 xv = *reinterpret_cast<const float4 *>(x + kk);
+                const float4 qv = *reinterpret_cast<const float4 *>(q + kk);
+                double t;
+                t = __dsub_rn((double)xv.x, (double)qv.x); s = __dadd_rn(s, __dmul_rn(t, t));
+                t = __dsub_rn((double)xv.y, (double)qv.y); s = __dadd_rn(s, __dmul_rn(t, t));
+                t = __dsub_rn((double)xv.z, (double)qv.z); s = __dadd_rn(s, __dmul_rn(t, t));
+                t = __dsub_rn((double)xv.w, (double)qv.w); s = __dadd_rn(s, __dmul_rn(t, t));
+            }
+            for (; kk < d; ++kk) {
+                const double t = __dsub_rn((double)x[kk], (double)q[kk]);
+                s = __dadd_rn(s, __dmul_rn(t, t));
+            }
+        } else {
+            s = sqdist_exact(x, q, d);
+        }
         flag[k] = s <= R2;
         dist[k] = (float)sqrt(s);
     }
@@ -369,7 +417,7 @@ bool launch_tc_window(const float *Qt, const float *Xt, const TcArgs &a, int sm_
     if (!make_map(&ma, Qt, a.m, a.kpad, TM) || !make_map(&mb, Xt, a.n, a.kpad, TN)) return false;
     cudaFuncSetAttribute(tc_window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     int g = (int)(a.total_items < sm_count ? a.total_items : sm_count);
-    SNN_LAUNCH(tc_window_kernel, g, 192, SMEM_BYTES, s, ma, mb, a);
+    SNN_LAUNCH(tc_window_kernel, g, THREADS, SMEM_BYTES, s, ma, mb, a);
     return true;
 }
 
