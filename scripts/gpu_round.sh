@@ -1,0 +1,27 @@
+#!/bin/bash
+# One gpurun call: GPU parity tests, benches per config, ncu launch list + full captures.
+# usage (under gpurun): bash scripts/gpu_round.sh TAG [stages...]
+#   stages: build tests bench ncu_launch ncu_full_c2 ncu_full_c3 ncu_full_c4 ncu_full_c5
+set -u
+TAG=${1:-run}; shift
+OUT=gpurun_out/$TAG; mkdir -p $OUT
+STAGES=${@:-build tests bench}
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,driver_version --format=csv > $OUT/gpu.txt 2>&1
+nproc > $OUT/nproc.txt; lscpu | grep -E 'Model name|^CPU\(s\)' >> $OUT/nproc.txt
+for s in $STAGES; do
+  case $s in
+    build) python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1 || { echo BUILD FAIL; tail -20 $OUT/build.log; exit 1; } ;;
+    tests) timeout 1200 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.txt 2>&1; echo "pytest rc=$?"; tail -3 $OUT/pytest_gpu.txt ;;
+    smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.txt 2>&1; echo "smoke rc=$?"; tail -2 $OUT/smoke.txt ;;
+    bench) timeout 600 python bench.py > $OUT/bench_c2.jsonl 2> $OUT/bench_c2.err; echo "bench c2 rc=$?"; tail -c 600 $OUT/bench_c2.jsonl
+           for c in c1 c3 c4 c5; do timeout 600 python bench.py --config $c --steps 10 --no-cpu-baseline > $OUT/bench_$c.jsonl 2> $OUT/bench_$c.err; echo "bench $c rc=$?"; done ;;
+    benchfast) for c in c2 c3 c4 c5; do timeout 600 python bench.py --config $c --steps 10 --no-cpu-baseline > $OUT/bench_$c.jsonl 2> $OUT/bench_$c.err; echo "bench $c rc=$?"; done ;;
+    ncu_launch) for c in c2 c3 c4 c5; do
+        CMD="python bench.py --config $c --steps 1 --warmup 3 --no-cpu-baseline"
+        $CMD > $OUT/plain_$c.log 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$c.csv $CMD > $OUT/ncu_launch_$c.log 2>&1; echo "ncu launch $c rc=$?"; done ;;
+    ncu_full_*) c=${s#ncu_full_}
+        case $c in c2|c5) K='regex:window_lowd';; *) K='regex:tc_window';; esac
+        CMD="python bench.py --config $c --steps 1 --warmup 3 --no-cpu-baseline"
+        $CMD > $OUT/plainf_$c.log 2>&1 && timeout 1200 ncu --set full --clock-control none --import-source on -k $K -s 6 -c 2 -o $OUT/full_$c $CMD > $OUT/ncu_full_$c.log 2>&1; echo "ncu full $c rc=$?" ;;
+  esac
+done
