@@ -33,6 +33,7 @@ struct Options {
     int tc = 1;          // use the tcgen05 path for d >= tc_min_d
     int tc_min_d = 32;
     int tc_tiles = 8;    // 256-candidate tiles per work item on the tensor-core path
+    int tc_diag = 0;     // diagnostics only (results invalid): 1 = no epilogue work, 2 = no MMA
 };
 static std::atomic<int64_t> g_last_ovf{0}, g_last_lost{0};
 static Options g_opt;
@@ -246,6 +247,11 @@ snn_status snn_set_option(const char *key, int64_t value) {
         g_opt.tc_tiles = (int)value;
         return SNN_OK;
     }
+    if (k == "tc_diag") {   // performance diagnostics only: results are NOT valid
+        if (value < 0 || value > 4) return fail(SNN_ERR_INVALID_ARGUMENT, "tc_diag must be 0..4");
+        g_opt.tc_diag = (int)value;
+        return SNN_OK;
+    }
     if (k == "variant") {
         if (value == 0) value = 1;
         if (value < 1 || value > 2) return fail(SNN_ERR_INVALID_ARGUMENT, "variant must be 1 or 2");
@@ -453,6 +459,7 @@ static snn_status query_tc(snn_index idx, Workspace &ws, cudaStream_t s, int sms
     t.kpad = idx->kpad; t.kblocks = idx->kpad / 32;
     t.blk_lo = blk_lo; t.blk_hi = blk_hi; t.item_start = item_start;
     t.nblocks = nblocks; t.total_items = total_items; t.chunk = chunk;
+    t.diag = g_opt.tc_diag;
     {
         const double c1h = 1.0 - c1 / 2;
         const double r2h = (R * R * (1.0 + 1e-12) * (1.0 + ldexp(1.0, -20)) + c0) / 2;
@@ -477,7 +484,8 @@ static snn_status query_tc(snn_index idx, Workspace &ws, cudaStream_t s, int sms
         CK(cudaStreamSynchronize(s), "tc filter");
         const int64_t np = (int64_t)*reinterpret_cast<unsigned long long *>(hp);
         if (np <= cap) { cap = np; break; }
-        cap = np;   // exact capacity, re-run once
+        // re-run once with room for the count plus every warp's partially used block
+        cap = np + (int64_t)sms * tc_claim_slack();
     }
     const int64_t P = cap;
     const int wtok = prof_begin(F_WRITE, s);

@@ -31,10 +31,12 @@ namespace {
 constexpr int TM = 128, TN = 256, TK = 32, STAGES = 4;
 constexpr int A_BYTES = TM * TK * 4, B_BYTES = TN * TK * 4, STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int STAGE_CAP = 8;                       // staged hits per epilogue thread per tile
+constexpr int ARING = 8;
+constexpr unsigned long long CLAIM = 256;          // pair-list slots claimed per warp atomic                           // x-bar slices in flight (decoupled from TMEM)
 constexpr int EPI = 512;                           // epilogue threads (16 warps)
 constexpr int COLS = TN / (EPI / 128);             // columns per epilogue thread
 constexpr int THREADS = 64 + EPI;
-constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 2 * TN * 4 + EPI * STAGE_CAP * 4 + 512;
+constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + ARING * TN * 4 + EPI * STAGE_CAP * 4 + 512;
 constexpr uint32_t IDESC = (1u << 4)               // D format F32
                          | (2u << 7) | (2u << 10)  // A, B format TF32
                          | ((uint32_t)(TN >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);   // N, M
@@ -126,21 +128,19 @@ tc_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
     uint8_t *gbase = smem_raw + (base - raw);
-    // carve: stages | a_vals[2][TN] | stage hits [EPI][STAGE_CAP] | barriers | tmem ptr
+    // carve: stages | a_vals[ARING][TN] | stage hits [EPI][STAGE_CAP] | barriers | tmem ptr
     float *a_vals = reinterpret_cast<float *>(gbase + STAGES * STAGE_BYTES);
-    int32_t *s_hits = reinterpret_cast<int32_t *>(gbase + STAGES * STAGE_BYTES + 2 * TN * 4);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(gbase + STAGES * STAGE_BYTES + 2 * TN * 4 + EPI * STAGE_CAP * 4);
+    int32_t *s_hits = reinterpret_cast<int32_t *>(gbase + STAGES * STAGE_BYTES + ARING * TN * 4);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(gbase + STAGES * STAGE_BYTES + ARING * TN * 4 + EPI * STAGE_CAP * 4);
     uint64_t *full = bars, *empty = bars + STAGES, *tfull = bars + 2 * STAGES, *tempty = bars + 2 * STAGES + 2;
-    uint64_t *afull = bars + 2 * STAGES + 4, *aempty = bars + 2 * STAGES + 6;
-    uint32_t *tmem_ptr = reinterpret_cast<uint32_t *>(bars + 2 * STAGES + 8);
+    uint64_t *afull = bars + 2 * STAGES + 4, *aempty = bars + 2 * STAGES + 4 + ARING;
+    uint32_t *tmem_ptr = reinterpret_cast<uint32_t *>(bars + 2 * STAGES + 4 + 2 * ARING);
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-        for (int s = 0; s < 2; ++s) {
-            mbar_init(&tfull[s], 1); mbar_init(&tempty[s], EPI);
-            mbar_init(&afull[s], 1); mbar_init(&aempty[s], EPI);
-        }
+        for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], EPI); }
+        for (int s = 0; s < ARING; ++s) { mbar_init(&afull[s], 1); mbar_init(&aempty[s], EPI); }
         fence_mbar_init();
     }
     if (warp == 1) {
@@ -167,8 +167,7 @@ tc_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     mbar_wait_u32(smem_u32(&aempty[aslot]), aph ^ 1);
                     mbar_arrive_expect_tx(&afull[aslot], TN * 4);
                     bulk_g2s(a_vals + aslot * TN, a.xbar + t0, TN * 4, &afull[aslot]);
-                    aslot ^= 1;
-                    if (aslot == 0) aph ^= 1;
+                    if (++aslot == ARING) { aslot = 0; aph ^= 1; }
                     for (int kb = 0; kb < a.kblocks; ++kb) {
                         mbar_wait_u32(smem_u32(&empty[stage]), phase ^ 1);
                         const uint32_t sa = base + stage * STAGE_BYTES, sb = sa + A_BYTES;
@@ -197,9 +196,11 @@ tc_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                         tc_fence_after();
                         const uint32_t sa = base + stage * STAGE_BYTES, sb = sa + A_BYTES;
                         const uint64_t da = sw128_desc(sa), db = sw128_desc(sb);
+                        if (a.diag != 2) {
 #pragma unroll
-                        for (int kk = 0; kk < TK / 8; ++kk)
-                            mma_tf32(dcol, da + 2 * kk, db + 2 * kk, (kb | kk) != 0);
+                            for (int kk = 0; kk < TK / 8; ++kk)
+                                mma_tf32(dcol, da + 2 * kk, db + 2 * kk, (kb | kk) != 0);
+                        }
                         mma_commit(smem_u32(&empty[stage]));
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
@@ -219,23 +220,28 @@ tc_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         const int row = quarter * 32 + lane;
         int32_t *my_hits = s_hits + et * STAGE_CAP;
         const float c1h = a.c1h;
-        uint32_t acc = 0, aphase = 0;
+        uint32_t acc = 0, aphase = 0, aslot = 0, aph = 0;
+        unsigned long long wcur = 0, wend = 0;   // this warp's claimed pair-list block
         for (int64_t item = blockIdx.x; item < a.total_items; item += gridDim.x) {
             int64_t b, c0, c1;
             tc_locate(a, item, b, c0, c1);
             const int64_t sp = b * TM + row;
             const float bi = sp < a.m ? fmaf(a.qbar[sp], c1h, -a.r2h) : INFINITY;
             for (int64_t t0 = c0; t0 < c1; t0 += TN) {
-                const float *av = a_vals + acc * TN + slice * COLS;
-                mbar_wait_u32(smem_u32(&afull[acc]), aphase);
+                const float *av = a_vals + aslot * TN + slice * COLS;
+                mbar_wait_u32(smem_u32(&afull[aslot]), aph);
                 mbar_wait_u32(smem_u32(&tfull[acc]), aphase);
                 tc_fence_after();
                 int nh = 0;
                 const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + acc * TN + slice * COLS;
 #pragma unroll 1
-                for (int ch = 0; ch < COLS / 32; ++ch) {
+                for (int ch = 0; ch < (a.diag == 1 ? 0 : COLS / 32); ++ch) {
                     float v[32];
                     tmem_ld32(taddr + ch * 32, v);
+                    if (a.diag == 3) {   // diagnostics: TMEM read only
+                        if (v[0] == 12345.f && v[31] == 1.f) nh = 1;
+                        continue;
+                    }
                     const float4 *a4 = reinterpret_cast<const float4 *>(av + ch * 32);
 #pragma unroll
                     for (int c4 = 0; c4 < 8; ++c4) {   // v = acc - xbar (1 - c1/2)
@@ -252,20 +258,24 @@ tc_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 #pragma unroll
                     for (int c = 0; c < 3; ++c) m[c] = fmaxf(fmaxf(m[3 * c], m[3 * c + 1]), m[3 * c + 2]);
                     const float mx = fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[9] > m[10] ? m[9] : m[10]));
-                    if (mx >= bi) {
+                    if (mx >= bi && a.diag != 4) {
+                        // rare (per lane): candidate mask, then one staged entry per set bit
+                        uint32_t mask = 0;
 #pragma unroll
-                        for (int c = 0; c < 32; ++c) {
-                            const int64_t jj = t0 + slice * COLS + ch * 32 + c;
-                            if (v[c] >= bi && jj < c1) {
-                                const int32_t j = (int32_t)jj;
-                                if (nh < STAGE_CAP) {
-                                    my_hits[nh++] = j;
-                                } else {   // rare: direct append
-                                    const unsigned long long k = atomicAdd(a.pair_count, 1ull);
-                                    if (k < (unsigned long long)a.pair_cap) {
-                                        a.pair_q[k] = (int32_t)sp;
-                                        a.pair_j[k] = j;
-                                    }
+                        for (int c = 0; c < 32; ++c) mask |= (v[c] >= bi ? 1u : 0u) << c;
+                        const int64_t jb = t0 + slice * COLS + ch * 32;
+                        while (mask) {
+                            const int c = __ffs(mask) - 1;
+                            mask &= mask - 1;
+                            const int64_t jj = jb + c;
+                            if (jj >= c1) break;
+                            if (nh < STAGE_CAP) {
+                                my_hits[nh++] = (int32_t)jj;
+                            } else {   // rare: direct append
+                                const unsigned long long k = atomicAdd(a.pair_count, 1ull);
+                                if (k < (unsigned long long)a.pair_cap) {
+                                    a.pair_q[k] = (int32_t)sp;
+                                    a.pair_j[k] = (int32_t)jj;
                                 }
                             }
                         }
@@ -273,8 +283,10 @@ tc_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 }
                 tc_fence_before();
                 mbar_arrive(smem_u32(&tempty[acc]));
-                mbar_arrive(smem_u32(&aempty[acc]));
-                // one atomic per warp per tile for the staged hits
+                mbar_arrive(smem_u32(&aempty[aslot]));
+                if (++aslot == ARING) { aslot = 0; aph ^= 1; }
+                // staged hits -> the warp's claimed block of the pair list (one global
+                // atomic per CLAIM slots instead of one per tile); unused slots get q = -1
                 if (__any_sync(0xffffffffu, nh > 0)) {
                     int incl = nh;
 #pragma unroll
@@ -283,10 +295,16 @@ tc_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                         if (lane >= o) incl += y;
                     }
                     const int total = __shfl_sync(0xffffffffu, incl, 31);
-                    unsigned long long wbase = 0;
-                    if (lane == 31) wbase = atomicAdd(a.pair_count, (unsigned long long)total);
-                    wbase = __shfl_sync(0xffffffffu, wbase, 31);
-                    const unsigned long long my0 = wbase + (unsigned long long)(incl - nh);
+                    if (wcur + (unsigned long long)total > wend) {
+                        for (unsigned long long k = wcur + lane; k < wend; k += 32)
+                            if (k < (unsigned long long)a.pair_cap) a.pair_q[k] = -1;
+                        const unsigned long long want = total > CLAIM ? (unsigned long long)total : CLAIM;
+                        unsigned long long wb = 0;
+                        if (lane == 0) wb = atomicAdd(a.pair_count, want);
+                        wcur = __shfl_sync(0xffffffffu, wb, 0);
+                        wend = wcur + want;
+                    }
+                    const unsigned long long my0 = wcur + (unsigned long long)(incl - nh);
                     for (int h = 0; h < nh; ++h) {
                         const unsigned long long k = my0 + h;
                         if (k < (unsigned long long)a.pair_cap) {
@@ -294,11 +312,14 @@ tc_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                             a.pair_j[k] = my_hits[h];
                         }
                     }
+                    wcur += (unsigned long long)total;
                 }
                 acc ^= 1;
                 if (acc == 0) aphase ^= 1;
             }
         }
+        for (unsigned long long k = wcur + lane; k < wend; k += 32)
+            if (k < (unsigned long long)a.pair_cap) a.pair_q[k] = -1;
     }
     tc_fence_before();
     __syncthreads();
@@ -341,6 +362,11 @@ __global__ void __launch_bounds__(256) recheck_pairs(const T *__restrict__ Xs, c
                                                      const int32_t *__restrict__ pq, const int32_t *__restrict__ pj,
                                                      int64_t npairs, double R2, uint32_t *flag, float *dist) {
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < npairs; k += (int64_t)gridDim.x * blockDim.x) {
+        if (pq[k] < 0) {   // unused slot of a claimed block
+            flag[k] = 0;
+            dist[k] = 0.f;
+            continue;
+        }
         const T *x = Xs + (int64_t)pj[k] * ld, *q = Qs + (int64_t)pq[k] * ld;
         double s = 0.0;
         if constexpr (sizeof(T) == 4) {   // rows are 16-byte aligned (ld % 4 == 0): vector loads,
@@ -400,6 +426,7 @@ static bool make_map(CUtensorMap *m, const float *ptr, int64_t rows, int kpad, i
 int tc_tile_rows() { return TM; }
 int tc_tile_cols() { return TN; }
 int tc_kpad(int d) { return (int)round_up(d, TK); }
+int64_t tc_claim_slack() { return (int64_t)(EPI / 32) * (int64_t)CLAIM; }
 
 void launch_gather_tf32(const void *X, bool f64, int64_t rows, int d, const uint32_t *perm, const float *mu_f,
                         float *out, float *half_norm, cudaStream_t s) {

@@ -18,11 +18,13 @@ struct TcArgs {
     int32_t *pair_q, *pair_j;            // candidate pairs (sorted query pos, sorted index pos)
     unsigned long long *pair_count;
     int64_t pair_cap;
+    int diag;               // 0; diagnostics: 1 = skip epilogue work, 2 = skip MMAs
 };
 
 int tc_tile_rows();   // queries per tile (128)
 int tc_tile_cols();   // candidates per tile (256)
 int tc_kpad(int d);   // d rounded up to 32
+int64_t tc_claim_slack();   // pair-list slots a CTA may leave unused (claimed blocks)
 
 // TF32 centred copy (row-major, kpad columns) + half norms of the centred rows.
 void launch_gather_tf32(const void *X, bool f64, int64_t rows, int d, const uint32_t *perm, const float *mu_f,
