@@ -34,6 +34,8 @@ struct Options {
     int tc_min_d = 32;
     int tc_tiles = 8;    // 256-candidate tiles per work item on the tensor-core path
     int tc_diag = 0;     // diagnostics only (results invalid): 1 = no epilogue work, 2 = no MMA
+    int tc_f16 = 1;      // tensor-core operands FP16 (scaled) instead of TF32
+    int tc_group = 32;   // query blocks per raster group (upper bound; L2 budget decides)
 };
 static std::atomic<int64_t> g_last_ovf{0}, g_last_lost{0};
 static Options g_opt;
@@ -167,6 +169,18 @@ int64_t row_elems(int d, int ld) { return ld ? ld : d; }
 
 using namespace snn;
 
+// FP16 tensor-core operands: scale 2^e with bound * 2^e in [2^14, 2^15) (no overflow; the
+// subnormal range only adds the absolute error term of the margin).  false if the bound
+// needs |e| > 60 (the TF32 / generic paths are used instead).
+static bool f16_exponent(double bound, int *e) {
+    if (!(bound > 0.0)) { *e = 0; return true; }
+    if (!std::isfinite(bound)) return false;
+    const int ex = 14 - ilogb(bound);
+    if (ex < -60 || ex > 60) return false;
+    *e = ex;
+    return bound * ldexp(1.0, ex) < 32768.0;
+}
+
 static void free_index(snn_index idx) {
     if (!idx) return;
     for (void *p : idx->owned) cudaFreeAsync(p, 0);
@@ -250,6 +264,13 @@ snn_status snn_set_option(const char *key, int64_t value) {
     if (k == "tc_diag") {   // performance diagnostics only: results are NOT valid
         if (value < 0 || value > 4) return fail(SNN_ERR_INVALID_ARGUMENT, "tc_diag must be 0..4");
         g_opt.tc_diag = (int)value;
+        return SNN_OK;
+    }
+    if (k == "tc_f16") { g_opt.tc_f16 = value < 0 ? 0 : 1; return SNN_OK; }
+    if (k == "tc_group") {
+        if (value == 0) value = 32;
+        if (value < 1 || value > 1 << 20) return fail(SNN_ERR_INVALID_ARGUMENT, "tc_group must be >= 1");
+        g_opt.tc_group = (int)value;
         return SNN_OK;
     }
     if (k == "variant") {
@@ -349,14 +370,6 @@ snn_status snn_build(const void *X, int64_t n, int32_t d, snn_dtype dt, void *st
                      sort_tmp, s);                                                 // K4
     launch_gather(Xd, f64, n, d, idx->ld, idx->n_pad, reinterpret_cast<const uint32_t *>(idx->perm),
                   idx->mu_d, idx->Xs, idx->xbar, s);                               // K5
-    if (idx->ld != 0 && g_opt.tc && !g_opt.force_generic && d >= g_opt.tc_min_d) {   // K5': TF32 copy
-        idx->tc = 1;
-        idx->kpad = tc_kpad(d);
-        CKI(own(&idx->Xt, (size_t)n * idx->kpad), "alloc TF32 copy");
-        launch_gather_tf32(Xd, f64, n, d, reinterpret_cast<const uint32_t *>(idx->perm), idx->mu_f,
-                           idx->Xt, idx->xbar, s);
-    }
-    prof_end(ptok, s, (double)n);
     CKI(cudaGetLastError(), "launch");
     double *hs = static_cast<double *>(t_pinned.p);
     CKI(cudaMemcpyAsync(hs, idx->stats, ST_COUNT * 8, cudaMemcpyDeviceToHost, s), "D2H stats");
@@ -368,6 +381,28 @@ snn_status snn_build(const void *X, int64_t n, int32_t d, snn_dtype dt, void *st
         free_index(idx);
         return fail(SNN_ERR_NONFINITE, "X contains NaN or Inf");
     }
+    if (idx->ld != 0 && g_opt.tc && !g_opt.force_generic && d >= g_opt.tc_min_d) {   // K5': TC operand copy
+        idx->tc = 1;
+        int e = 0;
+        idx->tc_f16 = g_opt.tc_f16 && f16_exponent(idx->h_stats[ST_XCMAX], &e);
+        idx->xexp = e;
+        idx->kpad = tc_kpad(d, idx->tc_f16);
+        if (idx->tc_f16) {
+            uint16_t *xt = nullptr;
+            CKI(own(&xt, (size_t)n * idx->kpad), "alloc FP16 copy");
+            idx->Xt = xt;
+            launch_gather_f16(Xd, f64, n, d, reinterpret_cast<const uint32_t *>(idx->perm), idx->mu_f,
+                              ldexpf(1.0f, e), idx->Xt, idx->xbar, s);
+        } else {
+            float *xt = nullptr;
+            CKI(own(&xt, (size_t)n * idx->kpad), "alloc TF32 copy");
+            idx->Xt = xt;
+            launch_gather_tf32(Xd, f64, n, d, reinterpret_cast<const uint32_t *>(idx->perm), idx->mu_f,
+                               xt, idx->xbar, s);
+        }
+        CKI(cudaGetLastError(), "launch");
+    }
+    prof_end(ptok, s, (double)n);
     *out = idx;
     return SNN_OK;
 #undef CKI
@@ -409,13 +444,25 @@ static snn_status make_empty_result(int64_t m, cudaStream_t s, snn_result *out) 
 // Tensor-core query path (d >= tc_min_d): K7 windows (128-query blocks) -> K9 tcgen05
 // candidate filter -> K10 exact fp64 recheck -> hits sorted (index position, then original
 // query id) with two stable radix passes -> CSR.
+// Returns SNN_ERR_UNSUPPORTED (no error message set) when the queries' magnitude does not
+// fit the index's FP16 operand scaling; the caller then uses the generic exact path.
 static snn_status query_tc(snn_index idx, Workspace &ws, cudaStream_t s, int sms, int64_t m, double R,
                            const void *Qs, const float *qkeys, const int32_t *qperm, const double *eq,
-                           const float *Qt, const float *qbar, const int *qflag, snn_result *out) {
+                           const void *Qd, const int *qflag, snn_result *out) {
     const bool f64 = idx->dt == SNN_F64;
+    const bool f16 = idx->tc_f16 != 0;
     const int D = idx->d, TM = tc_tile_rows(), TN = tc_tile_cols();
     const int chunk = TN * g_opt.tc_tiles;
     const int64_t nblocks = ceil_div(m, TM);
+    // grouped raster (tc.cu): G query blocks share each candidate chunk while it is in L2;
+    // their operand tiles (G x 128 x kpad) are budgeted at 48 MB of the 126 MB L2
+    const double a_bytes = (double)TM * idx->kpad * (f16 ? 2 : 4);
+    int64_t G = (int64_t)(48e6 / a_bytes);
+    if (G > g_opt.tc_group) G = g_opt.tc_group;
+    if (G > nblocks) G = nblocks;
+    if (G < 1) G = 1;
+    const int64_t ngroups = ceil_div(nblocks, G);
+    int64_t *grp_lo, *grp_items, *grp_start;
     int64_t *blk_lo, *blk_hi, *nitems, *item_start;
     unsigned long long *pcount, *wpairs;
     uint8_t *scan_tmp;
@@ -437,28 +484,67 @@ static snn_status query_tc(snn_index idx, Workspace &ws, cudaStream_t s, int sms
     w.blk_lo = blk_lo; w.blk_hi = blk_hi; w.nitems = nitems; w.pairs = wpairs;
     launch_block_windows(w, s);                                                    // K7
     CK(ws.alloc(&scan_tmp, scan_temp_bytes(m > nblocks ? m : nblocks) + 4096), "alloc");
-    exclusive_scan_i64(nitems, item_start, nblocks, scan_tmp, s);
+    CK(ws.alloc(&grp_lo, (size_t)ngroups), "alloc");
+    CK(ws.alloc(&grp_items, (size_t)ngroups), "alloc");
+    CK(ws.alloc(&grp_start, (size_t)ngroups + 1), "alloc");
+    launch_tc_group_items(blk_lo, blk_hi, nblocks, (int)G, chunk, grp_lo, grp_items, s);
+    exclusive_scan_i64(grp_items, grp_start, ngroups, scan_tmp, s);
     int64_t *hp = static_cast<int64_t *>(t_pinned.p);
-    CK(cudaMemcpyAsync(hp, item_start + nblocks, 8, cudaMemcpyDeviceToHost, s), "D2H items");
+    CK(cudaMemcpyAsync(hp, grp_start + ngroups, 8, cudaMemcpyDeviceToHost, s), "D2H items");
     CK(cudaMemcpyAsync(hp + 1, qflag, 4, cudaMemcpyDeviceToHost, s), "D2H flag");
     CK(cudaMemcpyAsync(hp + 2, wpairs, 8, cudaMemcpyDeviceToHost, s), "D2H pairs");
+    if (Qd) CK(cudaMemcpyAsync(hp + 3, eq + 1, 8, cudaMemcpyDeviceToHost, s), "D2H query bound");
     CK(cudaStreamSynchronize(s), "query windows");
     const int64_t total_items = hp[0];
     if (*reinterpret_cast<int *>(hp + 1)) return fail(SNN_ERR_NONFINITE, "Q contains NaN or Inf");
     const double pairs_eval = (double)*reinterpret_cast<unsigned long long *>(hp + 2);
+    // tensor-core operand A: the index copy itself (self-query) or the queries' copy
+    const void *Qt = idx->Xt;
+    const float *qbar = idx->xbar;
+    int qexp = idx->xexp;
+    if (Qd) {
+        const double qbound = *reinterpret_cast<double *>(hp + 3);
+        if (f16 && (!f16_exponent(qbound, &qexp) || qexp + idx->xexp < -120 || qexp + idx->xexp > 120))
+            return SNN_ERR_UNSUPPORTED;
+        float *qb = nullptr;
+        CK(ws.alloc(&qb, (size_t)m), "alloc");
+        if (f16) {
+            uint16_t *qt = nullptr;
+            CK(ws.alloc(&qt, (size_t)m * idx->kpad), "alloc");
+            launch_gather_f16(Qd, f64, m, D, reinterpret_cast<const uint32_t *>(qperm), idx->mu_f,
+                              ldexpf(1.0f, qexp), qt, qb, s);
+            Qt = qt;
+        } else {
+            float *qt = nullptr;
+            CK(ws.alloc(&qt, (size_t)m * idx->kpad), "alloc");
+            launch_gather_tf32(Qd, f64, m, D, reinterpret_cast<const uint32_t *>(qperm), idx->mu_f, qt, qb, s);
+            Qt = qt;
+        }
+        qbar = qb;
+    }
 
-    // separable margin (reading C20): TF32 operands treated as truncated (2^-10)
-    // plus fp32 centring, accumulation bound (d+2) 2^-22, fp32 evaluation slack.
-    const double u = ldexp(1.0, -10) + ldexp(1.0, -24);
+    // separable margin (reading C20): operand rounding u (FP16 round-to-nearest
+    // 2^-11, TF32 treated as truncated 2^-10) plus fp32 centring, accumulation bound
+    // (d+2) 2^-22, fp32 evaluation slack; FP16 subnormals add an absolute error eta per
+    // scaled coordinate (2^-25 / scale), bounded via ||x|| <= 1/2 + xbar.
+    const double u = (f16 ? ldexp(1.0, -11) : ldexp(1.0, -10)) + ldexp(1.0, -24);
     const double gacc = (D + 2) * ldexp(1.0, -22);
     const double ga = 2 * u + u * u + gacc * (1 + u) * (1 + u);
-    const double c1 = (2 * ga + ldexp(1.0, -21) + 8 * ldexp(1.0, -24)) * 1.01;
-    const double c0 = 1e-30;
+    double c1 = (2 * ga + ldexp(1.0, -21) + 8 * ldexp(1.0, -24)) * 1.01;
+    double c0 = 1e-30;
+    if (f16) {
+        const double ex = ldexp(1.0, -25 - idx->xexp), eqt = ldexp(1.0, -25 - qexp);
+        const double em = ex > eqt ? ex : eqt;
+        c1 += 2.0 * sqrt((double)D) * em * (1 + u) * 1.01;
+        c0 += (2.0 * sqrt((double)D) * em * (1 + u) + 2.0 * D * ex * eqt) * 1.01;
+    }
     TcArgs t{};
     t.xbar = idx->xbar; t.qbar = qbar; t.n = idx->n; t.m = m;
-    t.kpad = idx->kpad; t.kblocks = idx->kpad / 32;
-    t.blk_lo = blk_lo; t.blk_hi = blk_hi; t.item_start = item_start;
+    t.kpad = idx->kpad; t.kblocks = idx->kpad / (f16 ? 64 : 32);
+    t.blk_lo = blk_lo; t.blk_hi = blk_hi;
+    t.grp_lo = grp_lo; t.grp_start = grp_start; t.ngroups = ngroups; t.group = (int)G;
     t.nblocks = nblocks; t.total_items = total_items; t.chunk = chunk;
+    t.sc = f16 ? ldexpf(1.0f, idx->xexp + qexp) : 1.0f;
     t.diag = g_opt.tc_diag;
     {
         const double c1h = 1.0 - c1 / 2;
@@ -478,7 +564,7 @@ static snn_status query_tc(snn_index idx, Workspace &ws, cudaStream_t s, int sms
         t.pair_q = pq; t.pair_j = pj; t.pair_count = pcount; t.pair_cap = cap;
         CK(cudaMemsetAsync(pcount, 0, 8, s), "memset");
         const int ctok = prof_begin(F_COUNT, s);
-        if (!launch_tc_window(Qt, idx->Xt, t, sms, s)) return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");   // K9
+        if (!launch_tc_window(Qt, idx->Xt, f16, t, sms, s)) return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");   // K9
         prof_end(ctok, s, pairs_eval);
         CK(cudaMemcpyAsync(hp, pcount, 8, cudaMemcpyDeviceToHost, s), "D2H pair count");
         CK(cudaStreamSynchronize(s), "tc filter");
@@ -573,18 +659,18 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
     const double *eq = idx->stats + ST_EX_F;
     int *qflag = nullptr;
     unsigned long long *pairs = nullptr;
-    const float *Qt = idx->Xt, *qbar = idx->xbar;
+    const void *Qd = nullptr;   // raw device queries (tensor-core operand gather)
     CK(ws.alloc(&qflag, 2), "alloc");
     CK(ws.alloc(&pairs, 1), "alloc");
     CK(cudaMemsetAsync(qflag, 0, 8, s), "memset");
     CK(cudaMemsetAsync(pairs, 0, 8, s), "memset");
     if (!self) {
-        const void *Qd = Q;
+        const void *Qdev = Q;
         if (!is_device_ptr(Q)) {
             uint8_t *tmp = nullptr;
             CK(ws.alloc(&tmp, (size_t)m * D * es), "alloc staging");
             CK(cudaMemcpyAsync(tmp, Q, (size_t)m * D * es, cudaMemcpyHostToDevice, s), "H2D Q");
-            Qd = tmp;
+            Qdev = tmp;
         }
         double *qsums = nullptr, *eqd = nullptr;
         uint32_t *qmax = nullptr;
@@ -593,7 +679,7 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
         uint8_t *qs = nullptr, *sort_tmp = nullptr;
         CK(ws.alloc(&qsums, (size_t)D), "alloc");
         CK(ws.alloc(&qmax, (size_t)D), "alloc");
-        CK(ws.alloc(&eqd, 1), "alloc");
+        CK(ws.alloc(&eqd, 2), "alloc");
         CK(ws.alloc(&qk_raw, (size_t)m), "alloc");
         CK(ws.alloc(&qk, (size_t)m), "alloc");
         CK(ws.alloc(&qp, (size_t)m), "alloc");
@@ -602,24 +688,20 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
         CK(cudaMemsetAsync(qsums, 0, D * 8, s), "memset");
         CK(cudaMemsetAsync(qmax, 0, D * 4, s), "memset");
         // K6 query prep: finiteness + max |q| (E_q), keys (Alg. 2 l.2-3), sort, gather
-        launch_colstats(Qd, f64, m, D, qsums, qmax, qflag, s);
+        launch_colstats(Qdev, f64, m, D, qsums, qmax, qflag, s);
         launch_query_key_err(D, f64, qmax, idx->mu_d, idx->mu_f, idx->v_d, idx->v_f, eqd, s);
-        launch_keys(Qd, f64, m, D, idx->mu_d, idx->mu_f, idx->v_d, idx->v_f, qk_raw, s);
+        launch_keys(Qdev, f64, m, D, idx->mu_d, idx->mu_f, idx->v_d, idx->v_f, qk_raw, s);
         radix_sort_pairs(qk_raw, nullptr, qk, reinterpret_cast<uint32_t *>(qp), m, sort_tmp, s);
-        launch_gather(Qd, f64, m, D, ld, round_up(m, 4), reinterpret_cast<const uint32_t *>(qp), idx->mu_d, qs, nullptr, s);
+        launch_gather(Qdev, f64, m, D, ld, round_up(m, 4), reinterpret_cast<const uint32_t *>(qp), idx->mu_d, qs, nullptr, s);
         Qs = qs; qkeys = qk; qperm = qp; eq = eqd;
-        if (idx->tc) {   // TF32 centred queries + half norms (tensor-core operand A)
-            float *qt = nullptr, *qb = nullptr;
-            CK(ws.alloc(&qt, (size_t)m * idx->kpad), "alloc");
-            CK(ws.alloc(&qb, (size_t)m), "alloc");
-            launch_gather_tf32(Qd, f64, m, D, reinterpret_cast<const uint32_t *>(qp), idx->mu_f, qt, qb, s);
-            Qt = qt; qbar = qb;
-        }
+        Qd = Qdev;
     }
     if (idx->tc) {
-        snn_status r = query_tc(idx, ws, s, sms, m, R, Qs, qkeys, qperm, eq, Qt, qbar, qflag, out);
-        prof_end(qtok, s, (double)m);
-        return r;
+        snn_status r = query_tc(idx, ws, s, sms, m, R, Qs, qkeys, qperm, eq, Qd, qflag, out);
+        if (r != SNN_ERR_UNSUPPORTED) {
+            prof_end(qtok, s, (double)m);
+            return r;
+        }   // query magnitudes outside the FP16 operand range: generic exact path below
     }
     const bool generic = ld != 0;
     const int B = generic ? 64 : g_opt.query_block;

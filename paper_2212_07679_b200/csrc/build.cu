@@ -386,7 +386,7 @@ __global__ void finalize_direction(int d, const uint32_t *maxabs_bits, const dou
         sgn = (v_d[best] < 0.0) ? -1.0 : 1.0;
     }
     __syncthreads();
-    double nf = 0.0, nd = 0.0, ef = 0.0, ed = 0.0;
+    double nf = 0.0, nd = 0.0, ef = 0.0, ed = 0.0, xc = 0.0;
     for (int i = threadIdx.x; i < d; i += blockDim.x) {
         double vd = v_d[i] * sgn;
         v_d[i] = vd;
@@ -397,8 +397,11 @@ __global__ void finalize_direction(int d, const uint32_t *maxabs_bits, const dou
         double mx = (double)__uint_as_float(maxabs_bits[i]);
         ef += (mx + fabs((double)mu_f[i])) * fabs((double)vf);
         ed += (mx + fabs(mu_d[i])) * fabs(vd);
+        xc = fmax(xc, mx + fabs((double)mu_f[i]));
     }
     nf = warp_sum(nf); nd = warp_sum(nd); ef = warp_sum(ef); ed = warp_sum(ed);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) xc = fmax(xc, __shfl_xor_sync(0xffffffffu, xc, o));
     if (threadIdx.x == 0) {
         const double u = 5.9604644775390625e-08;  // 2^-24
         const double g = 2.0 * (d + 2) * u;
@@ -406,19 +409,26 @@ __global__ void finalize_direction(int d, const uint32_t *maxabs_bits, const dou
         stats[ST_WNORM_D] = sqrt(nd) * (1.0 + 1e-12);
         stats[ST_EX_F] = g * ef * (1.0 + 1e-10) + 1e-30;
         stats[ST_EX_D] = g * ed * (1.0 + 1e-10) + 1e-30;
+        stats[ST_XCMAX] = xc;
     }
 }
 
 __global__ void query_key_err(int d, bool f64, const uint32_t *maxabs_bits, const double *mu_d,
                               const float *mu_f, const double *v_d, const float *v_f, double *eq) {
-    double e = 0.0;
+    double e = 0.0, xc = 0.0;
     for (int i = threadIdx.x; i < d; i += blockDim.x) {
         double mx = (double)__uint_as_float(maxabs_bits[i]);
         e += f64 ? (mx + fabs(mu_d[i])) * fabs(v_d[i])
                  : (mx + fabs((double)mu_f[i])) * fabs((double)v_f[i]);
+        xc = fmax(xc, mx + fabs((double)mu_f[i]));
     }
     e = warp_sum(e);
-    if (threadIdx.x == 0) *eq = 2.0 * (d + 2) * 5.9604644775390625e-08 * e * (1.0 + 1e-10) + 1e-30;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) xc = fmax(xc, __shfl_xor_sync(0xffffffffu, xc, o));
+    if (threadIdx.x == 0) {
+        eq[0] = 2.0 * (d + 2) * 5.9604644775390625e-08 * e * (1.0 + 1e-10) + 1e-30;
+        eq[1] = xc;
+    }
 }
 
 // ------------------------------------------------------------------------------ K3

@@ -60,9 +60,11 @@ struct snn_index_s {
     double *stats = nullptr;   // ST_COUNT doubles
     double h_stats[snn::ST_COUNT] = {};
     int sm_count = 148;
-    int tc = 0;                // tensor-core (tcgen05 TF32) query path enabled
-    int kpad = 0;              // K padded to 32 for the TF32 copy
-    float *Xt = nullptr;       // n x kpad TF32-rounded centred copy (tensor-core operand)
+    int tc = 0;                // tensor-core (tcgen05) query path enabled
+    int tc_f16 = 0;            // operands FP16 (kind::f16, scaled by 2^xexp) instead of TF32
+    int xexp = 0;              // FP16 operand scale exponent of the index copy
+    int kpad = 0;              // K padded to 64 (FP16) / 32 (TF32)
+    void *Xt = nullptr;        // n x kpad centred tensor-core operand copy (FP16 or TF32)
     std::vector<void *> owned;
 };
 

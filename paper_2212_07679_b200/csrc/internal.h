@@ -20,12 +20,14 @@ void launch_gram(const void *X, bool f64, int64_t n, int d, const float *mu_f, d
 // stats[]: see enum Stat.  maxabs_bits/mu feed the key error bound E_x.
 enum Stat {
     ST_SIGMA1 = 0, ST_ITERS = 1, ST_WNORM_F = 2, ST_WNORM_D = 3, ST_EX_F = 4, ST_EX_D = 5,
+    ST_XCMAX = 6,   // max_k (max|x_k| + |mu_f_k|): bound on |fl32(x - mu_f)| (FP16 operand scale)
     ST_COUNT = 8
 };
 void launch_power_iteration(const double *G, int d, int max_iters, double tol,
                             const uint32_t *maxabs_bits, const double *mu_d, const float *mu_f,
                             double *v_d, float *v_f, double *stats, cudaStream_t s);
-// Key error bound for a query set: eq = 2(d+2)2^-24 sum_k (maxabs_k + |mu_k|)|v_k|.
+// Key error bound for a query set: eq[0] = 2(d+2)2^-24 sum_k (maxabs_k + |mu_k|)|v_k|;
+// eq[1] = max_k (maxabs_k + |mu_f_k|) (bound on the centred query coordinates).
 void launch_query_key_err(int d, bool f64, const uint32_t *maxabs_bits, const double *mu_d,
                           const float *mu_f, const double *v_d, const float *v_f, double *eq,
                           cudaStream_t s);

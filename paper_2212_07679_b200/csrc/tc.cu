@@ -1,24 +1,33 @@
 // tc.cu -- K9: windowed distance tiles on the 5th-generation tensor cores (tcgen05,
-// kind::tf32) for d >= 32, and K10: the exact fp64 recheck of the emitted pairs.
+// kind::f16 with power-of-two-scaled FP16 operands, or kind::tf32) for d >= 32, and K10:
+// the exact fp64 recheck of the emitted pairs.
 //
 // Filter (eq:ip2): with centred operands x_c = x - mu, q_c = q - mu,
 //   d^2 = 2 xbar + 2 qbar - 2 x_c.q_c,   xbar = x_c.x_c / 2 (Alg. 1 l.7).
 // The batched inner products X(J,:) [q_1..q_l] (the "gemm" of PAPER.md:218-219) are one
 // tcgen05.mma tile D[128 queries x 256 candidates] += Q_tile . X_tile^T per 8-wide K step,
-// TF32 operands (pre-rounded, cvt.rna) from shared memory (TMA, 128B swizzle), FP32
-// accumulators in TMEM.  The expanded form is NOT accurate under cancellation (DESIGN.md
+// operands pre-rounded to FP16 (x_c * 2^a, round-to-nearest; unit roundoff 2^-11, half
+// the bytes of TF32 at twice the MMA rate) or TF32 (cvt.rna) in shared memory (TMA,
+// 128B swizzle), FP32 accumulators in TMEM.  The expanded form is NOT accurate under cancellation (DESIGN.md
 // reading C4), so the epilogue only selects CANDIDATES with a rigorous separable margin
 //   |d^2_tc - d^2| <= c1 (xbar + qbar) + c0            (reading C20)
 // i.e. acc - xbar (1 - c1/2) >= qbar (1 - c1/2) - (R^2 (1+1e-12) + c0)/2,
 // and every candidate pair is re-decided by K10 with the oracle's exact fp64 sequence
 // (eq:ip1 on the original coordinates), which also produces the distance.
 //
-// Kernel structure (one CTA per SM, persistent over (query block, candidate chunk) items):
+// Work items are (query block, candidate chunk) pairs in a grouped raster order: for a
+// group of G consecutive query blocks, candidate chunk k of the group's union window is
+// visited by every block of the group before chunk k+1, so an index chunk is read from
+// HBM once per group and re-served from L2 (X of config 4 is 0.8-1.6 GB >> 126 MB L2).
+//
+// Kernel structure (one CTA per SM, persistent over the items):
 //   warp 0    : TMA producer  (cp.async.bulk.tensor.2d, mbarrier full/empty ring, 4 stages)
 //   warp 1    : TMEM allocator + single-thread tcgen05.mma issuer, tcgen05.commit
-//   warps 2-5 : epilogue: tcgen05.ld 32x32b.x32 -> registers, margin test, staged pair
-//               output with one atomic per warp per tile; TMEM double-buffered (2 x 256 cols)
+//   warps 2-17: epilogue: tcgen05.ld 32x32b.x32 -> registers, margin test (FFMA + 3-way
+//               max per 32 columns), per-lane candidate masks, staged pair output into
+//               per-warp claimed blocks; TMEM double-buffered (2 x 256 cols)
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <math.h>
 
 #include "common.cuh"
@@ -28,18 +37,24 @@
 namespace snn {
 namespace {
 
-constexpr int TM = 128, TN = 256, TK = 32, STAGES = 4;
-constexpr int A_BYTES = TM * TK * 4, B_BYTES = TN * TK * 4, STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int TM = 128, TN = 256, STAGES = 4;
+constexpr int KB_BYTES = 128;                      // bytes per operand row per K block (one swizzle atom)
+constexpr int A_BYTES = TM * KB_BYTES, B_BYTES = TN * KB_BYTES, STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int STAGE_CAP = 8;                       // staged hits per epilogue thread per tile
-constexpr int ARING = 8;
-constexpr unsigned long long CLAIM = 256;          // pair-list slots claimed per warp atomic                           // x-bar slices in flight (decoupled from TMEM)
+constexpr int ARING = 8;                           // x-bar slices in flight (decoupled from TMEM)
+constexpr unsigned long long CLAIM = 256;          // pair-list slots claimed per warp atomic
 constexpr int EPI = 512;                           // epilogue threads (16 warps)
 constexpr int COLS = TN / (EPI / 128);             // columns per epilogue thread
 constexpr int THREADS = 64 + EPI;
 constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + ARING * TN * 4 + EPI * STAGE_CAP * 4 + 512;
-constexpr uint32_t IDESC = (1u << 4)               // D format F32
-                         | (2u << 7) | (2u << 10)  // A, B format TF32
-                         | ((uint32_t)(TN >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);   // N, M
+// instruction descriptor: D format F32; A, B format F16 (0, kind::f16) or TF32 (2,
+// kind::tf32); both K-major; N >> 3 at bit 17, M >> 4 at bit 24
+template <bool F16>
+constexpr uint32_t idesc() {
+    return (1u << 4) | ((F16 ? 0u : 2u) << 7) | ((F16 ? 0u : 2u) << 10) |
+           ((uint32_t)(TN >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
+}
+template <bool F16> constexpr int k_elems() { return F16 ? 64 : 32; }   // elements per K block
 
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
     uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
@@ -58,12 +73,21 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map
         : "memory");
 }
 
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t acc) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(acc));
+template <bool F16>
+__device__ __forceinline__ void mma_op(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t acc) {
+    if constexpr (F16) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+            "l"(adesc), "l"(bdesc), "r"(idesc<true>()), "r"(acc));
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+            "l"(adesc), "l"(bdesc), "r"(idesc<false>()), "r"(acc));
+    }
 }
 
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
@@ -111,19 +135,30 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+// item -> (query block b, candidate range [c0, c1)); empty ranges (c0 >= c1) are skipped
+// by every role.  Group g holds blocks [gG, gG + Gc); its items are ordered (chunk k of
+// the group's union window, block), k-major.
 __device__ __forceinline__ void tc_locate(const TcArgs &a, int64_t item, int64_t &b, int64_t &c0, int64_t &c1) {
-    int64_t lo = 0, hi = a.nblocks;
+    int64_t lo = 0, hi = a.ngroups;
     while (hi - lo > 1) {
         int64_t mid = (lo + hi) >> 1;
-        if (a.item_start[mid] <= item) lo = mid; else hi = mid;
+        if (a.grp_start[mid] <= item) lo = mid; else hi = mid;
     }
-    b = lo;
-    c0 = a.blk_lo[b] + (item - a.item_start[b]) * a.chunk;
-    c1 = min(c0 + a.chunk, a.blk_hi[b]);
+    const int64_t g0 = lo * a.group;
+    const int64_t gc = min((int64_t)a.group, a.nblocks - g0);
+    const int64_t r = item - a.grp_start[lo];
+    const int64_t k = r / gc;
+    b = g0 + (r - k * gc);
+    const int64_t base = a.grp_lo[lo] + k * a.chunk;
+    c0 = max(base, a.blk_lo[b]);
+    c1 = min(base + a.chunk, a.blk_hi[b]);
+    if (c1 < c0) c1 = c0;
 }
 
+template <bool F16>
 __global__ void __launch_bounds__(THREADS, 1)
 tc_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcArgs a) {
+    constexpr int TK = k_elems<F16>();
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
@@ -198,8 +233,8 @@ tc_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                         const uint64_t da = sw128_desc(sa), db = sw128_desc(sb);
                         if (a.diag != 2) {
 #pragma unroll
-                            for (int kk = 0; kk < TK / 8; ++kk)
-                                mma_tf32(dcol, da + 2 * kk, db + 2 * kk, (kb | kk) != 0);
+                            for (int kk = 0; kk < 4; ++kk)   // 4 MMAs of 32 bytes of K each
+                                mma_op<F16>(dcol, da + 2 * kk, db + 2 * kk, (kb | kk) != 0);
                         }
                         mma_commit(smem_u32(&empty[stage]));
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -219,14 +254,14 @@ tc_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         const int slice = et >> 7;                    // 0..3
         const int row = quarter * 32 + lane;
         int32_t *my_hits = s_hits + et * STAGE_CAP;
-        const float c1h = a.c1h;
+        const float c1h = a.c1h * a.sc;   // acc is scaled by sc = 2^(a+b) (exact)
         uint32_t acc = 0, aphase = 0, aslot = 0, aph = 0;
         unsigned long long wcur = 0, wend = 0;   // this warp's claimed pair-list block
         for (int64_t item = blockIdx.x; item < a.total_items; item += gridDim.x) {
             int64_t b, c0, c1;
             tc_locate(a, item, b, c0, c1);
             const int64_t sp = b * TM + row;
-            const float bi = sp < a.m ? fmaf(a.qbar[sp], c1h, -a.r2h) : INFINITY;
+            const float bi = sp < a.m ? fmaf(a.qbar[sp], a.c1h, -a.r2h) * a.sc : INFINITY;
             for (int64_t t0 = c0; t0 < c1; t0 += TN) {
                 const float *av = a_vals + aslot * TN + slice * COLS;
                 mbar_wait_u32(smem_u32(&afull[aslot]), aph);
@@ -356,6 +391,38 @@ __global__ void __launch_bounds__(256) gather_tf32(const T *__restrict__ X, int6
     }
 }
 
+// FP16 centred, scaled copy: out[i][k] = rn_f16(fl32(X[perm[i]][k] - mu_f[k]) * scale),
+// scale = 2^e chosen on the host so that |x_c| * scale <= 2^15 (no overflow); zero padded
+// to kpad columns; half norms of the unscaled fp32 centred row (fp64 accumulation).
+template <typename T>
+__global__ void __launch_bounds__(256) gather_f16(const T *__restrict__ X, int64_t rows, int d, int kpad,
+                                                  const uint32_t *__restrict__ perm,
+                                                  const float *__restrict__ mu_f, float scale,
+                                                  __half *__restrict__ out, float *half_norm) {
+    const int l = threadIdx.x % 32;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; i < rows;
+         i += (int64_t)gridDim.x * blockDim.x / 32) {
+        const T *x = X + (int64_t)perm[i] * d;
+        double h = 0.0;
+        for (int k = 2 * l; k < kpad; k += 64) {
+            float v0 = 0.f, v1 = 0.f;
+            if (k < d) {
+                const float c = (float)((double)x[k] - (double)mu_f[k]);
+                h += (double)c * (double)c;
+                v0 = c * scale;
+            }
+            if (k + 1 < d) {
+                const float c = (float)((double)x[k + 1] - (double)mu_f[k + 1]);
+                h += (double)c * (double)c;
+                v1 = c * scale;
+            }
+            *reinterpret_cast<__half2 *>(out + i * kpad + k) = __halves2half2(__float2half_rn(v0), __float2half_rn(v1));
+        }
+        h = warp_sum(h);
+        if (l == 0 && half_norm) half_norm[i] = (float)(0.5 * h);
+    }
+}
+
 // K10: exact recheck of candidate pairs (oracle sequence on the original coordinates).
 template <typename T>
 __global__ void __launch_bounds__(256) recheck_pairs(const T *__restrict__ Xs, const T *__restrict__ Qs, int ld, int d,
@@ -411,41 +478,86 @@ static EncodeTiledFn get_encode() {
     return fn;
 }
 
-static bool make_map(CUtensorMap *m, const float *ptr, int64_t rows, int kpad, int box_rows) {
+static bool make_map(CUtensorMap *m, const void *ptr, bool f16, int64_t rows, int kpad, int box_rows) {
     EncodeTiledFn enc = get_encode();
     if (!enc) return false;
+    const int es_bytes = f16 ? 2 : 4;
     cuuint64_t dims[2] = {(cuuint64_t)kpad, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)kpad * 4};
-    cuuint32_t box[2] = {(cuuint32_t)TK, (cuuint32_t)box_rows};
+    cuuint64_t strides[1] = {(cuuint64_t)kpad * es_bytes};
+    cuuint32_t box[2] = {(cuuint32_t)(KB_BYTES / es_bytes), (cuuint32_t)box_rows};
     cuuint32_t es[2] = {1, 1};
-    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(ptr), dims, strides, box, es,
+    return enc(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void *>(ptr),
+               dims, strides, box, es,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 int tc_tile_rows() { return TM; }
 int tc_tile_cols() { return TN; }
-int tc_kpad(int d) { return (int)round_up(d, TK); }
+int tc_kpad(int d, bool f16) { return (int)round_up(d, f16 ? 64 : 32); }
 int64_t tc_claim_slack() { return (int64_t)(EPI / 32) * (int64_t)CLAIM; }
 
 void launch_gather_tf32(const void *X, bool f64, int64_t rows, int d, const uint32_t *perm, const float *mu_f,
                         float *out, float *half_norm, cudaStream_t s) {
     if (rows == 0) return;
-    const int kpad = tc_kpad(d);
+    const int kpad = tc_kpad(d, false);
     int64_t g = ceil_div(rows * 32, 256);
     if (g > 148 * 16) g = 148 * 16;
     if (f64) SNN_LAUNCH(gather_tf32<double>, (int)g, 256, 0, s, (const double *)X, rows, d, kpad, perm, mu_f, out, half_norm);
     else SNN_LAUNCH(gather_tf32<float>, (int)g, 256, 0, s, (const float *)X, rows, d, kpad, perm, mu_f, out, half_norm);
 }
 
-bool launch_tc_window(const float *Qt, const float *Xt, const TcArgs &a, int sm_count, cudaStream_t s) {
+void launch_gather_f16(const void *X, bool f64, int64_t rows, int d, const uint32_t *perm, const float *mu_f,
+                       float scale, void *out, float *half_norm, cudaStream_t s) {
+    if (rows == 0) return;
+    const int kpad = tc_kpad(d, true);
+    int64_t g = ceil_div(rows * 32, 256);
+    if (g > 148 * 16) g = 148 * 16;
+    __half *o = static_cast<__half *>(out);
+    if (f64) SNN_LAUNCH(gather_f16<double>, (int)g, 256, 0, s, (const double *)X, rows, d, kpad, perm, mu_f, scale, o, half_norm);
+    else SNN_LAUNCH(gather_f16<float>, (int)g, 256, 0, s, (const float *)X, rows, d, kpad, perm, mu_f, scale, o, half_norm);
+}
+
+bool launch_tc_window(const void *Qt, const void *Xt, bool f16, const TcArgs &a, int sm_count, cudaStream_t s) {
     if (a.total_items == 0) return true;
     CUtensorMap ma, mb;
-    if (!make_map(&ma, Qt, a.m, a.kpad, TM) || !make_map(&mb, Xt, a.n, a.kpad, TN)) return false;
-    cudaFuncSetAttribute(tc_window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (!make_map(&ma, Qt, f16, a.m, a.kpad, TM) || !make_map(&mb, Xt, f16, a.n, a.kpad, TN)) return false;
     int g = (int)(a.total_items < sm_count ? a.total_items : sm_count);
-    SNN_LAUNCH(tc_window_kernel, g, THREADS, SMEM_BYTES, s, ma, mb, a);
+    if (f16) {
+        cudaFuncSetAttribute(tc_window_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+        SNN_LAUNCH(tc_window_kernel<true>, g, THREADS, SMEM_BYTES, s, ma, mb, a);
+    } else {
+        cudaFuncSetAttribute(tc_window_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+        SNN_LAUNCH(tc_window_kernel<false>, g, THREADS, SMEM_BYTES, s, ma, mb, a);
+    }
     return true;
+}
+
+// Grouped raster of the work items: per group of G blocks, the union window [lo, hi)
+// and G_c x ceil((hi - lo) / chunk) items (some may be empty).
+__global__ void tc_group_items_kernel(const int64_t *blk_lo, const int64_t *blk_hi, int64_t nblocks, int group,
+                                      int chunk, int64_t ngroups, int64_t *grp_lo, int64_t *grp_items) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= ngroups) return;
+    const int64_t b0 = g * group, b1 = min(nblocks, b0 + group);
+    int64_t lo = INT64_MAX, hi = 0;
+    for (int64_t b = b0; b < b1; ++b) {
+        if (blk_hi[b] > blk_lo[b]) {
+            lo = min(lo, blk_lo[b]);
+            hi = max(hi, blk_hi[b]);
+        }
+    }
+    if (hi <= lo) { grp_lo[g] = 0; grp_items[g] = 0; return; }
+    grp_lo[g] = lo;
+    grp_items[g] = (b1 - b0) * ceil_div(hi - lo, chunk);
+}
+
+void launch_tc_group_items(const int64_t *blk_lo, const int64_t *blk_hi, int64_t nblocks, int group, int chunk,
+                           int64_t *grp_lo, int64_t *grp_items, cudaStream_t s) {
+    const int64_t ng = ceil_div(nblocks, group);
+    if (ng == 0) return;
+    SNN_LAUNCH(tc_group_items_kernel, (int)ceil_div(ng, 256), 256, 0, s, blk_lo, blk_hi, nblocks, group, chunk, ng,
+               grp_lo, grp_items);
 }
 
 void launch_recheck(const void *Xs, const void *Qs, bool f64, int ld, int d, const int32_t *pq, const int32_t *pj,

@@ -10,10 +10,13 @@ struct TcArgs {
     const float *qbar;      // query half norms (sorted, m)
     int64_t n, m;
     int kpad, kblocks;      // K padded to 32; kpad / 32
-    const int64_t *blk_lo, *blk_hi, *item_start;
-    int64_t nblocks, total_items;
+    const int64_t *blk_lo, *blk_hi;
+    const int64_t *grp_lo, *grp_start;   // grouped raster: union lo / first item per group
+    int64_t nblocks, ngroups, total_items;
+    int group;              // query blocks per raster group
     int chunk;              // candidates per work item (multiple of 256)
     float c1h;              // 1 - c1/2   (separable margin, reading C20)
+    float sc;               // operand scale product 2^(a+b) (FP16 operands), 1 for TF32
     float r2h;              // (R^2 (1 + 1e-12) + c0) / 2
     int32_t *pair_q, *pair_j;            // candidate pairs (sorted query pos, sorted index pos)
     unsigned long long *pair_count;
@@ -23,14 +26,20 @@ struct TcArgs {
 
 int tc_tile_rows();   // queries per tile (128)
 int tc_tile_cols();   // candidates per tile (256)
-int tc_kpad(int d);   // d rounded up to 32
+int tc_kpad(int d, bool f16);   // d rounded up to 64 (FP16) or 32 (TF32)
 int64_t tc_claim_slack();   // pair-list slots a CTA may leave unused (claimed blocks)
 
 // TF32 centred copy (row-major, kpad columns) + half norms of the centred rows.
 void launch_gather_tf32(const void *X, bool f64, int64_t rows, int d, const uint32_t *perm, const float *mu_f,
                         float *out, float *half_norm, cudaStream_t s);
+// FP16 centred copy scaled by `scale` (a power of two), zero padded to kpad = tc_kpad(d, true).
+void launch_gather_f16(const void *X, bool f64, int64_t rows, int d, const uint32_t *perm, const float *mu_f,
+                       float scale, void *out, float *half_norm, cudaStream_t s);
+// grp_lo / grp_items for ceil(nblocks / group) raster groups
+void launch_tc_group_items(const int64_t *blk_lo, const int64_t *blk_hi, int64_t nblocks, int group, int chunk,
+                           int64_t *grp_lo, int64_t *grp_items, cudaStream_t s);
 // false if the TMA tensor maps could not be created.
-bool launch_tc_window(const float *Qt, const float *Xt, const TcArgs &a, int sm_count, cudaStream_t s);
+bool launch_tc_window(const void *Qt, const void *Xt, bool f16, const TcArgs &a, int sm_count, cudaStream_t s);
 // K10: exact fp64 recheck of pairs on the original (row-major) coordinates.
 void launch_recheck(const void *Xs, const void *Qs, bool f64, int ld, int d, const int32_t *pq, const int32_t *pj,
                     int64_t npairs, double R2, uint32_t *flag, float *dist, cudaStream_t s);

@@ -368,17 +368,51 @@ def test_tc_and_generic_paths_agree_exactly(snn):
     assert np.array_equal(a.offsets, b.offsets)
 
 
+@pytest.mark.parametrize("f16", [1, -1])
 @pytest.mark.parametrize("d", [32, 48, 96])
-def test_tc_clustered_far_from_origin(snn, d):
+def test_tc_clustered_far_from_origin(snn, d, f16):
     """Tight clusters far from the origin and from each other: |x - mu| >> R, so the
-    expanded form cancels heavily; the margin must keep every true neighbour."""
+    expanded form cancels heavily; the margin must keep every true neighbour (FP16 and
+    TF32 operands)."""
+    import paper_2212_07679_b200 as p
     rng = np.random.default_rng(d)
     centers = rng.standard_normal((6, d)) * 50 + 300
     lab = rng.integers(0, 6, 6000)
     X = (centers[lab] + rng.standard_normal((6000, d)) * 0.05).astype(np.float32)
     R = float(0.05 * np.sqrt(2 * d))           # ~ typical within-cluster distance
-    gpu = run(snn, X, X[:700], R)
+    try:
+        p.snn_set_option("tc_f16", f16)
+        gpu = run(snn, X, X[:700], R)
+    finally:
+        p.snn_set_option("tc_f16", 0)
     compare(gpu, oracle.radius_query(X, X[:700], R))
+
+
+@pytest.mark.parametrize("xs,qs", [(1e-25, 1e-25), (1.0, 1e25), (1e15, 1e15), (1.0, 1e-30)])
+def test_tc_operand_scaling_extremes(snn, xs, qs):
+    """FP16 operands are scaled by powers of two; magnitudes outside the scalable range
+    (index or queries) fall back to TF32 / the generic kernel -- results stay exact."""
+    rng = np.random.default_rng(11)
+    X = (rng.standard_normal((3000, 40)) * xs).astype(np.float32)
+    Q = (rng.standard_normal((300, 40)) * qs).astype(np.float32)
+    Q[:50] = X[:50]
+    R = float(np.sqrt(2 * 40) * max(xs, qs) * 0.9)
+    compare(run(snn, X, Q, R), oracle.radius_query(X, Q, R))
+
+
+@pytest.mark.parametrize("group", [1, 3, 32])
+def test_tc_raster_groups(snn, group):
+    """Grouped raster order of the (query block, chunk) items, incl. empty items."""
+    import paper_2212_07679_b200 as p
+    w = workloads.c3(n=12000, m=1300)
+    ora = oracle.radius_query(w.X, w.Q, 1.8134)
+    try:
+        p.snn_set_option("tc_group", group)
+        p.snn_set_option("tc_tiles", 2)
+        compare(run(snn, w.X, w.Q, 1.8134), ora)
+    finally:
+        p.snn_set_option("tc_group", 0)
+        p.snn_set_option("tc_tiles", 0)
 
 
 def test_tc_tile_edges_and_tiles_option(snn):
@@ -389,8 +423,11 @@ def test_tc_tile_edges_and_tiles_option(snn):
     Q = rng.standard_normal((129, 64)).astype(np.float32)
     ora = oracle.radius_query(X, Q, 9.5)
     try:
-        for tiles in (1, 3, 8):
-            p.snn_set_option("tc_tiles", tiles)
-            compare(run(snn, X, Q, 9.5), ora)
+        for f16 in (1, -1):
+            p.snn_set_option("tc_f16", f16)
+            for tiles in (1, 3, 8):
+                p.snn_set_option("tc_tiles", tiles)
+                compare(run(snn, X, Q, 9.5), ora)
     finally:
         p.snn_set_option("tc_tiles", 0)
+        p.snn_set_option("tc_f16", 0)
