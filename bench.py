@@ -195,7 +195,7 @@ def config_block(w, args):
 
 
 # ----------------------------------------------------------------------------- roofline
-def roofline_block(args, w, prof, times, dev):
+def roofline_block(args, w, prof, times, dev, info):
     """Roofline of the dominant kernel, from CUDA-event times taken by the library on the
     launching stream (snn_profile_*) during the timed steps.
 
@@ -218,13 +218,21 @@ def roofline_block(args, w, prof, times, dev):
         traffic = tr.get(args.config, {}).get("dominant_kernel_dram_bytes_per_launch")
     except Exception:
         pass
-    if w.d >= 32:
-        kpad = (w.d + 31) // 32 * 32
-        flop_per_pair = 2 * kpad
-        peak = float(peaks.get("bf16_tflops", 1590.0)) * 0.5
-        kernel, bound = "tc_window_kernel (K9 tcgen05 kind::tf32 filter)", "tensor"
-        peak_src = f"TF32 dense = bf16_tflops {peaks.get('bf16_tflops')} x 0.5 ({src})"
-        work = f"2*kpad = {flop_per_pair} flop per evaluated pair (padded contraction)"
+    if info.get("tc_operand", 0):
+        f16 = info["tc_operand"] == 1
+        kpad = info["tc_kpad"]
+        flop_per_pair = 2 * w.d
+        if f16:
+            peak = float(peaks.get("bf16_tflops", 1590.0))
+            kernel = "tc_window_kernel<F16=true> (K9 tcgen05 kind::f16 filter)"
+            peak_src = f"FP16 dense = measured bf16_tflops {peaks.get('bf16_tflops')} (same tensor rate; {src})"
+        else:
+            peak = float(peaks.get("bf16_tflops", 1590.0)) * 0.5
+            kernel = "tc_window_kernel<F16=false> (K9 tcgen05 kind::tf32 filter)"
+            peak_src = f"TF32 dense = measured bf16_tflops {peaks.get('bf16_tflops')} x 0.5 (nominal 1.1 : 2.25 PF; {src})"
+        bound = "tensor"
+        work = (f"2d = {flop_per_pair} flop per evaluated pair (PAPER.md:216 expanded-form inner product; "
+                f"the MMA runs K = {kpad}, i.e. {2 * kpad} flop incl. padding)")
     else:
         flop_per_pair = 3 * w.d - 1
         peak = fp32_alu_peak_tflops(sm_max, n_sm)
@@ -274,6 +282,9 @@ def run_gpu(args):
 
     for _ in range(max(3, args.warmup)):
         nnz = step()
+    _idx = snn.snn_build(X)
+    info = snn.snn_index_info(_idx)
+    snn.snn_free(_idx)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
@@ -340,7 +351,7 @@ def run_gpu(args):
     metric = "DBSCAN points/s (index build + DBSCAN, n=2M)" if dbscan else METRIC
     unit = "points/s" if dbscan else "queries/s"
 
-    roofline = roofline_block(args, w, prof, times, dev)
+    roofline = roofline_block(args, w, prof, times, dev, info)
 
     line = {"metric": metric, "value": value, "unit": unit, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,

@@ -76,6 +76,10 @@ typedef struct {
     const int32_t *perm;       /* device, n: pi[sorted position] = original id      */
     const float *xbar;         /* device, n: half squared norms of centered sorted rows */
     const void *xs;            /* device, n x ld: original coordinates in key order */
+    int32_t tc_operand;        /* tensor-core filter operands: 0 none (FFMA / SIMT path),
+                                  1 FP16 (kind::f16, scaled by 2^tc_exp), 2 TF32         */
+    int32_t tc_kpad;           /* K of the tensor-core operand copy (padded d)          */
+    int32_t tc_exp;            /* FP16 operand scale exponent of the index copy         */
 } snn_index_info_t;
 
 /*

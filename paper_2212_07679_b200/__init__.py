@@ -53,7 +53,8 @@ class _Info(ctypes.Structure):
                 ("sigma1", ctypes.c_double), ("key_err", ctypes.c_double),
                 ("v1_norm", ctypes.c_double), ("mu", ctypes.c_void_p), ("v1", ctypes.c_void_p),
                 ("keys", ctypes.c_void_p), ("perm", ctypes.c_void_p), ("xbar", ctypes.c_void_p),
-                ("xs", ctypes.c_void_p)]
+                ("xs", ctypes.c_void_p), ("tc_operand", ctypes.c_int32), ("tc_kpad", ctypes.c_int32),
+                ("tc_exp", ctypes.c_int32)]
 
 
 _lib = None

@@ -36,6 +36,7 @@ struct Options {
     int tc_diag = 0;     // diagnostics only (results invalid): 1 = no epilogue work, 2 = no MMA
     int tc_f16 = 1;      // tensor-core operands FP16 (scaled) instead of TF32
     int tc_group = 32;   // query blocks per raster group (upper bound; L2 budget decides)
+    int tc_gram_min_d = 128;   // Gram matrix on the tensor cores for d >= this
 };
 static std::atomic<int64_t> g_last_ovf{0}, g_last_lost{0};
 static Options g_opt;
@@ -266,6 +267,12 @@ snn_status snn_set_option(const char *key, int64_t value) {
         g_opt.tc_diag = (int)value;
         return SNN_OK;
     }
+    if (k == "tc_gram_min_d") {
+        if (value == 0) value = 128;
+        if (value < 1) return fail(SNN_ERR_INVALID_ARGUMENT, "tc_gram_min_d must be >= 1");
+        g_opt.tc_gram_min_d = (int)value;
+        return SNN_OK;
+    }
     if (k == "tc_f16") { g_opt.tc_f16 = value < 0 ? 0 : 1; return SNN_OK; }
     if (k == "tc_group") {
         if (value == 0) value = 32;
@@ -362,9 +369,17 @@ snn_status snn_build(const void *X, int64_t n, int32_t d, snn_dtype dt, void *st
     const int ptok = prof_begin(F_BUILD, s);
     launch_colstats(Xd, f64, n, d, sums, maxabs, flag, s);                        // K1
     launch_finalize_mean(sums, n, d, idx->mu_d, idx->mu_f, s);
-    launch_gram(Xd, f64, n, d, idx->mu_f, G, s);                                  // K2a
+    bool gram_done = false;
+    if (d >= g_opt.tc_gram_min_d && !g_opt.force_generic) {                       // K2a (tcgen05)
+        uint8_t *gs = nullptr;
+        CKI(ws.alloc(&gs, gram_tc_scratch_bytes(n, d)), "alloc Gram scratch");
+        gram_done = launch_gram_tc(Xd, f64, n, d, maxabs, idx->mu_f, G, gs, sms, s);
+    }
+    if (!gram_done) launch_gram(Xd, f64, n, d, idx->mu_f, G, s);                  // K2a (SIMT)
+    double *pscratch = nullptr;
+    CKI(ws.alloc(&pscratch, power_scratch_doubles(d, sms)), "alloc");
     launch_power_iteration(G, d, g_opt.power_iters, 1e-7, maxabs, idx->mu_d, idx->mu_f,
-                           idx->v_d, idx->v_f, idx->stats, s);                     // K2b
+                           idx->v_d, idx->v_f, idx->stats, pscratch, s);            // K2b
     launch_keys(Xd, f64, n, d, idx->mu_d, idx->mu_f, idx->v_d, idx->v_f, keys_raw, s);  // K3
     radix_sort_pairs(keys_raw, nullptr, idx->keys, reinterpret_cast<uint32_t *>(idx->perm), n,
                      sort_tmp, s);                                                 // K4
@@ -881,6 +896,9 @@ snn_status snn_index_info(snn_index idx, snn_index_info_t *info) {
     info->v1_norm = idx->h_stats[f64 ? ST_WNORM_D : ST_WNORM_F];
     info->mu = idx->mu_d; info->v1 = idx->v_f; info->keys = idx->keys; info->perm = idx->perm;
     info->xbar = idx->xbar; info->xs = idx->Xs;
+    info->tc_operand = idx->tc ? (idx->tc_f16 ? 1 : 2) : 0;
+    info->tc_kpad = idx->kpad;
+    info->tc_exp = idx->xexp;
     return SNN_OK;
 }
 

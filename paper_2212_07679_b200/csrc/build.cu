@@ -15,10 +15,13 @@
 #include <float.h>
 #include <math.h>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "internal.h"
 
 namespace snn {
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -376,16 +379,123 @@ __global__ void __launch_bounds__(1024) power_generic(const double *__restrict__
     if (threadIdx.x == 0) { stats[ST_SIGMA1] = sqrt(fmax(lam, 0.0)); stats[ST_ITERS] = (double)iters; }
 }
 
+// Any d (17..16384): many CTAs, one grid barrier per iteration (cooperative launch).
+// Rows of G are split across the CTAs; every CTA keeps its own copy of v in shared
+// memory and forms the next v from the gathered y = G v, so the normalisation and the
+// convergence test (same data, same order in every CTA) are identical grid-wide.
+__device__ double block_sum_256(double v, double *red) {
+    const int w = threadIdx.x / kWarp, l = threadIdx.x % kWarp;
+    v = warp_sum(v);
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    double t = (l < (int)(blockDim.x / kWarp)) ? red[l] : 0.0;
+    return warp_sum(t);
+}
+
+__global__ void __launch_bounds__(256) power_coop(const double *__restrict__ G, int d, int max_iters, double tol,
+                                                  double *ybuf, double *part, double *v_out, double *stats) {
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ double sv[];   // v (d)
+    __shared__ double red[8];
+    const int w = threadIdx.x / kWarp, l = threadIdx.x % kWarp;
+    const int rpc = (d + (int)gridDim.x - 1) / (int)gridDim.x;
+    const int r0 = blockIdx.x * rpc, r1 = min(d, r0 + rpc);
+    double loc = 0.0;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) { sv[i] = G[(int64_t)i * d + i]; loc += sv[i] * sv[i]; }
+    const double nrm = block_sum_256(loc, red);
+    if (!(nrm > 0.0)) {   // all-zero centred data: v1 = e1 (reading C9)
+        if (blockIdx.x == 0) {
+            for (int i = threadIdx.x; i < d; i += blockDim.x) v_out[i] = (i == 0) ? 1.0 : 0.0;
+            if (threadIdx.x == 0) { stats[ST_SIGMA1] = 0.0; stats[ST_ITERS] = 0.0; }
+        }
+        return;
+    }
+    double inv = 1.0 / sqrt(nrm);
+    for (int i = threadIdx.x; i < d; i += blockDim.x) sv[i] *= inv;
+    __syncthreads();
+    bool restarted = false;
+    int iters = 0;
+    for (int it = 0; it < max_iters; ++it) {
+        double *y = ybuf + (it & 1) * d;
+        double *pb = part + (it & 1) * gridDim.x;
+        for (int row = r0 + w; row < r1; row += blockDim.x / kWarp) {
+            double sacc = 0.0;
+            const double *g = G + (int64_t)row * d;
+            for (int j = l; j < d; j += kWarp) sacc = fma(g[j], sv[j], sacc);
+            sacc = warp_sum(sacc);
+            if (l == 0) y[row] = sacc;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double ps = 0.0;
+            for (int row = r0; row < r1; ++row) ps += y[row] * y[row];
+            pb[blockIdx.x] = ps;
+        }
+        grid.sync();
+        loc = 0.0;
+        for (int c = threadIdx.x; c < (int)gridDim.x; c += blockDim.x) loc += __ldcg(&pb[c]);
+        const double ny = block_sum_256(loc, red);
+        if (!(ny > 0.0)) {
+            if (restarted) break;
+            restarted = true;    // start vector in the null space: restart at e_argmax(diag)
+            int best = 0;
+            for (int i = 1; i < d; ++i) if (G[(int64_t)i * d + i] > G[(int64_t)best * d + best]) best = i;
+            for (int i = threadIdx.x; i < d; i += blockDim.x) sv[i] = (i == best) ? 1.0 : 0.0;
+            __syncthreads();
+            continue;
+        }
+        inv = 1.0 / sqrt(ny);
+        loc = 0.0;
+        for (int i = threadIdx.x; i < d; i += blockDim.x) {
+            const double t = __ldcg(&y[i]) * inv - sv[i];
+            loc += t * t;
+        }
+        const double diff = block_sum_256(loc, red);
+        for (int i = threadIdx.x; i < d; i += blockDim.x) sv[i] = __ldcg(&y[i]) * inv;
+        __syncthreads();
+        iters = it + 1;
+        if (diff <= tol * tol) break;
+    }
+    // Rayleigh quotient for sigma1: lambda = v^T G v (partials per CTA, fixed order)
+    double *pb = part + 2 * gridDim.x;
+    double rq = 0.0;
+    for (int row = r0 + w; row < r1; row += blockDim.x / kWarp) {
+        double sacc = 0.0;
+        const double *g = G + (int64_t)row * d;
+        for (int j = l; j < d; j += kWarp) sacc = fma(g[j], sv[j], sacc);
+        sacc = warp_sum(sacc);
+        if (l == 0) rq += sv[row] * sacc;
+    }
+    const double rqs = block_sum_256(rq, red);
+    if (threadIdx.x == 0) pb[blockIdx.x] = rqs;
+    grid.sync();
+    if (blockIdx.x == 0) {
+        loc = 0.0;
+        for (int c = threadIdx.x; c < (int)gridDim.x; c += blockDim.x) loc += __ldcg(&pb[c]);
+        const double lam = block_sum_256(loc, red);
+        for (int i = threadIdx.x; i < d; i += blockDim.x) v_out[i] = sv[i];
+        if (threadIdx.x == 0) { stats[ST_SIGMA1] = sqrt(fmax(lam, 0.0)); stats[ST_ITERS] = (double)iters; }
+    }
+}
+
 // Sign fix (largest |entry| positive, lowest index on ties), fp32 copy, ||v||, E_x.
 __global__ void finalize_direction(int d, const uint32_t *maxabs_bits, const double *mu_d,
                                    const float *mu_f, double *v_d, float *v_f, double *stats) {
-    __shared__ double sgn;
-    if (threadIdx.x == 0) {
-        int best = 0;
-        for (int i = 1; i < d; ++i) if (fabs(v_d[i]) > fabs(v_d[best])) best = i;
-        sgn = (v_d[best] < 0.0) ? -1.0 : 1.0;
+    // largest |entry| (lowest index on ties): warp-parallel argmax
+    double bv = -1.0;
+    int bi = 0;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) {
+        const double a = fabs(v_d[i]);
+        if (a > bv) { bv = a; bi = i; }
     }
-    __syncthreads();
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    const double sgn = (v_d[bi] < 0.0) ? -1.0 : 1.0;
     double nf = 0.0, nd = 0.0, ef = 0.0, ed = 0.0, xc = 0.0;
     for (int i = threadIdx.x; i < d; i += blockDim.x) {
         double vd = v_d[i] * sgn;
@@ -639,17 +749,37 @@ void launch_gram(const void *X, bool f64, int64_t n, int d, const float *mu_f, d
     else SNN_LAUNCH(gram_tiled<float>, grid, kThreads, 0, s, (const float *)X, n, d, mu_f, G);
 }
 
+size_t power_scratch_doubles(int d, int sm_count) { return (size_t)2 * d + 3 * (size_t)sm_count + 64; }
+
 void launch_power_iteration(const double *G, int d, int max_iters, double tol,
                             const uint32_t *maxabs_bits, const double *mu_d, const float *mu_f,
-                            double *v_d, float *v_f, double *stats, cudaStream_t s) {
+                            double *v_d, float *v_f, double *stats, double *scratch, cudaStream_t s) {
     switch (d) {
 #define CASE(D) case D: SNN_LAUNCH(power_small<D>, 1, 32, 0, s, G, max_iters, v_d, stats); break;
         SNN_SMALL_D_CASES(CASE)
         CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
 #undef CASE
-        default:
+        default: {
+            int grid = 0, dev = 0, nsm = 148;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+            const size_t smem = (size_t)d * sizeof(double);
+            if (d <= 16384 && scratch &&
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&grid, power_coop, 256, smem) == cudaSuccess && grid > 0) {
+                grid = nsm < d ? nsm : d;
+                double *ybuf = scratch, *part = scratch + 2 * d;
+                int mi = max_iters;
+                double tl = tol;
+                void *args[] = {(void *)&G, (void *)&d, (void *)&mi, (void *)&tl, (void *)&ybuf, (void *)&part,
+                                (void *)&v_d, (void *)&stats};
+                count_launch();
+                if (smem > 48 * 1024) cudaFuncSetAttribute(power_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                if (cudaLaunchCooperativeKernel((const void *)power_coop, grid, 256, args, smem, s) == cudaSuccess) break;
+                cudaGetLastError();
+            }
             SNN_LAUNCH(power_generic, 1, 1024, (size_t)2 * d * sizeof(double), s, G, d, max_iters,
                        tol, v_d, stats);
+        }
     }
     SNN_LAUNCH(finalize_direction, 1, 32, 0, s, d, maxabs_bits, mu_d, mu_f, v_d, v_f, stats);
 }

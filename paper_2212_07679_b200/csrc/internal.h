@@ -16,6 +16,11 @@ void launch_finalize_mean(const double *sums, int64_t n, int d, double *mu_d, fl
 // K2a: G += sum_i (p_i - mu)(p_i - mu)^T (fp32 products, fp64 accumulation), G zeroed.
 void launch_gram(const void *X, bool f64, int64_t n, int d, const float *mu_f, double *G,
                  cudaStream_t s);
+// K2a on the tensor cores (tc_gram.cu, large d): same G from a transposed FP16 hi/lo split
+// copy of the centred X (scratch: gram_tc_scratch_bytes).  false if TMA maps are unavailable.
+size_t gram_tc_scratch_bytes(int64_t n, int d);
+bool launch_gram_tc(const void *X, bool f64, int64_t n, int d, const uint32_t *maxabs_bits, const float *mu_f,
+                    double *G, void *scratch, int sm_count, cudaStream_t s);
 // K2b: power iteration on G (d x d, fp64).  Writes v_d (fp64 unit), v_f (fp32), and
 // stats[]: see enum Stat.  maxabs_bits/mu feed the key error bound E_x.
 enum Stat {
@@ -23,9 +28,11 @@ enum Stat {
     ST_XCMAX = 6,   // max_k (max|x_k| + |mu_f_k|): bound on |fl32(x - mu_f)| (FP16 operand scale)
     ST_COUNT = 8
 };
+// scratch: power_scratch_doubles(d, sm_count) doubles (multi-CTA iteration for d > 16).
+size_t power_scratch_doubles(int d, int sm_count);
 void launch_power_iteration(const double *G, int d, int max_iters, double tol,
                             const uint32_t *maxabs_bits, const double *mu_d, const float *mu_f,
-                            double *v_d, float *v_f, double *stats, cudaStream_t s);
+                            double *v_d, float *v_f, double *stats, double *scratch, cudaStream_t s);
 // Key error bound for a query set: eq[0] = 2(d+2)2^-24 sum_k (maxabs_k + |mu_k|)|v_k|;
 // eq[1] = max_k (maxabs_k + |mu_f_k|) (bound on the centred query coordinates).
 void launch_query_key_err(int d, bool f64, const uint32_t *maxabs_bits, const double *mu_d,

@@ -206,10 +206,12 @@ def test_options_do_not_change_results(snn):
 def test_index_build_parity(snn):
     """Alg. 1 outputs: mean, v1, keys within the rigorous bound, stable sort, gather, xbar."""
     import paper_2212_07679_b200 as p
-    for d, n in ((3, 50000), (2, 7777), (64, 20000), (13, 3000)):
+    for d, n in ((3, 50000), (2, 7777), (64, 20000), (13, 3000), (300, 20000), (784, 5000)):
         w = workloads.c2(n=n) if d == 3 else None
+        # spectrum with a clear top gap (d >= 128: 1/sqrt(i) decay, lambda1/lambda2 = 2)
+        scale = np.linspace(3, 0.5, d) if d < 128 else 3.0 / np.sqrt(np.arange(1, d + 1))
         X = w.X if w else np.random.default_rng(d).standard_normal((n, d)).astype(np.float32) * \
-            np.linspace(3, 0.5, d).astype(np.float32)
+            scale.astype(np.float32)
         idx = p.Index(_dev(X))
         arr = idx.arrays()
         info = arr["info"]
@@ -232,6 +234,27 @@ def test_index_build_parity(snn):
         Xc = X[perm].astype(np.float64) - ref["mu"]
         np.testing.assert_allclose(xbar, 0.5 * np.einsum("ij,ij->i", Xc, Xc), rtol=1e-6)
         idx.free()
+
+
+def test_gram_tensor_core_matches_simt(snn):
+    """K2a on tcgen05 (FP16 hi/lo split, d >= 128) vs the SIMT fp32-product Gram: same v1
+    to ~fp32 accuracy, identical radius results."""
+    import paper_2212_07679_b200 as p
+    rng = np.random.default_rng(8)
+    d = 260
+    X = (rng.standard_normal((9000, d)) * (2.0 / np.sqrt(np.arange(1, d + 1))) + 5.0).astype(np.float32)
+    out = {}
+    try:
+        for thr in (128, 100000):
+            p.snn_set_option("tc_gram_min_d", thr)
+            idx = p.Index(_dev(X))
+            out[thr] = idx.arrays()["v1"].cpu().numpy().astype(np.float64)
+            idx.free()
+    finally:
+        p.snn_set_option("tc_gram_min_d", 0)
+    assert abs(out[128] @ out[100000]) > 1 - 1e-8
+    ref = oracle.build_index(X)["v1"]
+    assert abs(out[128] @ ref) > 1 - 1e-8
 
 
 def test_sort_ties_and_signed_zero(snn):
