@@ -15,6 +15,7 @@
 #include "internal.h"
 #include "query.h"
 #include "tc.h"
+#include "csr.h"
 #include "index.h"
 
 namespace snn {
@@ -459,6 +460,74 @@ static snn_status make_empty_result(int64_t m, cudaStream_t s, snn_result *out) 
 // Tensor-core query path (d >= tc_min_d): K7 windows (128-query blocks) -> K9 tcgen05
 // candidate filter -> K10 exact fp64 recheck -> hits sorted (index position, then original
 // query id) with two stable radix passes -> CSR.
+// K11 for the pair-list paths: rechecked pairs (flag = hit, dist) -> CSR in original query
+// order, rows by ascending sorted-index position (csr.cu); rows above the fused sort's
+// capacity fall back to two stable global radix passes.
+static snn_status pairs_to_csr(Workspace &ws, cudaStream_t s, int64_t m, int64_t P, const int32_t *pq,
+                               const int32_t *pj, const uint32_t *flag, const float *dist, const int32_t *qperm,
+                               const int32_t *perm, snn_result *out) {
+    int32_t *row_count, *maxrow;
+    uint8_t *scan_tmp;
+    CK(ws.alloc(&row_count, (size_t)m), "alloc");
+    CK(ws.alloc(&maxrow, 1), "alloc");
+    CK(ws.alloc(&scan_tmp, scan_temp_bytes(m > 0 ? m : 1) + 4096), "alloc");
+    CK(cudaMemsetAsync(row_count, 0, (size_t)m * 4, s), "memset");
+    CK(cudaMemsetAsync(maxrow, 0, 4, s), "memset");
+    snn_result r = new snn_result_s();
+    r->m = m;
+    auto bail = [&](cudaError_t e, const char *where) { snn_result_free(r); return cuda_fail(e, where); };
+    void *p = nullptr;
+    cudaError_t e = cudaMallocAsync(&p, (size_t)(m + 1) * 8, s);
+    if (e != cudaSuccess) return bail(e, "alloc offsets");
+    r->offsets = static_cast<int64_t *>(p);
+    launch_pairs_row_count(flag, pq, qperm, P, m, row_count, maxrow, s);
+    exclusive_scan_i32_to_i64(row_count, r->offsets, m, scan_tmp, s);
+    int64_t *hp = static_cast<int64_t *>(t_pinned.p);
+    if ((e = cudaMemcpyAsync(hp, r->offsets + m, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return bail(e, "D2H");
+    if ((e = cudaMemcpyAsync(hp + 1, maxrow, 4, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return bail(e, "D2H");
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return bail(e, "recheck");
+    const int64_t H = hp[0];
+    const int32_t mr = *reinterpret_cast<int32_t *>(hp + 1);
+    r->nnz = H;
+    if ((e = cudaMallocAsync(&p, (size_t)(H > 0 ? H : 1) * 4, s)) != cudaSuccess) return bail(e, "alloc indices");
+    r->indices = static_cast<int32_t *>(p);
+    if ((e = cudaMallocAsync(&p, (size_t)(H > 0 ? H : 1) * 4, s)) != cudaSuccess) return bail(e, "alloc distances");
+    r->distances = static_cast<float *>(p);
+    if (mr <= csr_row_sort_cap()) {
+        int32_t *cursor;
+        uint64_t *tmp;
+        if ((e = ws.alloc(&cursor, (size_t)m)) != cudaSuccess) return bail(e, "alloc");
+        if ((e = ws.alloc(&tmp, (size_t)(H > 0 ? H : 1))) != cudaSuccess) return bail(e, "alloc");
+        cudaMemsetAsync(cursor, 0, (size_t)m * 4, s);
+        launch_pairs_to_rows(flag, pq, pj, dist, qperm, P, m, r->offsets, cursor, tmp, perm, mr, r->indices,
+                             r->distances, s);
+    } else {   // a row larger than the fused sort's capacity: stable global radix passes
+        uint32_t *hq, *hj, *order1, *k2, *order2, *sk;
+        float *hd;
+        int64_t *pos;
+        uint8_t *scan2, *sort_tmp;
+        int32_t *rc2;
+        if ((e = ws.alloc(&pos, (size_t)P + 1)) != cudaSuccess) return bail(e, "alloc");
+        if ((e = ws.alloc(&scan2, scan_temp_bytes(P > 0 ? P : 1))) != cudaSuccess) return bail(e, "alloc");
+        if ((e = ws.alloc(&rc2, (size_t)m)) != cudaSuccess) return bail(e, "alloc");
+        cudaMemsetAsync(rc2, 0, (size_t)m * 4, s);
+        exclusive_scan_i32_to_i64(reinterpret_cast<const int32_t *>(flag), pos, P, scan2, s);
+        if ((e = ws.alloc(&hq, (size_t)H)) != cudaSuccess || (e = ws.alloc(&hj, (size_t)H)) != cudaSuccess ||
+            (e = ws.alloc(&hd, (size_t)H)) != cudaSuccess || (e = ws.alloc(&order1, (size_t)H)) != cudaSuccess ||
+            (e = ws.alloc(&k2, (size_t)H)) != cudaSuccess || (e = ws.alloc(&order2, (size_t)H)) != cudaSuccess ||
+            (e = ws.alloc(&sk, (size_t)H)) != cudaSuccess ||
+            (e = ws.alloc(&sort_tmp, radix_sort_temp_bytes(H > 0 ? H : 1))) != cudaSuccess)
+            return bail(e, "alloc");
+        launch_tc_scatter(flag, pos, pq, pj, dist, qperm, P, hq, hj, hd, rc2, s);
+        radix_sort_u32_pairs(hj, nullptr, sk, order1, H, sort_tmp, s);
+        launch_gather_u32(hq, order1, H, k2, s);
+        radix_sort_u32_pairs(k2, order1, sk, order2, H, sort_tmp, s);
+        launch_tc_write(order2, hj, hd, perm, H, r->indices, r->distances, s);
+    }
+    *out = r;
+    return SNN_OK;
+}
+
 // Returns SNN_ERR_UNSUPPORTED (no error message set) when the queries' magnitude does not
 // fit the index's FP16 operand scaling; the caller then uses the generic exact path.
 static snn_status query_tc(snn_index idx, Workspace &ws, cudaStream_t s, int sms, int64_t m, double R,
@@ -590,60 +659,22 @@ static snn_status query_tc(snn_index idx, Workspace &ws, cudaStream_t s, int sms
     }
     const int64_t P = cap;
     const int wtok = prof_begin(F_WRITE, s);
-    uint32_t *flag, *hq, *hj, *order1, *k2, *order2, *sk;
-    float *dist, *hd;
-    int64_t *pos;
-    int32_t *row_count;
-    uint8_t *sort_tmp;
+    uint32_t *flag;
+    float *dist;
     CK(ws.alloc(&flag, (size_t)P), "alloc");
     CK(ws.alloc(&dist, (size_t)P), "alloc");
-    CK(ws.alloc(&pos, (size_t)P + 1), "alloc");
-    CK(ws.alloc(&row_count, (size_t)m), "alloc");
-    CK(cudaMemsetAsync(row_count, 0, (size_t)m * 4, s), "memset");
     const int ld = idx->ld;
     launch_recheck(idx->Xs, Qs, f64, ld, D, pq, pj, P, R * R, flag, dist, s);            // K10
-    uint8_t *scan2;
-    CK(ws.alloc(&scan2, scan_temp_bytes(P > 0 ? P : 1)), "alloc");
-    exclusive_scan_i32_to_i64(reinterpret_cast<const int32_t *>(flag), pos, P, scan2, s);
-    CK(cudaMemcpyAsync(hp, pos + P, 8, cudaMemcpyDeviceToHost, s), "D2H hits");
-    CK(cudaStreamSynchronize(s), "recheck");
-    const int64_t H = hp[0];
-    CK(ws.alloc(&hq, (size_t)H), "alloc");
-    CK(ws.alloc(&hj, (size_t)H), "alloc");
-    CK(ws.alloc(&hd, (size_t)H), "alloc");
-    CK(ws.alloc(&order1, (size_t)H), "alloc");
-    CK(ws.alloc(&k2, (size_t)H), "alloc");
-    CK(ws.alloc(&order2, (size_t)H), "alloc");
-    CK(ws.alloc(&sk, (size_t)H), "alloc");
-    CK(ws.alloc(&sort_tmp, radix_sort_temp_bytes(H > 0 ? H : 1)), "alloc");
-    launch_tc_scatter(flag, pos, pq, pj, dist, qperm, P, hq, hj, hd, row_count, s);
-    // deterministic row order: stable sort by index position, then by original query id
-    radix_sort_u32_pairs(hj, nullptr, sk, order1, H, sort_tmp, s);
-    launch_gather_u32(hq, order1, H, k2, s);
-    radix_sort_u32_pairs(k2, order1, sk, order2, H, sort_tmp, s);
-
-    snn_result r = new snn_result_s();
-    r->m = m;
-    r->nnz = H;
-    auto bail = [&](cudaError_t e, const char *where) { snn_result_free(r); return cuda_fail(e, where); };
-    void *p = nullptr;
-    cudaError_t e = cudaMallocAsync(&p, (size_t)(m + 1) * 8, s);
-    if (e != cudaSuccess) return bail(e, "alloc offsets");
-    r->offsets = static_cast<int64_t *>(p);
-    e = cudaMallocAsync(&p, (size_t)(H > 0 ? H : 1) * 4, s);
-    if (e != cudaSuccess) return bail(e, "alloc indices");
-    r->indices = static_cast<int32_t *>(p);
-    e = cudaMallocAsync(&p, (size_t)(H > 0 ? H : 1) * 4, s);
-    if (e != cudaSuccess) return bail(e, "alloc distances");
-    r->distances = static_cast<float *>(p);
-    exclusive_scan_i32_to_i64(row_count, r->offsets, m, scan_tmp, s);
-    launch_tc_write(order2, hj, hd, idx->perm, H, r->indices, r->distances, s);
+    snn_result r = nullptr;
+    snn_status st = pairs_to_csr(ws, s, m, P, pq, pj, flag, dist, qperm, idx->perm, &r);   // K11
+    if (st != SNN_OK) return st;
+    const int64_t H = r->nnz;
     prof_end(wtok, s, (double)H);
-    g_last_ovf = P - H;   // candidates rejected by the exact recheck
+    g_last_ovf = P - H;   // pair-list slots that are not hits (rejected candidates + unused slots)
     g_last_lost = 0;
-    e = cudaGetLastError();
+    cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    if (e != cudaSuccess) return bail(e, "query");
+    if (e != cudaSuccess) { snn_result_free(r); return cuda_fail(e, "query"); }
     *out = r;
     return SNN_OK;
 }

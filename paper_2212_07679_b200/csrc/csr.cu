@@ -1,0 +1,164 @@
+// csr.cu -- K11 for the pair-list paths: candidate pairs that passed the exact recheck
+// -> CSR rows ("retrieve all data points" within R; rows in original query order,
+// entries in ascending sorted-index position, i.e. key order; ids via pi, Alg. 1 l.6).
+//
+//   count   : hits per original query row (atomics), largest row
+//   scan    : offsets (int64, m + 1)
+//   scatter : each hit to offsets[q] + atomic cursor -> (position << 32 | fp32 dist bits)
+//   sort    : every row sorted by sorted-index position (unique within a row, so the result
+//             is deterministic): warp bitonic sort in registers (<= 32) or shared memory
+//             (<= 512), one CTA per row in shared memory (<= 16384); the caller falls
+//             back to the global radix path beyond that.
+#include <stdint.h>
+
+#include "common.cuh"
+#include "csr.h"
+
+namespace snn {
+namespace {
+
+constexpr int WCAP = 512;         // entries per warp-sorted row
+constexpr int BCAP = 16384;       // entries per CTA-sorted row
+
+__global__ void pairs_row_count_kernel(const uint32_t *flag, const int32_t *pq, const int32_t *qperm, int64_t P,
+                                       int32_t *row_count) {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < P; k += (int64_t)gridDim.x * blockDim.x)
+        if (flag[k]) atomicAdd(&row_count[qperm[pq[k]]], 1);
+}
+
+__global__ void row_max_kernel(const int32_t *row_count, int64_t m, int32_t *maxrow) {
+    int32_t mx = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        mx = max(mx, row_count[i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0 && mx > 0) atomicMax(maxrow, mx);
+}
+
+__global__ void pairs_scatter_kernel(const uint32_t *flag, const int32_t *pq, const int32_t *pj, const float *dist,
+                                     const int32_t *qperm, int64_t P, const int64_t *offsets, int32_t *cursor,
+                                     uint64_t *tmp) {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < P; k += (int64_t)gridDim.x * blockDim.x) {
+        if (!flag[k]) continue;
+        const int32_t q = qperm[pq[k]];
+        const int64_t pos = offsets[q] + atomicAdd(&cursor[q], 1);
+        tmp[pos] = ((uint64_t)(uint32_t)pj[k] << 32) | (uint64_t)__float_as_uint(dist[k]);
+    }
+}
+
+__device__ __forceinline__ void emit(uint64_t v, const int32_t *perm, int32_t *out_idx, float *out_dist, int64_t pos) {
+    out_idx[pos] = perm[(uint32_t)(v >> 32)];
+    out_dist[pos] = __uint_as_float((uint32_t)v);
+}
+
+// one warp per row (rows with <= WCAP entries)
+__global__ void __launch_bounds__(256) rows_sort_warp_kernel(const int64_t *offsets, int64_t m, const uint64_t *tmp,
+                                                             const int32_t *perm, int32_t *out_idx, float *out_dist) {
+    __shared__ uint64_t sbuf[8][WCAP];
+    const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+    uint64_t *buf = sbuf[w];
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; r < m;
+         r += (int64_t)gridDim.x * blockDim.x / 32) {
+        const int64_t o0 = offsets[r];
+        const int cnt = (int)(offsets[r + 1] - o0);
+        if (cnt == 0 || cnt > WCAP) continue;
+        if (cnt <= 32) {   // registers + shuffles
+            uint64_t v = lane < cnt ? tmp[o0 + lane] : ~0ull;
+#pragma unroll
+            for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+                for (int j = k >> 1; j > 0; j >>= 1) {
+                    const uint64_t o = __shfl_xor_sync(0xffffffffu, v, j);
+                    const bool up = (lane & k) == 0;
+                    const bool lower = (lane & j) == 0;
+                    const uint64_t lo = v < o ? v : o, hi = v < o ? o : v;
+                    v = (lower == up) ? lo : hi;
+                }
+            }
+            if (lane < cnt) emit(v, perm, out_idx, out_dist, o0 + lane);
+            continue;
+        }
+        int S = 64;
+        while (S < cnt) S <<= 1;
+        for (int i = lane; i < S; i += 32) buf[i] = i < cnt ? tmp[o0 + i] : ~0ull;
+        __syncwarp();
+        for (int k = 2; k <= S; k <<= 1) {
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int i = lane; i < S; i += 32) {
+                    const int p = i ^ j;
+                    if (p > i) {
+                        const uint64_t a = buf[i], b = buf[p];
+                        const bool up = (i & k) == 0;
+                        if ((a > b) == up) { buf[i] = b; buf[p] = a; }
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        for (int i = lane; i < cnt; i += 32) emit(buf[i], perm, out_idx, out_dist, o0 + i);
+        __syncwarp();
+    }
+}
+
+// one CTA per row with WCAP < entries <= BCAP (dynamic shared memory, S x 8 bytes)
+__global__ void __launch_bounds__(1024) rows_sort_block_kernel(const int64_t *offsets, int64_t m, const uint64_t *tmp,
+                                                               const int32_t *perm, int32_t *out_idx, float *out_dist) {
+    extern __shared__ uint64_t bbuf[];
+    for (int64_t r = blockIdx.x; r < m; r += gridDim.x) {
+        const int64_t o0 = offsets[r];
+        const int cnt = (int)(offsets[r + 1] - o0);
+        if (cnt <= WCAP || cnt > BCAP) continue;   // uniform over the CTA
+        int S = 1024;
+        while (S < cnt) S <<= 1;
+        for (int i = threadIdx.x; i < S; i += blockDim.x) bbuf[i] = i < cnt ? tmp[o0 + i] : ~0ull;
+        __syncthreads();
+        for (int k = 2; k <= S; k <<= 1) {
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int i = threadIdx.x; i < S; i += blockDim.x) {
+                    const int p = i ^ j;
+                    if (p > i) {
+                        const uint64_t a = bbuf[i], b = bbuf[p];
+                        const bool up = (i & k) == 0;
+                        if ((a > b) == up) { bbuf[i] = b; bbuf[p] = a; }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        for (int i = threadIdx.x; i < cnt; i += blockDim.x) emit(bbuf[i], perm, out_idx, out_dist, o0 + i);
+        __syncthreads();
+    }
+}
+
+int grid_n(int64_t n, int per = 256) {
+    int64_t g = ceil_div(n, per);
+    return (int)(g < 1 ? 1 : (g > 148 * 16 ? 148 * 16 : g));
+}
+
+}  // namespace
+
+int csr_row_sort_cap() { return BCAP; }
+
+void launch_pairs_row_count(const uint32_t *flag, const int32_t *pq, const int32_t *qperm, int64_t P, int64_t m,
+                            int32_t *row_count, int32_t *maxrow, cudaStream_t s) {
+    if (P > 0) SNN_LAUNCH(pairs_row_count_kernel, grid_n(P), 256, 0, s, flag, pq, qperm, P, row_count);
+    if (m > 0) SNN_LAUNCH(row_max_kernel, grid_n(m), 256, 0, s, row_count, m, maxrow);
+}
+
+void launch_pairs_to_rows(const uint32_t *flag, const int32_t *pq, const int32_t *pj, const float *dist,
+                          const int32_t *qperm, int64_t P, int64_t m, const int64_t *offsets, int32_t *cursor,
+                          uint64_t *tmp, const int32_t *perm, int32_t max_row, int32_t *out_idx, float *out_dist,
+                          cudaStream_t s) {
+    if (P > 0) SNN_LAUNCH(pairs_scatter_kernel, grid_n(P), 256, 0, s, flag, pq, pj, dist, qperm, P, offsets, cursor, tmp);
+    if (m == 0 || max_row == 0) return;
+    SNN_LAUNCH(rows_sort_warp_kernel, grid_n(m * 32), 256, 0, s, offsets, m, tmp, perm, out_idx, out_dist);
+    if (max_row > WCAP) {
+        int S = 1024;
+        while (S < max_row && S < BCAP) S <<= 1;
+        const size_t smem = (size_t)S * 8;
+        cudaFuncSetAttribute(rows_sort_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        SNN_LAUNCH(rows_sort_block_kernel, 148 * 2, 1024, smem, s, offsets, m, tmp, perm, out_idx, out_dist);
+    }
+}
+
+}  // namespace snn

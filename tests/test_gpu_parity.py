@@ -423,6 +423,19 @@ def test_tc_operand_scaling_extremes(snn, xs, qs):
     compare(run(snn, X, Q, R), oracle.radius_query(X, Q, R))
 
 
+@pytest.mark.parametrize("nbig", [300, 3000, 20000])
+def test_tc_csr_row_sizes(snn, nbig):
+    """Rows of every size class of the CSR row sort (registers <= 32, warp <= 512,
+    CTA <= 16384, global radix fallback beyond): a dense blob plus scattered points."""
+    rng = np.random.default_rng(nbig)
+    d = 32
+    X = np.concatenate([rng.standard_normal((nbig, d)) * 0.01,
+                        rng.standard_normal((4000, d)) * 3.0]).astype(np.float32)
+    Q = np.concatenate([X[:5], X[-200:], rng.standard_normal((50, d)).astype(np.float32) * 0.01])
+    R = 1.0
+    compare(run(snn, X, Q, R), oracle.radius_query(X, Q, R))
+
+
 @pytest.mark.parametrize("group", [1, 3, 32])
 def test_tc_raster_groups(snn, group):
     """Grouped raster order of the (query block, chunk) items, incl. empty items."""
