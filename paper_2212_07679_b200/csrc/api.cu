@@ -38,6 +38,9 @@ struct Options {
     int tc_f16 = 1;      // tensor-core operands FP16 (scaled) instead of TF32
     int tc_group = 32;   // query blocks per raster group (upper bound; L2 budget decides)
     int tc_gram_min_d = 128;   // Gram matrix on the tensor cores for d >= this
+    int lowd_tc = 1;     // low-d (fp32, d <= 8) radius queries through the tensor-core filter
+    int lowd_tc_tiles = 8;     // 256-candidate tiles per work item (low-d tensor-core path)
+    int lowd_tc_group = 8;     // query blocks per raster group (low-d tensor-core path)
 };
 static std::atomic<int64_t> g_last_ovf{0}, g_last_lost{0};
 static Options g_opt;
@@ -272,6 +275,19 @@ snn_status snn_set_option(const char *key, int64_t value) {
         if (value == 0) value = 128;
         if (value < 1) return fail(SNN_ERR_INVALID_ARGUMENT, "tc_gram_min_d must be >= 1");
         g_opt.tc_gram_min_d = (int)value;
+        return SNN_OK;
+    }
+    if (k == "lowd_tc") { g_opt.lowd_tc = value < 0 ? 0 : 1; return SNN_OK; }
+    if (k == "lowd_tc_tiles") {
+        if (value == 0) value = 8;
+        if (value < 1 || value > 64) return fail(SNN_ERR_INVALID_ARGUMENT, "lowd_tc_tiles must be 1..64");
+        g_opt.lowd_tc_tiles = (int)value;
+        return SNN_OK;
+    }
+    if (k == "lowd_tc_group") {
+        if (value == 0) value = 8;
+        if (value < 1 || value > 1 << 20) return fail(SNN_ERR_INVALID_ARGUMENT, "lowd_tc_group must be >= 1");
+        g_opt.lowd_tc_group = (int)value;
         return SNN_OK;
     }
     if (k == "tc_f16") { g_opt.tc_f16 = value < 0 ? 0 : 1; return SNN_OK; }
@@ -679,6 +695,132 @@ static snn_status query_tc(snn_index idx, Workspace &ws, cudaStream_t s, int sms
     return SNN_OK;
 }
 
+// Low-d tensor-core query path (fp32 data, d <= 8, AoSoA4 copies): K7 windows (128-query
+// blocks, grouped raster) -> folded split-FP16 tcgen05 filter (tc_lowd.cu) -> exact fp64
+// recheck -> K11.  Returns SNN_ERR_UNSUPPORTED (no message) when the folded terms do not
+// fit FP16 (huge R relative to the data) -- the FFMA path is used then.
+static snn_status query_tcl(snn_index idx, Workspace &ws, cudaStream_t s, int sms, int64_t m, double R,
+                            const void *Qs, const float *qkeys, const int32_t *qperm, const double *eq, bool self,
+                            const int *qflag, snn_result *out) {
+    const int D = idx->d;
+    const int TM = 128, TN = 256, kc = tcl_kc(D);
+    const int chunk = TN * g_opt.lowd_tc_tiles;
+    const int64_t nblocks = ceil_div(m, TM);
+    int64_t G = g_opt.lowd_tc_group;
+    if (G > nblocks) G = nblocks;
+    if (G < 1) G = 1;
+    const int64_t ngroups = ceil_div(nblocks, G);
+    int64_t *blk_lo, *blk_hi, *nitems, *grp_lo, *grp_items, *grp_start;
+    unsigned long long *pcount, *wpairs;
+    uint8_t *scan_tmp;
+    CK(ws.alloc(&blk_lo, (size_t)nblocks), "alloc");
+    CK(ws.alloc(&blk_hi, (size_t)nblocks), "alloc");
+    CK(ws.alloc(&nitems, (size_t)nblocks), "alloc");
+    CK(ws.alloc(&grp_lo, (size_t)ngroups), "alloc");
+    CK(ws.alloc(&grp_items, (size_t)ngroups), "alloc");
+    CK(ws.alloc(&grp_start, (size_t)ngroups + 1), "alloc");
+    CK(ws.alloc(&pcount, 1), "alloc");
+    CK(ws.alloc(&wpairs, 1), "alloc");
+    CK(ws.alloc(&scan_tmp, scan_temp_bytes(ngroups + 1) + 4096), "alloc");
+    CK(cudaMemsetAsync(wpairs, 0, 8, s), "memset");
+    WindowSpec w;
+    w.qkeys = qkeys; w.m = m; w.B = TM; w.keys = idx->keys; w.n = idx->n; w.n_pad = idx->n_pad;
+    w.R = R;
+    w.wnorm = idx->stats + ST_WNORM_F;
+    w.ex = idx->stats + ST_EX_F;
+    w.eq = eq;
+    w.chunk = chunk;
+    w.blk_lo = blk_lo; w.blk_hi = blk_hi; w.nitems = nitems; w.pairs = wpairs;
+    launch_block_windows(w, s);                                                    // K7
+    launch_tc_group_items(blk_lo, blk_hi, nblocks, (int)G, chunk, grp_lo, grp_items, s);
+    exclusive_scan_i64(grp_items, grp_start, ngroups, scan_tmp, s);
+    int64_t *hp = static_cast<int64_t *>(t_pinned.p);
+    CK(cudaMemcpyAsync(hp, grp_start + ngroups, 8, cudaMemcpyDeviceToHost, s), "D2H items");
+    CK(cudaMemcpyAsync(hp + 1, qflag, 4, cudaMemcpyDeviceToHost, s), "D2H flag");
+    CK(cudaMemcpyAsync(hp + 2, wpairs, 8, cudaMemcpyDeviceToHost, s), "D2H pairs");
+    if (!self) CK(cudaMemcpyAsync(hp + 3, eq + 1, 8, cudaMemcpyDeviceToHost, s), "D2H query bound");
+    CK(cudaStreamSynchronize(s), "query windows");
+    const int64_t total_items = hp[0];
+    if (*reinterpret_cast<int *>(hp + 1)) return fail(SNN_ERR_NONFINITE, "Q contains NaN or Inf");
+    const double pairs_eval = (double)*reinterpret_cast<unsigned long long *>(hp + 2);
+    const double xb = idx->h_stats[ST_XCMAX];
+    const double qb = self ? xb : *reinterpret_cast<double *>(hp + 3);
+    const double bound = xb > qb ? xb : qb;
+    int e = 0;
+    if (bound > 0.0) {
+        if (!std::isfinite(bound)) return SNN_ERR_UNSUPPORTED;
+        e = 11 - ilogb(bound);   // |x * 2^e| < 2^12 for every centred coordinate
+        if (e < -40 || e > 40) return SNN_ERR_UNSUPPORTED;
+    }
+    // Rigorous margin (reading C20, low-d form): E <= (c1/2)(xbar + qbar) + c0/2
+    // bounds the error of the folded left side; see tc_lowd.cu for the operand layout.
+    const double u24 = ldexp(1.0, -24), u22 = ldexp(1.0, -22) * 1.0001;
+    const double us = u24 * 1.0001 + u22;                 // centring + two-half split
+    const double eta = ldexp(1.0, -25 - e);               // FP16 subnormal, per coordinate
+    const double eta2 = ldexp(1.0, -25 + 15 - 2 * e);     // FP16 subnormal of the folded scalars
+    const double gacc = (3.0 * D + 4 + 2) * ldexp(1.0, -22);
+    const double r2 = R * R * (1.0 + 1e-12) * (1.0 + ldexp(1.0, -20));
+    const double sd = sqrt((double)D);
+    const double c1 = 2.0 * 1.05 * (2 * us + us * us + u22 + 2 * u24 + u22 + 2.002 * gacc + eta * sd * (1 + us));
+    const double c0 = 2.0 * 1.05 * (eta * sd * (1 + us) + D * eta * eta + 2 * eta2 + (u22 + gacc) * (r2 / 2 * 1.01 + 1e-300));
+    const double c1h = 1.0 - c1 / 2;
+    const double r2h = (r2 + c0) / 2;
+    // FP16 range of the folded scalars (xbar' and b' below 65504)
+    const double s2 = ldexp(1.0, 2 * e - 15);
+    const double hmax = 0.5 * D * bound * bound * 1.001;
+    if (hmax * s2 >= 60000.0 || (hmax + r2h) * s2 >= 60000.0) return SNN_ERR_UNSUPPORTED;
+
+    uint16_t *cand = nullptr, *qry = nullptr;
+    CK(ws.alloc(&cand, (size_t)idx->n_pad * kc), "alloc");
+    CK(ws.alloc(&qry, (size_t)m * kc), "alloc");
+    const float *Xs = static_cast<const float *>(idx->Xs), *Qf = static_cast<const float *>(Qs);
+    if (self) {
+        launch_tcl_operands(Xs, D, idx->n, idx->n_pad, idx->mu_f, e, c1h, r2h, cand, qry, s);
+    } else {
+        launch_tcl_operands(Xs, D, idx->n, idx->n_pad, idx->mu_f, e, c1h, r2h, cand, nullptr, s);
+        launch_tcl_operands(Qf, D, m, m, idx->mu_f, e, c1h, r2h, nullptr, qry, s);
+    }
+    TclArgs t{};
+    t.n = idx->n; t.m = m;
+    t.blk_lo = blk_lo; t.blk_hi = blk_hi; t.grp_lo = grp_lo; t.grp_start = grp_start;
+    t.nblocks = nblocks; t.ngroups = ngroups; t.total_items = total_items; t.group = (int)G; t.chunk = chunk;
+    int64_t cap = (int64_t)64 * m;
+    if (cap < (int64_t(1) << 22)) cap = int64_t(1) << 22;
+    int32_t *pq = nullptr, *pj = nullptr;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        CK(ws.alloc(&pq, (size_t)cap), "alloc pairs");
+        CK(ws.alloc(&pj, (size_t)cap), "alloc pairs");
+        t.pair_q = pq; t.pair_j = pj; t.pair_count = pcount; t.pair_cap = cap;
+        CK(cudaMemsetAsync(pcount, 0, 8, s), "memset");
+        const int ctok = prof_begin(F_COUNT, s);
+        if (!launch_tcl_window(qry, cand, kc, idx->n_pad, t, sms, s)) return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        prof_end(ctok, s, pairs_eval);
+        CK(cudaMemcpyAsync(hp, pcount, 8, cudaMemcpyDeviceToHost, s), "D2H pair count");
+        CK(cudaStreamSynchronize(s), "tc filter");
+        const int64_t np = (int64_t)*reinterpret_cast<unsigned long long *>(hp);
+        if (np <= cap) { cap = np; break; }
+        cap = np + (int64_t)sms * tcl_claim_slack();
+    }
+    const int64_t P = cap;
+    const int wtok = prof_begin(F_WRITE, s);
+    uint32_t *flag;
+    float *dist;
+    CK(ws.alloc(&flag, (size_t)P), "alloc");
+    CK(ws.alloc(&dist, (size_t)P), "alloc");
+    launch_tcl_recheck(Xs, Qf, D, pq, pj, P, R * R, flag, dist, s);                // K10
+    snn_result r = nullptr;
+    snn_status st = pairs_to_csr(ws, s, m, P, pq, pj, flag, dist, qperm, idx->perm, &r);   // K11
+    if (st != SNN_OK) return st;
+    prof_end(wtok, s, (double)r->nnz);
+    g_last_ovf = P - r->nnz;
+    g_last_lost = 0;
+    cudaError_t ce = cudaGetLastError();
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
+    if (ce != cudaSuccess) { snn_result_free(r); return cuda_fail(ce, "query"); }
+    *out = r;
+    return SNN_OK;
+}
+
 static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d, snn_dtype dt,
                              double R, void *stream, snn_result *out) {
     if (!out) return fail(SNN_ERR_INVALID_ARGUMENT, "NULL output handle");
@@ -741,6 +883,13 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
         launch_gather(Qdev, f64, m, D, ld, round_up(m, 4), reinterpret_cast<const uint32_t *>(qp), idx->mu_d, qs, nullptr, s);
         Qs = qs; qkeys = qk; qperm = qp; eq = eqd;
         Qd = Qdev;
+    }
+    if (ld == 0 && !f64 && g_opt.lowd_tc && !g_opt.force_generic && tcl_supported(D)) {
+        snn_status r = query_tcl(idx, ws, s, sms, m, R, Qs, qkeys, qperm, eq, self, qflag, out);
+        if (r != SNN_ERR_UNSUPPORTED) {
+            prof_end(qtok, s, (double)m);
+            return r;
+        }   // folded terms outside the FP16 range: FFMA path below
     }
     if (idx->tc) {
         snn_status r = query_tc(idx, ws, s, sms, m, R, Qs, qkeys, qperm, eq, Qd, qflag, out);

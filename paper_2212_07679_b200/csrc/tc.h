@@ -56,3 +56,27 @@ void launch_gather_u32(const uint32_t *src, const uint32_t *idx, int64_t H, uint
 void launch_tc_write(const uint32_t *order, const uint32_t *hj, const float *hd, const int32_t *perm, int64_t H,
                      int32_t *out_idx, float *out_dist, cudaStream_t s);
 }  // namespace snn
+
+namespace snn {
+// Low-d tensor-core filter (tc_lowd.cu): folded split-FP16 operands, K = 3d + 4 (16 / 32).
+struct TclArgs {
+    int64_t n, m;
+    const int64_t *blk_lo, *blk_hi;
+    const int64_t *grp_lo, *grp_start;
+    int64_t nblocks, ngroups, total_items;
+    int group, chunk;
+    int32_t *pair_q, *pair_j;
+    unsigned long long *pair_count;
+    int64_t pair_cap;
+};
+int tcl_kc(int d);              // 16 (d <= 4) or 32 (d <= 8)
+bool tcl_supported(int d);
+int64_t tcl_claim_slack();
+// operand rows from an AoSoA4 fp32 sorted copy; cand: rows_pad x kc, qry: rows x kc (nullable)
+void launch_tcl_operands(const float *Xs, int d, int64_t rows, int64_t rows_pad, const float *mu_f, int e, double c1h,
+                         double r2h, void *cand, void *qry, cudaStream_t s);
+bool launch_tcl_window(const void *qry, const void *cand, int kc, int64_t cand_rows, const TclArgs &a, int sm_count,
+                       cudaStream_t s);
+void launch_tcl_recheck(const float *Xs, const float *Qs, int d, const int32_t *pq, const int32_t *pj, int64_t np,
+                        double R2, uint32_t *flag, float *dist, cudaStream_t s);
+}  // namespace snn

@@ -423,6 +423,48 @@ def test_tc_operand_scaling_extremes(snn, xs, qs):
     compare(run(snn, X, Q, R), oracle.radius_query(X, Q, R))
 
 
+@pytest.mark.parametrize("d", [1, 2, 3, 4, 5, 8])
+def test_lowd_tensor_core_vs_ffma_exact(snn, d):
+    """Low-d radius query through the folded split-FP16 tcgen05 filter (K = 16 / 32) and
+    through the FFMA direct-form kernel: bit-identical CSR, and equal to the oracle."""
+    import paper_2212_07679_b200 as p
+    rng = np.random.default_rng(100 + d)
+    centers = rng.random((16, d)) * 50 + 1000.0           # far from the origin: cancellation
+    X = (centers[rng.integers(0, 16, 12000)] + rng.standard_normal((12000, d))).astype(np.float32)
+    Q = np.concatenate([X[:1500], (X[1500:2500] + rng.standard_normal((1000, d)) * 0.3).astype(np.float32)])
+    R = 0.9
+    ora = oracle.radius_query(X, Q, R)
+    res = {}
+    try:
+        for tc in (1, -1):
+            p.snn_set_option("lowd_tc", tc)
+            res[tc] = (run(snn, X, Q, R), run(snn, X, None, R))
+    finally:
+        p.snn_set_option("lowd_tc", 0)
+    for tc in (1, -1):
+        compare(res[tc][0], ora)
+    a, b = res[1][0], res[-1][0]
+    assert np.array_equal(a.offsets, b.offsets) and np.array_equal(a.indices, b.indices)
+    assert np.array_equal(a.distances, b.distances)
+    a, b = res[1][1], res[-1][1]
+    assert np.array_equal(a.offsets, b.offsets) and np.array_equal(a.indices, b.indices)
+
+
+@pytest.mark.parametrize("tiles,group", [(1, 1), (3, 2), (8, 8), (16, 64)])
+def test_lowd_tensor_core_raster_options(snn, tiles, group):
+    import paper_2212_07679_b200 as p
+    w = workloads.c2(n=30000)
+    R = workloads.load_radii()["c2"]["R"]
+    ora = oracle.radius_query(w.X, w.X[:3000], R)
+    try:
+        p.snn_set_option("lowd_tc_tiles", tiles)
+        p.snn_set_option("lowd_tc_group", group)
+        compare(run(snn, w.X, w.X[:3000], R), ora)
+    finally:
+        p.snn_set_option("lowd_tc_tiles", 0)
+        p.snn_set_option("lowd_tc_group", 0)
+
+
 @pytest.mark.parametrize("nbig", [300, 3000, 20000])
 def test_tc_csr_row_sizes(snn, nbig):
     """Rows of every size class of the CSR row sort (registers <= 32, warp <= 512,
