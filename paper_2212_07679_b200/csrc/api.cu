@@ -710,7 +710,7 @@ static snn_status query_tcl(snn_index idx, Workspace &ws, cudaStream_t s, int sm
     if (G > nblocks) G = nblocks;
     if (G < 1) G = 1;
     const int64_t ngroups = ceil_div(nblocks, G);
-    int64_t *blk_lo, *blk_hi, *nitems, *grp_lo, *grp_items, *grp_start;
+    int64_t *blk_lo, *blk_hi, *nitems, *grp_lo, *grp_items, *grp_start, *bm_words, *bm_off;
     unsigned long long *pcount, *wpairs;
     uint8_t *scan_tmp;
     CK(ws.alloc(&blk_lo, (size_t)nblocks), "alloc");
@@ -719,12 +719,16 @@ static snn_status query_tcl(snn_index idx, Workspace &ws, cudaStream_t s, int sm
     CK(ws.alloc(&grp_lo, (size_t)ngroups), "alloc");
     CK(ws.alloc(&grp_items, (size_t)ngroups), "alloc");
     CK(ws.alloc(&grp_start, (size_t)ngroups + 1), "alloc");
+    CK(ws.alloc(&bm_words, (size_t)nblocks), "alloc");
+    CK(ws.alloc(&bm_off, (size_t)nblocks + 1), "alloc");
     CK(ws.alloc(&pcount, 1), "alloc");
     CK(ws.alloc(&wpairs, 1), "alloc");
-    CK(ws.alloc(&scan_tmp, scan_temp_bytes(ngroups + 1) + 4096), "alloc");
+    CK(ws.alloc(&scan_tmp, scan_temp_bytes((nblocks > m ? nblocks : m) + 1) + 4096), "alloc");
     CK(cudaMemsetAsync(wpairs, 0, 8, s), "memset");
     WindowSpec w;
-    w.qkeys = qkeys; w.m = m; w.B = TM; w.keys = idx->keys; w.n = idx->n; w.n_pad = idx->n_pad;
+    const int64_t n64 = round_up(idx->n, 64);   // 64-aligned windows (bitmap words)
+    w.qkeys = qkeys; w.m = m; w.B = TM; w.keys = idx->keys; w.n = idx->n; w.n_pad = n64;
+    w.align = 64;
     w.R = R;
     w.wnorm = idx->stats + ST_WNORM_F;
     w.ex = idx->stats + ST_EX_F;
@@ -734,8 +738,11 @@ static snn_status query_tcl(snn_index idx, Workspace &ws, cudaStream_t s, int sm
     launch_block_windows(w, s);                                                    // K7
     launch_tc_group_items(blk_lo, blk_hi, nblocks, (int)G, chunk, grp_lo, grp_items, s);
     exclusive_scan_i64(grp_items, grp_start, ngroups, scan_tmp, s);
+    launch_tcl_bm_sizes(blk_lo, blk_hi, nblocks, bm_words, s);
+    exclusive_scan_i64(bm_words, bm_off, nblocks, scan_tmp, s);
     int64_t *hp = static_cast<int64_t *>(t_pinned.p);
     CK(cudaMemcpyAsync(hp, grp_start + ngroups, 8, cudaMemcpyDeviceToHost, s), "D2H items");
+    CK(cudaMemcpyAsync(hp + 4, bm_off + nblocks, 8, cudaMemcpyDeviceToHost, s), "D2H bitmap size");
     CK(cudaMemcpyAsync(hp + 1, qflag, 4, cudaMemcpyDeviceToHost, s), "D2H flag");
     CK(cudaMemcpyAsync(hp + 2, wpairs, 8, cudaMemcpyDeviceToHost, s), "D2H pairs");
     if (!self) CK(cudaMemcpyAsync(hp + 3, eq + 1, 8, cudaMemcpyDeviceToHost, s), "D2H query bound");
@@ -743,6 +750,7 @@ static snn_status query_tcl(snn_index idx, Workspace &ws, cudaStream_t s, int sm
     const int64_t total_items = hp[0];
     if (*reinterpret_cast<int *>(hp + 1)) return fail(SNN_ERR_NONFINITE, "Q contains NaN or Inf");
     const double pairs_eval = (double)*reinterpret_cast<unsigned long long *>(hp + 2);
+    const int64_t bm_total = hp[4];
     const double xb = idx->h_stats[ST_XCMAX];
     const double qb = self ? xb : *reinterpret_cast<double *>(hp + 3);
     const double bound = xb > qb ? xb : qb;
@@ -771,50 +779,67 @@ static snn_status query_tcl(snn_index idx, Workspace &ws, cudaStream_t s, int sm
     if (hmax * s2 >= 60000.0 || (hmax + r2h) * s2 >= 60000.0) return SNN_ERR_UNSUPPORTED;
 
     uint16_t *cand = nullptr, *qry = nullptr;
-    CK(ws.alloc(&cand, (size_t)idx->n_pad * kc), "alloc");
+    CK(ws.alloc(&cand, (size_t)n64 * kc), "alloc");
     CK(ws.alloc(&qry, (size_t)m * kc), "alloc");
     const float *Xs = static_cast<const float *>(idx->Xs), *Qf = static_cast<const float *>(Qs);
     if (self) {
-        launch_tcl_operands(Xs, D, idx->n, idx->n_pad, idx->mu_f, e, c1h, r2h, cand, qry, s);
+        launch_tcl_operands(Xs, D, idx->n, n64, idx->mu_f, e, c1h, r2h, cand, qry, s);
     } else {
-        launch_tcl_operands(Xs, D, idx->n, idx->n_pad, idx->mu_f, e, c1h, r2h, cand, nullptr, s);
+        launch_tcl_operands(Xs, D, idx->n, n64, idx->mu_f, e, c1h, r2h, cand, nullptr, s);
         launch_tcl_operands(Qf, D, m, m, idx->mu_f, e, c1h, r2h, nullptr, qry, s);
     }
+    unsigned long long *bitmap = nullptr;
+    CK(ws.alloc(&bitmap, (size_t)(bm_total > 0 ? bm_total : 1)), "alloc bitmap");
+    CK(cudaMemsetAsync(bitmap, 0, (size_t)(bm_total > 0 ? bm_total : 1) * 8, s), "memset");
     TclArgs t{};
     t.n = idx->n; t.m = m;
     t.blk_lo = blk_lo; t.blk_hi = blk_hi; t.grp_lo = grp_lo; t.grp_start = grp_start;
     t.nblocks = nblocks; t.ngroups = ngroups; t.total_items = total_items; t.group = (int)G; t.chunk = chunk;
-    int64_t cap = (int64_t)64 * m;
-    if (cap < (int64_t(1) << 22)) cap = int64_t(1) << 22;
-    int32_t *pq = nullptr, *pj = nullptr;
-    for (int attempt = 0; attempt < 2; ++attempt) {
-        CK(ws.alloc(&pq, (size_t)cap), "alloc pairs");
-        CK(ws.alloc(&pj, (size_t)cap), "alloc pairs");
-        t.pair_q = pq; t.pair_j = pj; t.pair_count = pcount; t.pair_cap = cap;
-        CK(cudaMemsetAsync(pcount, 0, 8, s), "memset");
-        const int ctok = prof_begin(F_COUNT, s);
-        if (!launch_tcl_window(qry, cand, kc, idx->n_pad, t, sms, s)) return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-        prof_end(ctok, s, pairs_eval);
-        CK(cudaMemcpyAsync(hp, pcount, 8, cudaMemcpyDeviceToHost, s), "D2H pair count");
-        CK(cudaStreamSynchronize(s), "tc filter");
-        const int64_t np = (int64_t)*reinterpret_cast<unsigned long long *>(hp);
-        if (np <= cap) { cap = np; break; }
-        cap = np + (int64_t)sms * tcl_claim_slack();
-    }
-    const int64_t P = cap;
+    t.bitmap = bitmap; t.bm_off = bm_off;
+    const int ctok = prof_begin(F_COUNT, s);
+    if (!launch_tcl_window(qry, cand, kc, n64, t, sms, s)) return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    prof_end(ctok, s, pairs_eval);
+
+    // exact decision of the flagged chunks, then the CSR in key order (no sort)
     const int wtok = prof_begin(F_WRITE, s);
-    uint32_t *flag;
-    float *dist;
-    CK(ws.alloc(&flag, (size_t)P), "alloc");
-    CK(ws.alloc(&dist, (size_t)P), "alloc");
-    launch_tcl_recheck(Xs, Qf, D, pq, pj, P, R * R, flag, dist, s);                // K10
-    snn_result r = nullptr;
-    snn_status st = pairs_to_csr(ws, s, m, P, pq, pj, flag, dist, qperm, idx->perm, &r);   // K11
-    if (st != SNN_OK) return st;
-    prof_end(wtok, s, (double)r->nnz);
-    g_last_ovf = P - r->nnz;
+    TclPost pp{};
+    pp.n = idx->n; pp.m = m; pp.Xs = Xs; pp.Qs = Qf; pp.perm = idx->perm; pp.qperm = qperm;
+    pp.blk_lo = blk_lo; pp.blk_hi = blk_hi; pp.bm_off = bm_off; pp.bitmap = bitmap;
+    thresholds(R * R, D, &pp.T_in, &pp.T_out);
+    pp.R2 = R * R;
+    int64_t *fcnt, *foff;
+    int32_t *row_count;
+    CK(ws.alloc(&fcnt, (size_t)m), "alloc");
+    CK(ws.alloc(&foff, (size_t)m + 1), "alloc");
+    CK(ws.alloc(&row_count, (size_t)m), "alloc");
+    launch_tcl_flag_count(pp, fcnt, s);
+    exclusive_scan_i64(fcnt, foff, m, scan_tmp, s);
+    CK(cudaMemcpyAsync(hp, foff + m, 8, cudaMemcpyDeviceToHost, s), "D2H flagged");
+    CK(cudaStreamSynchronize(s), "tc filter");
+    const int64_t F = hp[0];
+    uint32_t *masks;
+    CK(ws.alloc(&masks, (size_t)(F > 0 ? F : 1)), "alloc");
+    launch_tcl_exact(pp, D, foff, masks, row_count, s);                           // exact decision
+    snn_result r = new snn_result_s();
+    r->m = m;
+    void *pm = nullptr;
+    cudaError_t ce = cudaMallocAsync(&pm, (size_t)(m + 1) * 8, s);
+    if (ce != cudaSuccess) { delete r; return cuda_fail(ce, "alloc offsets"); }
+    r->offsets = static_cast<int64_t *>(pm);
+    exclusive_scan_i32_to_i64(row_count, r->offsets, m, scan_tmp, s);
+    CK(cudaMemcpyAsync(hp, r->offsets + m, 8, cudaMemcpyDeviceToHost, s), "D2H nnz");
+    if ((ce = cudaStreamSynchronize(s)) != cudaSuccess) { snn_result_free(r); return cuda_fail(ce, "exact"); }
+    const int64_t H = hp[0];
+    r->nnz = H;
+    if ((ce = cudaMallocAsync(&pm, (size_t)(H > 0 ? H : 1) * 4, s)) != cudaSuccess) { snn_result_free(r); return cuda_fail(ce, "alloc"); }
+    r->indices = static_cast<int32_t *>(pm);
+    if ((ce = cudaMallocAsync(&pm, (size_t)(H > 0 ? H : 1) * 4, s)) != cudaSuccess) { snn_result_free(r); return cuda_fail(ce, "alloc"); }
+    r->distances = static_cast<float *>(pm);
+    launch_tcl_write(pp, D, foff, masks, r->offsets, r->indices, r->distances, s);   // K11
+    prof_end(wtok, s, (double)H);
+    g_last_ovf = F;   // flagged 32-candidate chunks
     g_last_lost = 0;
-    cudaError_t ce = cudaGetLastError();
+    ce = cudaGetLastError();
     if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
     if (ce != cudaSuccess) { snn_result_free(r); return cuda_fail(ce, "query"); }
     *out = r;

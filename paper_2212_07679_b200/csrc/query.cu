@@ -61,8 +61,9 @@ __global__ void block_windows(WindowSpec w) {
     const float hi_key = __fadd_ru(w.qkeys[s1], rpf);
     int64_t lo = lower_bound_f(w.keys, w.n, lo_key);
     int64_t hi = upper_bound_f(w.keys, w.n, hi_key);
-    lo &= ~(int64_t)3;                               // 16-byte aligned bulk copies
-    hi = min(round_up(hi, 4), w.n_pad);
+    const int64_t al = w.align > 4 ? w.align : 4;   // >= 4: 16-byte aligned bulk copies
+    lo -= lo % al;
+    hi = min(round_up(hi, al), w.n_pad);
     w.blk_lo[b] = lo;
     w.blk_hi[b] = hi;
     w.nitems[b] = hi > lo ? ceil_div(hi - lo, w.chunk) : 0;

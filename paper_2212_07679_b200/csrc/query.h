@@ -24,6 +24,7 @@ struct WindowSpec {
     const double *ex;       // device scalar E_x (index key error bound)
     const double *eq;       // device scalar E_q (query key error bound)
     int chunk;              // candidates per work item (multiple of 4)
+    int align = 4;          // window bounds rounded out to multiples of this (>= 4)
     int64_t *blk_lo, *blk_hi, *nitems;   // outputs, nblocks each
     unsigned long long *pairs;           // += sum over blocks of |window| x queries (zeroed)
 };

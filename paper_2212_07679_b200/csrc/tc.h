@@ -58,25 +58,39 @@ void launch_tc_write(const uint32_t *order, const uint32_t *hj, const float *hd,
 }  // namespace snn
 
 namespace snn {
-// Low-d tensor-core filter (tc_lowd.cu): folded split-FP16 operands, K = 3d + 4 (16 / 32).
+// Low-d tensor-core filter (tc_lowd.cu): folded split-FP16 operands, K = 3d + 4 (16 / 32),
+// output = candidate bitmap (one bit per query x 32-candidate chunk of its window).
 struct TclArgs {
     int64_t n, m;
-    const int64_t *blk_lo, *blk_hi;
+    const int64_t *blk_lo, *blk_hi;     // 64-aligned windows of 128-query blocks
     const int64_t *grp_lo, *grp_start;
     int64_t nblocks, ngroups, total_items;
     int group, chunk;
-    int32_t *pair_q, *pair_j;
-    unsigned long long *pair_count;
-    int64_t pair_cap;
+    unsigned long long *bitmap;         // zeroed; block b's rows start at bm_off[b]
+    const int64_t *bm_off;
+};
+// exact decision + CSR write over the bitmap
+struct TclPost {
+    int64_t n, m;
+    const float *Xs, *Qs;               // AoSoA4 sorted copies (index / queries)
+    const int32_t *perm, *qperm;
+    const int64_t *blk_lo, *blk_hi, *bm_off;
+    const unsigned long long *bitmap;
+    float T_in, T_out;                  // fp32 sure-in / sure-out thresholds (FFMA path's)
+    double R2;
 };
 int tcl_kc(int d);              // 16 (d <= 4) or 32 (d <= 8)
 bool tcl_supported(int d);
-int64_t tcl_claim_slack();
 // operand rows from an AoSoA4 fp32 sorted copy; cand: rows_pad x kc, qry: rows x kc (nullable)
 void launch_tcl_operands(const float *Xs, int d, int64_t rows, int64_t rows_pad, const float *mu_f, int e, double c1h,
                          double r2h, void *cand, void *qry, cudaStream_t s);
 bool launch_tcl_window(const void *qry, const void *cand, int kc, int64_t cand_rows, const TclArgs &a, int sm_count,
                        cudaStream_t s);
-void launch_tcl_recheck(const float *Xs, const float *Qs, int d, const int32_t *pq, const int32_t *pj, int64_t np,
-                        double R2, uint32_t *flag, float *dist, cudaStream_t s);
+void launch_tcl_bm_sizes(const int64_t *blk_lo, const int64_t *blk_hi, int64_t nblocks, int64_t *words,
+                         cudaStream_t s);
+void launch_tcl_flag_count(const TclPost &p, int64_t *fcnt, cudaStream_t s);
+void launch_tcl_exact(const TclPost &p, int d, const int64_t *foff, uint32_t *masks, int32_t *row_count,
+                      cudaStream_t s);
+void launch_tcl_write(const TclPost &p, int d, const int64_t *foff, const uint32_t *masks, const int64_t *offsets,
+                      int32_t *out_idx, float *out_dist, cudaStream_t s);
 }  // namespace snn

@@ -11,12 +11,17 @@
 // where v = x * 2^e = h + l is split into two FP16 halves (22 significant bits; the
 // dropped l.l term is ~2^-22 |x||q|), xbar' = xbar c1h 2^(2e-15) and
 // b' = -(qbar c1h - r2h) 2^(2e-15), also split.  A_i . B_j = 2^(2e) * (left side), so the
-// epilogue only tests the sign of the accumulator: a 3-way max tree over 32 columns and
-// one compare, with the rare candidate lanes emitting (query, index) pairs.  The pair
-// list is then decided exactly by the oracle's fp64 sequence (tcl_recheck) -- the filter
-// only has to be conservative, which the margin guarantees (derivation in api.cu and
-// DESIGN.md; the FFMA direct-form kernel stays the fallback whenever the scaled terms do
-// not fit FP16).
+// epilogue only tests the sign of the accumulator: a 3-way max tree over each run of 32
+// candidates and one compare.  The result is a BITMAP with one bit per (query, aligned
+// 32-candidate chunk of its window) that may hold a neighbour -- no per-element
+// extraction in the epilogue, no divergence.  The flagged chunks are then decided
+// exactly (tcl_exact: the FFMA kernel's fp32 direct-form classification with fp64
+// fallback, i.e. bit-identical membership with the oracle), and the CSR is written in
+// key order straight from the bitmap (tcl_write) -- no sort.  The filter only has to be
+// conservative, which the margin guarantees (derivation in api.cu and DESIGN.md; the
+// FFMA direct-form kernel stays the fallback whenever the scaled terms do not fit FP16).
+// Windows are aligned to 64 candidates so every epilogue thread's two 32-candidate
+// chunks of a tile share one 64-bit bitmap word (one atomic OR).
 //
 // The batched contraction X(J,:) [q_1 .. q_128] of PAPER.md:218-219 is one
 // tcgen05.mma (M = 128 queries, N = 256 candidates, K = 16 or 32) per tile: the query
@@ -35,15 +40,13 @@ namespace {
 using namespace tc5;
 
 constexpr int TM = 128, TN = 256, LSTAGES = 8;
-constexpr int STAGE_CAP = 8;
-constexpr unsigned long long CLAIM = 256;
 constexpr int EPI = 512;
 constexpr int COLS = TN / (EPI / 128);
 constexpr int THREADS = 64 + EPI;
 
 template <int KC> constexpr int row_bytes() { return KC * 2; }
 template <int KC> constexpr int smem_bytes() {
-    return 1024 + LSTAGES * TN * row_bytes<KC>() + 2 * TM * row_bytes<KC>() + EPI * STAGE_CAP * 4 + 512;
+    return 1024 + LSTAGES * TN * row_bytes<KC>() + 2 * TM * row_bytes<KC>() + 512;
 }
 // UMMA K-major descriptor for 32-byte (KC = 16) or 64-byte (KC = 32) swizzled rows:
 // 8-row core groups SBO = 8 * row bytes apart; layout type 6 = SWIZZLE_32B, 4 = SWIZZLE_64B.
@@ -84,10 +87,9 @@ tcl_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
     uint8_t *gbase = smem_raw + (base - raw);
-    // carve: B ring | A slots [2] | staged hits | barriers | tmem ptr
+    // carve: B ring | A slots [2] | barriers | tmem ptr
     const uint32_t a_base = base + LSTAGES * B_BYTES;
-    int32_t *s_hits = reinterpret_cast<int32_t *>(gbase + LSTAGES * B_BYTES + 2 * A_BYTES);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(gbase + LSTAGES * B_BYTES + 2 * A_BYTES + EPI * STAGE_CAP * 4);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(gbase + LSTAGES * B_BYTES + 2 * A_BYTES);
     uint64_t *full = bars, *empty = bars + LSTAGES, *tfull = bars + 2 * LSTAGES, *tempty = bars + 2 * LSTAGES + 2;
     uint64_t *afull = bars + 2 * LSTAGES + 4, *aempty = bars + 2 * LSTAGES + 6;
     uint32_t *tmem_ptr = reinterpret_cast<uint32_t *>(bars + 2 * LSTAGES + 8);
@@ -166,25 +168,28 @@ tcl_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
         }
     } else {
         // ------------------------------------------------------------ epilogue (EPI threads)
+        // 16 warps: warp w reads TMEM lane quarter (w % 4); the four warps of a quarter
+        // take 64-column slices of the 256-column tile.  One thread = one query row.
         const int et = threadIdx.x - 64;
         const int quarter = warp & 3;
         const int slice = et >> 7;
         const int row = quarter * 32 + lane;
-        int32_t *my_hits = s_hits + et * STAGE_CAP;
         uint32_t acc = 0, aphase = 0;
-        unsigned long long wcur = 0, wend = 0;
         for (int64_t item = blockIdx.x; item < a.total_items; item += gridDim.x) {
             int64_t b, c0, c1;
             tcl_locate(a, item, b, c0, c1);
             if (c1 <= c0) continue;
             const int64_t sp = b * TM + row;
             const bool active = sp < a.m;
+            const int64_t lo = a.blk_lo[b];
+            const int64_t wpr = ceil_div(a.blk_hi[b] - lo, 64 * 32);   // bitmap words per row
+            unsigned long long *bm = a.bitmap + a.bm_off[b] + (int64_t)row * wpr;
             for (int64_t t0 = c0; t0 < c1; t0 += TN) {
                 mbar_wait_u32(smem_u32(&tfull[acc]), aphase);
                 tc_fence_after();
-                int nh = 0;
                 const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + acc * TN + slice * COLS;
-#pragma unroll 1
+                uint32_t flags = 0;
+#pragma unroll
                 for (int ch = 0; ch < COLS / 32; ++ch) {
                     float v[32];
                     tmem_ld32(taddr + ch * 32, v);
@@ -195,63 +200,20 @@ tcl_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
                     const float m0 = fmaxf(fmaxf(m[0], m[1]), m[2]), m1 = fmaxf(fmaxf(m[3], m[4]), m[5]);
                     const float m2 = fmaxf(fmaxf(m[6], m[7]), m[8]), m3 = fmaxf(m[9], m[10]);
                     const float mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
-                    if (mx >= 0.f && active) {
-                        uint32_t mask = 0;
-#pragma unroll
-                        for (int c = 0; c < 32; ++c) mask |= (v[c] >= 0.f ? 1u : 0u) << c;
-                        const int64_t jb = t0 + slice * COLS + ch * 32;
-                        while (mask) {
-                            const int c = __ffs(mask) - 1;
-                            mask &= mask - 1;
-                            const int64_t jj = jb + c;
-                            if (jj >= c1) break;
-                            if (nh < STAGE_CAP) {
-                                my_hits[nh++] = (int32_t)jj;
-                            } else {
-                                const unsigned long long k = atomicAdd(a.pair_count, 1ull);
-                                if (k < (unsigned long long)a.pair_cap) {
-                                    a.pair_q[k] = (int32_t)sp;
-                                    a.pair_j[k] = (int32_t)jj;
-                                }
-                            }
-                        }
-                    }
+                    flags |= (mx >= 0.f ? 1u : 0u) << ch;
                 }
                 tc_fence_before();
                 mbar_arrive(smem_u32(&tempty[acc]));
-                if (__any_sync(0xffffffffu, nh > 0)) {
-                    int incl = nh;
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-                        if (lane >= o) incl += y;
-                    }
-                    const int total = __shfl_sync(0xffffffffu, incl, 31);
-                    if (wcur + (unsigned long long)total > wend) {
-                        for (unsigned long long k = wcur + lane; k < wend; k += 32)
-                            if (k < (unsigned long long)a.pair_cap) a.pair_q[k] = -1;
-                        const unsigned long long want = total > CLAIM ? (unsigned long long)total : CLAIM;
-                        unsigned long long wb = 0;
-                        if (lane == 0) wb = atomicAdd(a.pair_count, want);
-                        wcur = __shfl_sync(0xffffffffu, wb, 0);
-                        wend = wcur + want;
-                    }
-                    const unsigned long long my0 = wcur + (unsigned long long)(incl - nh);
-                    for (int h = 0; h < nh; ++h) {
-                        const unsigned long long k = my0 + h;
-                        if (k < (unsigned long long)a.pair_cap) {
-                            a.pair_q[k] = (int32_t)sp;
-                            a.pair_j[k] = my_hits[h];
-                        }
-                    }
-                    wcur += (unsigned long long)total;
+                const int64_t jb = t0 + slice * COLS;
+                if (flags && active && jb < c1) {
+                    if (jb + 32 >= c1) flags &= 1u;   // second chunk beyond this item's range
+                    const int64_t pos = (jb - lo) >> 5;             // even: windows are 64-aligned
+                    atomicOr(bm + (pos >> 6), (unsigned long long)flags << (pos & 63));
                 }
                 acc ^= 1;
                 if (acc == 0) aphase ^= 1;
             }
         }
-        for (unsigned long long k = wcur + lane; k < wend; k += 32)
-            if (k < (unsigned long long)a.pair_cap) a.pair_q[k] = -1;
     }
     tc_fence_before();
     __syncthreads();
@@ -322,24 +284,126 @@ __global__ void __launch_bounds__(256) tcl_operands(const float *__restrict__ Xs
     }
 }
 
-// exact recheck (oracle sequence, eq:ip1 in fp64) of pairs on the AoSoA4 copies
+// bitmap words per block (128 rows x ceil(chunks / 64))
+__global__ void tcl_bm_sizes_kernel(const int64_t *blk_lo, const int64_t *blk_hi, int64_t nblocks, int64_t *words) {
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b < nblocks) words[b] = TM * ceil_div(max((int64_t)0, blk_hi[b] - blk_lo[b]), 64 * 32);
+}
+
+// flagged chunks per query (sorted position): popcount of its bitmap row
+__global__ void tcl_flag_count_kernel(const TclPost p, int64_t *fcnt) {
+    for (int64_t sp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; sp < p.m;
+         sp += (int64_t)gridDim.x * blockDim.x / 32) {
+        const int lane = threadIdx.x % 32;
+        const int64_t b = sp / TM, row = sp % TM;
+        const int64_t wpr = ceil_div(max((int64_t)0, p.blk_hi[b] - p.blk_lo[b]), 64 * 32);
+        const unsigned long long *bm = p.bitmap + p.bm_off[b] + row * wpr;
+        int64_t c = 0;
+        for (int64_t w = lane; w < wpr; w += 32) c += __popcll(bm[w]);
+        c = warp_sum(c);
+        if (lane == 0) fcnt[sp] = c;
+    }
+}
+
+// Exact decision of every flagged chunk (one warp per query, lane = candidate): the FFMA
+// kernel's classification -- fp32 direct form (eq:ip1) on the original coordinates against
+// the rigorous T_in / T_out, oracle-order fp64 sequence in between -- so membership is
+// bit-identical to the oracle.  masks[foff[sp] + k] = hit mask of the k-th flagged chunk;
+// row_count[qperm[sp]] = hits.
 template <int D>
-__global__ void __launch_bounds__(256) tcl_recheck(const float *__restrict__ Xs, const float *__restrict__ Qs,
-                                                   const int32_t *__restrict__ pq, const int32_t *__restrict__ pj,
-                                                   int64_t npairs, double R2, uint32_t *flag, float *dist) {
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < npairs; k += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t q = pq[k];
-        if (q < 0) { flag[k] = 0; dist[k] = 0.f; continue; }
-        const int32_t j = pj[k];
-        double s = 0.0;
+__global__ void __launch_bounds__(256) tcl_exact_kernel(const TclPost p, const int64_t *foff, uint32_t *masks,
+                                                        int32_t *row_count) {
+    const int lane = threadIdx.x % 32;
+    for (int64_t sp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; sp < p.m;
+         sp += (int64_t)gridDim.x * blockDim.x / 32) {
+        const int64_t b = sp / TM, row = sp % TM;
+        const int64_t lo = p.blk_lo[b];
+        const int64_t wpr = ceil_div(max((int64_t)0, p.blk_hi[b] - lo), 64 * 32);
+        const unsigned long long *bm = p.bitmap + p.bm_off[b] + row * wpr;
+        float q[D];
+        double qd[D];
 #pragma unroll
-        for (int kk = 0; kk < D; ++kk) {
-            const double t = __dsub_rn((double)Xs[(j >> 2) * 4 * D + 4 * kk + (j & 3)],
-                                       (double)Qs[(q >> 2) * 4 * D + 4 * kk + (q & 3)]);
-            s = __dadd_rn(s, __dmul_rn(t, t));
+        for (int k = 0; k < D; ++k) { q[k] = p.Qs[(sp >> 2) * 4 * D + 4 * k + (sp & 3)]; qd[k] = q[k]; }
+        int64_t out = foff[sp];
+        int32_t hits = 0;
+        for (int64_t w = 0; w < wpr; ++w) {
+            unsigned long long bits = bm[w];
+            while (bits) {
+                const int c = __ffsll(bits) - 1;
+                bits &= bits - 1;
+                const int64_t j = lo + ((w * 64 + c) << 5) + lane;
+                bool hit = false;
+                if (j < p.n) {
+                    float x[D];
+                    float d2 = 0.f;
+#pragma unroll
+                    for (int k = 0; k < D; ++k) {
+                        x[k] = p.Xs[(j >> 2) * 4 * D + 4 * k + (j & 3)];
+                        const float t = x[k] - q[k];
+                        d2 = fmaf(t, t, d2);
+                    }
+                    if (d2 <= p.T_out) {
+                        hit = d2 <= p.T_in;
+                        if (!hit) {
+                            double s = 0.0;
+#pragma unroll
+                            for (int k = 0; k < D; ++k) {
+                                const double t = __dsub_rn((double)x[k], qd[k]);
+                                s = __dadd_rn(s, __dmul_rn(t, t));
+                            }
+                            hit = s <= p.R2;
+                        }
+                    }
+                }
+                const uint32_t msk = __ballot_sync(0xffffffffu, hit);
+                if (lane == 0) masks[out] = msk;
+                ++out;
+                hits += __popc(msk);
+            }
         }
-        flag[k] = s <= R2;
-        dist[k] = (float)sqrt(s);
+        if (lane == 0) row_count[p.qperm[sp]] = hits;
+    }
+}
+
+// CSR write in key order: for each flagged chunk (bitmap order = ascending candidate
+// position) its hits, ids via pi, distance = (float)sqrt of the oracle-order fp64 sum.
+template <int D>
+__global__ void __launch_bounds__(256) tcl_write_kernel(const TclPost p, const int64_t *foff, const uint32_t *masks,
+                                                        const int64_t *offsets, int32_t *out_idx, float *out_dist) {
+    const int lane = threadIdx.x % 32;
+    for (int64_t sp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; sp < p.m;
+         sp += (int64_t)gridDim.x * blockDim.x / 32) {
+        const int64_t b = sp / TM, row = sp % TM;
+        const int64_t lo = p.blk_lo[b];
+        const int64_t wpr = ceil_div(max((int64_t)0, p.blk_hi[b] - lo), 64 * 32);
+        const unsigned long long *bm = p.bitmap + p.bm_off[b] + row * wpr;
+        double qd[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) qd[k] = p.Qs[(sp >> 2) * 4 * D + 4 * k + (sp & 3)];
+        int64_t k = foff[sp];
+        int64_t pos = offsets[p.qperm[sp]];
+        for (int64_t w = 0; w < wpr; ++w) {
+            unsigned long long bits = bm[w];
+            while (bits) {
+                const int c = __ffsll(bits) - 1;
+                bits &= bits - 1;
+                const uint32_t msk = masks[k++];
+                if (!msk) continue;
+                if (msk & (1u << lane)) {
+                    const int64_t j = lo + ((w * 64 + c) << 5) + lane;
+                    double s = 0.0;
+#pragma unroll
+                    for (int kk = 0; kk < D; ++kk) {
+                        const double t = __dsub_rn((double)p.Xs[(j >> 2) * 4 * D + 4 * kk + (j & 3)], qd[kk]);
+                        s = __dadd_rn(s, __dmul_rn(t, t));
+                    }
+                    const int64_t o = pos + __popc(msk & lanemask_lt());
+                    out_idx[o] = p.perm[j];
+                    out_dist[o] = (float)sqrt(s);
+                }
+                pos += __popc(msk);
+            }
+        }
     }
 }
 
@@ -364,7 +428,6 @@ int gridn(int64_t n) {
 
 int tcl_kc(int d) { return 3 * d + 4 <= 16 ? 16 : 32; }
 bool tcl_supported(int d) { return d >= 1 && 3 * d + 4 <= 32; }
-int64_t tcl_claim_slack() { return (int64_t)(EPI / 32) * (int64_t)CLAIM; }
 
 void launch_tcl_operands(const float *Xs, int d, int64_t rows, int64_t rows_pad, const float *mu_f, int e, double c1h,
                          double r2h, void *cand, void *qry, cudaStream_t s) {
@@ -397,11 +460,31 @@ bool launch_tcl_window(const void *qry, const void *cand, int kc, int64_t cand_r
     return true;
 }
 
-void launch_tcl_recheck(const float *Xs, const float *Qs, int d, const int32_t *pq, const int32_t *pj, int64_t np,
-                        double R2, uint32_t *flag, float *dist, cudaStream_t s) {
-    if (np == 0) return;
-    const int g = gridn(np);
-#define CASE(D) case D: SNN_LAUNCH(tcl_recheck<D>, g, 256, 0, s, Xs, Qs, pq, pj, np, R2, flag, dist); break;
+void launch_tcl_bm_sizes(const int64_t *blk_lo, const int64_t *blk_hi, int64_t nblocks, int64_t *words,
+                         cudaStream_t s) {
+    if (nblocks == 0) return;
+    SNN_LAUNCH(tcl_bm_sizes_kernel, (int)ceil_div(nblocks, 256), 256, 0, s, blk_lo, blk_hi, nblocks, words);
+}
+
+void launch_tcl_flag_count(const TclPost &p, int64_t *fcnt, cudaStream_t s) {
+    if (p.m == 0) return;
+    SNN_LAUNCH(tcl_flag_count_kernel, gridn(p.m * 32), 256, 0, s, p, fcnt);
+}
+
+void launch_tcl_exact(const TclPost &p, int d, const int64_t *foff, uint32_t *masks, int32_t *row_count,
+                      cudaStream_t s) {
+    if (p.m == 0) return;
+    const int g = gridn(p.m * 32);
+#define CASE(D) case D: SNN_LAUNCH(tcl_exact_kernel<D>, g, 256, 0, s, p, foff, masks, row_count); break;
+    switch (d) { CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) default: break; }
+#undef CASE
+}
+
+void launch_tcl_write(const TclPost &p, int d, const int64_t *foff, const uint32_t *masks, const int64_t *offsets,
+                      int32_t *out_idx, float *out_dist, cudaStream_t s) {
+    if (p.m == 0) return;
+    const int g = gridn(p.m * 32);
+#define CASE(D) case D: SNN_LAUNCH(tcl_write_kernel<D>, g, 256, 0, s, p, foff, masks, offsets, out_idx, out_dist); break;
     switch (d) { CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) default: break; }
 #undef CASE
 }
