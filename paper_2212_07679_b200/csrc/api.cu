@@ -38,7 +38,7 @@ struct Options {
     int tc_f16 = 1;      // tensor-core operands FP16 (scaled) instead of TF32
     int tc_group = 32;   // query blocks per raster group (upper bound; L2 budget decides)
     int tc_gram_min_d = 128;   // Gram matrix on the tensor cores for d >= this
-    int lowd_tc = 1;     // low-d (fp32, d <= 8) radius queries through the tensor-core filter
+    int lowd_tc = 0;     // low-d (fp32, d <= 8) radius queries through the tensor-core filter (option; FFMA default)
     int lowd_tc_tiles = 8;     // 256-candidate tiles per work item (low-d tensor-core path)
     int lowd_tc_group = 8;     // query blocks per raster group (low-d tensor-core path)
 };
@@ -277,7 +277,7 @@ snn_status snn_set_option(const char *key, int64_t value) {
         g_opt.tc_gram_min_d = (int)value;
         return SNN_OK;
     }
-    if (k == "lowd_tc") { g_opt.lowd_tc = value < 0 ? 0 : 1; return SNN_OK; }
+    if (k == "lowd_tc") { g_opt.lowd_tc = value > 0 ? 1 : 0; return SNN_OK; }   // 0: default (off)
     if (k == "lowd_tc_tiles") {
         if (value == 0) value = 8;
         if (value < 1 || value > 64) return fail(SNN_ERR_INVALID_ARGUMENT, "lowd_tc_tiles must be 1..64");
@@ -696,37 +696,33 @@ static snn_status query_tc(snn_index idx, Workspace &ws, cudaStream_t s, int sms
 }
 
 // Low-d tensor-core query path (fp32 data, d <= 8, AoSoA4 copies): K7 windows (128-query
-// blocks, grouped raster) -> folded split-FP16 tcgen05 filter (tc_lowd.cu) -> exact fp64
-// recheck -> K11.  Returns SNN_ERR_UNSUPPORTED (no message) when the folded terms do not
-// fit FP16 (huge R relative to the data) -- the FFMA path is used then.
+// blocks, 64-aligned), grouped raster work list -> tcgen05 split-FP16 filter fused with
+// the exact decision (tc_lowd.cu) -> per-row totals -> CSR compaction in key order.
+// Returns SNN_ERR_UNSUPPORTED (no message) when the folded terms do not fit FP16 (huge R
+// relative to the data) -- the FFMA path is used then.
 static snn_status query_tcl(snn_index idx, Workspace &ws, cudaStream_t s, int sms, int64_t m, double R,
                             const void *Qs, const float *qkeys, const int32_t *qperm, const double *eq, bool self,
                             const int *qflag, snn_result *out) {
     const int D = idx->d;
     const int TM = 128, TN = 256, kc = tcl_kc(D);
-    const int chunk = TN * g_opt.lowd_tc_tiles;
+    const int chunk = TN * (g_opt.lowd_tc_tiles < 8 ? g_opt.lowd_tc_tiles : 8);   // <= 64 chunks of 32 per item
     const int64_t nblocks = ceil_div(m, TM);
     int64_t G = g_opt.lowd_tc_group;
     if (G > nblocks) G = nblocks;
     if (G < 1) G = 1;
-    const int64_t ngroups = ceil_div(nblocks, G);
-    int64_t *blk_lo, *blk_hi, *nitems, *grp_lo, *grp_items, *grp_start, *bm_words, *bm_off;
-    unsigned long long *pcount, *wpairs;
+    int64_t *blk_lo, *blk_hi, *nitems, *bcount, *bstart;
+    unsigned long long *wpairs;
     uint8_t *scan_tmp;
     CK(ws.alloc(&blk_lo, (size_t)nblocks), "alloc");
     CK(ws.alloc(&blk_hi, (size_t)nblocks), "alloc");
     CK(ws.alloc(&nitems, (size_t)nblocks), "alloc");
-    CK(ws.alloc(&grp_lo, (size_t)ngroups), "alloc");
-    CK(ws.alloc(&grp_items, (size_t)ngroups), "alloc");
-    CK(ws.alloc(&grp_start, (size_t)ngroups + 1), "alloc");
-    CK(ws.alloc(&bm_words, (size_t)nblocks), "alloc");
-    CK(ws.alloc(&bm_off, (size_t)nblocks + 1), "alloc");
-    CK(ws.alloc(&pcount, 1), "alloc");
+    CK(ws.alloc(&bcount, (size_t)nblocks), "alloc");
+    CK(ws.alloc(&bstart, (size_t)nblocks + 1), "alloc");
     CK(ws.alloc(&wpairs, 1), "alloc");
     CK(ws.alloc(&scan_tmp, scan_temp_bytes((nblocks > m ? nblocks : m) + 1) + 4096), "alloc");
     CK(cudaMemsetAsync(wpairs, 0, 8, s), "memset");
     WindowSpec w;
-    const int64_t n64 = round_up(idx->n, 64);   // 64-aligned windows (bitmap words)
+    const int64_t n64 = round_up(idx->n, 64);   // 64-aligned windows
     w.qkeys = qkeys; w.m = m; w.B = TM; w.keys = idx->keys; w.n = idx->n; w.n_pad = n64;
     w.align = 64;
     w.R = R;
@@ -736,13 +732,10 @@ static snn_status query_tcl(snn_index idx, Workspace &ws, cudaStream_t s, int sm
     w.chunk = chunk;
     w.blk_lo = blk_lo; w.blk_hi = blk_hi; w.nitems = nitems; w.pairs = wpairs;
     launch_block_windows(w, s);                                                    // K7
-    launch_tc_group_items(blk_lo, blk_hi, nblocks, (int)G, chunk, grp_lo, grp_items, s);
-    exclusive_scan_i64(grp_items, grp_start, ngroups, scan_tmp, s);
-    launch_tcl_bm_sizes(blk_lo, blk_hi, nblocks, bm_words, s);
-    exclusive_scan_i64(bm_words, bm_off, nblocks, scan_tmp, s);
+    launch_tcl_items(blk_lo, blk_hi, nblocks, (int)G, chunk, bcount, s);
+    exclusive_scan_i64(bcount, bstart, nblocks, scan_tmp, s);
     int64_t *hp = static_cast<int64_t *>(t_pinned.p);
-    CK(cudaMemcpyAsync(hp, grp_start + ngroups, 8, cudaMemcpyDeviceToHost, s), "D2H items");
-    CK(cudaMemcpyAsync(hp + 4, bm_off + nblocks, 8, cudaMemcpyDeviceToHost, s), "D2H bitmap size");
+    CK(cudaMemcpyAsync(hp, bstart + nblocks, 8, cudaMemcpyDeviceToHost, s), "D2H items");
     CK(cudaMemcpyAsync(hp + 1, qflag, 4, cudaMemcpyDeviceToHost, s), "D2H flag");
     CK(cudaMemcpyAsync(hp + 2, wpairs, 8, cudaMemcpyDeviceToHost, s), "D2H pairs");
     if (!self) CK(cudaMemcpyAsync(hp + 3, eq + 1, 8, cudaMemcpyDeviceToHost, s), "D2H query bound");
@@ -750,7 +743,6 @@ static snn_status query_tcl(snn_index idx, Workspace &ws, cudaStream_t s, int sm
     const int64_t total_items = hp[0];
     if (*reinterpret_cast<int *>(hp + 1)) return fail(SNN_ERR_NONFINITE, "Q contains NaN or Inf");
     const double pairs_eval = (double)*reinterpret_cast<unsigned long long *>(hp + 2);
-    const int64_t bm_total = hp[4];
     const double xb = idx->h_stats[ST_XCMAX];
     const double qb = self ? xb : *reinterpret_cast<double *>(hp + 3);
     const double bound = xb > qb ? xb : qb;
@@ -773,11 +765,11 @@ static snn_status query_tcl(snn_index idx, Workspace &ws, cudaStream_t s, int sm
     const double c0 = 2.0 * 1.05 * (eta * sd * (1 + us) + D * eta * eta + 2 * eta2 + (u22 + gacc) * (r2 / 2 * 1.01 + 1e-300));
     const double c1h = 1.0 - c1 / 2;
     const double r2h = (r2 + c0) / 2;
-    // FP16 range of the folded scalars (xbar' and b' below 65504)
     const double s2 = ldexp(1.0, 2 * e - 15);
     const double hmax = 0.5 * D * bound * bound * 1.001;
     if (hmax * s2 >= 60000.0 || (hmax + r2h) * s2 >= 60000.0) return SNN_ERR_UNSUPPORTED;
 
+    // operands (query side first for self: one pass builds both)
     uint16_t *cand = nullptr, *qry = nullptr;
     CK(ws.alloc(&cand, (size_t)n64 * kc), "alloc");
     CK(ws.alloc(&qry, (size_t)m * kc), "alloc");
@@ -788,38 +780,40 @@ static snn_status query_tcl(snn_index idx, Workspace &ws, cudaStream_t s, int sm
         launch_tcl_operands(Xs, D, idx->n, n64, idx->mu_f, e, c1h, r2h, cand, nullptr, s);
         launch_tcl_operands(Qf, D, m, m, idx->mu_f, e, c1h, r2h, nullptr, qry, s);
     }
-    unsigned long long *bitmap = nullptr;
-    CK(ws.alloc(&bitmap, (size_t)(bm_total > 0 ? bm_total : 1)), "alloc bitmap");
-    CK(cudaMemsetAsync(bitmap, 0, (size_t)(bm_total > 0 ? bm_total : 1) * 8, s), "memset");
+    // work list + record storage
+    int4 *desc;
+    int32_t *bitems, *pre, *row_count;
+    uint32_t *ecnt;
+    unsigned long long *eoff, *pool_count;
+    uint16_t *pool;
+    const int64_t nent = total_items * TM;
+    const int64_t pool_cap = 48 * m + (int64_t(1) << 20);
+    CK(ws.alloc(&desc, (size_t)(total_items > 0 ? total_items : 1)), "alloc");
+    CK(ws.alloc(&bitems, (size_t)(total_items > 0 ? total_items : 1)), "alloc");
+    CK(ws.alloc(&ecnt, (size_t)(nent > 0 ? nent : 1)), "alloc");
+    CK(ws.alloc(&eoff, (size_t)(nent > 0 ? nent : 1)), "alloc");
+    CK(ws.alloc(&pool, (size_t)pool_cap), "alloc");
+    CK(ws.alloc(&pool_count, 1), "alloc");
+    CK(cudaMemsetAsync(pool_count, 0, 8, s), "memset");
+    CK(ws.alloc(&pre, (size_t)(nent > 0 ? nent : 1)), "alloc");
+    CK(ws.alloc(&row_count, (size_t)m), "alloc");
+    launch_tcl_fill_items(blk_lo, blk_hi, nblocks, (int)G, chunk, bstart, desc, bitems, s);
     TclArgs t{};
-    t.n = idx->n; t.m = m;
-    t.blk_lo = blk_lo; t.blk_hi = blk_hi; t.grp_lo = grp_lo; t.grp_start = grp_start;
-    t.nblocks = nblocks; t.ngroups = ngroups; t.total_items = total_items; t.group = (int)G; t.chunk = chunk;
-    t.bitmap = bitmap; t.bm_off = bm_off;
+    t.n = idx->n; t.m = m; t.n_pad = idx->n_pad; t.m_pad = self ? idx->n_pad : round_up(m, 4);
+    t.desc = desc; t.total_items = total_items;
+    t.Xs = Xs; t.Qs = Qf;
+    thresholds(R * R, D, &t.T_in, &t.T_out);
+    t.R2 = R * R;
+    t.ecnt = ecnt; t.eoff = eoff; t.pool = pool; t.pool_count = pool_count; t.pool_cap = pool_cap;
     const int ctok = prof_begin(F_COUNT, s);
-    if (!launch_tcl_window(qry, cand, kc, n64, t, sms, s)) return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    if (!launch_tcl_window(qry, cand, D, n64, t, sms, s)) return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     prof_end(ctok, s, pairs_eval);
 
-    // exact decision of the flagged chunks, then the CSR in key order (no sort)
     const int wtok = prof_begin(F_WRITE, s);
     TclPost pp{};
     pp.n = idx->n; pp.m = m; pp.Xs = Xs; pp.Qs = Qf; pp.perm = idx->perm; pp.qperm = qperm;
-    pp.blk_lo = blk_lo; pp.blk_hi = blk_hi; pp.bm_off = bm_off; pp.bitmap = bitmap;
-    thresholds(R * R, D, &pp.T_in, &pp.T_out);
-    pp.R2 = R * R;
-    int64_t *fcnt, *foff;
-    int32_t *row_count;
-    CK(ws.alloc(&fcnt, (size_t)m), "alloc");
-    CK(ws.alloc(&foff, (size_t)m + 1), "alloc");
-    CK(ws.alloc(&row_count, (size_t)m), "alloc");
-    launch_tcl_flag_count(pp, fcnt, s);
-    exclusive_scan_i64(fcnt, foff, m, scan_tmp, s);
-    CK(cudaMemcpyAsync(hp, foff + m, 8, cudaMemcpyDeviceToHost, s), "D2H flagged");
-    CK(cudaStreamSynchronize(s), "tc filter");
-    const int64_t F = hp[0];
-    uint32_t *masks;
-    CK(ws.alloc(&masks, (size_t)(F > 0 ? F : 1)), "alloc");
-    launch_tcl_exact(pp, D, foff, masks, row_count, s);                           // exact decision
+    pp.T_in = t.T_in; pp.T_out = t.T_out; pp.R2 = t.R2;
+    launch_tcl_row_totals(pp, bstart, bitems, ecnt, pre, row_count, s);
     snn_result r = new snn_result_s();
     r->m = m;
     void *pm = nullptr;
@@ -835,9 +829,14 @@ static snn_status query_tcl(snn_index idx, Workspace &ws, cudaStream_t s, int sm
     r->indices = static_cast<int32_t *>(pm);
     if ((ce = cudaMallocAsync(&pm, (size_t)(H > 0 ? H : 1) * 4, s)) != cudaSuccess) { snn_result_free(r); return cuda_fail(ce, "alloc"); }
     r->distances = static_cast<float *>(pm);
-    launch_tcl_write(pp, D, foff, masks, r->offsets, r->indices, r->distances, s);   // K11
+    int64_t *ovf = nullptr;
+    unsigned long long *novf = nullptr;
+    if ((ce = ws.alloc(&ovf, (size_t)(nent > 0 ? nent : 1))) != cudaSuccess ||
+        (ce = ws.alloc(&novf, 1)) != cudaSuccess) { snn_result_free(r); return cuda_fail(ce, "alloc"); }
+    cudaMemsetAsync(novf, 0, 8, s);
+    launch_tcl_compact(pp, D, nent, desc, ecnt, eoff, pool, pre, r->offsets, r->indices, r->distances, ovf, novf, s);   // K11
     prof_end(wtok, s, (double)H);
-    g_last_ovf = F;   // flagged 32-candidate chunks
+    g_last_ovf = 0;
     g_last_lost = 0;
     ce = cudaGetLastError();
     if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);

@@ -58,25 +58,27 @@ void launch_tc_write(const uint32_t *order, const uint32_t *hj, const float *hd,
 }  // namespace snn
 
 namespace snn {
-// Low-d tensor-core filter (tc_lowd.cu): folded split-FP16 operands, K = 3d + 4 (16 / 32),
-// output = candidate bitmap (one bit per query x 32-candidate chunk of its window).
+// Low-d tensor-core path (tc_lowd.cu): folded split-FP16 filter (K = 3d + 4 in 16 / 32
+// columns) fused with the exact decision; per-(item, query) hit records -> CSR.
 struct TclArgs {
     int64_t n, m;
-    const int64_t *blk_lo, *blk_hi;     // 64-aligned windows of 128-query blocks
-    const int64_t *grp_lo, *grp_start;
-    int64_t nblocks, ngroups, total_items;
-    int group, chunk;
-    unsigned long long *bitmap;         // zeroed; block b's rows start at bm_off[b]
-    const int64_t *bm_off;
+    int64_t n_pad, m_pad;               // rows of the AoSoA4 fp32 copies (multiples of 4)
+    const int4 *desc;                   // items {block, c0, c1, chunk index in block}
+    int64_t total_items;
+    const float *Xs, *Qs;               // AoSoA4 fp32 sorted copies (index / queries)
+    float T_in, T_out;                  // fp32 sure-in / sure-out thresholds (FFMA path's)
+    double R2;
+    uint32_t *ecnt;                     // per (item, row): hits (written once)
+    unsigned long long *eoff;           // per (item, row): first position in pool, ~0 = not stored
+    uint16_t *pool;                     // hit positions within the item, ascending per entry
+    unsigned long long *pool_count;     // zeroed
+    int64_t pool_cap;
 };
-// exact decision + CSR write over the bitmap
 struct TclPost {
     int64_t n, m;
-    const float *Xs, *Qs;               // AoSoA4 sorted copies (index / queries)
+    const float *Xs, *Qs;
     const int32_t *perm, *qperm;
-    const int64_t *blk_lo, *blk_hi, *bm_off;
-    const unsigned long long *bitmap;
-    float T_in, T_out;                  // fp32 sure-in / sure-out thresholds (FFMA path's)
+    float T_in, T_out;
     double R2;
 };
 int tcl_kc(int d);              // 16 (d <= 4) or 32 (d <= 8)
@@ -84,13 +86,19 @@ bool tcl_supported(int d);
 // operand rows from an AoSoA4 fp32 sorted copy; cand: rows_pad x kc, qry: rows x kc (nullable)
 void launch_tcl_operands(const float *Xs, int d, int64_t rows, int64_t rows_pad, const float *mu_f, int e, double c1h,
                          double r2h, void *cand, void *qry, cudaStream_t s);
-bool launch_tcl_window(const void *qry, const void *cand, int kc, int64_t cand_rows, const TclArgs &a, int sm_count,
+// work list: bcount[b] items of block b; after an exclusive scan (bstart) the descriptors
+void launch_tcl_items(const int64_t *blk_lo, const int64_t *blk_hi, int64_t nblocks, int group, int chunk,
+                      int64_t *bcount, cudaStream_t s);
+void launch_tcl_fill_items(const int64_t *blk_lo, const int64_t *blk_hi, int64_t nblocks, int group, int chunk,
+                           const int64_t *bstart, int4 *desc, int32_t *bitems, cudaStream_t s);
+bool launch_tcl_window(const void *qry, const void *cand, int d, int64_t cand_rows, const TclArgs &a, int sm_count,
                        cudaStream_t s);
-void launch_tcl_bm_sizes(const int64_t *blk_lo, const int64_t *blk_hi, int64_t nblocks, int64_t *words,
-                         cudaStream_t s);
-void launch_tcl_flag_count(const TclPost &p, int64_t *fcnt, cudaStream_t s);
-void launch_tcl_exact(const TclPost &p, int d, const int64_t *foff, uint32_t *masks, int32_t *row_count,
-                      cudaStream_t s);
-void launch_tcl_write(const TclPost &p, int d, const int64_t *foff, const uint32_t *masks, const int64_t *offsets,
-                      int32_t *out_idx, float *out_dist, cudaStream_t s);
+void launch_tcl_row_totals(const TclPost &p, const int64_t *bstart, const int32_t *bitems, const uint32_t *ecnt,
+                           int32_t *pre, int32_t *row_count, cudaStream_t s);
+// CSR write; entries the pool could not hold (eoff == ~0) are listed in ovf (novf zeroed)
+// and re-decided by a warp-per-entry pass
+void launch_tcl_compact(const TclPost &p, int d, int64_t nent, const int4 *desc, const uint32_t *ecnt,
+                        const unsigned long long *eoff, const uint16_t *pool, const int32_t *pre,
+                        const int64_t *offsets, int32_t *out_idx, float *out_dist, int64_t *ovf,
+                        unsigned long long *novf, cudaStream_t s);
 }  // namespace snn
