@@ -38,6 +38,7 @@ struct Options {
     int tc_f16 = 1;      // tensor-core operands FP16 (scaled) instead of TF32
     int tc_group = 32;   // query blocks per raster group (upper bound; L2 budget decides)
     int tc_gram_min_d = 128;   // Gram matrix on the tensor cores for d >= this
+    int simt_filter = 0; // low-d fp32 scan: expanded-form SIMT pre-filter (option; measured slower on c2/c5)
     int lowd_tc = 0;     // low-d (fp32, d <= 8) radius queries through the tensor-core filter (option; FFMA default)
     int lowd_tc_tiles = 8;     // 256-candidate tiles per work item (low-d tensor-core path)
     int lowd_tc_group = 8;     // query blocks per raster group (low-d tensor-core path)
@@ -96,6 +97,8 @@ static void prof_drain() {
     }
     g_prof.pending.clear();
 }
+
+bool dbscan_simt_filter() { return g_opt.simt_filter != 0; }
 
 snn_status fail(snn_status st, const std::string &msg) {
     t_err = msg;
@@ -277,6 +280,7 @@ snn_status snn_set_option(const char *key, int64_t value) {
         g_opt.tc_gram_min_d = (int)value;
         return SNN_OK;
     }
+    if (k == "simt_filter") { g_opt.simt_filter = value > 0 ? 1 : 0; return SNN_OK; }   // 0: default (off)
     if (k == "lowd_tc") { g_opt.lowd_tc = value > 0 ? 1 : 0; return SNN_OK; }   // 0: default (off)
     if (k == "lowd_tc_tiles") {
         if (value == 0) value = 8;
@@ -412,6 +416,13 @@ snn_status snn_build(const void *X, int64_t n, int32_t d, snn_dtype dt, void *st
     if (nonfinite) {
         free_index(idx);
         return fail(SNN_ERR_NONFINITE, "X contains NaN or Inf");
+    }
+    if (idx->ld == 0 && !f64) {   // low-d fp32: expanded-form filter rows (scan variant 3)
+        double c1h = 1.0, r2h = 0.0;
+        simt_filter_consts(d, 1.0, &c1h, &r2h);
+        CKI(own(&idx->Xf, (size_t)idx->n_pad * (d + 1)), "alloc filter rows");
+        idx->xf_c1h = c1h;
+        launch_filter_rows(static_cast<const float *>(idx->Xs), d, n, idx->n_pad, idx->mu_f, c1h, idx->Xf, s);
     }
     if (idx->ld != 0 && g_opt.tc && !g_opt.force_generic && d >= g_opt.tc_min_d) {   // K5': TC operand copy
         idx->tc = 1;
@@ -992,6 +1003,11 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
     a.offsets = r->offsets; a.out_idx = nullptr; a.out_dist = nullptr;
     a.sm_count = sms;
     a.variant = g_opt.variant;
+    if (!generic && !f64 && idx->Xf && g_opt.simt_filter) {
+        double c1h = 1.0, r2h = 0.0;
+        simt_filter_consts(D, R, &c1h, &r2h);
+        a.Xf = idx->Xf; a.c1h = idx->xf_c1h; a.r2h = r2h; a.mu_f = idx->mu_f;
+    }
     if (total_items == 0) {
         cudaMemsetAsync(row_count, 0, (size_t)m * 4, s);
     } else {

@@ -161,6 +161,11 @@ snn_status dbscan_impl(snn_index idx, double eps, int32_t min_pts, int32_t *labe
     a.cnt = cnt; a.pre = cnt; a.cap = 0; a.variant = 1;
     a.sm_count = idx->sm_count;
     a.core = core; a.parent = parent; a.best = best; a.min_pts = min_pts;
+    if (!f64 && idx->Xf && dbscan_simt_filter()) {   // expanded-form SIMT pre-filter (option)
+        double c1h = 1.0, r2h = 0.0;
+        simt_filter_consts(idx->d, eps, &c1h, &r2h);
+        a.Xf = idx->Xf; a.c1h = idx->xf_c1h; a.r2h = r2h; a.mu_f = idx->mu_f;
+    }
 
     unsigned long long *hp_pairs = reinterpret_cast<unsigned long long *>(hbuf);
     CKD(cudaMemcpyAsync(hp_pairs, pairs, 8, cudaMemcpyDeviceToHost, s), "D2H");

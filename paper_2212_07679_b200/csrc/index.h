@@ -65,6 +65,8 @@ struct snn_index_s {
     int xexp = 0;              // FP16 operand scale exponent of the index copy
     int kpad = 0;              // K padded to 64 (FP16) / 32 (TF32)
     void *Xt = nullptr;        // n x kpad centred tensor-core operand copy (FP16 or TF32)
+    float *Xf = nullptr;       // low-d fp32: expanded-form filter rows (AoSoA4, d+1 floats)
+    double xf_c1h = 1.0;       // c1h the filter rows were built with
     std::vector<void *> owned;
 };
 
@@ -77,6 +79,7 @@ struct snn_result_s {
 
 
 namespace snn {
+bool dbscan_simt_filter();   // option simt_filter (api.cu)
 snn_status dbscan_impl(snn_index idx, double eps, int32_t min_pts, int32_t *labels,
                        int32_t *n_clusters, cudaStream_t s);
 }

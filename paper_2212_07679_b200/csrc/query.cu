@@ -259,7 +259,11 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
     const int tid = threadIdx.x;
     const T *Xs = static_cast<const T *>(a.Xs);
     const T *Qs = static_cast<const T *>(a.Qs);
-    const size_t buf_bytes = (size_t)a.chunk * D * sizeof(T);
+    // G == 3: expanded-form filter rows (AoSoA4, D+1 floats per row) staged after the
+    // original coordinates of the chunk
+    constexpr int FW = G == 3 ? D + 1 : 0;
+    const size_t orig_bytes = (size_t)a.chunk * D * sizeof(T);
+    const size_t buf_bytes = orig_bytes + (size_t)a.chunk * FW * 4;
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem + 2 * buf_bytes);
     const int64_t n_work = MODE == M_FIX ? a.n_ovf : a.total_items;
     auto item_of = [&](int64_t w) -> int64_t { return MODE == M_FIX ? (int64_t)a.ovf_items[w] : w; };
@@ -273,9 +277,11 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
         int64_t b, c0, c1;
         locate(a, item, b, c0, c1);
         const uint32_t bytes = (uint32_t)((c1 - c0) * D * sizeof(T));
+        const uint32_t fbytes = (uint32_t)((c1 - c0) * FW * 4);
         fence_proxy_async_smem();
-        mbar_arrive_expect_tx(&bar[sidx], bytes);
+        mbar_arrive_expect_tx(&bar[sidx], bytes + fbytes);
         bulk_g2s(smem + sidx * buf_bytes, Xs + c0 * D, bytes, &bar[sidx]);
+        if (FW) bulk_g2s(smem + sidx * buf_bytes + orig_bytes, a.Xf + c0 * FW, fbytes, &bar[sidx]);
     };
     uint32_t phase[2] = {0u, 0u};
     int64_t w = blockIdx.x;
@@ -314,6 +320,20 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
                 uint64_t nq[D];
 #pragma unroll
                 for (int k = 0; k < D; ++k) nq[k] = f2pack(-q[k], -q[k]);
+                // expanded-form filter operands of this query: centred coordinates and the
+                // rigorous threshold thr = r2h - qbar c1h (fp64, rounded up)
+                uint64_t nqc[FW > 0 ? D : 1];
+                float thr = 0.f;
+                if constexpr (G == 3) {
+                    double qb = 0.0;
+#pragma unroll
+                    for (int k = 0; k < D; ++k) {
+                        const float qc = (float)((double)q[k] - (double)a.mu_f[k]);
+                        qb += (double)qc * (double)qc;
+                        nqc[k] = f2pack(-qc, -qc);
+                    }
+                    thr = __double2float_ru(a.r2h - 0.5 * qb * a.c1h);
+                }
                 int g = 0;
                 if (MODE != M_FIX) {
                     // straight-line hit path (taken by ~1 lane of a warp at a time): 4-bit
@@ -355,6 +375,49 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
                         }
                         em.c += __popc(m);
                     };
+                    // G == 3: expanded form eq:ip2 as a cheap conservative filter (PAPER.md:211-216,
+                    // margin of reading C20 for fp32 FFMA chains), acc = xbar' - x_c.q_c per
+                    // candidate, 2 FFMA2 per coordinate and 4 candidates; candidates go to the
+                    // exact direct-form classification below (identical decisions)
+                    if constexpr (G == 3) {
+                        const float4 *f4 = reinterpret_cast<const float4 *>(smem + sidx * buf_bytes + orig_bytes);
+                        for (; g + 1 < ngroups; g += 2) {
+                            float4 fa[D + 1], fb[D + 1];
+#pragma unroll
+                            for (int k = 0; k <= D; ++k) { fa[k] = f4[g * (D + 1) + k]; fb[k] = f4[(g + 1) * (D + 1) + k]; }
+                            uint64_t la = f2pack(fa[D].x, fa[D].y), ha = f2pack(fa[D].z, fa[D].w);
+                            uint64_t lb = f2pack(fb[D].x, fb[D].y), hb = f2pack(fb[D].z, fb[D].w);
+#pragma unroll
+                            for (int k = 0; k < D; ++k) {
+                                la = f2fma(f2pack(fa[k].x, fa[k].y), nqc[k], la);
+                                ha = f2fma(f2pack(fa[k].z, fa[k].w), nqc[k], ha);
+                                lb = f2fma(f2pack(fb[k].x, fb[k].y), nqc[k], lb);
+                                hb = f2fma(f2pack(fb[k].z, fb[k].w), nqc[k], hb);
+                            }
+                            const float2 ea = f2unpack(la), eb = f2unpack(ha), ec = f2unpack(lb), ed = f2unpack(hb);
+                            const float mnf = fminf(fminf(fminf(ea.x, ea.y), fminf(eb.x, eb.y)),
+                                                    fminf(fminf(ec.x, ec.y), fminf(ed.x, ed.y)));
+                            if (mnf <= thr) {
+                                float4 xa[D], xb[D];
+#pragma unroll
+                                for (int k = 0; k < D; ++k) { xa[k] = g4[g * D + k]; xb[k] = g4[(g + 1) * D + k]; }
+                                uint64_t pla, pha, plb, phb;
+                                group_d2<D>(xa, nq, pla, pha);
+                                group_d2<D>(xb, nq, plb, phb);
+                                const float2 pa = f2unpack(pla), qa = f2unpack(pha), pb = f2unpack(plb), qb = f2unpack(phb);
+                                uint32_t ia = mask4(pa.x, pa.y, qa.x, qa.y, T_in);
+                                uint32_t ib = mask4(pb.x, pb.y, qb.x, qb.y, T_in);
+                                const uint32_t oa = mask4(pa.x, pa.y, qa.x, qa.y, T_out);
+                                const uint32_t ob = mask4(pb.x, pb.y, qb.x, qb.y, T_out);
+                                if ((ia ^ oa) | (ib ^ ob)) {
+                                    ia |= resolve4<D>(oa & ~ia, xa, q, R2);
+                                    ib |= resolve4<D>(ob & ~ib, xb, q, R2);
+                                }
+                                if (ia) emit0(g, ia);
+                                if (ib) emit0(g + 1, ib);
+                            }
+                        }
+                    }
                     for (; G == 2 && g + 1 < ngroups; g += 2) {
                         float4 xa[D], xb[D];
 #pragma unroll
@@ -663,8 +726,11 @@ int persistent_grid(K kernel, int threads, size_t smem, int64_t items, int sm_co
 
 template <typename T, int D, int MODE>
 void run_lowd(const PassArgs &a, cudaStream_t s) {
-    const size_t smem = (size_t)2 * a.chunk * D * sizeof(T) + 16;
-    auto k = a.variant == 1 ? window_lowd<T, D, MODE, 1> : window_lowd<T, D, MODE, 2>;
+    const bool exp = sizeof(T) == 4 && MODE != M_FIX && a.Xf != nullptr &&
+                     (size_t)2 * a.chunk * (D * sizeof(T) + (D + 1) * 4) + 16 <= 200 * 1024;
+    const size_t smem = (size_t)2 * a.chunk * (D * sizeof(T) + (exp ? (D + 1) * 4 : 0)) + 16;
+    auto k = exp ? window_lowd<T, D, MODE, 3>
+                 : (a.variant == 1 ? window_lowd<T, D, MODE, 1> : window_lowd<T, D, MODE, 2>);
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int64_t work = MODE == M_FIX ? a.n_ovf : a.total_items;
     int g = persistent_grid(k, a.B, smem, work, a.sm_count);
@@ -760,6 +826,49 @@ void launch_row_totals(const int32_t *cnt, int32_t *pre, const int64_t *item_sta
                        int B, const int32_t *qperm, int32_t *row_count, cudaStream_t s) {
     if (m == 0) return;
     SNN_LAUNCH(row_totals, (int)ceil_div(m, 256), 256, 0, s, cnt, pre, item_start, m, B, qperm, row_count);
+}
+
+namespace {
+// Expanded-form filter rows (G == 3 scan variant): AoSoA4 with D+1 floats per row,
+// x_c = fl32(x - mu_f) and xbar' = fl32(c1h * 0.5 * ||x_c||^2) (fp64 sum); padding rows
+// [n, n_pad) get x_c = 0, xbar' = +inf (never candidates).
+template <int D>
+__global__ void __launch_bounds__(256) filter_rows_kernel(const float *__restrict__ Xs, int64_t n, int64_t n_pad,
+                                                          const float *__restrict__ mu_f, double c1h, float *Xf) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_pad; i += (int64_t)gridDim.x * blockDim.x) {
+        float c[D];
+        double hb = 0.0;
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            c[k] = i < n ? (float)((double)Xs[(i >> 2) * 4 * D + 4 * k + (i & 3)] - (double)mu_f[k]) : 0.f;
+            hb += (double)c[k] * (double)c[k];
+        }
+        float *o = Xf + (i >> 2) * 4 * (D + 1) + (i & 3);
+#pragma unroll
+        for (int k = 0; k < D; ++k) o[4 * k] = c[k];
+        o[4 * D] = i < n ? (float)(0.5 * hb * c1h) : INFINITY;
+    }
+}
+}  // namespace
+
+void launch_filter_rows(const float *Xs, int d, int64_t n, int64_t n_pad, const float *mu_f, double c1h, float *Xf,
+                        cudaStream_t s) {
+    int64_t g = ceil_div(n_pad, 256);
+    if (g > 148 * 16) g = 148 * 16;
+    if (g < 1) g = 1;
+#define CASE(D) case D: SNN_LAUNCH(filter_rows_kernel<D>, (int)g, 256, 0, s, Xs, n, n_pad, mu_f, c1h, Xf); break;
+    switch (d) { CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) default: break; }
+#undef CASE
+}
+
+void simt_filter_consts(int d, double R, double *c1h, double *r2h) {
+    // |acc - (xbar c1h - x.q)| <= (c1/2)(xbar + qbar) + c0/2 for acc = fl(xbar' - sum x_c q_c)
+    // (FFMA chain): xbar' rounding 3u, centring of x and q 2u, chain d * 2.02 u, qbar 2.02 u
+    const double u = ldexp(1.0, -24);
+    const double c1 = 2.0 * 1.05 * u * (3.0 + 2.01 + 2.02 * d + 2.02);
+    const double c0 = 2.0 * 1.05 * (2.0 * d + 6.0) * ldexp(1.0, -149);
+    *c1h = 1.0 - c1 / 2;
+    *r2h = (R * R * (1.0 + 1e-12) * (1.0 + ldexp(1.0, -20)) + c0) / 2;
 }
 
 }  // namespace snn

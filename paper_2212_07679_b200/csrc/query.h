@@ -66,7 +66,17 @@ struct PassArgs {
     int32_t *parent;        // union-find parents
     int32_t *best;          // M_BORDER: smallest original id of a core neighbour (atomicMin)
     int32_t min_pts;        // M_COUNT: counts are only needed up to min_pts (early exit)
+    // expanded-form SIMT filter (scan variant 3; nullptr = off): AoSoA4 rows with D+1
+    // floats (centred coordinates, xbar c1h), the margin constants and mu_f
+    const float *Xf = nullptr;
+    double c1h = 1.0, r2h = 0.0;
+    const float *mu_f = nullptr;
 };
+// filter rows for the expanded-form scan variant from the AoSoA4 sorted copy
+void launch_filter_rows(const float *Xs, int d, int64_t n, int64_t n_pad, const float *mu_f, double c1h, float *Xf,
+                        cudaStream_t s);
+// margin constants of the expanded-form fp32 filter (reading C20, SIMT form)
+void simt_filter_consts(int d, double R, double *c1h, double *r2h);
 
 bool lowd_supported(int d);   // d handled by the register-resident low-d kernels
 

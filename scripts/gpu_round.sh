@@ -1,7 +1,7 @@
 #!/bin/bash
-# One gpurun call: GPU parity tests, benches per config, ncu launch list + full captures.
+# One gpurun call: GPU parity tests, benches per config, ncu launch lists + full captures.
 # usage (under gpurun): bash scripts/gpu_round.sh TAG [stages...]
-#   stages: build tests bench ncu_launch ncu_full_c2 ncu_full_c3 ncu_full_c4 ncu_full_c5
+#   stages: build tests smoke bench benchfast ncu_launch ncu_full_c2 ncu_full_c3 ncu_full_c4 ncu_full_c5 ncu_gram_c4
 set -u
 TAG=${1:-run}; shift
 OUT=gpurun_out/$TAG; mkdir -p $OUT
@@ -13,9 +13,10 @@ for s in $STAGES; do
     build) python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1 || { echo BUILD FAIL; tail -20 $OUT/build.log; exit 1; } ;;
     tests) timeout 1200 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.txt 2>&1; echo "pytest rc=$?"; tail -3 $OUT/pytest_gpu.txt ;;
     smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.txt 2>&1; echo "smoke rc=$?"; tail -2 $OUT/smoke.txt ;;
-    bench) timeout 600 python bench.py > $OUT/bench_c2.jsonl 2> $OUT/bench_c2.err; echo "bench c2 rc=$?"; tail -c 600 $OUT/bench_c2.jsonl
+    bench) timeout 600 python bench.py > $OUT/bench_c2.jsonl 2> $OUT/bench_c2.err; echo "bench c2 rc=$?"
            for c in c1 c3 c4 c5; do timeout 600 python bench.py --config $c --steps 10 --no-cpu-baseline > $OUT/bench_$c.jsonl 2> $OUT/bench_$c.err; echo "bench $c rc=$?"; done ;;
     benchfast) for c in c2 c3 c4 c5; do timeout 600 python bench.py --config $c --steps 10 --no-cpu-baseline > $OUT/bench_$c.jsonl 2> $OUT/bench_$c.err; echo "bench $c rc=$?"; done ;;
+    reference) timeout 600 python bench.py --impl reference --steps 3 > $OUT/bench_reference.jsonl 2> $OUT/bench_reference.err; echo "reference rc=$?" ;;
     ncu_launch) for c in c2 c3 c4 c5; do
         CMD="python bench.py --config $c --steps 1 --warmup 3 --no-cpu-baseline"
         $CMD > $OUT/plain_$c.log 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$c.csv $CMD > $OUT/ncu_launch_$c.log 2>&1; echo "ncu launch $c rc=$?"; done ;;
@@ -23,5 +24,8 @@ for s in $STAGES; do
         case $c in c2|c5) K='regex:window_lowd';; *) K='regex:tc_window';; esac
         CMD="python bench.py --config $c --steps 1 --warmup 3 --no-cpu-baseline"
         $CMD > $OUT/plainf_$c.log 2>&1 && timeout 1200 ncu --set full --clock-control none --import-source on -k $K -s 6 -c 2 -o $OUT/full_$c $CMD > $OUT/ncu_full_$c.log 2>&1; echo "ncu full $c rc=$?" ;;
+    ncu_gram_c4)
+        CMD="python bench.py --config c4 --steps 1 --warmup 3 --no-cpu-baseline"
+        $CMD > $OUT/plaing_c4.log 2>&1 && timeout 1200 ncu --set full --clock-control none --import-source on -k regex:gram_tc -s 3 -c 1 -o $OUT/gram_c4 $CMD > $OUT/ncu_gram_c4.log 2>&1; echo "ncu gram c4 rc=$?" ;;
   esac
 done

@@ -450,6 +450,34 @@ def test_lowd_tensor_core_vs_ffma_exact(snn, d):
     assert np.array_equal(a.offsets, b.offsets) and np.array_equal(a.indices, b.indices)
 
 
+@pytest.mark.parametrize("d", [1, 2, 3, 5, 8])
+def test_simt_expanded_filter_vs_direct_exact(snn, d):
+    """Low-d scan with the expanded-form fp32 pre-filter (eq:ip2 with the rigorous margin)
+    vs the plain direct-form scan: bit-identical CSR and DBSCAN labels, equal to the oracle."""
+    import paper_2212_07679_b200 as p
+    rng = np.random.default_rng(200 + d)
+    centers = rng.random((12, d)) * 40 + 3000.0            # far from the origin: cancellation
+    X = (centers[rng.integers(0, 12, 15000)] + rng.standard_normal((15000, d))).astype(np.float32)
+    Q = np.concatenate([X[:1000], (X[1000:2000] + rng.standard_normal((1000, d)) * 0.5).astype(np.float32)])
+    R = 0.8
+    res = {}
+    try:
+        for f in (1, -1):
+            p.snn_set_option("simt_filter", f)
+            idx = p.Index(_dev(X))
+            lab, k = idx.dbscan(R, 4)
+            res[f] = (idx.query(_dev(Q), R), idx.query_self(R), lab, k)
+            idx.free()
+    finally:
+        p.snn_set_option("simt_filter", 0)
+    compare(res[1][0], oracle.radius_query(X, Q, R))
+    for i in (0, 1):
+        a, b = res[1][i], res[-1][i]
+        assert np.array_equal(a.offsets, b.offsets) and np.array_equal(a.indices, b.indices)
+        assert np.array_equal(a.distances, b.distances)
+    assert res[1][3] == res[-1][3] and np.array_equal(res[1][2], res[-1][2])
+
+
 @pytest.mark.parametrize("tiles,group", [(1, 1), (3, 2), (8, 8), (16, 64)])
 def test_lowd_tensor_core_raster_options(snn, tiles, group):
     import paper_2212_07679_b200 as p
