@@ -75,6 +75,25 @@ __global__ void final_labels(const int32_t *lab, const uint8_t *core, const int3
     }
 }
 
+// non-core flags (for the compacted border query)
+__global__ void noncore_flags(const uint8_t *core, int64_t n, int32_t *flag) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        flag[i] = core[i] ? 0 : 1;
+}
+
+// compacted border queries: list of non-core sorted positions, their keys and AoSoA4 rows
+template <typename T>
+__global__ void gather_noncore(const uint8_t *core, const int64_t *pos, int64_t n, int d, const T *Xs,
+                               const float *keys, int32_t *list, float *qkeys, T *Qb) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        if (core[i]) continue;
+        const int64_t t = pos[i];
+        list[t] = (int32_t)i;
+        qkeys[t] = keys[i];
+        for (int k = 0; k < d; ++k) Qb[(t >> 2) * 4 * d + 4 * k + (t & 3)] = Xs[(i >> 2) * 4 * d + 4 * k + (i & 3)];
+    }
+}
+
 int grid_n(int64_t n) {
     int64_t g = ceil_div(n, 256);
     return (int)(g < 148 * 16 ? (g < 1 ? 1 : g) : 148 * 16);
@@ -161,6 +180,7 @@ snn_status dbscan_impl(snn_index idx, double eps, int32_t min_pts, int32_t *labe
     a.cnt = cnt; a.pre = cnt; a.cap = 0; a.variant = 1;
     a.sm_count = idx->sm_count;
     a.core = core; a.parent = parent; a.best = best; a.min_pts = min_pts;
+    a.n_index = n;
     if (!f64 && idx->Xf && dbscan_simt_filter()) {   // expanded-form SIMT pre-filter (option)
         double c1h = 1.0, r2h = 0.0;
         simt_filter_consts(idx->d, eps, &c1h, &r2h);
@@ -176,13 +196,65 @@ snn_status dbscan_impl(snn_index idx, double eps, int32_t min_pts, int32_t *labe
     prof_end(ctok, s, pairs_eval);
     launch_row_totals(cnt, cnt, item_start, n, B, nullptr, count, s);
     SNN_LAUNCH(init_core, grid_n(n), 256, 0, s, count, n, min_pts, core, parent, minid, best);
-    launch_lowd_mode(3, a, s);                                              // unions
+    {   // unions over the clipped windows (pairs j > i only: block b starts at its first position)
+        int64_t *lo2, *nit2, *st2;
+        CKD(ws.alloc(&lo2, (size_t)nblocks), "alloc");
+        CKD(ws.alloc(&nit2, (size_t)nblocks), "alloc");
+        CKD(ws.alloc(&st2, (size_t)nblocks + 1), "alloc");
+        launch_truncate_windows(blk_lo, blk_hi, nblocks, B, chunk, lo2, nit2, s);
+        exclusive_scan_i64(nit2, st2, nblocks, scan_tmp, s);
+        CKD(cudaMemcpyAsync(hbuf, st2 + nblocks, 8, cudaMemcpyDeviceToHost, s), "D2H");
+        CKD(cudaStreamSynchronize(s), "dbscan union windows");
+        PassArgs au = a;
+        au.blk_lo = lo2; au.item_start = st2; au.total_items = hbuf[0];
+        launch_lowd_mode(3, au, s);                                          // unions
+    }
     SNN_LAUNCH(flatten, grid_n(n), 256, 0, s, parent, core, idx->perm, n, minid);
     CKD(cudaMemsetAsync(flag, 0, (size_t)n * 4, s), "memset");
     SNN_LAUNCH(flag_roots, grid_n(n), 256, 0, s, parent, core, minid, n, flag);
     exclusive_scan_i32_to_i64(flag, rank, n, scan_tmp, s);                  // canonical ranks
     SNN_LAUNCH(core_labels, grid_n(n), 256, 0, s, parent, core, minid, rank, idx->perm, n, lab, inv);
-    launch_lowd_mode(4, a, s);                                              // border points
+    {   // border points: a radius query of the compacted non-core points only
+        int64_t *npos;
+        CKD(ws.alloc(&npos, (size_t)n + 1), "alloc");
+        SNN_LAUNCH(noncore_flags, grid_n(n), 256, 0, s, core, n, flag);
+        exclusive_scan_i32_to_i64(flag, npos, n, scan_tmp, s);
+        CKD(cudaMemcpyAsync(hbuf, npos + n, 8, cudaMemcpyDeviceToHost, s), "D2H");
+        CKD(cudaStreamSynchronize(s), "dbscan non-core");
+        const int64_t nb = hbuf[0];
+        if (nb > 0) {
+            const size_t es = f64 ? 8 : 4;
+            int32_t *list;
+            float *qk;
+            uint8_t *qb;
+            int64_t *lo3, *hi3, *nit3, *st3;
+            const int64_t nb3 = ceil_div(nb, B);
+            CKD(ws.alloc(&list, (size_t)nb), "alloc");
+            CKD(ws.alloc(&qk, (size_t)nb), "alloc");
+            CKD(ws.alloc(&qb, (size_t)round_up(nb, 4) * idx->d * es), "alloc");
+            CKD(ws.alloc(&lo3, (size_t)nb3), "alloc");
+            CKD(ws.alloc(&hi3, (size_t)nb3), "alloc");
+            CKD(ws.alloc(&nit3, (size_t)nb3), "alloc");
+            CKD(ws.alloc(&st3, (size_t)nb3 + 1), "alloc");
+            if (f64) SNN_LAUNCH(gather_noncore<double>, grid_n(n), 256, 0, s, core, npos, n, idx->d,
+                                (const double *)idx->Xs, idx->keys, list, qk, (double *)qb);
+            else SNN_LAUNCH(gather_noncore<float>, grid_n(n), 256, 0, s, core, npos, n, idx->d,
+                            (const float *)idx->Xs, idx->keys, list, qk, (float *)qb);
+            WindowSpec w3 = w;
+            w3.qkeys = qk; w3.m = nb;
+            w3.blk_lo = lo3; w3.blk_hi = hi3; w3.nitems = nit3; w3.pairs = pairs;
+            launch_block_windows(w3, s);
+            exclusive_scan_i64(nit3, st3, nb3, scan_tmp, s);
+            CKD(cudaMemcpyAsync(hbuf, st3 + nb3, 8, cudaMemcpyDeviceToHost, s), "D2H");
+            CKD(cudaStreamSynchronize(s), "dbscan border windows");
+            PassArgs ab = a;
+            ab.Qs = qb; ab.m = nb; ab.qperm = list;
+            ab.blk_lo = lo3; ab.blk_hi = hi3; ab.item_start = st3;
+            ab.nblocks = nb3; ab.total_items = hbuf[0];
+            ab.cnt = nullptr; ab.pre = nullptr;
+            launch_lowd_mode(4, ab, s);                                      // border points
+        }
+    }
     SNN_LAUNCH(final_labels, grid_n(n), 256, 0, s, lab, core, best, inv, idx->perm, n, out);
     if (!dev_out) CKD(cudaMemcpyAsync(labels, out, (size_t)n * 4, cudaMemcpyDeviceToHost, s), "D2H labels");
     CKD(cudaMemcpyAsync(hbuf + 1, rank + n, 8, cudaMemcpyDeviceToHost, s), "D2H K");

@@ -305,7 +305,9 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
             if (active) em.pos = a.offsets[a.qperm[sp]] + a.pre[e];
         }
         if (MODE == M_UNION) active = active && a.core[sp] && c1 - 1 > sp;   // pairs j > i only
-        if (MODE == M_BORDER) active = active && !a.core[sp];
+        // M_BORDER over a compacted query list: qperm maps to the index position
+        const int64_t bpos = (MODE == M_BORDER && a.qperm) ? (active ? (int64_t)a.qperm[sp] : 0) : sp;
+        if (MODE == M_BORDER) active = active && !a.core[bpos];
         int32_t best = 0x7fffffff;   // M_BORDER: smallest original id of a core neighbour
         int32_t uroot = -1;          // M_UNION: cached union-find root of this query
         if (MODE == M_UNION && active) uroot = uf_rep(a.parent, (int32_t)sp);
@@ -511,7 +513,7 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
             if (__syncthreads_or(lost) && tid == 0) a.ovf_items[atomicAdd(a.ovf_count, 1)] = (int32_t)item;
         } else {
             if (MODE == M_COUNT) a.cnt[e] = em.c;
-            if (MODE == M_BORDER && active && best != 0x7fffffff) atomicMin(&a.best[sp], best);
+            if (MODE == M_BORDER && active && best != 0x7fffffff) atomicMin(&a.best[bpos], best);
             __syncthreads();
         }
     }
@@ -869,6 +871,26 @@ void simt_filter_consts(int d, double R, double *c1h, double *r2h) {
     const double c0 = 2.0 * 1.05 * (2.0 * d + 6.0) * ldexp(1.0, -149);
     *c1h = 1.0 - c1 / 2;
     *r2h = (R * R * (1.0 + 1e-12) * (1.0 + ldexp(1.0, -20)) + c0) / 2;
+}
+
+namespace {
+// DBSCAN union pass: only pairs j > i are united, so block b's window starts at its own
+// first position (rounded down to 4).
+__global__ void truncate_windows_kernel(const int64_t *blk_lo, const int64_t *blk_hi, int64_t nblocks, int B,
+                                        int chunk, int64_t *lo2, int64_t *nitems2) {
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nblocks) return;
+    const int64_t lo = max(blk_lo[b], (b * B) & ~(int64_t)3), hi = blk_hi[b];
+    lo2[b] = lo;
+    nitems2[b] = hi > lo ? ceil_div(hi - lo, chunk) : 0;
+}
+}  // namespace
+
+void launch_truncate_windows(const int64_t *blk_lo, const int64_t *blk_hi, int64_t nblocks, int B, int chunk,
+                             int64_t *lo2, int64_t *nitems2, cudaStream_t s) {
+    if (nblocks == 0) return;
+    SNN_LAUNCH(truncate_windows_kernel, (int)ceil_div(nblocks, 256), 256, 0, s, blk_lo, blk_hi, nblocks, B, chunk,
+               lo2, nitems2);
 }
 
 }  // namespace snn

@@ -66,12 +66,16 @@ struct PassArgs {
     int32_t *parent;        // union-find parents
     int32_t *best;          // M_BORDER: smallest original id of a core neighbour (atomicMin)
     int32_t min_pts;        // M_COUNT: counts are only needed up to min_pts (early exit)
+    int64_t n_index = 0;    // M_UNION: number of index points (parent array length)
     // expanded-form SIMT filter (scan variant 3; nullptr = off): AoSoA4 rows with D+1
     // floats (centred coordinates, xbar c1h), the margin constants and mu_f
     const float *Xf = nullptr;
     double c1h = 1.0, r2h = 0.0;
     const float *mu_f = nullptr;
 };
+// DBSCAN union pass work list: window of block b clipped to start at its first position
+void launch_truncate_windows(const int64_t *blk_lo, const int64_t *blk_hi, int64_t nblocks, int B, int chunk,
+                             int64_t *lo2, int64_t *nitems2, cudaStream_t s);
 // filter rows for the expanded-form scan variant from the AoSoA4 sorted copy
 void launch_filter_rows(const float *Xs, int d, int64_t n, int64_t n_pad, const float *mu_f, double c1h, float *Xf,
                         cudaStream_t s);
