@@ -38,6 +38,7 @@ struct Options {
     int tc_f16 = 1;      // tensor-core operands FP16 (scaled) instead of TF32
     int tc_group = 32;   // query blocks per raster group (upper bound; L2 budget decides)
     int tc_gram_min_d = 128;   // Gram matrix on the tensor cores for d >= this
+    int window_all = 0;  // ablation "brute force 2": windows = all points
     int simt_filter = 0; // low-d fp32 scan: expanded-form SIMT pre-filter (option; measured slower on c2/c5)
     int lowd_tc = 0;     // low-d (fp32, d <= 8) radius queries through the tensor-core filter (option; FFMA default)
     int lowd_tc_tiles = 8;     // 256-candidate tiles per work item (low-d tensor-core path)
@@ -270,7 +271,7 @@ snn_status snn_set_option(const char *key, int64_t value) {
         return SNN_OK;
     }
     if (k == "tc_diag") {   // performance diagnostics only: results are NOT valid
-        if (value < 0 || value > 4) return fail(SNN_ERR_INVALID_ARGUMENT, "tc_diag must be 0..4");
+        if (value < 0 || value > 2) return fail(SNN_ERR_INVALID_ARGUMENT, "tc_diag must be 0..2");
         g_opt.tc_diag = (int)value;
         return SNN_OK;
     }
@@ -280,6 +281,7 @@ snn_status snn_set_option(const char *key, int64_t value) {
         g_opt.tc_gram_min_d = (int)value;
         return SNN_OK;
     }
+    if (k == "window_all") { g_opt.window_all = value > 0 ? 1 : 0; return SNN_OK; }
     if (k == "simt_filter") { g_opt.simt_filter = value > 0 ? 1 : 0; return SNN_OK; }   // 0: default (off)
     if (k == "lowd_tc") { g_opt.lowd_tc = value > 0 ? 1 : 0; return SNN_OK; }   // 0: default (off)
     if (k == "lowd_tc_tiles") {
@@ -592,6 +594,7 @@ static snn_status query_tc(snn_index idx, Workspace &ws, cudaStream_t s, int sms
     w.ex = idx->stats + (f64 ? ST_EX_D : ST_EX_F);
     w.eq = eq;
     w.chunk = chunk;
+    w.all = g_opt.window_all;
     w.blk_lo = blk_lo; w.blk_hi = blk_hi; w.nitems = nitems; w.pairs = wpairs;
     launch_block_windows(w, s);                                                    // K7
     CK(ws.alloc(&scan_tmp, scan_temp_bytes(m > nblocks ? m : nblocks) + 4096), "alloc");
@@ -741,6 +744,7 @@ static snn_status query_tcl(snn_index idx, Workspace &ws, cudaStream_t s, int sm
     w.ex = idx->stats + ST_EX_F;
     w.eq = eq;
     w.chunk = chunk;
+    w.all = g_opt.window_all;
     w.blk_lo = blk_lo; w.blk_hi = blk_hi; w.nitems = nitems; w.pairs = wpairs;
     launch_block_windows(w, s);                                                    // K7
     launch_tcl_items(blk_lo, blk_hi, nblocks, (int)G, chunk, bcount, s);
@@ -951,6 +955,7 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
     w.ex = idx->stats + (f64 ? ST_EX_D : ST_EX_F);
     w.eq = eq;
     w.chunk = chunk;
+    w.all = g_opt.window_all;
     w.blk_lo = blk_lo; w.blk_hi = blk_hi; w.nitems = nitems; w.pairs = pairs;
     launch_block_windows(w, s);                                                    // K7
     exclusive_scan_i64(nitems, item_start, nblocks, scan_tmp, s);

@@ -61,6 +61,7 @@ __global__ void block_windows(WindowSpec w) {
     const float hi_key = __fadd_ru(w.qkeys[s1], rpf);
     int64_t lo = lower_bound_f(w.keys, w.n, lo_key);
     int64_t hi = upper_bound_f(w.keys, w.n, hi_key);
+    if (w.all) { lo = 0; hi = w.n; }   // ablation: no pruning
     const int64_t al = w.align > 4 ? w.align : 4;   // >= 4: 16-byte aligned bulk copies
     lo -= lo % al;
     hi = min(round_up(hi, al), w.n_pad);

@@ -25,6 +25,7 @@ struct WindowSpec {
     const double *eq;       // device scalar E_q (query key error bound)
     int chunk;              // candidates per work item (multiple of 4)
     int align = 4;          // window bounds rounded out to multiples of this (>= 4)
+    int all = 0;            // ablation ("brute force 2"): window = every point
     int64_t *blk_lo, *blk_hi, *nitems;   // outputs, nblocks each
     unsigned long long *pairs;           // += sum over blocks of |window| x queries (zeroed)
 };

@@ -198,14 +198,11 @@ tc_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 tc_fence_after();
                 int nh = 0;
                 const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + acc * TN + slice * COLS;
+                const int nch = a.diag == 1 ? 0 : COLS / 32;   // diag 1: no epilogue work
 #pragma unroll 1
-                for (int ch = 0; ch < (a.diag == 1 ? 0 : COLS / 32); ++ch) {
+                for (int ch = 0; ch < nch; ++ch) {
                     float v[32];
                     tmem_ld32(taddr + ch * 32, v);
-                    if (a.diag == 3) {   // diagnostics: TMEM read only
-                        if (v[0] == 12345.f && v[31] == 1.f) nh = 1;
-                        continue;
-                    }
                     const float4 *a4 = reinterpret_cast<const float4 *>(av + ch * 32);
 #pragma unroll
                     for (int c4 = 0; c4 < 8; ++c4) {   // v = acc - xbar (1 - c1/2)
@@ -222,7 +219,7 @@ tc_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 #pragma unroll
                     for (int c = 0; c < 3; ++c) m[c] = fmaxf(fmaxf(m[3 * c], m[3 * c + 1]), m[3 * c + 2]);
                     const float mx = fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[9] > m[10] ? m[9] : m[10]));
-                    if (mx >= bi && a.diag != 4) {
+                    if (mx >= bi) {
                         // rare (per lane): candidate mask, then one staged entry per set bit
                         uint32_t mask = 0;
 #pragma unroll

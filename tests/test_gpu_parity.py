@@ -493,6 +493,24 @@ def test_lowd_tensor_core_raster_options(snn, tiles, group):
         p.snn_set_option("lowd_tc_group", 0)
 
 
+@pytest.mark.parametrize("d", [3, 64])
+def test_window_all_ablation_identical(snn, d):
+    """'Brute force 2' ablation (window = every point): identical CSR."""
+    import paper_2212_07679_b200 as p
+    rng = np.random.default_rng(d)
+    X = rng.standard_normal((6000, d)).astype(np.float32)
+    Q = rng.standard_normal((700, d)).astype(np.float32)
+    R = float(np.sqrt(d)) * 0.6
+    a = run(snn, X, Q, R)
+    try:
+        p.snn_set_option("window_all", 1)
+        b = run(snn, X, Q, R)
+    finally:
+        p.snn_set_option("window_all", 0)
+    assert np.array_equal(a.offsets, b.offsets) and np.array_equal(a.indices, b.indices)
+    assert np.array_equal(a.distances, b.distances)
+
+
 @pytest.mark.parametrize("nbig", [300, 3000, 20000])
 def test_tc_csr_row_sizes(snn, nbig):
     """Rows of every size class of the CSR row sort (registers <= 32, warp <= 512,
