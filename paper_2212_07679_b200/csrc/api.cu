@@ -36,6 +36,7 @@ struct Options {
     int tc_tiles = 8;    // 256-candidate tiles per work item on the tensor-core path
     int tc_diag = 0;     // diagnostics only (results invalid): 1 = no epilogue work, 2 = no MMA
     int tc_f16 = 1;      // tensor-core operands FP16 (scaled) instead of TF32
+    int tc_ares = 1;     // K9: query tile resident per work item when K is one block
     int tc_group = 32;   // query blocks per raster group (upper bound; L2 budget decides)
     int tc_gram_min_d = 128;   // Gram matrix on the tensor cores for d >= this
     int window_all = 0;  // ablation "brute force 2": windows = all points
@@ -296,6 +297,7 @@ snn_status snn_set_option(const char *key, int64_t value) {
         g_opt.lowd_tc_group = (int)value;
         return SNN_OK;
     }
+    if (k == "tc_ares") { g_opt.tc_ares = value < 0 ? 0 : 1; return SNN_OK; }
     if (k == "tc_f16") { g_opt.tc_f16 = value < 0 ? 0 : 1; return SNN_OK; }
     if (k == "tc_group") {
         if (value == 0) value = 32;
@@ -660,6 +662,7 @@ static snn_status query_tc(snn_index idx, Workspace &ws, cudaStream_t s, int sms
     t.nblocks = nblocks; t.total_items = total_items; t.chunk = chunk;
     t.sc = f16 ? ldexpf(1.0f, idx->xexp + qexp) : 1.0f;
     t.diag = g_opt.tc_diag;
+    t.ares = g_opt.tc_ares;
     {
         const double c1h = 1.0 - c1 / 2;
         const double r2h = (R * R * (1.0 + 1e-12) * (1.0 + ldexp(1.0, -20)) + c0) / 2;

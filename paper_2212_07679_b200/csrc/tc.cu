@@ -49,6 +49,10 @@ constexpr int EPI = 512;                           // epilogue threads (16 warps
 constexpr int COLS = TN / (EPI / 128);             // columns per epilogue thread
 constexpr int THREADS = 64 + EPI;
 constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + ARING * TN * 4 + EPI * STAGE_CAP * 4 + 512;
+// ARES (one K block): the query tile is loaded once per work item into one of two
+// resident slots; the ring then streams only candidate tiles (a third fewer operand bytes)
+constexpr int STAGES_R = 5;
+constexpr int SMEM_BYTES_R = 1024 + STAGES_R * B_BYTES + 2 * A_BYTES + ARING * TN * 4 + EPI * STAGE_CAP * 4 + 512;
 // instruction descriptor: D format F32; A, B format F16 (0, kind::f16) or TF32 (2,
 // kind::tf32); both K-major; N >> 3 at bit 17, M >> 4 at bit 24
 template <bool F16>
@@ -84,26 +88,32 @@ __device__ __forceinline__ void tc_locate(const TcArgs &a, int64_t item, int64_t
     if (c1 < c0) c1 = c0;
 }
 
-template <bool F16>
+template <bool F16, bool ARES>
 __global__ void __launch_bounds__(THREADS, 1)
 tc_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcArgs a) {
     constexpr int TK = k_elems<F16>();
+    constexpr int NST = ARES ? STAGES_R : STAGES;              // ring stages
+    constexpr int SB = ARES ? B_BYTES : STAGE_BYTES;           // bytes per ring stage
+    constexpr int RING = NST * SB + (ARES ? 2 * A_BYTES : 0);  // ring (+ resident query slots)
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
     uint8_t *gbase = smem_raw + (base - raw);
-    // carve: stages | a_vals[ARING][TN] | stage hits [EPI][STAGE_CAP] | barriers | tmem ptr
-    float *a_vals = reinterpret_cast<float *>(gbase + STAGES * STAGE_BYTES);
-    int32_t *s_hits = reinterpret_cast<int32_t *>(gbase + STAGES * STAGE_BYTES + ARING * TN * 4);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(gbase + STAGES * STAGE_BYTES + ARING * TN * 4 + EPI * STAGE_CAP * 4);
-    uint64_t *full = bars, *empty = bars + STAGES, *tfull = bars + 2 * STAGES, *tempty = bars + 2 * STAGES + 2;
-    uint64_t *afull = bars + 2 * STAGES + 4, *aempty = bars + 2 * STAGES + 4 + ARING;
-    uint32_t *tmem_ptr = reinterpret_cast<uint32_t *>(bars + 2 * STAGES + 4 + 2 * ARING);
+    // carve: stages [| query slots] | a_vals[ARING][TN] | stage hits [EPI][STAGE_CAP] | barriers | tmem ptr
+    const uint32_t qbase = base + NST * SB;   // ARES: resident query tiles
+    float *a_vals = reinterpret_cast<float *>(gbase + RING);
+    int32_t *s_hits = reinterpret_cast<int32_t *>(gbase + RING + ARING * TN * 4);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(gbase + RING + ARING * TN * 4 + EPI * STAGE_CAP * 4);
+    uint64_t *full = bars, *empty = bars + NST, *tfull = bars + 2 * NST, *tempty = bars + 2 * NST + 2;
+    uint64_t *afull = bars + 2 * NST + 4, *aempty = bars + 2 * NST + 4 + ARING;
+    uint64_t *qfull = bars + 2 * NST + 4 + 2 * ARING, *qempty = qfull + 2;
+    uint32_t *tmem_ptr = reinterpret_cast<uint32_t *>(qfull + 4);
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
         for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], EPI); }
+        for (int s = 0; s < 2; ++s) { mbar_init(&qfull[s], 1); mbar_init(&qempty[s], 1); }
         for (int s = 0; s < ARING; ++s) { mbar_init(&afull[s], 1); mbar_init(&aempty[s], EPI); }
         fence_mbar_init();
     }
@@ -121,11 +131,18 @@ tc_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         if (lane == 0) {
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
-            int stage = 0;
-            uint32_t phase = 0, aslot = 0, aph = 0;
+            int stage = 0, qs = 0;
+            uint32_t phase = 0, aslot = 0, aph = 0, qph = 0;
             for (int64_t item = blockIdx.x; item < a.total_items; item += gridDim.x) {
                 int64_t b, c0, c1;
                 tc_locate(a, item, b, c0, c1);
+                if (ARES) {
+                    if (c1 <= c0) continue;
+                    mbar_wait_u32(smem_u32(&qempty[qs]), qph ^ 1);
+                    mbar_arrive_expect_tx(&qfull[qs], A_BYTES);
+                    tma_load_2d(qbase + qs * A_BYTES, &tmA, smem_u32(&qfull[qs]), 0, (int)(b * TM));
+                    if (++qs == 2) { qs = 0; qph ^= 1; }
+                }
                 for (int64_t t0 = c0; t0 < c1; t0 += TN) {
                     // x-bar slice of this tile -> a-ring slot (read by the epilogue)
                     mbar_wait_u32(smem_u32(&aempty[aslot]), aph ^ 1);
@@ -134,11 +151,11 @@ tc_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     if (++aslot == ARING) { aslot = 0; aph ^= 1; }
                     for (int kb = 0; kb < a.kblocks; ++kb) {
                         mbar_wait_u32(smem_u32(&empty[stage]), phase ^ 1);
-                        const uint32_t sa = base + stage * STAGE_BYTES, sb = sa + A_BYTES;
-                        mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
-                        tma_load_2d(sa, &tmA, smem_u32(&full[stage]), kb * TK, (int)(b * TM));
+                        const uint32_t sa = base + stage * SB, sb = ARES ? sa : sa + A_BYTES;
+                        mbar_arrive_expect_tx(&full[stage], SB);
+                        if (!ARES) tma_load_2d(sa, &tmA, smem_u32(&full[stage]), kb * TK, (int)(b * TM));
                         tma_load_2d(sb, &tmB, smem_u32(&full[stage]), kb * TK, (int)t0);
-                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                        if (++stage == NST) { stage = 0; phase ^= 1; }
                     }
                 }
             }
@@ -146,11 +163,16 @@ tc_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
         if (lane == 0) {
-            int stage = 0;
-            uint32_t phase = 0, acc = 0, aphase = 0;
+            int stage = 0, qs = 0;
+            uint32_t phase = 0, acc = 0, aphase = 0, qph = 0;
             for (int64_t item = blockIdx.x; item < a.total_items; item += gridDim.x) {
                 int64_t b, c0, c1;
                 tc_locate(a, item, b, c0, c1);
+                if (ARES) {
+                    if (c1 <= c0) continue;
+                    mbar_wait_u32(smem_u32(&qfull[qs]), qph);
+                    tc_fence_after();
+                }
                 for (int64_t t0 = c0; t0 < c1; t0 += TN) {
                     mbar_wait_u32(smem_u32(&tempty[acc]), aphase ^ 1);
                     tc_fence_after();
@@ -158,7 +180,8 @@ tc_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     for (int kb = 0; kb < a.kblocks; ++kb) {
                         mbar_wait_u32(smem_u32(&full[stage]), phase);
                         tc_fence_after();
-                        const uint32_t sa = base + stage * STAGE_BYTES, sb = sa + A_BYTES;
+                        const uint32_t sa = ARES ? qbase + qs * A_BYTES : base + stage * SB;
+                        const uint32_t sb = ARES ? base + stage * SB : sa + A_BYTES;
                         const uint64_t da = sw128_desc(sa), db = sw128_desc(sb);
                         if (a.diag != 2) {
 #pragma unroll
@@ -166,11 +189,15 @@ tc_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                                 mma_op<F16>(dcol, da + 2 * kk, db + 2 * kk, (kb | kk) != 0);
                         }
                         mma_commit(smem_u32(&empty[stage]));
-                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                        if (++stage == NST) { stage = 0; phase ^= 1; }
                     }
                     mma_commit(smem_u32(&tfull[acc]));
                     acc ^= 1;
                     if (acc == 0) aphase ^= 1;
+                }
+                if (ARES) {   // the query slot is free once this item's MMAs retire
+                    mma_commit(smem_u32(&qempty[qs]));
+                    if (++qs == 2) { qs = 0; qph ^= 1; }
                 }
             }
         }
@@ -433,13 +460,15 @@ bool launch_tc_window(const void *Qt, const void *Xt, bool f16, const TcArgs &a,
     CUtensorMap ma, mb;
     if (!make_map(&ma, Qt, f16, a.m, a.kpad, TM) || !make_map(&mb, Xt, f16, a.n, a.kpad, TN)) return false;
     int g = (int)(a.total_items < sm_count ? a.total_items : sm_count);
-    if (f16) {
-        cudaFuncSetAttribute(tc_window_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-        SNN_LAUNCH(tc_window_kernel<true>, g, THREADS, SMEM_BYTES, s, ma, mb, a);
-    } else {
-        cudaFuncSetAttribute(tc_window_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-        SNN_LAUNCH(tc_window_kernel<false>, g, THREADS, SMEM_BYTES, s, ma, mb, a);
-    }
+    const bool ares = a.kblocks == 1 && a.ares;
+#define TCW(F, R, SM)                                                                               \
+    do {                                                                                            \
+        cudaFuncSetAttribute(tc_window_kernel<F, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM); \
+        SNN_LAUNCH((tc_window_kernel<F, R>), g, THREADS, SM, s, ma, mb, a);                          \
+    } while (0)
+    if (f16) { if (ares) TCW(true, true, SMEM_BYTES_R); else TCW(true, false, SMEM_BYTES); }
+    else { if (ares) TCW(false, true, SMEM_BYTES_R); else TCW(false, false, SMEM_BYTES); }
+#undef TCW
     return true;
 }
 

@@ -22,6 +22,7 @@ struct TcArgs {
     unsigned long long *pair_count;
     int64_t pair_cap;
     int diag;               // 0; diagnostics: 1 = skip epilogue work, 2 = skip MMAs
+    int ares;               // resident query tile per work item when K fits one block
 };
 
 int tc_tile_rows();   // queries per tile (128)

@@ -549,9 +549,12 @@ def test_tc_tile_edges_and_tiles_option(snn):
     try:
         for f16 in (1, -1):
             p.snn_set_option("tc_f16", f16)
-            for tiles in (1, 3, 8):
-                p.snn_set_option("tc_tiles", tiles)
-                compare(run(snn, X, Q, 9.5), ora)
+            for ares in (1, -1):
+                p.snn_set_option("tc_ares", ares)
+                for tiles in (1, 3, 8):
+                    p.snn_set_option("tc_tiles", tiles)
+                    compare(run(snn, X, Q, 9.5), ora)
     finally:
         p.snn_set_option("tc_tiles", 0)
         p.snn_set_option("tc_f16", 0)
+        p.snn_set_option("tc_ares", 0)
