@@ -8,7 +8,8 @@
 // windowed classification of the radius query (bit-identical to the fp64 oracle).
 //
 // Pipeline on the sorted index (neighbour lists are never materialised):
-//   windows (K7, R = eps) -> M_COUNT pass -> per-point counts -> core flags
+//   windows (K7, R = eps) -> core counts (chunks in order per block, early exit once
+//   every point of the block has min_pts neighbours) -> core flags
 //   -> M_UNION pass (core i, core j > i: lock-free union-find) -> flatten
 //   -> per-root smallest original id -> flag + scan over original ids = canonical ranks
 //   -> core labels -> M_BORDER pass (non-core points) -> labels scattered to original order.
@@ -192,9 +193,8 @@ snn_status dbscan_impl(snn_index idx, double eps, int32_t min_pts, int32_t *labe
     CKD(cudaStreamSynchronize(s), "dbscan pairs");
     const double pairs_eval = (double)*hp_pairs;
     const int ctok = prof_begin(F_COUNT, s);
-    launch_lowd_mode(2, a, s);                                              // counts
+    launch_core_counts(a, count, s);                                        // counts (to min_pts)
     prof_end(ctok, s, pairs_eval);
-    launch_row_totals(cnt, cnt, item_start, n, B, nullptr, count, s);
     SNN_LAUNCH(init_core, grid_n(n), 256, 0, s, count, n, min_pts, core, parent, minid, best);
     {   // unions over the clipped windows (pairs j > i only: block b starts at its first position)
         int64_t *lo2, *nit2, *st2;

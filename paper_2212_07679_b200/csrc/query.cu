@@ -894,4 +894,118 @@ void launch_truncate_windows(const int64_t *blk_lo, const int64_t *blk_hi, int64
                lo2, nitems2);
 }
 
+namespace {
+// DBSCAN core flags need |N_eps(i)| only up to min_pts.  One CTA per query block walks
+// the block's candidate chunks in order (TMA double buffer) and stops as soon as every
+// query of the block has min_pts hits (config 5: the first chunk usually suffices);
+// same exact classification as the radius query.  count = min(|N_eps|, >= min_pts).
+template <typename T, int D>
+__global__ void __launch_bounds__(256) core_count_kernel(PassArgs a, int32_t *count) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int tid = threadIdx.x;
+    const T *Xs = static_cast<const T *>(a.Xs);
+    const size_t buf_bytes = (size_t)a.chunk * D * sizeof(T);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + 2 * buf_bytes);
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    auto issue = [&](int64_t item, int sidx) {
+        int64_t b, c0, c1;
+        locate(a, item, b, c0, c1);
+        const uint32_t bytes = (uint32_t)((c1 - c0) * D * sizeof(T));
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&bar[sidx], bytes);
+        bulk_g2s(smem + sidx * buf_bytes, Xs + c0 * D, bytes, &bar[sidx]);
+    };
+    uint32_t phase[2] = {0u, 0u};
+    const float T_in = a.T_in, T_out = a.T_out;
+    const double R2 = a.R2;
+    const int32_t mp = a.min_pts;
+    for (int64_t b = blockIdx.x; b < a.nblocks; b += gridDim.x) {
+        const int64_t sp = b * a.B + tid;
+        const bool active = sp < a.m;
+        T q[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) q[k] = active ? Xs[(sp >> 2) * 4 * D + k * 4 + (sp & 3)] : (T)0;
+        const int64_t i0 = a.item_start[b], i1 = a.item_start[b + 1];
+        int32_t c = 0;
+        if (tid == 0 && i0 < i1) issue(i0, 0);
+        for (int64_t item = i0; item < i1; ++item) {
+            const int sidx = (int)((item - i0) & 1);
+            if (tid == 0 && item + 1 < i1) issue(item + 1, sidx ^ 1);
+            int64_t bb, c0, c1;
+            locate(a, item, bb, c0, c1);
+            mbar_wait(&bar[sidx], phase[sidx]);
+            phase[sidx] ^= 1u;
+            if (active && c < mp) {
+                const int ngroups = (int)((c1 - c0) >> 2);
+                if constexpr (sizeof(T) == 4) {
+                    const float4 *g4 = reinterpret_cast<const float4 *>(smem + sidx * buf_bytes);
+                    uint64_t nq[D];
+#pragma unroll
+                    for (int k = 0; k < D; ++k) nq[k] = f2pack(-q[k], -q[k]);
+                    for (int g = 0; g < ngroups && c < mp; ++g) {
+                        float4 xa[D];
+#pragma unroll
+                        for (int k = 0; k < D; ++k) xa[k] = g4[g * D + k];
+                        uint64_t la, ha;
+                        group_d2<D>(xa, nq, la, ha);
+                        const float2 pa = f2unpack(la), qa = f2unpack(ha);
+                        if (fminf(fminf(pa.x, pa.y), fminf(qa.x, qa.y)) <= T_out) {
+                            uint32_t ia = mask4(pa.x, pa.y, qa.x, qa.y, T_in);
+                            const uint32_t oa = mask4(pa.x, pa.y, qa.x, qa.y, T_out);
+                            if (ia ^ oa) ia |= resolve4<D>(oa & ~ia, xa, q, R2);
+                            c += __popc(ia);
+                        }
+                    }
+                } else {
+                    const T *gb = reinterpret_cast<const T *>(smem + sidx * buf_bytes);
+                    for (int g = 0; g < ngroups && c < mp; ++g) {
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            double s2 = 0.0;
+#pragma unroll
+                            for (int k = 0; k < D; ++k) {
+                                const double t = __dsub_rn(gb[g * 4 * D + k * 4 + i], q[k]);
+                                s2 = __dadd_rn(s2, __dmul_rn(t, t));
+                            }
+                            c += s2 <= R2;
+                        }
+                    }
+                }
+            }
+            if (!__syncthreads_or(active && c < mp)) {   // every query of the block is decided
+                if (item + 1 < i1) {                       // drain the prefetched chunk
+                    const int ns = sidx ^ 1;
+                    mbar_wait(&bar[ns], phase[ns]);
+                    phase[ns] ^= 1u;
+                }
+                break;
+            }
+        }
+        if (active) count[sp] = c;
+        __syncthreads();
+    }
+}
+
+template <typename T, int D>
+void run_core_count(const PassArgs &a, int32_t *count, cudaStream_t s) {
+    const size_t smem = (size_t)2 * a.chunk * D * sizeof(T) + 16;
+    auto k = core_count_kernel<T, D>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int g = persistent_grid(k, a.B, smem, a.nblocks, a.sm_count);
+    SNN_LAUNCH(k, g, a.B, smem, s, a, count);
+}
+}  // namespace
+
+void launch_core_counts(const PassArgs &a, int32_t *count, cudaStream_t s) {
+    if (a.nblocks == 0) return;
+#define FN(T, D) run_core_count<T, D>(a, count, s)
+    SNN_LOWD_DISPATCH(FN)
+#undef FN
+}
+
 }  // namespace snn

@@ -74,6 +74,9 @@ struct PassArgs {
     double c1h = 1.0, r2h = 0.0;
     const float *mu_f = nullptr;
 };
+// DBSCAN core counts with early exit: count[sp] = |N_eps| if < min_pts, else some value
+// >= min_pts (one CTA per query block, chunks in order, stop when the block is decided)
+void launch_core_counts(const PassArgs &a, int32_t *count, cudaStream_t s);
 // DBSCAN union pass work list: window of block b clipped to start at its first position
 void launch_truncate_windows(const int64_t *blk_lo, const int64_t *blk_hi, int64_t nblocks, int B, int chunk,
                              int64_t *lo2, int64_t *nitems2, cudaStream_t s);
