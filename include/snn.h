@@ -130,7 +130,10 @@ void snn_result_free(snn_result r); /* NULL ok */
  * eps-adjacency; a non-core point with a core neighbour takes the cluster of its
  * smallest-id core neighbour; others are noise (-1); clusters are numbered 0..K-1 by
  * increasing smallest core id.  labels: n int32, host or device, ORIGINAL order.
- * *n_clusters (host) receives K.  The neighbour lists are never materialised.
+ * *n_clusters (host) receives K.  d <= 8: fused count / union / border passes over the
+ * candidate windows (neighbour lists are never materialised); larger d: the exact
+ * self-query CSR (snn_query_self) feeds the same count / union / border steps.
+ * Errors: NULL arguments, eps < 0 or non-finite, min_pts < 1 -> SNN_ERR_INVALID_ARGUMENT.
  */
 snn_status snn_dbscan(snn_index idx, double eps, int32_t min_pts, int32_t *labels,
                       int32_t *n_clusters, void *stream);

@@ -1138,7 +1138,17 @@ snn_status snn_dbscan(snn_index idx, double eps, int32_t min_pts, int32_t *label
     snn_status st = device_check(&sms);
     if (st != SNN_OK) return st;
     const int tok = prof_begin(F_DBSCAN, static_cast<cudaStream_t>(stream));
-    st = dbscan_impl(idx, eps, min_pts, labels, n_clusters, static_cast<cudaStream_t>(stream));
+    if (idx->ld == 0) {   // low d: fused passes over the windows, neighbour lists never built
+        st = dbscan_impl(idx, eps, min_pts, labels, n_clusters, static_cast<cudaStream_t>(stream));
+    } else {              // any d: DBSCAN over the exact self-query CSR
+        snn_result r = nullptr;
+        st = query_impl(idx, nullptr, idx->n, idx->d, idx->dt, eps, stream, &r);
+        if (st == SNN_OK) {
+            st = dbscan_from_csr(r->offsets, r->indices, idx->n, min_pts, labels, n_clusters,
+                                 static_cast<cudaStream_t>(stream));
+            snn_result_free(r);
+        }
+    }
     prof_end(tok, static_cast<cudaStream_t>(stream), (double)idx->n);
     return st;
 }

@@ -95,6 +95,71 @@ __global__ void gather_noncore(const uint8_t *core, const int64_t *pos, int64_t 
     }
 }
 
+// --- any d: DBSCAN over the exact self-query CSR (original order, original ids) -------
+__device__ __forceinline__ int32_t uf_find_c(volatile int32_t *p, int32_t x) {
+    int32_t cur = p[x];
+    if (cur != x) {
+        int32_t next, prev = x;
+        while (cur > (next = p[cur])) {
+            p[prev] = next;
+            prev = cur;
+            cur = next;
+        }
+    }
+    return cur;
+}
+__device__ __forceinline__ void uf_unite_c(int32_t *p, int32_t a, int32_t b) {
+    volatile int32_t *vp = p;
+    int32_t ra = uf_find_c(vp, a), rb = uf_find_c(vp, b);
+    while (ra != rb) {
+        if (ra < rb) { const int32_t t = ra; ra = rb; rb = t; }
+        const int32_t old = atomicCAS(&p[ra], ra, rb);
+        if (old == ra) break;
+        ra = uf_find_c(vp, old);
+        rb = uf_find_c(vp, rb);
+    }
+}
+
+__global__ void csr_counts(const int64_t *off, int64_t n, int32_t *count) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        count[i] = (int32_t)min((int64_t)0x7fffffff, off[i + 1] - off[i]);
+}
+
+// warp per row: union core i with every core neighbour j > i
+__global__ void csr_union(const int64_t *off, const int32_t *idx, const uint8_t *core, int64_t n, int32_t *parent) {
+    const int lane = threadIdx.x % 32;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; i < n;
+         i += (int64_t)gridDim.x * blockDim.x / 32) {
+        if (!core[i]) continue;
+        for (int64_t k = off[i] + lane; k < off[i + 1]; k += 32) {
+            const int32_t j = idx[k];
+            if (j > i && core[j]) uf_unite_c(parent, (int32_t)i, j);
+        }
+    }
+}
+
+// warp per non-core row: smallest original id among core neighbours
+__global__ void csr_border(const int64_t *off, const int32_t *idx, const uint8_t *core, int64_t n, int32_t *best) {
+    const int lane = threadIdx.x % 32;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; i < n;
+         i += (int64_t)gridDim.x * blockDim.x / 32) {
+        if (core[i]) continue;
+        int32_t b = 0x7fffffff;
+        for (int64_t k = off[i] + lane; k < off[i + 1]; k += 32) {
+            const int32_t j = idx[k];
+            if (core[j]) b = min(b, j);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) b = min(b, __shfl_xor_sync(0xffffffffu, b, o));
+        if (lane == 0) best[i] = b;
+    }
+}
+
+__global__ void iota32(int32_t *p, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = (int32_t)i;
+}
+
 int grid_n(int64_t n) {
     int64_t g = ceil_div(n, 256);
     return (int)(g < 148 * 16 ? (g < 1 ? 1 : g) : 148 * 16);
@@ -104,8 +169,6 @@ int grid_n(int64_t n) {
 
 snn_status dbscan_impl(snn_index idx, double eps, int32_t min_pts, int32_t *labels,
                        int32_t *n_clusters, cudaStream_t s) {
-    if (idx->ld != 0)
-        return fail(SNN_ERR_UNSUPPORTED, "snn_dbscan: only the low-d layout (d <= 8) is supported");
     const int64_t n = idx->n;
     const bool f64 = idx->dt == SNN_F64;
     const int B = 256, chunk = 2048;
@@ -261,6 +324,55 @@ snn_status dbscan_impl(snn_index idx, double eps, int32_t min_pts, int32_t *labe
     CKD(cudaGetLastError(), "launch");
     CKD(cudaStreamSynchronize(s), "dbscan");
     *n_clusters = (int32_t)hbuf[1];
+    return SNN_OK;
+#undef CKD
+}
+
+// DBSCAN for any d from the exact self-query CSR (rows and ids in original order): same
+// semantics and canonical numbering as the low-d pipeline (reading C18).
+snn_status dbscan_from_csr(const int64_t *off, const int32_t *nidx, int64_t n, int32_t min_pts, int32_t *labels,
+                           int32_t *n_clusters, cudaStream_t s) {
+    Workspace ws(s);
+#define CKD(expr, where)                                       \
+    do {                                                       \
+        cudaError_t _e = (expr);                               \
+        if (_e != cudaSuccess) return cuda_fail(_e, where);    \
+    } while (0)
+    int32_t *count, *parent, *minid, *best, *flag, *lab, *inv, *out, *iota;
+    int64_t *rank, *hbuf;
+    uint8_t *core, *scan_tmp;
+    CKD(ws.alloc(&count, (size_t)n), "alloc");
+    CKD(ws.alloc(&core, (size_t)n), "alloc");
+    CKD(ws.alloc(&parent, (size_t)n), "alloc");
+    CKD(ws.alloc(&minid, (size_t)n), "alloc");
+    CKD(ws.alloc(&best, (size_t)n), "alloc");
+    CKD(ws.alloc(&flag, (size_t)n), "alloc");
+    CKD(ws.alloc(&rank, (size_t)n + 1), "alloc");
+    CKD(ws.alloc(&lab, (size_t)n), "alloc");
+    CKD(ws.alloc(&inv, (size_t)n), "alloc");
+    CKD(ws.alloc(&iota, (size_t)n), "alloc");
+    CKD(ws.alloc(&scan_tmp, scan_temp_bytes(n)), "alloc");
+    CKD(cudaMallocHost(&hbuf, 16), "pinned");
+    struct HostFree { void *p; ~HostFree() { cudaFreeHost(p); } } hf{hbuf};
+    const bool dev_out = is_device_ptr(labels);
+    if (dev_out) out = labels; else CKD(ws.alloc(&out, (size_t)n), "alloc");
+    const int g = grid_n(n), gw = grid_n(n * 32);
+    SNN_LAUNCH(iota32, g, 256, 0, s, iota, n);
+    SNN_LAUNCH(csr_counts, g, 256, 0, s, off, n, count);
+    SNN_LAUNCH(init_core, g, 256, 0, s, count, n, min_pts, core, parent, minid, best);
+    SNN_LAUNCH(csr_union, gw, 256, 0, s, off, nidx, core, n, parent);
+    SNN_LAUNCH(flatten, g, 256, 0, s, parent, core, iota, n, minid);
+    CKD(cudaMemsetAsync(flag, 0, (size_t)n * 4, s), "memset");
+    SNN_LAUNCH(flag_roots, g, 256, 0, s, parent, core, minid, n, flag);
+    exclusive_scan_i32_to_i64(flag, rank, n, scan_tmp, s);
+    SNN_LAUNCH(core_labels, g, 256, 0, s, parent, core, minid, rank, iota, n, lab, inv);
+    SNN_LAUNCH(csr_border, gw, 256, 0, s, off, nidx, core, n, best);
+    SNN_LAUNCH(final_labels, g, 256, 0, s, lab, core, best, inv, iota, n, out);
+    if (!dev_out) CKD(cudaMemcpyAsync(labels, out, (size_t)n * 4, cudaMemcpyDeviceToHost, s), "D2H labels");
+    CKD(cudaMemcpyAsync(hbuf, rank + n, 8, cudaMemcpyDeviceToHost, s), "D2H K");
+    CKD(cudaGetLastError(), "launch");
+    CKD(cudaStreamSynchronize(s), "dbscan");
+    *n_clusters = (int32_t)hbuf[0];
     return SNN_OK;
 #undef CKD
 }

@@ -80,6 +80,8 @@ struct snn_result_s {
 
 namespace snn {
 bool dbscan_simt_filter();   // option simt_filter (api.cu)
+snn_status dbscan_from_csr(const int64_t *off, const int32_t *nidx, int64_t n, int32_t min_pts, int32_t *labels,
+                           int32_t *n_clusters, cudaStream_t s);
 snn_status dbscan_impl(snn_index idx, double eps, int32_t min_pts, int32_t *labels,
                        int32_t *n_clusters, cudaStream_t s);
 }

@@ -344,6 +344,20 @@ def test_dbscan_full_parity(snn, n, seed, box, eps, mp, dt):
     assert np.array_equal(lab, ref)
 
 
+@pytest.mark.parametrize("d,dt", [(16, np.float32), (40, np.float32), (12, np.float64)])
+def test_dbscan_high_d_parity(snn, d, dt):
+    """d > 8: DBSCAN over the exact self-query CSR; labels equal the oracle's."""
+    rng = np.random.default_rng(d)
+    centers = rng.standard_normal((6, d)) * 6
+    X = np.concatenate([centers[rng.integers(0, 6, 3000)] + rng.standard_normal((3000, d)) * 0.6,
+                        rng.standard_normal((300, d)) * 8]).astype(dt)
+    eps = float(np.sqrt(d) * 0.55)
+    lab, K = _gpu_dbscan(snn, X, eps, 6)
+    ref, Kr, _ = oracle.dbscan(X, eps, 6)
+    assert K == Kr and K >= 2
+    assert np.array_equal(lab, ref)
+
+
 def test_dbscan_c5_full_size_sampled(snn):
     """BASELINE config 5 at full size (n = 2M): sampled points checked one by one."""
     w = workloads.c5()
