@@ -37,8 +37,8 @@ struct Options {
     int tc_diag = 0;     // diagnostics only (results invalid): 1 = no epilogue work, 2 = no MMA
     int tc_f16 = 1;      // tensor-core operands FP16 (scaled) instead of TF32
     int tc_ares = 1;     // K9: query tile resident per work item when K is one block
-    int tc_group = 32;   // query blocks per raster group (upper bound; L2 budget decides)
-    int tc_gram_min_d = 128;   // Gram matrix on the tensor cores for d >= this
+    int tc_group = 128;  // query blocks per raster group (upper bound; L2 budget decides)
+    int tc_gram_min_d = 32;    // Gram matrix on the tensor cores for d >= this
     int window_all = 0;  // ablation "brute force 2": windows = all points
     int simt_filter = 0; // low-d fp32 scan: expanded-form SIMT pre-filter (option; measured slower on c2/c5)
     int lowd_tc = 0;     // low-d (fp32, d <= 8) radius queries through the tensor-core filter (option; FFMA default)
@@ -277,7 +277,7 @@ snn_status snn_set_option(const char *key, int64_t value) {
         return SNN_OK;
     }
     if (k == "tc_gram_min_d") {
-        if (value == 0) value = 128;
+        if (value == 0) value = 32;
         if (value < 1) return fail(SNN_ERR_INVALID_ARGUMENT, "tc_gram_min_d must be >= 1");
         g_opt.tc_gram_min_d = (int)value;
         return SNN_OK;
@@ -300,7 +300,7 @@ snn_status snn_set_option(const char *key, int64_t value) {
     if (k == "tc_ares") { g_opt.tc_ares = value < 0 ? 0 : 1; return SNN_OK; }
     if (k == "tc_f16") { g_opt.tc_f16 = value < 0 ? 0 : 1; return SNN_OK; }
     if (k == "tc_group") {
-        if (value == 0) value = 32;
+        if (value == 0) value = 128;
         if (value < 1 || value > 1 << 20) return fail(SNN_ERR_INVALID_ARGUMENT, "tc_group must be >= 1");
         g_opt.tc_group = (int)value;
         return SNN_OK;
