@@ -39,6 +39,7 @@ struct Options {
     int tc_ares = 1;     // K9: query tile resident per work item when K is one block
     int tc_group = 128;  // query blocks per raster group (upper bound; L2 budget decides)
     int tc_gram_min_d = 32;    // Gram matrix on the tensor cores for d >= this
+    int symmetric = 1;   // low-d self-queries: each unordered pair evaluated once
     int window_all = 0;  // ablation "brute force 2": windows = all points
     int simt_filter = 0; // low-d fp32 scan: expanded-form SIMT pre-filter (option; measured slower on c2/c5)
     int lowd_tc = 0;     // low-d (fp32, d <= 8) radius queries through the tensor-core filter (option; FFMA default)
@@ -282,6 +283,7 @@ snn_status snn_set_option(const char *key, int64_t value) {
         g_opt.tc_gram_min_d = (int)value;
         return SNN_OK;
     }
+    if (k == "symmetric") { g_opt.symmetric = value < 0 ? 0 : 1; return SNN_OK; }
     if (k == "window_all") { g_opt.window_all = value > 0 ? 1 : 0; return SNN_OK; }
     if (k == "simt_filter") { g_opt.simt_filter = value > 0 ? 1 : 0; return SNN_OK; }   // 0: default (off)
     if (k == "lowd_tc") { g_opt.lowd_tc = value > 0 ? 1 : 0; return SNN_OK; }   // 0: default (off)
@@ -864,7 +866,7 @@ static snn_status query_tcl(snn_index idx, Workspace &ws, cudaStream_t s, int sm
 }
 
 static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d, snn_dtype dt,
-                             double R, void *stream, snn_result *out) {
+                             double R, void *stream, snn_result *out, bool allow_sym = true) {
     if (!out) return fail(SNN_ERR_INVALID_ARGUMENT, "NULL output handle");
     *out = nullptr;
     if (!idx) return fail(SNN_ERR_INVALID_ARGUMENT, "NULL index");
@@ -961,6 +963,14 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
     w.all = g_opt.window_all;
     w.blk_lo = blk_lo; w.blk_hi = blk_hi; w.nitems = nitems; w.pairs = pairs;
     launch_block_windows(w, s);                                                    // K7
+    // symmetric self-query: every unordered pair once -- block b scans only candidates
+    // from its own first position on (j > i); mirrored hits fill the L part of row j
+    const bool sym = self && !generic && allow_sym && g_opt.symmetric && !g_opt.window_all;
+    int64_t *blk_lo_s = blk_lo;
+    if (sym) {
+        CK(ws.alloc(&blk_lo_s, (size_t)nblocks), "alloc");
+        launch_truncate_windows(blk_lo, blk_hi, nblocks, B, chunk, blk_lo_s, nitems, s);
+    }
     exclusive_scan_i64(nitems, item_start, nblocks, scan_tmp, s);
     int64_t *hp = static_cast<int64_t *>(t_pinned.p);
     CK(cudaMemcpyAsync(hp, item_start + nblocks, 8, cudaMemcpyDeviceToHost, s), "D2H items");
@@ -999,10 +1009,20 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
     PassArgs a{};
     a.Xs = idx->Xs; a.Qs = Qs; a.ld = ld; a.d = D; a.f64 = f64; a.m = m;
     a.perm = idx->perm; a.qperm = qperm;
-    a.blk_lo = blk_lo; a.blk_hi = blk_hi; a.item_start = item_start;
+    a.blk_lo = blk_lo_s; a.blk_hi = blk_hi; a.item_start = item_start;
     a.nblocks = nblocks; a.total_items = total_items;
     a.B = B; a.chunk = chunk;
     a.R2 = R * R;
+    int32_t *maxl = nullptr;
+    if (sym) {
+        a.sym = 1;
+        CK(ws.alloc(&a.lcnt, (size_t)m), "alloc");
+        CK(ws.alloc(&a.lcur, (size_t)m), "alloc");
+        CK(ws.alloc(&maxl, 1), "alloc");
+        CK(cudaMemsetAsync(a.lcnt, 0, (size_t)m * 4, s), "memset");
+        CK(cudaMemsetAsync(a.lcur, 0, (size_t)m * 4, s), "memset");
+        CK(cudaMemsetAsync(maxl, 0, 4, s), "memset");
+    }
     thresholds(a.R2, D, &a.T_in, &a.T_out);
     a.cnt = cnt; a.pre = pre; a.slots = slots; a.cap = cap;
     a.ovf_items = ovf; a.ovf_count = ovf ? ovf + total_items : nullptr; a.n_ovf = 0;
@@ -1017,23 +1037,32 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
         a.Xf = idx->Xf; a.c1h = idx->xf_c1h; a.r2h = r2h; a.mu_f = idx->mu_f;
     }
     if (total_items == 0) {
-        cudaMemsetAsync(row_count, 0, (size_t)m * 4, s);
+        if (sym) launch_row_totals_sym(cnt, pre, item_start, m, B, qperm, a.lcnt, row_count, maxl, s);
+        else cudaMemsetAsync(row_count, 0, (size_t)m * 4, s);
     } else {
         const int ctok = prof_begin(F_COUNT, s);
         if (generic) launch_generic_pass(false, a, s);                           // K8 count
         else launch_lowd_scan(a, s);                                             // K8 scan
         prof_end(ctok, s, pairs_eval);
-        launch_row_totals(cnt, pre, item_start, m, B, qperm, row_count, s);      // K11
+        if (sym) launch_row_totals_sym(cnt, pre, item_start, m, B, qperm, a.lcnt, row_count, maxl, s);
+        else launch_row_totals(cnt, pre, item_start, m, B, qperm, row_count, s);  // K11
     }
     exclusive_scan_i32_to_i64(row_count, r->offsets, m, scan_tmp, s);
     {
         cudaError_t e = cudaMemcpyAsync(hp, r->offsets + m, 8, cudaMemcpyDeviceToHost, s);
         if (e == cudaSuccess && a.ovf_count)
             e = cudaMemcpyAsync(hp + 1, a.ovf_count, 8, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess && maxl) e = cudaMemcpyAsync(hp + 2, maxl, 4, cudaMemcpyDeviceToHost, s);
         if (e == cudaSuccess) e = cudaStreamSynchronize(s);
         if (e != cudaSuccess) return bail(e, "query count");
     }
     r->nnz = hp[0];
+    const int32_t max_l = sym ? *reinterpret_cast<int32_t *>(hp + 2) : 0;
+    if (sym && max_l > 16384) {   // a huge mirrored row: redo unsymmetric
+        snn_result_free(r);
+        prof_end(qtok, s, 0.0);
+        return query_impl(idx, Q, m, d, dt, R, stream, out, false);
+    }
     a.n_ovf = a.ovf_count ? reinterpret_cast<int32_t *>(hp + 1)[0] : 0;
     a.n_ovf_rec = a.ovf_count ? reinterpret_cast<int32_t *>(hp + 1)[1] : 0;
     {
@@ -1046,6 +1075,7 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
         r->distances = static_cast<float *>(p);
     }
     a.out_idx = r->indices; a.out_dist = r->distances;
+    if (sym) CK(ws.alloc(&a.tmpL, (size_t)(r->nnz > 0 ? r->nnz : 1)), "alloc mirrored entries");
     if (r->nnz > 0) {
         const int wtok = prof_begin(F_WRITE, s);
         if (generic) {
@@ -1053,6 +1083,7 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
         } else {
             launch_lowd_compact(a, s);                                           // K11 compact
             launch_lowd_fix(a, s);                                               // overflow fix
+            if (sym) launch_sym_lsort(a, max_l, s);                              // mirrored rows
         }
         prof_end(wtok, s, generic ? pairs_eval : (double)r->nnz);
     }

@@ -128,9 +128,26 @@ struct Emitter {
     const PassArgs &a;
     uint16_t *slot;
     int64_t e, c0, pos;
+    int64_t sp = 0;
     int32_t c = 0, rec = 0;
     bool lost = false;
+    // symmetric self-query: keep candidates j > sp of group g, count their mirrored hits
+    __device__ __forceinline__ uint32_t symf(int g, uint32_t mask) const {
+        if (!a.sym || !mask) return mask;
+        const int64_t jb = c0 + 4 * g;
+        if (jb + 3 <= sp) return 0;
+        if (jb <= sp) mask &= ~((2u << (sp - jb)) - 1u);
+        uint32_t mm = mask;
+        while (mm) {
+            const int i = __ffs(mm) - 1;
+            mm &= mm - 1;
+            atomicAdd(&a.lcnt[jb + i], 1);
+        }
+        return mask;
+    }
     __device__ __forceinline__ void record(int g, uint32_t mask) {   // MODE 0
+        mask = symf(g, mask);
+        if (!mask) return;
         const uint32_t v = ((uint32_t)g << 4) | mask;
         if (rec < a.cap) {
             slot[rec] = (uint16_t)v;
@@ -143,10 +160,16 @@ struct Emitter {
         c += __popc(mask);
     }
     __device__ __forceinline__ void write(int64_t j, double s) {      // MODE 1
+        if (a.sym && j <= sp) return;
+        const float dd = (float)sqrt(s);
         a.out_idx[pos] = a.perm[j];
-        a.out_dist[pos] = (float)sqrt(s);
+        a.out_dist[pos] = dd;
         ++pos;
         ++c;
+        if (a.sym) {   // mirrored entry into row j's L segment
+            const int32_t k = atomicAdd(&a.lcur[j], 1);
+            a.tmpL[a.offsets[a.qperm[j]] + k] = ((unsigned long long)sp << 32) | __float_as_uint(dd);
+        }
     }
 };
 
@@ -301,6 +324,7 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
         const int64_t e = item * a.B + tid;
         T q[D];
         Emitter<T, D, MODE> em{a, a.slots + (size_t)e * a.cap, e, c0, 0};
+        em.sp = sp;
         if (MODE == M_FIX) {
             active = active && a.cnt[e] < 0;   // lost-entry flag (sign bit)
             if (active) em.pos = a.offsets[a.qperm[sp]] + a.pre[e];
@@ -346,6 +370,10 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
                     const int cap = a.cap;
                     auto emit0 = [&](int gg, uint32_t m) {
                         if (MODE == M_SCAN) {
+                            if (a.sym) {
+                                m = em.symf(gg, m);
+                                if (!m) return;
+                            }
                             const uint32_t v = ((uint32_t)gg << 4) | m;
                             if (em.rec < cap) {
                                 slotp[em.rec] = (uint16_t)v;
@@ -525,7 +553,7 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
 // per (item, query) entry expands its slot records (the first `cap` records).
 template <typename T, int D>
 __device__ __forceinline__ void expand_record(const PassArgs &a, int64_t c0, uint32_t v,
-                                              const T (&q)[D], int64_t &pos) {
+                                              const T (&q)[D], int64_t &pos, int64_t sp) {
     const T *Xs = static_cast<const T *>(a.Xs);
     const int64_t g = c0 / 4 + (v >> 4);
     uint32_t mask = v & 15u;
@@ -535,9 +563,15 @@ __device__ __forceinline__ void expand_record(const PassArgs &a, int64_t c0, uin
         T x[D];
 #pragma unroll
         for (int k = 0; k < D; ++k) x[k] = Xs[g * 4 * D + k * 4 + i];
+        const float dd = (float)sqrt(sqdist_exact(x, q, D));
         a.out_idx[pos] = a.perm[g * 4 + i];
-        a.out_dist[pos] = (float)sqrt(sqdist_exact(x, q, D));
+        a.out_dist[pos] = dd;
         ++pos;
+        if (a.sym) {   // mirrored entry into row j's L segment (sorted afterwards)
+            const int64_t j = g * 4 + i;
+            const int32_t k = atomicAdd(&a.lcur[j], 1);
+            a.tmpL[a.offsets[a.qperm[j]] + k] = ((unsigned long long)sp << 32) | __float_as_uint(dd);
+        }
     }
 }
 
@@ -558,7 +592,7 @@ __global__ void __launch_bounds__(256) compact_lowd(PassArgs a) {
 #pragma unroll
         for (int k = 0; k < D; ++k) q[k] = Qs[(sp >> 2) * 4 * D + k * 4 + (sp & 3)];
         const uint16_t *slot = a.slots + (size_t)e * a.cap;
-        for (int r = 0; r < a.cap && pos < end; ++r) expand_record<T, D>(a, c0, slot[r], q, pos);
+        for (int r = 0; r < a.cap && pos < end; ++r) expand_record<T, D>(a, c0, slot[r], q, pos, sp);
     }
 }
 
@@ -578,7 +612,7 @@ __global__ void __launch_bounds__(256) compact_overflow(PassArgs a, int64_t n_re
         T q[D];
 #pragma unroll
         for (int kk = 0; kk < D; ++kk) q[kk] = Qs[(sp >> 2) * 4 * D + kk * 4 + (sp & 3)];
-        expand_record<T, D>(a, c0, r.v, q, pos);
+        expand_record<T, D>(a, c0, r.v, q, pos, sp);
     }
 }
 
@@ -717,6 +751,101 @@ __global__ void row_totals(const int32_t *cnt, int32_t *pre, const int64_t *item
     row_count[qperm ? qperm[sp] : sp] = run;
 }
 
+__global__ void row_totals_sym(const int32_t *cnt, int32_t *pre, const int64_t *item_start, int64_t m, int B,
+                               const int32_t *qperm, const int32_t *lcnt, int32_t *row_count, int32_t *maxl) {
+    const int64_t sp = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (sp >= m) return;
+    const int64_t b = sp / B, t = sp % B;
+    const int32_t l = lcnt[sp];
+    int32_t run = l + 1;   // L segment, then the point itself
+    for (int64_t item = item_start[b]; item < item_start[b + 1]; ++item) {
+        int32_t c = cnt[item * B + t] & 0x7fffffff;
+        pre[item * B + t] = run;
+        run += c;
+    }
+    row_count[qperm[sp]] = run;
+    atomicMax(maxl, l);
+}
+
+// L segments: warp per row, bitonic sort of (position << 32 | distance bits) in registers
+// (<= 32) or shared memory (<= 512); the CTA variant takes rows up to 16384.
+constexpr int kLWarp = 512, kLBlock = 16384;
+__device__ __forceinline__ void lemit(const PassArgs &a, unsigned long long v, int64_t pos) {
+    a.out_idx[pos] = a.perm[(uint32_t)(v >> 32)];
+    a.out_dist[pos] = __uint_as_float((uint32_t)v);
+}
+__global__ void __launch_bounds__(256) sym_lsort_warp(PassArgs a) {
+    __shared__ unsigned long long sbuf[8][kLWarp];
+    const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+    unsigned long long *buf = sbuf[w];
+    for (int64_t sp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; sp < a.m;
+         sp += (int64_t)gridDim.x * blockDim.x / 32) {
+        const int64_t o0 = a.offsets[a.qperm[sp]];
+        const int cnt = a.lcnt[sp];
+        if (lane == 0) { a.out_idx[o0 + cnt] = a.perm[sp]; a.out_dist[o0 + cnt] = 0.f; }   // the point itself
+        if (cnt == 0 || cnt > kLWarp) continue;
+        if (cnt <= 32) {
+            unsigned long long v = lane < cnt ? a.tmpL[o0 + lane] : ~0ull;
+#pragma unroll
+            for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+                for (int j = k >> 1; j > 0; j >>= 1) {
+                    const unsigned long long o = __shfl_xor_sync(0xffffffffu, v, j);
+                    const bool up = (lane & k) == 0, lower = (lane & j) == 0;
+                    const unsigned long long lo = v < o ? v : o, hi = v < o ? o : v;
+                    v = (lower == up) ? lo : hi;
+                }
+            }
+            if (lane < cnt) lemit(a, v, o0 + lane);
+            continue;
+        }
+        int S = 64;
+        while (S < cnt) S <<= 1;
+        for (int i = lane; i < S; i += 32) buf[i] = i < cnt ? a.tmpL[o0 + i] : ~0ull;
+        __syncwarp();
+        for (int k = 2; k <= S; k <<= 1) {
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int i = lane; i < S; i += 32) {
+                    const int p = i ^ j;
+                    if (p > i) {
+                        const unsigned long long x = buf[i], y = buf[p];
+                        if ((x > y) == ((i & k) == 0)) { buf[i] = y; buf[p] = x; }
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        for (int i = lane; i < cnt; i += 32) lemit(a, buf[i], o0 + i);
+        __syncwarp();
+    }
+}
+__global__ void __launch_bounds__(1024) sym_lsort_block(PassArgs a) {
+    extern __shared__ unsigned long long lbuf[];
+    for (int64_t sp = blockIdx.x; sp < a.m; sp += gridDim.x) {
+        const int cnt = a.lcnt[sp];
+        if (cnt <= kLWarp || cnt > kLBlock) continue;
+        const int64_t o0 = a.offsets[a.qperm[sp]];
+        int S = 1024;
+        while (S < cnt) S <<= 1;
+        for (int i = threadIdx.x; i < S; i += blockDim.x) lbuf[i] = i < cnt ? a.tmpL[o0 + i] : ~0ull;
+        __syncthreads();
+        for (int k = 2; k <= S; k <<= 1) {
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int i = threadIdx.x; i < S; i += blockDim.x) {
+                    const int p = i ^ j;
+                    if (p > i) {
+                        const unsigned long long x = lbuf[i], y = lbuf[p];
+                        if ((x > y) == ((i & k) == 0)) { lbuf[i] = y; lbuf[p] = x; }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        for (int i = threadIdx.x; i < cnt; i += blockDim.x) lemit(a, lbuf[i], o0 + i);
+        __syncthreads();
+    }
+}
+
 template <typename K>
 int persistent_grid(K kernel, int threads, size_t smem, int64_t items, int sm_count) {
     int occ = 1;
@@ -823,6 +952,25 @@ void launch_lowd_compact(const PassArgs &a, cudaStream_t s) {
 void launch_generic_pass(bool write, const PassArgs &a, cudaStream_t s) {
     if (a.total_items == 0) return;
     if (a.f64) run_generic<double>(write, a, s); else run_generic<float>(write, a, s);
+}
+
+void launch_row_totals_sym(const int32_t *cnt, int32_t *pre, const int64_t *item_start, int64_t m, int B,
+                           const int32_t *qperm, const int32_t *lcnt, int32_t *row_count, int32_t *maxl,
+                           cudaStream_t s) {
+    if (m == 0) return;
+    SNN_LAUNCH(row_totals_sym, (int)ceil_div(m, 256), 256, 0, s, cnt, pre, item_start, m, B, qperm, lcnt, row_count,
+               maxl);
+}
+
+void launch_sym_lsort(const PassArgs &a, int32_t max_l, cudaStream_t s) {
+    if (a.m == 0) return;
+    int64_t g = ceil_div(a.m * 32, 256);
+    if (g > 148 * 16) g = 148 * 16;
+    SNN_LAUNCH(sym_lsort_warp, (int)g, 256, 0, s, a);
+    if (max_l <= kLWarp) return;
+    const size_t smem = (size_t)kLBlock * 8;
+    cudaFuncSetAttribute(sym_lsort_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    SNN_LAUNCH(sym_lsort_block, 148 * 2, 1024, smem, s, a);
 }
 
 void launch_row_totals(const int32_t *cnt, int32_t *pre, const int64_t *item_start, int64_t m,

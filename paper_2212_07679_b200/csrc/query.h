@@ -68,6 +68,13 @@ struct PassArgs {
     int32_t *best;          // M_BORDER: smallest original id of a core neighbour (atomicMin)
     int32_t min_pts;        // M_COUNT: counts are only needed up to min_pts (early exit)
     int64_t n_index = 0;    // M_UNION: number of index points (parent array length)
+    // symmetric self-query (each unordered pair evaluated once): the scan keeps only
+    // candidates j > i (U rows) and counts the mirrored hits per candidate; the mirrored
+    // entries (L rows) are scattered during compaction and sorted per row afterwards
+    int sym = 0;
+    int32_t *lcnt = nullptr;             // per sorted position: |{j < i : i in U(j)}|
+    int32_t *lcur = nullptr;             // per sorted position: scatter cursor (zeroed)
+    unsigned long long *tmpL = nullptr;  // nnz: (position << 32 | fp32 distance bits) at row start
     // expanded-form SIMT filter (scan variant 3; nullptr = off): AoSoA4 rows with D+1
     // floats (centred coordinates, xbar c1h), the margin constants and mu_f
     const float *Xf = nullptr;
@@ -99,6 +106,12 @@ void launch_lowd_mode(int mode, const PassArgs &a, cudaStream_t s);
 // Generic-d path (row-major, any d): count pass + write pass (write recomputes).
 void launch_generic_pass(bool write, const PassArgs &a, cudaStream_t s);
 
+// symmetric self-query: totals = U hits + L hits + self; pre[e] starts after L + self
+void launch_row_totals_sym(const int32_t *cnt, int32_t *pre, const int64_t *item_start, int64_t m, int B,
+                           const int32_t *qperm, const int32_t *lcnt, int32_t *row_count, int32_t *maxl,
+                           cudaStream_t s);
+// symmetric self-query: sort every row's L segment by position, write it and the self entry
+void launch_sym_lsort(const PassArgs &a, int32_t max_l, cudaStream_t s);
 // K11 helper: per-row totals over a block's items; pre = exclusive per-item prefixes
 // (pre may alias cnt); row_count[qperm[sp]] = total (qperm NULL: row_count[sp]).
 void launch_row_totals(const int32_t *cnt, int32_t *pre, const int64_t *item_start, int64_t m,

@@ -492,6 +492,29 @@ def test_simt_expanded_filter_vs_direct_exact(snn, d):
     assert res[1][3] == res[-1][3] and np.array_equal(res[1][2], res[-1][2])
 
 
+@pytest.mark.parametrize("d,dt,R", [(1, np.float32, 0.002), (2, np.float32, 0.02), (3, np.float32, 0.6),
+                                    (3, np.float64, 0.6), (8, np.float32, 1.5), (2, np.float32, 0.0)])
+def test_symmetric_self_query_identical(snn, d, dt, R):
+    """Self-query with each unordered pair evaluated once (mirrored L rows, sorted) vs the
+    two-sided scan: bit-identical CSR (key order, distances), equal to the oracle."""
+    import paper_2212_07679_b200 as p
+    rng = np.random.default_rng(300 + d)
+    centers = rng.random((10, d)) * 30
+    X = (centers[rng.integers(0, 10, 9000)] + rng.standard_normal((9000, d))).astype(dt)
+    X[100:140] = X[0]                                     # duplicates (R = 0 hits)
+    res = {}
+    try:
+        for f in (1, -1):
+            p.snn_set_option("symmetric", f)
+            res[f] = run(snn, X, None, R)
+    finally:
+        p.snn_set_option("symmetric", 0)
+    a, b = res[1], res[-1]
+    assert np.array_equal(a.offsets, b.offsets) and np.array_equal(a.indices, b.indices)
+    assert np.array_equal(a.distances, b.distances)
+    compare(a, oracle.radius_query(X, X, R))
+
+
 @pytest.mark.parametrize("tiles,group", [(1, 1), (3, 2), (8, 8), (16, 64)])
 def test_lowd_tensor_core_raster_options(snn, tiles, group):
     import paper_2212_07679_b200 as p
