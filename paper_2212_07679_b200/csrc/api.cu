@@ -1017,10 +1017,9 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
     if (sym) {
         a.sym = 1;
         CK(ws.alloc(&a.lcnt, (size_t)m), "alloc");
-        CK(ws.alloc(&a.lcur, (size_t)m), "alloc");
+        CK(ws.alloc(&a.lpos, (size_t)m), "alloc");
         CK(ws.alloc(&maxl, 1), "alloc");
         CK(cudaMemsetAsync(a.lcnt, 0, (size_t)m * 4, s), "memset");
-        CK(cudaMemsetAsync(a.lcur, 0, (size_t)m * 4, s), "memset");
         CK(cudaMemsetAsync(maxl, 0, 4, s), "memset");
     }
     thresholds(a.R2, D, &a.T_in, &a.T_out);
@@ -1075,7 +1074,10 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
         r->distances = static_cast<float *>(p);
     }
     a.out_idx = r->indices; a.out_dist = r->distances;
-    if (sym) CK(ws.alloc(&a.tmpL, (size_t)(r->nnz > 0 ? r->nnz : 1)), "alloc mirrored entries");
+    if (sym) {
+        CK(ws.alloc(&a.tmpL, (size_t)(r->nnz > 0 ? r->nnz : 1)), "alloc mirrored entries");
+        launch_sym_lpos_init(a, s);
+    }
     if (r->nnz > 0) {
         const int wtok = prof_begin(F_WRITE, s);
         if (generic) {

@@ -123,7 +123,7 @@ __device__ __forceinline__ float lane4(const float4 &v, int i) {   // i is unrol
 // Hit masks -> output.  MODE 0 records (g << 4 | mask) in the entry's slot list, or, once
 // `cap` slots are used, appends (entry, hits-before, record) to the global overflow list;
 // MODE 1 (fix) writes the CSR entries directly.
-template <typename T, int D, int MODE>
+template <typename T, int D, int MODE, bool SYM = false>
 struct Emitter {
     const PassArgs &a;
     uint16_t *slot;
@@ -133,7 +133,7 @@ struct Emitter {
     bool lost = false;
     // symmetric self-query: keep candidates j > sp of group g, count their mirrored hits
     __device__ __forceinline__ uint32_t symf(int g, uint32_t mask) const {
-        if (!a.sym || !mask) return mask;
+        if (!SYM || !mask) return mask;
         const int64_t jb = c0 + 4 * g;
         if (jb + 3 <= sp) return 0;
         if (jb <= sp) mask &= ~((2u << (sp - jb)) - 1u);
@@ -160,16 +160,14 @@ struct Emitter {
         c += __popc(mask);
     }
     __device__ __forceinline__ void write(int64_t j, double s) {      // MODE 1
-        if (a.sym && j <= sp) return;
+        if (SYM && j <= sp) return;
         const float dd = (float)sqrt(s);
         a.out_idx[pos] = a.perm[j];
         a.out_dist[pos] = dd;
         ++pos;
         ++c;
-        if (a.sym) {   // mirrored entry into row j's L segment
-            const int32_t k = atomicAdd(&a.lcur[j], 1);
-            a.tmpL[a.offsets[a.qperm[j]] + k] = ((unsigned long long)sp << 32) | __float_as_uint(dd);
-        }
+        if (SYM)   // mirrored entry into row j's L segment
+            a.tmpL[atomicAdd(&a.lpos[j], 1ull)] = ((unsigned long long)sp << 32) | __float_as_uint(dd);
     }
 };
 
@@ -277,7 +275,7 @@ __device__ __forceinline__ void uf_unite(int32_t *p, int32_t a, int32_t b) {
     }
 }
 
-template <typename T, int D, int MODE, int G>
+template <typename T, int D, int MODE, int G, bool SYM = false>
 __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int tid = threadIdx.x;
@@ -323,7 +321,7 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
         bool active = sp < a.m;
         const int64_t e = item * a.B + tid;
         T q[D];
-        Emitter<T, D, MODE> em{a, a.slots + (size_t)e * a.cap, e, c0, 0};
+        Emitter<T, D, MODE, SYM> em{a, a.slots + (size_t)e * a.cap, e, c0, 0};
         em.sp = sp;
         if (MODE == M_FIX) {
             active = active && a.cnt[e] < 0;   // lost-entry flag (sign bit)
@@ -370,7 +368,7 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
                     const int cap = a.cap;
                     auto emit0 = [&](int gg, uint32_t m) {
                         if (MODE == M_SCAN) {
-                            if (a.sym) {
+                            if constexpr (SYM) {
                                 m = em.symf(gg, m);
                                 if (!m) return;
                             }
@@ -567,11 +565,8 @@ __device__ __forceinline__ void expand_record(const PassArgs &a, int64_t c0, uin
         a.out_idx[pos] = a.perm[g * 4 + i];
         a.out_dist[pos] = dd;
         ++pos;
-        if (a.sym) {   // mirrored entry into row j's L segment (sorted afterwards)
-            const int64_t j = g * 4 + i;
-            const int32_t k = atomicAdd(&a.lcur[j], 1);
-            a.tmpL[a.offsets[a.qperm[j]] + k] = ((unsigned long long)sp << 32) | __float_as_uint(dd);
-        }
+        if (a.sym)   // mirrored entry into row j's L segment (sorted afterwards)
+            a.tmpL[atomicAdd(&a.lpos[g * 4 + i], 1ull)] = ((unsigned long long)sp << 32) | __float_as_uint(dd);
     }
 }
 
@@ -780,8 +775,8 @@ __global__ void __launch_bounds__(256) sym_lsort_warp(PassArgs a) {
     unsigned long long *buf = sbuf[w];
     for (int64_t sp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; sp < a.m;
          sp += (int64_t)gridDim.x * blockDim.x / 32) {
-        const int64_t o0 = a.offsets[a.qperm[sp]];
         const int cnt = a.lcnt[sp];
+        const int64_t o0 = (int64_t)a.lpos[sp] - cnt;   // the row start (cursor advanced by cnt)
         if (lane == 0) { a.out_idx[o0 + cnt] = a.perm[sp]; a.out_dist[o0 + cnt] = 0.f; }   // the point itself
         if (cnt == 0 || cnt > kLWarp) continue;
         if (cnt <= 32) {
@@ -824,7 +819,7 @@ __global__ void __launch_bounds__(1024) sym_lsort_block(PassArgs a) {
     for (int64_t sp = blockIdx.x; sp < a.m; sp += gridDim.x) {
         const int cnt = a.lcnt[sp];
         if (cnt <= kLWarp || cnt > kLBlock) continue;
-        const int64_t o0 = a.offsets[a.qperm[sp]];
+        const int64_t o0 = (int64_t)a.lpos[sp] - cnt;
         int S = 1024;
         while (S < cnt) S <<= 1;
         for (int i = threadIdx.x; i < S; i += blockDim.x) lbuf[i] = i < cnt ? a.tmpL[o0 + i] : ~0ull;
@@ -861,8 +856,10 @@ void run_lowd(const PassArgs &a, cudaStream_t s) {
     const bool exp = sizeof(T) == 4 && MODE != M_FIX && a.Xf != nullptr &&
                      (size_t)2 * a.chunk * (D * sizeof(T) + (D + 1) * 4) + 16 <= 200 * 1024;
     const size_t smem = (size_t)2 * a.chunk * (D * sizeof(T) + (exp ? (D + 1) * 4 : 0)) + 16;
+    constexpr bool SYMOK = MODE == M_SCAN || MODE == M_FIX;   // symmetric self-query variants
     auto k = exp ? window_lowd<T, D, MODE, 3>
                  : (a.variant == 1 ? window_lowd<T, D, MODE, 1> : window_lowd<T, D, MODE, 2>);
+    if (SYMOK && a.sym) k = window_lowd<T, D, MODE, 1, SYMOK>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int64_t work = MODE == M_FIX ? a.n_ovf : a.total_items;
     int g = persistent_grid(k, a.B, smem, work, a.sm_count);
@@ -960,6 +957,18 @@ void launch_row_totals_sym(const int32_t *cnt, int32_t *pre, const int64_t *item
     if (m == 0) return;
     SNN_LAUNCH(row_totals_sym, (int)ceil_div(m, 256), 256, 0, s, cnt, pre, item_start, m, B, qperm, lcnt, row_count,
                maxl);
+}
+
+__global__ void sym_lpos_init(PassArgs a) {
+    for (int64_t sp = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; sp < a.m; sp += (int64_t)gridDim.x * blockDim.x)
+        a.lpos[sp] = (unsigned long long)a.offsets[a.qperm[sp]];
+}
+
+void launch_sym_lpos_init(const PassArgs &a, cudaStream_t s) {
+    if (a.m == 0) return;
+    int64_t g = ceil_div(a.m, 256);
+    if (g > 148 * 16) g = 148 * 16;
+    SNN_LAUNCH(sym_lpos_init, (int)g, 256, 0, s, a);
 }
 
 void launch_sym_lsort(const PassArgs &a, int32_t max_l, cudaStream_t s) {

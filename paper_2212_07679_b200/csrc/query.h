@@ -73,7 +73,7 @@ struct PassArgs {
     // entries (L rows) are scattered during compaction and sorted per row afterwards
     int sym = 0;
     int32_t *lcnt = nullptr;             // per sorted position: |{j < i : i in U(j)}|
-    int32_t *lcur = nullptr;             // per sorted position: scatter cursor (zeroed)
+    unsigned long long *lpos = nullptr;  // per sorted position: next L slot (starts at the row start)
     unsigned long long *tmpL = nullptr;  // nnz: (position << 32 | fp32 distance bits) at row start
     // expanded-form SIMT filter (scan variant 3; nullptr = off): AoSoA4 rows with D+1
     // floats (centred coordinates, xbar c1h), the margin constants and mu_f
@@ -110,6 +110,8 @@ void launch_generic_pass(bool write, const PassArgs &a, cudaStream_t s);
 void launch_row_totals_sym(const int32_t *cnt, int32_t *pre, const int64_t *item_start, int64_t m, int B,
                            const int32_t *qperm, const int32_t *lcnt, int32_t *row_count, int32_t *maxl,
                            cudaStream_t s);
+// symmetric self-query: L cursors = CSR row starts (lpos[sp] = offsets[qperm[sp]])
+void launch_sym_lpos_init(const PassArgs &a, cudaStream_t s);
 // symmetric self-query: sort every row's L segment by position, write it and the self entry
 void launch_sym_lsort(const PassArgs &a, int32_t max_l, cudaStream_t s);
 // K11 helper: per-row totals over a block's items; pre = exclusive per-item prefixes
