@@ -52,7 +52,7 @@ static Options g_opt;
 static thread_local std::string t_err;
 
 // ------------------------------------------------------------------ kernel-time profiler
-static const char *kFamNames[F_N] = {"build", "window_count", "window_write", "query", "dbscan"};
+static const char *kFamNames[F_N] = {"build", "window_count", "window_write", "query", "dbscan", "dbscan_union"};
 struct ProfRec {
     int fam;
     cudaEvent_t a, b;
@@ -969,7 +969,8 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
     int64_t *blk_lo_s = blk_lo;
     if (sym) {
         CK(ws.alloc(&blk_lo_s, (size_t)nblocks), "alloc");
-        launch_truncate_windows(blk_lo, blk_hi, nblocks, B, chunk, blk_lo_s, nitems, s);
+        CK(cudaMemsetAsync(pairs, 0, 8, s), "memset");   // evaluated pairs = the clipped windows
+        launch_truncate_windows(blk_lo, blk_hi, nblocks, B, chunk, blk_lo_s, nitems, m, idx->n, pairs, s);
     }
     exclusive_scan_i64(nitems, item_start, nblocks, scan_tmp, s);
     int64_t *hp = static_cast<int64_t *>(t_pinned.p);

@@ -188,7 +188,7 @@ snn_status dbscan_impl(snn_index idx, double eps, int32_t min_pts, int32_t *labe
     CKD(ws.alloc(&item_start, (size_t)nblocks + 1), "alloc");
     CKD(ws.alloc(&pairs, 1), "alloc");
     CKD(ws.alloc(&scan_tmp, scan_temp_bytes(n > nblocks ? n : nblocks)), "alloc");
-    CKD(cudaMallocHost(&hbuf, 16), "pinned");
+    CKD(cudaMallocHost(&hbuf, 32), "pinned");
     struct HostFree { void *p; ~HostFree() { cudaFreeHost(p); } } hf{hbuf};
     CKD(cudaMemsetAsync(pairs, 0, 8, s), "memset");
     WindowSpec w;
@@ -256,21 +256,29 @@ snn_status dbscan_impl(snn_index idx, double eps, int32_t min_pts, int32_t *labe
     CKD(cudaStreamSynchronize(s), "dbscan pairs");
     const double pairs_eval = (double)*hp_pairs;
     const int ctok = prof_begin(F_COUNT, s);
-    launch_core_counts(a, count, s);                                        // counts (to min_pts)
-    prof_end(ctok, s, pairs_eval);
+    CKD(cudaMemsetAsync(pairs, 0, 8, s), "memset");
+    launch_core_counts(a, count, pairs, s);                                 // counts (to min_pts)
     SNN_LAUNCH(init_core, grid_n(n), 256, 0, s, count, n, min_pts, core, parent, minid, best);
     {   // unions over the clipped windows (pairs j > i only: block b starts at its first position)
         int64_t *lo2, *nit2, *st2;
         CKD(ws.alloc(&lo2, (size_t)nblocks), "alloc");
         CKD(ws.alloc(&nit2, (size_t)nblocks), "alloc");
         CKD(ws.alloc(&st2, (size_t)nblocks + 1), "alloc");
-        launch_truncate_windows(blk_lo, blk_hi, nblocks, B, chunk, lo2, nit2, s);
+        unsigned long long *upairs;
+        CKD(ws.alloc(&upairs, 1), "alloc");
+        CKD(cudaMemsetAsync(upairs, 0, 8, s), "memset");
+        launch_truncate_windows(blk_lo, blk_hi, nblocks, B, chunk, lo2, nit2, n, n, upairs, s);
         exclusive_scan_i64(nit2, st2, nblocks, scan_tmp, s);
         CKD(cudaMemcpyAsync(hbuf, st2 + nblocks, 8, cudaMemcpyDeviceToHost, s), "D2H");
+        CKD(cudaMemcpyAsync(hbuf + 2, pairs, 8, cudaMemcpyDeviceToHost, s), "D2H");
+        CKD(cudaMemcpyAsync(hbuf + 3, upairs, 8, cudaMemcpyDeviceToHost, s), "D2H");
         CKD(cudaStreamSynchronize(s), "dbscan union windows");
+        prof_end(ctok, s, (double)*reinterpret_cast<unsigned long long *>(hbuf + 2));   // pairs evaluated
         PassArgs au = a;
         au.blk_lo = lo2; au.item_start = st2; au.total_items = hbuf[0];
+        const int utok = prof_begin(F_UNION, s);
         launch_lowd_mode(3, au, s);                                          // unions
+        prof_end(utok, s, (double)*reinterpret_cast<unsigned long long *>(hbuf + 3));
     }
     SNN_LAUNCH(flatten, grid_n(n), 256, 0, s, parent, core, idx->perm, n, minid);
     CKD(cudaMemsetAsync(flag, 0, (size_t)n * 4, s), "memset");
@@ -352,7 +360,7 @@ snn_status dbscan_from_csr(const int64_t *off, const int32_t *nidx, int64_t n, i
     CKD(ws.alloc(&inv, (size_t)n), "alloc");
     CKD(ws.alloc(&iota, (size_t)n), "alloc");
     CKD(ws.alloc(&scan_tmp, scan_temp_bytes(n)), "alloc");
-    CKD(cudaMallocHost(&hbuf, 16), "pinned");
+    CKD(cudaMallocHost(&hbuf, 32), "pinned");
     struct HostFree { void *p; ~HostFree() { cudaFreeHost(p); } } hf{hbuf};
     const bool dev_out = is_device_ptr(labels);
     if (dev_out) out = labels; else CKD(ws.alloc(&out, (size_t)n), "alloc");

@@ -13,7 +13,7 @@
 namespace snn {
 snn_status fail(snn_status st, const std::string &msg);
 // kernel-time profiler families (snn_profile_*)
-enum Fam { F_BUILD = 0, F_COUNT = 1, F_WRITE = 2, F_QUERY = 3, F_DBSCAN = 4, F_N = 5 };
+enum Fam { F_BUILD = 0, F_COUNT = 1, F_WRITE = 2, F_QUERY = 3, F_DBSCAN = 4, F_UNION = 5, F_N = 6 };
 int prof_begin(int fam, cudaStream_t s);                 // -1 when profiling is off
 void prof_end(int tok, cudaStream_t s, double units);
 snn_status cuda_fail(cudaError_t e, const char *where);

@@ -1035,20 +1035,24 @@ namespace {
 // DBSCAN union pass: only pairs j > i are united, so block b's window starts at its own
 // first position (rounded down to 4).
 __global__ void truncate_windows_kernel(const int64_t *blk_lo, const int64_t *blk_hi, int64_t nblocks, int B,
-                                        int chunk, int64_t *lo2, int64_t *nitems2) {
+                                        int chunk, int64_t *lo2, int64_t *nitems2, int64_t m, int64_t n,
+                                        unsigned long long *pairs) {
     const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= nblocks) return;
     const int64_t lo = max(blk_lo[b], (b * B) & ~(int64_t)3), hi = blk_hi[b];
     lo2[b] = lo;
     nitems2[b] = hi > lo ? ceil_div(hi - lo, chunk) : 0;
+    const int64_t vh = min(hi, n), nq = min((int64_t)B, m - b * B);   // candidate pairs evaluated
+    if (pairs && vh > lo && nq > 0) atomicAdd(pairs, (unsigned long long)((vh - lo) * nq));
 }
 }  // namespace
 
 void launch_truncate_windows(const int64_t *blk_lo, const int64_t *blk_hi, int64_t nblocks, int B, int chunk,
-                             int64_t *lo2, int64_t *nitems2, cudaStream_t s) {
+                             int64_t *lo2, int64_t *nitems2, int64_t m, int64_t n, unsigned long long *pairs,
+                             cudaStream_t s) {
     if (nblocks == 0) return;
     SNN_LAUNCH(truncate_windows_kernel, (int)ceil_div(nblocks, 256), 256, 0, s, blk_lo, blk_hi, nblocks, B, chunk,
-               lo2, nitems2);
+               lo2, nitems2, m, n, pairs);
 }
 
 namespace {
@@ -1057,7 +1061,7 @@ namespace {
 // query of the block has min_pts hits (config 5: the first chunk usually suffices);
 // same exact classification as the radius query.  count = min(|N_eps|, >= min_pts).
 template <typename T, int D>
-__global__ void __launch_bounds__(256) core_count_kernel(PassArgs a, int32_t *count) {
+__global__ void __launch_bounds__(256) core_count_kernel(PassArgs a, int32_t *count, unsigned long long *evaluated) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int tid = threadIdx.x;
     const T *Xs = static_cast<const T *>(a.Xs);
@@ -1081,6 +1085,7 @@ __global__ void __launch_bounds__(256) core_count_kernel(PassArgs a, int32_t *co
     const float T_in = a.T_in, T_out = a.T_out;
     const double R2 = a.R2;
     const int32_t mp = a.min_pts;
+    unsigned long long ev = 0;   // candidate pairs this thread evaluated (roofline accounting)
     for (int64_t b = blockIdx.x; b < a.nblocks; b += gridDim.x) {
         const int64_t sp = b * a.B + tid;
         const bool active = sp < a.m;
@@ -1104,7 +1109,8 @@ __global__ void __launch_bounds__(256) core_count_kernel(PassArgs a, int32_t *co
                     uint64_t nq[D];
 #pragma unroll
                     for (int k = 0; k < D; ++k) nq[k] = f2pack(-q[k], -q[k]);
-                    for (int g = 0; g < ngroups && c < mp; ++g) {
+                    int g = 0;
+                    for (; g < ngroups && c < mp; ++g) {
                         float4 xa[D];
 #pragma unroll
                         for (int k = 0; k < D; ++k) xa[k] = g4[g * D + k];
@@ -1118,6 +1124,7 @@ __global__ void __launch_bounds__(256) core_count_kernel(PassArgs a, int32_t *co
                             c += __popc(ia);
                         }
                     }
+                    ev += 4ull * g;
                 } else {
                     const T *gb = reinterpret_cast<const T *>(smem + sidx * buf_bytes);
                     for (int g = 0; g < ngroups && c < mp; ++g) {
@@ -1132,6 +1139,7 @@ __global__ void __launch_bounds__(256) core_count_kernel(PassArgs a, int32_t *co
                             c += s2 <= R2;
                         }
                     }
+                    ev += 4ull * ngroups;
                 }
             }
             if (!__syncthreads_or(active && c < mp)) {   // every query of the block is decided
@@ -1146,21 +1154,25 @@ __global__ void __launch_bounds__(256) core_count_kernel(PassArgs a, int32_t *co
         if (active) count[sp] = c;
         __syncthreads();
     }
+    if (evaluated) {
+        ev = warp_sum(ev);
+        if ((threadIdx.x & 31) == 0 && ev) atomicAdd(evaluated, ev);
+    }
 }
 
 template <typename T, int D>
-void run_core_count(const PassArgs &a, int32_t *count, cudaStream_t s) {
+void run_core_count(const PassArgs &a, int32_t *count, unsigned long long *evaluated, cudaStream_t s) {
     const size_t smem = (size_t)2 * a.chunk * D * sizeof(T) + 16;
     auto k = core_count_kernel<T, D>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int g = persistent_grid(k, a.B, smem, a.nblocks, a.sm_count);
-    SNN_LAUNCH(k, g, a.B, smem, s, a, count);
+    SNN_LAUNCH(k, g, a.B, smem, s, a, count, evaluated);
 }
 }  // namespace
 
-void launch_core_counts(const PassArgs &a, int32_t *count, cudaStream_t s) {
+void launch_core_counts(const PassArgs &a, int32_t *count, unsigned long long *evaluated, cudaStream_t s) {
     if (a.nblocks == 0) return;
-#define FN(T, D) run_core_count<T, D>(a, count, s)
+#define FN(T, D) run_core_count<T, D>(a, count, evaluated, s)
     SNN_LOWD_DISPATCH(FN)
 #undef FN
 }

@@ -83,10 +83,12 @@ struct PassArgs {
 };
 // DBSCAN core counts with early exit: count[sp] = |N_eps| if < min_pts, else some value
 // >= min_pts (one CTA per query block, chunks in order, stop when the block is decided)
-void launch_core_counts(const PassArgs &a, int32_t *count, cudaStream_t s);
+void launch_core_counts(const PassArgs &a, int32_t *count, unsigned long long *evaluated, cudaStream_t s);
 // DBSCAN union pass work list: window of block b clipped to start at its first position
+// (pairs, nullable, += candidate pairs of the clipped windows for m queries / n points)
 void launch_truncate_windows(const int64_t *blk_lo, const int64_t *blk_hi, int64_t nblocks, int B, int chunk,
-                             int64_t *lo2, int64_t *nitems2, cudaStream_t s);
+                             int64_t *lo2, int64_t *nitems2, int64_t m, int64_t n, unsigned long long *pairs,
+                             cudaStream_t s);
 // filter rows for the expanded-form scan variant from the AoSoA4 sorted copy
 void launch_filter_rows(const float *Xs, int d, int64_t n, int64_t n_pad, const float *mu_f, double c1h, float *Xf,
                         cudaStream_t s);
