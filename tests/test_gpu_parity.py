@@ -515,6 +515,23 @@ def test_symmetric_self_query_identical(snn, d, dt, R):
     compare(a, oracle.radius_query(X, X, R))
 
 
+@pytest.mark.parametrize("d,n", [(3, 20000), (2, 30000), (64, 6000)])
+def test_everything_is_a_neighbour(snn, d, n):
+    """R larger than the data diameter: every row holds all n points (slot overflow, lost
+    entries and the fix pass, the symmetric path's huge-row fallback, pair-list capacity
+    retries); rows in key order, distances exact."""
+    rng = np.random.default_rng(d)
+    X = rng.random((n, d)).astype(np.float32)
+    R = float(np.sqrt(d)) * 2.0
+    res = run(snn, X, None, R)
+    assert np.array_equal(np.diff(res.offsets), np.full(n, n))
+    for r in (0, n // 2, n - 1):   # each row: a permutation of all points, exact distances
+        ids = res.indices[res.offsets[r]:res.offsets[r + 1]]
+        assert np.array_equal(np.sort(ids), np.arange(n))
+        dd = np.sqrt(((X[ids].astype(np.float64) - X[r].astype(np.float64)) ** 2).sum(axis=1)).astype(np.float32)
+        assert np.array_equal(res.distances[res.offsets[r]:res.offsets[r + 1]], dd)
+
+
 @pytest.mark.parametrize("tiles,group", [(1, 1), (3, 2), (8, 8), (16, 64)])
 def test_lowd_tensor_core_raster_options(snn, tiles, group):
     import paper_2212_07679_b200 as p
