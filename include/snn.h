@@ -34,6 +34,19 @@ extern "C" {
 
 typedef enum { SNN_F32 = 0, SNN_F64 = 1 } snn_dtype;
 
+/* Distance of an index (§3 "other distances"):
+ *  EUCLIDEAN  ||p - q||, radius R.
+ *  COSINE     cdist(u, v) = 1 - u.v on unit vectors; 2 cdist = ||u - v||^2,
+ *             so a cosine radius r is the Euclidean radius sqrt(2 r) on normalized rows.
+ *  ANGULAR    theta(u, v) <= alpha  iff  ||u - v||^2 <= 2 - 2 cos(alpha);
+ *             radius alpha in radians.
+ * For COSINE / ANGULAR the rows of X and Q are normalized on the device with the exact
+ * rule u_k = x_k / sqrt(sum_k x_k^2) (fp64, left-to-right sum, correctly rounded sqrt and
+ * division, then rounded to the input dtype); the search itself is the exact Euclidean
+ * search on the normalized rows with the mapped radius (computed in fp64), and returned
+ * distances are converted back to the metric (r = d^2 / 2, alpha = 2 asin(d / 2)). */
+typedef enum { SNN_METRIC_EUCLIDEAN = 0, SNN_METRIC_COSINE = 1, SNN_METRIC_ANGULAR = 2 } snn_metric;
+
 typedef enum {
     SNN_OK = 0,
     SNN_ERR_INVALID_ARGUMENT = 1, /* NULL pointer, d < 1, m < 0, R < 0 or non-finite, ... */
@@ -80,6 +93,7 @@ typedef struct {
                                   1 FP16 (kind::f16, scaled by 2^tc_exp), 2 TF32         */
     int32_t tc_kpad;           /* K of the tensor-core operand copy (padded d)          */
     int32_t tc_exp;            /* FP16 operand scale exponent of the index copy         */
+    int32_t metric;            /* snn_metric                                            */
 } snn_index_info_t;
 
 /*
@@ -94,6 +108,13 @@ typedef struct {
  */
 snn_status snn_build(const void *X, int64_t n, int32_t d, snn_dtype dt, void *stream,
                      snn_index *out);
+
+/* snn_build for a metric (snn_metric).  EUCLIDEAN == snn_build.  COSINE / ANGULAR: rows
+ * are normalized first (see snn_metric); a zero row -> SNN_ERR_INVALID_ARGUMENT.  Radii
+ * of snn_query_radius / snn_query_self / snn_dbscan on this index are in the metric's
+ * units (cosine distance in [0, 2], angle in radians), and so are returned distances. */
+snn_status snn_build_metric(const void *X, int64_t n, int32_t d, snn_dtype dt, int32_t metric,
+                            void *stream, snn_index *out);
 
 /*
  * snn_query_radius -- Algorithm 2 "SNN Query" for a batch of m

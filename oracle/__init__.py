@@ -15,6 +15,10 @@ Contents (each function cites the passage it follows):
                         step in fp64 numpy, the SVD of eq:svd via LAPACK.
 * ``candidate_range``, ``alg2_query``   Algorithm 2 "SNN Query", the
                         Cauchy-Schwarz window of eq:lower.
+* ``normalize_rows``, ``metric_radius``, ``metric_distance``, ``metric_radius_query``,
+  ``cosine_distance``, ``angular_distance``   cosine / angular distance through the
+                        Euclidean search on normalized rows (DESIGN.md
+                        reading C21); the direct definitions pin the reduction.
 
 Parity pins live in ``tests/test_oracle.py`` (hand examples, closed forms, library
 cross-checks, invariants).  No function here is "parity unpinned".
@@ -238,3 +242,70 @@ def alg2_query(index: dict, P, q, R: float) -> np.ndarray:
     R2 = float(R) * float(R)
     out = [int(i) for i in ids if sqdist(P[i], q) <= R2]
     return np.array(sorted(out), dtype=np.int64)
+
+
+# ----------------------------------------------------------------- metrics
+METRICS = {"euclidean": 0, "cosine": 1, "angular": 2}
+
+
+def cosine_distance(p, q) -> float:
+    """Definition (PAPER.md:59-61): cdist(p, q) = 1 - p.q / (||p|| ||q||), fp64."""
+    p, q = np.asarray(p, dtype=np.float64), np.asarray(q, dtype=np.float64)
+    return float(1.0 - (p @ q) / (np.linalg.norm(p) * np.linalg.norm(q)))
+
+
+def angular_distance(p, q) -> float:
+    """Definition (PAPER.md:67-69): theta(p, q) = arccos(p.q / (||p|| ||q||)), fp64."""
+    p, q = np.asarray(p, dtype=np.float64), np.asarray(q, dtype=np.float64)
+    c = (p @ q) / (np.linalg.norm(p) * np.linalg.norm(q))
+    return float(np.arccos(np.clip(c, -1.0, 1.0)))
+
+
+def normalize_rows(P) -> np.ndarray:
+    """u_i = p_i / ||p_i|| with DESIGN.md reading C21's rule: fp64 sum of
+    squares left to right, correctly rounded sqrt and division, rounded to the input
+    dtype.  A zero row raises ValueError."""
+    P = np.asarray(P)
+    dt = P.dtype if P.dtype in (np.float32, np.float64) else np.float64
+    X = P.astype(np.float64)
+    s = np.zeros(X.shape[0], dtype=np.float64)
+    for k in range(X.shape[1]):            # left to right over the coordinates
+        s = s + X[:, k] * X[:, k]
+    if np.any(s <= 0.0):
+        raise ValueError("zero row")
+    return (X / np.sqrt(s)[:, None]).astype(dt)
+
+
+def metric_radius(metric: str, r: float) -> float:
+    """Euclidean radius on unit vectors equivalent to metric radius r: 2 cdist = ||u-v||^2
+     -> sqrt(2 r); theta <= alpha iff ||u-v||^2 <= 2 - 2 cos(alpha)
+     -> sqrt(2 - 2 cos alpha), every pair (3.0) for alpha >= pi."""
+    import math
+    if metric == "cosine":
+        return math.sqrt(2.0 * r)
+    if metric == "angular":
+        return 3.0 if r >= math.pi else math.sqrt(2.0 - 2.0 * math.cos(r))
+    return float(r)
+
+
+def metric_distance(metric: str, e) -> np.ndarray:
+    """Metric value of a returned float32 Euclidean distance e on unit vectors:
+    cdist = e^2 / 2, theta = 2 asin(e / 2) (chord length), fp64 then
+    float32."""
+    e = np.asarray(e, dtype=np.float64)
+    if metric == "cosine":
+        return (0.5 * e * e).astype(np.float32)
+    if metric == "angular":
+        return (2.0 * np.arcsin(np.minimum(1.0, 0.5 * e))).astype(np.float32)
+    return e.astype(np.float32)
+
+
+def metric_radius_query(P, Q, r: float, metric: str) -> dict:
+    """Fixed-radius search under ``metric``: ``radius_query`` on the
+    normalized rows with the mapped radius; adds ``dist`` = the metric value of every hit's
+    float32 Euclidean distance (``metric_distance``)."""
+    U, V = normalize_rows(P), normalize_rows(Q)
+    out = radius_query(U, V, metric_radius(metric, r), band_rel=0.0)
+    out["dist"] = metric_distance(metric, np.sqrt(out["s"]).astype(np.float32))
+    out["U"], out["V"] = U, V
+    return out

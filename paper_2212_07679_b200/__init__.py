@@ -29,7 +29,7 @@ STATUS = {0: "SNN_OK", 1: "SNN_ERR_INVALID_ARGUMENT", 2: "SNN_ERR_EMPTY",
           3: "SNN_ERR_NONFINITE", 4: "SNN_ERR_DIM_MISMATCH", 5: "SNN_ERR_OUT_OF_MEMORY",
           6: "SNN_ERR_CUDA", 7: "SNN_ERR_UNSUPPORTED"}
 
-EXPORTS = ["snn_build", "snn_query_radius", "snn_query_self", "snn_result_csr",
+EXPORTS = ["snn_build", "snn_build_metric", "snn_query_radius", "snn_query_self", "snn_result_csr",
            "snn_result_copy", "snn_result_free", "snn_dbscan", "snn_free", "snn_last_error",
            "snn_index_info", "snn_launch_count", "snn_set_option", "snn_profile_enable",
            "snn_profile_read"]
@@ -54,7 +54,10 @@ class _Info(ctypes.Structure):
                 ("v1_norm", ctypes.c_double), ("mu", ctypes.c_void_p), ("v1", ctypes.c_void_p),
                 ("keys", ctypes.c_void_p), ("perm", ctypes.c_void_p), ("xbar", ctypes.c_void_p),
                 ("xs", ctypes.c_void_p), ("tc_operand", ctypes.c_int32), ("tc_kpad", ctypes.c_int32),
-                ("tc_exp", ctypes.c_int32)]
+                ("tc_exp", ctypes.c_int32), ("metric", ctypes.c_int32)]
+
+# snn_metric (include/snn.h)
+METRICS = {"euclidean": 0, "cosine": 1, "angular": 2}
 
 
 _lib = None
@@ -72,6 +75,7 @@ def load_library(path: str = LIB_PATH):
     P, i64, i32, f64 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_double
     sig = {
         "snn_build": ([P, i64, i32, ctypes.c_int, P, ctypes.POINTER(P)], ctypes.c_int),
+        "snn_build_metric": ([P, i64, i32, ctypes.c_int, i32, P, ctypes.POINTER(P)], ctypes.c_int),
         "snn_query_radius": ([P, P, i64, i32, ctypes.c_int, f64, P, ctypes.POINTER(P)], ctypes.c_int),
         "snn_query_self": ([P, f64, P, ctypes.POINTER(P)], ctypes.c_int),
         "snn_result_csr": ([P, ctypes.POINTER(_CSR)], ctypes.c_int),
@@ -164,6 +168,17 @@ def snn_build(X, stream=None):
     p, n, d, code, _keep = _ptr_dtype(X)
     h = ctypes.c_void_p()
     _check(lib.snn_build(p, n, d, code, _stream_ptr(stream), ctypes.byref(h)))
+    return h
+
+
+def snn_build_metric(X, metric, stream=None):
+    """snn_build for metric "euclidean" | "cosine" | "angular" (or its snn_metric code);
+    cosine / angular normalize the rows on the device."""
+    lib = load_library()
+    code_m = METRICS[metric] if isinstance(metric, str) else int(metric)
+    p, n, d, code, _keep = _ptr_dtype(X)
+    h = ctypes.c_void_p()
+    _check(lib.snn_build_metric(p, n, d, code, code_m, _stream_ptr(stream), ctypes.byref(h)))
     return h
 
 
@@ -298,8 +313,9 @@ def _fetch(result, device: str, stream=None) -> CSR:
 class Index:
     """Owns an SNN index built on the current CUDA device (Algorithm 1)."""
 
-    def __init__(self, X, stream=None):
-        self._h = snn_build(X, stream)
+    def __init__(self, X, stream=None, metric: str = "euclidean"):
+        self._h = snn_build_metric(X, metric, stream)
+        self.metric = metric
         info = snn_index_info(self._h)
         self.n, self.d = int(info["n"]), int(info["d"])
         self.dtype = "f64" if info["dtype"] == SNN_F64 else "f32"

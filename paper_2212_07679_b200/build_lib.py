@@ -7,7 +7,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "lib")
 OUT = os.path.join(OUT_DIR, "libsnn.so")
-SOURCES = ["api.cu", "build.cu", "radix_sort.cu", "scan.cu", "query.cu", "dbscan.cu", "tc.cu", "tc_gram.cu", "csr.cu", "tc_lowd.cu"]
+SOURCES = ["api.cu", "build.cu", "radix_sort.cu", "scan.cu", "query.cu", "dbscan.cu", "tc.cu", "tc_gram.cu", "csr.cu", "tc_lowd.cu", "metric.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]

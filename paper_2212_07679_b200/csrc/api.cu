@@ -328,7 +328,7 @@ snn_status snn_set_option(const char *key, int64_t value) {
     return fail(SNN_ERR_INVALID_ARGUMENT, "unknown option " + k);
 }
 
-snn_status snn_build(const void *X, int64_t n, int32_t d, snn_dtype dt, void *stream, snn_index *out) {
+static snn_status build_impl(const void *X, int64_t n, int32_t d, snn_dtype dt, void *stream, snn_index *out) {
     if (!out) return fail(SNN_ERR_INVALID_ARGUMENT, "NULL output handle");
     *out = nullptr;
     if (n == 0) return fail(SNN_ERR_EMPTY, "empty dataset");
@@ -1101,8 +1101,92 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
     return SNN_OK;
 }
 
+snn_status snn_build(const void *X, int64_t n, int32_t d, snn_dtype dt, void *stream, snn_index *out) {
+    return build_impl(X, n, d, dt, stream, out);
+}
+
+// Metric adapters: COSINE / ANGULAR run the exact Euclidean machinery
+// on rows normalized by launch_normalize_rows, with the radius mapped by metric_radius.
+static snn_status normalized_copy(const void *X, int64_t n, int32_t d, snn_dtype dt, cudaStream_t s,
+                                  Workspace &ws, const void **Xn) {
+    const size_t es = dt == SNN_F64 ? 8 : 4;
+    const void *Xd = X;
+    if (!is_device_ptr(X)) {
+        uint8_t *tmp = nullptr;
+        CK(ws.alloc(&tmp, (size_t)n * d * es), "alloc staging");
+        CK(cudaMemcpyAsync(tmp, X, (size_t)n * d * es, cudaMemcpyHostToDevice, s), "H2D");
+        Xd = tmp;
+    }
+    uint8_t *u = nullptr;
+    int *flag = nullptr;
+    CK(ws.alloc(&u, (size_t)n * d * es), "alloc normalized rows");
+    CK(ws.alloc(&flag, 1), "alloc");
+    CK(cudaMemsetAsync(flag, 0, 4, s), "memset");
+    launch_normalize_rows(Xd, dt == SNN_F64, n, d, u, flag, s);
+    int h = 0;
+    CK(cudaMemcpyAsync(&h, flag, 4, cudaMemcpyDeviceToHost, s), "D2H flag");
+    CK(cudaStreamSynchronize(s), "normalize");
+    if (h) return fail(SNN_ERR_INVALID_ARGUMENT, "zero row: cosine / angular distance undefined");
+    *Xn = u;
+    return SNN_OK;
+}
+
+static bool metric_radius_ok(double r) { return r >= 0.0 && isfinite(r); }
+
+snn_status snn_build_metric(const void *X, int64_t n, int32_t d, snn_dtype dt, int32_t metric, void *stream,
+                            snn_index *out) {
+    if (metric < SNN_METRIC_EUCLIDEAN || metric > SNN_METRIC_ANGULAR) {
+        if (out) *out = nullptr;
+        return fail(SNN_ERR_INVALID_ARGUMENT, "unknown metric");
+    }
+    if (metric == SNN_METRIC_EUCLIDEAN) return build_impl(X, n, d, dt, stream, out);
+    if (!out) return fail(SNN_ERR_INVALID_ARGUMENT, "NULL output handle");
+    *out = nullptr;
+    if (n == 0) return fail(SNN_ERR_EMPTY, "empty dataset");
+    if (!X || n < 0 || d < 1 || (dt != SNN_F32 && dt != SNN_F64))
+        return fail(SNN_ERR_INVALID_ARGUMENT, "invalid argument to snn_build_metric");
+    if (n >= (int64_t(1) << 30)) return fail(SNN_ERR_UNSUPPORTED, "n >= 2^30 is not supported");
+    int sms = 0;
+    snn_status st = device_check(&sms);
+    if (st != SNN_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Workspace ws(s);
+    const void *Xn = nullptr;
+    if ((st = normalized_copy(X, n, d, dt, s, ws, &Xn)) != SNN_OK) return st;
+    if ((st = build_impl(Xn, n, d, dt, stream, out)) != SNN_OK) return st;
+    (*out)->metric = metric;
+    return SNN_OK;
+}
+
+static snn_status metric_query(snn_index idx, const void *Q, int64_t m, int32_t d, snn_dtype dt, double r,
+                               void *stream, snn_result *out) {
+    if (!out) return fail(SNN_ERR_INVALID_ARGUMENT, "NULL output handle");
+    *out = nullptr;
+    if (m < 0 || !metric_radius_ok(r)) return fail(SNN_ERR_INVALID_ARGUMENT, "negative or non-finite radius / m < 0");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const double Re = metric_radius(idx->metric, r);
+    snn_status st;
+    Workspace ws(s);
+    if (Q && m > 0) {
+        if (d != idx->d || dt != idx->dt) return fail(SNN_ERR_DIM_MISMATCH, "query dimension / dtype differs from the index");
+        const void *Qn = nullptr;
+        int sms = 0;
+        if ((st = device_check(&sms)) != SNN_OK) return st;
+        if ((st = normalized_copy(Q, m, d, dt, s, ws, &Qn)) != SNN_OK) return st;
+        st = query_impl(idx, Qn, m, d, dt, Re, stream, out);
+    } else {
+        st = query_impl(idx, Q, m, d, dt, Re, stream, out);
+    }
+    if (st != SNN_OK) return st;
+    launch_metric_distances(idx->metric, (*out)->distances, (*out)->nnz, s);
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) { snn_result_free(*out); *out = nullptr; return cuda_fail(e, "metric distances"); }
+    return SNN_OK;
+}
+
 snn_status snn_query_radius(snn_index idx, const void *Q, int64_t m, int32_t d, snn_dtype dt,
                             double R, void *stream, snn_result *out) {
+    if (idx && idx->metric != SNN_METRIC_EUCLIDEAN && Q) return metric_query(idx, Q, m, d, dt, R, stream, out);
     if (!Q && m > 0) return fail(SNN_ERR_INVALID_ARGUMENT, "NULL query pointer");
     if (!Q) {   // m == 0 with NULL Q: still validate the header
         if (out) *out = nullptr;
@@ -1119,6 +1203,7 @@ snn_status snn_query_radius(snn_index idx, const void *Q, int64_t m, int32_t d, 
 
 snn_status snn_query_self(snn_index idx, double R, void *stream, snn_result *out) {
     if (!idx) return fail(SNN_ERR_INVALID_ARGUMENT, "NULL index");
+    if (idx->metric != SNN_METRIC_EUCLIDEAN) return metric_query(idx, nullptr, idx->n, idx->d, idx->dt, R, stream, out);
     return query_impl(idx, nullptr, idx->n, idx->d, idx->dt, R, stream, out);
 }
 
@@ -1161,6 +1246,7 @@ snn_status snn_index_info(snn_index idx, snn_index_info_t *info) {
     info->tc_operand = idx->tc ? (idx->tc_f16 ? 1 : 2) : 0;
     info->tc_kpad = idx->kpad;
     info->tc_exp = idx->xexp;
+    info->metric = idx->metric;
     return SNN_OK;
 }
 
@@ -1171,6 +1257,7 @@ snn_status snn_dbscan(snn_index idx, double eps, int32_t min_pts, int32_t *label
     int sms = 0;
     snn_status st = device_check(&sms);
     if (st != SNN_OK) return st;
+    eps = metric_radius(idx->metric, eps);   // PAPER.md:57-72 (identity for EUCLIDEAN)
     const int tok = prof_begin(F_DBSCAN, static_cast<cudaStream_t>(stream));
     if (idx->ld == 0) {   // low d: fused passes over the windows, neighbour lists never built
         st = dbscan_impl(idx, eps, min_pts, labels, n_clusters, static_cast<cudaStream_t>(stream));

@@ -65,6 +65,7 @@ struct snn_index_s {
     int xexp = 0;              // FP16 operand scale exponent of the index copy
     int kpad = 0;              // K padded to 64 (FP16) / 32 (TF32)
     void *Xt = nullptr;        // n x kpad centred tensor-core operand copy (FP16 or TF32)
+    int metric = 0;            // snn_metric (COSINE / ANGULAR: rows normalized at build)
     float *Xf = nullptr;       // low-d fp32: expanded-form filter rows (AoSoA4, d+1 floats)
     double xf_c1h = 1.0;       // c1h the filter rows were built with
     std::vector<void *> owned;
@@ -80,6 +81,11 @@ struct snn_result_s {
 
 namespace snn {
 bool dbscan_simt_filter();   // option simt_filter (api.cu)
+// metric adapters (metric.cu): exact row normalization (flag = 1 on a zero row), radius
+// mapping and in-place distance conversion
+void launch_normalize_rows(const void *X, bool f64, int64_t n, int d, void *out, int *zero_flag, cudaStream_t s);
+double metric_radius(int metric, double r);
+void launch_metric_distances(int metric, float *dist, int64_t nnz, cudaStream_t s);
 snn_status dbscan_from_csr(const int64_t *off, const int32_t *nidx, int64_t n, int32_t min_pts, int32_t *labels,
                            int32_t *n_clusters, cudaStream_t s);
 snn_status dbscan_impl(snn_index idx, double eps, int32_t min_pts, int32_t *labels,

@@ -612,3 +612,90 @@ def test_tc_tile_edges_and_tiles_option(snn):
         p.snn_set_option("tc_tiles", 0)
         p.snn_set_option("tc_f16", 0)
         p.snn_set_option("tc_ares", 0)
+
+
+# --------------------------------------------------------------------------- metrics (f3)
+def _metric_compare(gpu, ora, metric):
+    """Row sets identical (ids sorted per row) and distances equal to the oracle's metric
+    value of float32(sqrt(s)): cosine bit for bit (fp64 e^2/2 on both sides), angular
+    within 1 float32 ulp (device vs libm asin)."""
+    g_off, o_off = np.asarray(gpu.offsets), np.asarray(ora["offsets"])
+    np.testing.assert_array_equal(g_off, o_off)
+    g_idx, g_d = np.asarray(gpu.indices), np.asarray(gpu.distances)
+    rows = np.repeat(np.arange(len(g_off) - 1), np.diff(g_off))
+    order = np.lexsort((g_idx, rows))
+    np.testing.assert_array_equal(g_idx[order], ora["indices"])
+    if metric == "cosine":
+        np.testing.assert_array_equal(g_d[order], ora["dist"])
+    else:
+        np.testing.assert_array_max_ulp(g_d[order], ora["dist"], maxulp=1)
+
+
+@pytest.mark.parametrize("metric", ["cosine", "angular"])
+@pytest.mark.parametrize("n,m,d,dt", [(3000, 400, 3, np.float32), (2000, 300, 3, np.float64),
+                                      (1500, 200, 8, np.float32), (900, 120, 64, np.float32),
+                                      (600, 70, 33, np.float64)])
+def test_metric_query_parity(snn, metric, n, m, d, dt):
+    rng = np.random.default_rng(700 + d)
+    X = (rng.standard_normal((n, d)) + 0.3).astype(dt)
+    Q = (rng.standard_normal((m, d)) + 0.3).astype(dt)
+    # radius at a small quantile of the metric over a sample
+    U, V = oracle.normalize_rows(X[:300]).astype(np.float64), oracle.normalize_rows(Q[:40]).astype(np.float64)
+    cosd = 1.0 - V @ U.T
+    q = float(np.quantile(cosd, 0.02))
+    r = q if metric == "cosine" else float(np.arccos(1.0 - q))
+    idx = snn.Index(_dev(X), metric=metric)
+    try:
+        assert idx.info()["metric"] == oracle.METRICS[metric]
+        gpu = idx.query(_dev(Q), r)
+        ora = oracle.metric_radius_query(X, Q, r, metric)
+        assert ora["offsets"][-1] > m
+        _metric_compare(gpu, ora, metric)
+        gpu_h = idx.query(Q, r)                  # host queries (normalized on the device)
+        _metric_compare(gpu_h, ora, metric)
+        gs = idx.query_self(r)
+        _metric_compare(gs, oracle.metric_radius_query(X, X, r, metric), metric)
+    finally:
+        idx.free()
+
+
+@pytest.mark.parametrize("metric,d", [("cosine", 3), ("angular", 3), ("cosine", 40)])
+def test_metric_dbscan_parity(snn, metric, d):
+    rng = np.random.default_rng(800 + d)
+    if d <= 3:
+        X = (rng.standard_normal((3000, d)) + 0.2).astype(np.float32)
+        eps = 0.004 if metric == "cosine" else 0.09
+    else:                                        # 10 directional clusters + 100 outliers
+        C = rng.standard_normal((10, d))
+        X = np.concatenate([C[rng.integers(0, 10, 2900)] + 0.3 * rng.standard_normal((2900, d)),
+                            rng.standard_normal((100, d))]).astype(np.float32)
+        eps = 0.1
+    idx = snn.Index(_dev(X), metric=metric)
+    try:
+        labels, K = idx.dbscan(eps, 5)
+    finally:
+        idx.free()
+    lab, K_o, _ = oracle.dbscan(oracle.normalize_rows(X), oracle.metric_radius(metric, eps), 5)
+    assert K == K_o and K > 1
+    np.testing.assert_array_equal(labels, lab)
+
+
+def test_metric_errors(snn):
+    X = np.ones((100, 4), dtype=np.float32)
+    X[50] = 0.0
+    with pytest.raises(snn.SnnError, match="INVALID_ARGUMENT"):
+        snn.Index(_dev(X), metric="cosine")
+    X[50] = 1.0
+    idx = snn.Index(_dev(X), metric="angular")
+    try:
+        Q = np.zeros((3, 4), dtype=np.float32)
+        with pytest.raises(snn.SnnError, match="INVALID_ARGUMENT"):
+            idx.query(_dev(Q), 0.1)
+        with pytest.raises(snn.SnnError, match="INVALID_ARGUMENT"):
+            idx.query_self(-0.1)
+        gs = idx.query_self(4.0)                  # alpha >= pi: every pair
+        assert int(np.asarray(gs.offsets)[-1]) == 100 * 100
+    finally:
+        idx.free()
+    with pytest.raises(snn.SnnError, match="INVALID_ARGUMENT"):
+        snn.snn_build_metric(_dev(X), 7)

@@ -347,3 +347,45 @@ def test_dbscan_vs_scipy_csgraph(seed):
             ref[i] = ref[min(cn)]
     assert K == len(order)
     assert (ref == lab).all()
+
+
+# ---------------------------------------------------------------- metrics
+def test_metric_hand_values():
+    """Textbook values of the definitions and of the reductions."""
+    assert oracle.cosine_distance([1, 0], [0, 1]) == pytest.approx(1.0)
+    assert oracle.cosine_distance([1, 0], [-3, 0]) == pytest.approx(2.0)
+    assert oracle.cosine_distance([1, 1], [2, 2]) == pytest.approx(0.0, abs=1e-15)
+    assert oracle.angular_distance([1, 0], [0, 5]) == pytest.approx(math.pi / 2)
+    assert oracle.angular_distance([1, 0], [1, 1]) == pytest.approx(math.pi / 4)
+    np.testing.assert_array_equal(oracle.normalize_rows(np.array([[3.0, 4.0]])), [[0.6, 0.8]])
+    # unit vectors at angle a have chord 2 sin(a/2): both radius maps and the inverse
+    for a in (0.1, 0.7, math.pi / 2, 2.5):
+        chord = 2 * math.sin(a / 2)
+        assert oracle.metric_radius("angular", a) == pytest.approx(chord, rel=1e-12)
+        assert oracle.metric_radius("cosine", 1 - math.cos(a)) == pytest.approx(chord, rel=1e-12)
+        assert float(oracle.metric_distance("angular", np.float32(chord))) == pytest.approx(a, rel=1e-6)
+        assert float(oracle.metric_distance("cosine", np.float32(chord))) == pytest.approx(1 - math.cos(a), rel=1e-6)
+    assert oracle.metric_radius("angular", math.pi) >= 2.0
+    with pytest.raises(ValueError):
+        oracle.normalize_rows(np.array([[1.0, 2.0], [0.0, 0.0]]))
+
+
+@pytest.mark.parametrize("metric,dtype", [("cosine", np.float64), ("angular", np.float64),
+                                          ("cosine", np.float32), ("angular", np.float32)])
+def test_metric_query_matches_definition(metric, dtype):
+    """The Euclidean reduction on normalized rows returns exactly the pairs the direct
+    definition puts within r (pairs within 1e-6 of the boundary excluded), with the metric
+    value of each hit within float32 rounding of the definition."""
+    rng = np.random.default_rng(7)
+    P = (rng.standard_normal((150, 5)) + 0.5).astype(dtype)
+    Q = (rng.standard_normal((40, 5)) + 0.5).astype(dtype)
+    direct = oracle.cosine_distance if metric == "cosine" else oracle.angular_distance
+    r = 0.3 if metric == "cosine" else 0.8
+    out = oracle.metric_radius_query(P, Q, r, metric)
+    got = {(j, int(i)) for j in range(len(Q)) for i in out["indices"][out["offsets"][j]:out["offsets"][j + 1]]}
+    D = np.array([[direct(q, p) for p in P] for q in Q])
+    want = {(j, i) for j in range(len(Q)) for i in range(len(P)) if D[j, i] <= r}
+    amb = {(j, i) for j in range(len(Q)) for i in range(len(P)) if abs(D[j, i] - r) <= 1e-6}
+    assert (got ^ want) <= amb and len(want) > 50
+    rows = np.repeat(np.arange(len(Q)), np.diff(out["offsets"]))
+    np.testing.assert_allclose(out["dist"], D[rows, out["indices"]], atol=2e-6)
