@@ -44,8 +44,20 @@ typedef enum { SNN_F32 = 0, SNN_F64 = 1 } snn_dtype;
  * rule u_k = x_k / sqrt(sum_k x_k^2) (fp64, left-to-right sum, correctly rounded sqrt and
  * division, then rounded to the input dtype); the search itself is the exact Euclidean
  * search on the normalized rows with the mapped radius (computed in fp64), and returned
- * distances are converted back to the metric (r = d^2 / 2, alpha = 2 asin(d / 2)). */
-typedef enum { SNN_METRIC_EUCLIDEAN = 0, SNN_METRIC_COSINE = 1, SNN_METRIC_ANGULAR = 2 } snn_metric;
+ * distances are converted back to the metric (r = d^2 / 2, alpha = 2 asin(d / 2)).
+ *  MANHATTAN  ||p - q||_1 <= R.  Since ||.||_2 <= ||.||_1 the Euclidean search with the same
+ *             R returns a superset; an exact fp64 post-filter (sum of
+ *             |p_k - q_k| left to right) keeps the hits; distance = float(L1).
+ *  MIPS       inner-product similarity p^T q >= tau (the radius argument is tau, any finite
+ *             value): the index holds p~ = [sqrt(xi^2 - |p|^2), p],
+ *             xi = max |p|, queries q~ = [0, q], so |p~ - q~|^2 = xi^2 + |q|^2 - 2 p^T q; the
+ *             Euclidean search with radius^2 = (xi^2 + max|q|^2)(1 + 4e-6) - 2 tau (+ slack)
+ *             returns a superset, an exact fp64 post-filter (sum of p_k q_k left to right)
+ *             keeps p^T q >= tau; "distance" = float(p^T q).  snn_index_info.d is d + 1.
+ *  MANHATTAN / MIPS keep a copy of the input rows for the filter; snn_dbscan rejects them
+ *  (SNN_ERR_UNSUPPORTED). */
+typedef enum { SNN_METRIC_EUCLIDEAN = 0, SNN_METRIC_COSINE = 1, SNN_METRIC_ANGULAR = 2,
+               SNN_METRIC_MANHATTAN = 3, SNN_METRIC_MIPS = 4 } snn_metric;
 
 typedef enum {
     SNN_OK = 0,

@@ -19,6 +19,9 @@ Contents (each function cites the passage it follows):
   ``cosine_distance``, ``angular_distance``   cosine / angular distance through the
                         Euclidean search on normalized rows (DESIGN.md
                         reading C21); the direct definitions pin the reduction.
+* ``manhattan_query``, ``inner_product_query``, ``mips_transform``   Manhattan radius
+                        search and inner-product threshold search (MIPS
+                        transform), brute force by definition (reading C22).
 
 Parity pins live in ``tests/test_oracle.py`` (hand examples, closed forms, library
 cross-checks, invariants).  No function here is "parity unpinned".
@@ -309,3 +312,50 @@ def metric_radius_query(P, Q, r: float, metric: str) -> dict:
     out["dist"] = metric_distance(metric, np.sqrt(out["s"]).astype(np.float32))
     out["U"], out["V"] = U, V
     return out
+
+
+def manhattan_query(P, Q, R: float) -> dict:
+    """Brute force ||p_i - q_j||_1 <= R: fp64 sum of |p_k - q_k| left to
+    right (reading C22).  CSR over queries, ids ascending, ``dist`` = float32(L1)."""
+    P, Q = _f64(P), _f64(Q)
+    offs, ids, vals = [0], [], []
+    for q in Q:
+        v = np.zeros(P.shape[0])
+        for k in range(P.shape[1]):
+            v = v + np.abs(P[:, k] - q[k])
+        hit = np.nonzero(v <= R)[0]
+        ids.append(hit)
+        vals.append(v[hit])
+        offs.append(offs[-1] + len(hit))
+    return {"offsets": np.array(offs, dtype=np.int64),
+            "indices": np.concatenate(ids).astype(np.int32) if ids else np.zeros(0, np.int32),
+            "dist": np.concatenate(vals).astype(np.float32) if vals else np.zeros(0, np.float32)}
+
+
+def inner_product_query(P, Q, tau: float) -> dict:
+    """Brute force p_i^T q_j >= tau (the fixed-threshold form of PAPER.md:73-78's maximum
+    inner product similarity, reading C22): fp64 sum of p_k q_k left to right, no FMA.
+    CSR over queries, ids ascending, ``dist`` = float32(p^T q)."""
+    P, Q = _f64(P), _f64(Q)
+    offs, ids, vals = [0], [], []
+    for q in Q:
+        v = np.zeros(P.shape[0])
+        for k in range(P.shape[1]):
+            v = v + P[:, k] * q[k]
+        hit = np.nonzero(v >= tau)[0]
+        ids.append(hit)
+        vals.append(v[hit])
+        offs.append(offs[-1] + len(hit))
+    return {"offsets": np.array(offs, dtype=np.int64),
+            "indices": np.concatenate(ids).astype(np.int32) if ids else np.zeros(0, np.int32),
+            "dist": np.concatenate(vals).astype(np.float32) if vals else np.zeros(0, np.float32)}
+
+
+def mips_transform(P, Q):
+    """PAPER.md:73-76: p~_i = [sqrt(xi^2 - |p_i|^2), p_i], xi = max_i |p_i|, q~ = [0, q] (fp64)."""
+    P, Q = _f64(P), _f64(Q)
+    n2 = (P * P).sum(axis=1)
+    xi2 = n2.max()
+    Pt = np.concatenate([np.sqrt(np.maximum(0.0, xi2 - n2))[:, None], P], axis=1)
+    Qt = np.concatenate([np.zeros((Q.shape[0], 1)), Q], axis=1)
+    return Pt, Qt, float(xi2)

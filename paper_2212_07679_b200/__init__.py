@@ -57,7 +57,7 @@ class _Info(ctypes.Structure):
                 ("tc_exp", ctypes.c_int32), ("metric", ctypes.c_int32)]
 
 # snn_metric (include/snn.h)
-METRICS = {"euclidean": 0, "cosine": 1, "angular": 2}
+METRICS = {"euclidean": 0, "cosine": 1, "angular": 2, "manhattan": 3, "mips": 4}
 
 
 _lib = None

@@ -1133,13 +1133,147 @@ static snn_status normalized_copy(const void *X, int64_t n, int32_t d, snn_dtype
 
 static bool metric_radius_ok(double r) { return r >= 0.0 && isfinite(r); }
 
+// device copy of n x d rows (host input staged); owned by ws
+static snn_status device_rows(const void *X, int64_t n, int32_t d, size_t es, cudaStream_t s, Workspace &ws,
+                              const void **Xd) {
+    if (is_device_ptr(X)) { *Xd = X; return SNN_OK; }
+    uint8_t *tmp = nullptr;
+    CK(ws.alloc(&tmp, (size_t)n * d * es), "alloc staging");
+    CK(cudaMemcpyAsync(tmp, X, (size_t)n * d * es, cudaMemcpyHostToDevice, s), "H2D");
+    *Xd = tmp;
+    return SNN_OK;
+}
+
+// MANHATTAN: index of the input rows; MIPS: index of p~ = [sqrt(xi^2 - |p|^2), p]
+// (PAPER.md:73-76).  Both keep the input rows (original order) for the exact post-filter.
+static snn_status build_filtered(const void *X, int64_t n, int32_t d, snn_dtype dt, int32_t metric, void *stream,
+                                 snn_index *out) {
+    if (!out) return fail(SNN_ERR_INVALID_ARGUMENT, "NULL output handle");
+    *out = nullptr;
+    if (n == 0) return fail(SNN_ERR_EMPTY, "empty dataset");
+    if (!X || n < 0 || d < 1 || (dt != SNN_F32 && dt != SNN_F64))
+        return fail(SNN_ERR_INVALID_ARGUMENT, "invalid argument to snn_build_metric");
+    if (n >= (int64_t(1) << 30)) return fail(SNN_ERR_UNSUPPORTED, "n >= 2^30 is not supported");
+    int sms = 0;
+    snn_status st = device_check(&sms);
+    if (st != SNN_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t es = dt == SNN_F64 ? 8 : 4;
+    Workspace ws(s);
+    const void *Xd = nullptr;
+    if ((st = device_rows(X, n, d, es, s, ws, &Xd)) != SNN_OK) return st;
+    void *Xo = nullptr;
+    CK(cudaMallocAsync(&Xo, (size_t)n * d * es, s), "alloc Xo");
+    cudaError_t e = cudaMemcpyAsync(Xo, Xd, (size_t)n * d * es, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) { cudaFreeAsync(Xo, s); return cuda_fail(e, "copy Xo"); }
+    double xi2 = 0.0;
+    if (metric == SNN_METRIC_MIPS) {
+        double *nrm2 = nullptr;
+        unsigned long long *mx = nullptr;
+        uint8_t *Xt = nullptr;
+        if (ws.alloc(&nrm2, (size_t)n) != cudaSuccess || ws.alloc(&mx, 1) != cudaSuccess ||
+            ws.alloc(&Xt, (size_t)n * (d + 1) * es) != cudaSuccess) {
+            cudaFreeAsync(Xo, s);
+            return fail(SNN_ERR_OUT_OF_MEMORY, "alloc MIPS rows");
+        }
+        cudaMemsetAsync(mx, 0, 8, s);
+        launch_sq_norms(Xd, dt == SNN_F64, n, d, nrm2, mx, s);
+        launch_mips_rows(Xd, dt == SNN_F64, n, d, nrm2, mx, Xt, s);
+        unsigned long long h = 0;
+        cudaMemcpyAsync(&h, mx, 8, cudaMemcpyDeviceToHost, s);
+        if ((e = cudaStreamSynchronize(s)) != cudaSuccess) { cudaFreeAsync(Xo, s); return cuda_fail(e, "MIPS rows"); }
+        memcpy(&xi2, &h, 8);
+        st = build_impl(Xt, n, d + 1, dt, stream, out);
+    } else {
+        st = build_impl(Xd, n, d, dt, stream, out);
+    }
+    if (st != SNN_OK) { cudaFreeAsync(Xo, s); return st; }
+    (*out)->metric = metric;
+    (*out)->d_in = d;
+    (*out)->Xo = Xo;
+    (*out)->owned.push_back(Xo);
+    (*out)->xi2 = xi2;
+    return SNN_OK;
+}
+
+// MANHATTAN / MIPS query: Euclidean candidate superset, then the exact post-filter
+static snn_status filtered_query(snn_index idx, const void *Q, int64_t m, double r, void *stream, snn_result *out) {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const bool f64 = idx->dt == SNN_F64;
+    const size_t es = f64 ? 8 : 4;
+    const int d = idx->d_in;
+    Workspace ws(s);
+    snn_status st;
+    const void *Qo = idx->Xo;   // self query: the index's own input rows
+    if (Q && (st = device_rows(Q, m, d, es, s, ws, &Qo)) != SNN_OK) return st;
+    snn_result cand = nullptr;
+    double thr = r;
+    if (idx->metric == SNN_METRIC_MANHATTAN) {   // ||.||_2 <= ||.||_1: the L2 ball of radius r covers the L1 ball
+        st = Q ? query_impl(idx, Qo, m, d, idx->dt, r, stream, &cand) : query_impl(idx, nullptr, m, d, idx->dt, r, stream, &cand);
+    } else {   // p^T q >= tau  =>  ||p~ - q~||^2 = |p~|^2 + |q|^2 - 2 p^T q <= xi^2 (1 + 2^-20) + |q|^2 - 2 tau
+        double *nrm2 = nullptr;
+        unsigned long long *mx = nullptr;
+        uint8_t *Qt = nullptr;
+        CK(ws.alloc(&nrm2, (size_t)m), "alloc");
+        CK(ws.alloc(&mx, 1), "alloc");
+        CK(ws.alloc(&Qt, (size_t)m * (d + 1) * es), "alloc");
+        CK(cudaMemsetAsync(mx, 0, 8, s), "memset");
+        launch_sq_norms(Qo, f64, m, d, nrm2, mx, s);
+        launch_mips_rows(Qo, f64, m, d, nrm2, nullptr, Qt, s);
+        unsigned long long h = 0;
+        CK(cudaMemcpyAsync(&h, mx, 8, cudaMemcpyDeviceToHost, s), "D2H");
+        CK(cudaStreamSynchronize(s), "MIPS queries");
+        double q2;
+        memcpy(&q2, &h, 8);
+        // slack 4e-6 relative covers the rounded first coordinate (<= 2^-20 of xi^2) and the
+        // fp64 rounding of the search's squared distances
+        const double R2 = (idx->xi2 + q2) * (1.0 + 4e-6) - 2.0 * r + 8e-6 * fabs(r);
+        const double Re = R2 > 0.0 ? sqrt(R2) : 0.0;
+        st = query_impl(idx, Qt, m, d + 1, idx->dt, Re, stream, &cand);
+    }
+    if (st != SNN_OK) return st;
+    const int64_t nnz = cand->nnz;
+    uint8_t *keep = nullptr;
+    float *val = nullptr;
+    int32_t *rowcnt = nullptr;
+    void *temp = nullptr;
+    snn_result r2 = new snn_result_s();
+    r2->m = m;
+    auto bail = [&](cudaError_t e, const char *w) { snn_result_free(cand); snn_result_free(r2); return cuda_fail(e, w); };
+    cudaError_t e;
+    if ((e = ws.alloc(&keep, (size_t)nnz)) != cudaSuccess) return bail(e, "alloc");
+    if ((e = ws.alloc(&val, (size_t)nnz)) != cudaSuccess) return bail(e, "alloc");
+    if ((e = ws.alloc(&rowcnt, (size_t)m + 1)) != cudaSuccess) return bail(e, "alloc");
+    if ((e = ws.alloc((uint8_t **)&temp, scan_temp_bytes(m + 1))) != cudaSuccess) return bail(e, "alloc");
+    void *p = nullptr;
+    if ((e = cudaMallocAsync(&p, (size_t)(m + 1) * 8, s)) != cudaSuccess) return bail(e, "alloc offsets");
+    r2->offsets = static_cast<int64_t *>(p);
+    cudaMemsetAsync(rowcnt + m, 0, 4, s);
+    launch_csr_filter(idx->metric, f64, cand->offsets, m, cand->indices, idx->Xo, Qo, d, thr, keep, val, rowcnt, s);
+    exclusive_scan_i32_to_i64(rowcnt, r2->offsets, m + 1, temp, s);
+    int64_t tot = 0;
+    if ((e = cudaMemcpyAsync(&tot, r2->offsets + m, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return bail(e, "D2H");
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return bail(e, "filter");
+    r2->nnz = tot;
+    if ((e = cudaMallocAsync(&p, (size_t)(tot > 0 ? tot : 1) * 4, s)) != cudaSuccess) return bail(e, "alloc");
+    r2->indices = static_cast<int32_t *>(p);
+    if ((e = cudaMallocAsync(&p, (size_t)(tot > 0 ? tot : 1) * 4, s)) != cudaSuccess) return bail(e, "alloc");
+    r2->distances = static_cast<float *>(p);
+    launch_csr_compact(cand->offsets, m, cand->indices, keep, val, r2->offsets, r2->indices, r2->distances, s);
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return bail(e, "compact");
+    snn_result_free(cand);
+    *out = r2;
+    return SNN_OK;
+}
+
 snn_status snn_build_metric(const void *X, int64_t n, int32_t d, snn_dtype dt, int32_t metric, void *stream,
                             snn_index *out) {
-    if (metric < SNN_METRIC_EUCLIDEAN || metric > SNN_METRIC_ANGULAR) {
+    if (metric < SNN_METRIC_EUCLIDEAN || metric > SNN_METRIC_MIPS) {
         if (out) *out = nullptr;
         return fail(SNN_ERR_INVALID_ARGUMENT, "unknown metric");
     }
     if (metric == SNN_METRIC_EUCLIDEAN) return build_impl(X, n, d, dt, stream, out);
+    if (metric == SNN_METRIC_MANHATTAN || metric == SNN_METRIC_MIPS) return build_filtered(X, n, d, dt, metric, stream, out);
     if (!out) return fail(SNN_ERR_INVALID_ARGUMENT, "NULL output handle");
     *out = nullptr;
     if (n == 0) return fail(SNN_ERR_EMPTY, "empty dataset");
@@ -1155,6 +1289,7 @@ snn_status snn_build_metric(const void *X, int64_t n, int32_t d, snn_dtype dt, i
     if ((st = normalized_copy(X, n, d, dt, s, ws, &Xn)) != SNN_OK) return st;
     if ((st = build_impl(Xn, n, d, dt, stream, out)) != SNN_OK) return st;
     (*out)->metric = metric;
+    (*out)->d_in = d;
     return SNN_OK;
 }
 
@@ -1162,7 +1297,18 @@ static snn_status metric_query(snn_index idx, const void *Q, int64_t m, int32_t 
                                void *stream, snn_result *out) {
     if (!out) return fail(SNN_ERR_INVALID_ARGUMENT, "NULL output handle");
     *out = nullptr;
-    if (m < 0 || !metric_radius_ok(r)) return fail(SNN_ERR_INVALID_ARGUMENT, "negative or non-finite radius / m < 0");
+    const bool mips = idx->metric == SNN_METRIC_MIPS;
+    if (m < 0 || !(mips ? isfinite(r) : metric_radius_ok(r)))
+        return fail(SNN_ERR_INVALID_ARGUMENT, "negative or non-finite radius / m < 0");
+    if (Q && m > 0 && (d != idx->d_in || dt != idx->dt))
+        return fail(SNN_ERR_DIM_MISMATCH, "query dimension / dtype differs from the index");
+    if (idx->metric == SNN_METRIC_MANHATTAN || mips) {
+        int sms = 0;
+        snn_status st0 = device_check(&sms);
+        if (st0 != SNN_OK) return st0;
+        if (m == 0) return make_empty_result(0, static_cast<cudaStream_t>(stream), out);
+        return filtered_query(idx, Q, m, r, stream, out);
+    }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const double Re = metric_radius(idx->metric, r);
     snn_status st;
@@ -1257,6 +1403,8 @@ snn_status snn_dbscan(snn_index idx, double eps, int32_t min_pts, int32_t *label
     int sms = 0;
     snn_status st = device_check(&sms);
     if (st != SNN_OK) return st;
+    if (idx->metric == SNN_METRIC_MANHATTAN || idx->metric == SNN_METRIC_MIPS)
+        return fail(SNN_ERR_UNSUPPORTED, "snn_dbscan: Euclidean, cosine and angular indexes only");
     eps = metric_radius(idx->metric, eps);   // PAPER.md:57-72 (identity for EUCLIDEAN)
     const int tok = prof_begin(F_DBSCAN, static_cast<cudaStream_t>(stream));
     if (idx->ld == 0) {   // low d: fused passes over the windows, neighbour lists never built

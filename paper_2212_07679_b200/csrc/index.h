@@ -65,7 +65,10 @@ struct snn_index_s {
     int xexp = 0;              // FP16 operand scale exponent of the index copy
     int kpad = 0;              // K padded to 64 (FP16) / 32 (TF32)
     void *Xt = nullptr;        // n x kpad centred tensor-core operand copy (FP16 or TF32)
-    int metric = 0;            // snn_metric (COSINE / ANGULAR: rows normalized at build)
+    int metric = 0;            // snn_metric (COSINE / ANGULAR: rows normalized at build; MIPS: d = input d + 1)
+    int d_in = 0;              // input dimension (d - 1 for MIPS)
+    void *Xo = nullptr;        // MANHATTAN / MIPS: input rows, original order (post-filter)
+    double xi2 = 0.0;          // MIPS: max_i ||p_i||^2
     float *Xf = nullptr;       // low-d fp32: expanded-form filter rows (AoSoA4, d+1 floats)
     double xf_c1h = 1.0;       // c1h the filter rows were built with
     std::vector<void *> owned;
@@ -86,6 +89,14 @@ bool dbscan_simt_filter();   // option simt_filter (api.cu)
 void launch_normalize_rows(const void *X, bool f64, int64_t n, int d, void *out, int *zero_flag, cudaStream_t s);
 double metric_radius(int metric, double r);
 void launch_metric_distances(int metric, float *dist, int64_t nnz, cudaStream_t s);
+void launch_sq_norms(const void *X, bool f64, int64_t n, int d, double *nrm2, unsigned long long *max_bits,
+                     cudaStream_t s);
+void launch_mips_rows(const void *X, bool f64, int64_t n, int d, const double *nrm2,
+                      const unsigned long long *xi2_bits, void *out, cudaStream_t s);
+void launch_csr_filter(int metric, bool f64, const int64_t *off, int64_t m, const int32_t *ind, const void *Xo,
+                       const void *Qo, int d, double thr, uint8_t *keep, float *val, int32_t *rowcnt, cudaStream_t s);
+void launch_csr_compact(const int64_t *off, int64_t m, const int32_t *ind, const uint8_t *keep, const float *val,
+                        const int64_t *noff, int32_t *nind, float *ndist, cudaStream_t s);
 snn_status dbscan_from_csr(const int64_t *off, const int32_t *nidx, int64_t n, int32_t min_pts, int32_t *labels,
                            int32_t *n_clusters, cudaStream_t s);
 snn_status dbscan_impl(snn_index idx, double eps, int32_t min_pts, int32_t *labels,

@@ -699,3 +699,59 @@ def test_metric_errors(snn):
         idx.free()
     with pytest.raises(snn.SnnError, match="INVALID_ARGUMENT"):
         snn.snn_build_metric(_dev(X), 7)
+
+
+def _filtered_compare(gpu, ora):
+    """Rows identical (ids sorted per row), values bit-identical (fp64 left-to-right sum on
+    both sides, rounded to float32)."""
+    g_off = np.asarray(gpu.offsets)
+    np.testing.assert_array_equal(g_off, ora["offsets"])
+    g_idx, g_d = np.asarray(gpu.indices), np.asarray(gpu.distances)
+    rows = np.repeat(np.arange(len(g_off) - 1), np.diff(g_off))
+    order = np.lexsort((g_idx, rows))
+    np.testing.assert_array_equal(g_idx[order], ora["indices"])
+    np.testing.assert_array_equal(g_d[order], ora["dist"])
+
+
+@pytest.mark.parametrize("n,m,d,dt", [(3000, 300, 2, np.float32), (2000, 200, 3, np.float64),
+                                      (1200, 100, 8, np.float32), (800, 80, 40, np.float32)])
+def test_manhattan_parity(snn, n, m, d, dt):
+    rng = np.random.default_rng(900 + d)
+    X = (rng.standard_normal((n, d)) * rng.uniform(0.5, 2, d)).astype(dt)
+    Q = (rng.standard_normal((m, d)) * rng.uniform(0.5, 2, d)).astype(dt)
+    L1 = np.abs(X[:300, None, :].astype(np.float64) - Q[None, :30, :]).sum(-1)
+    R = float(np.quantile(L1, 0.03))
+    idx = snn.Index(_dev(X), metric="manhattan")
+    try:
+        _filtered_compare(idx.query(_dev(Q), R), oracle.manhattan_query(X, Q, R))
+        _filtered_compare(idx.query(Q, R), oracle.manhattan_query(X, Q, R))
+        _filtered_compare(idx.query_self(R), oracle.manhattan_query(X, X, R))
+        with pytest.raises(snn.SnnError, match="UNSUPPORTED"):
+            idx.dbscan(R, 5)
+    finally:
+        idx.free()
+
+
+@pytest.mark.parametrize("n,m,d,dt", [(3000, 300, 3, np.float32), (2000, 200, 5, np.float64),
+                                      (1000, 100, 64, np.float32)])
+def test_inner_product_parity(snn, n, m, d, dt):
+    rng = np.random.default_rng(950 + d)
+    X = (rng.standard_normal((n, d)) * rng.uniform(0.2, 2, (n, 1))).astype(dt)
+    Q = rng.standard_normal((m, d)).astype(dt)
+    G = Q[:30].astype(np.float64) @ X[:300].T.astype(np.float64)
+    tau = float(np.quantile(G, 0.97))
+    idx = snn.Index(_dev(X), metric="mips")
+    try:
+        assert idx.info()["d"] == d + 1
+        ora = oracle.inner_product_query(X, Q, tau)
+        assert ora["offsets"][-1] > m
+        _filtered_compare(idx.query(_dev(Q), tau), ora)
+        _filtered_compare(idx.query_self(tau), oracle.inner_product_query(X, X, tau))
+        # negative threshold: far more pairs, still exact
+        t2 = float(np.quantile(G, 0.6))
+        _filtered_compare(idx.query(_dev(Q[:20]), t2), oracle.inner_product_query(X, Q[:20], t2))
+        # threshold above every product: empty
+        big = float(np.abs(G).max() * 10 + 10)
+        assert int(np.asarray(idx.query(_dev(Q), big).offsets)[-1]) == 0
+    finally:
+        idx.free()

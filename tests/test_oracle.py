@@ -389,3 +389,42 @@ def test_metric_query_matches_definition(metric, dtype):
     assert (got ^ want) <= amb and len(want) > 50
     rows = np.repeat(np.arange(len(Q)), np.diff(out["offsets"]))
     np.testing.assert_allclose(out["dist"], D[rows, out["indices"]], atol=2e-6)
+
+
+def test_manhattan_and_inner_product_oracles():
+    """Brute-force L1 / inner-product searches against scipy's cityblock distance and the
+    BLAS product (away from the threshold), plus the two facts the GPU reductions rest on:
+    every L1 hit is an L2 hit for the same R, and the MIPS transform gives
+    |p~ - q~|^2 = xi^2 + |q|^2 - 2 p^T q."""
+    from scipy.spatial.distance import cdist
+    rng = np.random.default_rng(11)
+    P = rng.standard_normal((300, 6))
+    Q = rng.standard_normal((30, 6))
+    R = 2.5
+    man = oracle.manhattan_query(P, Q, R)
+    D1 = cdist(Q, P, "cityblock")
+    rows = np.repeat(np.arange(30), np.diff(man["offsets"]))
+    got = set(zip(rows.tolist(), man["indices"].tolist()))
+    want = set(zip(*np.nonzero(D1 <= R)))
+    amb = set(zip(*np.nonzero(np.abs(D1 - R) < 1e-9)))
+    assert (got ^ want) <= amb and len(want) > 30
+    np.testing.assert_allclose(man["dist"], D1[rows, man["indices"]], rtol=1e-6)
+    l2 = oracle.radius_query(P, Q, R, band_rel=0.0)
+    l2rows = np.repeat(np.arange(30), np.diff(l2["offsets"]))
+    assert got <= set(zip(l2rows.tolist(), l2["indices"].tolist()))
+    tau = 2.0
+    ip = oracle.inner_product_query(P, Q, tau)
+    G = Q @ P.T
+    rows = np.repeat(np.arange(30), np.diff(ip["offsets"]))
+    got = set(zip(rows.tolist(), ip["indices"].tolist()))
+    want = set(zip(*np.nonzero(G >= tau)))
+    amb = set(zip(*np.nonzero(np.abs(G - tau) < 1e-9)))
+    assert (got ^ want) <= amb and len(want) > 30
+    np.testing.assert_allclose(ip["dist"], G[rows, ip["indices"]], rtol=1e-6, atol=1e-6)
+    Pt, Qt, xi2 = oracle.mips_transform(P, Q)
+    np.testing.assert_allclose(np.linalg.norm(Pt, axis=1) ** 2, xi2, rtol=1e-12)
+    lhs = ((Pt[None, :, :] - Qt[:, None, :]) ** 2).sum(-1)
+    rhs = xi2 + (Q * Q).sum(1)[:, None] - 2 * G
+    np.testing.assert_allclose(lhs, rhs, rtol=1e-10, atol=1e-10)
+    # the argmax statement of PAPER.md:76
+    np.testing.assert_array_equal(lhs.argmin(axis=1), G.argmax(axis=1))
