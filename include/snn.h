@@ -121,6 +121,27 @@ typedef struct {
 snn_status snn_build(const void *X, int64_t n, int32_t d, snn_dtype dt, void *stream,
                      snn_index *out);
 
+/* Streaming append ("applicable in an online streaming setting"): adds k rows Y
+ * (k x d row-major, device or host pointer, the index's dtype; the index's metric applies,
+ * COSINE / ANGULAR rows are normalized) with ids n .. n+k-1.  mu and v1 stay frozen: the
+ * window bound of eq:lower holds for any fixed unit vector and centring,
+ * so results stay exact; only pruning may degrade if the new rows drift.  Keys of the new
+ * rows under (mu, v1), one stable re-sort (ties by original id), key error bounds and the
+ * tensor-core operand copy recomputed.  Errors: DIM_MISMATCH; NONFINITE (index unchanged);
+ * UNSUPPORTED for MIPS (xi would change) or n + k >= 2^30.  k = 0 is a no-op.
+ * Synchronizes the stream. */
+snn_status snn_append(snn_index idx, const void *Y, int64_t k, int32_t d, snn_dtype dt, void *stream);
+
+/* Save / load the built index (all device arrays; no rebuild on load).  File: "SNNG",
+ * u32 version 1, 23 int64 header words, then the arrays in a fixed order, little endian.
+ * snn_load validates the magic ("bad magic"), version ("unsupported version"), header
+ * ("invalid header"), length ("truncated" / "trailing bytes") and the index invariants
+ * (keys sorted and finite, perm a permutation) before touching the device; all of these
+ * return SNN_ERR_INVALID_ARGUMENT.  A loaded index answers queries bit-identically, and
+ * save -> load -> save writes identical bytes.  Both synchronize the stream. */
+snn_status snn_save(snn_index idx, const char *path, void *stream);
+snn_status snn_load(const char *path, void *stream, snn_index *out);
+
 /* snn_build for a metric (snn_metric).  EUCLIDEAN == snn_build.  COSINE / ANGULAR: rows
  * are normalized first (see snn_metric); a zero row -> SNN_ERR_INVALID_ARGUMENT.  Radii
  * of snn_query_radius / snn_query_self / snn_dbscan on this index are in the metric's

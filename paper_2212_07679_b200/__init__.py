@@ -29,7 +29,7 @@ STATUS = {0: "SNN_OK", 1: "SNN_ERR_INVALID_ARGUMENT", 2: "SNN_ERR_EMPTY",
           3: "SNN_ERR_NONFINITE", 4: "SNN_ERR_DIM_MISMATCH", 5: "SNN_ERR_OUT_OF_MEMORY",
           6: "SNN_ERR_CUDA", 7: "SNN_ERR_UNSUPPORTED"}
 
-EXPORTS = ["snn_build", "snn_build_metric", "snn_query_radius", "snn_query_self", "snn_result_csr",
+EXPORTS = ["snn_build", "snn_build_metric", "snn_append", "snn_save", "snn_load", "snn_query_radius", "snn_query_self", "snn_result_csr",
            "snn_result_copy", "snn_result_free", "snn_dbscan", "snn_free", "snn_last_error",
            "snn_index_info", "snn_launch_count", "snn_set_option", "snn_profile_enable",
            "snn_profile_read"]
@@ -76,6 +76,9 @@ def load_library(path: str = LIB_PATH):
     sig = {
         "snn_build": ([P, i64, i32, ctypes.c_int, P, ctypes.POINTER(P)], ctypes.c_int),
         "snn_build_metric": ([P, i64, i32, ctypes.c_int, i32, P, ctypes.POINTER(P)], ctypes.c_int),
+        "snn_append": ([P, P, i64, i32, ctypes.c_int, P], ctypes.c_int),
+        "snn_save": ([P, ctypes.c_char_p, P], ctypes.c_int),
+        "snn_load": ([ctypes.c_char_p, P, ctypes.POINTER(P)], ctypes.c_int),
         "snn_query_radius": ([P, P, i64, i32, ctypes.c_int, f64, P, ctypes.POINTER(P)], ctypes.c_int),
         "snn_query_self": ([P, f64, P, ctypes.POINTER(P)], ctypes.c_int),
         "snn_result_csr": ([P, ctypes.POINTER(_CSR)], ctypes.c_int),
@@ -227,6 +230,22 @@ def snn_free(index) -> None:
         load_library().snn_free(index)
 
 
+def snn_append(index, Y, stream=None) -> None:
+    """Streaming append: rows Y (k x d) get ids n .. n+k-1; mu, v1 frozen."""
+    p, k, d, code, _keep = _ptr_dtype(Y)
+    _check(load_library().snn_append(index, p, k, d, code, _stream_ptr(stream)))
+
+
+def snn_save(index, path: str, stream=None) -> None:
+    _check(load_library().snn_save(index, os.fsencode(path), _stream_ptr(stream)))
+
+
+def snn_load(path: str, stream=None):
+    h = ctypes.c_void_p()
+    _check(load_library().snn_load(os.fsencode(path), _stream_ptr(stream), ctypes.byref(h)))
+    return h
+
+
 def snn_index_info(index) -> dict:
     v = _Info()
     _check(load_library().snn_index_info(index, ctypes.byref(v)))
@@ -313,12 +332,26 @@ def _fetch(result, device: str, stream=None) -> CSR:
 class Index:
     """Owns an SNN index built on the current CUDA device (Algorithm 1)."""
 
-    def __init__(self, X, stream=None, metric: str = "euclidean"):
-        self._h = snn_build_metric(X, metric, stream)
-        self.metric = metric
+    def __init__(self, X, stream=None, metric: str = "euclidean", _handle=None):
+        self._h = _handle if _handle is not None else snn_build_metric(X, metric, stream)
+        self._sync()
+
+    def _sync(self):
         info = snn_index_info(self._h)
         self.n, self.d = int(info["n"]), int(info["d"])
         self.dtype = "f64" if info["dtype"] == SNN_F64 else "f32"
+        self.metric = {v: k for k, v in METRICS.items()}[int(info["metric"])]
+
+    @classmethod
+    def load(cls, path: str, stream=None) -> "Index":
+        return cls(None, _handle=snn_load(path, stream))
+
+    def save(self, path: str, stream=None) -> None:
+        snn_save(self._h, path, stream)
+
+    def append(self, Y, stream=None) -> None:
+        snn_append(self._h, Y, stream)
+        self._sync()
 
     def info(self) -> dict:
         return snn_index_info(self._h)

@@ -343,7 +343,7 @@ static snn_status build_impl(const void *X, int64_t n, int32_t d, snn_dtype dt, 
     const size_t es = f64 ? 8 : 4;
 
     snn_index idx = new snn_index_s();
-    idx->n = n; idx->d = d; idx->dt = dt; idx->sm_count = sms;
+    idx->n = n; idx->d = d; idx->d_in = d; idx->dt = dt; idx->sm_count = sms;
     idx->ld = row_stride(d);
     idx->n_pad = round_up(n, 4);
     Workspace ws(s);
@@ -1327,6 +1327,268 @@ static snn_status metric_query(snn_index idx, const void *Q, int64_t m, int32_t 
     launch_metric_distances(idx->metric, (*out)->distances, (*out)->nnz, s);
     cudaError_t e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) { snn_result_free(*out); *out = nullptr; return cuda_fail(e, "metric distances"); }
+    return SNN_OK;
+}
+
+// ------------------------------------------------------------------ streaming append (f4)
+// PAPER.md:33 ("online streaming"): mu and v1 stay frozen -- the window bound of eq:lower
+// holds for any fixed unit vector and centring -- the new rows get keys
+// under the frozen (mu, v1), and the key order is rebuilt by one stable sort of [old rows in
+// key order ; new rows] (old rows first, so equal keys stay ordered by original id).  The
+// key error bounds and the FP16 operand scale are recomputed for the grown data; every
+// per-row array (Xs, xbar, filter rows, tensor-core copy, kept input rows) is regathered.
+static void swap_owned(snn_index idx, void *old_p, void *new_p, cudaStream_t s) {
+    for (auto &p : idx->owned)
+        if (p == old_p) { p = new_p; if (old_p) cudaFreeAsync(old_p, s); return; }
+    idx->owned.push_back(new_p);
+}
+
+snn_status snn_append(snn_index idx, const void *Y, int64_t k, int32_t d, snn_dtype dt, void *stream) {
+    if (!idx) return fail(SNN_ERR_INVALID_ARGUMENT, "NULL index");
+    if (k < 0 || (k > 0 && !Y)) return fail(SNN_ERR_INVALID_ARGUMENT, "k < 0 or NULL rows");
+    if (idx->metric == SNN_METRIC_MIPS) return fail(SNN_ERR_UNSUPPORTED, "append to a MIPS index (xi would change)");
+    if (d != idx->d_in || dt != idx->dt) return fail(SNN_ERR_DIM_MISMATCH, "row dimension / dtype differs from the index");
+    if (k == 0) return SNN_OK;
+    const int64_t n0 = idx->n, n1 = n0 + k;
+    if (n1 >= (int64_t(1) << 30)) return fail(SNN_ERR_UNSUPPORTED, "n >= 2^30 is not supported");
+    int sms = 0;
+    snn_status st = device_check(&sms);
+    if (st != SNN_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const bool f64 = idx->dt == SNN_F64;
+    const size_t es = f64 ? 8 : 4;
+    const int D = idx->d, ld = idx->ld;
+    const int64_t np1 = round_up(n1, 4);
+    Workspace ws(s);
+    const void *Yin = nullptr, *Yd = nullptr;
+    if ((st = device_rows(Y, k, d, es, s, ws, &Yin)) != SNN_OK) return st;
+    Yd = Yin;
+    if (idx->metric == SNN_METRIC_COSINE || idx->metric == SNN_METRIC_ANGULAR)
+        if ((st = normalized_copy(Yin, k, d, dt, s, ws, &Yd)) != SNN_OK) return st;
+    uint8_t *S = nullptr, *sort_tmp = nullptr;
+    double *sums = nullptr;
+    uint32_t *maxabs = nullptr, *src = nullptr;
+    int *flag = nullptr;
+    float *keys_raw = nullptr;
+    CK(ws.alloc(&S, (size_t)n1 * D * es), "alloc rows");
+    CK(ws.alloc(&sums, (size_t)D), "alloc");
+    CK(ws.alloc(&maxabs, (size_t)D), "alloc");
+    CK(ws.alloc(&flag, 1), "alloc");
+    CK(ws.alloc(&keys_raw, (size_t)n1), "alloc");
+    CK(ws.alloc(&src, (size_t)n1), "alloc");
+    CK(ws.alloc(&sort_tmp, radix_sort_temp_bytes(n1)), "alloc sort");
+    CK(cudaMemsetAsync(sums, 0, (size_t)D * 8, s), "memset");
+    CK(cudaMemsetAsync(maxabs, 0, (size_t)D * 4, s), "memset");
+    CK(cudaMemsetAsync(flag, 0, 4, s), "memset");
+    launch_unpack_rows(idx->Xs, f64, n0, D, ld, S, s);
+    CK(cudaMemcpyAsync(S + (size_t)n0 * D * es, Yd, (size_t)k * D * es, cudaMemcpyDeviceToDevice, s), "copy rows");
+    launch_colstats(S, f64, n1, D, sums, maxabs, flag, s);
+    int hflag = 0;
+    CK(cudaMemcpyAsync(&hflag, flag, 4, cudaMemcpyDeviceToHost, s), "D2H");
+    CK(cudaStreamSynchronize(s), "append");
+    if (hflag) return fail(SNN_ERR_NONFINITE, "appended rows contain NaN or Inf");   // index unchanged
+
+    float *keys1 = nullptr, *xbar1 = nullptr, *Xf1 = nullptr;
+    int32_t *perm1 = nullptr;
+    void *Xs1 = nullptr, *Xt1 = nullptr, *Xo1 = nullptr;
+    std::vector<void *> fresh;
+    auto grab = [&](void **p, size_t bytes) {
+        cudaError_t e = cudaMallocAsync(p, bytes ? bytes : 16, s);
+        if (e == cudaSuccess) fresh.push_back(*p);
+        return e;
+    };
+    auto bail = [&](cudaError_t e, const char *w) {
+        for (void *p : fresh) cudaFreeAsync(p, s);
+        return cuda_fail(e, w);
+    };
+    cudaError_t e;
+    if ((e = grab((void **)&keys1, (size_t)n1 * 4)) != cudaSuccess) return bail(e, "alloc keys");
+    if ((e = grab((void **)&perm1, (size_t)n1 * 4)) != cudaSuccess) return bail(e, "alloc perm");
+    if ((e = grab((void **)&xbar1, (size_t)(np1 + 256) * 4)) != cudaSuccess) return bail(e, "alloc xbar");
+    if ((e = grab(&Xs1, (size_t)np1 * row_elems(D, ld) * es)) != cudaSuccess) return bail(e, "alloc Xs");
+    launch_keys(S, f64, n1, D, idx->mu_d, idx->mu_f, idx->v_d, idx->v_f, keys_raw, s);          // K3
+    radix_sort_pairs(keys_raw, nullptr, keys1, src, n1, sort_tmp, s);                            // K4
+    launch_append_perm(src, n0, n1, idx->perm, perm1, s);
+    launch_gather(S, f64, n1, D, ld, np1, src, idx->mu_d, Xs1, xbar1, s);                        // K5
+    launch_key_bounds(D, maxabs, idx->mu_d, idx->mu_f, idx->v_d, idx->v_f, idx->stats, s);
+    double *hs = static_cast<double *>(t_pinned.p);
+    if ((e = cudaMemcpyAsync(hs, idx->stats, ST_COUNT * 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return bail(e, "D2H");
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return bail(e, "append");
+    memcpy(idx->h_stats, hs, sizeof(idx->h_stats));
+    if (idx->Xf) {
+        if ((e = grab((void **)&Xf1, (size_t)np1 * (D + 1) * 4)) != cudaSuccess) return bail(e, "alloc filter rows");
+        launch_filter_rows(static_cast<const float *>(Xs1), D, n1, np1, idx->mu_f, idx->xf_c1h, Xf1, s);
+    }
+    int tc_f16 = idx->tc_f16, xexp = idx->xexp, kpad = idx->kpad;
+    if (idx->tc) {
+        int ex = 0;
+        tc_f16 = idx->tc_f16 && f16_exponent(idx->h_stats[ST_XCMAX], &ex);
+        xexp = ex;
+        kpad = tc_kpad(D, tc_f16);
+        if ((e = grab(&Xt1, (size_t)n1 * kpad * (tc_f16 ? 2 : 4))) != cudaSuccess) return bail(e, "alloc operand copy");
+        if (tc_f16)
+            launch_gather_f16(S, f64, n1, D, src, idx->mu_f, ldexpf(1.0f, ex), Xt1, xbar1, s);
+        else
+            launch_gather_tf32(S, f64, n1, D, src, idx->mu_f, static_cast<float *>(Xt1), xbar1, s);
+    }
+    if (idx->Xo) {   // MANHATTAN: input rows in original order
+        if ((e = grab(&Xo1, (size_t)n1 * d * es)) != cudaSuccess) return bail(e, "alloc rows");
+        cudaMemcpyAsync(Xo1, idx->Xo, (size_t)n0 * d * es, cudaMemcpyDeviceToDevice, s);
+        cudaMemcpyAsync(static_cast<uint8_t *>(Xo1) + (size_t)n0 * d * es, Yin, (size_t)k * d * es,
+                        cudaMemcpyDeviceToDevice, s);
+    }
+    if ((e = cudaGetLastError()) != cudaSuccess || (e = cudaStreamSynchronize(s)) != cudaSuccess) return bail(e, "append");
+    swap_owned(idx, idx->keys, keys1, s); idx->keys = keys1;
+    swap_owned(idx, idx->perm, perm1, s); idx->perm = perm1;
+    swap_owned(idx, idx->xbar, xbar1, s); idx->xbar = xbar1;
+    swap_owned(idx, idx->Xs, Xs1, s); idx->Xs = Xs1;
+    if (Xf1) { swap_owned(idx, idx->Xf, Xf1, s); idx->Xf = Xf1; }
+    if (Xt1) { swap_owned(idx, idx->Xt, Xt1, s); idx->Xt = Xt1; }
+    if (Xo1) { swap_owned(idx, idx->Xo, Xo1, s); idx->Xo = Xo1; }
+    idx->tc_f16 = tc_f16; idx->xexp = xexp; idx->kpad = kpad;
+    idx->n = n1; idx->n_pad = np1;
+    return SNN_OK;
+}
+
+// ------------------------------------------------------------------ save / load (f4)
+// File: "SNNG", u32 version 1, 23 int64 header words, then the device arrays in a fixed
+// order (all little endian, host byte order of x86-64 / aarch64).  Loading validates the
+// header, the file length and the index invariants (keys sorted and finite, perm a
+// permutation) before touching the device; the loaded index answers queries bit-identically.
+namespace {
+constexpr uint32_t kVersion = 1;
+constexpr int kHdr = 15 + ST_COUNT;
+
+struct Section { void **dev; size_t bytes; };
+
+std::vector<Section> sections(snn_index idx, bool has_xf, bool has_xo) {
+    const size_t es = idx->dt == SNN_F64 ? 8 : 4;
+    const int64_t n = idx->n, np = idx->n_pad;
+    const int D = idx->d;
+    std::vector<Section> v = {
+        {(void **)&idx->mu_d, (size_t)D * 8}, {(void **)&idx->mu_f, (size_t)D * 4},
+        {(void **)&idx->v_d, (size_t)D * 8},  {(void **)&idx->v_f, (size_t)D * 4},
+        {(void **)&idx->stats, (size_t)(ST_COUNT + 2) * 8},
+        {(void **)&idx->keys, (size_t)n * 4}, {(void **)&idx->perm, (size_t)n * 4},
+        {(void **)&idx->xbar, (size_t)(np + 256) * 4},
+        {(void **)&idx->Xs, (size_t)np * row_elems(D, idx->ld) * es}};
+    if (has_xf) v.push_back({(void **)&idx->Xf, (size_t)np * (D + 1) * 4});
+    if (idx->tc) v.push_back({(void **)&idx->Xt, (size_t)n * idx->kpad * (idx->tc_f16 ? 2 : 4)});
+    if (has_xo) v.push_back({(void **)&idx->Xo, (size_t)n * idx->d_in * es});
+    return v;
+}
+
+int64_t dbits(double x) { int64_t b; memcpy(&b, &x, 8); return b; }
+double bitsd(int64_t b) { double x; memcpy(&x, &b, 8); return x; }
+}  // namespace
+
+snn_status snn_save(snn_index idx, const char *path, void *stream) {
+    if (!idx || !path) return fail(SNN_ERR_INVALID_ARGUMENT, "NULL argument");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int64_t h[kHdr] = {idx->n, idx->n_pad, idx->d, idx->ld, (int64_t)idx->dt, idx->metric, idx->d_in, idx->tc,
+                       idx->tc_f16, idx->xexp, idx->kpad, idx->Xf != nullptr, idx->Xo != nullptr,
+                       dbits(idx->xi2), dbits(idx->xf_c1h)};
+    for (int i = 0; i < ST_COUNT; ++i) h[15 + i] = dbits(idx->h_stats[i]);
+    FILE *f = fopen(path, "wb");
+    if (!f) return fail(SNN_ERR_INVALID_ARGUMENT, std::string("cannot open for writing: ") + path);
+    bool ok = fwrite("SNNG", 1, 4, f) == 4 && fwrite(&kVersion, 4, 1, f) == 1 && fwrite(h, 8, kHdr, f) == (size_t)kHdr;
+    std::vector<uint8_t> buf;
+    for (const Section &sec : sections(idx, idx->Xf != nullptr, idx->Xo != nullptr)) {
+        if (!ok) break;
+        buf.resize(sec.bytes);
+        cudaError_t e = cudaMemcpyAsync(buf.data(), *sec.dev, sec.bytes, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) { fclose(f); return cuda_fail(e, "save"); }
+        ok = fwrite(buf.data(), 1, sec.bytes, f) == sec.bytes;
+    }
+    if (fclose(f) != 0) ok = false;
+    return ok ? SNN_OK : fail(SNN_ERR_INVALID_ARGUMENT, std::string("write failed: ") + path);
+}
+
+snn_status snn_load(const char *path, void *stream, snn_index *out) {
+    if (!path || !out) return fail(SNN_ERR_INVALID_ARGUMENT, "NULL argument");
+    *out = nullptr;
+    FILE *f = fopen(path, "rb");
+    if (!f) return fail(SNN_ERR_INVALID_ARGUMENT, std::string("cannot open: ") + path);
+    std::vector<uint8_t> file;
+    {
+        uint8_t tmp[1 << 16];
+        size_t r;
+        while ((r = fread(tmp, 1, sizeof(tmp), f)) > 0) file.insert(file.end(), tmp, tmp + r);
+        fclose(f);
+    }
+    const size_t head = 8 + 8 * (size_t)kHdr;
+    if (file.size() < 8 || memcmp(file.data(), "SNNG", 4) != 0) return fail(SNN_ERR_INVALID_ARGUMENT, "bad magic");
+    uint32_t ver;
+    memcpy(&ver, file.data() + 4, 4);
+    if (ver != kVersion) return fail(SNN_ERR_INVALID_ARGUMENT, "unsupported version");
+    if (file.size() < head) return fail(SNN_ERR_INVALID_ARGUMENT, "truncated");
+    int64_t h[kHdr];
+    memcpy(h, file.data() + 8, 8 * (size_t)kHdr);
+    snn_index_s tmpl;
+    tmpl.n = h[0]; tmpl.n_pad = h[1]; tmpl.d = (int)h[2]; tmpl.ld = (int)h[3]; tmpl.dt = (snn_dtype)h[4];
+    tmpl.metric = (int)h[5]; tmpl.d_in = (int)h[6]; tmpl.tc = (int)h[7]; tmpl.tc_f16 = (int)h[8];
+    tmpl.xexp = (int)h[9]; tmpl.kpad = (int)h[10];
+    const bool has_xf = h[11] != 0, has_xo = h[12] != 0;
+    tmpl.xi2 = bitsd(h[13]); tmpl.xf_c1h = bitsd(h[14]);
+    for (int i = 0; i < ST_COUNT; ++i) tmpl.h_stats[i] = bitsd(h[15 + i]);
+    const int64_t n = tmpl.n;
+    const int D = tmpl.d;
+    const bool hdr_ok =
+        n >= 1 && n < (int64_t(1) << 30) && tmpl.n_pad == round_up(n, 4) && D >= 1 && h[2] < (1 << 24) &&
+        (h[4] == SNN_F32 || h[4] == SNN_F64) && h[5] >= SNN_METRIC_EUCLIDEAN && h[5] <= SNN_METRIC_MIPS &&
+        tmpl.d_in == (tmpl.metric == SNN_METRIC_MIPS ? D - 1 : D) &&
+        (tmpl.ld == 0 ? lowd_supported(D) : (tmpl.ld >= D && tmpl.ld < D + 4)) &&
+        (!tmpl.tc || (tmpl.ld != 0 && tmpl.kpad == tc_kpad(D, tmpl.tc_f16 != 0))) &&
+        (!has_xf || (tmpl.ld == 0 && tmpl.dt == SNN_F32)) &&
+        (has_xo == (tmpl.metric == SNN_METRIC_MANHATTAN || tmpl.metric == SNN_METRIC_MIPS));
+    if (!hdr_ok) return fail(SNN_ERR_INVALID_ARGUMENT, "invalid header");
+    std::vector<Section> secs = sections(&tmpl, has_xf, has_xo);
+    size_t total = head;
+    for (const Section &sec : secs) total += sec.bytes;
+    if (file.size() < total) return fail(SNN_ERR_INVALID_ARGUMENT, "truncated");
+    if (file.size() > total) return fail(SNN_ERR_INVALID_ARGUMENT, "trailing bytes");
+    // invariants: keys (section 5) non-decreasing and finite, perm (section 6) a permutation
+    {
+        size_t off = head;
+        for (int i = 0; i < 5; ++i) off += secs[i].bytes;
+        const float *keys = reinterpret_cast<const float *>(file.data() + off);
+        const int32_t *perm = reinterpret_cast<const int32_t *>(file.data() + off + secs[5].bytes);
+        std::vector<uint8_t> seen((size_t)n, 0);
+        for (int64_t i = 0; i < n; ++i) {
+            float kf;
+            int32_t p;
+            memcpy(&kf, keys + i, 4);
+            memcpy(&p, perm + i, 4);
+            if (!std::isfinite(kf) || (i > 0 && !(keys[i - 1] <= kf)))
+                return fail(SNN_ERR_INVALID_ARGUMENT, "invalid index: keys not sorted");
+            if (p < 0 || p >= n || seen[p]) return fail(SNN_ERR_INVALID_ARGUMENT, "invalid index: perm is not a permutation");
+            seen[p] = 1;
+        }
+    }
+    int sms = 0;
+    snn_status st = device_check(&sms);
+    if (st != SNN_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    snn_index idx = new snn_index_s();
+    *idx = tmpl;
+    idx->sm_count = sms;
+    idx->owned.clear();
+    std::vector<Section> dst = sections(idx, has_xf, has_xo);
+    size_t off = head;
+    for (const Section &sec : dst) {
+        void *p = nullptr;
+        cudaError_t e = cudaMallocAsync(&p, sec.bytes ? sec.bytes : 16, s);
+        if (e != cudaSuccess) { free_index(idx); return cuda_fail(e, "alloc"); }
+        idx->owned.push_back(p);
+        *sec.dev = p;
+        e = cudaMemcpyAsync(p, file.data() + off, sec.bytes, cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) { free_index(idx); return cuda_fail(e, "H2D"); }
+        off += sec.bytes;
+    }
+    cudaError_t e = cudaStreamSynchronize(s);   // `file` is pageable: copies complete before return
+    if (e != cudaSuccess) { free_index(idx); return cuda_fail(e, "load"); }
+    *out = idx;
     return SNN_OK;
 }
 

@@ -698,6 +698,25 @@ __global__ void __launch_bounds__(kThreads) gather_generic(const T *__restrict__
     }
 }
 
+// inverse of K5's layout (streaming append): rows [0, n) of Xs back to row-major n x d
+template <typename T>
+__global__ void unpack_rows(const T *__restrict__ Xs, int64_t n, int d, int ld, T *__restrict__ out) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n * d; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / d;
+        const int k = (int)(e - i * d);
+        out[e] = ld == 0 ? Xs[(i >> 2) * 4 * d + k * 4 + (i & 3)] : Xs[i * ld + k];
+    }
+}
+
+// streaming append: sorted position -> original id from the merge sort's source rows
+__global__ void append_perm(const uint32_t *__restrict__ src, int64_t n_old, int64_t n_new,
+                            const int32_t *__restrict__ perm_old, int32_t *__restrict__ perm_new) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_new; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t r = src[i];
+        perm_new[i] = r < n_old ? perm_old[r] : (int32_t)r;
+    }
+}
+
 int grid_for(int64_t items, int per_block = kThreads, int cap = 148 * 16) {
     int64_t g = ceil_div(items, per_block);
     if (g < 1) g = 1;
@@ -831,6 +850,23 @@ void launch_gather(const void *X, bool f64, int64_t n, int d, int ld, int64_t n_
     const int gw = grid_for(n_pad * kWarp);
     if (f64) SNN_LAUNCH(gather_generic<double>, gw, kThreads, 0, s, (const double *)X, n, d, ld, n_pad, perm, mu_d, (double *)Xs, xbar);
     else SNN_LAUNCH(gather_generic<float>, gw, kThreads, 0, s, (const float *)X, n, d, ld, n_pad, perm, mu_d, (float *)Xs, xbar);
+}
+
+void launch_unpack_rows(const void *Xs, bool f64, int64_t n, int d, int ld, void *out, cudaStream_t s) {
+    if (n == 0) return;
+    const int g = grid_for(n * d);
+    if (f64) SNN_LAUNCH(unpack_rows<double>, g, kThreads, 0, s, (const double *)Xs, n, d, ld, (double *)out);
+    else SNN_LAUNCH(unpack_rows<float>, g, kThreads, 0, s, (const float *)Xs, n, d, ld, (float *)out);
+}
+
+void launch_key_bounds(int d, const uint32_t *maxabs_bits, const double *mu_d, const float *mu_f, double *v_d,
+                       float *v_f, double *stats, cudaStream_t s) {
+    SNN_LAUNCH(finalize_direction, 1, 32, 0, s, d, maxabs_bits, mu_d, mu_f, v_d, v_f, stats);
+}
+
+void launch_append_perm(const uint32_t *src, int64_t n_old, int64_t n_new, const int32_t *perm_old, int32_t *perm_new,
+                        cudaStream_t s) {
+    SNN_LAUNCH(append_perm, grid_for(n_new), kThreads, 0, s, src, n_old, n_new, perm_old, perm_new);
 }
 
 }  // namespace snn

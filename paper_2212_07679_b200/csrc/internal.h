@@ -50,6 +50,15 @@ void launch_gather(const void *X, bool f64, int64_t n, int d, int ld, int64_t n_
                    const uint32_t *perm, const double *mu_d, void *Xs, float *xbar,
                    cudaStream_t s);
 
+// Streaming append: Xs rows [0, n) (either layout) back to row-major n x d; the key error
+// bounds / operand scale of stats[] recomputed for new maxabs with mu, v1 frozen (v1 is
+// already sign-fixed, so finalize_direction leaves it unchanged).
+void launch_unpack_rows(const void *Xs, bool f64, int64_t n, int d, int ld, void *out, cudaStream_t s);
+void launch_append_perm(const uint32_t *src, int64_t n_old, int64_t n_new, const int32_t *perm_old, int32_t *perm_new,
+                        cudaStream_t s);
+void launch_key_bounds(int d, const uint32_t *maxabs_bits, const double *mu_d, const float *mu_f, double *v_d,
+                       float *v_f, double *stats, cudaStream_t s);
+
 // ----------------------------------------------------------------------- sort (radix_sort.cu)
 // Stable ascending sort of fp32 keys (finite) with uint32 payload.  If vals_in == nullptr
 // the payload is the iota 0..n-1.  Outputs in keys_out / vals_out.  temp_bytes() tells

@@ -83,3 +83,28 @@ def test_missing_library_fails_loudly(tmp_path):
             p.load_library(str(tmp_path / "nope.so"))
     finally:
         p._lib = saved
+
+
+def test_snn_load_rejects_bad_files_without_touching_the_device(libpath, tmp_path):
+    """snn_load validates magic, version, header and length on the host first (the SPEC
+    io_persist error cases) -- runnable without a GPU."""
+    import struct
+    import paper_2212_07679_b200 as p
+    p.load_library()
+    hdr = [5, 8, 2, 0, 0, 0, 2, 0, 0, 0, 0, 0, 0, 0, 0] + [0] * 8   # n=5, n_pad=8, d=2, ld=0, f32, euclidean
+    cases = {
+        "bad magic": b"XXXX" + struct.pack("<I", 1) + struct.pack("<23q", *hdr),
+        "unsupported version": b"SNNG" + struct.pack("<I", 2) + struct.pack("<23q", *hdr),
+        "truncated": b"SNNG" + struct.pack("<I", 1) + struct.pack("<23q", *hdr)[:40],
+        "invalid header": b"SNNG" + struct.pack("<I", 1) + struct.pack("<23q", *([5, 7] + hdr[2:])),
+    }
+    # correct header, payload one byte short
+    cases["truncated "] = cases["unsupported version"][:4] + struct.pack("<I", 1) + \
+        struct.pack("<23q", *hdr) + b"\0" * 100
+    for want, blob in cases.items():
+        f = tmp_path / "x.snn"
+        f.write_bytes(blob)
+        with pytest.raises(p.SnnError, match=want.strip()):
+            p.snn_load(str(f))
+    with pytest.raises(p.SnnError, match="cannot open"):
+        p.snn_load(str(tmp_path / "missing.snn"))

@@ -755,3 +755,175 @@ def test_inner_product_parity(snn, n, m, d, dt):
         assert int(np.asarray(idx.query(_dev(Q), big).offsets)[-1]) == 0
     finally:
         idx.free()
+
+
+# --------------------------------------------------------------------------- streaming append + save/load (f4)
+def _csr_equal(a, b):
+    np.testing.assert_array_equal(np.asarray(a.offsets), np.asarray(b.offsets))
+    np.testing.assert_array_equal(np.asarray(a.indices), np.asarray(b.indices))
+    np.testing.assert_array_equal(np.asarray(a.distances).view(np.uint32), np.asarray(b.distances).view(np.uint32))
+
+
+def _check_key_order(idx):
+    arr = idx.arrays()
+    keys, perm = arr["keys"].cpu().numpy(), arr["perm"].cpu().numpy()
+    assert np.all(np.diff(keys) >= 0)
+    np.testing.assert_array_equal(np.sort(perm), np.arange(idx.n))
+    ties = np.diff(keys) == 0
+    assert np.all(np.diff(perm)[ties] > 0), "equal keys not ordered by original id"
+
+
+@pytest.mark.parametrize("d,dt", [(2, np.float32), (3, np.float64), (8, np.float32), (20, np.float32),
+                                  (64, np.float32), (40, np.float64), (130, np.float32)])
+def test_append_parity(snn, d, dt):
+    """Append in batches (mu, v1 frozen) == brute force on the grown data."""
+    rng = np.random.default_rng(1000 + d)
+    X0 = (rng.standard_normal((3000, d)) * rng.uniform(0.5, 2, d)).astype(dt)
+    B1 = (rng.standard_normal((700, d)) * rng.uniform(0.5, 2, d) + 0.5).astype(dt)
+    B2 = np.concatenate([X0[5:6], X0[:3] * 1.0001, 8 * rng.standard_normal((10, d))]).astype(dt)  # twin, near twins, outliers
+    B3 = (rng.standard_normal((1, d))).astype(dt)
+    Q = (rng.standard_normal((300, d)) * rng.uniform(0.5, 2, d)).astype(dt)
+    R = float(np.quantile(np.linalg.norm(X0[:200, None, :].astype(np.float64) - Q[None, :40, :], axis=-1), 0.03))
+    idx = snn.Index(_dev(X0))
+    try:
+        idx.append(_dev(B1))
+        idx.append(B2)                         # host rows
+        idx.append(_dev(B3))
+        idx.append(_dev(B3[:0]))               # k = 0: no-op
+        X = np.concatenate([X0, B1, B2, B3])
+        assert idx.n == len(X)
+        _check_key_order(idx)
+        compare(idx.query(_dev(Q), R), oracle.radius_query(X, Q, R))
+        compare(idx.query_self(R), oracle.radius_query(X, X, R))
+        z = idx.query(_dev(X[[5, 3000 + 700]]), 0.0)      # the appended twin of row 5
+        assert {5, 3700} <= set(np.asarray(z.indices)[: np.asarray(z.offsets)[1]].tolist())
+    finally:
+        idx.free()
+
+
+def test_append_spec_examples(snn):
+    """SPEC append_point examples: D3 + (9,12) -> alpha (-5, 0, 5, 10), new id 3 at
+    sorted position 3; a duplicate is found with R = 0; a single-point index grows to n = 2."""
+    idx = snn.Index(np.array([[0, 0], [3, 4], [6, 8]], dtype=np.float64))
+    try:
+        idx.append(np.array([[9, 12]], dtype=np.float64))
+        arr = idx.arrays()
+        np.testing.assert_allclose(arr["keys"].cpu().numpy(), [-5, 0, 5, 10], atol=1e-5)
+        np.testing.assert_array_equal(arr["perm"].cpu().numpy(), [0, 1, 2, 3])
+        idx.append(np.array([[3, 4]], dtype=np.float64))
+        r = idx.query(np.array([[3, 4]], dtype=np.float64), 0.0)
+        assert sorted(np.asarray(r.indices).tolist()) == [1, 4]
+    finally:
+        idx.free()
+    one = snn.Index(np.array([[7, 7]], dtype=np.float32))
+    try:
+        one.append(np.array([[1, 2]], dtype=np.float32))
+        assert one.n == 2
+        _check_key_order(one)
+        r = one.query_self(10.0)
+        assert int(np.asarray(r.offsets)[-1]) == 4
+    finally:
+        one.free()
+
+
+def test_append_metrics_and_errors(snn):
+    rng = np.random.default_rng(1100)
+    X0 = (rng.standard_normal((2000, 3)) + 0.3).astype(np.float32)
+    B = (rng.standard_normal((500, 3)) + 0.3).astype(np.float32)
+    Q = (rng.standard_normal((200, 3)) + 0.3).astype(np.float32)
+    X = np.concatenate([X0, B])
+    idx = snn.Index(_dev(X0), metric="cosine")
+    try:
+        idx.append(_dev(B))
+        _metric_compare(idx.query(_dev(Q), 0.002), oracle.metric_radius_query(X, Q, 0.002, "cosine"), "cosine")
+        bad = B[:2].copy()
+        bad[1, 0] = np.nan
+        before = idx.query(_dev(Q), 0.002)
+        with pytest.raises(snn.SnnError, match="INVALID_ARGUMENT|NONFINITE"):
+            idx.append(_dev(bad))
+        assert idx.n == len(X)
+        _csr_equal(before, idx.query(_dev(Q), 0.002))   # unchanged
+        with pytest.raises(snn.SnnError, match="DIM_MISMATCH"):
+            idx.append(_dev(np.ones((2, 4), dtype=np.float32)))
+    finally:
+        idx.free()
+    man = snn.Index(_dev(X0), metric="manhattan")
+    try:
+        man.append(B)
+        _filtered_compare(man.query(_dev(Q), 0.3), oracle.manhattan_query(X, Q, 0.3))
+    finally:
+        man.free()
+    mips = snn.Index(_dev(X0), metric="mips")
+    try:
+        with pytest.raises(snn.SnnError, match="UNSUPPORTED"):
+            mips.append(_dev(B))
+    finally:
+        mips.free()
+    plain = snn.Index(_dev(X0))
+    try:
+        bad = B[:3].copy()
+        bad[2, 1] = np.inf
+        with pytest.raises(snn.SnnError, match="NONFINITE"):
+            plain.append(_dev(bad))
+        assert plain.n == len(X0)
+    finally:
+        plain.free()
+
+
+@pytest.mark.parametrize("metric,d,dt", [("euclidean", 3, np.float32), ("euclidean", 2, np.float64),
+                                         ("euclidean", 20, np.float32), ("euclidean", 64, np.float32),
+                                         ("cosine", 3, np.float32), ("manhattan", 4, np.float32),
+                                         ("mips", 8, np.float64)])
+def test_save_load_roundtrip(snn, tmp_path, metric, d, dt):
+    """Loaded index answers bit-identically; save -> load -> save writes identical bytes."""
+    rng = np.random.default_rng(1200 + d)
+    X = (rng.standard_normal((2500, d)) + 0.2).astype(dt)
+    Q = (rng.standard_normal((200, d)) + 0.2).astype(dt)
+    r = {"euclidean": 0.4 if d <= 3 else 4.0, "cosine": 0.002, "manhattan": 0.6, "mips": 6.0}[metric]
+    a = snn.Index(_dev(X), metric=metric)
+    p1, p2 = str(tmp_path / "a.snn"), str(tmp_path / "b.snn")
+    try:
+        a.save(p1)
+        b = snn.Index.load(p1)
+        try:
+            assert (b.n, b.d, b.metric) == (a.n, a.d, metric)
+            _csr_equal(a.query(_dev(Q), r), b.query(_dev(Q), r))
+            _csr_equal(a.query_self(r), b.query_self(r))
+            if metric in ("euclidean", "cosine"):
+                la, ka = a.dbscan(r, 4)
+                lb, kb = b.dbscan(r, 4)
+                assert ka == kb
+                np.testing.assert_array_equal(la, lb)
+            b.save(p2)
+        finally:
+            b.free()
+        assert open(p1, "rb").read() == open(p2, "rb").read()
+    finally:
+        a.free()
+
+
+def test_load_rejects_broken_invariants(snn, tmp_path):
+    X = np.random.default_rng(1300).standard_normal((100, 3)).astype(np.float32)
+    a = snn.Index(_dev(X))
+    p = str(tmp_path / "a.snn")
+    try:
+        a.save(p)
+    finally:
+        a.free()
+    blob = bytearray(open(p, "rb").read())
+    head = 8 + 8 * 23
+    off_keys = head + 3 * 8 + 3 * 4 + 3 * 8 + 3 * 4 + 10 * 8     # mu_d mu_f v_d v_f stats
+    off_perm = off_keys + 100 * 4
+    bad = bytearray(blob)
+    bad[off_perm:off_perm + 4] = bad[off_perm + 4:off_perm + 8]   # duplicate id
+    open(p, "wb").write(bad)
+    with pytest.raises(snn.SnnError, match="permutation"):
+        snn.Index.load(p)
+    bad = bytearray(blob)
+    bad[off_keys:off_keys + 4] = np.float32(1e30).tobytes()       # first key too large
+    open(p, "wb").write(bad)
+    with pytest.raises(snn.SnnError, match="sorted"):
+        snn.Index.load(p)
+    open(p, "wb").write(blob + b"\0")
+    with pytest.raises(snn.SnnError, match="trailing"):
+        snn.Index.load(p)
