@@ -45,6 +45,7 @@ struct Options {
     int lowd_tc = 0;     // low-d (fp32, d <= 8) radius queries through the tensor-core filter (option; FFMA default)
     int lowd_tc_tiles = 8;     // 256-candidate tiles per work item (low-d tensor-core path)
     int lowd_tc_group = 8;     // query blocks per raster group (low-d tensor-core path)
+    int compact = 0;           // low-d compaction: 0 = per hit, 1 = per record group (vector loads)
 };
 static std::atomic<int64_t> g_last_ovf{0}, g_last_lost{0};
 static Options g_opt;
@@ -253,6 +254,7 @@ snn_status snn_set_option(const char *key, int64_t value) {
         g_opt.chunk = (int)value;
         return SNN_OK;
     }
+    if (k == "compact") { g_opt.compact = value ? 1 : 0; return SNN_OK; }
     if (k == "cap") {
         if (value == 0) value = 64;
         if (value < 1 || value > 1024) return fail(SNN_ERR_INVALID_ARGUMENT, "cap must be 1..1024");
@@ -1031,6 +1033,7 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
     a.offsets = r->offsets; a.out_idx = nullptr; a.out_dist = nullptr;
     a.sm_count = sms;
     a.variant = g_opt.variant;
+    a.variant2 = g_opt.compact;
     if (!generic && !f64 && idx->Xf && g_opt.simt_filter) {
         double c1h = 1.0, r2h = 0.0;
         simt_filter_consts(D, R, &c1h, &r2h);

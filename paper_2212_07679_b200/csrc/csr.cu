@@ -6,7 +6,7 @@
 //   scan    : offsets (int64, m + 1)
 //   scatter : each hit to offsets[q] + atomic cursor -> (position << 32 | fp32 dist bits)
 //   sort    : every row sorted by sorted-index position (unique within a row, so the result
-//             is deterministic): warp bitonic sort in registers (<= 32) or shared memory
+//             is deterministic): warp rank sort in registers (<= 32), bitonic in shared memory
 //             (<= 512), one CTA per row in shared memory (<= 16384); the caller falls
 //             back to the global radix path beyond that.
 #include <stdint.h>
@@ -62,20 +62,12 @@ __global__ void __launch_bounds__(256) rows_sort_warp_kernel(const int64_t *offs
         const int64_t o0 = offsets[r];
         const int cnt = (int)(offsets[r + 1] - o0);
         if (cnt == 0 || cnt > WCAP) continue;
-        if (cnt <= 32) {   // registers + shuffles
-            uint64_t v = lane < cnt ? tmp[o0 + lane] : ~0ull;
-#pragma unroll
-            for (int k = 2; k <= 32; k <<= 1) {
-#pragma unroll
-                for (int j = k >> 1; j > 0; j >>= 1) {
-                    const uint64_t o = __shfl_xor_sync(0xffffffffu, v, j);
-                    const bool up = (lane & k) == 0;
-                    const bool lower = (lane & j) == 0;
-                    const uint64_t lo = v < o ? v : o, hi = v < o ? o : v;
-                    v = (lower == up) ? lo : hi;
-                }
-            }
-            if (lane < cnt) emit(v, perm, out_idx, out_dist, o0 + lane);
+        if (cnt <= 32) {   // rank sort in registers: positions are unique within a row
+            const uint64_t v = lane < cnt ? tmp[o0 + lane] : ~0ull;
+            const uint32_t key = (uint32_t)(v >> 32);
+            int rank = 0;
+            for (int j = 0; j < cnt; ++j) rank += __shfl_sync(0xffffffffu, key, j) < key;
+            if (lane < cnt) emit(v, perm, out_idx, out_dist, o0 + rank);
             continue;
         }
         int S = 64;

@@ -116,6 +116,14 @@ __device__ __forceinline__ uint64_t f2fma(uint64_t a, uint64_t b, uint64_t c) {
 // Per-4-candidate hit mask -> output.  MODE 0 records (g << 4 | mask) in the entry's
 // slot list, or, once `cap` slots are used, appends (entry, hits-before, record) to the
 // global overflow list; MODE 1 (fix) writes the CSR entries directly.
+// 16-byte shared-memory load from a 32-bit shared address (keeps the address arithmetic
+// out of the hot loop)
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+    return v;
+}
+
 __device__ __forceinline__ float lane4(const float4 &v, int i) {   // i is unrolled (static)
     return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
 }
@@ -150,7 +158,7 @@ struct Emitter {
         if (!mask) return;
         const uint32_t v = ((uint32_t)g << 4) | mask;
         if (rec < a.cap) {
-            slot[rec] = (uint16_t)v;
+            slot[(size_t)rec * a.B] = (uint16_t)v;
         } else {
             const int32_t k = atomicAdd(a.ovf_rec_count, 1);
             if (k < a.ovf_rec_cap) a.ovf_rec[k] = OvfRec{(int32_t)e, c, v};
@@ -321,7 +329,9 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
         bool active = sp < a.m;
         const int64_t e = item * a.B + tid;
         T q[D];
-        Emitter<T, D, MODE, SYM> em{a, a.slots + (size_t)e * a.cap, e, c0, 0};
+        // slot records item-major, record-major, thread-minor: record r of entry (item, t)
+        // at slots[(item * cap + r) * B + t] (coalesced across the CTA's threads)
+        Emitter<T, D, MODE, SYM> em{a, a.slots + (size_t)item * a.B * a.cap + tid, e, c0, 0};
         em.sp = sp;
         if (MODE == M_FIX) {
             active = active && a.cnt[e] < 0;   // lost-entry flag (sign bit)
@@ -336,9 +346,16 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
         if (MODE == M_UNION && active) uroot = uf_rep(a.parent, (int32_t)sp);
 #pragma unroll
         for (int k = 0; k < D; ++k) q[k] = active ? Qs[(sp >> 2) * 4 * D + k * 4 + (sp & 3)] : (T)0;
+        // the deferred-hit scan loop (fp32, G == 1) runs warp-converged: lanes without a
+        // query take a NaN query (every comparison false, no hits)
+        constexpr bool CONV = MODE == M_SCAN && G == 1 && sizeof(T) == 4;
+        if (CONV && !active) {
+#pragma unroll
+            for (int k = 0; k < D; ++k) q[k] = (T)NAN;
+        }
         mbar_wait(&bar[sidx], phase[sidx]);
         phase[sidx] ^= 1u;
-        if (active) {
+        if (active || CONV) {
             const int ngroups = (int)((c1 - c0) >> 2);
             if constexpr (sizeof(T) == 4) {
                 const float4 *g4 = reinterpret_cast<const float4 *>(smem + sidx * buf_bytes);
@@ -374,7 +391,7 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
                             }
                             const uint32_t v = ((uint32_t)gg << 4) | m;
                             if (em.rec < cap) {
-                                slotp[em.rec] = (uint16_t)v;
+                                slotp[(size_t)em.rec * a.B] = (uint16_t)v;
                             } else {
                                 const int32_t k = atomicAdd(a.ovf_rec_count, 1);
                                 if (k < a.ovf_rec_cap) a.ovf_rec[k] = OvfRec{(int32_t)e, em.c, v};
@@ -470,6 +487,73 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
                             if (ib) emit0(g + 1, ib);
                         }
                     }
+                    // G == 1: the hit path is deferred.  A candidate group with a pair <= T_out
+                    // only pushes (g << 4 | T_out mask) into a 4-record per-lane FIFO (64-bit
+                    // register); when any lane's FIFO is full the whole warp drains its FIFOs
+                    // together (recomputing the group's d^2 from shared memory, exact
+                    // classification, emission), so the expensive path runs convergently
+                    // instead of once per hitting lane.  Records keep their g order.
+                    uint64_t pend = 0;
+                    int npend = 0;
+                    auto drain = [&]() {
+#pragma unroll 1
+                        for (int r = 0; r < 4; ++r) {
+                            if (r < npend) {
+                                const uint32_t rec = (uint32_t)(pend >> (16 * r)) & 0xffffu;
+                                const int gg = (int)(rec >> 4);
+                                const uint32_t oa = rec & 15u;
+                                float4 xa[D];
+#pragma unroll
+                                for (int k = 0; k < D; ++k) xa[k] = g4[gg * D + k];
+                                uint64_t la, ha;
+                                group_d2<D>(xa, nq, la, ha);
+                                const float2 pa = f2unpack(la), qa = f2unpack(ha);
+                                uint32_t ia = mask4(pa.x, pa.y, qa.x, qa.y, T_in);
+                                if (ia ^ oa) ia |= resolve4<D>(oa & ~ia, xa, q, R2);
+                                if (ia) emit0(gg, ia);
+                            }
+                        }
+                        pend = 0;
+                        npend = 0;
+                    };
+                    constexpr bool LAZY = CONV;
+                    const float t_out = T_out;
+                    auto push = [&](int gg, uint32_t m) {
+                        pend |= (uint64_t)(((uint32_t)gg << 4) | m) << (16 * npend);
+                        ++npend;
+                    };
+                    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(g4);
+                    for (; LAZY && g + 1 < ngroups; g += 2) {   // 2 groups (8 pairs) per step
+                        float4 xa[D], xb[D];
+                        const uint32_t ga = sbase + (uint32_t)g * (16u * D);
+#pragma unroll
+                        for (int k = 0; k < D; ++k) { xa[k] = lds128(ga + 16u * k); xb[k] = lds128(ga + 16u * (D + k)); }
+                        uint64_t la, ha, lb, hb;
+                        group_d2<D>(xa, nq, la, ha);
+                        group_d2<D>(xb, nq, lb, hb);
+                        const float2 pa = f2unpack(la), qa = f2unpack(ha), pb = f2unpack(lb), qb = f2unpack(hb);
+                        const float mn = fminf(fminf(fminf(pa.x, pa.y), fminf(qa.x, qa.y)),
+                                               fminf(fminf(pb.x, pb.y), fminf(qb.x, qb.y)));
+                        if (mn <= t_out) {
+                            const uint32_t oa = mask4(pa.x, pa.y, qa.x, qa.y, t_out);
+                            const uint32_t ob = mask4(pb.x, pb.y, qb.x, qb.y, t_out);
+                            if (oa) push(g, oa);
+                            if (ob) push(g + 1, ob);
+                        }
+                        if (__any_sync(0xffffffffu, npend >= 3)) drain();   // FIFO holds 4
+                    }
+                    for (; LAZY && g < ngroups; ++g) {
+                        float4 xa[D];
+#pragma unroll
+                        for (int k = 0; k < D; ++k) xa[k] = g4[g * D + k];
+                        uint64_t la, ha;
+                        group_d2<D>(xa, nq, la, ha);
+                        const float2 pa = f2unpack(la), qa = f2unpack(ha);
+                        if (fminf(fminf(pa.x, pa.y), fminf(qa.x, qa.y)) <= t_out)
+                            push(g, mask4(pa.x, pa.y, qa.x, qa.y, t_out));
+                        if (__any_sync(0xffffffffu, npend >= 4)) drain();
+                    }
+                    if (LAZY) drain();
                     for (; g < ngroups; ++g) {
                         float4 xa[D];
 #pragma unroll
@@ -549,9 +633,57 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
 // Compaction of the recorded hits into the CSR: original ids via pi and distances as
 // (float)sqrt of the oracle-order fp64 squared distance.  One CTA per item; one thread
 // per (item, query) entry expands its slot records (the first `cap` records).
+// One record = one candidate group g (4 consecutive sorted positions) and its hit mask.
+// The group's rows are one AoSoA4 block (D x 4 values, loaded with vector loads), the
+// mirrored cursors are claimed first so the atomics overlap the loads and the fp64 math.
 template <typename T, int D>
 __device__ __forceinline__ void expand_record(const PassArgs &a, int64_t c0, uint32_t v,
                                               const T (&q)[D], int64_t &pos, int64_t sp) {
+    const T *Xs = static_cast<const T *>(a.Xs);
+    const int64_t g = c0 / 4 + (v >> 4);
+    const uint32_t mask = v & 15u;
+    unsigned long long mp[4] = {0, 0, 0, 0};
+    if (a.sym) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            if (mask & (1u << i)) mp[i] = atomicAdd(&a.lpos[g * 4 + i], 1ull);
+    }
+    int32_t id[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) id[i] = (mask & (1u << i)) ? a.perm[g * 4 + i] : 0;
+    T x[D][4];
+    if constexpr (sizeof(T) == 4) {
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            const float4 t = *reinterpret_cast<const float4 *>(Xs + g * 4 * D + k * 4);
+            x[k][0] = t.x; x[k][1] = t.y; x[k][2] = t.z; x[k][3] = t.w;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            const double2 t0 = *reinterpret_cast<const double2 *>(Xs + g * 4 * D + k * 4);
+            const double2 t1 = *reinterpret_cast<const double2 *>(Xs + g * 4 * D + k * 4 + 2);
+            x[k][0] = t0.x; x[k][1] = t0.y; x[k][2] = t1.x; x[k][3] = t1.y;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        if (!(mask & (1u << i))) continue;
+        T xi[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) xi[k] = x[k][i];
+        const float dd = (float)sqrt(sqdist_exact(xi, q, D));
+        a.out_idx[pos] = id[i];
+        a.out_dist[pos] = dd;
+        ++pos;
+        if (a.sym)   // mirrored entry into row j's L segment (sorted afterwards)
+            a.tmpL[mp[i]] = ((unsigned long long)sp << 32) | __float_as_uint(dd);
+    }
+}
+
+template <typename T, int D>
+__device__ __forceinline__ void expand_record_hits(const PassArgs &a, int64_t c0, uint32_t v,
+                                                   const T (&q)[D], int64_t &pos, int64_t sp) {
     const T *Xs = static_cast<const T *>(a.Xs);
     const int64_t g = c0 / 4 + (v >> 4);
     uint32_t mask = v & 15u;
@@ -565,7 +697,7 @@ __device__ __forceinline__ void expand_record(const PassArgs &a, int64_t c0, uin
         a.out_idx[pos] = a.perm[g * 4 + i];
         a.out_dist[pos] = dd;
         ++pos;
-        if (a.sym)   // mirrored entry into row j's L segment (sorted afterwards)
+        if (a.sym)
             a.tmpL[atomicAdd(&a.lpos[g * 4 + i], 1ull)] = ((unsigned long long)sp << 32) | __float_as_uint(dd);
     }
 }
@@ -586,8 +718,14 @@ __global__ void __launch_bounds__(256) compact_lowd(PassArgs a) {
         T q[D];
 #pragma unroll
         for (int k = 0; k < D; ++k) q[k] = Qs[(sp >> 2) * 4 * D + k * 4 + (sp & 3)];
-        const uint16_t *slot = a.slots + (size_t)e * a.cap;
-        for (int r = 0; r < a.cap && pos < end; ++r) expand_record<T, D>(a, c0, slot[r], q, pos, sp);
+        const uint16_t *slot = a.slots + (size_t)item * a.B * a.cap + threadIdx.x;
+        uint32_t v = slot[0];
+        for (int r = 0; r < a.cap && pos < end; ++r) {
+            const uint32_t nv = (r + 1 < a.cap) ? slot[(size_t)(r + 1) * a.B] : 0u;   // prefetch
+            if (a.variant2) expand_record<T, D>(a, c0, v, q, pos, sp);
+            else expand_record_hits<T, D>(a, c0, v, q, pos, sp);
+            v = nv;
+        }
     }
 }
 
@@ -779,19 +917,12 @@ __global__ void __launch_bounds__(256) sym_lsort_warp(PassArgs a) {
         const int64_t o0 = (int64_t)a.lpos[sp] - cnt;   // the row start (cursor advanced by cnt)
         if (lane == 0) { a.out_idx[o0 + cnt] = a.perm[sp]; a.out_dist[o0 + cnt] = 0.f; }   // the point itself
         if (cnt == 0 || cnt > kLWarp) continue;
-        if (cnt <= 32) {
-            unsigned long long v = lane < cnt ? a.tmpL[o0 + lane] : ~0ull;
-#pragma unroll
-            for (int k = 2; k <= 32; k <<= 1) {
-#pragma unroll
-                for (int j = k >> 1; j > 0; j >>= 1) {
-                    const unsigned long long o = __shfl_xor_sync(0xffffffffu, v, j);
-                    const bool up = (lane & k) == 0, lower = (lane & j) == 0;
-                    const unsigned long long lo = v < o ? v : o, hi = v < o ? o : v;
-                    v = (lower == up) ? lo : hi;
-                }
-            }
-            if (lane < cnt) lemit(a, v, o0 + lane);
+        if (cnt <= 32) {   // rank sort: positions are unique within a row
+            const unsigned long long v = lane < cnt ? a.tmpL[o0 + lane] : ~0ull;
+            const uint32_t key = (uint32_t)(v >> 32);
+            int rank = 0;
+            for (int j = 0; j < cnt; ++j) rank += __shfl_sync(0xffffffffu, key, j) < key;
+            if (lane < cnt) lemit(a, v, o0 + rank);
             continue;
         }
         int S = 64;

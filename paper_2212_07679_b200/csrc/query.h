@@ -44,6 +44,7 @@ struct PassArgs {
     const int64_t *blk_lo, *blk_hi, *item_start;
     int64_t nblocks, total_items;
     int B, chunk;
+    int variant2 = 0;       // compaction variant (option compact): 0 per hit, 1 per group
     float T_in, T_out;      // fp32 sure-in / sure-out thresholds on the fp32 d^2
     double R2;              // R*R (fp64), the oracle's threshold
     int32_t *cnt;           // total_items x B hit counts (count / scan pass)

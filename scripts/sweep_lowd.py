@@ -1,6 +1,6 @@
 """Time the low-d scan pass under option variants on a config (GPU tuning sweep).
 
-  python scripts/sweep_lowd.py c2
+  python scripts/sweep_lowd.py c2 ['{"option": [values], ...}']
 """
 import itertools
 import json
@@ -34,6 +34,8 @@ def main():
     w = workloads.CONFIGS[name]()
     X = torch.from_numpy(w.X).cuda()
     grid = {"variant": [1, 2], "chunk": [1024, 2048, 4096], "query_block": [128, 256], "cap": [32, 64]}
+    if len(sys.argv) > 2:
+        grid = json.loads(sys.argv[2])
     keys = list(grid)
     measure(X, w.R, 2)
     for vals in itertools.product(*[grid[k] for k in keys]):
