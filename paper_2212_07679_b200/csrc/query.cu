@@ -493,24 +493,34 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
                     // together (recomputing the group's d^2 from shared memory, exact
                     // classification, emission), so the expensive path runs convergently
                     // instead of once per hitting lane.  Records keep their g order.
+                    // records: index of a GS-group step (g / GS) whose 4 GS pairs have a d^2 <= T_out
+                    constexpr int GS = 2;   // 4 measured slower (more records, costlier drains)
+                    static_assert(GS == 2, "the step loop below is written for 2 groups");
                     uint64_t pend = 0;
                     int npend = 0;
                     auto drain = [&]() {
 #pragma unroll 1
                         for (int r = 0; r < 4; ++r) {
                             if (r < npend) {
-                                const uint32_t rec = (uint32_t)(pend >> (16 * r)) & 0xffffu;
-                                const int gg = (int)(rec >> 4);
-                                const uint32_t oa = rec & 15u;
-                                float4 xa[D];
+                                const int g0 = GS * (int)((uint32_t)(pend >> (16 * r)) & 0xffffu);
 #pragma unroll
-                                for (int k = 0; k < D; ++k) xa[k] = g4[gg * D + k];
-                                uint64_t la, ha;
-                                group_d2<D>(xa, nq, la, ha);
-                                const float2 pa = f2unpack(la), qa = f2unpack(ha);
-                                uint32_t ia = mask4(pa.x, pa.y, qa.x, qa.y, T_in);
-                                if (ia ^ oa) ia |= resolve4<D>(oa & ~ia, xa, q, R2);
-                                if (ia) emit0(gg, ia);
+                                for (int h = 0; h < GS; ++h) {
+                                    const int gg = g0 + h;
+                                    if (gg < ngroups) {
+                                        float4 xa[D];
+#pragma unroll
+                                        for (int k = 0; k < D; ++k) xa[k] = g4[gg * D + k];
+                                        uint64_t la, ha;
+                                        group_d2<D>(xa, nq, la, ha);
+                                        const float2 pa = f2unpack(la), qa = f2unpack(ha);
+                                        const uint32_t oa = mask4(pa.x, pa.y, qa.x, qa.y, T_out);
+                                        if (oa) {
+                                            uint32_t ia = mask4(pa.x, pa.y, qa.x, qa.y, T_in);
+                                            if (ia ^ oa) ia |= resolve4<D>(oa & ~ia, xa, q, R2);
+                                            if (ia) emit0(gg, ia);
+                                        }
+                                    }
+                                }
                             }
                         }
                         pend = 0;
@@ -518,14 +528,10 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
                     };
                     constexpr bool LAZY = CONV;
                     const float t_out = T_out;
-                    auto push = [&](int gg, uint32_t m) {
-                        pend |= (uint64_t)(((uint32_t)gg << 4) | m) << (16 * npend);
-                        ++npend;
-                    };
                     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(g4);
-                    for (; LAZY && g + 1 < ngroups; g += 2) {   // 2 groups (8 pairs) per step
+                    uint32_t ga = sbase;
+                    for (; LAZY && g + 1 < ngroups; g += 2, ga += 32u * D) {   // 2 groups (8 pairs) per step
                         float4 xa[D], xb[D];
-                        const uint32_t ga = sbase + (uint32_t)g * (16u * D);
 #pragma unroll
                         for (int k = 0; k < D; ++k) { xa[k] = lds128(ga + 16u * k); xb[k] = lds128(ga + 16u * (D + k)); }
                         uint64_t la, ha, lb, hb;
@@ -535,23 +541,28 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
                         const float mn = fminf(fminf(fminf(pa.x, pa.y), fminf(qa.x, qa.y)),
                                                fminf(fminf(pb.x, pb.y), fminf(qb.x, qb.y)));
                         if (mn <= t_out) {
-                            const uint32_t oa = mask4(pa.x, pa.y, qa.x, qa.y, t_out);
-                            const uint32_t ob = mask4(pb.x, pb.y, qb.x, qb.y, t_out);
-                            if (oa) push(g, oa);
-                            if (ob) push(g + 1, ob);
+                            pend |= (uint64_t)(uint32_t)(g >> 1) << (16 * npend);
+                            ++npend;
                         }
-                        if (__any_sync(0xffffffffu, npend >= 3)) drain();   // FIFO holds 4
+                        if (__any_sync(0xffffffffu, npend >= 4)) drain();   // FIFO holds 4
                     }
-                    for (; LAZY && g < ngroups; ++g) {
-                        float4 xa[D];
+                    if (LAZY && g < ngroups) {   // tail groups (fewer than GS): one record
+                        float mn = INFINITY;
+                        for (int gg = g; gg < ngroups; ++gg) {
+                            float4 xa[D];
 #pragma unroll
-                        for (int k = 0; k < D; ++k) xa[k] = g4[g * D + k];
-                        uint64_t la, ha;
-                        group_d2<D>(xa, nq, la, ha);
-                        const float2 pa = f2unpack(la), qa = f2unpack(ha);
-                        if (fminf(fminf(pa.x, pa.y), fminf(qa.x, qa.y)) <= t_out)
-                            push(g, mask4(pa.x, pa.y, qa.x, qa.y, t_out));
-                        if (__any_sync(0xffffffffu, npend >= 4)) drain();
+                            for (int k = 0; k < D; ++k) xa[k] = g4[gg * D + k];
+                            uint64_t la, ha;
+                            group_d2<D>(xa, nq, la, ha);
+                            const float2 pa = f2unpack(la), qa = f2unpack(ha);
+                            mn = fminf(mn, fminf(fminf(pa.x, pa.y), fminf(qa.x, qa.y)));
+                        }
+                        if (mn <= t_out) {
+                            if (npend == 4) drain();
+                            pend |= (uint64_t)(uint32_t)(g / GS) << (16 * npend);
+                            ++npend;
+                        }
+                        g = ngroups;
                     }
                     if (LAZY) drain();
                     for (; g < ngroups; ++g) {
