@@ -348,14 +348,14 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
         for (int k = 0; k < D; ++k) q[k] = active ? Qs[(sp >> 2) * 4 * D + k * 4 + (sp & 3)] : (T)0;
         // the deferred-hit scan loop (fp32, G == 1) runs warp-converged: lanes without a
         // query take a NaN query (every comparison false, no hits)
-        constexpr bool CONV = MODE == M_SCAN && G == 1 && sizeof(T) == 4;
+        constexpr bool CONV = MODE == M_SCAN && G == 1 && sizeof(T) == 4;   // DBSCAN modes: measured slower
         if (CONV && !active) {
 #pragma unroll
             for (int k = 0; k < D; ++k) q[k] = (T)NAN;
         }
         mbar_wait(&bar[sidx], phase[sidx]);
         phase[sidx] ^= 1u;
-        if (active || CONV) {
+        if (CONV ? __any_sync(0xffffffffu, active) : active) {   // CONV: whole warps
             const int ngroups = (int)((c1 - c0) >> 2);
             if constexpr (sizeof(T) == 4) {
                 const float4 *g4 = reinterpret_cast<const float4 *>(smem + sidx * buf_bytes);
