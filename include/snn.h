@@ -229,6 +229,16 @@ snn_status snn_profile_read(const char *family, double *ms, uint64_t *launches, 
  *                    (1..1024); further records go to a global overflow list
  *   "ovf_records"    capacity of that overflow list (entries that do not fit are
  *                    recomputed by a fix pass)
+ *   "variant"        low-d scan loop: 1 = deferred-hit 2-group loop (default), 2 = 8-pair
+ *                    direct loop
+ *   "symmetric"      -1 = evaluate every pair twice in low-d self-queries (default: once)
+ *   "stage_rows"     -1 = compaction writes final rows directly (default: key-order staging
+ *                    buffer, then whole-row moves)
+ *   "window_all"     1 = brute-force ablation: every query scans all n candidates
+ *   "simt_filter"    1 = low-d fp32 expanded-form pre-filter (default off)
+ *   "lowd_tc", "lowd_tc_tiles", "lowd_tc_group"   low-d tcgen05 path (default off)
+ *   "tc", "tc_min_d", "tc_tiles", "tc_f16", "tc_group", "tc_diag", "tc_gram_min_d"
+ *                    tensor-core path selection and tiling (tests / sweeps)
  * "force_generic" is read by snn_build (it fixes the sorted copy's layout).
  * Returns SNN_ERR_INVALID_ARGUMENT for an unknown key or bad value. */
 snn_status snn_set_option(const char *key, int64_t value);

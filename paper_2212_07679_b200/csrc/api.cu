@@ -40,12 +40,12 @@ struct Options {
     int tc_group = 128;  // query blocks per raster group (upper bound; L2 budget decides)
     int tc_gram_min_d = 32;    // Gram matrix on the tensor cores for d >= this
     int symmetric = 1;   // low-d self-queries: each unordered pair evaluated once
+    int stage_rows = 1;  // low-d: assemble rows in key order, then move each row whole
     int window_all = 0;  // ablation "brute force 2": windows = all points
     int simt_filter = 0; // low-d fp32 scan: expanded-form SIMT pre-filter (option; measured slower on c2/c5)
     int lowd_tc = 0;     // low-d (fp32, d <= 8) radius queries through the tensor-core filter (option; FFMA default)
     int lowd_tc_tiles = 8;     // 256-candidate tiles per work item (low-d tensor-core path)
     int lowd_tc_group = 8;     // query blocks per raster group (low-d tensor-core path)
-    int compact = 0;           // low-d compaction: 0 = per hit, 1 = per record group (vector loads)
 };
 static std::atomic<int64_t> g_last_ovf{0}, g_last_lost{0};
 static Options g_opt;
@@ -254,7 +254,6 @@ snn_status snn_set_option(const char *key, int64_t value) {
         g_opt.chunk = (int)value;
         return SNN_OK;
     }
-    if (k == "compact") { g_opt.compact = value ? 1 : 0; return SNN_OK; }
     if (k == "cap") {
         if (value == 0) value = 64;
         if (value < 1 || value > 1024) return fail(SNN_ERR_INVALID_ARGUMENT, "cap must be 1..1024");
@@ -286,6 +285,7 @@ snn_status snn_set_option(const char *key, int64_t value) {
         return SNN_OK;
     }
     if (k == "symmetric") { g_opt.symmetric = value < 0 ? 0 : 1; return SNN_OK; }
+    if (k == "stage_rows") { g_opt.stage_rows = value < 0 ? 0 : 1; return SNN_OK; }
     if (k == "window_all") { g_opt.window_all = value > 0 ? 1 : 0; return SNN_OK; }
     if (k == "simt_filter") { g_opt.simt_filter = value > 0 ? 1 : 0; return SNN_OK; }   // 0: default (off)
     if (k == "lowd_tc") { g_opt.lowd_tc = value > 0 ? 1 : 0; return SNN_OK; }   // 0: default (off)
@@ -1017,6 +1017,13 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
     a.B = B; a.chunk = chunk;
     a.R2 = R * R;
     int32_t *maxl = nullptr;
+    const bool stage = !generic && g_opt.stage_rows;
+    int32_t *srow = nullptr;
+    int64_t *soff = nullptr;
+    if (stage) {
+        CK(ws.alloc(&srow, (size_t)m), "alloc");
+        CK(ws.alloc(&soff, (size_t)m + 1), "alloc");
+    }
     if (sym) {
         a.sym = 1;
         CK(ws.alloc(&a.lcnt, (size_t)m), "alloc");
@@ -1033,24 +1040,28 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
     a.offsets = r->offsets; a.out_idx = nullptr; a.out_dist = nullptr;
     a.sm_count = sms;
     a.variant = g_opt.variant;
-    a.variant2 = g_opt.compact;
     if (!generic && !f64 && idx->Xf && g_opt.simt_filter) {
         double c1h = 1.0, r2h = 0.0;
         simt_filter_consts(D, R, &c1h, &r2h);
         a.Xf = idx->Xf; a.c1h = idx->xf_c1h; a.r2h = r2h; a.mu_f = idx->mu_f;
     }
     if (total_items == 0) {
-        if (sym) launch_row_totals_sym(cnt, pre, item_start, m, B, qperm, a.lcnt, row_count, maxl, s);
+        if (sym) launch_row_totals_sym(cnt, pre, item_start, m, B, qperm, a.lcnt, row_count, maxl, srow, s);
         else cudaMemsetAsync(row_count, 0, (size_t)m * 4, s);
+        if (srow) cudaMemsetAsync(srow, 0, (size_t)m * 4, s);
     } else {
         const int ctok = prof_begin(F_COUNT, s);
         if (generic) launch_generic_pass(false, a, s);                           // K8 count
         else launch_lowd_scan(a, s);                                             // K8 scan
         prof_end(ctok, s, pairs_eval);
-        if (sym) launch_row_totals_sym(cnt, pre, item_start, m, B, qperm, a.lcnt, row_count, maxl, s);
-        else launch_row_totals(cnt, pre, item_start, m, B, qperm, row_count, s);  // K11
+        if (sym) launch_row_totals_sym(cnt, pre, item_start, m, B, qperm, a.lcnt, row_count, maxl, srow, s);
+        else launch_row_totals(cnt, pre, item_start, m, B, qperm, row_count, srow, s);  // K11
     }
     exclusive_scan_i32_to_i64(row_count, r->offsets, m, scan_tmp, s);
+    if (stage) {
+        exclusive_scan_i32_to_i64(srow, soff, m, scan_tmp, s);   // key-order row starts
+        a.soff = soff;
+    }
     {
         cudaError_t e = cudaMemcpyAsync(hp, r->offsets + m, 8, cudaMemcpyDeviceToHost, s);
         if (e == cudaSuccess && a.ovf_count)
@@ -1078,6 +1089,8 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
         r->distances = static_cast<float *>(p);
     }
     a.out_idx = r->indices; a.out_dist = r->distances;
+    if (stage)   // the compaction and fix passes assemble rows in key order here
+        CK(ws.alloc(&a.stage, (size_t)(r->nnz > 0 ? r->nnz : 1)), "alloc staged rows");
     if (sym) {
         CK(ws.alloc(&a.tmpL, (size_t)(r->nnz > 0 ? r->nnz : 1)), "alloc mirrored entries");
         launch_sym_lpos_init(a, s);
@@ -1089,7 +1102,7 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
         } else {
             launch_lowd_compact(a, s);                                           // K11 compact
             launch_lowd_fix(a, s);                                               // overflow fix
-            if (sym) launch_sym_lsort(a, max_l, s);                              // mirrored rows
+            launch_rows_finalize(a, max_l, s);                                   // rows -> CSR
         }
         prof_end(wtok, s, generic ? pairs_eval : (double)r->nnz);
     }

@@ -31,6 +31,21 @@ namespace snn {
 namespace {
 
 // ---------------------------------------------------------------------------- K7
+// one CSR entry: into the staging buffer (one 8-byte store) or the final arrays
+__device__ __forceinline__ void put_entry(const PassArgs &a, int64_t pos, int32_t id, float dist) {
+    if (a.stage) {
+        a.stage[pos] = ((unsigned long long)__float_as_uint(dist) << 32) | (uint32_t)id;
+    } else {
+        a.out_idx[pos] = id;
+        a.out_dist[pos] = dist;
+    }
+}
+
+// where row sp is assembled: its key-order start (staged rows) or its final CSR row
+__device__ __forceinline__ int64_t row_base(const PassArgs &a, int64_t sp) {
+    return a.soff ? a.soff[sp] : a.offsets[a.qperm[sp]];
+}
+
 __device__ __forceinline__ int64_t lower_bound_f(const float *a, int64_t n, float x) {
     int64_t lo = 0, hi = n;
     while (lo < hi) {
@@ -170,8 +185,7 @@ struct Emitter {
     __device__ __forceinline__ void write(int64_t j, double s) {      // MODE 1
         if (SYM && j <= sp) return;
         const float dd = (float)sqrt(s);
-        a.out_idx[pos] = a.perm[j];
-        a.out_dist[pos] = dd;
+        put_entry(a, pos, a.perm[j], dd);
         ++pos;
         ++c;
         if (SYM)   // mirrored entry into row j's L segment
@@ -335,7 +349,7 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
         em.sp = sp;
         if (MODE == M_FIX) {
             active = active && a.cnt[e] < 0;   // lost-entry flag (sign bit)
-            if (active) em.pos = a.offsets[a.qperm[sp]] + a.pre[e];
+            if (active) em.pos = row_base(a, sp) + a.pre[e];
         }
         if (MODE == M_UNION) active = active && a.core[sp] && c1 - 1 > sp;   // pairs j > i only
         // M_BORDER over a compacted query list: qperm maps to the index position
@@ -644,56 +658,8 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
 // Compaction of the recorded hits into the CSR: original ids via pi and distances as
 // (float)sqrt of the oracle-order fp64 squared distance.  One CTA per item; one thread
 // per (item, query) entry expands its slot records (the first `cap` records).
-// One record = one candidate group g (4 consecutive sorted positions) and its hit mask.
-// The group's rows are one AoSoA4 block (D x 4 values, loaded with vector loads), the
-// mirrored cursors are claimed first so the atomics overlap the loads and the fp64 math.
 template <typename T, int D>
 __device__ __forceinline__ void expand_record(const PassArgs &a, int64_t c0, uint32_t v,
-                                              const T (&q)[D], int64_t &pos, int64_t sp) {
-    const T *Xs = static_cast<const T *>(a.Xs);
-    const int64_t g = c0 / 4 + (v >> 4);
-    const uint32_t mask = v & 15u;
-    unsigned long long mp[4] = {0, 0, 0, 0};
-    if (a.sym) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-            if (mask & (1u << i)) mp[i] = atomicAdd(&a.lpos[g * 4 + i], 1ull);
-    }
-    int32_t id[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) id[i] = (mask & (1u << i)) ? a.perm[g * 4 + i] : 0;
-    T x[D][4];
-    if constexpr (sizeof(T) == 4) {
-#pragma unroll
-        for (int k = 0; k < D; ++k) {
-            const float4 t = *reinterpret_cast<const float4 *>(Xs + g * 4 * D + k * 4);
-            x[k][0] = t.x; x[k][1] = t.y; x[k][2] = t.z; x[k][3] = t.w;
-        }
-    } else {
-#pragma unroll
-        for (int k = 0; k < D; ++k) {
-            const double2 t0 = *reinterpret_cast<const double2 *>(Xs + g * 4 * D + k * 4);
-            const double2 t1 = *reinterpret_cast<const double2 *>(Xs + g * 4 * D + k * 4 + 2);
-            x[k][0] = t0.x; x[k][1] = t0.y; x[k][2] = t1.x; x[k][3] = t1.y;
-        }
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        if (!(mask & (1u << i))) continue;
-        T xi[D];
-#pragma unroll
-        for (int k = 0; k < D; ++k) xi[k] = x[k][i];
-        const float dd = (float)sqrt(sqdist_exact(xi, q, D));
-        a.out_idx[pos] = id[i];
-        a.out_dist[pos] = dd;
-        ++pos;
-        if (a.sym)   // mirrored entry into row j's L segment (sorted afterwards)
-            a.tmpL[mp[i]] = ((unsigned long long)sp << 32) | __float_as_uint(dd);
-    }
-}
-
-template <typename T, int D>
-__device__ __forceinline__ void expand_record_hits(const PassArgs &a, int64_t c0, uint32_t v,
                                                    const T (&q)[D], int64_t &pos, int64_t sp) {
     const T *Xs = static_cast<const T *>(a.Xs);
     const int64_t g = c0 / 4 + (v >> 4);
@@ -705,8 +671,7 @@ __device__ __forceinline__ void expand_record_hits(const PassArgs &a, int64_t c0
 #pragma unroll
         for (int k = 0; k < D; ++k) x[k] = Xs[g * 4 * D + k * 4 + i];
         const float dd = (float)sqrt(sqdist_exact(x, q, D));
-        a.out_idx[pos] = a.perm[g * 4 + i];
-        a.out_dist[pos] = dd;
+        put_entry(a, pos, a.perm[g * 4 + i], dd);
         ++pos;
         if (a.sym)
             a.tmpL[atomicAdd(&a.lpos[g * 4 + i], 1ull)] = ((unsigned long long)sp << 32) | __float_as_uint(dd);
@@ -724,7 +689,7 @@ __global__ void __launch_bounds__(256) compact_lowd(PassArgs a) {
         const int64_t e = item * a.B + threadIdx.x;
         const int32_t cv = a.cnt[e];
         if (cv <= 0) continue;   // no hits, or lost entry (sign bit): the fix pass writes it
-        int64_t pos = a.offsets[a.qperm[sp]] + a.pre[e];
+        int64_t pos = row_base(a, sp) + a.pre[e];
         const int64_t end = pos + cv;
         T q[D];
 #pragma unroll
@@ -733,8 +698,7 @@ __global__ void __launch_bounds__(256) compact_lowd(PassArgs a) {
         uint32_t v = slot[0];
         for (int r = 0; r < a.cap && pos < end; ++r) {
             const uint32_t nv = (r + 1 < a.cap) ? slot[(size_t)(r + 1) * a.B] : 0u;   // prefetch
-            if (a.variant2) expand_record<T, D>(a, c0, v, q, pos, sp);
-            else expand_record_hits<T, D>(a, c0, v, q, pos, sp);
+            expand_record<T, D>(a, c0, v, q, pos, sp);
             v = nv;
         }
     }
@@ -752,7 +716,7 @@ __global__ void __launch_bounds__(256) compact_overflow(PassArgs a, int64_t n_re
         int64_t b, c0, c1;
         locate(a, item, b, c0, c1);
         const int64_t sp = b * a.B + t;
-        int64_t pos = a.offsets[a.qperm[sp]] + a.pre[r.e] + r.before;
+        int64_t pos = row_base(a, sp) + a.pre[r.e] + r.before;
         T q[D];
 #pragma unroll
         for (int kk = 0; kk < D; ++kk) q[kk] = Qs[(sp >> 2) * 4 * D + kk * 4 + (sp & 3)];
@@ -882,7 +846,7 @@ __global__ void __launch_bounds__(256) window_generic(PassArgs a) {
 }
 
 __global__ void row_totals(const int32_t *cnt, int32_t *pre, const int64_t *item_start, int64_t m,
-                           int B, const int32_t *qperm, int32_t *row_count) {
+                           int B, const int32_t *qperm, int32_t *row_count, int32_t *srow) {
     const int64_t sp = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (sp >= m) return;
     const int64_t b = sp / B, t = sp % B;
@@ -893,10 +857,12 @@ __global__ void row_totals(const int32_t *cnt, int32_t *pre, const int64_t *item
         run += c;
     }
     row_count[qperm ? qperm[sp] : sp] = run;
+    if (srow) srow[sp] = run;
 }
 
 __global__ void row_totals_sym(const int32_t *cnt, int32_t *pre, const int64_t *item_start, int64_t m, int B,
-                               const int32_t *qperm, const int32_t *lcnt, int32_t *row_count, int32_t *maxl) {
+                               const int32_t *qperm, const int32_t *lcnt, int32_t *row_count, int32_t *maxl,
+                               int32_t *srow) {
     const int64_t sp = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (sp >= m) return;
     const int64_t b = sp / B, t = sp % B;
@@ -908,6 +874,7 @@ __global__ void row_totals_sym(const int32_t *cnt, int32_t *pre, const int64_t *
         run += c;
     }
     row_count[qperm[sp]] = run;
+    if (srow) srow[sp] = run;
     atomicMax(maxl, l);
 }
 
@@ -918,27 +885,42 @@ __device__ __forceinline__ void lemit(const PassArgs &a, unsigned long long v, i
     a.out_idx[pos] = a.perm[(uint32_t)(v >> 32)];
     a.out_dist[pos] = __uint_as_float((uint32_t)v);
 }
-__global__ void __launch_bounds__(256) sym_lsort_warp(PassArgs a) {
+// Warp per row.  Symmetric self-query: the row's L segment (mirrored entries, arrival order)
+// is sorted by position -- rank sort in registers (<= 32 entries; positions are unique), a
+// shared-memory bitonic sort (<= 512; longer rows: rows_lsort_block) -- and written with
+// the self entry.  Staged rows: the rest of the row is copied from the key-order staging
+// buffer to the row's original-id position.
+__global__ void __launch_bounds__(256) rows_finalize_warp(PassArgs a) {
     __shared__ unsigned long long sbuf[8][kLWarp];
     const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
     unsigned long long *buf = sbuf[w];
     for (int64_t sp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; sp < a.m;
          sp += (int64_t)gridDim.x * blockDim.x / 32) {
-        const int cnt = a.lcnt[sp];
-        const int64_t o0 = (int64_t)a.lpos[sp] - cnt;   // the row start (cursor advanced by cnt)
-        if (lane == 0) { a.out_idx[o0 + cnt] = a.perm[sp]; a.out_dist[o0 + cnt] = 0.f; }   // the point itself
+        const int cnt = a.sym ? a.lcnt[sp] : 0;
+        const int64_t src = a.soff ? a.soff[sp] : (int64_t)a.lpos[sp] - cnt;   // L cursor advanced by cnt
+        const int64_t dst = a.soff ? a.offsets[a.qperm[sp]] : src;
+        if (a.soff) {   // U part (after L and self) or the whole row
+            const int64_t k0 = a.sym ? cnt + 1 : 0, len = a.soff[sp + 1] - src;
+            for (int64_t k = k0 + lane; k < len; k += 32) {
+                const unsigned long long v = a.stage[src + k];
+                a.out_idx[dst + k] = (int32_t)(uint32_t)v;
+                a.out_dist[dst + k] = __uint_as_float((uint32_t)(v >> 32));
+            }
+        }
+        if (!a.sym) continue;
+        if (lane == 0) { a.out_idx[dst + cnt] = a.perm[sp]; a.out_dist[dst + cnt] = 0.f; }   // the point itself
         if (cnt == 0 || cnt > kLWarp) continue;
         if (cnt <= 32) {   // rank sort: positions are unique within a row
-            const unsigned long long v = lane < cnt ? a.tmpL[o0 + lane] : ~0ull;
+            const unsigned long long v = lane < cnt ? a.tmpL[src + lane] : ~0ull;
             const uint32_t key = (uint32_t)(v >> 32);
             int rank = 0;
             for (int j = 0; j < cnt; ++j) rank += __shfl_sync(0xffffffffu, key, j) < key;
-            if (lane < cnt) lemit(a, v, o0 + rank);
+            if (lane < cnt) lemit(a, v, dst + rank);
             continue;
         }
         int S = 64;
         while (S < cnt) S <<= 1;
-        for (int i = lane; i < S; i += 32) buf[i] = i < cnt ? a.tmpL[o0 + i] : ~0ull;
+        for (int i = lane; i < S; i += 32) buf[i] = i < cnt ? a.tmpL[src + i] : ~0ull;
         __syncwarp();
         for (int k = 2; k <= S; k <<= 1) {
             for (int j = k >> 1; j > 0; j >>= 1) {
@@ -952,16 +934,17 @@ __global__ void __launch_bounds__(256) sym_lsort_warp(PassArgs a) {
                 __syncwarp();
             }
         }
-        for (int i = lane; i < cnt; i += 32) lemit(a, buf[i], o0 + i);
+        for (int i = lane; i < cnt; i += 32) lemit(a, buf[i], dst + i);
         __syncwarp();
     }
 }
-__global__ void __launch_bounds__(1024) sym_lsort_block(PassArgs a) {
+__global__ void __launch_bounds__(1024) rows_lsort_block(PassArgs a) {
     extern __shared__ unsigned long long lbuf[];
     for (int64_t sp = blockIdx.x; sp < a.m; sp += gridDim.x) {
         const int cnt = a.lcnt[sp];
         if (cnt <= kLWarp || cnt > kLBlock) continue;
-        const int64_t o0 = (int64_t)a.lpos[sp] - cnt;
+        const int64_t o0 = a.soff ? a.soff[sp] : (int64_t)a.lpos[sp] - cnt;
+        const int64_t dst = a.soff ? a.offsets[a.qperm[sp]] : o0;
         int S = 1024;
         while (S < cnt) S <<= 1;
         for (int i = threadIdx.x; i < S; i += blockDim.x) lbuf[i] = i < cnt ? a.tmpL[o0 + i] : ~0ull;
@@ -978,7 +961,7 @@ __global__ void __launch_bounds__(1024) sym_lsort_block(PassArgs a) {
                 __syncthreads();
             }
         }
-        for (int i = threadIdx.x; i < cnt; i += blockDim.x) lemit(a, lbuf[i], o0 + i);
+        for (int i = threadIdx.x; i < cnt; i += blockDim.x) lemit(a, lbuf[i], dst + i);
         __syncthreads();
     }
 }
@@ -1095,15 +1078,15 @@ void launch_generic_pass(bool write, const PassArgs &a, cudaStream_t s) {
 
 void launch_row_totals_sym(const int32_t *cnt, int32_t *pre, const int64_t *item_start, int64_t m, int B,
                            const int32_t *qperm, const int32_t *lcnt, int32_t *row_count, int32_t *maxl,
-                           cudaStream_t s) {
+                           int32_t *srow, cudaStream_t s) {
     if (m == 0) return;
     SNN_LAUNCH(row_totals_sym, (int)ceil_div(m, 256), 256, 0, s, cnt, pre, item_start, m, B, qperm, lcnt, row_count,
-               maxl);
+               maxl, srow);
 }
 
 __global__ void sym_lpos_init(PassArgs a) {
     for (int64_t sp = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; sp < a.m; sp += (int64_t)gridDim.x * blockDim.x)
-        a.lpos[sp] = (unsigned long long)a.offsets[a.qperm[sp]];
+        a.lpos[sp] = (unsigned long long)row_base(a, sp);
 }
 
 void launch_sym_lpos_init(const PassArgs &a, cudaStream_t s) {
@@ -1113,21 +1096,21 @@ void launch_sym_lpos_init(const PassArgs &a, cudaStream_t s) {
     SNN_LAUNCH(sym_lpos_init, (int)g, 256, 0, s, a);
 }
 
-void launch_sym_lsort(const PassArgs &a, int32_t max_l, cudaStream_t s) {
-    if (a.m == 0) return;
+void launch_rows_finalize(const PassArgs &a, int32_t max_l, cudaStream_t s) {
+    if (a.m == 0 || (!a.sym && !a.soff)) return;
     int64_t g = ceil_div(a.m * 32, 256);
     if (g > 148 * 16) g = 148 * 16;
-    SNN_LAUNCH(sym_lsort_warp, (int)g, 256, 0, s, a);
-    if (max_l <= kLWarp) return;
+    SNN_LAUNCH(rows_finalize_warp, (int)g, 256, 0, s, a);
+    if (!a.sym || max_l <= kLWarp) return;
     const size_t smem = (size_t)kLBlock * 8;
-    cudaFuncSetAttribute(sym_lsort_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    SNN_LAUNCH(sym_lsort_block, 148 * 2, 1024, smem, s, a);
+    cudaFuncSetAttribute(rows_lsort_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    SNN_LAUNCH(rows_lsort_block, 148 * 2, 1024, smem, s, a);
 }
 
 void launch_row_totals(const int32_t *cnt, int32_t *pre, const int64_t *item_start, int64_t m,
-                       int B, const int32_t *qperm, int32_t *row_count, cudaStream_t s) {
+                       int B, const int32_t *qperm, int32_t *row_count, int32_t *srow, cudaStream_t s) {
     if (m == 0) return;
-    SNN_LAUNCH(row_totals, (int)ceil_div(m, 256), 256, 0, s, cnt, pre, item_start, m, B, qperm, row_count);
+    SNN_LAUNCH(row_totals, (int)ceil_div(m, 256), 256, 0, s, cnt, pre, item_start, m, B, qperm, row_count, srow);
 }
 
 namespace {

@@ -44,7 +44,6 @@ struct PassArgs {
     const int64_t *blk_lo, *blk_hi, *item_start;
     int64_t nblocks, total_items;
     int B, chunk;
-    int variant2 = 0;       // compaction variant (option compact): 0 per hit, 1 per group
     float T_in, T_out;      // fp32 sure-in / sure-out thresholds on the fp32 d^2
     double R2;              // R*R (fp64), the oracle's threshold
     int32_t *cnt;           // total_items x B hit counts (count / scan pass)
@@ -76,6 +75,11 @@ struct PassArgs {
     int32_t *lcnt = nullptr;             // per sorted position: |{j < i : i in U(j)}|
     unsigned long long *lpos = nullptr;  // per sorted position: next L slot (starts at the row start)
     unsigned long long *tmpL = nullptr;  // nnz: (position << 32 | fp32 distance bits) at row start
+    // staged rows (low-d path): the compaction writes every row at its key-order start
+    // soff[sp] (so concurrent CTAs write neighbouring memory), rows_finalize then moves
+    // each row whole to its original-id position offsets[qperm[sp]]
+    const int64_t *soff = nullptr;
+    unsigned long long *stage = nullptr;   // staged entries: (fp32 distance bits << 32 | id)
     // expanded-form SIMT filter (scan variant 3; nullptr = off): AoSoA4 rows with D+1
     // floats (centred coordinates, xbar c1h), the margin constants and mu_f
     const float *Xf = nullptr;
@@ -110,16 +114,18 @@ void launch_lowd_mode(int mode, const PassArgs &a, cudaStream_t s);
 void launch_generic_pass(bool write, const PassArgs &a, cudaStream_t s);
 
 // symmetric self-query: totals = U hits + L hits + self; pre[e] starts after L + self
+// srow (nullable): the same totals in key order (staged rows)
 void launch_row_totals_sym(const int32_t *cnt, int32_t *pre, const int64_t *item_start, int64_t m, int B,
                            const int32_t *qperm, const int32_t *lcnt, int32_t *row_count, int32_t *maxl,
-                           cudaStream_t s);
-// symmetric self-query: L cursors = CSR row starts (lpos[sp] = offsets[qperm[sp]])
+                           int32_t *srow, cudaStream_t s);
+// symmetric self-query: L cursors = row starts (lpos[sp] = row base of sp)
 void launch_sym_lpos_init(const PassArgs &a, cudaStream_t s);
-// symmetric self-query: sort every row's L segment by position, write it and the self entry
-void launch_sym_lsort(const PassArgs &a, int32_t max_l, cudaStream_t s);
+// rows -> final CSR: symmetric self-query: sort every row's L segment by position, write it
+// and the self entry; staged rows: move every row to offsets[qperm[sp]]
+void launch_rows_finalize(const PassArgs &a, int32_t max_l, cudaStream_t s);
 // K11 helper: per-row totals over a block's items; pre = exclusive per-item prefixes
 // (pre may alias cnt); row_count[qperm[sp]] = total (qperm NULL: row_count[sp]).
 void launch_row_totals(const int32_t *cnt, int32_t *pre, const int64_t *item_start, int64_t m,
-                       int B, const int32_t *qperm, int32_t *row_count, cudaStream_t s);
+                       int B, const int32_t *qperm, int32_t *row_count, int32_t *srow, cudaStream_t s);
 
 }  // namespace snn
