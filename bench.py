@@ -263,6 +263,9 @@ def run_gpu(args):
     torch.cuda.set_device(dev)
     import paper_2212_07679_b200 as snn
     snn.load_library()
+    for kv in args.opt:   # tuning A/B: --opt key=value (snn_set_option)
+        k, v = kv.split("=")
+        snn.snn_set_option(k, int(v))
     w = workload(args.config)
     X = torch.from_numpy(w.X).to(dev)
     Qd = None if w.Q is None else torch.from_numpy(w.Q).to(dev)
@@ -392,6 +395,7 @@ def main():
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--opt", action="append", default=[], help="library option key=value (A/B runs)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

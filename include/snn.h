@@ -235,7 +235,8 @@ snn_status snn_profile_read(const char *family, double *ms, uint64_t *launches, 
  *   "stage_rows"     -1 = compaction writes final rows directly (default: key-order staging
  *                    buffer, then whole-row moves)
  *   "window_all"     1 = brute-force ablation: every query scans all n candidates
- *   "simt_filter"    1 = low-d fp32 expanded-form pre-filter (default off)
+ *   "simt_filter"    low-d fp32 expanded-form pre-filter: default on for radius queries and
+ *                    off for DBSCAN; 1 = on everywhere, -1 = off everywhere
  *   "lowd_tc", "lowd_tc_tiles", "lowd_tc_group"   low-d tcgen05 path (default off)
  *   "tc", "tc_min_d", "tc_tiles", "tc_f16", "tc_group", "tc_diag", "tc_gram_min_d"
  *                    tensor-core path selection and tiling (tests / sweeps)

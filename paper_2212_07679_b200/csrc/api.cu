@@ -42,7 +42,9 @@ struct Options {
     int symmetric = 1;   // low-d self-queries: each unordered pair evaluated once
     int stage_rows = 1;  // low-d: assemble rows in key order, then move each row whole
     int window_all = 0;  // ablation "brute force 2": windows = all points
-    int simt_filter = 0; // low-d fp32 scan: expanded-form SIMT pre-filter (option; measured slower on c2/c5)
+    // low-d fp32 expanded-form SIMT pre-filter: 0 = default (radius queries on: faster on
+    // c2; DBSCAN passes off: dense hits make it slower on c5), 1 = on everywhere, -1 = off
+    int simt_filter = 0;
     int lowd_tc = 0;     // low-d (fp32, d <= 8) radius queries through the tensor-core filter (option; FFMA default)
     int lowd_tc_tiles = 8;     // 256-candidate tiles per work item (low-d tensor-core path)
     int lowd_tc_group = 8;     // query blocks per raster group (low-d tensor-core path)
@@ -102,7 +104,7 @@ static void prof_drain() {
     g_prof.pending.clear();
 }
 
-bool dbscan_simt_filter() { return g_opt.simt_filter != 0; }
+bool dbscan_simt_filter() { return g_opt.simt_filter > 0; }
 
 snn_status fail(snn_status st, const std::string &msg) {
     t_err = msg;
@@ -287,7 +289,7 @@ snn_status snn_set_option(const char *key, int64_t value) {
     if (k == "symmetric") { g_opt.symmetric = value < 0 ? 0 : 1; return SNN_OK; }
     if (k == "stage_rows") { g_opt.stage_rows = value < 0 ? 0 : 1; return SNN_OK; }
     if (k == "window_all") { g_opt.window_all = value > 0 ? 1 : 0; return SNN_OK; }
-    if (k == "simt_filter") { g_opt.simt_filter = value > 0 ? 1 : 0; return SNN_OK; }   // 0: default (off)
+    if (k == "simt_filter") { g_opt.simt_filter = value > 0 ? 1 : (value < 0 ? -1 : 0); return SNN_OK; }
     if (k == "lowd_tc") { g_opt.lowd_tc = value > 0 ? 1 : 0; return SNN_OK; }   // 0: default (off)
     if (k == "lowd_tc_tiles") {
         if (value == 0) value = 8;
@@ -1040,7 +1042,7 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
     a.offsets = r->offsets; a.out_idx = nullptr; a.out_dist = nullptr;
     a.sm_count = sms;
     a.variant = g_opt.variant;
-    if (!generic && !f64 && idx->Xf && g_opt.simt_filter) {
+    if (!generic && !f64 && idx->Xf && g_opt.simt_filter >= 0) {
         double c1h = 1.0, r2h = 0.0;
         simt_filter_consts(D, R, &c1h, &r2h);
         a.Xf = idx->Xf; a.c1h = idx->xf_c1h; a.r2h = r2h; a.mu_f = idx->mu_f;

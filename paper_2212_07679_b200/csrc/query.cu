@@ -303,10 +303,10 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
     const int tid = threadIdx.x;
     const T *Xs = static_cast<const T *>(a.Xs);
     const T *Qs = static_cast<const T *>(a.Qs);
-    // G == 3: expanded-form filter rows (AoSoA4, D+1 floats per row) staged after the
-    // original coordinates of the chunk
+    // G == 3: only the expanded-form filter rows (AoSoA4, D+1 floats per row) are staged;
+    // the exact classification of the few groups that pass reads the rows from global memory
     constexpr int FW = G == 3 ? D + 1 : 0;
-    const size_t orig_bytes = (size_t)a.chunk * D * sizeof(T);
+    const size_t orig_bytes = G == 3 ? 0 : (size_t)a.chunk * D * sizeof(T);
     const size_t buf_bytes = orig_bytes + (size_t)a.chunk * FW * 4;
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem + 2 * buf_bytes);
     const int64_t n_work = MODE == M_FIX ? a.n_ovf : a.total_items;
@@ -320,11 +320,11 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
     auto issue = [&](int64_t item, int sidx) {
         int64_t b, c0, c1;
         locate(a, item, b, c0, c1);
-        const uint32_t bytes = (uint32_t)((c1 - c0) * D * sizeof(T));
+        const uint32_t bytes = G == 3 ? 0u : (uint32_t)((c1 - c0) * D * sizeof(T));
         const uint32_t fbytes = (uint32_t)((c1 - c0) * FW * 4);
         fence_proxy_async_smem();
         mbar_arrive_expect_tx(&bar[sidx], bytes + fbytes);
-        bulk_g2s(smem + sidx * buf_bytes, Xs + c0 * D, bytes, &bar[sidx]);
+        if (G != 3) bulk_g2s(smem + sidx * buf_bytes, Xs + c0 * D, bytes, &bar[sidx]);
         if (FW) bulk_g2s(smem + sidx * buf_bytes + orig_bytes, a.Xf + c0 * FW, fbytes, &bar[sidx]);
     };
     uint32_t phase[2] = {0u, 0u};
@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
         for (int k = 0; k < D; ++k) q[k] = active ? Qs[(sp >> 2) * 4 * D + k * 4 + (sp & 3)] : (T)0;
         // the deferred-hit scan loop (fp32, G == 1) runs warp-converged: lanes without a
         // query take a NaN query (every comparison false, no hits)
-        constexpr bool CONV = MODE == M_SCAN && G == 1 && sizeof(T) == 4;   // DBSCAN modes: measured slower
+        constexpr bool CONV = MODE == M_SCAN && (G == 1 || G == 3) && sizeof(T) == 4;   // DBSCAN modes: measured slower
         if (CONV && !active) {
 #pragma unroll
             for (int k = 0; k < D; ++k) q[k] = (T)NAN;
@@ -372,7 +372,8 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
         if (CONV ? __any_sync(0xffffffffu, active) : active) {   // CONV: whole warps
             const int ngroups = (int)((c1 - c0) >> 2);
             if constexpr (sizeof(T) == 4) {
-                const float4 *g4 = reinterpret_cast<const float4 *>(smem + sidx * buf_bytes);
+                const float4 *g4 = G == 3 ? reinterpret_cast<const float4 *>(Xs) + (c0 >> 2) * D
+                                          : reinterpret_cast<const float4 *>(smem + sidx * buf_bytes);
                 uint64_t nq[D];
 #pragma unroll
                 for (int k = 0; k < D; ++k) nq[k] = f2pack(-q[k], -q[k]);
@@ -439,7 +440,7 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
                     // margin of reading C20 for fp32 FFMA chains), acc = xbar' - x_c.q_c per
                     // candidate, 2 FFMA2 per coordinate and 4 candidates; candidates go to the
                     // exact direct-form classification below (identical decisions)
-                    if constexpr (G == 3) {
+                    if constexpr (G == 3 && !CONV) {
                         const float4 *f4 = reinterpret_cast<const float4 *>(smem + sidx * buf_bytes + orig_bytes);
                         for (; g + 1 < ngroups; g += 2) {
                             float4 fa[D + 1], fb[D + 1];
@@ -544,7 +545,7 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
                     const float t_out = T_out;
                     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(g4);
                     uint32_t ga = sbase;
-                    for (; LAZY && g + 1 < ngroups; g += 2, ga += 32u * D) {   // 2 groups (8 pairs) per step
+                    for (; LAZY && G == 1 && g + 1 < ngroups; g += 2, ga += 32u * D) {   // 2 groups (8 pairs) per step
                         float4 xa[D], xb[D];
 #pragma unroll
                         for (int k = 0; k < D; ++k) { xa[k] = lds128(ga + 16u * k); xb[k] = lds128(ga + 16u * (D + k)); }
@@ -559,6 +560,38 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
                             ++npend;
                         }
                         if (__any_sync(0xffffffffu, npend >= 4)) drain();   // FIFO holds 4
+                    }
+                    // G == 3: the expanded form eq:ip2 as a conservative filter
+                    // over the staged rows, acc = xbar' - x_c.q_c (one FFMA2 per coordinate and
+                    // 2 candidates) against the rigorous threshold thr (margin of reading C20);
+                    // the drain classifies the passing steps exactly in the direct form
+                    if constexpr (LAZY && G == 3) {
+                        uint32_t fa_addr = (uint32_t)__cvta_generic_to_shared(smem + sidx * buf_bytes + orig_bytes);
+                        for (; g + 1 < ngroups; g += 2, fa_addr += 32u * (D + 1)) {
+                            float4 fa[D + 1], fb[D + 1];
+#pragma unroll
+                            for (int k = 0; k <= D; ++k) {
+                                fa[k] = lds128(fa_addr + 16u * k);
+                                fb[k] = lds128(fa_addr + 16u * (D + 1 + k));
+                            }
+                            uint64_t la = f2pack(fa[D].x, fa[D].y), ha = f2pack(fa[D].z, fa[D].w);
+                            uint64_t lb = f2pack(fb[D].x, fb[D].y), hb = f2pack(fb[D].z, fb[D].w);
+#pragma unroll
+                            for (int k = 0; k < D; ++k) {
+                                la = f2fma(f2pack(fa[k].x, fa[k].y), nqc[k], la);
+                                ha = f2fma(f2pack(fa[k].z, fa[k].w), nqc[k], ha);
+                                lb = f2fma(f2pack(fb[k].x, fb[k].y), nqc[k], lb);
+                                hb = f2fma(f2pack(fb[k].z, fb[k].w), nqc[k], hb);
+                            }
+                            const float2 ea = f2unpack(la), eb = f2unpack(ha), ec = f2unpack(lb), ed = f2unpack(hb);
+                            const float mnf = fminf(fminf(fminf(ea.x, ea.y), fminf(eb.x, eb.y)),
+                                                    fminf(fminf(ec.x, ec.y), fminf(ed.x, ed.y)));
+                            if (mnf <= thr) {
+                                pend |= (uint64_t)(uint32_t)(g >> 1) << (16 * npend);
+                                ++npend;
+                            }
+                            if (__any_sync(0xffffffffu, npend >= 4)) drain();
+                        }
                     }
                     if (LAZY && g < ngroups) {   // tail groups (fewer than GS): one record
                         float mn = INFINITY;
@@ -978,13 +1011,14 @@ int persistent_grid(K kernel, int threads, size_t smem, int64_t items, int sm_co
 
 template <typename T, int D, int MODE>
 void run_lowd(const PassArgs &a, cudaStream_t s) {
+    // G == 3 (expanded-form filter, option simt_filter) stages only the filter rows
     const bool exp = sizeof(T) == 4 && MODE != M_FIX && a.Xf != nullptr &&
-                     (size_t)2 * a.chunk * (D * sizeof(T) + (D + 1) * 4) + 16 <= 200 * 1024;
-    const size_t smem = (size_t)2 * a.chunk * (D * sizeof(T) + (exp ? (D + 1) * 4 : 0)) + 16;
+                     (size_t)2 * a.chunk * (D + 1) * 4 + 16 <= 200 * 1024;
+    const size_t smem = (size_t)2 * a.chunk * (exp ? (D + 1) * 4 : D * sizeof(T)) + 16;
     constexpr bool SYMOK = MODE == M_SCAN || MODE == M_FIX;   // symmetric self-query variants
     auto k = exp ? window_lowd<T, D, MODE, 3>
                  : (a.variant == 1 ? window_lowd<T, D, MODE, 1> : window_lowd<T, D, MODE, 2>);
-    if (SYMOK && a.sym) k = window_lowd<T, D, MODE, 1, SYMOK>;
+    if (SYMOK && a.sym) k = exp ? window_lowd<T, D, MODE, 3, SYMOK> : window_lowd<T, D, MODE, 1, SYMOK>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int64_t work = MODE == M_FIX ? a.n_ovf : a.total_items;
     int g = persistent_grid(k, a.B, smem, work, a.sm_count);
