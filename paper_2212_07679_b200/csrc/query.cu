@@ -1222,7 +1222,13 @@ namespace {
 template <typename T, int D>
 __global__ void __launch_bounds__(256) core_count_kernel(PassArgs a, int32_t *count, unsigned long long *evaluated) {
     extern __shared__ __align__(128) uint8_t smem[];
-    const int tid = threadIdx.x;
+    // the block's still-undecided queries, packed into the lowest threads after every chunk
+    // (so warps whose queries all reached min_pts stop working, not just idle lanes)
+    __shared__ T s_q[256 * D];
+    __shared__ int32_t s_c[256];
+    __shared__ int16_t s_id[256];
+    __shared__ int32_t s_wsum[8];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const T *Xs = static_cast<const T *>(a.Xs);
     const size_t buf_bytes = (size_t)a.chunk * D * sizeof(T);
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem + 2 * buf_bytes);
@@ -1246,33 +1252,59 @@ __global__ void __launch_bounds__(256) core_count_kernel(PassArgs a, int32_t *co
     const int32_t mp = a.min_pts;
     unsigned long long ev = 0;   // candidate pairs this thread evaluated (roofline accounting)
     for (int64_t b = blockIdx.x; b < a.nblocks; b += gridDim.x) {
-        const int64_t sp = b * a.B + tid;
-        const bool active = sp < a.m;
-        T q[D];
+        const int64_t sp0 = b * a.B;
+        const int nqb = (int)min((int64_t)a.B, a.m - sp0);
+        if (tid < nqb) {
+            const int64_t sp = sp0 + tid;
+            s_id[tid] = (int16_t)tid;
+            s_c[tid] = 0;
 #pragma unroll
-        for (int k = 0; k < D; ++k) q[k] = active ? Xs[(sp >> 2) * 4 * D + k * 4 + (sp & 3)] : (T)0;
+            for (int k = 0; k < D; ++k) s_q[tid * D + k] = Xs[(sp >> 2) * 4 * D + k * 4 + (sp & 3)];
+        }
+        int n_und = nqb;
         const int64_t i0 = a.item_start[b], i1 = a.item_start[b + 1];
-        int32_t c = 0;
-        if (tid == 0 && i0 < i1) issue(i0, 0);
-        for (int64_t item = i0; item < i1; ++item) {
-            const int sidx = (int)((item - i0) & 1);
-            if (tid == 0 && item + 1 < i1) issue(item + 1, sidx ^ 1);
+        // visit the block's own chunk first, then alternate outwards: the nearest keys
+        // decide most points within the first chunks (early exit below)
+        const int64_t nit = i1 - i0;
+        const int64_t kd = nit > 0 ? min(max((sp0 - a.blk_lo[b]) / a.chunk, (int64_t)0), nit - 1) : 0;
+        const int64_t up = nit - 1 - kd, mn = min(up, kd);
+        auto order = [&](int64_t k) -> int64_t {
+            if (k <= 2 * mn) return i0 + kd + ((k & 1) ? (k + 1) / 2 : -(k / 2));
+            const int64_t r = k - 2 * mn;
+            return i0 + (up > kd ? kd + mn + r : kd - mn - r);
+        };
+        __syncthreads();
+        if (tid == 0 && nit > 0) issue(order(0), 0);
+        for (int64_t k = 0; k < nit; ++k) {
+            const int64_t item = order(k);
+            const int sidx = (int)(k & 1);
+            if (tid == 0 && k + 1 < nit) issue(order(k + 1), sidx ^ 1);
             int64_t bb, c0, c1;
             locate(a, item, bb, c0, c1);
+            const bool mine = tid < n_und;
+            T q[D];
+            int32_t c = 0;
+            int16_t id = 0;
+            if (mine) {
+                id = s_id[tid];
+                c = s_c[tid];
+#pragma unroll
+                for (int kk = 0; kk < D; ++kk) q[kk] = s_q[tid * D + kk];
+            }
             mbar_wait(&bar[sidx], phase[sidx]);
             phase[sidx] ^= 1u;
-            if (active && c < mp) {
+            if (mine) {
                 const int ngroups = (int)((c1 - c0) >> 2);
                 if constexpr (sizeof(T) == 4) {
                     const float4 *g4 = reinterpret_cast<const float4 *>(smem + sidx * buf_bytes);
                     uint64_t nq[D];
 #pragma unroll
-                    for (int k = 0; k < D; ++k) nq[k] = f2pack(-q[k], -q[k]);
+                    for (int kk = 0; kk < D; ++kk) nq[kk] = f2pack(-q[kk], -q[kk]);
                     int g = 0;
                     for (; g < ngroups && c < mp; ++g) {
                         float4 xa[D];
 #pragma unroll
-                        for (int k = 0; k < D; ++k) xa[k] = g4[g * D + k];
+                        for (int kk = 0; kk < D; ++kk) xa[kk] = g4[g * D + kk];
                         uint64_t la, ha;
                         group_d2<D>(xa, nq, la, ha);
                         const float2 pa = f2unpack(la), qa = f2unpack(ha);
@@ -1286,23 +1318,45 @@ __global__ void __launch_bounds__(256) core_count_kernel(PassArgs a, int32_t *co
                     ev += 4ull * g;
                 } else {
                     const T *gb = reinterpret_cast<const T *>(smem + sidx * buf_bytes);
-                    for (int g = 0; g < ngroups && c < mp; ++g) {
+                    int g = 0;
+                    for (; g < ngroups && c < mp; ++g) {
 #pragma unroll
                         for (int i = 0; i < 4; ++i) {
                             double s2 = 0.0;
 #pragma unroll
-                            for (int k = 0; k < D; ++k) {
-                                const double t = __dsub_rn(gb[g * 4 * D + k * 4 + i], q[k]);
+                            for (int kk = 0; kk < D; ++kk) {
+                                const double t = __dsub_rn(gb[g * 4 * D + kk * 4 + i], q[kk]);
                                 s2 = __dadd_rn(s2, __dmul_rn(t, t));
                             }
                             c += s2 <= R2;
                         }
                     }
-                    ev += 4ull * ngroups;
+                    ev += 4ull * g;
                 }
             }
-            if (!__syncthreads_or(active && c < mp)) {   // every query of the block is decided
-                if (item + 1 < i1) {                       // drain the prefetched chunk
+            // decided queries write their count; the undecided ones are packed to the front
+            const bool und = mine && c < mp;
+            if (mine && !und) count[sp0 + id] = c;
+            const unsigned bal = __ballot_sync(0xffffffffu, und);
+            if (lane == 0) s_wsum[wid] = __popc(bal);
+            __syncthreads();   // also: every thread has read its old list entry
+            int pos = __popc(bal & ((1u << lane) - 1)), total = 0;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) {
+                const int v = s_wsum[w];
+                pos += w < wid ? v : 0;
+                total += v;
+            }
+            if (und) {
+                s_id[pos] = id;
+                s_c[pos] = c;
+#pragma unroll
+                for (int kk = 0; kk < D; ++kk) s_q[pos * D + kk] = q[kk];
+            }
+            n_und = total;
+            __syncthreads();
+            if (n_und == 0) {                 // every query of the block is decided
+                if (k + 1 < nit) {            // drain the prefetched chunk
                     const int ns = sidx ^ 1;
                     mbar_wait(&bar[ns], phase[ns]);
                     phase[ns] ^= 1u;
@@ -1310,7 +1364,7 @@ __global__ void __launch_bounds__(256) core_count_kernel(PassArgs a, int32_t *co
                 break;
             }
         }
-        if (active) count[sp] = c;
+        if (tid < n_und) count[sp0 + s_id[tid]] = s_c[tid];   // never reached min_pts
         __syncthreads();
     }
     if (evaluated) {
