@@ -927,3 +927,28 @@ def test_load_rejects_broken_invariants(snn, tmp_path):
     open(p, "wb").write(blob + b"\0")
     with pytest.raises(snn.SnnError, match="trailing"):
         snn.Index.load(p)
+
+
+@pytest.mark.parametrize("d", [2, 3, 6])
+def test_row_staging_and_symmetry_options_identical(snn, d):
+    """Key-order row staging (default) vs direct final-row writes, symmetric vs two-sided
+    self-queries, expanded filter on/off: bit-identical CSR, equal to the oracle."""
+    import paper_2212_07679_b200 as p
+    rng = np.random.default_rng(1400 + d)
+    X = (rng.random((20000, d)) * 20).astype(np.float32)
+    R = {2: 0.12, 3: 0.5, 6: 2.5}[d]
+    outs = []
+    try:
+        for st, sy, sf in [(1, 1, 0), (-1, 1, 0), (1, -1, 0), (-1, -1, -1), (1, 1, -1)]:
+            p.snn_set_option("stage_rows", st)
+            p.snn_set_option("symmetric", sy)
+            p.snn_set_option("simt_filter", sf)
+            outs.append(run(snn, X, None, R))
+    finally:
+        for k in ("stage_rows", "symmetric", "simt_filter"):
+            p.snn_set_option(k, 0)
+    compare(outs[0], oracle.radius_query(X, X, R))
+    for o in outs[1:]:
+        np.testing.assert_array_equal(np.asarray(o.offsets), np.asarray(outs[0].offsets))
+        np.testing.assert_array_equal(np.asarray(o.indices), np.asarray(outs[0].indices))
+        np.testing.assert_array_equal(np.asarray(o.distances), np.asarray(outs[0].distances))
