@@ -11,8 +11,10 @@ workloads/radii.json).  Inputs are resident in HBM; L2 (126 MB) is flushed by wr
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl snn|reference] [--config c2]
 
 Multi-GPU (torchrun, one rank per GPU): every rank runs an independent replica of the
-workload (weak scaling, no data-path collective); timings are the
-max over ranks.  ``--impl reference`` times the CPU oracle (fp64 brute force) on a bounded
+workload (weak scaling, no data-path collective); with ``--shard``
+the ranks split ONE query set instead (snn_query_*_part: contiguous, work-balanced ranges of
+key-sorted query blocks on a replicated index; strong scaling).  Timings are the max over
+ranks.  ``--impl reference`` times the CPU oracle (fp64 brute force) on a bounded
 sample of the same workload, rank 0 only.
 """
 from __future__ import annotations
@@ -191,7 +193,8 @@ def config_block(w, args):
                         f"{'self-query' if w.Q is None else f'm={w.m} queries'}, R={w.R:.6g}",
             "n": w.n, "m": w.m, "d": w.d, "R": w.R, "input_dtype": str(w.X.dtype),
             "l2": "flushed (256 MB write) before every timed step",
-            "parallelism": f"replicas x{args.gpus} (weak scaling)"}
+            "parallelism": (f"query shards x{args.gpus} (snn_query_*_part, strong scaling)" if args.shard
+                            else f"replicas x{args.gpus} (weak scaling)")}
 
 
 # ----------------------------------------------------------------------------- roofline
@@ -273,6 +276,7 @@ def run_gpu(args):
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
 
     dbscan = w.dbscan_min_pts is not None
+    shard = args.shard and world > 1 and not dbscan
     labels_d = torch.empty(w.n, dtype=torch.int32, device=dev) if dbscan else None
 
     def step():
@@ -281,7 +285,11 @@ def run_gpu(args):
             k = snn.snn_dbscan(idx, R, w.dbscan_min_pts, labels_d)
             snn.snn_free(idx)
             return k
-        r = snn.snn_query_self(idx, R) if Qd is None else snn.snn_query_radius(idx, Qd, R)
+        if shard:   # this rank's work-balanced share of one query set
+            r = (snn.snn_query_self_part(idx, R, rank, world) if Qd is None
+                 else snn.snn_query_radius_part(idx, Qd, R, rank, world))
+        else:
+            r = snn.snn_query_self(idx, R) if Qd is None else snn.snn_query_radius(idx, Qd, R)
         nnz = snn.snn_result_csr(r)["nnz"]
         snn.snn_result_free(r)
         snn.snn_free(idx)
@@ -324,7 +332,7 @@ def run_gpu(args):
     if world > 1:
         torch.distributed.barrier()
     total_ms = max_over_ranks(sum(times), world, dev)
-    units = weak_units(w.m * args.steps, world)
+    units = w.m * args.steps if shard else weak_units(w.m * args.steps, world)
     value = units / (total_ms / 1e3)
 
     # ---- end to end through the C ABI with HOST buffers (copies inside the timed region)
@@ -344,7 +352,11 @@ def run_gpu(args):
         if dbscan:
             snn.snn_dbscan(idx, R, w.dbscan_min_pts, labels_h)
         else:
-            r = snn.snn_query_self(idx, R) if Qh is None else snn.snn_query_radius(idx, Qh, R)
+            if shard:
+                r = (snn.snn_query_self_part(idx, R, rank, world) if Qh is None
+                     else snn.snn_query_radius_part(idx, Qh, R, rank, world))
+            else:
+                r = snn.snn_query_self(idx, R) if Qh is None else snn.snn_query_radius(idx, Qh, R)
             snn.snn_result_copy(r, off_h, idx_h, dist_h)
             snn.snn_result_free(r)
         snn.snn_free(idx)
@@ -353,7 +365,7 @@ def run_gpu(args):
         if i >= args.warmup:
             e2e_times.append(e0.elapsed_time(e1))
     e2e_ms = max_over_ranks(sum(e2e_times), world, dev)
-    e2e_value = weak_units(w.m * args.steps, world) / (e2e_ms / 1e3)
+    e2e_value = (w.m * args.steps if shard else weak_units(w.m * args.steps, world)) / (e2e_ms / 1e3)
     h2d = w.X.nbytes + (0 if w.Q is None else w.Q.nbytes)
     d2h = w.n * 4 if dbscan else (w.m + 1) * 8 + nnz * 8
     metric = "DBSCAN points/s (index build + DBSCAN, n=2M)" if dbscan else METRIC
@@ -363,7 +375,7 @@ def run_gpu(args):
 
     line = {"metric": metric, "value": value, "unit": unit, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong" if shard else "weak", "vs_baseline": None,
             "dtype": "f64" if w.X.dtype == np.float64 else "f32", "data": "synthetic",
             "config": config_block(w, args),
             "build_ms": prof["build"]["ms"] / max(1, prof["build"]["launches"]),
@@ -396,6 +408,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--opt", action="append", default=[], help="library option key=value (A/B runs)")
+    ap.add_argument("--shard", action="store_true",
+                    help="N>1: split one query set across the ranks (strong scaling) instead of replicas")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

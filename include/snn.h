@@ -167,6 +167,22 @@ snn_status snn_query_radius(snn_index idx, const void *Q, int64_t m, int32_t d, 
  * index was built from (every point is its own neighbour), without re-projecting X. */
 snn_status snn_query_self(snn_index idx, double R, void *stream, snn_result *out);
 
+/* Query sharding across GPUs (queries are independent,
+ * batching only forms a union of windows).  Every GPU holds a replicated index (built from
+ * the same X) and calls the _part variant with its rank: the key-sorted query blocks are
+ * split into `nparts` contiguous ranges balanced by window length (the work), and part
+ * `part` computes only its blocks.  The result is a CSR over ALL m queries in which rows
+ * of other parts are empty, so the parts' results are disjoint and their union (per row)
+ * is exactly the unpartitioned result; no data-path collective is needed (results stay
+ * sharded; an all-gather of per-part nnz rebases offsets if a global CSR is wanted).
+ * Self-queries use two-sided windows here (the mirrored half of a symmetric scan would
+ * cross parts).  Errors as snn_query_radius / snn_query_self, plus INVALID_ARGUMENT
+ * unless 0 <= part < nparts. */
+snn_status snn_query_radius_part(snn_index idx, const void *Q, int64_t m, int32_t d, snn_dtype dt, double R,
+                                 int32_t part, int32_t nparts, void *stream, snn_result *out);
+snn_status snn_query_self_part(snn_index idx, double R, int32_t part, int32_t nparts, void *stream,
+                               snn_result *out);
+
 /* CSR view (device pointers, valid until snn_result_free). */
 snn_status snn_result_csr(snn_result r, snn_csr *view);
 

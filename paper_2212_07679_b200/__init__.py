@@ -29,7 +29,8 @@ STATUS = {0: "SNN_OK", 1: "SNN_ERR_INVALID_ARGUMENT", 2: "SNN_ERR_EMPTY",
           3: "SNN_ERR_NONFINITE", 4: "SNN_ERR_DIM_MISMATCH", 5: "SNN_ERR_OUT_OF_MEMORY",
           6: "SNN_ERR_CUDA", 7: "SNN_ERR_UNSUPPORTED"}
 
-EXPORTS = ["snn_build", "snn_build_metric", "snn_append", "snn_save", "snn_load", "snn_query_radius", "snn_query_self", "snn_result_csr",
+EXPORTS = ["snn_build", "snn_build_metric", "snn_append", "snn_save", "snn_load",
+           "snn_query_radius_part", "snn_query_self_part", "snn_query_radius", "snn_query_self", "snn_result_csr",
            "snn_result_copy", "snn_result_free", "snn_dbscan", "snn_free", "snn_last_error",
            "snn_index_info", "snn_launch_count", "snn_set_option", "snn_profile_enable",
            "snn_profile_read"]
@@ -81,6 +82,8 @@ def load_library(path: str = LIB_PATH):
         "snn_load": ([ctypes.c_char_p, P, ctypes.POINTER(P)], ctypes.c_int),
         "snn_query_radius": ([P, P, i64, i32, ctypes.c_int, f64, P, ctypes.POINTER(P)], ctypes.c_int),
         "snn_query_self": ([P, f64, P, ctypes.POINTER(P)], ctypes.c_int),
+        "snn_query_radius_part": ([P, P, i64, i32, ctypes.c_int, f64, i32, i32, P, ctypes.POINTER(P)], ctypes.c_int),
+        "snn_query_self_part": ([P, f64, i32, i32, P, ctypes.POINTER(P)], ctypes.c_int),
         "snn_result_csr": ([P, ctypes.POINTER(_CSR)], ctypes.c_int),
         "snn_result_copy": ([P, P, P, P, P], ctypes.c_int),
         "snn_result_free": ([P], None),
@@ -198,6 +201,24 @@ def snn_query_self(index, R: float, stream=None):
     lib = load_library()
     h = ctypes.c_void_p()
     _check(lib.snn_query_self(index, float(R), _stream_ptr(stream), ctypes.byref(h)))
+    return h
+
+
+def snn_query_radius_part(index, Q, R: float, part: int, nparts: int, stream=None):
+    """This GPU's share of a sharded query: CSR over all queries, rows
+    of other parts empty."""
+    lib = load_library()
+    p, m, d, code, _keep = _ptr_dtype(Q)
+    h = ctypes.c_void_p()
+    _check(lib.snn_query_radius_part(index, p, m, d, code, float(R), int(part), int(nparts),
+                                     _stream_ptr(stream), ctypes.byref(h)))
+    return h
+
+
+def snn_query_self_part(index, R: float, part: int, nparts: int, stream=None):
+    lib = load_library()
+    h = ctypes.c_void_p()
+    _check(lib.snn_query_self_part(index, float(R), int(part), int(nparts), _stream_ptr(stream), ctypes.byref(h)))
     return h
 
 
@@ -359,15 +380,17 @@ class Index:
     def arrays(self) -> dict:
         return index_arrays(self._h)
 
-    def query(self, Q, R: float, device: str = "cpu", stream=None) -> CSR:
-        r = snn_query_radius(self._h, Q, R, stream)
+    def query(self, Q, R: float, device: str = "cpu", stream=None, part: int = 0, nparts: int = 1) -> CSR:
+        r = (snn_query_radius(self._h, Q, R, stream) if nparts == 1
+             else snn_query_radius_part(self._h, Q, R, part, nparts, stream))
         try:
             return _fetch(r, device, stream)
         finally:
             snn_result_free(r)
 
-    def query_self(self, R: float, device: str = "cpu", stream=None) -> CSR:
-        r = snn_query_self(self._h, R, stream)
+    def query_self(self, R: float, device: str = "cpu", stream=None, part: int = 0, nparts: int = 1) -> CSR:
+        r = (snn_query_self(self._h, R, stream) if nparts == 1
+             else snn_query_self_part(self._h, R, part, nparts, stream))
         try:
             return _fetch(r, device, stream)
         finally:

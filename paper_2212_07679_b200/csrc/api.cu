@@ -195,6 +195,26 @@ static bool f16_exponent(double bound, int *e) {
     return bound * ldexp(1.0, ex) < 32768.0;
 }
 
+// Query sharding across GPUs: set for the duration of one
+// snn_query_*_part call on this thread, read by every query path after its K7 windows.
+struct PartSpec { int part = 0, nparts = 1; };
+static thread_local PartSpec t_part;
+struct PartGuard {
+    PartGuard(int p, int n) { t_part.part = p; t_part.nparts = n; }
+    ~PartGuard() { t_part = PartSpec(); }
+};
+static cudaError_t apply_part(Workspace &ws, cudaStream_t s, int64_t *blk_lo, int64_t *blk_hi, int64_t *nitems,
+                              int64_t nblocks) {
+    if (t_part.nparts <= 1 || nblocks == 0) return cudaSuccess;
+    int64_t *tmp = nullptr;
+    uint8_t *st = nullptr;
+    cudaError_t e = ws.alloc(&tmp, (size_t)(2 * nblocks + 1));
+    if (e == cudaSuccess) e = ws.alloc(&st, scan_temp_bytes(nblocks) + 4096);
+    if (e != cudaSuccess) return e;
+    launch_restrict_part(blk_lo, blk_hi, nitems, nblocks, t_part.part, t_part.nparts, tmp, st, s);
+    return cudaGetLastError();
+}
+
 static void free_index(snn_index idx) {
     if (!idx) return;
     for (void *p : idx->owned) cudaFreeAsync(p, 0);
@@ -605,6 +625,7 @@ static snn_status query_tc(snn_index idx, Workspace &ws, cudaStream_t s, int sms
     w.all = g_opt.window_all;
     w.blk_lo = blk_lo; w.blk_hi = blk_hi; w.nitems = nitems; w.pairs = wpairs;
     launch_block_windows(w, s);                                                    // K7
+    CK(apply_part(ws, s, blk_lo, blk_hi, nitems, nblocks), "query part");
     CK(ws.alloc(&scan_tmp, scan_temp_bytes(m > nblocks ? m : nblocks) + 4096), "alloc");
     CK(ws.alloc(&grp_lo, (size_t)ngroups), "alloc");
     CK(ws.alloc(&grp_items, (size_t)ngroups), "alloc");
@@ -756,6 +777,7 @@ static snn_status query_tcl(snn_index idx, Workspace &ws, cudaStream_t s, int sm
     w.all = g_opt.window_all;
     w.blk_lo = blk_lo; w.blk_hi = blk_hi; w.nitems = nitems; w.pairs = wpairs;
     launch_block_windows(w, s);                                                    // K7
+    CK(apply_part(ws, s, blk_lo, blk_hi, nitems, nblocks), "query part");
     launch_tcl_items(blk_lo, blk_hi, nblocks, (int)G, chunk, bcount, s);
     exclusive_scan_i64(bcount, bstart, nblocks, scan_tmp, s);
     int64_t *hp = static_cast<int64_t *>(t_pinned.p);
@@ -967,9 +989,10 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
     w.all = g_opt.window_all;
     w.blk_lo = blk_lo; w.blk_hi = blk_hi; w.nitems = nitems; w.pairs = pairs;
     launch_block_windows(w, s);                                                    // K7
+    CK(apply_part(ws, s, blk_lo, blk_hi, nitems, nblocks), "query part");
     // symmetric self-query: every unordered pair once -- block b scans only candidates
     // from its own first position on (j > i); mirrored hits fill the L part of row j
-    const bool sym = self && !generic && allow_sym && g_opt.symmetric && !g_opt.window_all;
+    const bool sym = self && !generic && allow_sym && g_opt.symmetric && !g_opt.window_all && t_part.nparts <= 1;
     int64_t *blk_lo_s = blk_lo;
     if (sym) {
         CK(ws.alloc(&blk_lo_s, (size_t)nblocks), "alloc");
@@ -1631,6 +1654,26 @@ snn_status snn_query_self(snn_index idx, double R, void *stream, snn_result *out
     if (!idx) return fail(SNN_ERR_INVALID_ARGUMENT, "NULL index");
     if (idx->metric != SNN_METRIC_EUCLIDEAN) return metric_query(idx, nullptr, idx->n, idx->d, idx->dt, R, stream, out);
     return query_impl(idx, nullptr, idx->n, idx->d, idx->dt, R, stream, out);
+}
+
+snn_status snn_query_radius_part(snn_index idx, const void *Q, int64_t m, int32_t d, snn_dtype dt, double R,
+                                 int32_t part, int32_t nparts, void *stream, snn_result *out) {
+    if (nparts < 1 || part < 0 || part >= nparts) {
+        if (out) *out = nullptr;
+        return fail(SNN_ERR_INVALID_ARGUMENT, "need 0 <= part < nparts");
+    }
+    PartGuard g(part, nparts);
+    return snn_query_radius(idx, Q, m, d, dt, R, stream, out);
+}
+
+snn_status snn_query_self_part(snn_index idx, double R, int32_t part, int32_t nparts, void *stream,
+                               snn_result *out) {
+    if (nparts < 1 || part < 0 || part >= nparts) {
+        if (out) *out = nullptr;
+        return fail(SNN_ERR_INVALID_ARGUMENT, "need 0 <= part < nparts");
+    }
+    PartGuard g(part, nparts);
+    return snn_query_self(idx, R, stream, out);
 }
 
 snn_status snn_result_csr(snn_result r, snn_csr *view) {

@@ -26,6 +26,7 @@
 
 #include "common.cuh"
 #include "query.h"
+#include "internal.h"
 
 namespace snn {
 namespace {
@@ -1041,6 +1042,41 @@ void run_generic(bool write, const PassArgs &a, cudaStream_t s) {
 }  // namespace
 
 bool lowd_supported(int d) { return d >= 1 && d <= 8; }
+
+namespace {
+// multi-GPU query sharding: work of a query block = its window length
+__global__ void part_len_kernel(const int64_t *lo, const int64_t *hi, int64_t nb, int64_t *len) {
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x)
+        len[b] = hi[b] - lo[b];
+}
+// block b belongs to the part whose share of the total work contains the block's midpoint
+// (contiguous, work-balanced ranges of key-sorted query blocks); other blocks get an empty
+// window, so every path (low d, generic, tensor core) skips them and their rows are empty
+__global__ void restrict_part_kernel(int64_t *lo, int64_t *hi, int64_t *nitems, const int64_t *pre, int64_t nb,
+                                     int part, int nparts) {
+    const double total = (double)pre[nb];
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+        int owner;
+        if (total > 0) owner = (int)(((double)pre[b] + 0.5 * (double)(hi[b] - lo[b])) / total * nparts);
+        else owner = (int)(b * nparts / nb);
+        if (owner >= nparts) owner = nparts - 1;
+        if (owner != part) {
+            hi[b] = lo[b];
+            if (nitems) nitems[b] = 0;
+        }
+    }
+}
+}  // namespace
+
+void launch_restrict_part(int64_t *blk_lo, int64_t *blk_hi, int64_t *nitems, int64_t nblocks, int part, int nparts,
+                          int64_t *tmp, void *scan_tmp, cudaStream_t s) {
+    if (nblocks == 0 || nparts <= 1) return;
+    int64_t g = ceil_div(nblocks, 256);
+    if (g > 148 * 16) g = 148 * 16;
+    SNN_LAUNCH(part_len_kernel, (int)g, 256, 0, s, blk_lo, blk_hi, nblocks, tmp);
+    exclusive_scan_i64(tmp, tmp + nblocks, nblocks, scan_tmp, s);
+    SNN_LAUNCH(restrict_part_kernel, (int)g, 256, 0, s, blk_lo, blk_hi, nitems, tmp + nblocks, nblocks, part, nparts);
+}
 
 void launch_block_windows(const WindowSpec &w, cudaStream_t s) {
     const int64_t nb = ceil_div(w.m, w.B);

@@ -30,6 +30,11 @@ struct WindowSpec {
     unsigned long long *pairs;           // += sum over blocks of |window| x queries (zeroed)
 };
 void launch_block_windows(const WindowSpec &w, cudaStream_t s);
+// multi-GPU query sharding: keep only the query blocks of `part` (contiguous key-order
+// ranges balanced by window length); other blocks get empty windows.  tmp: 2 nblocks + 1
+// int64; scan_tmp: scan_temp_bytes(nblocks).
+void launch_restrict_part(int64_t *blk_lo, int64_t *blk_hi, int64_t *nitems, int64_t nblocks, int part, int nparts,
+                          int64_t *tmp, void *scan_tmp, cudaStream_t s);
 
 // K8: windowed exact radius test over the work list.
 struct PassArgs {

@@ -952,3 +952,40 @@ def test_row_staging_and_symmetry_options_identical(snn, d):
         np.testing.assert_array_equal(np.asarray(o.offsets), np.asarray(outs[0].offsets))
         np.testing.assert_array_equal(np.asarray(o.indices), np.asarray(outs[0].indices))
         np.testing.assert_array_equal(np.asarray(o.distances), np.asarray(outs[0].distances))
+
+
+# --------------------------------------------------------------------------- query sharding (§8(e))
+@pytest.mark.parametrize("d,dt,self_q,nparts", [(3, np.float32, True, 3), (2, np.float64, False, 4),
+                                                (64, np.float32, False, 3), (20, np.float64, True, 2),
+                                                (3, np.float32, False, 8)])
+def test_query_parts_partition_the_result(snn, d, dt, self_q, nparts):
+    """snn_query_*_part: every row is computed by exactly one part, the parts' rows equal the
+    unpartitioned result (and the oracle), and the work split is balanced."""
+    rng = np.random.default_rng(1500 + d)
+    X = (rng.standard_normal((6000, d)) * rng.uniform(0.5, 2, d)).astype(dt)
+    Q = None if self_q else (rng.standard_normal((6000, d)) * rng.uniform(0.5, 2, d)).astype(dt)
+    R = float(np.quantile(np.linalg.norm(X[:300, None, :].astype(np.float64) - X[None, 300:400, :], axis=-1), 0.02))
+    idx = snn.Index(_dev(X))
+    try:
+        full = idx.query_self(R) if self_q else idx.query(_dev(Q), R)
+        parts = [idx.query_self(R, part=p, nparts=nparts) if self_q else idx.query(_dev(Q), R, part=p, nparts=nparts)
+                 for p in range(nparts)]
+        with pytest.raises(snn.SnnError, match="INVALID_ARGUMENT"):
+            idx.query_self(R, part=nparts, nparts=nparts)
+    finally:
+        idx.free()
+    m = len(np.asarray(full.offsets)) - 1
+    lens = np.stack([np.diff(np.asarray(p.offsets)) for p in parts])
+    full_len = np.diff(np.asarray(full.offsets))
+    assert ((lens > 0).sum(axis=0) <= 1).all(), "a row computed by two parts"
+    np.testing.assert_array_equal(lens.sum(axis=0), full_len)
+    for p in parts:
+        off = np.asarray(p.offsets)
+        for r in np.nonzero(np.diff(off))[0]:
+            np.testing.assert_array_equal(np.asarray(p.indices)[off[r]:off[r + 1]],
+                                          np.asarray(full.indices)[full.offsets[r]:full.offsets[r + 1]])
+            np.testing.assert_array_equal(np.asarray(p.distances)[off[r]:off[r + 1]],
+                                          np.asarray(full.distances)[full.offsets[r]:full.offsets[r + 1]])
+    totals = lens.sum(axis=1)
+    assert totals.min() > 0 and totals.max() < 3 * totals.mean()
+    compare(full, oracle.radius_query(X, X if self_q else Q, R))
