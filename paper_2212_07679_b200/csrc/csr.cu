@@ -96,10 +96,24 @@ __global__ void __launch_bounds__(256) rows_sort_warp_kernel(const int64_t *offs
 __global__ void __launch_bounds__(1024) rows_sort_block_kernel(const int64_t *offsets, int64_t m, const uint64_t *tmp,
                                                                const int32_t *perm, int32_t *out_idx, float *out_dist) {
     extern __shared__ uint64_t bbuf[];
-    for (int64_t r = blockIdx.x; r < m; r += gridDim.x) {
+    __shared__ int64_t s_rows[1024];
+    __shared__ int s_nrows;
+    // this CTA's rows are blockIdx.x + k * gridDim.x; find the long ones 1024 at a time (one
+    // parallel round of offset loads instead of one dependent round trip per row)
+    for (int64_t k0 = 0; blockIdx.x + k0 * gridDim.x < m; k0 += blockDim.x) {
+        if (threadIdx.x == 0) s_nrows = 0;
+        __syncthreads();
+        const int64_t rr = blockIdx.x + (k0 + threadIdx.x) * gridDim.x;
+        if (rr < m) {
+            const int64_t c = offsets[rr + 1] - offsets[rr];
+            if (c > WCAP && c <= BCAP) s_rows[atomicAdd(&s_nrows, 1)] = rr;
+        }
+        __syncthreads();
+        const int nr = s_nrows;
+    for (int t = 0; t < nr; ++t) {
+        const int64_t r = s_rows[t];
         const int64_t o0 = offsets[r];
         const int cnt = (int)(offsets[r + 1] - o0);
-        if (cnt <= WCAP || cnt > BCAP) continue;   // uniform over the CTA
         int S = 1024;
         while (S < cnt) S <<= 1;
         for (int i = threadIdx.x; i < S; i += blockDim.x) bbuf[i] = i < cnt ? tmp[o0 + i] : ~0ull;
@@ -119,6 +133,7 @@ __global__ void __launch_bounds__(1024) rows_sort_block_kernel(const int64_t *of
         }
         for (int i = threadIdx.x; i < cnt; i += blockDim.x) emit(bbuf[i], perm, out_idx, out_dist, o0 + i);
         __syncthreads();
+    }
     }
 }
 
