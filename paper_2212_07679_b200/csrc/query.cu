@@ -678,8 +678,9 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
                             const float2 pa = f2unpack(la), qa = f2unpack(ha);
                             mn = fminf(mn, fminf(fminf(pa.x, pa.y), fminf(qa.x, qa.y)));
                         }
-                        if (mn <= t_out) {
-                            if (npend == 4) drain();
+                        const bool flag = mn <= t_out;
+                        if (__any_sync(0xffffffffu, flag && npend == 4)) drain();   // drains run converged
+                        if (flag) {
                             pend |= (uint64_t)(uint32_t)(g / GS) << (16 * npend);
                             ++npend;
                         }
