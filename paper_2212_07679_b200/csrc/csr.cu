@@ -64,10 +64,36 @@ __global__ void __launch_bounds__(256) rows_sort_warp_kernel(const int64_t *offs
         if (cnt == 0 || cnt > WCAP) continue;
         if (cnt <= 32) {   // rank sort in registers: positions are unique within a row
             const uint64_t v = lane < cnt ? tmp[o0 + lane] : ~0ull;
-            const uint32_t key = (uint32_t)(v >> 32);
+            const uint32_t key = (uint32_t)(v >> 32);   // lanes >= cnt: ~0, never "<"
             int rank = 0;
-            for (int j = 0; j < cnt; ++j) rank += __shfl_sync(0xffffffffu, key, j) < key;
+            for (int j = 0; j < cnt; j += 4) {
+                rank += __shfl_sync(0xffffffffu, key, j) < key;
+                rank += __shfl_sync(0xffffffffu, key, j + 1) < key;
+                rank += __shfl_sync(0xffffffffu, key, j + 2) < key;
+                rank += __shfl_sync(0xffffffffu, key, j + 3) < key;
+            }
             if (lane < cnt) emit(v, perm, out_idx, out_dist, o0 + rank);
+            continue;
+        }
+        if (cnt <= 64) {   // two entries per lane
+            const uint64_t v0 = tmp[o0 + lane];
+            const uint64_t v1 = lane + 32 < cnt ? tmp[o0 + lane + 32] : ~0ull;
+            const uint32_t k0 = (uint32_t)(v0 >> 32), k1 = (uint32_t)(v1 >> 32);
+            int r0 = 0, r1 = 0;
+#pragma unroll 4
+            for (int j = 0; j < 32; ++j) {
+                const uint32_t kj = __shfl_sync(0xffffffffu, k0, j);
+                r0 += kj < k0;
+                r1 += kj < k1;
+            }
+            for (int j = 0; j < cnt - 32; j += 2) {
+                const uint32_t kj = __shfl_sync(0xffffffffu, k1, j);
+                const uint32_t kk = __shfl_sync(0xffffffffu, k1, j + 1);
+                r0 += (kj < k0) + (kk < k0);
+                r1 += (kj < k1) + (kk < k1);
+            }
+            emit(v0, perm, out_idx, out_dist, o0 + r0);
+            if (lane + 32 < cnt) emit(v1, perm, out_idx, out_dist, o0 + r1);
             continue;
         }
         int S = 64;

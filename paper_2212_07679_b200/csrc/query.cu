@@ -1020,10 +1020,36 @@ __global__ void __launch_bounds__(256) rows_finalize_warp(PassArgs a) {
         if (cnt == 0 || cnt > kLWarp) continue;
         if (cnt <= 32) {   // rank sort: positions are unique within a row
             const unsigned long long v = lane < cnt ? a.tmpL[src + lane] : ~0ull;
-            const uint32_t key = (uint32_t)(v >> 32);
+            const uint32_t key = (uint32_t)(v >> 32);   // lanes >= cnt: ~0, never "<"
             int rank = 0;
-            for (int j = 0; j < cnt; ++j) rank += __shfl_sync(0xffffffffu, key, j) < key;
+            for (int j = 0; j < cnt; j += 4) {
+                rank += __shfl_sync(0xffffffffu, key, j) < key;
+                rank += __shfl_sync(0xffffffffu, key, j + 1) < key;
+                rank += __shfl_sync(0xffffffffu, key, j + 2) < key;
+                rank += __shfl_sync(0xffffffffu, key, j + 3) < key;
+            }
             if (lane < cnt) lemit(a, v, dst + rank);
+            continue;
+        }
+        if (cnt <= 64) {   // two entries per lane, rank sort in registers
+            const unsigned long long v0 = a.tmpL[src + lane];
+            const unsigned long long v1 = lane + 32 < cnt ? a.tmpL[src + lane + 32] : ~0ull;
+            const uint32_t k0 = (uint32_t)(v0 >> 32), k1 = (uint32_t)(v1 >> 32);
+            int r0 = 0, r1 = 0;
+#pragma unroll 4
+            for (int j = 0; j < 32; ++j) {
+                const uint32_t kj = __shfl_sync(0xffffffffu, k0, j);
+                r0 += kj < k0;
+                r1 += kj < k1;
+            }
+            for (int j = 0; j < cnt - 32; j += 2) {
+                const uint32_t kj = __shfl_sync(0xffffffffu, k1, j);
+                const uint32_t kk = __shfl_sync(0xffffffffu, k1, j + 1);
+                r0 += (kj < k0) + (kk < k0);
+                r1 += (kj < k1) + (kk < k1);
+            }
+            lemit(a, v0, dst + r0);
+            if (lane + 32 < cnt) lemit(a, v1, dst + r1);
             continue;
         }
         int S = 64;
