@@ -102,13 +102,11 @@ __global__ void __launch_bounds__(256) rows_sort_warp_kernel(const int64_t *offs
         __syncwarp();
         for (int k = 2; k <= S; k <<= 1) {
             for (int j = k >> 1; j > 0; j >>= 1) {
-                for (int i = lane; i < S; i += 32) {
-                    const int p = i ^ j;
-                    if (p > i) {
-                        const uint64_t a = buf[i], b = buf[p];
-                        const bool up = (i & k) == 0;
-                        if ((a > b) == up) { buf[i] = b; buf[p] = a; }
-                    }
+                for (int t = lane; t < S / 2; t += 32) {   // one compare-exchange pair per thread
+                    const int i = 2 * t - (t & (j - 1)), p = i + j;
+                    const uint64_t a = buf[i], b = buf[p];
+                    const bool up = (i & k) == 0;
+                    if ((a > b) == up) { buf[i] = b; buf[p] = a; }
                 }
                 __syncwarp();
             }
@@ -146,13 +144,11 @@ __global__ void __launch_bounds__(1024) rows_sort_block_kernel(const int64_t *of
         __syncthreads();
         for (int k = 2; k <= S; k <<= 1) {
             for (int j = k >> 1; j > 0; j >>= 1) {
-                for (int i = threadIdx.x; i < S; i += blockDim.x) {
-                    const int p = i ^ j;
-                    if (p > i) {
-                        const uint64_t a = bbuf[i], b = bbuf[p];
-                        const bool up = (i & k) == 0;
-                        if ((a > b) == up) { bbuf[i] = b; bbuf[p] = a; }
-                    }
+                for (int t = threadIdx.x; t < S / 2; t += blockDim.x) {   // one compare-exchange pair per thread
+                    const int i = 2 * t - (t & (j - 1)), p = i + j;
+                    const uint64_t a = bbuf[i], b = bbuf[p];
+                    const bool up = (i & k) == 0;
+                    if ((a > b) == up) { bbuf[i] = b; bbuf[p] = a; }
                 }
                 __syncthreads();
             }

@@ -1058,12 +1058,10 @@ __global__ void __launch_bounds__(256) rows_finalize_warp(PassArgs a) {
         __syncwarp();
         for (int k = 2; k <= S; k <<= 1) {
             for (int j = k >> 1; j > 0; j >>= 1) {
-                for (int i = lane; i < S; i += 32) {
-                    const int p = i ^ j;
-                    if (p > i) {
-                        const unsigned long long x = buf[i], y = buf[p];
-                        if ((x > y) == ((i & k) == 0)) { buf[i] = y; buf[p] = x; }
-                    }
+                for (int t = lane; t < S / 2; t += 32) {   // one compare-exchange pair per thread
+                    const int i = 2 * t - (t & (j - 1)), p = i + j;
+                    const unsigned long long x = buf[i], y = buf[p];
+                    if ((x > y) == ((i & k) == 0)) { buf[i] = y; buf[p] = x; }
                 }
                 __syncwarp();
             }
@@ -1085,12 +1083,10 @@ __global__ void __launch_bounds__(1024) rows_lsort_block(PassArgs a) {
         __syncthreads();
         for (int k = 2; k <= S; k <<= 1) {
             for (int j = k >> 1; j > 0; j >>= 1) {
-                for (int i = threadIdx.x; i < S; i += blockDim.x) {
-                    const int p = i ^ j;
-                    if (p > i) {
-                        const unsigned long long x = lbuf[i], y = lbuf[p];
-                        if ((x > y) == ((i & k) == 0)) { lbuf[i] = y; lbuf[p] = x; }
-                    }
+                for (int t = threadIdx.x; t < S / 2; t += blockDim.x) {   // one compare-exchange pair per thread
+                    const int i = 2 * t - (t & (j - 1)), p = i + j;
+                    const unsigned long long x = lbuf[i], y = lbuf[p];
+                    if ((x > y) == ((i & k) == 0)) { lbuf[i] = y; lbuf[p] = x; }
                 }
                 __syncthreads();
             }
