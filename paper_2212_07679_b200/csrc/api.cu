@@ -1038,6 +1038,12 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
     a.Xs = idx->Xs; a.Qs = Qs; a.ld = ld; a.d = D; a.f64 = f64; a.m = m;
     a.perm = idx->perm; a.qperm = qperm;
     a.blk_lo = blk_lo_s; a.blk_hi = blk_hi; a.item_start = item_start;
+    if (total_items > 0 && total_items < (int64_t(1) << 31)) {
+        int32_t *ib = nullptr;
+        CK(ws.alloc(&ib, (size_t)total_items), "alloc item blocks");
+        launch_item_blocks(item_start, nblocks, ib, s);
+        a.item_block = ib;
+    }
     a.nblocks = nblocks; a.total_items = total_items;
     a.B = B; a.chunk = chunk;
     a.R2 = R * R;

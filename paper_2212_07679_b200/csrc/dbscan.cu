@@ -226,6 +226,12 @@ snn_status dbscan_impl(snn_index idx, double eps, int32_t min_pts, int32_t *labe
     a.perm = idx->perm; a.qperm = idx->perm;
     a.blk_lo = blk_lo; a.blk_hi = blk_hi; a.item_start = item_start;
     a.nblocks = nblocks; a.total_items = total_items;
+    if (total_items > 0 && total_items < (int64_t(1) << 31)) {   // item -> block table (locate)
+        int32_t *ib = nullptr;
+        CKD(ws.alloc(&ib, (size_t)total_items), "alloc");
+        launch_item_blocks(item_start, nblocks, ib, s);
+        a.item_block = ib;
+    }
     a.B = B; a.chunk = chunk;
     a.R2 = eps * eps;
     {   // same rigorous fp32 thresholds as the radius query (api.cu)
@@ -276,6 +282,13 @@ snn_status dbscan_impl(snn_index idx, double eps, int32_t min_pts, int32_t *labe
         prof_end(ctok, s, (double)*reinterpret_cast<unsigned long long *>(hbuf + 2));   // pairs evaluated
         PassArgs au = a;
         au.blk_lo = lo2; au.item_start = st2; au.total_items = hbuf[0];
+        au.item_block = nullptr;
+        if (au.total_items > 0 && au.total_items < (int64_t(1) << 31)) {
+            int32_t *ib2 = nullptr;
+            CKD(ws.alloc(&ib2, (size_t)au.total_items), "alloc");
+            launch_item_blocks(st2, nblocks, ib2, s);
+            au.item_block = ib2;
+        }
         const int utok = prof_begin(F_UNION, s);
         launch_lowd_mode(3, au, s);                                          // unions
         prof_end(utok, s, (double)*reinterpret_cast<unsigned long long *>(hbuf + 3));
@@ -322,6 +335,7 @@ snn_status dbscan_impl(snn_index idx, double eps, int32_t min_pts, int32_t *labe
             ab.Qs = qb; ab.m = nb; ab.qperm = list;
             ab.blk_lo = lo3; ab.blk_hi = hi3; ab.item_start = st3;
             ab.nblocks = nb3; ab.total_items = hbuf[0];
+            ab.item_block = nullptr;   // its own work list: binary-search locate
             ab.cnt = nullptr; ab.pre = nullptr;
             launch_lowd_mode(4, ab, s);                                      // border points
         }

@@ -92,12 +92,16 @@ __global__ void block_windows(WindowSpec w) {
 // ---------------------------------------------------------------------------- common
 __device__ __forceinline__ void locate(const PassArgs &a, int64_t item, int64_t &b, int64_t &c0,
                                        int64_t &c1) {
-    int64_t lo = 0, hi = a.nblocks;   // largest b with item_start[b] <= item
-    while (hi - lo > 1) {
-        int64_t mid = (lo + hi) >> 1;
-        if (a.item_start[mid] <= item) lo = mid; else hi = mid;
+    if (a.item_block) {   // one load instead of a dependent binary search
+        b = a.item_block[item];
+    } else {
+        int64_t lo = 0, hi = a.nblocks;   // largest b with item_start[b] <= item
+        while (hi - lo > 1) {
+            int64_t mid = (lo + hi) >> 1;
+            if (a.item_start[mid] <= item) lo = mid; else hi = mid;
+        }
+        b = lo;
     }
-    b = lo;
     c0 = a.blk_lo[b] + (item - a.item_start[b]) * a.chunk;
     c1 = min(c0 + a.chunk, a.blk_hi[b]);
 }
@@ -1172,6 +1176,20 @@ void launch_restrict_part(int64_t *blk_lo, int64_t *blk_hi, int64_t *nitems, int
     SNN_LAUNCH(part_len_kernel, (int)g, 256, 0, s, blk_lo, blk_hi, nblocks, tmp);
     exclusive_scan_i64(tmp, tmp + nblocks, nblocks, scan_tmp, s);
     SNN_LAUNCH(restrict_part_kernel, (int)g, 256, 0, s, blk_lo, blk_hi, nitems, tmp + nblocks, nblocks, part, nparts);
+}
+
+namespace {
+__global__ void item_blocks_kernel(const int64_t *item_start, int64_t nblocks, int32_t *item_block) {
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nblocks; b += (int64_t)gridDim.x * blockDim.x)
+        for (int64_t it = item_start[b]; it < item_start[b + 1]; ++it) item_block[it] = (int32_t)b;
+}
+}  // namespace
+
+void launch_item_blocks(const int64_t *item_start, int64_t nblocks, int32_t *item_block, cudaStream_t s) {
+    if (nblocks == 0) return;
+    int64_t g = ceil_div(nblocks, 256);
+    if (g > 148 * 16) g = 148 * 16;
+    SNN_LAUNCH(item_blocks_kernel, (int)g, 256, 0, s, item_start, nblocks, item_block);
 }
 
 void launch_block_windows(const WindowSpec &w, cudaStream_t s) {

@@ -30,6 +30,9 @@ struct WindowSpec {
     unsigned long long *pairs;           // += sum over blocks of |window| x queries (zeroed)
 };
 void launch_block_windows(const WindowSpec &w, cudaStream_t s);
+// item_block[item] = the query block of every work item (item_start: exclusive scan of the
+// per-block item counts, nblocks + 1 entries)
+void launch_item_blocks(const int64_t *item_start, int64_t nblocks, int32_t *item_block, cudaStream_t s);
 // multi-GPU query sharding: keep only the query blocks of `part` (contiguous key-order
 // ranges balanced by window length); other blocks get empty windows.  tmp: 2 nblocks + 1
 // int64; scan_tmp: scan_temp_bytes(nblocks).
@@ -47,6 +50,7 @@ struct PassArgs {
     const int32_t *perm;    // sorted index position -> original id
     const int32_t *qperm;   // sorted query position -> original query id
     const int64_t *blk_lo, *blk_hi, *item_start;
+    const int32_t *item_block = nullptr;   // work item -> query block (else binary search)
     int64_t nblocks, total_items;
     int B, chunk;
     float T_in, T_out;      // fp32 sure-in / sure-out thresholds on the fp32 d^2
