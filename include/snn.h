@@ -84,6 +84,14 @@ typedef struct {
     const float *distances;    /* nnz Euclidean distances, = (float)sqrt(s_fp64)  */
 } snn_csr;
 
+/* Spectrum diagnostic (eq:svd; sigma_2 enters the analysis of the
+ * window, eq:sigma2): sigma[0..k) = the k largest singular values of the centred data the
+ * index was BUILT from (appended rows are not included), by power iteration with
+ * deflation on the kept Gram matrix (fp64, one CTA on the device; k <= min(d, 16); MIPS
+ * indexes: of the d + 1 transformed rows).  sigma: host array of k doubles.  Diagnostic
+ * only -- the search uses v1 from the build.  Synchronizes the stream. */
+snn_status snn_index_sigma(snn_index idx, int32_t k, double *sigma, void *stream);
+
 /* Diagnostics of a built index (Algorithm 1 outputs). */
 typedef struct {
     int64_t n;
@@ -132,7 +140,7 @@ snn_status snn_build(const void *X, int64_t n, int32_t d, snn_dtype dt, void *st
  * Synchronizes the stream. */
 snn_status snn_append(snn_index idx, const void *Y, int64_t k, int32_t d, snn_dtype dt, void *stream);
 
-/* Save / load the built index (all device arrays; no rebuild on load).  File: "SNNG",
+/* Save / load the built index (all device arrays incl. the kept Gram; no rebuild on load).  File: "SNNG",
  * u32 version 1, 23 int64 header words, then the arrays in a fixed order, little endian.
  * snn_load validates the magic ("bad magic"), version ("unsupported version"), header
  * ("invalid header"), length ("truncated" / "trailing bytes") and the index invariants

@@ -30,7 +30,7 @@ STATUS = {0: "SNN_OK", 1: "SNN_ERR_INVALID_ARGUMENT", 2: "SNN_ERR_EMPTY",
           6: "SNN_ERR_CUDA", 7: "SNN_ERR_UNSUPPORTED"}
 
 EXPORTS = ["snn_build", "snn_build_metric", "snn_append", "snn_save", "snn_load",
-           "snn_query_radius_part", "snn_query_self_part", "snn_query_radius", "snn_query_self", "snn_result_csr",
+           "snn_query_radius_part", "snn_query_self_part", "snn_index_sigma", "snn_query_radius", "snn_query_self", "snn_result_csr",
            "snn_result_copy", "snn_result_free", "snn_dbscan", "snn_free", "snn_last_error",
            "snn_index_info", "snn_launch_count", "snn_set_option", "snn_profile_enable",
            "snn_profile_read"]
@@ -91,6 +91,7 @@ def load_library(path: str = LIB_PATH):
         "snn_free": ([P], None),
         "snn_last_error": ([], ctypes.c_char_p),
         "snn_index_info": ([P, ctypes.POINTER(_Info)], ctypes.c_int),
+        "snn_index_sigma": ([P, i32, P, P], ctypes.c_int),
         "snn_launch_count": ([], ctypes.c_uint64),
         "snn_set_option": ([ctypes.c_char_p, i64], ctypes.c_int),
         "snn_profile_enable": ([ctypes.c_int], ctypes.c_int),
@@ -267,6 +268,13 @@ def snn_load(path: str, stream=None):
     return h
 
 
+def snn_index_sigma(index, k: int = 2, stream=None) -> np.ndarray:
+    """The k largest singular values of the centred build data (eq:svd)."""
+    out = np.zeros(int(k), dtype=np.float64)
+    _check(load_library().snn_index_sigma(index, int(k), ctypes.c_void_p(out.ctypes.data), _stream_ptr(stream)))
+    return out
+
+
 def snn_index_info(index) -> dict:
     v = _Info()
     _check(load_library().snn_index_info(index, ctypes.byref(v)))
@@ -376,6 +384,9 @@ class Index:
 
     def info(self) -> dict:
         return snn_index_info(self._h)
+
+    def sigma(self, k: int = 2) -> np.ndarray:
+        return snn_index_sigma(self._h, k)
 
     def arrays(self) -> dict:
         return index_arrays(self._h)

@@ -408,7 +408,8 @@ static snn_status build_impl(const void *X, int64_t n, int32_t d, snn_dtype dt, 
     CKI(ws.alloc(&sums, (size_t)d), "alloc");
     CKI(ws.alloc(&maxabs, (size_t)d), "alloc");
     CKI(ws.alloc(&flag, 1), "alloc");
-    CKI(ws.alloc(&G, (size_t)d * d), "alloc Gram");
+    CKI(own(&G, (size_t)d * d), "alloc Gram");   // kept: snn_index_sigma
+    idx->G = G;
     CKI(ws.alloc(&keys_raw, (size_t)n), "alloc");
     CKI(ws.alloc(&sort_tmp, radix_sort_temp_bytes(n)), "alloc sort");
     CKI(cudaMemsetAsync(sums, 0, d * 8, s), "memset");
@@ -1516,6 +1517,7 @@ std::vector<Section> sections(snn_index idx, bool has_xf, bool has_xo) {
         {(void **)&idx->mu_d, (size_t)D * 8}, {(void **)&idx->mu_f, (size_t)D * 4},
         {(void **)&idx->v_d, (size_t)D * 8},  {(void **)&idx->v_f, (size_t)D * 4},
         {(void **)&idx->stats, (size_t)(ST_COUNT + 2) * 8},
+        {(void **)&idx->G, (size_t)D * D * 8},
         {(void **)&idx->keys, (size_t)n * 4}, {(void **)&idx->perm, (size_t)n * 4},
         {(void **)&idx->xbar, (size_t)(np + 256) * 4},
         {(void **)&idx->Xs, (size_t)np * row_elems(D, idx->ld) * es}};
@@ -1597,10 +1599,14 @@ snn_status snn_load(const char *path, void *stream, snn_index *out) {
     if (file.size() > total) return fail(SNN_ERR_INVALID_ARGUMENT, "trailing bytes");
     // invariants: keys (section 5) non-decreasing and finite, perm (section 6) a permutation
     {
-        size_t off = head;
-        for (int i = 0; i < 5; ++i) off += secs[i].bytes;
-        const float *keys = reinterpret_cast<const float *>(file.data() + off);
-        const int32_t *perm = reinterpret_cast<const int32_t *>(file.data() + off + secs[5].bytes);
+        size_t off = head, off_keys = 0, off_perm = 0;
+        for (const Section &sec : secs) {   // locate the keys and perm sections
+            if (sec.dev == (void **)&tmpl.keys) off_keys = off;
+            if (sec.dev == (void **)&tmpl.perm) off_perm = off;
+            off += sec.bytes;
+        }
+        const float *keys = reinterpret_cast<const float *>(file.data() + off_keys);
+        const int32_t *perm = reinterpret_cast<const int32_t *>(file.data() + off_perm);
         std::vector<uint8_t> seen((size_t)n, 0);
         for (int64_t i = 0; i < n; ++i) {
             float kf;
@@ -1706,6 +1712,24 @@ void snn_result_free(snn_result r) {
     if (r->indices) cudaFreeAsync(r->indices, 0);
     if (r->distances) cudaFreeAsync(r->distances, 0);
     delete r;
+}
+
+snn_status snn_index_sigma(snn_index idx, int32_t k, double *sigma, void *stream) {
+    if (!idx || !sigma) return fail(SNN_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (k < 1 || k > 16 || k > idx->d) return fail(SNN_ERR_INVALID_ARGUMENT, "need 1 <= k <= min(d, 16)");
+    int sms = 0;
+    snn_status st = device_check(&sms);
+    if (st != SNN_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Workspace ws(s);
+    double *scratch = nullptr, *dsig = nullptr;
+    CK(ws.alloc(&scratch, (size_t)(k + 2) * idx->d), "alloc");
+    CK(ws.alloc(&dsig, (size_t)k), "alloc");
+    launch_spectrum(idx->G, idx->d, k, scratch, dsig, s);
+    CK(cudaGetLastError(), "spectrum");
+    CK(cudaMemcpyAsync(sigma, dsig, (size_t)k * 8, cudaMemcpyDeviceToHost, s), "D2H");
+    CK(cudaStreamSynchronize(s), "spectrum");
+    return SNN_OK;
 }
 
 snn_status snn_index_info(snn_index idx, snn_index_info_t *info) {

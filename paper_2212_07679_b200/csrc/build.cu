@@ -869,4 +869,76 @@ void launch_append_perm(const uint32_t *src, int64_t n_old, int64_t n_new, const
     SNN_LAUNCH(append_perm, grid_for(n_new), kThreads, 0, s, src, n_old, n_new, perm_old, perm_new);
 }
 
+namespace {
+__device__ double spec_block_sum(double v, double *red) {
+    v = warp_sum(v);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (threadIdx.x < 32) {
+        t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+        t = warp_sum(t);
+        if (threadIdx.x == 0) red[32] = t;
+    }
+    __syncthreads();
+    return red[32];
+}
+
+// Top-k eigenvalues of the stored Gram G = Xc^T Xc (d x d, fp64) by power iteration with
+// deflation (y = G x - sum_l lambda_l (u_l . x) u_l), one CTA; sigma_l = sqrt(lambda_l) are
+// the singular values of the centred data (eq:svd).  Diagnostic only:
+// the search uses v1 from the build.  u: k x d scratch, x/y: d each.
+__global__ void __launch_bounds__(1024) spectrum_kernel(const double *__restrict__ G, int d, int k, int max_iters,
+                                                        double *u, double *x, double *y, double *sigma) {
+    __shared__ double red[33];
+    __shared__ double s_lam[16];
+    for (int l = 0; l < k; ++l) {
+        // start vector: deterministic, not orthogonal to any eigenvector in general
+        for (int c = threadIdx.x; c < d; c += blockDim.x) x[c] = 1.0 + 0.37 * (double)((c * 7919) % 13) / 13.0;
+        __syncthreads();
+        double nx = sqrt(spec_block_sum([&] { double t = 0; for (int c = threadIdx.x; c < d; c += blockDim.x) t += x[c] * x[c]; return t; }(), red));
+        for (int c = threadIdx.x; c < d; c += blockDim.x) x[c] /= nx;
+        __syncthreads();
+        double lam = 0.0, prev = -1.0;
+        for (int it = 0; it < max_iters; ++it) {
+            for (int r = threadIdx.x; r < d; r += blockDim.x) {
+                double t = 0.0;
+                for (int c = 0; c < d; ++c) t += G[(size_t)r * d + c] * x[c];
+                y[r] = t;
+            }
+            __syncthreads();
+            for (int p = 0; p < l; ++p) {   // deflate the eigenpairs found so far
+                double t = 0.0;
+                for (int c = threadIdx.x; c < d; c += blockDim.x) t += u[(size_t)p * d + c] * x[c];
+                const double dp = spec_block_sum(t, red);
+                for (int c = threadIdx.x; c < d; c += blockDim.x) y[c] -= s_lam[p] * dp * u[(size_t)p * d + c];
+                __syncthreads();
+            }
+            double t1 = 0.0, t2 = 0.0;
+            for (int c = threadIdx.x; c < d; c += blockDim.x) { t1 += x[c] * y[c]; t2 += y[c] * y[c]; }
+            lam = spec_block_sum(t1, red);          // Rayleigh quotient (x unit)
+            const double ny = sqrt(spec_block_sum(t2, red));
+            if (!(ny > 0.0)) { lam = 0.0; break; }
+            for (int c = threadIdx.x; c < d; c += blockDim.x) x[c] = y[c] / ny;
+            __syncthreads();
+            if (fabs(lam - prev) <= 1e-13 * fabs(lam)) break;
+            prev = lam;
+        }
+        for (int c = threadIdx.x; c < d; c += blockDim.x) u[(size_t)l * d + c] = x[c];
+        if (threadIdx.x == 0) {
+            s_lam[l] = lam;
+            sigma[l] = sqrt(fmax(lam, 0.0));
+        }
+        __syncthreads();
+    }
+}
+}  // namespace
+
+void launch_spectrum(const double *G, int d, int k, double *scratch, double *sigma, cudaStream_t s) {
+    SNN_LAUNCH(spectrum_kernel, 1, 1024, 0, s, G, d, k, 2000, scratch, scratch + (size_t)k * d,
+               scratch + (size_t)k * d + d, sigma);
+}
+
 }  // namespace snn

@@ -58,6 +58,7 @@ struct snn_index_s {
     double *v_d = nullptr;
     float *v_f = nullptr;
     double *stats = nullptr;   // ST_COUNT doubles
+    double *G = nullptr;       // d x d Gram of the centred build data (spectrum diagnostics)
     double h_stats[snn::ST_COUNT] = {};
     int sm_count = 148;
     int tc = 0;                // tensor-core (tcgen05) query path enabled

@@ -56,6 +56,9 @@ void launch_gather(const void *X, bool f64, int64_t n, int d, int ld, int64_t n_
 void launch_unpack_rows(const void *Xs, bool f64, int64_t n, int d, int ld, void *out, cudaStream_t s);
 void launch_append_perm(const uint32_t *src, int64_t n_old, int64_t n_new, const int32_t *perm_old, int32_t *perm_new,
                         cudaStream_t s);
+// sigma[0..k) = top-k singular values of the centred data from the Gram G (power
+// iteration with deflation, one CTA; k <= 16).  scratch: (k + 2) d doubles.
+void launch_spectrum(const double *G, int d, int k, double *scratch, double *sigma, cudaStream_t s);
 void launch_key_bounds(int d, const uint32_t *maxabs_bits, const double *mu_d, const float *mu_f, double *v_d,
                        float *v_f, double *stats, cudaStream_t s);
 

@@ -912,7 +912,7 @@ def test_load_rejects_broken_invariants(snn, tmp_path):
         a.free()
     blob = bytearray(open(p, "rb").read())
     head = 8 + 8 * 23
-    off_keys = head + 3 * 8 + 3 * 4 + 3 * 8 + 3 * 4 + 10 * 8     # mu_d mu_f v_d v_f stats
+    off_keys = head + 3 * 8 + 3 * 4 + 3 * 8 + 3 * 4 + 10 * 8 + 3 * 3 * 8   # mu_d mu_f v_d v_f stats G
     off_perm = off_keys + 100 * 4
     bad = bytearray(blob)
     bad[off_perm:off_perm + 4] = bad[off_perm + 4:off_perm + 8]   # duplicate id
@@ -989,3 +989,33 @@ def test_query_parts_partition_the_result(snn, d, dt, self_q, nparts):
     totals = lens.sum(axis=1)
     assert totals.min() > 0 and totals.max() < 3 * totals.mean()
     compare(full, oracle.radius_query(X, X if self_q else Q, R))
+
+
+# --------------------------------------------------------------------------- spectrum diagnostic (a2)
+@pytest.mark.parametrize("d,dt,s_ratio", [(3, np.float32, 0.1), (3, np.float64, 0.5), (20, np.float32, 0.5),
+                                          (64, np.float32, None), (200, np.float32, None)])
+def test_index_sigma_vs_oracle_svd(snn, d, dt, s_ratio):
+    """snn_index_sigma (power iteration with deflation on the kept Gram) vs the oracle's
+    SVD singular values of the centred data (eq:svd); the elongated Gaussian of PAPER.md:324
+    gives sigma2/sigma1 -> s.  d = 200 exercises the tensor-core Gram."""
+    rng = np.random.default_rng(1600 + d)
+    n = 40000
+    if s_ratio is not None:
+        X = rng.standard_normal((n, d)) * np.array([1.0] + [s_ratio] * (d - 1))
+    else:
+        X = rng.standard_normal((n, d)) / np.sqrt(np.arange(1, d + 1))
+    X = X.astype(dt)
+    k = 4 if d > 3 else 2
+    idx = snn.Index(_dev(X))
+    try:
+        sig = idx.sigma(k)
+    finally:
+        idx.free()
+    P = X.astype(np.float64)
+    _, S = oracle.principal_direction(oracle.center(P, oracle.column_mean(P)))
+    tol = 2e-3 if d >= 128 else 1e-5   # FP16 hi/lo tensor-core Gram vs the fp64 SIMT Gram
+    np.testing.assert_allclose(sig[:2], S[:2], rtol=tol)
+    if s_ratio is not None:
+        assert abs(sig[1] / sig[0] - s_ratio) < 0.05
+    if d > 3:   # well separated spectrum (1/sqrt(i) scales): the deflated values match too
+        np.testing.assert_allclose(sig, S[:k], rtol=max(tol, 1e-4))
