@@ -140,6 +140,16 @@ def workload(name: str):
 
 
 # ----------------------------------------------------------------------------- oracle
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def oracle_sample_rate(w, target_s: float):
     """Oracle (fp64 brute force, host cores) on a bounded sample of the workload's
     queries: returns (queries/s, sample size, seconds, threads)."""
@@ -182,7 +192,7 @@ def run_reference(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_block(w, args),
             "cpu_baseline": {"value": value, "unit": "queries/s", "cores": threads,
-                             "kind": "oracle", "sample": sample},
+                             "kind": "oracle", "sample": sample, "cpu": cpu_model()},
             "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -247,8 +257,17 @@ def roofline_block(args, w, prof, times, dev, info):
         peak_src = f"FP32 FMA issue peak at {sm_max:.0f} MHz x {n_sm} SMs (sm_max_mhz, {src})"
         work = f"{flop_per_pair} flop per evaluated candidate pair (eq:ip1)"
     achieved = (flop_per_pair * kunits / klaunch) / (kms / klaunch * 1e-3) / 1e12 if klaunch else 0.0
+    # the secondary (non-binding) roofline SURVEY.md §8(d) asks for: the same kernel's ncu DRAM
+    # bytes per launch over its measured duration, against the measured copy bandwidth
+    hbm = None
+    if traffic and klaunch:
+        gbps = traffic / (kms / klaunch * 1e-3) / 1e9
+        hbm_peak = float(peaks.get("hbm_gbs", 0.0) or 0.0)
+        hbm = {"achieved_gbps": gbps, "peak_gbps": hbm_peak or None,
+               "frac": gbps / hbm_peak if hbm_peak else None,
+               "note": "ncu dram bytes per launch (cold, serialised capture) / live kernel time; not binding"}
     return {"kernel": kernel, "bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-            "frac": achieved / peak if peak else None, "traffic": traffic, "peak_source": peak_src,
+            "frac": achieved / peak if peak else None, "traffic": traffic, "hbm": hbm, "peak_source": peak_src,
             "work": f"{work}; {kunits / max(klaunch, 1):.4g} pairs per launch",
             "kernel_ms_per_launch": kms / max(klaunch, 1),
             "share_of_step": kms / sum(times) if times else None}
@@ -389,7 +408,7 @@ def run_gpu(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not dbscan:
         rate, k, dt, threads = oracle_sample_rate(w, args.cpu_seconds)
         line["cpu_baseline"] = {"value": rate, "unit": "queries/s", "cores": threads,
-                                "kind": "oracle",
+                                "kind": "oracle", "cpu": cpu_model(),
                                 "sample": f"first {k} of {w.m} queries vs all {w.n} points, "
                                           f"fp64 brute force ({dt:.1f} s)"}
     if rank == 0:
