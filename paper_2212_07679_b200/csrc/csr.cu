@@ -51,6 +51,23 @@ __device__ __forceinline__ void emit(uint64_t v, const int32_t *perm, int32_t *o
     out_dist[pos] = __uint_as_float((uint32_t)v);
 }
 
+// Bitonic stages j = jtop .. 1 of merge size k on a 64-element segment held in registers
+// (a = element base + lane, b = element base + 32 + lane): no shared memory, no barrier.
+__device__ __forceinline__ void seg_stages(uint64_t &a, uint64_t &b, int base, int k, int jtop, int lane) {
+    for (int j = jtop; j > 0; j >>= 1) {
+        if (j == 32) {
+            const bool up = ((base + lane) & k) == 0;
+            if ((a > b) == up) { const uint64_t t = a; a = b; b = t; }
+        } else {
+            const uint64_t pa = __shfl_xor_sync(0xffffffffu, a, j), pb = __shfl_xor_sync(0xffffffffu, b, j);
+            const bool lower = (lane & j) == 0;
+            const bool upa = ((base + lane) & k) == 0, upb = ((base + 32 + lane) & k) == 0;
+            a = (lower == upa) ? (a < pa ? a : pa) : (a < pa ? pa : a);
+            b = (lower == upb) ? (b < pb ? b : pb) : (b < pb ? pb : b);
+        }
+    }
+}
+
 // one warp per row (rows with <= WCAP entries)
 __global__ void __launch_bounds__(256) rows_sort_warp_kernel(const int64_t *offsets, int64_t m, const uint64_t *tmp,
                                                              const int32_t *perm, int32_t *out_idx, float *out_dist) {
@@ -140,18 +157,35 @@ __global__ void __launch_bounds__(1024) rows_sort_block_kernel(const int64_t *of
         const int cnt = (int)(offsets[r + 1] - o0);
         int S = 1024;
         while (S < cnt) S <<= 1;
-        for (int i = threadIdx.x; i < S; i += blockDim.x) bbuf[i] = i < cnt ? tmp[o0 + i] : ~0ull;
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+        // merges up to 64 elements: each warp sorts its 64-element segments in registers
+        for (int sg = wid; sg < S / 64; sg += nw) {
+            const int base = sg * 64;
+            uint64_t a = base + lane < cnt ? tmp[o0 + base + lane] : ~0ull;
+            uint64_t b = base + 32 + lane < cnt ? tmp[o0 + base + 32 + lane] : ~0ull;
+            for (int k = 2; k <= 64; k <<= 1) seg_stages(a, b, base, k, k >> 1, lane);
+            bbuf[base + lane] = a;
+            bbuf[base + 32 + lane] = b;
+        }
         __syncthreads();
-        for (int k = 2; k <= S; k <<= 1) {
-            for (int j = k >> 1; j > 0; j >>= 1) {
-                for (int t = threadIdx.x; t < S / 2; t += blockDim.x) {   // one compare-exchange pair per thread
-                    const int i = 2 * t - (t & (j - 1)), p = i + j;
-                    const uint64_t a = bbuf[i], b = bbuf[p];
+        for (int k = 128; k <= S; k <<= 1) {
+            for (int j = k >> 1; j >= 64; j >>= 1) {   // cross-segment stages in shared memory
+                for (int pt = threadIdx.x; pt < S / 2; pt += blockDim.x) {   // one compare-exchange pair per thread
+                    const int i = 2 * pt - (pt & (j - 1)), p = i + j;
+                    const uint64_t x = bbuf[i], y = bbuf[p];
                     const bool up = (i & k) == 0;
-                    if ((a > b) == up) { bbuf[i] = b; bbuf[p] = a; }
+                    if ((x > y) == up) { bbuf[i] = y; bbuf[p] = x; }
                 }
                 __syncthreads();
             }
+            for (int sg = wid; sg < S / 64; sg += nw) {   // stages j <= 32 in registers
+                const int base = sg * 64;
+                uint64_t a = bbuf[base + lane], b = bbuf[base + 32 + lane];
+                seg_stages(a, b, base, k, 32, lane);
+                bbuf[base + lane] = a;
+                bbuf[base + 32 + lane] = b;
+            }
+            __syncthreads();
         }
         for (int i = threadIdx.x; i < cnt; i += blockDim.x) emit(bbuf[i], perm, out_idx, out_dist, o0 + i);
         __syncthreads();
