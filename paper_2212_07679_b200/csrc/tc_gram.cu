@@ -54,11 +54,12 @@ template <typename T>
 __global__ void __launch_bounds__(256) gram_transpose_split(const T *__restrict__ X, int64_t n, int d, int64_t ldt,
                                                             const float *__restrict__ mu_f, const int *e_ptr,
                                                             __half *__restrict__ XT_h, __half *__restrict__ XT_l) {
-    __shared__ float tile[64][65];
-    const int64_t r0 = (int64_t)blockIdx.x * 64;
+    // 128 rows x 64 columns per CTA: every output column gets a 256-byte contiguous run
+    __shared__ float tile[128][65];
+    const int64_t r0 = (int64_t)blockIdx.x * 128;
     const int c0 = blockIdx.y * 64;
     const float sc = ldexpf(1.0f, *e_ptr);
-    for (int e = threadIdx.x; e < 64 * 64; e += 256) {
+    for (int e = threadIdx.x; e < 128 * 64; e += 256) {
         const int r = e / 64, c = e % 64;
         const int64_t row = r0 + r;
         const int col = c0 + c;
@@ -70,8 +71,8 @@ __global__ void __launch_bounds__(256) gram_transpose_split(const T *__restrict_
         tile[r][c] = v;
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < 64 * 32; e += 256) {
-        const int c = e / 32, r2 = (e % 32) * 2;
+    for (int e = threadIdx.x; e < 64 * 64; e += 256) {
+        const int c = e / 64, r2 = (e % 64) * 2;
         const int col = c0 + c;
         const int64_t row = r0 + r2;
         if (col >= d || row >= ldt) continue;
@@ -220,7 +221,7 @@ bool launch_gram_tc(const void *X, bool f64, int64_t n, int d, const uint32_t *m
     CUtensorMap mh, ml;
     if (!make_map_t(&mh, XT_h, d, ldt) || !make_map_t(&ml, XT_l, d, ldt)) return false;
     SNN_LAUNCH(gram_scale_kernel, 1, 32, 0, s, d, maxabs_bits, mu_f, e_dev);
-    dim3 tg((unsigned)ceil_div(ldt, 64), (unsigned)ceil_div(d, 64));
+    dim3 tg((unsigned)ceil_div(ldt, 128), (unsigned)ceil_div(d, 64));
     if (f64) SNN_LAUNCH(gram_transpose_split<double>, tg, 256, 0, s, (const double *)X, n, d, ldt, mu_f, e_dev, XT_h, XT_l);
     else SNN_LAUNCH(gram_transpose_split<float>, tg, 256, 0, s, (const float *)X, n, d, ldt, mu_f, e_dev, XT_h, XT_l);
     const int nt = (int)ceil_div(d, GT);
