@@ -1296,9 +1296,8 @@ static snn_status filtered_query(snn_index idx, const void *Q, int64_t m, double
     void *p = nullptr;
     if ((e = cudaMallocAsync(&p, (size_t)(m + 1) * 8, s)) != cudaSuccess) return bail(e, "alloc offsets");
     r2->offsets = static_cast<int64_t *>(p);
-    cudaMemsetAsync(rowcnt + m, 0, 4, s);
     launch_csr_filter(idx->metric, f64, cand->offsets, m, cand->indices, idx->Xo, Qo, d, thr, keep, val, rowcnt, s);
-    exclusive_scan_i32_to_i64(rowcnt, r2->offsets, m + 1, temp, s);
+    exclusive_scan_i32_to_i64(rowcnt, r2->offsets, m, temp, s);   // offsets[0..m], offsets[m] = total
     int64_t tot = 0;
     if ((e = cudaMemcpyAsync(&tot, r2->offsets + m, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return bail(e, "D2H");
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return bail(e, "filter");
