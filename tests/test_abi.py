@@ -108,3 +108,12 @@ def test_snn_load_rejects_bad_files_without_touching_the_device(libpath, tmp_pat
             p.snn_load(str(f))
     with pytest.raises(p.SnnError, match="cannot open"):
         p.snn_load(str(tmp_path / "missing.snn"))
+
+
+def test_header_is_plain_c(tmp_path):
+    """include/snn.h compiles as C99 and as C++17 on its own (no torch / CUDA types in the
+    boundary)."""
+    src = tmp_path / "h.c"
+    src.write_text('#include "include/snn.h"\nint main(void) { return 0; }\n')
+    subprocess.check_call(["gcc", "-std=c99", "-Wall", "-Werror", "-fsyntax-only", "-I", ROOT, str(src)])
+    subprocess.check_call(["g++", "-std=c++17", "-Wall", "-Werror", "-fsyntax-only", "-x", "c++", "-I", ROOT, str(src)])
