@@ -39,13 +39,22 @@ __device__ __forceinline__ int32_t find_root(const int32_t *p, int32_t x) {
 }
 
 // flatten + smallest original id per root
+// (warp-aggregated: lanes whose points share a root -- neighbours in key order usually do
+// -- combine their ids first, so a big cluster's root sees one atomic per warp, not per point)
 __global__ void flatten(int32_t *parent, const uint8_t *core, const int32_t *perm, int64_t n,
                         int32_t *minid) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        if (!core[i]) continue;
-        const int32_t r = find_root(parent, (int32_t)i);
-        parent[i] = r;
-        atomicMin(&minid[r], perm[i]);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {   // warp-uniform trips
+        const int64_t i = base + threadIdx.x;
+        int32_t r = -1, v = 0x7fffffff;
+        if (i < n && core[i]) {
+            r = find_root(parent, (int32_t)i);
+            parent[i] = r;
+            v = perm[i];
+        }
+        const unsigned peers = __match_any_sync(0xffffffffu, r);
+        v = __reduce_min_sync(peers, v);
+        if (r >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1) atomicMin(&minid[r], v);
     }
 }
 
