@@ -258,6 +258,8 @@ snn_status snn_profile_read(const char *family, double *ms, uint64_t *launches, 
  *   "symmetric"      -1 = evaluate every pair twice in low-d self-queries (default: once)
  *   "stage_rows"     -1 = compaction writes final rows directly (default: key-order staging
  *                    buffer, then whole-row moves)
+ *   "balanced_compact" -1 = per-entry compaction threads (default for symmetric self-queries:
+ *                    one slot record per thread after CTA scans)
  *   "window_all"     1 = brute-force ablation: every query scans all n candidates
  *   "simt_filter"    low-d fp32 expanded-form pre-filter: default on for radius queries and
  *                    off for DBSCAN; 1 = on everywhere, -1 = off everywhere

@@ -758,6 +758,7 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
         if (MODE == M_SCAN) {
             const bool lost = active && em.lost;
             if (tid < a.B) a.cnt[e] = em.c | (lost ? (int32_t)0x80000000 : 0);
+            if (a.nrec && tid < a.B) a.nrec[e] = (uint16_t)(em.rec < a.cap ? em.rec : a.cap);
             if (__syncthreads_or(lost) && tid == 0) a.ovf_items[atomicAdd(a.ovf_count, 1)] = (int32_t)item;
         } else {
             if (MODE == M_COUNT) a.cnt[e] = em.c;
@@ -812,6 +813,92 @@ __global__ void __launch_bounds__(256) compact_lowd(PassArgs a) {
             const uint32_t nv = (r + 1 < a.cap) ? slot[(size_t)(r + 1) * a.B] : 0u;   // prefetch
             expand_record<T, D>(a, c0, v, q, pos, sp);
             v = nv;
+        }
+    }
+}
+
+// Balanced compaction: the CTA lists its item's slot records (entries in order, records in
+// order) and gives one record per thread, so an entry with many hits no longer holds the
+// whole CTA; a record's place in its row is its entry's row base plus the prefix sum of
+// the hit counts of the entry's earlier records (CTA scans).
+template <typename T, int D>
+__global__ void __launch_bounds__(256) compact_lowd_bal(PassArgs a) {
+    __shared__ int32_t s_rstart[257];
+    __shared__ int64_t s_base[256];
+    __shared__ int32_t s_hbase[256];
+    __shared__ T s_q[256 * D];
+    __shared__ int32_t s_wsum[8];
+    const T *Qs = static_cast<const T *>(a.Qs);
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    auto block_excl = [&](int v, int &total) {   // exclusive block scan (256 threads)
+        int incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) s_wsum[wid] = incl;
+        __syncthreads();
+        int before = 0;
+        total = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+            const int x = s_wsum[w];
+            before += w < wid ? x : 0;
+            total += x;
+        }
+        __syncthreads();
+        return before + incl - v;
+    };
+    for (int64_t item = blockIdx.x; item < a.total_items; item += gridDim.x) {
+        int64_t b, c0, c1;
+        locate(a, item, b, c0, c1);
+        const int64_t sp = b * a.B + tid;
+        const int64_t e = item * a.B + tid;
+        int nr = 0;
+        if (sp < a.m) {
+            const int32_t cv = a.cnt[e];
+            if (cv > 0) {   // cv < 0: lost entry (the fix pass writes it)
+                nr = a.nrec[e];
+                s_base[tid] = row_base(a, sp) + a.pre[e];
+#pragma unroll
+                for (int k = 0; k < D; ++k) s_q[tid * D + k] = Qs[(sp >> 2) * 4 * D + k * 4 + (sp & 3)];
+            }
+        }
+        int R = 0;
+        const int rs = block_excl(nr, R);
+        s_rstart[tid] = rs;
+        if (tid == 0) s_rstart[256] = R;
+        __syncthreads();
+        int carry = 0;
+        for (int k0 = 0; k0 < R; k0 += 256) {
+            const int k = k0 + tid;
+            int owner = 0, r = 0;
+            uint32_t v = 0;
+            if (k < R) {   // owner = last entry with rstart <= k
+                int lo = 0, hi = 256;
+                while (hi - lo > 1) {
+                    const int mid = (lo + hi) >> 1;
+                    if (s_rstart[mid] <= k) lo = mid; else hi = mid;
+                }
+                owner = lo;
+                r = k - s_rstart[owner];
+                v = a.slots[((size_t)item * a.cap + r) * a.B + owner];
+            }
+            const int h = k < R ? __popc(v & 15u) : 0;
+            int hsum = 0;
+            const int hex = block_excl(h, hsum) + carry;
+            if (k < R && r == 0) s_hbase[owner] = hex;
+            __syncthreads();
+            if (k < R) {
+                int64_t pos = s_base[owner] + (hex - s_hbase[owner]);
+                T q[D];
+#pragma unroll
+                for (int kk = 0; kk < D; ++kk) q[kk] = s_q[owner * D + kk];
+                expand_record<T, D>(a, c0, v, q, pos, b * a.B + owner);
+            }
+            carry += hsum;
+            __syncthreads();
         }
     }
 }
@@ -1248,7 +1335,8 @@ void launch_lowd_compact(const PassArgs &a, cudaStream_t s) {
     const int go = (int)(ceil_div(n_rec, 256) < 148 * 8 ? ceil_div(n_rec, 256) : 148 * 8);
 #define FN(T, D)                                                                         \
     do {                                                                                 \
-        SNN_LAUNCH((compact_lowd<T, D>), g, a.B, 0, s, a);                               \
+        if (a.nrec && a.B == 256) SNN_LAUNCH((compact_lowd_bal<T, D>), g, 256, 0, s, a); \
+        else SNN_LAUNCH((compact_lowd<T, D>), g, a.B, 0, s, a);                          \
         if (n_rec > 0) SNN_LAUNCH((compact_overflow<T, D>), go, 256, 0, s, a, n_rec);    \
     } while (0)
     SNN_LOWD_DISPATCH(FN)

@@ -58,6 +58,7 @@ struct PassArgs {
     int32_t *cnt;           // total_items x B hit counts (count / scan pass)
     int32_t *pre;           // total_items x B exclusive per-row prefixes (after row totals)
     uint16_t *slots;        // low-d scan pass: total_items x B x cap chunk-local hit indices
+    uint16_t *nrec = nullptr;   // records in the slots per (item, query) entry (balanced compaction)
     int cap;
     OvfRec *ovf_rec;        // low-d: records beyond `cap` (global overflow list)
     int32_t *ovf_rec_count; // device counter for ovf_rec

@@ -932,20 +932,23 @@ def test_load_rejects_broken_invariants(snn, tmp_path):
 @pytest.mark.parametrize("d", [2, 3, 6])
 def test_row_staging_and_symmetry_options_identical(snn, d):
     """Key-order row staging (default) vs direct final-row writes, symmetric vs two-sided
-    self-queries, expanded filter on/off: bit-identical CSR, equal to the oracle."""
+    self-queries, expanded filter on/off, balanced vs per-entry compaction: bit-identical
+    CSR, equal to the oracle."""
     import paper_2212_07679_b200 as p
     rng = np.random.default_rng(1400 + d)
     X = (rng.random((20000, d)) * 20).astype(np.float32)
     R = {2: 0.12, 3: 0.5, 6: 2.5}[d]
     outs = []
     try:
-        for st, sy, sf in [(1, 1, 0), (-1, 1, 0), (1, -1, 0), (-1, -1, -1), (1, 1, -1)]:
+        for st, sy, sf, bc in [(1, 1, 0, 0), (-1, 1, 0, 0), (1, -1, 0, 0), (-1, -1, -1, 0), (1, 1, -1, 0),
+                               (1, 1, 0, -1), (-1, 1, -1, -1)]:
             p.snn_set_option("stage_rows", st)
             p.snn_set_option("symmetric", sy)
             p.snn_set_option("simt_filter", sf)
+            p.snn_set_option("balanced_compact", bc)
             outs.append(run(snn, X, None, R))
     finally:
-        for k in ("stage_rows", "symmetric", "simt_filter"):
+        for k in ("stage_rows", "symmetric", "simt_filter", "balanced_compact"):
             p.snn_set_option(k, 0)
     compare(outs[0], oracle.radius_query(X, X, R))
     for o in outs[1:]:
