@@ -22,7 +22,8 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libsnn.so")
+# SNN_LIB: an alternative in-tree build of the same library (A/B timing of two builds)
+LIB_PATH = os.environ.get("SNN_LIB") or os.path.join(_HERE, "lib", "libsnn.so")
 
 SNN_F32, SNN_F64 = 0, 1
 STATUS = {0: "SNN_OK", 1: "SNN_ERR_INVALID_ARGUMENT", 2: "SNN_ERR_EMPTY",

@@ -534,7 +534,7 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
 #pragma unroll 1
                             for (int r = 0; r < rmax; ++r) {
                                 if (r < npend) {
-                                    const int g0 = GS * (int)((uint32_t)(pend >> (16 * r)) & 0xffffu);
+                                    const int g0 = GS * (int)((uint32_t)(pend >> (16 * (npend - 1 - r))) & 0xffffu);
 #pragma unroll
                                     for (int h = 0; h < GS; ++h) {
                                         const int gg = g0 + h;
@@ -569,7 +569,7 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
                             uint8_t *dres = s_dres + wq * 128;
                             float *dq = s_dq + wq * 32 * D;
                             for (int r = 0; r < npend; ++r)
-                                drec[excl + r] = ((uint32_t)lane << 16) | ((uint32_t)(pend >> (16 * r)) & 0xffffu);
+                                drec[excl + r] = ((uint32_t)lane << 16) | ((uint32_t)(pend >> (16 * (npend - 1 - r))) & 0xffffu);
 #pragma unroll
                             for (int k = 0; k < D; ++k) dq[lane * D + k] = (float)q[k];
                             __syncwarp();
@@ -609,7 +609,7 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
                             for (int r = 0; r < npend; ++r) {
                                 const uint32_t res = dres[excl + r];
                                 if (res) {
-                                    const int g0 = GS * (int)((uint32_t)(pend >> (16 * r)) & 0xffffu);
+                                    const int g0 = GS * (int)((uint32_t)(pend >> (16 * (npend - 1 - r))) & 0xffffu);
                                     if (res & 15u) emit0(g0, res & 15u);
                                     if (res >> 4) emit0(g0 + 1, res >> 4);
                                 }
@@ -634,7 +634,7 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
                         const float mn = fminf(fminf(fminf(pa.x, pa.y), fminf(qa.x, qa.y)),
                                                fminf(fminf(pb.x, pb.y), fminf(qb.x, qb.y)));
                         if (mn <= t_out) {
-                            pend |= (uint64_t)(uint32_t)(g >> 1) << (16 * npend);
+                            pend = (pend << 16) | (uint32_t)(g >> 1);   // FIFO: newest record in the low bits
                             ++npend;
                         }
                         if (__any_sync(0xffffffffu, npend >= 4)) drain();   // FIFO holds 4
@@ -665,7 +665,7 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
                             const float mnf = fminf(fminf(fminf(ea.x, ea.y), fminf(eb.x, eb.y)),
                                                     fminf(fminf(ec.x, ec.y), fminf(ed.x, ed.y)));
                             if (mnf <= thr) {
-                                pend |= (uint64_t)(uint32_t)(g >> 1) << (16 * npend);
+                                pend = (pend << 16) | (uint32_t)(g >> 1);   // FIFO: newest record in the low bits
                                 ++npend;
                             }
                             if (__any_sync(0xffffffffu, npend >= 4)) drain();
@@ -685,7 +685,7 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
                         const bool flag = mn <= t_out;
                         if (__any_sync(0xffffffffu, flag && npend == 4)) drain();   // drains run converged
                         if (flag) {
-                            pend |= (uint64_t)(uint32_t)(g / GS) << (16 * npend);
+                            pend = (pend << 16) | (uint32_t)(g / GS);
                             ++npend;
                         }
                         g = ngroups;
