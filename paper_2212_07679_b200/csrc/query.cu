@@ -662,8 +662,10 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
                                 hb = f2fma(f2pack(fb[k].z, fb[k].w), nqc[k], hb);
                             }
                             const float2 ea = f2unpack(la), eb = f2unpack(ha), ec = f2unpack(lb), ed = f2unpack(hb);
-                            const float mnf = fminf(fminf(fminf(ea.x, ea.y), fminf(eb.x, eb.y)),
-                                                    fminf(fminf(ec.x, ec.y), fminf(ed.x, ed.y)));
+                            // 8-way min as 3-input mins (FMNMX3): 4 instructions
+                            const float m1 = fminf(fminf(ea.x, ea.y), eb.x), m2 = fminf(fminf(eb.y, ec.x), ec.y);
+                            const float m3 = fminf(fminf(ed.x, ed.y), m1);
+                            const float mnf = fminf(m2, m3);
                             if (mnf <= thr) {
                                 pend = (pend << 16) | (uint32_t)(g >> 1);   // FIFO: newest record in the low bits
                                 ++npend;
