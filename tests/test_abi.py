@@ -117,3 +117,14 @@ def test_header_is_plain_c(tmp_path):
     src.write_text('#include "include/snn.h"\nint main(void) { return 0; }\n')
     subprocess.check_call(["gcc", "-std=c99", "-Wall", "-Werror", "-fsyntax-only", "-I", ROOT, str(src)])
     subprocess.check_call(["g++", "-std=c++17", "-Wall", "-Werror", "-fsyntax-only", "-x", "c++", "-I", ROOT, str(src)])
+
+
+def test_c_demo_links_against_the_library(libpath, tmp_path):
+    """examples/c_api_demo.c (plain C99, no CUDA headers) compiles and links against
+    lib/libsnn.so: the boundary is usable without Python."""
+    exe = tmp_path / "c_api_demo"
+    libdir = os.path.dirname(libpath)
+    subprocess.check_call(["gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                           os.path.join(ROOT, "examples", "c_api_demo.c"), "-L", libdir, "-lsnn",
+                           f"-Wl,-rpath,{libdir}", "-o", str(exe)])
+    assert exe.exists()

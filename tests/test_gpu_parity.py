@@ -1022,3 +1022,19 @@ def test_index_sigma_vs_oracle_svd(snn, d, dt, s_ratio):
         assert abs(sig[1] / sig[0] - s_ratio) < 0.05
     if d > 3:   # well separated spectrum (1/sqrt(i) scales): the deflated values match too
         np.testing.assert_allclose(sig, S[:k], rtol=max(tol, 1e-4))
+
+
+def test_c_demo_runs(snn, tmp_path):
+    """The plain-C example builds, queries (every point finds itself), copies the CSR to
+    the host and runs DBSCAN through the C ABI alone."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    libdir = os.path.join(root, "paper_2212_07679_b200", "lib")
+    exe = tmp_path / "c_api_demo"
+    subprocess.check_call(["gcc", "-std=c99", "-I", os.path.join(root, "include"),
+                           os.path.join(root, "examples", "c_api_demo.c"), "-L", libdir, "-lsnn",
+                           f"-Wl,-rpath,{libdir}", "-o", str(exe)])
+    out = subprocess.check_output([str(exe)]).decode().split()
+    n, m, nnz, k = map(int, out)
+    assert n == m == 4096 and nnz > n and k >= 1
