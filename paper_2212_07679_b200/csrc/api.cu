@@ -437,8 +437,12 @@ static snn_status build_impl(const void *X, int64_t n, int32_t d, snn_dtype dt, 
     launch_keys(Xd, f64, n, d, idx->mu_d, idx->mu_f, idx->v_d, idx->v_f, keys_raw, s);  // K3
     radix_sort_pairs(keys_raw, nullptr, idx->keys, reinterpret_cast<uint32_t *>(idx->perm), n,
                      sort_tmp, s);                                                 // K4
-    launch_gather(Xd, f64, n, d, idx->ld, idx->n_pad, reinterpret_cast<const uint32_t *>(idx->perm),
-                  idx->mu_d, idx->Xs, idx->xbar, s);                               // K5
+    // tensor-core indexes gather after the stats sync (the FP16 scale needs max|x_c|), fused
+    // with the operand copy; all others here
+    const bool tc_cand = idx->ld != 0 && g_opt.tc && !g_opt.force_generic && d >= g_opt.tc_min_d;
+    if (!tc_cand)
+        launch_gather(Xd, f64, n, d, idx->ld, idx->n_pad, reinterpret_cast<const uint32_t *>(idx->perm),
+                      idx->mu_d, idx->Xs, idx->xbar, s);                           // K5
     CKI(cudaGetLastError(), "launch");
     double *hs = static_cast<double *>(t_pinned.p);
     CKI(cudaMemcpyAsync(hs, idx->stats, ST_COUNT * 8, cudaMemcpyDeviceToHost, s), "D2H stats");
@@ -457,19 +461,21 @@ static snn_status build_impl(const void *X, int64_t n, int32_t d, snn_dtype dt, 
         idx->xf_c1h = c1h;
         launch_filter_rows(static_cast<const float *>(idx->Xs), d, n, idx->n_pad, idx->mu_f, c1h, idx->Xf, s);
     }
-    if (idx->ld != 0 && g_opt.tc && !g_opt.force_generic && d >= g_opt.tc_min_d) {   // K5': TC operand copy
+    if (tc_cand) {   // K5 + K5': sorted copy and tensor-core operand copy
         idx->tc = 1;
         int e = 0;
         idx->tc_f16 = g_opt.tc_f16 && f16_exponent(idx->h_stats[ST_XCMAX], &e);
         idx->xexp = e;
         idx->kpad = tc_kpad(d, idx->tc_f16);
-        if (idx->tc_f16) {
+        if (idx->tc_f16) {   // one pass over X writes both copies and the half norms
             uint16_t *xt = nullptr;
             CKI(own(&xt, (size_t)n * idx->kpad), "alloc FP16 copy");
             idx->Xt = xt;
-            launch_gather_f16(Xd, f64, n, d, reinterpret_cast<const uint32_t *>(idx->perm), idx->mu_f,
-                              ldexpf(1.0f, e), idx->Xt, idx->xbar, s);
+            launch_gather_xs_f16(Xd, f64, n, idx->n_pad, d, idx->ld, reinterpret_cast<const uint32_t *>(idx->perm),
+                                 idx->mu_f, ldexpf(1.0f, e), idx->Xs, idx->Xt, idx->xbar, s);
         } else {
+            launch_gather(Xd, f64, n, d, idx->ld, idx->n_pad, reinterpret_cast<const uint32_t *>(idx->perm),
+                          idx->mu_d, idx->Xs, idx->xbar, s);                       // K5
             float *xt = nullptr;
             CKI(own(&xt, (size_t)n * idx->kpad), "alloc TF32 copy");
             idx->Xt = xt;

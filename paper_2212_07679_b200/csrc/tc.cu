@@ -412,6 +412,50 @@ __global__ void __launch_bounds__(256) recheck_pairs(const T *__restrict__ Xs, c
     }
 }
 
+// Fused K5 for FP16 tensor-core indexes: one read of X[perm[i]] writes the sorted copy
+// (stride ld, zero pad, NaN sentinel rows [n, n_pad)), the scaled FP16 centred operand
+// row (kpad, zero pad) and the half norm of the fp32 centred row (fp64 accumulation) --
+// the same values as gather_generic + gather_f16.
+template <typename T>
+__global__ void __launch_bounds__(256) gather_xs_f16(const T *__restrict__ X, int64_t n, int64_t n_pad, int d, int ld,
+                                                     int kpad, const uint32_t *__restrict__ perm,
+                                                     const float *__restrict__ mu_f, float scale, T *__restrict__ Xs,
+                                                     __half *__restrict__ out, float *half_norm) {
+    const int l = threadIdx.x % 32;
+    const int kmax = ld > kpad ? ld : kpad;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; i < n_pad;
+         i += (int64_t)gridDim.x * blockDim.x / 32) {
+        if (i >= n) {   // sentinel rows: never candidates
+            for (int k = l; k < ld; k += 32) Xs[i * ld + k] = (k < d) ? (T)NAN : (T)0;
+            if (l == 0 && half_norm) half_norm[i] = NAN;
+            continue;
+        }
+        const T *x = X + (int64_t)perm[i] * d;
+        double h = 0.0;
+        for (int k = 2 * l; k < kmax; k += 64) {
+            const T a0 = k < d ? x[k] : (T)0, a1 = k + 1 < d ? x[k + 1] : (T)0;
+            if (k < ld) Xs[i * ld + k] = a0;
+            if (k + 1 < ld) Xs[i * ld + k + 1] = a1;
+            if (k < kpad) {
+                float v0 = 0.f, v1 = 0.f;
+                if (k < d) {
+                    const float c = (float)((double)a0 - (double)mu_f[k]);
+                    h += (double)c * (double)c;
+                    v0 = c * scale;
+                }
+                if (k + 1 < d) {
+                    const float c = (float)((double)a1 - (double)mu_f[k + 1]);
+                    h += (double)c * (double)c;
+                    v1 = c * scale;
+                }
+                *reinterpret_cast<__half2 *>(out + i * kpad + k) = __halves2half2(__float2half_rn(v0), __float2half_rn(v1));
+            }
+        }
+        h = warp_sum(h);
+        if (l == 0 && half_norm) half_norm[i] = (float)(0.5 * h);
+    }
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------------- host side
@@ -453,6 +497,19 @@ void launch_gather_f16(const void *X, bool f64, int64_t rows, int d, const uint3
     __half *o = static_cast<__half *>(out);
     if (f64) SNN_LAUNCH(gather_f16<double>, (int)g, 256, 0, s, (const double *)X, rows, d, kpad, perm, mu_f, scale, o, half_norm);
     else SNN_LAUNCH(gather_f16<float>, (int)g, 256, 0, s, (const float *)X, rows, d, kpad, perm, mu_f, scale, o, half_norm);
+}
+
+void launch_gather_xs_f16(const void *X, bool f64, int64_t n, int64_t n_pad, int d, int ld, const uint32_t *perm,
+                          const float *mu_f, float scale, void *Xs, void *out, float *half_norm, cudaStream_t s) {
+    if (n_pad == 0) return;
+    const int kpad = tc_kpad(d, true);
+    int64_t g = ceil_div(n_pad * 32, 256);
+    if (g > 148 * 16) g = 148 * 16;
+    __half *o = static_cast<__half *>(out);
+    if (f64) SNN_LAUNCH(gather_xs_f16<double>, (int)g, 256, 0, s, (const double *)X, n, n_pad, d, ld, kpad, perm, mu_f,
+                        scale, (double *)Xs, o, half_norm);
+    else SNN_LAUNCH(gather_xs_f16<float>, (int)g, 256, 0, s, (const float *)X, n, n_pad, d, ld, kpad, perm, mu_f, scale,
+                    (float *)Xs, o, half_norm);
 }
 
 bool launch_tc_window(const void *Qt, const void *Xt, bool f16, const TcArgs &a, int sm_count, cudaStream_t s) {

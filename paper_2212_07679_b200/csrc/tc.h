@@ -34,6 +34,9 @@ int64_t tc_claim_slack();   // pair-list slots a CTA may leave unused (claimed b
 void launch_gather_tf32(const void *X, bool f64, int64_t rows, int d, const uint32_t *perm, const float *mu_f,
                         float *out, float *half_norm, cudaStream_t s);
 // FP16 centred copy scaled by `scale` (a power of two), zero padded to kpad = tc_kpad(d, true).
+// Fused sorted copy + FP16 operand copy + half norms (one read of X; FP16 indexes).
+void launch_gather_xs_f16(const void *X, bool f64, int64_t n, int64_t n_pad, int d, int ld, const uint32_t *perm,
+                          const float *mu_f, float scale, void *Xs, void *out, float *half_norm, cudaStream_t s);
 void launch_gather_f16(const void *X, bool f64, int64_t rows, int d, const uint32_t *perm, const float *mu_f,
                        float scale, void *out, float *half_norm, cudaStream_t s);
 // grp_lo / grp_items for ceil(nblocks / group) raster groups
