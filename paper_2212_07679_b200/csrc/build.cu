@@ -238,7 +238,9 @@ __global__ void power_small(const double *__restrict__ G, int max_iters, double 
     const int squarings = max_iters >= 64 ? 24 : 0;
 #pragma unroll
     for (int j = 0; j < D; ++j) m[j] /= gmax;
+    int done_sq = 0;
     for (int it = 0; it < squarings; ++it) {
+        ++done_sq;
         double r[D];
 #pragma unroll
         for (int j = 0; j < D; ++j) r[j] = 0.0;
@@ -252,8 +254,16 @@ __global__ void power_small(const double *__restrict__ G, int max_iters, double 
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         if (!(mx > 0.0)) break;
+        double ch = 0.0;   // converged to the rank-1 projector: stop squaring early
 #pragma unroll
-        for (int j = 0; j < D; ++j) m[j] = (l < D) ? r[j] / mx : 0.0;
+        for (int j = 0; j < D; ++j) {
+            const double nm = (l < D) ? r[j] / mx : 0.0;
+            ch = fmax(ch, fabs(nm - m[j]));
+            m[j] = nm;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ch = fmax(ch, __shfl_xor_sync(0xffffffffu, ch, o));
+        if (ch < 1e-15) break;
     }
     // column with the largest diagonal entry (lowest index on ties)
     double diag = 0.0;
@@ -277,7 +287,7 @@ __global__ void power_small(const double *__restrict__ G, int max_iters, double 
     double g[D];
 #pragma unroll
     for (int j = 0; j < D; ++j) g[j] = (l < D) ? G[l * D + j] : 0.0;
-    int iters = squarings;
+    int iters = done_sq;
     const int polish = squarings ? 4 : max_iters;
     for (int it = 0; it < polish; ++it) {
         double y = 0.0;
