@@ -793,7 +793,7 @@ void launch_power_iteration(const double *G, int d, int max_iters, double tol,
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
             const size_t smem = (size_t)d * sizeof(double);
-            if (d <= 16384 && scratch &&
+            if (d > 128 && d <= 16384 && scratch &&   // d <= 128: one CTA (power_generic) is faster than grid barriers
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&grid, power_coop, 256, smem) == cudaSuccess && grid > 0) {
                 grid = nsm < d ? nsm : d;
                 double *ybuf = scratch, *part = scratch + 2 * d;
