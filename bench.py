@@ -37,6 +37,7 @@ import workloads  # noqa: E402
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 TRAFFIC_PATH = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 METRIC = "radius queries/s at n=1M (index build + self-queries)"
+METRIC_DBSCAN = "DBSCAN points/s (index build + DBSCAN, n=2M)"
 
 
 # ----------------------------------------------------------------------------- helpers
@@ -151,19 +152,35 @@ def cpu_model() -> str:
 
 
 def oracle_sample_rate(w, target_s: float):
-    """Oracle (fp64 brute force, host cores) on a bounded sample of the workload's
-    queries: returns (queries/s, sample size, seconds, threads)."""
+    """Oracle (fp64 brute force, host cores) on a bounded sample of the workload: returns
+    (units/s, sample size, seconds, threads, sample description).
+
+    Radius queries: the first k queries against all n points (``oracle.radius_query``).
+    DBSCAN (config 5): the eps-neighbourhood counts of the first k points against all n
+    points (``oracle.neighbour_counts``) -- the first of the brute-force DBSCAN's passes, so
+    the rate is an upper bound on the oracle's DBSCAN points/s."""
     import oracle
-    Q = w.queries
+    dbscan = w.dbscan_min_pts is not None
+
+    def run(k):
+        if dbscan:
+            oracle.neighbour_counts(w.X, w.R, np.arange(k))
+        else:
+            oracle.radius_query(w.X, w.queries[:k], w.R)
     k = min(64, w.m)
     t = time.perf_counter()
-    oracle.radius_query(w.X, Q[:k], w.R)
+    run(k)
     dt = time.perf_counter() - t
     k2 = int(min(w.m, max(k, k * target_s / max(dt, 1e-6))))
     t = time.perf_counter()
-    oracle.radius_query(w.X, Q[:k2], w.R)
+    run(k2)
     dt2 = time.perf_counter() - t
-    return k2 / dt2, k2, dt2, oracle.num_threads()
+    if dbscan:
+        sample = (f"eps-neighbourhood counts of the first {k2} of {w.n} points vs all {w.n} points "
+                  f"(the brute-force DBSCAN's first pass; upper bound on its points/s), fp64 ({dt2:.1f} s)")
+    else:
+        sample = f"first {k2} of {w.m} queries vs all {w.n} points, fp64 brute force ({dt2:.1f} s)"
+    return k2 / dt2, k2, dt2, oracle.num_threads(), sample
 
 
 def run_reference(args):
@@ -172,28 +189,38 @@ def run_reference(args):
         return
     import oracle
     w = workload(args.config)
+    dbscan = w.dbscan_min_pts is not None
     # per-step sample sized so the whole --steps/--warmup run ends in ~1-2 minutes
-    rate, _, _, threads = oracle_sample_rate(w, 2.0)
+    rate, _, _, threads, _ = oracle_sample_rate(w, 2.0)
     per_step = int(max(8, min(w.m, rate * 60.0 / max(1, args.steps + args.warmup))))
-    Q = w.queries
+
+    def run(s0, k):
+        if dbscan:
+            oracle.neighbour_counts(w.X, w.R, np.arange(s0, s0 + k))
+        else:
+            oracle.radius_query(w.X, w.queries[s0:s0 + k], w.R)
     for i in range(args.warmup):
-        oracle.radius_query(w.X, Q[:per_step], w.R)
+        run(0, per_step)
     t = time.perf_counter()
     for i in range(args.steps):
-        s0 = (i * per_step) % max(1, w.m - per_step + 1)
-        oracle.radius_query(w.X, Q[s0:s0 + per_step], w.R)
+        run((i * per_step) % max(1, w.m - per_step + 1), per_step)
     dt = time.perf_counter() - t
     value = per_step * args.steps / dt
-    sample = (f"{per_step} of {w.m} queries per step against all {w.n} points "
-              f"(fp64 brute force, no index build)")
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "queries/s",
+    if dbscan:
+        sample = (f"eps-neighbourhood counts of {per_step} of {w.n} points per step vs all {w.n} points "
+                  f"(fp64 brute force; the DBSCAN oracle's first pass, an upper bound on its points/s)")
+    else:
+        sample = (f"{per_step} of {w.m} queries per step against all {w.n} points "
+                  f"(fp64 brute force, no index build)")
+    unit = "points/s" if dbscan else "queries/s"
+    line = {"impl": "reference", "metric": METRIC_DBSCAN if dbscan else METRIC, "value": value, "unit": unit,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_block(w, args),
-            "cpu_baseline": {"value": value, "unit": "queries/s", "cores": threads,
+            "cpu_baseline": {"value": value, "unit": unit, "cores": threads,
                              "kind": "oracle", "sample": sample, "cpu": cpu_model()},
-            "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0,
+            "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -387,7 +414,7 @@ def run_gpu(args):
     e2e_value = (w.m * args.steps if shard else weak_units(w.m * args.steps, world)) / (e2e_ms / 1e3)
     h2d = w.X.nbytes + (0 if w.Q is None else w.Q.nbytes)
     d2h = w.n * 4 if dbscan else (w.m + 1) * 8 + nnz * 8
-    metric = "DBSCAN points/s (index build + DBSCAN, n=2M)" if dbscan else METRIC
+    metric = METRIC_DBSCAN if dbscan else METRIC
     unit = "points/s" if dbscan else "queries/s"
 
     roofline = roofline_block(args, w, prof, times, dev, info)
@@ -405,12 +432,10 @@ def run_gpu(args):
             "e2e": {"value": e2e_value, "unit": unit, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.steps},
             "roofline": roofline}
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and not dbscan:
-        rate, k, dt, threads = oracle_sample_rate(w, args.cpu_seconds)
-        line["cpu_baseline"] = {"value": rate, "unit": "queries/s", "cores": threads,
-                                "kind": "oracle", "cpu": cpu_model(),
-                                "sample": f"first {k} of {w.m} queries vs all {w.n} points, "
-                                          f"fp64 brute force ({dt:.1f} s)"}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, k, dt, threads, sample = oracle_sample_rate(w, args.cpu_seconds)
+        line["cpu_baseline"] = {"value": rate, "unit": unit, "cores": threads,
+                                "kind": "oracle", "cpu": cpu_model(), "sample": sample}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -9,7 +9,12 @@ Contents (each function cites the passage it follows):
 * ``radius_query``      brute-force fixed-radius search = the problem's definition
                         (§3.2; exactness claim PAPER.md:31),
                         fp64 eq:ip1, in C (``snn_oracle.c``).
-* ``dbscan``            brute-force DBSCAN with DESIGN.md reading C18.
+* ``radius_query(grid=True)``  the same result for d <= 3 from grid-pruned pairs (same
+                        per-pair test; full-size parity digests of configs 2 and 5).
+* ``dbscan``            DBSCAN with DESIGN.md reading C18: ascending-id
+                        scan with FIFO expansion over brute-force neighbourhoods; ``grid=True``
+                        computes the same labels by components for d <= 3.
+* ``neighbour_counts``  eps-neighbourhood sizes of sampled points (DBSCAN's core test).
 * ``column_mean``, ``center``, ``principal_direction``, ``scores``, ``sort_index``,
   ``half_norms``, ``build_index``   Algorithm 1 "SNN Index" step by
                         step in fp64 numpy, the SVD of eq:svd via LAPACK.
@@ -65,6 +70,12 @@ def _load():
         lib.oracle_dbscan.restype = ctypes.c_int64
         lib.oracle_neighbour_counts.argtypes = [P, i64, i32, f64, P, i64, P]
         lib.oracle_neighbour_counts.restype = ctypes.c_int
+        lib.oracle_grid_radius_count.argtypes = [P, i64, P, i64, i32, f64, f64, P]
+        lib.oracle_grid_radius_count.restype = ctypes.c_int
+        lib.oracle_grid_radius_fill.argtypes = [P, i64, P, i64, i32, f64, f64, P, P, P]
+        lib.oracle_grid_radius_fill.restype = ctypes.c_int
+        lib.oracle_grid_dbscan.argtypes = [P, i64, i32, f64, i32, P, P]
+        lib.oracle_grid_dbscan.restype = ctypes.c_int64
         lib.oracle_sqdist.argtypes = [P, P, i32]
         lib.oracle_sqdist.restype = ctypes.c_double
         lib.oracle_num_threads.restype = ctypes.c_int
@@ -96,8 +107,13 @@ def sqdist(p, q) -> float:
 
 
 # ----------------------------------------------------------------- radius query
-def radius_query(P, Q, R: float, band_rel: float = 1e-5) -> dict:
+def radius_query(P, Q, R: float, band_rel: float = 1e-5, grid: bool = False) -> dict:
     """Brute force: all (j, i) with s(p_i, q_j) <= (R*R)(1+band_rel).
+
+    ``grid=True`` (d <= 3 only) evaluates only the pairs in adjacent grid cells of side
+    >= R(1+1e-6) (``oracle_grid_radius_*`` in ``snn_oracle.c``, with the argument why no hit
+    is skipped); the per-pair test is the same, so the result is identical (pinned against
+    the brute force in ``tests/test_oracle.py``).  Used for full-size d <= 3 parity.
 
     Returns CSR over queries (row j = query j, ids ascending): ``offsets`` (m+1 int64),
     ``indices`` (int32 original ids), ``s`` (fp64 squared distance), plus ``R2`` = R*R.
@@ -112,23 +128,28 @@ def radius_query(P, Q, R: float, band_rel: float = 1e-5) -> dict:
     if Q.shape[1] != d:
         raise ValueError("dimension mismatch")
     lib = _load()
+    if grid and d > 3:
+        raise ValueError("grid oracle is for d <= 3")
+    count_fn = lib.oracle_grid_radius_count if grid else lib.oracle_radius_count
+    fill_fn = lib.oracle_grid_radius_fill if grid else lib.oracle_radius_fill
     counts = np.zeros(m, dtype=np.int64)
-    if lib.oracle_radius_count(P.ctypes.data, n, Q.ctypes.data, m, d, float(R),
-                               float(band_rel), counts.ctypes.data):
+    if count_fn(P.ctypes.data, n, Q.ctypes.data, m, d, float(R), float(band_rel), counts.ctypes.data):
         raise ValueError("oracle_radius_count failed")
     offsets = np.zeros(m + 1, dtype=np.int64)
     np.cumsum(counts, out=offsets[1:])
     nnz = int(offsets[-1])
     idx = np.empty(max(nnz, 1), dtype=np.int32)
     s = np.empty(max(nnz, 1), dtype=np.float64)
-    if lib.oracle_radius_fill(P.ctypes.data, n, Q.ctypes.data, m, d, float(R), float(band_rel),
-                              offsets.ctypes.data, idx.ctypes.data, s.ctypes.data):
+    if fill_fn(P.ctypes.data, n, Q.ctypes.data, m, d, float(R), float(band_rel),
+               offsets.ctypes.data, idx.ctypes.data, s.ctypes.data):
         raise ValueError("oracle_radius_fill failed")
     return {"offsets": offsets, "indices": idx[:nnz], "s": s[:nnz], "R2": float(R) * float(R)}
 
 
 def neighbour_counts(P, eps: float, ids) -> np.ndarray:
-    """|{j : s(p_j, p_i) <= eps^2}| (self included) for the sampled ids, one by one."""
+    """|{j : s(p_j, p_i) <= eps^2}| (self included) for the sampled ids, one by one: the
+    eps-neighbourhood size DBSCAN's core test uses (reading C18), eq:ip1
+    in fp64 against every point."""
     P = _f64(P)
     ids = np.ascontiguousarray(ids, dtype=np.int64)
     out = np.zeros(ids.shape[0], dtype=np.int64)
@@ -137,17 +158,25 @@ def neighbour_counts(P, eps: float, ids) -> np.ndarray:
     return out
 
 
-def dbscan(P, eps: float, min_pts: int):
-    """Brute-force DBSCAN with DESIGN.md reading C18.
+def dbscan(P, eps: float, min_pts: int, grid: bool = False):
+    """DBSCAN with DESIGN.md reading C18: the textbook scan in ascending
+    id with FIFO expansion, brute-force neighbourhoods (``oracle_dbscan``).
+
+    ``grid=True`` (d <= 3): the same labels computed as connected components of the core
+    graph over grid-pruned pairs (``oracle_grid_dbscan``; border point -> smallest cluster
+    number among its core neighbours = the first cluster the FIFO scan reaches it with);
+    pinned against the brute force in ``tests/test_oracle.py``.  Used for full-size C5.
 
     Returns (labels int32[n], K, counts int64[n]).
     """
     P = _f64(P)
     n, d = P.shape
+    if grid and d > 3:
+        raise ValueError("grid oracle is for d <= 3")
     labels = np.empty(n, dtype=np.int32)
     counts = np.empty(n, dtype=np.int64)
-    K = _load().oracle_dbscan(P.ctypes.data, n, d, float(eps), int(min_pts),
-                              labels.ctypes.data, counts.ctypes.data)
+    fn = _load().oracle_grid_dbscan if grid else _load().oracle_dbscan
+    K = fn(P.ctypes.data, n, d, float(eps), int(min_pts), labels.ctypes.data, counts.ctypes.data)
     if K < 0:
         raise ValueError("oracle_dbscan failed")
     return labels, int(K), counts

@@ -2,9 +2,11 @@
 //
 // Readings (C18): closed eps-balls including the point itself; core iff
 // |N_eps(i)| >= min_pts; clusters = connected components of core points under
-// eps-adjacency; a non-core point with >= 1 core neighbour takes the cluster of its
-// smallest-original-id core neighbour; other points are noise (-1); clusters are numbered
-// 0..K-1 by increasing smallest original core id.  All neighbourhood tests use the exact
+// eps-adjacency; a non-core point with >= 1 core neighbour takes the first cluster that
+// reaches it in the ascending-id scan with FIFO expansion (scikit-learn's
+// order), i.e. the smallest cluster number among its core neighbours; other
+// points are noise (-1); clusters are numbered 0..K-1 by increasing smallest original core
+// id.  All neighbourhood tests use the exact
 // windowed classification of the radius query (bit-identical to the fp64 oracle).
 //
 // Pipeline on the sorted index (neighbour lists are never materialised):
@@ -65,22 +67,19 @@ __global__ void flag_roots(const int32_t *parent, const uint8_t *core, const int
         if (core[i] && parent[i] == i) flag[minid[i]] = 1;
 }
 
-// labels of core points (sorted order) and inverse permutation
+// labels of core points (sorted order)
 __global__ void core_labels(const int32_t *parent, const uint8_t *core, const int32_t *minid,
-                            const int64_t *rank, const int32_t *perm, int64_t n, int32_t *lab,
-                            int32_t *inv) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+                            const int64_t *rank, int64_t n, int32_t *lab) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         lab[i] = core[i] ? (int32_t)rank[minid[parent[i]]] : -1;
-        inv[perm[i]] = (int32_t)i;
-    }
 }
 
-// border points: cluster of the smallest-id core neighbour; scatter to original order
+// border points: smallest cluster number among core neighbours; scatter to original order
 __global__ void final_labels(const int32_t *lab, const uint8_t *core, const int32_t *best,
-                             const int32_t *inv, const int32_t *perm, int64_t n, int32_t *out) {
+                             const int32_t *perm, int64_t n, int32_t *out) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         int32_t l = lab[i];
-        if (!core[i]) l = (best[i] != 0x7fffffff) ? lab[inv[best[i]]] : -1;
+        if (!core[i]) l = (best[i] != 0x7fffffff) ? best[i] : -1;
         out[perm[i]] = l;
     }
 }
@@ -147,8 +146,9 @@ __global__ void csr_union(const int64_t *off, const int32_t *idx, const uint8_t 
     }
 }
 
-// warp per non-core row: smallest original id among core neighbours
-__global__ void csr_border(const int64_t *off, const int32_t *idx, const uint8_t *core, int64_t n, int32_t *best) {
+// warp per non-core row: smallest cluster number among core neighbours
+__global__ void csr_border(const int64_t *off, const int32_t *idx, const uint8_t *core, const int32_t *lab,
+                           int64_t n, int32_t *best) {
     const int lane = threadIdx.x % 32;
     for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; i < n;
          i += (int64_t)gridDim.x * blockDim.x / 32) {
@@ -156,7 +156,7 @@ __global__ void csr_border(const int64_t *off, const int32_t *idx, const uint8_t
         int32_t b = 0x7fffffff;
         for (int64_t k = off[i] + lane; k < off[i + 1]; k += 32) {
             const int32_t j = idx[k];
-            if (core[j]) b = min(b, j);
+            if (core[j]) b = min(b, lab[j]);
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) b = min(b, __shfl_xor_sync(0xffffffffu, b, o));
@@ -214,7 +214,7 @@ snn_status dbscan_impl(snn_index idx, double eps, int32_t min_pts, int32_t *labe
     CKD(cudaStreamSynchronize(s), "dbscan windows");
     const int64_t total_items = hbuf[0];
 
-    int32_t *cnt, *count, *parent, *minid, *best, *flag, *lab, *inv, *out;
+    int32_t *cnt, *count, *parent, *minid, *best, *flag, *lab, *out;
     int64_t *rank;
     uint8_t *core;
     CKD(ws.alloc(&cnt, (size_t)total_items * B), "alloc");
@@ -226,7 +226,6 @@ snn_status dbscan_impl(snn_index idx, double eps, int32_t min_pts, int32_t *labe
     CKD(ws.alloc(&flag, (size_t)n), "alloc");
     CKD(ws.alloc(&rank, (size_t)n + 1), "alloc");
     CKD(ws.alloc(&lab, (size_t)n), "alloc");
-    CKD(ws.alloc(&inv, (size_t)n), "alloc");
     const bool dev_out = is_device_ptr(labels);
     if (dev_out) out = labels; else CKD(ws.alloc(&out, (size_t)n), "alloc");
 
@@ -306,7 +305,7 @@ snn_status dbscan_impl(snn_index idx, double eps, int32_t min_pts, int32_t *labe
     CKD(cudaMemsetAsync(flag, 0, (size_t)n * 4, s), "memset");
     SNN_LAUNCH(flag_roots, grid_n(n), 256, 0, s, parent, core, minid, n, flag);
     exclusive_scan_i32_to_i64(flag, rank, n, scan_tmp, s);                  // canonical ranks
-    SNN_LAUNCH(core_labels, grid_n(n), 256, 0, s, parent, core, minid, rank, idx->perm, n, lab, inv);
+    SNN_LAUNCH(core_labels, grid_n(n), 256, 0, s, parent, core, minid, rank, n, lab);
     {   // border points: a radius query of the compacted non-core points only
         int64_t *npos;
         CKD(ws.alloc(&npos, (size_t)n + 1), "alloc");
@@ -346,10 +345,11 @@ snn_status dbscan_impl(snn_index idx, double eps, int32_t min_pts, int32_t *labe
             ab.nblocks = nb3; ab.total_items = hbuf[0];
             ab.item_block = nullptr;   // its own work list: binary-search locate
             ab.cnt = nullptr; ab.pre = nullptr;
+            ab.blab = lab;
             launch_lowd_mode(4, ab, s);                                      // border points
         }
     }
-    SNN_LAUNCH(final_labels, grid_n(n), 256, 0, s, lab, core, best, inv, idx->perm, n, out);
+    SNN_LAUNCH(final_labels, grid_n(n), 256, 0, s, lab, core, best, idx->perm, n, out);
     if (!dev_out) CKD(cudaMemcpyAsync(labels, out, (size_t)n * 4, cudaMemcpyDeviceToHost, s), "D2H labels");
     CKD(cudaMemcpyAsync(hbuf + 1, rank + n, 8, cudaMemcpyDeviceToHost, s), "D2H K");
     CKD(cudaGetLastError(), "launch");
@@ -369,7 +369,7 @@ snn_status dbscan_from_csr(const int64_t *off, const int32_t *nidx, int64_t n, i
         cudaError_t _e = (expr);                               \
         if (_e != cudaSuccess) return cuda_fail(_e, where);    \
     } while (0)
-    int32_t *count, *parent, *minid, *best, *flag, *lab, *inv, *out, *iota;
+    int32_t *count, *parent, *minid, *best, *flag, *lab, *out, *iota;
     int64_t *rank, *hbuf;
     uint8_t *core, *scan_tmp;
     CKD(ws.alloc(&count, (size_t)n), "alloc");
@@ -380,7 +380,6 @@ snn_status dbscan_from_csr(const int64_t *off, const int32_t *nidx, int64_t n, i
     CKD(ws.alloc(&flag, (size_t)n), "alloc");
     CKD(ws.alloc(&rank, (size_t)n + 1), "alloc");
     CKD(ws.alloc(&lab, (size_t)n), "alloc");
-    CKD(ws.alloc(&inv, (size_t)n), "alloc");
     CKD(ws.alloc(&iota, (size_t)n), "alloc");
     CKD(ws.alloc(&scan_tmp, scan_temp_bytes(n)), "alloc");
     CKD(cudaMallocHost(&hbuf, 32), "pinned");
@@ -396,9 +395,9 @@ snn_status dbscan_from_csr(const int64_t *off, const int32_t *nidx, int64_t n, i
     CKD(cudaMemsetAsync(flag, 0, (size_t)n * 4, s), "memset");
     SNN_LAUNCH(flag_roots, g, 256, 0, s, parent, core, minid, n, flag);
     exclusive_scan_i32_to_i64(flag, rank, n, scan_tmp, s);
-    SNN_LAUNCH(core_labels, g, 256, 0, s, parent, core, minid, rank, iota, n, lab, inv);
-    SNN_LAUNCH(csr_border, gw, 256, 0, s, off, nidx, core, n, best);
-    SNN_LAUNCH(final_labels, g, 256, 0, s, lab, core, best, inv, iota, n, out);
+    SNN_LAUNCH(core_labels, g, 256, 0, s, parent, core, minid, rank, n, lab);
+    SNN_LAUNCH(csr_border, gw, 256, 0, s, off, nidx, core, lab, n, best);
+    SNN_LAUNCH(final_labels, g, 256, 0, s, lab, core, best, iota, n, out);
     if (!dev_out) CKD(cudaMemcpyAsync(labels, out, (size_t)n * 4, cudaMemcpyDeviceToHost, s), "D2H labels");
     CKD(cudaMemcpyAsync(hbuf, rank + n, 8, cudaMemcpyDeviceToHost, s), "D2H K");
     CKD(cudaGetLastError(), "launch");

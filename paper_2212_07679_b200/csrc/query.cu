@@ -273,7 +273,7 @@ __device__ __forceinline__ void group_d2(const float4 (&xv)[D], const uint64_t (
 //   M_FIX    recompute entries whose records were lost; write CSR directly
 //   M_COUNT  DBSCAN: |N_eps(i)| (self included)
 //   M_UNION  DBSCAN: union core i with every core neighbour j > i (sorted positions)
-//   M_BORDER DBSCAN: for non-core i, the smallest original id among core neighbours
+//   M_BORDER DBSCAN: for non-core i, the smallest cluster number among core neighbours
 enum { M_SCAN = 0, M_FIX = 1, M_COUNT = 2, M_UNION = 3, M_BORDER = 4 };
 
 // Lock-free union-find over sorted positions (parent[x] <= x: every link goes from the
@@ -366,7 +366,7 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
         // M_BORDER over a compacted query list: qperm maps to the index position
         const int64_t bpos = (MODE == M_BORDER && a.qperm) ? (active ? (int64_t)a.qperm[sp] : 0) : sp;
         if (MODE == M_BORDER) active = active && !a.core[bpos];
-        int32_t best = 0x7fffffff;   // M_BORDER: smallest original id of a core neighbour
+        int32_t best = 0x7fffffff;   // M_BORDER: smallest cluster number of a core neighbour
         int32_t uroot = -1;          // M_UNION: cached union-find root of this query
         if (MODE == M_UNION && active) uroot = uf_rep(a.parent, (int32_t)sp);
 #pragma unroll
@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
                                 const int i = __ffs(m) - 1;
                                 m &= m - 1;
                                 const int64_t j = c0 + gg * 4 + i;
-                                if (a.core[j]) best = min(best, a.perm[j]);
+                                if (a.core[j]) best = min(best, a.blab[j]);
                             }
                         }
                         em.c += __popc(m);
@@ -750,7 +750,7 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
                                     uf_unite(a.parent, (int32_t)sp, (int32_t)j);
                                     uroot = uf_rep(a.parent, (int32_t)sp);
                                 }
-                                if (MODE == M_BORDER && a.core[j]) best = min(best, a.perm[j]);
+                                if (MODE == M_BORDER && a.core[j]) best = min(best, a.blab[j]);
                             }
                         }
                     }

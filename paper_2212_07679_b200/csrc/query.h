@@ -75,7 +75,8 @@ struct PassArgs {
     // DBSCAN modes (sorted positions)
     const uint8_t *core;    // core flags
     int32_t *parent;        // union-find parents
-    int32_t *best;          // M_BORDER: smallest original id of a core neighbour (atomicMin)
+    int32_t *best;          // M_BORDER: smallest cluster number of a core neighbour (atomicMin)
+    const int32_t *blab = nullptr;   // M_BORDER: cluster number of each sorted position (core points)
     int32_t min_pts;        // M_COUNT: counts are only needed up to min_pts (early exit)
     int64_t n_index = 0;    // M_UNION: number of index points (parent array length)
     // symmetric self-query (each unordered pair evaluated once): the scan keeps only

@@ -14,7 +14,8 @@ for s in $STAGES; do
     tests) timeout 1200 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.txt 2>&1; echo "pytest rc=$?"; tail -3 $OUT/pytest_gpu.txt ;;
     smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.txt 2>&1; echo "smoke rc=$?"; tail -2 $OUT/smoke.txt ;;
     bench) timeout 600 python bench.py > $OUT/bench_c2.jsonl 2> $OUT/bench_c2.err; echo "bench c2 rc=$?"
-           for c in c1 c3 c4 c5; do timeout 600 python bench.py --config $c --steps 10 --no-cpu-baseline > $OUT/bench_$c.jsonl 2> $OUT/bench_$c.err; echo "bench $c rc=$?"; done ;;
+           for c in c1 c3 c4 c5; do timeout 600 python bench.py --config $c --steps 10 > $OUT/bench_$c.jsonl 2> $OUT/bench_$c.err; echo "bench $c rc=$?"; done ;;
+    parity_full) rm -f $OUT/full_parity.jsonl; SNN_PARITY_RECORD=$OUT/full_parity.jsonl timeout 1200 python -m pytest tests/test_full_parity.py -m gpu -v > $OUT/pytest_full_parity.txt 2>&1; echo "parity_full rc=$?"; tail -8 $OUT/pytest_full_parity.txt ;;
     benchfast) for c in c2 c3 c4 c5; do timeout 600 python bench.py --config $c --steps 10 --no-cpu-baseline > $OUT/bench_$c.jsonl 2> $OUT/bench_$c.err; echo "bench $c rc=$?"; done ;;
     reference) timeout 600 python bench.py --impl reference --steps 3 > $OUT/bench_reference.jsonl 2> $OUT/bench_reference.err; echo "reference rc=$?" ;;
     ncu_launch) for c in c2 c3 c4 c5; do
@@ -24,6 +25,10 @@ for s in $STAGES; do
         case $c in c2|c5) K='regex:window_lowd';; *) K='regex:tc_window';; esac
         CMD="python bench.py --config $c --steps 1 --warmup 3 --no-cpu-baseline"
         $CMD > $OUT/plainf_$c.log 2>&1 && timeout 1200 ncu --set full --clock-control none --import-source on -k $K -s 6 -c 2 -o $OUT/full_$c $CMD > $OUT/ncu_full_$c.log 2>&1; echo "ncu full $c rc=$?" ;;
+    ncu_dbscan_c5)
+        CMD="python bench.py --config c5 --steps 1 --warmup 3 --no-cpu-baseline"
+        $CMD > $OUT/plaind_c5.log 2>&1 && timeout 1200 ncu --set full --clock-control none --import-source on -k regex:core_count -s 3 -c 1 -o $OUT/core_c5 $CMD > $OUT/ncu_core_c5.log 2>&1; echo "ncu core c5 rc=$?"
+        timeout 1200 ncu --set full --clock-control none --import-source on -k regex:window_lowd -s 6 -c 1 -o $OUT/union_c5 $CMD > $OUT/ncu_union_c5.log 2>&1; echo "ncu union c5 rc=$?" ;;
     ncu_gram_c4)
         CMD="python bench.py --config c4 --steps 1 --warmup 3 --no-cpu-baseline"
         $CMD > $OUT/plaing_c4.log 2>&1 && timeout 1200 ncu --set full --clock-control none --import-source on -k regex:gram_tc -s 3 -c 1 -o $OUT/gram_c4 $CMD > $OUT/ncu_gram_c4.log 2>&1; echo "ncu gram c4 rc=$?" ;;

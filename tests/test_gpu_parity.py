@@ -330,6 +330,22 @@ def test_dbscan_spec_examples_gpu(snn):
     assert K == 1 and (lab == 0).all()
 
 
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_dbscan_border_rule_gpu(snn, dt):
+    """Border point within eps of cores of two clusters: it joins the first cluster the
+    ascending-id FIFO scan reaches it with (cluster 0), not the cluster of its smallest-id
+    core neighbour (tests/test_oracle.py hand example); both the d <= 8 pipeline and the
+    CSR pipeline (d = 9: same points padded with zero coordinates)."""
+    x = {0: 0.0, 7: 0.3, 8: 0.6, 9: 1.0, 1: 3.0, 2: 3.3, 3: 3.6, 4: 4.0, 5: 2.0, 6: 50.0}
+    P = np.array([[x[i], 0.0] for i in range(10)], dtype=dt)
+    lab, K = _gpu_dbscan(snn, P, 1.05, 4)
+    assert K == 2 and lab.tolist() == [0, 1, 1, 1, 1, 0, -1, 0, 0, 0]
+    P9 = np.zeros((10, 9), dtype=dt)
+    P9[:, 0] = P[:, 0]
+    lab, K = _gpu_dbscan(snn, P9, 1.05, 4)
+    assert K == 2 and lab.tolist() == [0, 1, 1, 1, 1, 0, -1, 0, 0, 0]
+
+
 @pytest.mark.parametrize("n,seed,box,eps,mp,dt", [(20000, 4, 1000.0, 3.0, 5, np.float32),
                                                   (15000, 7, 300.0, 3.0, 5, np.float32),
                                                   (8000, 9, 200.0, 2.5, 4, np.float64),
@@ -381,7 +397,7 @@ def test_dbscan_c5_full_size_sampled(snn):
         else:
             allc = oracle.neighbour_counts(w.X, w.R, nb) >= w.dbscan_min_pts
             core_nb = nb[allc]
-            expect = lab[core_nb.min()] if len(core_nb) else -1
+            expect = lab[core_nb].min() if len(core_nb) else -1   # first cluster reaching it
             assert lab[i] == expect
 
 

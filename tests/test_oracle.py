@@ -341,12 +341,112 @@ def test_dbscan_vs_scipy_csgraph(seed):
     for i in cid:                      # canonical numbering by min core id
         order.setdefault(comp[i], len(order))
         ref[i] = order[comp[i]]
-    for i in np.nonzero(~core)[0]:
-        cn = [j for j in nb[i] if core[j]]
+    for i in np.nonzero(~core)[0]:     # border: first cluster the ascending FIFO scan reaches it with
+        cn = [ref[j] for j in nb[i] if core[j]]
         if cn:
-            ref[i] = ref[min(cn)]
+            ref[i] = min(cn)
     assert K == len(order)
     assert (ref == lab).all()
+    lg, Kg, cg = oracle.dbscan(P, eps, mp, grid=True)
+    assert Kg == K and np.array_equal(lg, lab) and np.array_equal(cg, cnt)
+
+
+def test_dbscan_border_goes_to_first_cluster_reaching_it():
+    """Hand example for the border rule (reading C18): cluster A = ids
+    {0, 7, 8, 9} (min core id 0 -> cluster 0), cluster B = ids {1, 2, 3, 4} (cluster 1);
+    border id 5 at x = 2 is within eps of A's core 9 (x = 1) and B's core 1 (x = 3).  The
+    ascending-id FIFO scan expands A first and labels 5 with A (cluster 0), although its
+    smallest-id core neighbour (1) is in B.  scikit-learn's DBSCAN (the implementation the
+    paper plugs SNN into) gives the same labels."""
+    x = {0: 0.0, 7: 0.3, 8: 0.6, 9: 1.0, 1: 3.0, 2: 3.3, 3: 3.6, 4: 4.0, 5: 2.0, 6: 50.0}
+    P = np.array([[x[i]] for i in range(10)])
+    lab, K, cnt = oracle.dbscan(P, 1.05, 4)
+    assert cnt.tolist() == [4, 5, 4, 4, 4, 3, 1, 4, 4, 5]
+    assert K == 2
+    assert lab.tolist() == [0, 1, 1, 1, 1, 0, -1, 0, 0, 0]
+    lg, Kg, _ = oracle.dbscan(P, 1.05, 4, grid=True)
+    assert Kg == 2 and lg.tolist() == lab.tolist()
+    from sklearn.cluster import DBSCAN
+    sk = DBSCAN(eps=1.05, min_samples=4, algorithm="brute").fit(P).labels_
+    assert sk.tolist() == lab.tolist()
+
+
+@pytest.mark.parametrize("seed,n,box,eps,mp", [(5, 2500, 120.0, 3.0, 5), (6, 2000, 60.0, 2.0, 8),
+                                                 (7, 3000, 300.0, 4.0, 3)])
+def test_dbscan_matches_scikit_learn(seed, n, box, eps, mp):
+    """scikit-learn's DBSCAN (brute-force neighbourhoods, PAPER.md:594 compares against it)
+    on C5-recipe data: labels equal element by element, brute-force and grid oracle alike.
+    Instances with a pair within 1e-9 of eps are rejected (sklearn computes distances by
+    another formula)."""
+    from scipy.spatial import cKDTree
+    from sklearn.cluster import DBSCAN
+    P = workloads.c5(n=n, seed=seed, box=box).X.astype(np.float64)
+    pairs = cKDTree(P).query_pairs(eps * (1 + 1e-9), output_type="ndarray")
+    dd = np.linalg.norm(P[pairs[:, 0]] - P[pairs[:, 1]], axis=1)
+    assert not np.any(np.abs(dd - eps) < 1e-9 * eps)
+    sk = DBSCAN(eps=eps, min_samples=mp, algorithm="brute").fit(P).labels_
+    lab, K, _ = oracle.dbscan(P, eps, mp)
+    assert np.array_equal(sk, lab) and K == sk.max() + 1 and K >= 2
+    lg, Kg, _ = oracle.dbscan(P, eps, mp, grid=True)
+    assert np.array_equal(lg, lab) and Kg == K
+
+
+def test_neighbour_counts_pins():
+    """oracle.neighbour_counts (DBSCAN's eps-neighbourhood sizes, self included): the hand
+    chain's counts, the brute-force radius query's row lengths and scipy cKDTree's ball
+    counts agree on sampled ids."""
+    P = np.array([[10.0], [0.0], [1.0], [2.0], [3.0], [4.0], [50.0], [11.0], [12.0]])
+    assert oracle.neighbour_counts(P, 1.0, np.arange(9)).tolist() == [2, 2, 3, 3, 3, 2, 1, 3, 2]
+    assert oracle.neighbour_counts(P, 1.0, [6, 2, 2]).tolist() == [1, 3, 3]
+    from scipy.spatial import cKDTree
+    w = workloads.c5(n=6000, seed=12, box=150.0)
+    ids = np.random.default_rng(3).choice(w.n, 300, replace=False)
+    cnt = oracle.neighbour_counts(w.X, 3.0, ids)
+    res = oracle.radius_query(w.X, w.X[ids], 3.0, band_rel=0.0)
+    assert np.array_equal(cnt, np.diff(res["offsets"]))
+    P64 = w.X.astype(np.float64)
+    ball = cKDTree(P64).query_ball_point(P64[ids], 3.0)
+    pairs = cKDTree(P64).query_pairs(3.0 * (1 + 1e-9), output_type="ndarray")
+    dd = np.linalg.norm(P64[pairs[:, 0]] - P64[pairs[:, 1]], axis=1)
+    assert not np.any(np.abs(dd - 3.0) < 1e-9 * 3.0)
+    assert cnt.tolist() == [len(b) for b in ball]
+    assert cnt.min() >= 1                     # self included
+
+
+# --------------------------------------------------------------------------- grid oracle (d <= 3)
+def _same_csr(a, b):
+    assert np.array_equal(a["offsets"], b["offsets"])
+    assert np.array_equal(a["indices"], b["indices"])
+    assert np.array_equal(a["s"], b["s"])
+
+
+@pytest.mark.parametrize("d,seed,n,m,R", [(1, 0, 3000, 500, 0.002), (2, 1, 4000, 700, 0.03),
+                                          (3, 2, 5000, 900, 0.08), (3, 3, 2000, 2000, 0.5),
+                                          (2, 4, 3000, 300, 2.5)])
+def test_grid_radius_query_equals_brute_force(d, seed, n, m, R):
+    """Grid-pruned oracle (d <= 3) == brute force, row by row (ids, fp64 s, band pairs),
+    random data plus queries outside the data's box."""
+    rng = np.random.default_rng(seed)
+    P = rng.random((n, d)).astype(np.float32)
+    Q = (rng.random((m, d)) * 1.2 - 0.1).astype(np.float32)
+    _same_csr(oracle.radius_query(P, Q, R, grid=True), oracle.radius_query(P, Q, R))
+    _same_csr(oracle.radius_query(P, P, R, grid=True), oracle.radius_query(P, P, R))
+
+
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_grid_radius_query_lattice_boundaries_duplicates(d):
+    """Integer lattice: many pairs at exactly R (3-4-5 and axis pairs) and points exactly on
+    cell boundaries; duplicates; R = 0 (coincidences only); a far outlier that makes the
+    extent/R ratio exceed 2^20 (cell side grows)."""
+    g = np.stack(np.meshgrid(*[np.arange(12.0)] * d, indexing="ij"), -1).reshape(-1, d)
+    base = np.concatenate([g * 5.0, g[:50] * 5.0])
+    for P in (base, np.concatenate([base, np.full((1, d), 1e8)])):
+        for R in (5.0, 25.0, 0.0, 7.0710678118654755):
+            _same_csr(oracle.radius_query(P, P, R, grid=True), oracle.radius_query(P, P, R))
+    P = base
+    Q = g[::7] * 5.0 + 2.5
+    _same_csr(oracle.radius_query(P, Q, 2.5 * np.sqrt(d), grid=True),
+              oracle.radius_query(P, Q, 2.5 * np.sqrt(d)))
 
 
 # ---------------------------------------------------------------- metrics (PAPER.md:57-72)
