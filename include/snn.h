@@ -20,8 +20,11 @@
  *  - Errors: a non-OK status is returned and snn_last_error() gives a thread-local
  *    message.  Output handles are left NULL on error.  Nothing is leaked on error.
  *  - Index ids are 0-based original row numbers of X; n must be < 2^30.
- *  - Thread safety: an index is immutable after snn_build; concurrent queries on one
- *    index (different streams / threads) are allowed; snn_free must not race a query.
+ *  - Thread safety: an index is immutable after snn_build; concurrent queries and DBSCAN
+ *    runs on one index (different streams / threads) are allowed, each
+ *    with its own workspace; snn_append / snn_free must not race a query.  Options
+ *    (snn_set_option) and the last-query diagnostics are per thread; the profiler
+ *    (snn_profile_*) is process-wide.
  */
 #ifndef SNN_H
 #define SNN_H
@@ -244,7 +247,9 @@ uint64_t snn_launch_count(void);
 snn_status snn_profile_enable(int on);
 snn_status snn_profile_read(const char *family, double *ms, uint64_t *launches, double *units);
 
-/* Test / tuning hooks (process-global; not thread-safe; 0 restores the default):
+/* Test / tuning hooks.  Options are PER CALLING THREAD: snn_set_option changes the options
+ * of the calls this thread makes (every thread starts from the defaults), so concurrent
+ * callers never switch each other's paths.  0 restores the default:
  *   "force_generic"  1 = use the generic-d FFMA tile kernel even for d <= 16
  *   "query_block"    queries per block for the low-d kernel (32..256, multiple of 32)
  *   "chunk"          candidates per work item (multiple of 64)
@@ -261,6 +266,10 @@ snn_status snn_profile_read(const char *family, double *ms, uint64_t *launches, 
  *   "balanced_compact" -1 = per-entry compaction threads (default for symmetric self-queries:
  *                    one slot record per thread after CTA scans)
  *   "window_all"     1 = brute-force ablation: every query scans all n candidates
+ *   "finalize_order" -1 = row assembly walks rows in key order (default: original-id order,
+ *                    sequential CSR writes)
+ *   "union_load"     DBSCAN union pass: how the parent[j] pre-check is loaded (0 volatile,
+ *                    1 ld.relaxed.gpu, 2 ld.global.cg; every value is a valid filter)
  *   "simt_filter"    low-d fp32 expanded-form pre-filter: default on for radius queries and
  *                    off for DBSCAN; 1 = on everywhere, -1 = off everywhere
  *   "lowd_tc", "lowd_tc_tiles", "lowd_tc_group"   low-d tcgen05 path (default off)
@@ -269,6 +278,8 @@ snn_status snn_profile_read(const char *family, double *ms, uint64_t *launches, 
  * "force_generic" is read by snn_build (it fixes the sorted copy's layout).
  * Returns SNN_ERR_INVALID_ARGUMENT for an unknown key or bad value. */
 snn_status snn_set_option(const char *key, int64_t value);
+/* The calling thread's current value of an option (same keys as snn_set_option). */
+snn_status snn_get_option(const char *key, int64_t *value);
 
 #ifdef __cplusplus
 }

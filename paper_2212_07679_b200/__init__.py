@@ -33,7 +33,7 @@ STATUS = {0: "SNN_OK", 1: "SNN_ERR_INVALID_ARGUMENT", 2: "SNN_ERR_EMPTY",
 EXPORTS = ["snn_build", "snn_build_metric", "snn_append", "snn_save", "snn_load",
            "snn_query_radius_part", "snn_query_self_part", "snn_index_sigma", "snn_query_radius", "snn_query_self", "snn_result_csr",
            "snn_result_copy", "snn_result_free", "snn_dbscan", "snn_free", "snn_last_error",
-           "snn_index_info", "snn_launch_count", "snn_set_option", "snn_profile_enable",
+           "snn_index_info", "snn_launch_count", "snn_set_option", "snn_get_option", "snn_profile_enable",
            "snn_profile_read"]
 
 
@@ -95,6 +95,7 @@ def load_library(path: str = LIB_PATH):
         "snn_index_sigma": ([P, i32, P, P], ctypes.c_int),
         "snn_launch_count": ([], ctypes.c_uint64),
         "snn_set_option": ([ctypes.c_char_p, i64], ctypes.c_int),
+        "snn_get_option": ([ctypes.c_char_p, ctypes.c_void_p], ctypes.c_int),
         "snn_profile_enable": ([ctypes.c_int], ctypes.c_int),
         "snn_profile_read": ([ctypes.c_char_p, ctypes.POINTER(f64), ctypes.POINTER(ctypes.c_uint64),
                               ctypes.POINTER(f64)], ctypes.c_int),
@@ -157,6 +158,12 @@ def snn_launch_count() -> int:
 
 def snn_set_option(key: str, value: int) -> None:
     _check(load_library().snn_set_option(key.encode(), int(value)))
+
+
+def snn_get_option(key: str) -> int:
+    v = ctypes.c_int64(0)
+    _check(load_library().snn_get_option(key.encode(), ctypes.addressof(v)))
+    return int(v.value)
 
 
 def snn_profile_enable(on: bool) -> None:

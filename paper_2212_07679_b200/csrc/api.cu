@@ -49,9 +49,14 @@ struct Options {
     int lowd_tc = 0;     // low-d (fp32, d <= 8) radius queries through the tensor-core filter (option; FFMA default)
     int lowd_tc_tiles = 8;     // 256-candidate tiles per work item (low-d tensor-core path)
     int lowd_tc_group = 8;     // query blocks per raster group (low-d tensor-core path)
+    int union_load = 0;        // DBSCAN union pass: parent pre-check load (0 volatile, 1 relaxed.gpu, 2 ld.cg)
+    int finalize_order = 1;    // staged rows: rows_finalize walks rows in original-id order (sequential CSR writes)
 };
-static std::atomic<int64_t> g_last_ovf{0}, g_last_lost{0};
-static Options g_opt;
+// Options are per calling thread (snn_set_option changes only the calling thread's calls;
+// every thread starts from the defaults above), so concurrent callers cannot switch each
+// other's paths.  The last-query diagnostics are per thread for the same reason.
+static thread_local int64_t g_last_ovf = 0, g_last_lost = 0;
+static thread_local Options g_opt;
 
 static thread_local std::string t_err;
 
@@ -106,6 +111,7 @@ static void prof_drain() {
 }
 
 bool dbscan_simt_filter() { return g_opt.simt_filter > 0; }
+int dbscan_union_load() { return g_opt.union_load; }
 
 snn_status fail(snn_status st, const std::string &msg) {
     t_err = msg;
@@ -174,9 +180,10 @@ struct Pinned {
 static thread_local Pinned t_pinned;
 
 // row stride of the sorted copy: 0 = AoSoA4 layout (low-d kernels), else padded row-major
+int generic_stride(int d) { return d == 1 ? 1 : d == 2 ? 2 : (int)round_up(d, 4); }
 int row_stride(int d) {
     if (lowd_supported(d) && !g_opt.force_generic) return 0;
-    return d == 1 ? 1 : d == 2 ? 2 : (int)round_up(d, 4);
+    return generic_stride(d);
 }
 int64_t row_elems(int d, int ld) { return ld ? ld : d; }
 
@@ -222,6 +229,27 @@ static void free_index(snn_index idx) {
     delete idx;
 }
 
+// Padding rows [n, n_pad) as the build writes them: NaN coordinates (zero stride padding),
+// NaN half norms, filter rows x_c = 0 with xbar' = +inf (build.cu gather_*, query.cu
+// filter_rows_kernel).
+template <typename T>
+__global__ void restore_sentinels(T *Xs, int ld, int D, int64_t n, int64_t n_pad, float *xbar, float *Xf) {
+    for (int64_t t = threadIdx.x; t < (n_pad - n) * (ld ? ld : D); t += blockDim.x) {
+        const int64_t i = n + t / (ld ? ld : D);
+        const int k = (int)(t % (ld ? ld : D));
+        if (ld) Xs[i * ld + k] = k < D ? (T)NAN : (T)0;
+        else Xs[(i >> 2) * 4 * D + 4 * k + (i & 3)] = (T)NAN;
+    }
+    for (int64_t i = n + threadIdx.x; i < n_pad; i += blockDim.x) {
+        xbar[i] = NAN;
+        if (Xf) {
+            float *o = Xf + (i >> 2) * 4 * (D + 1) + (i & 3);
+            for (int k = 0; k < D; ++k) o[4 * k] = 0.f;
+            o[4 * D] = INFINITY;
+        }
+    }
+}
+
 extern "C" {
 
 snn_status snn_profile_enable(int on) {
@@ -238,13 +266,13 @@ snn_status snn_profile_read(const char *family, double *ms, uint64_t *launches, 
     if (strcmp(family, "overflow") == 0) {   // hit-slot overflows of the last low-d query
         if (ms) *ms = 0.0;
         if (launches) *launches = 0;
-        if (units) *units = (double)g_last_ovf.load();
+        if (units) *units = (double)g_last_ovf;
         return SNN_OK;
     }
     if (strcmp(family, "lost") == 0) {   // items re-run by the fix pass in the last query
         if (ms) *ms = 0.0;
         if (launches) *launches = 0;
-        if (units) *units = (double)g_last_lost.load();
+        if (units) *units = (double)g_last_lost;
         return SNN_OK;
     }
     for (int f = 0; f < F_N; ++f) {
@@ -260,6 +288,26 @@ snn_status snn_profile_read(const char *family, double *ms, uint64_t *launches, 
 
 const char *snn_last_error(void) { return t_err.c_str(); }
 uint64_t snn_launch_count(void) { return g_launches.load(); }
+
+snn_status snn_get_option(const char *key, int64_t *value) {
+    if (!key || !value) return fail(SNN_ERR_INVALID_ARGUMENT, "NULL argument");
+    static const struct { const char *name; int Options::*field; } kInt[] = {
+        {"force_generic", &Options::force_generic}, {"query_block", &Options::query_block},
+        {"chunk", &Options::chunk}, {"power_iters", &Options::power_iters}, {"cap", &Options::cap},
+        {"variant", &Options::variant}, {"tc", &Options::tc}, {"tc_min_d", &Options::tc_min_d},
+        {"tc_tiles", &Options::tc_tiles}, {"tc_diag", &Options::tc_diag}, {"tc_f16", &Options::tc_f16},
+        {"tc_ares", &Options::tc_ares}, {"tc_group", &Options::tc_group},
+        {"tc_gram_min_d", &Options::tc_gram_min_d}, {"symmetric", &Options::symmetric},
+        {"stage_rows", &Options::stage_rows}, {"balanced_compact", &Options::balanced_compact},
+        {"window_all", &Options::window_all}, {"simt_filter", &Options::simt_filter},
+        {"lowd_tc", &Options::lowd_tc}, {"lowd_tc_tiles", &Options::lowd_tc_tiles},
+        {"lowd_tc_group", &Options::lowd_tc_group}, {"union_load", &Options::union_load},
+        {"finalize_order", &Options::finalize_order}};
+    for (const auto &o : kInt)
+        if (strcmp(key, o.name) == 0) { *value = g_opt.*(o.field); return SNN_OK; }
+    if (strcmp(key, "ovf_records") == 0) { *value = g_opt.ovf_rec_cap; return SNN_OK; }
+    return fail(SNN_ERR_INVALID_ARGUMENT, std::string("unknown option ") + key);
+}
 
 snn_status snn_set_option(const char *key, int64_t value) {
     if (!key) return fail(SNN_ERR_INVALID_ARGUMENT, "NULL option key");
@@ -326,6 +374,12 @@ snn_status snn_set_option(const char *key, int64_t value) {
         return SNN_OK;
     }
     if (k == "tc_ares") { g_opt.tc_ares = value < 0 ? 0 : 1; return SNN_OK; }
+    if (k == "finalize_order") { g_opt.finalize_order = value < 0 ? 0 : 1; return SNN_OK; }
+    if (k == "union_load") {
+        if (value < 0 || value > 2) return fail(SNN_ERR_INVALID_ARGUMENT, "union_load must be 0..2");
+        g_opt.union_load = (int)value;
+        return SNN_OK;
+    }
     if (k == "tc_f16") { g_opt.tc_f16 = value < 0 ? 0 : 1; return SNN_OK; }
     if (k == "tc_group") {
         if (value == 0) value = 128;
@@ -711,9 +765,11 @@ static snn_status query_tc(snn_index idx, Workspace &ws, cudaStream_t s, int sms
     int64_t cap = g_opt.ovf_rec_cap > 0 ? (int64_t)64 * m : 0;
     if (cap < (int64_t(1) << 22)) cap = int64_t(1) << 22;
     int32_t *pq = nullptr, *pj = nullptr;
-    for (int attempt = 0; attempt < 2; ++attempt) {
+    int64_t np = 0, used_cap = 0;
+    for (int attempt = 0; attempt < 3; ++attempt) {
         CK(ws.alloc(&pq, (size_t)cap), "alloc pairs");
         CK(ws.alloc(&pj, (size_t)cap), "alloc pairs");
+        used_cap = cap;
         t.pair_q = pq; t.pair_j = pj; t.pair_count = pcount; t.pair_cap = cap;
         CK(cudaMemsetAsync(pcount, 0, 8, s), "memset");
         const int ctok = prof_begin(F_COUNT, s);
@@ -721,12 +777,15 @@ static snn_status query_tc(snn_index idx, Workspace &ws, cudaStream_t s, int sms
         prof_end(ctok, s, pairs_eval);
         CK(cudaMemcpyAsync(hp, pcount, 8, cudaMemcpyDeviceToHost, s), "D2H pair count");
         CK(cudaStreamSynchronize(s), "tc filter");
-        const int64_t np = (int64_t)*reinterpret_cast<unsigned long long *>(hp);
-        if (np <= cap) { cap = np; break; }
-        // re-run once with room for the count plus every warp's partially used block
+        np = (int64_t)*reinterpret_cast<unsigned long long *>(hp);
+        if (np <= used_cap) break;
+        // re-run with room for the count plus every warp's partially used block
         cap = np + (int64_t)sms * tc_claim_slack();
     }
-    const int64_t P = cap;
+    // the claim count is deterministic (items map statically to CTAs), so the first re-run
+    // fits; never read past the buffers if it did not
+    if (np > used_cap) return fail(SNN_ERR_OUT_OF_MEMORY, "tensor-core pair list still overflowed after re-runs");
+    const int64_t P = np;
     const int wtok = prof_begin(F_WRITE, s);
     uint32_t *flag;
     float *dist;
@@ -876,8 +935,8 @@ static snn_status query_tcl(snn_index idx, Workspace &ws, cudaStream_t s, int sm
     if (ce != cudaSuccess) { delete r; return cuda_fail(ce, "alloc offsets"); }
     r->offsets = static_cast<int64_t *>(pm);
     exclusive_scan_i32_to_i64(row_count, r->offsets, m, scan_tmp, s);
-    CK(cudaMemcpyAsync(hp, r->offsets + m, 8, cudaMemcpyDeviceToHost, s), "D2H nnz");
-    if ((ce = cudaStreamSynchronize(s)) != cudaSuccess) { snn_result_free(r); return cuda_fail(ce, "exact"); }
+    if ((ce = cudaMemcpyAsync(hp, r->offsets + m, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+        (ce = cudaStreamSynchronize(s)) != cudaSuccess) { snn_result_free(r); return cuda_fail(ce, "exact"); }
     const int64_t H = hp[0];
     r->nnz = H;
     if ((ce = cudaMallocAsync(&pm, (size_t)(H > 0 ? H : 1) * 4, s)) != cudaSuccess) { snn_result_free(r); return cuda_fail(ce, "alloc"); }
@@ -1037,6 +1096,11 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
     snn_result r = new snn_result_s();
     r->m = m;
     auto bail = [&](cudaError_t e, const char *where) { snn_result_free(r); return cuda_fail(e, where); };
+#define CKR(expr, where)                          \
+    do {                                          \
+        cudaError_t _e = (expr);                  \
+        if (_e != cudaSuccess) return bail(_e, where); \
+    } while (0)
     {
         void *p = nullptr;
         cudaError_t e = cudaMallocAsync(&p, (size_t)(m + 1) * 8, s);
@@ -1049,7 +1113,7 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
     a.blk_lo = blk_lo_s; a.blk_hi = blk_hi; a.item_start = item_start;
     if (total_items > 0 && total_items < (int64_t(1) << 31)) {
         int32_t *ib = nullptr;
-        CK(ws.alloc(&ib, (size_t)total_items), "alloc item blocks");
+        CKR(ws.alloc(&ib, (size_t)total_items), "alloc item blocks");
         launch_item_blocks(item_start, nblocks, ib, s);
         a.item_block = ib;
     }
@@ -1061,23 +1125,23 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
     int32_t *srow = nullptr;
     int64_t *soff = nullptr;
     if (stage) {
-        CK(ws.alloc(&srow, (size_t)m), "alloc");
-        CK(ws.alloc(&soff, (size_t)m + 1), "alloc");
+        CKR(ws.alloc(&srow, (size_t)m), "alloc");
+        CKR(ws.alloc(&soff, (size_t)m + 1), "alloc");
     }
     if (sym) {
         a.sym = 1;
-        CK(ws.alloc(&a.lcnt, (size_t)m), "alloc");
-        CK(ws.alloc(&a.lpos, (size_t)m), "alloc");
-        CK(ws.alloc(&maxl, 1), "alloc");
-        CK(cudaMemsetAsync(a.lcnt, 0, (size_t)m * 4, s), "memset");
-        CK(cudaMemsetAsync(maxl, 0, 4, s), "memset");
+        CKR(ws.alloc(&a.lcnt, (size_t)m), "alloc");
+        CKR(ws.alloc(&a.lpos, (size_t)m), "alloc");
+        CKR(ws.alloc(&maxl, 1), "alloc");
+        CKR(cudaMemsetAsync(a.lcnt, 0, (size_t)m * 4, s), "memset");
+        CKR(cudaMemsetAsync(maxl, 0, 4, s), "memset");
     }
     thresholds(a.R2, D, &a.T_in, &a.T_out);
     a.cnt = cnt; a.pre = pre; a.slots = slots; a.cap = cap;
     // balanced compaction: measured faster for symmetric self-queries (1.22 -> 1.09 ms on
     // config 2), slower for two-sided ones (0.92 -> 1.04 ms)
     if (!generic && sym && g_opt.balanced_compact && B == 256) {   // record counts per entry
-        CK(ws.alloc(&a.nrec, (size_t)total_items * B), "alloc record counts");
+        CKR(ws.alloc(&a.nrec, (size_t)total_items * B), "alloc record counts");
     }
     a.ovf_items = ovf; a.ovf_count = ovf ? ovf + total_items : nullptr; a.n_ovf = 0;
     a.ovf_rec = ovf_rec; a.ovf_rec_count = ovf ? ovf + total_items + 1 : nullptr;
@@ -1120,6 +1184,7 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
     if (sym && max_l > 16384) {   // a huge mirrored row: redo unsymmetric
         snn_result_free(r);
         prof_end(qtok, s, 0.0);
+        ws.free_all();   // the slots and counts of this attempt: do not hold them across the re-run
         return query_impl(idx, Q, m, d, dt, R, stream, out, false);
     }
     a.n_ovf = a.ovf_count ? reinterpret_cast<int32_t *>(hp + 1)[0] : 0;
@@ -1134,10 +1199,17 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
         r->distances = static_cast<float *>(p);
     }
     a.out_idx = r->indices; a.out_dist = r->distances;
-    if (stage)   // the compaction and fix passes assemble rows in key order here
-        CK(ws.alloc(&a.stage, (size_t)(r->nnz > 0 ? r->nnz : 1)), "alloc staged rows");
+    if (stage) {   // the compaction and fix passes assemble rows in key order here
+        CKR(ws.alloc(&a.stage, (size_t)(r->nnz > 0 ? r->nnz : 1)), "alloc staged rows");
+        if (g_opt.finalize_order) {   // finalize walks the rows in original-id order
+            int32_t *qinv = nullptr;
+            CKR(ws.alloc(&qinv, (size_t)m), "alloc inverse permutation");
+            launch_invert_perm(qperm, m, qinv, s);
+            a.qinv = qinv;
+        }
+    }
     if (sym) {
-        CK(ws.alloc(&a.tmpL, (size_t)(r->nnz > 0 ? r->nnz : 1)), "alloc mirrored entries");
+        CKR(ws.alloc(&a.tmpL, (size_t)(r->nnz > 0 ? r->nnz : 1)), "alloc mirrored entries");
         launch_sym_lpos_init(a, s);
     }
     if (r->nnz > 0) {
@@ -1160,6 +1232,7 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
     if (e != cudaSuccess) return bail(e, "query");
     *out = r;
     return SNN_OK;
+#undef CKR
 }
 
 snn_status snn_build(const void *X, int64_t n, int32_t d, snn_dtype dt, void *stream, snn_index *out) {
@@ -1470,11 +1543,18 @@ snn_status snn_append(snn_index idx, const void *Y, int64_t k, int32_t d, snn_dt
     radix_sort_pairs(keys_raw, nullptr, keys1, src, n1, sort_tmp, s);                            // K4
     launch_append_perm(src, n0, n1, idx->perm, perm1, s);
     launch_gather(S, f64, n1, D, ld, np1, src, idx->mu_d, Xs1, xbar1, s);                        // K5
-    launch_key_bounds(D, maxabs, idx->mu_d, idx->mu_f, idx->v_d, idx->v_f, idx->stats, s);
+    // grown-data key bounds into a fresh stats block: committed with the other arrays below,
+    // so a failure leaves the index exactly as it was
+    double *stats1 = nullptr;
+    if ((e = grab((void **)&stats1, (size_t)(ST_COUNT + 2) * 8)) != cudaSuccess) return bail(e, "alloc stats");
+    if ((e = cudaMemcpyAsync(stats1, idx->stats, (size_t)(ST_COUNT + 2) * 8, cudaMemcpyDeviceToDevice, s)) != cudaSuccess)
+        return bail(e, "copy stats");
+    launch_key_bounds(D, maxabs, idx->mu_d, idx->mu_f, idx->v_d, idx->v_f, stats1, s);
     double *hs = static_cast<double *>(t_pinned.p);
-    if ((e = cudaMemcpyAsync(hs, idx->stats, ST_COUNT * 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return bail(e, "D2H");
+    double h_stats1[ST_COUNT];
+    if ((e = cudaMemcpyAsync(hs, stats1, ST_COUNT * 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return bail(e, "D2H");
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return bail(e, "append");
-    memcpy(idx->h_stats, hs, sizeof(idx->h_stats));
+    memcpy(h_stats1, hs, sizeof(h_stats1));
     if (idx->Xf) {
         if ((e = grab((void **)&Xf1, (size_t)np1 * (D + 1) * 4)) != cudaSuccess) return bail(e, "alloc filter rows");
         launch_filter_rows(static_cast<const float *>(Xs1), D, n1, np1, idx->mu_f, idx->xf_c1h, Xf1, s);
@@ -1482,7 +1562,7 @@ snn_status snn_append(snn_index idx, const void *Y, int64_t k, int32_t d, snn_dt
     int tc_f16 = idx->tc_f16, xexp = idx->xexp, kpad = idx->kpad;
     if (idx->tc) {
         int ex = 0;
-        tc_f16 = idx->tc_f16 && f16_exponent(idx->h_stats[ST_XCMAX], &ex);
+        tc_f16 = idx->tc_f16 && f16_exponent(h_stats1[ST_XCMAX], &ex);
         xexp = ex;
         kpad = tc_kpad(D, tc_f16);
         if ((e = grab(&Xt1, (size_t)n1 * kpad * (tc_f16 ? 2 : 4))) != cudaSuccess) return bail(e, "alloc operand copy");
@@ -1498,6 +1578,8 @@ snn_status snn_append(snn_index idx, const void *Y, int64_t k, int32_t d, snn_dt
                         cudaMemcpyDeviceToDevice, s);
     }
     if ((e = cudaGetLastError()) != cudaSuccess || (e = cudaStreamSynchronize(s)) != cudaSuccess) return bail(e, "append");
+    swap_owned(idx, idx->stats, stats1, s); idx->stats = stats1;
+    memcpy(idx->h_stats, h_stats1, sizeof(idx->h_stats));
     swap_owned(idx, idx->keys, keys1, s); idx->keys = keys1;
     swap_owned(idx, idx->perm, perm1, s); idx->perm = perm1;
     swap_owned(idx, idx->xbar, xbar1, s); idx->xbar = xbar1;
@@ -1599,7 +1681,8 @@ snn_status snn_load(const char *path, void *stream, snn_index *out) {
         n >= 1 && n < (int64_t(1) << 30) && tmpl.n_pad == round_up(n, 4) && D >= 1 && h[2] < (1 << 24) &&
         (h[4] == SNN_F32 || h[4] == SNN_F64) && h[5] >= SNN_METRIC_EUCLIDEAN && h[5] <= SNN_METRIC_MIPS &&
         tmpl.d_in == (tmpl.metric == SNN_METRIC_MIPS ? D - 1 : D) &&
-        (tmpl.ld == 0 ? lowd_supported(D) : (tmpl.ld >= D && tmpl.ld < D + 4)) &&
+        // the layouts build produces (the float4 / bulk loads rely on them)
+        (tmpl.ld == 0 ? lowd_supported(D) : tmpl.ld == generic_stride(D)) &&
         (!tmpl.tc || (tmpl.ld != 0 && tmpl.kpad == tc_kpad(D, tmpl.tc_f16 != 0))) &&
         (!has_xf || (tmpl.ld == 0 && tmpl.dt == SNN_F32)) &&
         (has_xo == (tmpl.metric == SNN_METRIC_MANHATTAN || tmpl.metric == SNN_METRIC_MIPS));
@@ -1651,7 +1734,14 @@ snn_status snn_load(const char *path, void *stream, snn_index *out) {
         if (e != cudaSuccess) { free_index(idx); return cuda_fail(e, "H2D"); }
         off += sec.bytes;
     }
-    cudaError_t e = cudaStreamSynchronize(s);   // `file` is pageable: copies complete before return
+    // the padding rows [n, n_pad) are sentinels the query kernels rely on (never hits, never
+    // compacted): rewrite them instead of trusting the file
+    if (idx->dt == SNN_F64)
+        SNN_LAUNCH(restore_sentinels<double>, 1, 128, 0, s, (double *)idx->Xs, idx->ld, D, n, idx->n_pad, idx->xbar, idx->Xf);
+    else
+        SNN_LAUNCH(restore_sentinels<float>, 1, 128, 0, s, (float *)idx->Xs, idx->ld, D, n, idx->n_pad, idx->xbar, idx->Xf);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);   // `file` is pageable: copies complete before return
     if (e != cudaSuccess) { free_index(idx); return cuda_fail(e, "load"); }
     *out = idx;
     return SNN_OK;

@@ -289,6 +289,7 @@ snn_status dbscan_impl(snn_index idx, double eps, int32_t min_pts, int32_t *labe
         CKD(cudaStreamSynchronize(s), "dbscan union windows");
         prof_end(ctok, s, (double)*reinterpret_cast<unsigned long long *>(hbuf + 2));   // pairs evaluated
         PassArgs au = a;
+        au.uload = dbscan_union_load();
         au.blk_lo = lo2; au.item_start = st2; au.total_items = hbuf[0];
         au.item_block = nullptr;
         if (au.total_items > 0 && au.total_items < (int64_t(1) << 31)) {

@@ -37,6 +37,10 @@ struct Workspace {
         *out = static_cast<T *>(p);
         return e;
     }
+    void free_all() {
+        for (void *p : ptrs) cudaFreeAsync(p, s);
+        ptrs.clear();
+    }
     void release(void *p) {   // hand ownership to the caller
         std::vector<void *> keep;
         for (void *q : ptrs) if (q != p) keep.push_back(q);
@@ -85,6 +89,7 @@ struct snn_result_s {
 
 namespace snn {
 bool dbscan_simt_filter();   // option simt_filter (api.cu)
+int dbscan_union_load();     // option union_load (api.cu)
 // metric adapters (metric.cu): exact row normalization (flag = 1 on a zero row), radius
 // mapping and in-place distance conversion
 void launch_normalize_rows(const void *X, bool f64, int64_t n, int d, void *out, int *zero_flag, cudaStream_t s);

@@ -276,6 +276,12 @@ __device__ __forceinline__ void group_d2(const float4 (&xv)[D], const uint64_t (
 //   M_BORDER DBSCAN: for non-core i, the smallest cluster number among core neighbours
 enum { M_SCAN = 0, M_FIX = 1, M_COUNT = 2, M_UNION = 3, M_BORDER = 4 };
 
+__device__ __forceinline__ int32_t ld_relaxed_gpu(const int32_t *p) {
+    int32_t v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
 // Lock-free union-find over sorted positions (parent[x] <= x: every link goes from the
 // larger root to the smaller, so chains decrease and path halving is race-benign).
 __device__ __forceinline__ int32_t uf_rep(volatile int32_t *p, int32_t x) {
@@ -429,7 +435,11 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
                                 m &= m - 1;
                                 const int64_t j = c0 + gg * 4 + i;
                                 if (j > sp) {   // parent < 0: not core; == root: already joined
-                                    const int32_t pj = reinterpret_cast<volatile int32_t *>(a.parent)[j];
+                                    // any value parent[j] ever held is a safe filter: links only
+                                    // merge components, so pj == uroot means j is already joined
+                                    const int32_t pj = a.uload == 0 ? reinterpret_cast<volatile int32_t *>(a.parent)[j]
+                                                     : a.uload == 1 ? ld_relaxed_gpu(a.parent + j)
+                                                                    : __ldcg(a.parent + j);
                                     if (pj >= 0 && pj != uroot) {
                                         uf_unite(a.parent, (int32_t)sp, (int32_t)j);
                                         uroot = uf_rep(a.parent, (int32_t)sp);
@@ -1095,11 +1105,15 @@ __global__ void __launch_bounds__(256) rows_finalize_warp(PassArgs a) {
     __shared__ unsigned long long sbuf[8][kLWarp];
     const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
     unsigned long long *buf = sbuf[w];
-    for (int64_t sp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; sp < a.m;
-         sp += (int64_t)gridDim.x * blockDim.x / 32) {
+    // staged rows with the inverse permutation: warps walk the OUTPUT rows in original-id
+    // order, so consecutive warps write consecutive CSR memory (whole sectors; random row
+    // writes leave partial sectors that HBM's ECC turns into read-modify-writes)
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; r < a.m;
+         r += (int64_t)gridDim.x * blockDim.x / 32) {
+        const int64_t sp = a.qinv ? (int64_t)a.qinv[r] : r;
         const int cnt = a.sym ? a.lcnt[sp] : 0;
         const int64_t src = a.soff ? a.soff[sp] : (int64_t)a.lpos[sp] - cnt;   // L cursor advanced by cnt
-        const int64_t dst = a.soff ? a.offsets[a.qperm[sp]] : src;
+        const int64_t dst = a.soff ? a.offsets[a.qinv ? r : a.qperm[sp]] : src;
         if (a.soff) {   // U part (after L and self) or the whole row
             const int64_t k0 = a.sym ? cnt + 1 : 0, len = a.soff[sp + 1] - src;
             for (int64_t k = k0 + lane; k < len; k += 32) {
@@ -1368,6 +1382,18 @@ void launch_sym_lpos_init(const PassArgs &a, cudaStream_t s) {
     int64_t g = ceil_div(a.m, 256);
     if (g > 148 * 16) g = 148 * 16;
     SNN_LAUNCH(sym_lpos_init, (int)g, 256, 0, s, a);
+}
+
+__global__ void invert_perm_kernel(const int32_t *perm, int64_t m, int32_t *inv) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        inv[perm[i]] = (int32_t)i;
+}
+
+void launch_invert_perm(const int32_t *perm, int64_t m, int32_t *inv, cudaStream_t s) {
+    if (m == 0) return;
+    int64_t g = ceil_div(m, 256);
+    if (g > 148 * 16) g = 148 * 16;
+    SNN_LAUNCH(invert_perm_kernel, (int)g, 256, 0, s, perm, m, inv);
 }
 
 void launch_rows_finalize(const PassArgs &a, int32_t max_l, cudaStream_t s) {

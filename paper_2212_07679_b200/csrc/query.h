@@ -79,6 +79,7 @@ struct PassArgs {
     const int32_t *blab = nullptr;   // M_BORDER: cluster number of each sorted position (core points)
     int32_t min_pts;        // M_COUNT: counts are only needed up to min_pts (early exit)
     int64_t n_index = 0;    // M_UNION: number of index points (parent array length)
+    int uload = 0;          // M_UNION pre-check load of parent[j]: 0 volatile, 1 ld.relaxed.gpu, 2 ld.cg
     // symmetric self-query (each unordered pair evaluated once): the scan keeps only
     // candidates j > i (U rows) and counts the mirrored hits per candidate; the mirrored
     // entries (L rows) are scattered during compaction and sorted per row afterwards
@@ -91,6 +92,7 @@ struct PassArgs {
     // each row whole to its original-id position offsets[qperm[sp]]
     const int64_t *soff = nullptr;
     unsigned long long *stage = nullptr;   // staged entries: (fp32 distance bits << 32 | id)
+    const int32_t *qinv = nullptr;         // inverse of qperm (original id -> key position): rows_finalize order
     // expanded-form SIMT filter (scan variant 3; nullptr = off): AoSoA4 rows with D+1
     // floats (centred coordinates, xbar c1h), the margin constants and mu_f
     const float *Xf = nullptr;
@@ -134,6 +136,7 @@ void launch_sym_lpos_init(const PassArgs &a, cudaStream_t s);
 // rows -> final CSR: symmetric self-query: sort every row's L segment by position, write it
 // and the self entry; staged rows: move every row to offsets[qperm[sp]]
 void launch_rows_finalize(const PassArgs &a, int32_t max_l, cudaStream_t s);
+void launch_invert_perm(const int32_t *perm, int64_t m, int32_t *inv, cudaStream_t s);
 // K11 helper: per-row totals over a block's items; pre = exclusive per-item prefixes
 // (pre may alias cnt); row_count[qperm[sp]] = total (qperm NULL: row_count[sp]).
 void launch_row_totals(const int32_t *cnt, int32_t *pre, const int64_t *item_start, int64_t m,

@@ -61,7 +61,7 @@ def radius(name: str):
         step = 1024
         for s0 in range(0, w.m, step):
             r = oracle.radius_query(w.X, Q[s0:s0 + step], w.R)
-            c, b = digest.oracle_csr_digests(r, step)
+            c, b = digest.oracle_csr_digests(r, step, row0=s0)
             cnts.append(c)
             rdig.append(b)   # one block per chunk (chunk == block)
             print(f"  {name}: {min(w.m, s0 + step)}/{w.m} queries, {time.time() - t0:.0f} s", flush=True)

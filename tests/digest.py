@@ -38,13 +38,13 @@ def _seg_sums(h: np.ndarray, offsets: np.ndarray) -> np.ndarray:
     return cs[offsets[1:]] - cs[offsets[:-1]]
 
 
-def csr_digests(offsets, indices, dist_f32, block: int = 1024):
+def csr_digests(offsets, indices, dist_f32, block: int = 1024, row0: int = 0):
     """(counts int64[m], block digests uint64[ceil(m/block)]) of a CSR result whose
-    distances are float32."""
+    distances are float32; its row j is query row0 + j of the whole result."""
     offsets = np.asarray(offsets, dtype=np.int64)
     m = len(offsets) - 1
     counts = np.diff(offsets)
-    rows = np.repeat(np.arange(m, dtype=np.uint64), counts)
+    rows = np.repeat(np.arange(row0, row0 + m, dtype=np.uint64), counts)
     bits = np.ascontiguousarray(dist_f32, dtype=np.float32).view(np.uint32).astype(np.uint64)
     key = (np.asarray(indices).astype(np.uint64) << np.uint64(32)) | bits
     h = mix64(mix64(rows) ^ key)
@@ -55,16 +55,16 @@ def csr_digests(offsets, indices, dist_f32, block: int = 1024):
     return counts, _seg_sums(row_dig, boff)
 
 
-def oracle_csr_digests(res: dict, block: int = 1024):
-    """Digests of an oracle.radius_query result: hits only (s <= R*R), distance =
-    float32(sqrt(s))."""
+def oracle_csr_digests(res: dict, block: int = 1024, row0: int = 0):
+    """Digests of an oracle.radius_query result (for queries row0, row0 + 1, ...): hits
+    only (s <= R*R), distance = float32(sqrt(s))."""
     keep = res["s"] <= res["R2"]
     off = np.asarray(res["offsets"], dtype=np.int64)
     rows = np.repeat(np.arange(len(off) - 1), np.diff(off))
     cnt = np.bincount(rows[keep], minlength=len(off) - 1)
     noff = np.zeros(len(off), dtype=np.int64)
     np.cumsum(cnt, out=noff[1:])
-    return csr_digests(noff, res["indices"][keep], np.sqrt(res["s"][keep]).astype(np.float32), block)
+    return csr_digests(noff, res["indices"][keep], np.sqrt(res["s"][keep]).astype(np.float32), block, row0)
 
 
 def label_digests(labels, block: int = 4096) -> np.ndarray:

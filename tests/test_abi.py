@@ -97,6 +97,7 @@ def test_snn_load_rejects_bad_files_without_touching_the_device(libpath, tmp_pat
         "unsupported version": b"SNNG" + struct.pack("<I", 2) + struct.pack("<23q", *hdr),
         "truncated": b"SNNG" + struct.pack("<I", 1) + struct.pack("<23q", *hdr)[:40],
         "invalid header": b"SNNG" + struct.pack("<I", 1) + struct.pack("<23q", *([5, 7] + hdr[2:])),
+        "invalid header ": b"SNNG" + struct.pack("<I", 1) + struct.pack("<23q", *(hdr[:3] + [3] + hdr[4:])),
     }
     # correct header, payload one byte short
     cases["truncated "] = cases["unsupported version"][:4] + struct.pack("<I", 1) + \
@@ -128,3 +129,29 @@ def test_c_demo_links_against_the_library(libpath, tmp_path):
                            os.path.join(ROOT, "examples", "c_api_demo.c"), "-L", libdir, "-lsnn",
                            f"-Wl,-rpath,{libdir}", "-o", str(exe)])
     assert exe.exists()
+
+
+def test_options_are_per_thread(libpath):
+    """snn_set_option changes only the calling thread's options (include/snn.h): a second
+    thread starts from the defaults and its changes do not leak back (no GPU needed)."""
+    import threading
+    import paper_2212_07679_b200 as p
+    p.load_library()
+    p.snn_set_option("tc_tiles", 4)
+    seen = {}
+
+    def other():
+        seen["tc_tiles"] = p.snn_get_option("tc_tiles")
+        p.snn_set_option("chunk", 1024)
+        seen["chunk"] = p.snn_get_option("chunk")
+    try:
+        t = threading.Thread(target=other)
+        t.start()
+        t.join()
+        assert seen == {"tc_tiles": 8, "chunk": 1024}
+        assert p.snn_get_option("tc_tiles") == 4 and p.snn_get_option("chunk") == 2048
+        with pytest.raises(p.SnnError, match="unknown option"):
+            p.snn_get_option("no_such_option")
+    finally:
+        p.snn_set_option("tc_tiles", 0)
+    assert p.snn_get_option("tc_tiles") == 8

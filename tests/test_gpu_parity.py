@@ -945,6 +945,46 @@ def test_load_rejects_broken_invariants(snn, tmp_path):
         snn.Index.load(p)
 
 
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_load_rewrites_padding_sentinels(snn, tmp_path, dt):
+    """A file whose padding rows [n, n_pad) hold finite values (here: the origin, right next
+    to the queries) loads to an index that answers exactly like the saved one: snn_load
+    rewrites the sentinels the kernels rely on instead of trusting the file."""
+    rng = np.random.default_rng(1301)
+    n, d = 4097, 2                        # n_pad = 4100: three padding rows
+    X = (rng.random((n, d)) - 0.5).astype(dt)
+    Q = (rng.random((50, d)) * 0.02 - 0.01).astype(dt)
+    a = snn.Index(_dev(X))
+    p = str(tmp_path / "a.snn")
+    try:
+        a.save(p)
+        ref_q, ref_s = a.query(_dev(Q), 0.05), a.query_self(0.05)
+    finally:
+        a.free()
+    blob = bytearray(open(p, "rb").read())
+    es, npad = np.dtype(dt).itemsize, 4100
+    xf = npad * (d + 1) * 4 if dt == np.float32 else 0        # filter rows (low-d fp32) follow Xs
+    xs0 = len(blob) - xf - npad * d * es
+    g = n >> 2
+    for r in range(n & 3, 4):
+        for k in range(d):
+            o = xs0 + (g * 4 * d + 4 * k + r) * es
+            blob[o:o + es] = np.zeros(1, dt).tobytes()         # finite padding coordinates
+            if xf:
+                o = xs0 + npad * d * es + (g * 4 * (d + 1) + 4 * k + r) * 4
+                blob[o:o + 4] = np.float32(0).tobytes()
+        if xf:
+            o = xs0 + npad * d * es + (g * 4 * (d + 1) + 4 * d + r) * 4
+            blob[o:o + 4] = np.float32(0).tobytes()            # xbar' 0 instead of +inf
+    open(p, "wb").write(bytes(blob))
+    b = snn.Index.load(p)
+    try:
+        _csr_equal(ref_q, b.query(_dev(Q), 0.05))
+        _csr_equal(ref_s, b.query_self(0.05))
+    finally:
+        b.free()
+
+
 @pytest.mark.parametrize("d", [2, 3, 6])
 def test_row_staging_and_symmetry_options_identical(snn, d):
     """Key-order row staging (default) vs direct final-row writes, symmetric vs two-sided
@@ -1054,3 +1094,60 @@ def test_c_demo_runs(snn, tmp_path):
     out = subprocess.check_output([str(exe)]).decode().split()
     n, m, nnz, k = map(int, out)
     assert n == m == 4096 and nnz > n and k >= 1
+
+
+# --------------------------------------------------------------------------- concurrency
+@pytest.mark.parametrize("kind", ["c2", "c3", "dbscan"])
+def test_concurrent_queries_on_one_index(snn, kind):
+    """Two host threads, each on its own CUDA stream, query ONE index at the same time
+    (the library releases the GIL in every call); one of them runs with different
+    per-thread options (two-sided scan / SIMT generic path).  Every result is bit-identical
+    to the serial one."""
+    import threading
+    import torch
+    import paper_2212_07679_b200 as p
+    if kind == "c2":
+        w = workloads.c2(n=200000)
+        X, Q, R = w.X, None, 0.5866
+    elif kind == "c3":
+        w = workloads.c3(n=30000, m=3000)
+        X, Q, R = w.X, w.Q, 1.8134
+    else:
+        w = workloads.c5(n=100000, seed=4, box=400.0)
+        X, Q, R = w.X, None, 3.0
+    idx = snn.Index(_dev(X))
+    Qd = None if Q is None else _dev(Q)
+
+    def once(stream):
+        with torch.cuda.stream(stream):
+            if kind == "dbscan":
+                return idx.dbscan(R, 5, stream=stream)
+            return idx.query_self(R, stream=stream) if Qd is None else idx.query(Qd, R, stream=stream)
+    try:
+        ref = once(torch.cuda.current_stream())
+        out, errs = {}, []
+
+        def worker(tid):
+            try:
+                if tid == 1:   # per-thread options: another (bit-identical) path
+                    p.snn_set_option("symmetric", -1)
+                    p.snn_set_option("tc", -1)
+                st = torch.cuda.Stream()
+                out[tid] = [once(st) for _ in range(3)]
+            except Exception as e:   # pragma: no cover - reported below
+                errs.append(e)
+        th = [threading.Thread(target=worker, args=(t,)) for t in range(2)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        assert not errs, errs
+        assert p.snn_get_option("symmetric") == 1 and p.snn_get_option("tc") == 1   # main thread untouched
+        for tid in range(2):
+            for r in out[tid]:
+                if kind == "dbscan":
+                    assert r[1] == ref[1] and np.array_equal(r[0], ref[0])
+                else:
+                    _csr_equal(ref, r)
+    finally:
+        idx.free()
