@@ -10,11 +10,14 @@ workloads/radii.json).  Inputs are resident in HBM; L2 (126 MB) is flushed by wr
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl snn|reference] [--config c2]
 
-Multi-GPU (torchrun, one rank per GPU): every rank runs an independent replica of the
-workload (weak scaling, no data-path collective); with ``--shard``
-the ranks split ONE query set instead (snn_query_*_part: contiguous, work-balanced ranges of
-key-sorted query blocks on a replicated index; strong scaling).  Timings are the max over
-ranks.  ``--impl reference`` times the CPU oracle (fp64 brute force) on a bounded
+Multi-GPU (torchrun, one rank per GPU): the ranks split ONE query set (default; strong
+scaling): every rank builds the replicated index and runs snn_query_*_part -- contiguous,
+work-balanced ranges of key-sorted query blocks; a partitioned self-query stays symmetric
+(each unordered pair once; ghost blocks before a part supply its rows' mirrored entries) --
+and one all-gather of the per-part nnz rebases the parts into one global CSR
+(paper_2212_07679_b200/shard.py).  ``--replicas`` (and DBSCAN, which has no cross-shard
+merge) runs an independent replica per rank instead (weak scaling).  Timings are the max
+over ranks.  ``--impl reference`` times the CPU oracle (fp64 brute force) on a bounded
 sample of the same workload, rank 0 only.
 """
 from __future__ import annotations
@@ -230,8 +233,9 @@ def config_block(w, args):
                         f"{'self-query' if w.Q is None else f'm={w.m} queries'}, R={w.R:.6g}",
             "n": w.n, "m": w.m, "d": w.d, "R": w.R, "input_dtype": str(w.X.dtype),
             "l2": "flushed (256 MB write) before every timed step",
-            "parallelism": (f"query shards x{args.gpus} (snn_query_*_part, strong scaling)" if args.shard
-                            else f"replicas x{args.gpus} (weak scaling)")}
+            "parallelism": (f"replicas x{args.gpus} (weak scaling)" if (args.gpus <= 1 or args.replicas or w.dbscan_min_pts is not None)
+                            else f"query shards x{args.gpus} (snn_query_*_part, symmetric self-query split, "
+                                 f"nnz all-gather rebase; strong scaling)")}
 
 
 # ----------------------------------------------------------------------------- roofline
@@ -322,7 +326,11 @@ def run_gpu(args):
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
 
     dbscan = w.dbscan_min_pts is not None
-    shard = args.shard and world > 1 and not dbscan
+    # N > 1: one query set split across the ranks (strong scaling) unless --replicas;
+    # DBSCAN (config 5) has no cross-shard union-find merge: replicas
+    shard = world > 1 and not dbscan and not args.replicas
+    if shard:
+        from paper_2212_07679_b200 import shard as shard_mod
     labels_d = torch.empty(w.n, dtype=torch.int32, device=dev) if dbscan else None
 
     def step():
@@ -337,6 +345,9 @@ def run_gpu(args):
         else:
             r = snn.snn_query_self(idx, R) if Qd is None else snn.snn_query_radius(idx, Qd, R)
         nnz = snn.snn_result_csr(r)["nnz"]
+        if shard:   # rebase: every part's first global entry (one all-gather of the part sizes)
+            _, total, _ = shard_mod.part_bases(nnz, device=dev)
+            nnz = total
         snn.snn_result_free(r)
         snn.snn_free(idx)
         return nnz
@@ -404,16 +415,72 @@ def run_gpu(args):
             else:
                 r = snn.snn_query_self(idx, R) if Qh is None else snn.snn_query_radius(idx, Qh, R)
             snn.snn_result_copy(r, off_h, idx_h, dist_h)
+            if shard:
+                shard_mod.part_bases(snn.snn_result_csr(r)["nnz"], device=dev)
             snn.snn_result_free(r)
         snn.snn_free(idx)
         e1.record()
         e1.synchronize()
         if i >= args.warmup:
             e2e_times.append(e0.elapsed_time(e1))
-    e2e_ms = max_over_ranks(sum(e2e_times), world, dev)
+    e2e_serial_ms = max_over_ranks(sum(e2e_times), world, dev)
+    e2e_ms, e2e_mode = e2e_serial_ms, "serial: every step's H2D, build, query and D2H back to back"
+    if not dbscan:
+        # pipelined: step k's CSR copy-out (snn_result_copy_async on a copy stream, into one of
+        # two pinned host buffer sets) runs under step k+1's H2D + build + query; the timed
+        # region ends when the last step's copy has landed in host memory
+        off_h2 = torch.empty_like(off_h).pin_memory()
+        idx_h2 = torch.empty_like(idx_h).pin_memory()
+        dist_h2 = torch.empty_like(dist_h).pin_memory()
+        bufs = [(off_h, idx_h, dist_h), (off_h2, idx_h2, dist_h2)]
+        cs = torch.cuda.Stream(device=dev)
+        pending = []
+        ev_start = torch.cuda.Event(enable_timing=True)
+        for i in range(args.warmup + args.steps):
+            if i == args.warmup:
+                for rr, ev in pending:
+                    ev.synchronize()
+                    snn.snn_result_free(rr)
+                pending = []
+                torch.cuda.synchronize()
+                if world > 1:
+                    torch.distributed.barrier()
+                ev_start.record()
+            flush.fill_(1.0)
+            idx = snn.snn_build(Xh)
+            if shard:
+                r = (snn.snn_query_self_part(idx, R, rank, world) if Qh is None
+                     else snn.snn_query_radius_part(idx, Qh, R, rank, world))
+            else:
+                r = snn.snn_query_self(idx, R) if Qh is None else snn.snn_query_radius(idx, Qh, R)
+            if len(pending) == 2:                 # buffer set i % 2 was step i-2's: retire it
+                rr, ev = pending.pop(0)
+                ev.synchronize()
+                snn.snn_result_free(rr)
+            cs.wait_stream(torch.cuda.current_stream())
+            snn.snn_result_copy_async(r, *bufs[i % 2], stream=cs)
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(cs)
+            pending.append((r, ev))
+            if shard:
+                shard_mod.part_bases(snn.snn_result_csr(r)["nnz"], device=dev)
+            snn.snn_free(idx)
+        last = pending[-1][1]
+        last.synchronize()
+        piped_ms = ev_start.elapsed_time(last)
+        for rr, ev in pending:
+            ev.synchronize()
+            snn.snn_result_free(rr)
+        e2e_ms = max_over_ranks(piped_ms, world, dev)
+        e2e_mode = ("pipelined: step k's D2H copy (snn_result_copy_async, copy stream, double-buffered "
+                    "pinned host CSR) overlaps step k+1's H2D + build + query")
     e2e_value = (w.m * args.steps if shard else weak_units(w.m * args.steps, world)) / (e2e_ms / 1e3)
-    h2d = w.X.nbytes + (0 if w.Q is None else w.Q.nbytes)
-    d2h = w.n * 4 if dbscan else (w.m + 1) * 8 + nnz * 8
+    # bytes per step of the whole job: replicas copy everything on every rank; shards copy
+    # X (replicated build) and the offsets on every rank, each entry once (nnz = all parts)
+    h2d = (w.X.nbytes + (0 if w.Q is None else w.Q.nbytes)) * world
+    d2h = (w.n * 4 if dbscan else (w.m + 1) * 8 + nnz * 8) * (1 if world == 1 else world)
+    if shard:
+        d2h = (w.m + 1) * 8 * world + nnz * 8
     metric = METRIC_DBSCAN if dbscan else METRIC
     unit = "points/s" if dbscan else "queries/s"
 
@@ -430,7 +497,8 @@ def run_gpu(args):
             "breakdown_ms_per_step": {k: v["ms"] / args.steps for k, v in prof.items()},
             "clocks": clocks, "gpu_launches": launches,
             "e2e": {"value": e2e_value, "unit": unit, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.steps},
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.steps, "mode": e2e_mode,
+                    "serial_ms_per_step": e2e_serial_ms / args.steps},
             "roofline": roofline}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, k, dt, threads, sample = oracle_sample_rate(w, args.cpu_seconds)
@@ -452,8 +520,9 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=25.0)   # the 64-query probe overestimates: ~10-15 s real
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--opt", action="append", default=[], help="library option key=value (A/B runs)")
-    ap.add_argument("--shard", action="store_true",
-                    help="N>1: split one query set across the ranks (strong scaling) instead of replicas")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: every rank runs its own replica (weak scaling) instead of splitting one query set")
+    ap.add_argument("--shard", action="store_true", help="(default for N>1; kept for compatibility)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

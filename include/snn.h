@@ -91,8 +91,12 @@ typedef struct {
  * window, eq:sigma2): sigma[0..k) = the k largest singular values of the centred data the
  * index was BUILT from (appended rows are not included), by power iteration with
  * deflation on the kept Gram matrix (fp64, one CTA on the device; k <= min(d, 16); MIPS
- * indexes: of the d + 1 transformed rows).  sigma: host array of k doubles.  Diagnostic
- * only -- the search uses v1 from the build.  Synchronizes the stream. */
+ * indexes: of the d + 1 transformed rows).  A large tensor-core build (n*d >= 2^27,
+ * option "gram_rows") keeps only the Gram matrix of a strided row sample -- v1 only steers
+ * the pruning -- and then this call first recomputes the full Gram matrix from the rows
+ * currently indexed (appended rows included, centred at the build mean).  sigma: host array
+ * of k doubles.  Diagnostic only -- the search uses v1 from the build.  Synchronizes the
+ * stream. */
 snn_status snn_index_sigma(snn_index idx, int32_t k, double *sigma, void *stream);
 
 /* Diagnostics of a built index (Algorithm 1 outputs). */
@@ -186,13 +190,25 @@ snn_status snn_query_self(snn_index idx, double R, void *stream, snn_result *out
  * of other parts are empty, so the parts' results are disjoint and their union (per row)
  * is exactly the unpartitioned result; no data-path collective is needed (results stay
  * sharded; an all-gather of per-part nnz rebases offsets if a global CSR is wanted).
- * Self-queries use two-sided windows here (the mirrored half of a symmetric scan would
- * cross parts).  Errors as snn_query_radius / snn_query_self, plus INVALID_ARGUMENT
- * unless 0 <= part < nparts. */
+ * Self-queries stay symmetric (each unordered pair evaluated once): the part owns the
+ * rows of its blocks, and the blocks before it whose windows reach its first position run
+ * as ghost blocks clipped to its candidates, supplying its rows' mirrored entries (the
+ * pairs crossing a part boundary are evaluated by both parts; nothing is exchanged).
+ * Errors as snn_query_radius / snn_query_self, plus INVALID_ARGUMENT unless
+ * 0 <= part < nparts. */
 snn_status snn_query_radius_part(snn_index idx, const void *Q, int64_t m, int32_t d, snn_dtype dt, double R,
                                  int32_t part, int32_t nparts, void *stream, snn_result *out);
 snn_status snn_query_self_part(snn_index idx, double R, int32_t part, int32_t nparts, void *stream,
                                snn_result *out);
+
+/* Asynchronous copy of the CSR to caller-owned buffers (as snn_result_copy): the copies
+ * are enqueued on `stream` and the call returns at once; the buffers are valid after the
+ * stream synchronizes.  A later snn_result_free(r) is ordered after these copies (the
+ * device buffers are released on `stream`).  With pinned host buffers the device-to-host
+ * transfer overlaps whatever the caller runs next on other streams (bench.py's pipelined
+ * end-to-end mode: step k's copy-out runs under step k+1's build and query). */
+snn_status snn_result_copy_async(snn_result r, int64_t *offsets, int32_t *indices, float *distances,
+                                 void *stream);
 
 /* CSR view (device pointers, valid until snn_result_free). */
 snn_status snn_result_csr(snn_result r, snn_csr *view);
@@ -266,6 +282,9 @@ snn_status snn_profile_read(const char *family, double *ms, uint64_t *launches, 
  *   "balanced_compact" -1 = per-entry compaction threads (default for symmetric self-queries:
  *                    one slot record per thread after CTA scans)
  *   "window_all"     1 = brute-force ablation: every query scans all n candidates
+ *   "gram_rows", "gram_min_elems"   tensor-core Gram of a build with n*d >= gram_min_elems
+ *                    (default 2^27) uses every ceil(n / gram_rows)-th row (default 65536;
+ *                    -1 = every row)
  *   "finalize_order" -1 = row assembly walks rows in key order (default: original-id order,
  *                    sequential CSR writes)
  *   "union_load"     DBSCAN union pass: how the parent[j] pre-check is loaded (0 volatile,

@@ -32,7 +32,7 @@ STATUS = {0: "SNN_OK", 1: "SNN_ERR_INVALID_ARGUMENT", 2: "SNN_ERR_EMPTY",
 
 EXPORTS = ["snn_build", "snn_build_metric", "snn_append", "snn_save", "snn_load",
            "snn_query_radius_part", "snn_query_self_part", "snn_index_sigma", "snn_query_radius", "snn_query_self", "snn_result_csr",
-           "snn_result_copy", "snn_result_free", "snn_dbscan", "snn_free", "snn_last_error",
+           "snn_result_copy", "snn_result_copy_async", "snn_result_free", "snn_dbscan", "snn_free", "snn_last_error",
            "snn_index_info", "snn_launch_count", "snn_set_option", "snn_get_option", "snn_profile_enable",
            "snn_profile_read"]
 
@@ -87,6 +87,7 @@ def load_library(path: str = LIB_PATH):
         "snn_query_self_part": ([P, f64, i32, i32, P, ctypes.POINTER(P)], ctypes.c_int),
         "snn_result_csr": ([P, ctypes.POINTER(_CSR)], ctypes.c_int),
         "snn_result_copy": ([P, P, P, P, P], ctypes.c_int),
+        "snn_result_copy_async": ([P, P, P, P, P], ctypes.c_int),
         "snn_result_free": ([P], None),
         "snn_dbscan": ([P, f64, i32, P, ctypes.POINTER(i32), P], ctypes.c_int),
         "snn_free": ([P], None),
@@ -248,6 +249,19 @@ def snn_result_copy(result, offsets, indices=None, distances=None, stream=None) 
         return ctypes.c_void_p(a.ctypes.data)
     _check(load_library().snn_result_copy(result, ptr(offsets), ptr(indices), ptr(distances),
                                           _stream_ptr(stream)))
+
+
+def snn_result_copy_async(result, offsets, indices=None, distances=None, stream=None) -> None:
+    """Enqueue the copy on `stream` and return (buffers valid after the stream syncs; a
+    later snn_result_free is ordered after the copy)."""
+    def ptr(a):
+        if a is None:
+            return None
+        if hasattr(a, "data_ptr"):
+            return ctypes.c_void_p(a.data_ptr())
+        return ctypes.c_void_p(a.ctypes.data)
+    _check(load_library().snn_result_copy_async(result, ptr(offsets), ptr(indices), ptr(distances),
+                                                _stream_ptr(stream)))
 
 
 def snn_result_free(result) -> None:

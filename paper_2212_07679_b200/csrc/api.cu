@@ -51,6 +51,8 @@ struct Options {
     int lowd_tc_group = 8;     // query blocks per raster group (low-d tensor-core path)
     int union_load = 0;        // DBSCAN union pass: parent pre-check load (0 volatile, 1 relaxed.gpu, 2 ld.cg)
     int finalize_order = 1;    // staged rows: rows_finalize walks rows in original-id order (sequential CSR writes)
+    int gram_rows = 65536;     // tensor-core Gram of a large build: rows sampled (stride) down to ~this many
+    int64_t gram_min_elems = int64_t(1) << 27;   // ... when n*d is at least this
 };
 // Options are per calling thread (snn_set_option changes only the calling thread's calls;
 // every thread starts from the defaults above), so concurrent callers cannot switch each
@@ -302,10 +304,11 @@ snn_status snn_get_option(const char *key, int64_t *value) {
         {"window_all", &Options::window_all}, {"simt_filter", &Options::simt_filter},
         {"lowd_tc", &Options::lowd_tc}, {"lowd_tc_tiles", &Options::lowd_tc_tiles},
         {"lowd_tc_group", &Options::lowd_tc_group}, {"union_load", &Options::union_load},
-        {"finalize_order", &Options::finalize_order}};
+        {"finalize_order", &Options::finalize_order}, {"gram_rows", &Options::gram_rows}};
     for (const auto &o : kInt)
         if (strcmp(key, o.name) == 0) { *value = g_opt.*(o.field); return SNN_OK; }
     if (strcmp(key, "ovf_records") == 0) { *value = g_opt.ovf_rec_cap; return SNN_OK; }
+    if (strcmp(key, "gram_min_elems") == 0) { *value = g_opt.gram_min_elems; return SNN_OK; }
     return fail(SNN_ERR_INVALID_ARGUMENT, std::string("unknown option ") + key);
 }
 
@@ -374,6 +377,8 @@ snn_status snn_set_option(const char *key, int64_t value) {
         return SNN_OK;
     }
     if (k == "tc_ares") { g_opt.tc_ares = value < 0 ? 0 : 1; return SNN_OK; }
+    if (k == "gram_rows") { g_opt.gram_rows = value == 0 ? 65536 : (value < 0 ? 0 : (int)value); return SNN_OK; }
+    if (k == "gram_min_elems") { g_opt.gram_min_elems = value == 0 ? (int64_t(1) << 27) : value; return SNN_OK; }
     if (k == "finalize_order") { g_opt.finalize_order = value < 0 ? 0 : 1; return SNN_OK; }
     if (k == "union_load") {
         if (value < 0 || value > 2) return fail(SNN_ERR_INVALID_ARGUMENT, "union_load must be 0..2");
@@ -478,12 +483,25 @@ static snn_status build_impl(const void *X, int64_t n, int32_t d, snn_dtype dt, 
     launch_colstats(Xd, f64, n, d, sums, maxabs, flag, s);                        // K1
     launch_finalize_mean(sums, n, d, idx->mu_d, idx->mu_f, s);
     bool gram_done = false;
+    double gstride = 1.0;
     if (d >= g_opt.tc_gram_min_d && !g_opt.force_generic) {                       // K2a (tcgen05)
-        uint8_t *gs = nullptr;
-        CKI(ws.alloc(&gs, gram_tc_scratch_bytes(n, d)), "alloc Gram scratch");
-        gram_done = launch_gram_tc(Xd, f64, n, d, maxabs, idx->mu_f, G, gs, sms, s);
+        // v1 only steers pruning (any unit vector keeps the results exact), so a
+        // large build takes the Gram matrix over every st-th row (~gram_rows rows): the
+        // direction of a strided sample of the data; snn_index_sigma recomputes the full one
+        int64_t st = 1;
+        if (g_opt.gram_rows > 0 && n > 2 * (int64_t)g_opt.gram_rows && (double)n * d >= (double)g_opt.gram_min_elems)
+            st = ceil_div(n, (int64_t)g_opt.gram_rows);
+        const int64_t ns = ceil_div(n, st);
+        uint8_t *gsc = nullptr;
+        CKI(ws.alloc(&gsc, gram_tc_scratch_bytes(ns, d)), "alloc Gram scratch");
+        gram_done = launch_gram_tc(Xd, f64, ns, d, st * d, maxabs, 0.0, idx->mu_f, G, gsc, sms, s);
+        if (gram_done && st > 1) {
+            launch_scale_f64(G, (int64_t)d * d, (double)n / (double)ns, s);   // unbiased for the full data
+            gstride = (double)st;
+        }
     }
     if (!gram_done) launch_gram(Xd, f64, n, d, idx->mu_f, G, s);                  // K2a (SIMT)
+    CKI(cudaMemcpyAsync(idx->stats + ST_GSTRIDE, &gstride, 8, cudaMemcpyHostToDevice, s), "H2D");
     double *pscratch = nullptr;
     CKI(ws.alloc(&pscratch, power_scratch_doubles(d, sms)), "alloc");
     launch_power_iteration(G, d, g_opt.power_iters, 1e-7, maxabs, idx->mu_d, idx->mu_f,
@@ -1057,10 +1075,20 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
     w.all = g_opt.window_all;
     w.blk_lo = blk_lo; w.blk_hi = blk_hi; w.nitems = nitems; w.pairs = pairs;
     launch_block_windows(w, s);                                                    // K7
-    CK(apply_part(ws, s, blk_lo, blk_hi, nitems, nblocks), "query part");
     // symmetric self-query: every unordered pair once -- block b scans only candidates
     // from its own first position on (j > i); mirrored hits fill the L part of row j
-    const bool sym = self && !generic && allow_sym && g_opt.symmetric && !g_opt.window_all && t_part.nparts <= 1;
+    const bool sym = self && !generic && allow_sym && g_opt.symmetric && !g_opt.window_all;
+    int64_t *own_dev = nullptr;   // partitioned symmetric self-query: this part's row range
+    if (sym && t_part.nparts > 1) {
+        int64_t *tmp = nullptr;
+        uint8_t *stp = nullptr;
+        CK(ws.alloc(&tmp, (size_t)(2 * nblocks + 4)), "alloc");
+        CK(ws.alloc(&stp, scan_temp_bytes(nblocks) + 4096), "alloc");
+        CK(ws.alloc(&own_dev, 2), "alloc");
+        launch_restrict_part_sym(blk_lo, blk_hi, nitems, nblocks, B, m, t_part.part, t_part.nparts, tmp, stp, own_dev, s);
+    } else {
+        CK(apply_part(ws, s, blk_lo, blk_hi, nitems, nblocks), "query part");
+    }
     int64_t *blk_lo_s = blk_lo;
     if (sym) {
         CK(ws.alloc(&blk_lo_s, (size_t)nblocks), "alloc");
@@ -1072,9 +1100,11 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
     CK(cudaMemcpyAsync(hp, item_start + nblocks, 8, cudaMemcpyDeviceToHost, s), "D2H items");
     CK(cudaMemcpyAsync(hp + 1, qflag, 4, cudaMemcpyDeviceToHost, s), "D2H flag");
     CK(cudaMemcpyAsync(hp + 2, pairs, 8, cudaMemcpyDeviceToHost, s), "D2H pairs");
+    if (own_dev) CK(cudaMemcpyAsync(hp + 3, own_dev, 16, cudaMemcpyDeviceToHost, s), "D2H part range");
     CK(cudaStreamSynchronize(s), "query windows");
     const int64_t total_items = hp[0];
     const double pairs_eval = (double)*reinterpret_cast<unsigned long long *>(hp + 2);
+    const int64_t own_lo = own_dev ? hp[3] : 0, own_hi = own_dev ? hp[4] : INT64_MAX;
     if (*reinterpret_cast<int *>(hp + 1)) return fail(SNN_ERR_NONFINITE, "Q contains NaN or Inf");
 
     int32_t *cnt = nullptr, *pre = nullptr, *row_count = nullptr, *ovf = nullptr;
@@ -1120,6 +1150,8 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
     a.nblocks = nblocks; a.total_items = total_items;
     a.B = B; a.chunk = chunk;
     a.R2 = R * R;
+    a.n_index = idx->n;
+    a.own_lo = own_lo; a.own_hi = own_hi;
     int32_t *maxl = nullptr;
     const bool stage = !generic && g_opt.stage_rows;
     int32_t *srow = nullptr;
@@ -1155,7 +1187,7 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
         a.Xf = idx->Xf; a.c1h = idx->xf_c1h; a.r2h = r2h; a.mu_f = idx->mu_f;
     }
     if (total_items == 0) {
-        if (sym) launch_row_totals_sym(cnt, pre, item_start, m, B, qperm, a.lcnt, row_count, maxl, srow, s);
+        if (sym) launch_row_totals_sym(cnt, pre, item_start, m, B, qperm, a.lcnt, row_count, maxl, srow, own_lo, own_hi, s);
         else cudaMemsetAsync(row_count, 0, (size_t)m * 4, s);
         if (srow) cudaMemsetAsync(srow, 0, (size_t)m * 4, s);
     } else {
@@ -1163,7 +1195,7 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
         if (generic) launch_generic_pass(false, a, s);                           // K8 count
         else launch_lowd_scan(a, s);                                             // K8 scan
         prof_end(ctok, s, pairs_eval);
-        if (sym) launch_row_totals_sym(cnt, pre, item_start, m, B, qperm, a.lcnt, row_count, maxl, srow, s);
+        if (sym) launch_row_totals_sym(cnt, pre, item_start, m, B, qperm, a.lcnt, row_count, maxl, srow, own_lo, own_hi, s);
         else launch_row_totals(cnt, pre, item_start, m, B, qperm, row_count, srow, s);  // K11
     }
     exclusive_scan_i32_to_i64(row_count, r->offsets, m, scan_tmp, s);
@@ -1808,11 +1840,22 @@ snn_status snn_result_copy(snn_result r, int64_t *offsets, int32_t *indices,
     return SNN_OK;
 }
 
+snn_status snn_result_copy_async(snn_result r, int64_t *offsets, int32_t *indices, float *distances, void *stream) {
+    if (!r || !offsets) return fail(SNN_ERR_INVALID_ARGUMENT, "NULL argument");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    CK(cudaMemcpyAsync(offsets, r->offsets, (size_t)(r->m + 1) * 8, cudaMemcpyDefault, s), "copy offsets");
+    if (indices && r->nnz) CK(cudaMemcpyAsync(indices, r->indices, (size_t)r->nnz * 4, cudaMemcpyDefault, s), "copy indices");
+    if (distances && r->nnz) CK(cudaMemcpyAsync(distances, r->distances, (size_t)r->nnz * 4, cudaMemcpyDefault, s), "copy distances");
+    r->free_stream = s;   // snn_result_free is ordered after these copies
+    return SNN_OK;
+}
+
 void snn_result_free(snn_result r) {
     if (!r) return;
-    if (r->offsets) cudaFreeAsync(r->offsets, 0);
-    if (r->indices) cudaFreeAsync(r->indices, 0);
-    if (r->distances) cudaFreeAsync(r->distances, 0);
+    cudaStream_t s = r->free_stream;
+    if (r->offsets) cudaFreeAsync(r->offsets, s);
+    if (r->indices) cudaFreeAsync(r->indices, s);
+    if (r->distances) cudaFreeAsync(r->distances, s);
     delete r;
 }
 
@@ -1827,7 +1870,20 @@ snn_status snn_index_sigma(snn_index idx, int32_t k, double *sigma, void *stream
     double *scratch = nullptr, *dsig = nullptr;
     CK(ws.alloc(&scratch, (size_t)(k + 2) * idx->d), "alloc");
     CK(ws.alloc(&dsig, (size_t)k), "alloc");
-    launch_spectrum(idx->G, idx->d, k, scratch, dsig, s);
+    const double *G = idx->G;
+    if (idx->h_stats[ST_GSTRIDE] > 1.0) {   // the build's Gram is a row sample: the full one from the index rows
+        const int d = idx->d;
+        double *Gf = nullptr;
+        uint8_t *gsc = nullptr;
+        CK(ws.alloc(&Gf, (size_t)d * d), "alloc Gram");
+        CK(ws.alloc(&gsc, gram_tc_scratch_bytes(idx->n, d)), "alloc Gram scratch");
+        CK(cudaMemsetAsync(Gf, 0, (size_t)d * d * 8, s), "memset");
+        if (!launch_gram_tc(idx->Xs, idx->dt == SNN_F64, idx->n, d, idx->ld, nullptr, idx->h_stats[ST_XCMAX], idx->mu_f,
+                            Gf, gsc, sms, s))
+            return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        G = Gf;
+    }
+    launch_spectrum(G, idx->d, k, scratch, dsig, s);
     CK(cudaGetLastError(), "spectrum");
     CK(cudaMemcpyAsync(sigma, dsig, (size_t)k * 8, cudaMemcpyDeviceToHost, s), "D2H");
     CK(cudaStreamSynchronize(s), "spectrum");

@@ -756,6 +756,18 @@ void launch_colstats(const void *X, bool f64, int64_t n, int d, double *sums,
     else SNN_LAUNCH(colstats_generic<float>, gb, kThreads, 0, s, (const float *)X, n, d, rpb, sums, maxabs_bits, nonfinite);
 }
 
+namespace {
+__global__ void scale_f64_kernel(double *x, int64_t count, double f) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+        x[i] *= f;
+}
+}  // namespace
+
+void launch_scale_f64(double *x, int64_t count, double f, cudaStream_t s) {
+    if (count == 0) return;
+    SNN_LAUNCH(scale_f64_kernel, grid_for(count, kThreads, 148 * 4), kThreads, 0, s, x, count, f);
+}
+
 void launch_finalize_mean(const double *sums, int64_t n, int d, double *mu_d, float *mu_f,
                           cudaStream_t s) {
     SNN_LAUNCH(finalize_mean, (int)ceil_div(d, 256), 256, 0, s, sums, n, d, mu_d, mu_f);

@@ -7,6 +7,23 @@
 #error "This library targets sm_100a (B200) only"
 #endif
 
+// Device-side bounds checks of the debug build (lib/libsnn_debug.so, -DSNN_DEBUG; the
+// stand-in for compute-sanitizer, which this GPU pool does not allow): a failed check
+// prints its location and traps (sticky launch error -> SNN_ERR_CUDA).  Free otherwise.
+#ifdef SNN_DEBUG
+#include <cstdio>
+#define SNN_DASSERT(cond)                                                                   \
+    do {                                                                                    \
+        if (!(cond)) {                                                                      \
+            printf("SNN_DASSERT failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, \
+                   #cond, (int)blockIdx.x, (int)threadIdx.x);                               \
+            __trap();                                                                       \
+        }                                                                                   \
+    } while (0)
+#else
+#define SNN_DASSERT(cond) do { } while (0)
+#endif
+
 namespace snn {
 
 // Process-wide count of kernels launched by this library (snn_launch_count()).

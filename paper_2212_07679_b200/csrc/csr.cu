@@ -42,6 +42,7 @@ __global__ void pairs_scatter_kernel(const uint32_t *flag, const int32_t *pq, co
         if (!flag[k]) continue;
         const int32_t q = qperm[pq[k]];
         const int64_t pos = offsets[q] + atomicAdd(&cursor[q], 1);
+        SNN_DASSERT(pos < offsets[q + 1]);
         tmp[pos] = ((uint64_t)(uint32_t)pj[k] << 32) | (uint64_t)__float_as_uint(dist[k]);
     }
 }

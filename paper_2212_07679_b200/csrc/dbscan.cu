@@ -117,6 +117,7 @@ __device__ __forceinline__ int32_t uf_find_c(volatile int32_t *p, int32_t x) {
     return cur;
 }
 __device__ __forceinline__ void uf_unite_c(int32_t *p, int32_t a, int32_t b) {
+    SNN_DASSERT(a >= 0 && b >= 0 && p[a] >= 0 && p[b] >= 0);
     volatile int32_t *vp = p;
     int32_t ra = uf_find_c(vp, a), rb = uf_find_c(vp, b);
     while (ra != rb) {

@@ -19,13 +19,17 @@ void launch_gram(const void *X, bool f64, int64_t n, int d, const float *mu_f, d
 // K2a on the tensor cores (tc_gram.cu, large d): same G from a transposed FP16 hi/lo split
 // copy of the centred X (scratch: gram_tc_scratch_bytes).  false if TMA maps are unavailable.
 size_t gram_tc_scratch_bytes(int64_t n, int d);
-bool launch_gram_tc(const void *X, bool f64, int64_t n, int d, const uint32_t *maxabs_bits, const float *mu_f,
-                    double *G, void *scratch, int sm_count, cudaStream_t s);
+// rs = elements between consecutive rows used (d: every row of a row-major X); the FP16
+// scale comes from the column maxima, or from xc_bound when maxabs_bits is nullptr.
+bool launch_gram_tc(const void *X, bool f64, int64_t n, int d, int64_t rs, const uint32_t *maxabs_bits,
+                    double xc_bound, const float *mu_f, double *G, void *scratch, int sm_count, cudaStream_t s);
+void launch_scale_f64(double *x, int64_t count, double f, cudaStream_t s);
 // K2b: power iteration on G (d x d, fp64).  Writes v_d (fp64 unit), v_f (fp32), and
 // stats[]: see enum Stat.  maxabs_bits/mu feed the key error bound E_x.
 enum Stat {
     ST_SIGMA1 = 0, ST_ITERS = 1, ST_WNORM_F = 2, ST_WNORM_D = 3, ST_EX_F = 4, ST_EX_D = 5,
     ST_XCMAX = 6,   // max_k (max|x_k| + |mu_f_k|): bound on |fl32(x - mu_f)| (FP16 operand scale)
+    ST_GSTRIDE = 7, // row sampling stride of the kept Gram matrix (<= 1: every build row)
     ST_COUNT = 8
 };
 // scratch: power_scratch_doubles(d, sm_count) doubles (multi-CTA iteration for d > 16).

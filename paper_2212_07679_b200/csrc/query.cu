@@ -34,6 +34,7 @@ namespace {
 // ---------------------------------------------------------------------------- K7
 // one CSR entry: into the staging buffer (one 8-byte store) or the final arrays
 __device__ __forceinline__ void put_entry(const PassArgs &a, int64_t pos, int32_t id, float dist) {
+    SNN_DASSERT(pos >= 0 && pos < a.offsets[a.m]);
     if (a.stage) {
         a.stage[pos] = ((unsigned long long)__float_as_uint(dist) << 32) | (uint32_t)id;
     } else {
@@ -104,6 +105,7 @@ __device__ __forceinline__ void locate(const PassArgs &a, int64_t item, int64_t 
     }
     c0 = a.blk_lo[b] + (item - a.item_start[b]) * a.chunk;
     c1 = min(c0 + a.chunk, a.blk_hi[b]);
+    SNN_DASSERT(b >= 0 && b < a.nblocks && c0 >= 0 && (c0 & 3) == 0 && c0 < c1);
 }
 
 // ---------------------------------------------------------------------------- K8 low d
@@ -169,7 +171,7 @@ struct Emitter {
         while (mm) {
             const int i = __ffs(mm) - 1;
             mm &= mm - 1;
-            atomicAdd(&a.lcnt[jb + i], 1);
+            if (jb + i < a.own_hi) atomicAdd(&a.lcnt[jb + i], 1);   // rows of later parts: theirs
         }
         return mask;
     }
@@ -190,11 +192,14 @@ struct Emitter {
     __device__ __forceinline__ void write(int64_t j, double s) {      // MODE 1
         if (SYM && j <= sp) return;
         const float dd = (float)sqrt(s);
-        put_entry(a, pos, a.perm[j], dd);
+        if (sp >= a.own_lo) put_entry(a, pos, a.perm[j], dd);   // ghost queries: mirrors only
         ++pos;
         ++c;
-        if (SYM)   // mirrored entry into row j's L segment
-            a.tmpL[atomicAdd(&a.lpos[j], 1ull)] = ((unsigned long long)sp << 32) | __float_as_uint(dd);
+        if (SYM && j < a.own_hi) {   // mirrored entry into row j's L segment
+            const unsigned long long k = atomicAdd(&a.lpos[j], 1ull);
+            SNN_DASSERT(k < (unsigned long long)a.offsets[a.m]);
+            a.tmpL[k] = ((unsigned long long)sp << 32) | __float_as_uint(dd);
+        }
     }
 };
 
@@ -297,6 +302,7 @@ __device__ __forceinline__ int32_t uf_rep(volatile int32_t *p, int32_t x) {
     return cur;
 }
 __device__ __forceinline__ void uf_unite(int32_t *p, int32_t a, int32_t b) {
+    SNN_DASSERT(a >= 0 && b >= 0 && p[a] >= 0 && p[b] >= 0);   // both core points
     volatile int32_t *vp = p;
     int32_t ra = uf_rep(vp, a), rb = uf_rep(vp, b);
     while (ra != rb) {
@@ -796,10 +802,14 @@ __device__ __forceinline__ void expand_record(const PassArgs &a, int64_t c0, uin
 #pragma unroll
         for (int k = 0; k < D; ++k) x[k] = Xs[g * 4 * D + k * 4 + i];
         const float dd = (float)sqrt(sqdist_exact(x, q, D));
-        put_entry(a, pos, a.perm[g * 4 + i], dd);
+        SNN_DASSERT(a.n_index <= 0 || g * 4 + i < a.n_index);
+        if (sp >= a.own_lo) put_entry(a, pos, a.perm[g * 4 + i], dd);   // ghost queries: mirrors only
         ++pos;
-        if (a.sym)
-            a.tmpL[atomicAdd(&a.lpos[g * 4 + i], 1ull)] = ((unsigned long long)sp << 32) | __float_as_uint(dd);
+        if (a.sym && g * 4 + i < a.own_hi) {
+            const unsigned long long k = atomicAdd(&a.lpos[g * 4 + i], 1ull);
+            SNN_DASSERT(k < (unsigned long long)a.offsets[a.m]);
+            a.tmpL[k] = ((unsigned long long)sp << 32) | __float_as_uint(dd);
+        }
     }
 }
 
@@ -1073,9 +1083,14 @@ __global__ void row_totals(const int32_t *cnt, int32_t *pre, const int64_t *item
 
 __global__ void row_totals_sym(const int32_t *cnt, int32_t *pre, const int64_t *item_start, int64_t m, int B,
                                const int32_t *qperm, const int32_t *lcnt, int32_t *row_count, int32_t *maxl,
-                               int32_t *srow) {
+                               int32_t *srow, int64_t own_lo, int64_t own_hi) {
     const int64_t sp = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (sp >= m) return;
+    if (sp < own_lo || sp >= own_hi) {   // another part's row (partitioned self-query)
+        row_count[qperm[sp]] = 0;
+        if (srow) srow[sp] = 0;
+        return;
+    }
     const int64_t b = sp / B, t = sp % B;
     const int32_t l = lcnt[sp];
     int32_t run = l + 1;   // L segment, then the point itself
@@ -1093,6 +1108,7 @@ __global__ void row_totals_sym(const int32_t *cnt, int32_t *pre, const int64_t *
 // (<= 32) or shared memory (<= 512); the CTA variant takes rows up to 16384.
 constexpr int kLWarp = 512, kLBlock = 16384;
 __device__ __forceinline__ void lemit(const PassArgs &a, unsigned long long v, int64_t pos) {
+    SNN_DASSERT(pos >= 0 && pos < a.offsets[a.m] && (int64_t)(v >> 32) < a.m);
     a.out_idx[pos] = a.perm[(uint32_t)(v >> 32)];
     a.out_dist[pos] = __uint_as_float((uint32_t)v);
 }
@@ -1111,11 +1127,13 @@ __global__ void __launch_bounds__(256) rows_finalize_warp(PassArgs a) {
     for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; r < a.m;
          r += (int64_t)gridDim.x * blockDim.x / 32) {
         const int64_t sp = a.qinv ? (int64_t)a.qinv[r] : r;
+        if (sp < a.own_lo || sp >= a.own_hi) continue;   // another part's (empty) row
         const int cnt = a.sym ? a.lcnt[sp] : 0;
         const int64_t src = a.soff ? a.soff[sp] : (int64_t)a.lpos[sp] - cnt;   // L cursor advanced by cnt
         const int64_t dst = a.soff ? a.offsets[a.qinv ? r : a.qperm[sp]] : src;
         if (a.soff) {   // U part (after L and self) or the whole row
             const int64_t k0 = a.sym ? cnt + 1 : 0, len = a.soff[sp + 1] - src;
+            SNN_DASSERT(src >= 0 && src + len <= a.offsets[a.m] && dst + len <= a.offsets[a.m]);
             for (int64_t k = k0 + lane; k < len; k += 32) {
                 const unsigned long long v = a.stage[src + k];
                 a.out_idx[dst + k] = (int32_t)(uint32_t)v;
@@ -1255,14 +1273,18 @@ __global__ void part_len_kernel(const int64_t *lo, const int64_t *hi, int64_t nb
 // block b belongs to the part whose share of the total work contains the block's midpoint
 // (contiguous, work-balanced ranges of key-sorted query blocks); other blocks get an empty
 // window, so every path (low d, generic, tensor core) skips them and their rows are empty
+__device__ __forceinline__ int part_owner(const int64_t *lo, const int64_t *hi, const int64_t *pre, int64_t nb,
+                                          int64_t b, int nparts) {
+    const double total = (double)pre[nb];
+    int owner;
+    if (total > 0) owner = (int)(((double)pre[b] + 0.5 * (double)(hi[b] - lo[b])) / total * nparts);
+    else owner = (int)(b * nparts / nb);
+    return owner >= nparts ? nparts - 1 : owner;
+}
 __global__ void restrict_part_kernel(int64_t *lo, int64_t *hi, int64_t *nitems, const int64_t *pre, int64_t nb,
                                      int part, int nparts) {
-    const double total = (double)pre[nb];
     for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
-        int owner;
-        if (total > 0) owner = (int)(((double)pre[b] + 0.5 * (double)(hi[b] - lo[b])) / total * nparts);
-        else owner = (int)(b * nparts / nb);
-        if (owner >= nparts) owner = nparts - 1;
+        const int owner = part_owner(lo, hi, pre, nb, b, nparts);
         if (owner != part) {
             hi[b] = lo[b];
             if (nitems) nitems[b] = 0;
@@ -1270,6 +1292,50 @@ __global__ void restrict_part_kernel(int64_t *lo, int64_t *hi, int64_t *nitems, 
     }
 }
 }  // namespace
+
+// Symmetric self-query split (each unordered pair once): part p owns the
+// rows of its blocks [b0, b1) (key positions [b0 B, b1 B)).  Its own blocks scan their
+// windows as usual (pairs j > i); blocks before b0 whose windows reach b0 B are GHOST
+// blocks, clipped to candidates j >= b0 B: their hits only supply the mirrored L entries of
+// this part's rows (the owning part of those queries evaluates the same pairs for its U
+// rows).  own[0..1] = the part's row range in key positions.
+__global__ void part_range_kernel(const int64_t *lo, const int64_t *hi, const int64_t *pre, int64_t nb, int part,
+                                  int nparts, unsigned long long *own_blocks) {
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x)
+        if (part_owner(lo, hi, pre, nb, b, nparts) == part) {
+            atomicMin(&own_blocks[0], (unsigned long long)b);
+            atomicMax(&own_blocks[1], (unsigned long long)(b + 1));
+        }
+}
+__global__ void restrict_part_sym_kernel(int64_t *lo, int64_t *hi, int64_t *nitems, int64_t nb, int B, int64_t m,
+                                         const unsigned long long *own_blocks, int64_t *own) {
+    const int64_t b0 = (int64_t)own_blocks[0], b1 = (int64_t)own_blocks[1];
+    const int64_t p0 = b0 * B;
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+        if (b >= b0 && b < b1) continue;                         // own block
+        if (b < b0 && hi[b] > p0) lo[b] = lo[b] > p0 ? lo[b] : p0;   // ghost block (p0 is 4-aligned)
+        else hi[b] = lo[b];                                      // another part's block
+        if (nitems) nitems[b] = 0;                               // recomputed by the j > i clip
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        own[0] = b1 > b0 ? p0 : 0;
+        own[1] = b1 > b0 ? min(b1 * (int64_t)B, m) : 0;
+    }
+}
+
+void launch_restrict_part_sym(int64_t *blk_lo, int64_t *blk_hi, int64_t *nitems, int64_t nblocks, int B, int64_t m,
+                              int part, int nparts, int64_t *tmp, void *scan_tmp, int64_t *own, cudaStream_t s) {
+    if (nblocks == 0 || nparts <= 1) return;
+    int64_t g = ceil_div(nblocks, 256);
+    if (g > 148 * 16) g = 148 * 16;
+    unsigned long long *ob = reinterpret_cast<unsigned long long *>(tmp + 2 * nblocks + 1);
+    const unsigned long long init[2] = {(unsigned long long)nblocks, 0ull};
+    cudaMemcpyAsync(ob, init, sizeof(init), cudaMemcpyHostToDevice, s);
+    SNN_LAUNCH(part_len_kernel, (int)g, 256, 0, s, blk_lo, blk_hi, nblocks, tmp);
+    exclusive_scan_i64(tmp, tmp + nblocks, nblocks, scan_tmp, s);
+    SNN_LAUNCH(part_range_kernel, (int)g, 256, 0, s, blk_lo, blk_hi, tmp + nblocks, nblocks, part, nparts, ob);
+    SNN_LAUNCH(restrict_part_sym_kernel, (int)g, 256, 0, s, blk_lo, blk_hi, nitems, nblocks, B, m, ob, own);
+}
 
 void launch_restrict_part(int64_t *blk_lo, int64_t *blk_hi, int64_t *nitems, int64_t nblocks, int part, int nparts,
                           int64_t *tmp, void *scan_tmp, cudaStream_t s) {
@@ -1366,10 +1432,10 @@ void launch_generic_pass(bool write, const PassArgs &a, cudaStream_t s) {
 
 void launch_row_totals_sym(const int32_t *cnt, int32_t *pre, const int64_t *item_start, int64_t m, int B,
                            const int32_t *qperm, const int32_t *lcnt, int32_t *row_count, int32_t *maxl,
-                           int32_t *srow, cudaStream_t s) {
+                           int32_t *srow, int64_t own_lo, int64_t own_hi, cudaStream_t s) {
     if (m == 0) return;
     SNN_LAUNCH(row_totals_sym, (int)ceil_div(m, 256), 256, 0, s, cnt, pre, item_start, m, B, qperm, lcnt, row_count,
-               maxl, srow);
+               maxl, srow, own_lo, own_hi);
 }
 
 __global__ void sym_lpos_init(PassArgs a) {

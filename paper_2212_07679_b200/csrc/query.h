@@ -36,6 +36,8 @@ void launch_item_blocks(const int64_t *item_start, int64_t nblocks, int32_t *ite
 // multi-GPU query sharding: keep only the query blocks of `part` (contiguous key-order
 // ranges balanced by window length); other blocks get empty windows.  tmp: 2 nblocks + 1
 // int64; scan_tmp: scan_temp_bytes(nblocks).
+void launch_restrict_part_sym(int64_t *blk_lo, int64_t *blk_hi, int64_t *nitems, int64_t nblocks, int B, int64_t m,
+                              int part, int nparts, int64_t *tmp, void *scan_tmp, int64_t *own, cudaStream_t s);
 void launch_restrict_part(int64_t *blk_lo, int64_t *blk_hi, int64_t *nitems, int64_t nblocks, int part, int nparts,
                           int64_t *tmp, void *scan_tmp, cudaStream_t s);
 
@@ -93,6 +95,10 @@ struct PassArgs {
     const int64_t *soff = nullptr;
     unsigned long long *stage = nullptr;   // staged entries: (fp32 distance bits << 32 | id)
     const int32_t *qinv = nullptr;         // inverse of qperm (original id -> key position): rows_finalize order
+    // partitioned symmetric self-query: the rows this part owns (key positions); queries
+    // before own_lo are ghost queries (mirrored entries only), mirrors into rows >= own_hi
+    // are left to their owning part
+    int64_t own_lo = 0, own_hi = INT64_MAX;
     // expanded-form SIMT filter (scan variant 3; nullptr = off): AoSoA4 rows with D+1
     // floats (centred coordinates, xbar c1h), the margin constants and mu_f
     const float *Xf = nullptr;
@@ -130,7 +136,7 @@ void launch_generic_pass(bool write, const PassArgs &a, cudaStream_t s);
 // srow (nullable): the same totals in key order (staged rows)
 void launch_row_totals_sym(const int32_t *cnt, int32_t *pre, const int64_t *item_start, int64_t m, int B,
                            const int32_t *qperm, const int32_t *lcnt, int32_t *row_count, int32_t *maxl,
-                           int32_t *srow, cudaStream_t s);
+                           int32_t *srow, int64_t own_lo, int64_t own_hi, cudaStream_t s);
 // symmetric self-query: L cursors = row starts (lpos[sp] = row base of sp)
 void launch_sym_lpos_init(const PassArgs &a, cudaStream_t s);
 // rows -> final CSR: symmetric self-query: sort every row's L segment by position, write it

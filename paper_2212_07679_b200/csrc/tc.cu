@@ -257,6 +257,7 @@ tc_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                             mask &= mask - 1;
                             const int64_t jj = jb + c;
                             if (jj >= c1) break;
+                            SNN_DASSERT(sp < a.m && jj < a.n);
                             if (nh < STAGE_CAP) {
                                 my_hits[nh++] = (int32_t)jj;
                             } else {   // rare: direct append
@@ -387,6 +388,7 @@ __global__ void __launch_bounds__(256) recheck_pairs(const T *__restrict__ Xs, c
             dist[k] = 0.f;
             continue;
         }
+        SNN_DASSERT(pj[k] >= 0 && (ld & 3) == 0);
         const T *x = Xs + (int64_t)pj[k] * ld, *q = Qs + (int64_t)pq[k] * ld;
         double s = 0.0;
         if constexpr (sizeof(T) == 4) {   // rows are 16-byte aligned (ld % 4 == 0): vector loads,

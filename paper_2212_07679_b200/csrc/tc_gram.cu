@@ -35,9 +35,11 @@ constexpr int G_THREADS = 192;
 constexpr int G_SMEM = 1024 + G_STAGES * G_STAGE + 256;
 constexpr uint32_t G_IDESC = make_idesc(true, 128, 256);
 
-__global__ void gram_scale_kernel(int d, const uint32_t *maxabs_bits, const float *mu_f, int *e_out) {
-    double xc = 0.0;
-    for (int i = threadIdx.x; i < d; i += 32)
+// xc = max_k (max|x_k| + |mu_k|) from the column maxima, or the stored bound xc_bound
+// (maxabs_bits == nullptr: the index's ST_XCMAX)
+__global__ void gram_scale_kernel(int d, const uint32_t *maxabs_bits, const float *mu_f, double xc_bound, int *e_out) {
+    double xc = maxabs_bits ? 0.0 : xc_bound;
+    for (int i = threadIdx.x; maxabs_bits && i < d; i += 32)
         xc = fmax(xc, (double)__uint_as_float(maxabs_bits[i]) + fabs((double)mu_f[i]));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) xc = fmax(xc, __shfl_xor_sync(0xffffffffu, xc, o));
@@ -48,10 +50,11 @@ __global__ void gram_scale_kernel(int d, const uint32_t *maxabs_bits, const floa
     }
 }
 
-// XT_h[k][i] + XT_l[k][i] = fl32(X[i][k] - mu_f[k]) * 2^e (clamped to the FP16 range);
-// rows i in [n, ldt) are zero.
+// XT_h[k][i] + XT_l[k][i] = fl32(X[i rs + k] - mu_f[k]) * 2^e (clamped to the FP16 range);
+// rows i in [n, ldt) are zero.  rs = elements between consecutive rows used (d for all
+// rows of a row-major X; a multiple of d samples every rs/d-th row; ld for the index copy).
 template <typename T>
-__global__ void __launch_bounds__(256) gram_transpose_split(const T *__restrict__ X, int64_t n, int d, int64_t ldt,
+__global__ void __launch_bounds__(256) gram_transpose_split(const T *__restrict__ X, int64_t n, int d, int64_t rs, int64_t ldt,
                                                             const float *__restrict__ mu_f, const int *e_ptr,
                                                             __half *__restrict__ XT_h, __half *__restrict__ XT_l) {
     // 128 rows x 64 columns per CTA: every output column gets a 256-byte contiguous run
@@ -65,7 +68,7 @@ __global__ void __launch_bounds__(256) gram_transpose_split(const T *__restrict_
         const int col = c0 + c;
         float v = 0.f;
         if (row < n && col < d) {
-            v = (float)((double)X[row * d + col] - (double)mu_f[col]) * sc;
+            v = (float)((double)X[row * rs + col] - (double)mu_f[col]) * sc;
             v = fminf(fmaxf(v, -65504.f), 65504.f);
         }
         tile[r][c] = v;
@@ -210,8 +213,8 @@ size_t gram_tc_scratch_bytes(int64_t n, int d) {
     return (size_t)2 * d * ldt * sizeof(__half) + 256;
 }
 
-bool launch_gram_tc(const void *X, bool f64, int64_t n, int d, const uint32_t *maxabs_bits, const float *mu_f,
-                    double *G, void *scratch, int sm_count, cudaStream_t s) {
+bool launch_gram_tc(const void *X, bool f64, int64_t n, int d, int64_t rs, const uint32_t *maxabs_bits,
+                    double xc_bound, const float *mu_f, double *G, void *scratch, int sm_count, cudaStream_t s) {
     if (n == 0) return true;
     const int64_t ldt = round_up(n, 8);
     uint8_t *p = static_cast<uint8_t *>(scratch);
@@ -220,10 +223,10 @@ bool launch_gram_tc(const void *X, bool f64, int64_t n, int d, const uint32_t *m
     __half *XT_l = XT_h + (int64_t)d * ldt;
     CUtensorMap mh, ml;
     if (!make_map_t(&mh, XT_h, d, ldt) || !make_map_t(&ml, XT_l, d, ldt)) return false;
-    SNN_LAUNCH(gram_scale_kernel, 1, 32, 0, s, d, maxabs_bits, mu_f, e_dev);
+    SNN_LAUNCH(gram_scale_kernel, 1, 32, 0, s, d, maxabs_bits, mu_f, xc_bound, e_dev);
     dim3 tg((unsigned)ceil_div(ldt, 128), (unsigned)ceil_div(d, 64));
-    if (f64) SNN_LAUNCH(gram_transpose_split<double>, tg, 256, 0, s, (const double *)X, n, d, ldt, mu_f, e_dev, XT_h, XT_l);
-    else SNN_LAUNCH(gram_transpose_split<float>, tg, 256, 0, s, (const float *)X, n, d, ldt, mu_f, e_dev, XT_h, XT_l);
+    if (f64) SNN_LAUNCH(gram_transpose_split<double>, tg, 256, 0, s, (const double *)X, n, d, rs, ldt, mu_f, e_dev, XT_h, XT_l);
+    else SNN_LAUNCH(gram_transpose_split<float>, tg, 256, 0, s, (const float *)X, n, d, rs, ldt, mu_f, e_dev, XT_h, XT_l);
     const int nt = (int)ceil_div(d, GT);
     const int tiles = nt * (nt + 1) / 2;
     const int64_t nkb = ceil_div(ldt, GKR);

@@ -1050,6 +1050,59 @@ def test_query_parts_partition_the_result(snn, d, dt, self_q, nparts):
     compare(full, oracle.radius_query(X, X if self_q else Q, R))
 
 
+@pytest.mark.parametrize("d,dt,nparts,opts", [(2, np.float32, 8, {}), (3, np.float64, 5, {}),
+                                               (3, np.float32, 4, {"stage_rows": -1}),
+                                               (3, np.float32, 3, {"balanced_compact": -1, "cap": 1, "ovf_records": 50}),
+                                               (6, np.float32, 2, {"finalize_order": -1})])
+def test_symmetric_query_parts(snn, d, dt, nparts, opts):
+    """Partitioned SYMMETRIC self-queries (each unordered pair evaluated once, SURVEY.md
+    §8(e)): every part owns a contiguous key range of rows; ghost blocks before it supply
+    the mirrored entries of its rows.  The parts' rows are disjoint and bit-identical to the
+    unpartitioned result, and together they evaluate about half the pairs of two-sided parts
+    (under the staging / compaction / overflow-fix variants too)."""
+    import paper_2212_07679_b200 as p
+    rng = np.random.default_rng(1550 + d + nparts)
+    n = 40000
+    X = (rng.random((n, d)) * 30).astype(dt)
+    R = {2: 0.15, 3: 0.6, 6: 4.0}[d]
+    idx = snn.Index(_dev(X))
+
+    def pairs_of(fn):
+        p.snn_profile_enable(True)
+        out = fn()
+        pe = p.snn_profile_read("window_count")["units"]
+        p.snn_profile_enable(False)
+        return out, pe
+    try:
+        for k, v in opts.items():
+            p.snn_set_option(k, v)
+        full = idx.query_self(R)
+        parts, pe_sym = [], 0.0
+        for q in range(nparts):
+            r, pe = pairs_of(lambda: idx.query_self(R, part=q, nparts=nparts))
+            parts.append(r)
+            pe_sym += pe
+        p.snn_set_option("symmetric", -1)
+        pe_two = sum(pairs_of(lambda: idx.query_self(R, part=q, nparts=nparts))[1] for q in range(nparts))
+    finally:
+        for k in list(opts) + ["symmetric"]:
+            p.snn_set_option(k, 0)
+        idx.free()
+    lens = np.stack([np.diff(np.asarray(q.offsets)) for q in parts])
+    assert ((lens > 0).sum(axis=0) == 1).all(), "every row in exactly one part (self is a neighbour)"
+    np.testing.assert_array_equal(lens.sum(axis=0), np.diff(np.asarray(full.offsets)))
+    for q in parts:
+        off = np.asarray(q.offsets)
+        rows = np.nonzero(np.diff(off))[0]
+        sel = np.concatenate([np.arange(off[r], off[r + 1]) for r in rows])
+        fsel = np.concatenate([np.arange(full.offsets[r], full.offsets[r + 1]) for r in rows])
+        np.testing.assert_array_equal(np.asarray(q.indices)[sel], np.asarray(full.indices)[fsel])
+        np.testing.assert_array_equal(np.asarray(q.distances)[sel].view(np.uint32),
+                                      np.asarray(full.distances)[fsel].view(np.uint32))
+    assert pe_sym < 0.65 * pe_two, (pe_sym, pe_two)
+    compare(full, oracle.radius_query(X, X, R))
+
+
 # --------------------------------------------------------------------------- spectrum diagnostic (a2)
 @pytest.mark.parametrize("d,dt,s_ratio", [(3, np.float32, 0.1), (3, np.float64, 0.5), (20, np.float32, 0.5),
                                           (64, np.float32, None), (200, np.float32, None)])
@@ -1078,6 +1131,38 @@ def test_index_sigma_vs_oracle_svd(snn, d, dt, s_ratio):
         assert abs(sig[1] / sig[0] - s_ratio) < 0.05
     if d > 3:   # well separated spectrum (1/sqrt(i) scales): the deflated values match too
         np.testing.assert_allclose(sig, S[:k], rtol=max(tol, 1e-4))
+
+
+@pytest.mark.parametrize("d", [64, 200])
+def test_sampled_gram_build(snn, d):
+    """A build whose tensor-core Gram uses a strided row sample (options gram_min_elems /
+    gram_rows force it on a small instance): v1 is still close to the oracle's principal
+    direction, the query results are exactly the oracle's (v1 only steers pruning,
+    SPEC.md:132), and snn_index_sigma recomputes the full Gram (matches the oracle SVD)."""
+    import paper_2212_07679_b200 as p
+    rng = np.random.default_rng(1700 + d)
+    n = 30000
+    X = (rng.standard_normal((n, d)) / np.sqrt(np.arange(1, d + 1))).astype(np.float32)
+    Q = (rng.standard_normal((300, d)) / np.sqrt(np.arange(1, d + 1))).astype(np.float32)
+    R = 1.9 if d == 64 else 2.1
+    try:
+        p.snn_set_option("gram_min_elems", 1)
+        p.snn_set_option("gram_rows", 2000)
+        idx = snn.Index(_dev(X))
+    finally:
+        p.snn_set_option("gram_min_elems", 0)
+        p.snn_set_option("gram_rows", 0)
+    try:
+        v = idx.arrays()["v1"].cpu().numpy().astype(np.float64)
+        got = idx.query(_dev(Q), R)
+        sig = idx.sigma(2)
+    finally:
+        idx.free()
+    P = X.astype(np.float64)
+    v1, S = oracle.principal_direction(oracle.center(P, oracle.column_mean(P)))
+    assert abs(float(np.dot(v, v1))) / np.linalg.norm(v) > 0.99
+    np.testing.assert_allclose(sig, S[:2], rtol=2e-3)
+    compare(got, oracle.radius_query(X, Q, R))
 
 
 def test_c_demo_runs(snn, tmp_path):
