@@ -433,9 +433,14 @@ def run_gpu(args):
         idx_h2 = torch.empty_like(idx_h).pin_memory()
         dist_h2 = torch.empty_like(dist_h).pin_memory()
         bufs = [(off_h, idx_h, dist_h), (off_h2, idx_h2, dist_h2)]
+        # two non-blocking streams (compute, copy): the legacy default stream would order
+        # the compute behind the copies
+        comp = torch.cuda.Stream(device=dev)
         cs = torch.cuda.Stream(device=dev)
         pending = []
         ev_start = torch.cuda.Event(enable_timing=True)
+        tl = [] if os.environ.get("SNN_BENCH_TIMELINE") else None   # diagnostics: per-step stream timeline
+        torch.cuda.synchronize()
         for i in range(args.warmup + args.steps):
             if i == args.warmup:
                 for rr, ev in pending:
@@ -445,22 +450,33 @@ def run_gpu(args):
                 torch.cuda.synchronize()
                 if world > 1:
                     torch.distributed.barrier()
-                ev_start.record()
-            flush.fill_(1.0)
-            idx = snn.snn_build(Xh)
-            if shard:
-                r = (snn.snn_query_self_part(idx, R, rank, world) if Qh is None
-                     else snn.snn_query_radius_part(idx, Qh, R, rank, world))
-            else:
-                r = snn.snn_query_self(idx, R) if Qh is None else snn.snn_query_radius(idx, Qh, R)
+                ev_start.record(comp)
+            if tl is not None:
+                e_s = torch.cuda.Event(enable_timing=True)
+                e_s.record(comp)
+                h_s = time.perf_counter()
+            with torch.cuda.stream(comp):
+                flush.fill_(1.0)
+                idx = snn.snn_build(Xh, stream=comp)
+                if shard:
+                    r = (snn.snn_query_self_part(idx, R, rank, world, stream=comp) if Qh is None
+                         else snn.snn_query_radius_part(idx, Qh, R, rank, world, stream=comp))
+                else:
+                    r = (snn.snn_query_self(idx, R, stream=comp) if Qh is None
+                         else snn.snn_query_radius(idx, Qh, R, stream=comp))
             if len(pending) == 2:                 # buffer set i % 2 was step i-2's: retire it
                 rr, ev = pending.pop(0)
                 ev.synchronize()
                 snn.snn_result_free(rr)
-            cs.wait_stream(torch.cuda.current_stream())
+            cs.wait_stream(comp)
+            if tl is not None:
+                e_c = torch.cuda.Event(enable_timing=True)
+                e_c.record(cs)
             snn.snn_result_copy_async(r, *bufs[i % 2], stream=cs)
             ev = torch.cuda.Event(enable_timing=True)
             ev.record(cs)
+            if tl is not None:
+                tl.append((e_s, e_c, ev, time.perf_counter() - h_s))
             pending.append((r, ev))
             if shard:
                 shard_mod.part_bases(snn.snn_result_csr(r)["nnz"], device=dev)
@@ -468,6 +484,10 @@ def run_gpu(args):
         last = pending[-1][1]
         last.synchronize()
         piped_ms = ev_start.elapsed_time(last)
+        if tl:
+            for k, (a, c, d, hs) in enumerate(tl):
+                print(f"step {k}: compute from {tl[0][0].elapsed_time(a):8.2f}  copy {tl[0][0].elapsed_time(c):8.2f} -> "
+                      f"{tl[0][0].elapsed_time(d):8.2f}  host {hs * 1e3:.2f} ms", file=sys.stderr)
         for rr, ev in pending:
             ev.synchronize()
             snn.snn_result_free(rr)

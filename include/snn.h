@@ -287,8 +287,9 @@ snn_status snn_profile_read(const char *family, double *ms, uint64_t *launches, 
  *                    -1 = every row)
  *   "finalize_order" -1 = row assembly walks rows in key order (default: original-id order,
  *                    sequential CSR writes)
- *   "union_load"     DBSCAN union pass: how the parent[j] pre-check is loaded (0 volatile,
- *                    1 ld.relaxed.gpu, 2 ld.global.cg; every value is a valid filter)
+ *   "union_load"     DBSCAN union pass: how the parent[j] pre-check is loaded (1 = default
+ *                    ld.relaxed.gpu, -1 volatile, 2 ld.global.cg; every value is a valid
+ *                    filter; snn_get_option reports 0 volatile / 1 relaxed / 2 cg)
  *   "simt_filter"    low-d fp32 expanded-form pre-filter: default on for radius queries and
  *                    off for DBSCAN; 1 = on everywhere, -1 = off everywhere
  *   "lowd_tc", "lowd_tc_tiles", "lowd_tc_group"   low-d tcgen05 path (default off)

@@ -49,7 +49,7 @@ struct Options {
     int lowd_tc = 0;     // low-d (fp32, d <= 8) radius queries through the tensor-core filter (option; FFMA default)
     int lowd_tc_tiles = 8;     // 256-candidate tiles per work item (low-d tensor-core path)
     int lowd_tc_group = 8;     // query blocks per raster group (low-d tensor-core path)
-    int union_load = 0;        // DBSCAN union pass: parent pre-check load (0 volatile, 1 relaxed.gpu, 2 ld.cg)
+    int union_load = 1;        // DBSCAN union pass: parent pre-check load (0 volatile, 1 relaxed.gpu, 2 ld.cg)
     int finalize_order = 1;    // staged rows: rows_finalize walks rows in original-id order (sequential CSR writes)
     int gram_rows = 65536;     // tensor-core Gram of a large build: rows sampled (stride) down to ~this many
     int64_t gram_min_elems = int64_t(1) << 27;   // ... when n*d is at least this
@@ -381,8 +381,8 @@ snn_status snn_set_option(const char *key, int64_t value) {
     if (k == "gram_min_elems") { g_opt.gram_min_elems = value == 0 ? (int64_t(1) << 27) : value; return SNN_OK; }
     if (k == "finalize_order") { g_opt.finalize_order = value < 0 ? 0 : 1; return SNN_OK; }
     if (k == "union_load") {
-        if (value < 0 || value > 2) return fail(SNN_ERR_INVALID_ARGUMENT, "union_load must be 0..2");
-        g_opt.union_load = (int)value;
+        if (value < -1 || value > 2) return fail(SNN_ERR_INVALID_ARGUMENT, "union_load must be -1..2");
+        g_opt.union_load = value == -1 ? 0 : (value == 0 ? 1 : (int)value);   // 0: the default (relaxed)
         return SNN_OK;
     }
     if (k == "tc_f16") { g_opt.tc_f16 = value < 0 ? 0 : 1; return SNN_OK; }
@@ -501,7 +501,7 @@ static snn_status build_impl(const void *X, int64_t n, int32_t d, snn_dtype dt, 
         }
     }
     if (!gram_done) launch_gram(Xd, f64, n, d, idx->mu_f, G, s);                  // K2a (SIMT)
-    CKI(cudaMemcpyAsync(idx->stats + ST_GSTRIDE, &gstride, 8, cudaMemcpyHostToDevice, s), "H2D");
+    launch_set_f64(idx->stats + ST_GSTRIDE, gstride, s);
     double *pscratch = nullptr;
     CKI(ws.alloc(&pscratch, power_scratch_doubles(d, sms)), "alloc");
     launch_power_iteration(G, d, g_opt.power_iters, 1e-7, maxabs, idx->mu_d, idx->mu_f,
@@ -517,8 +517,8 @@ static snn_status build_impl(const void *X, int64_t n, int32_t d, snn_dtype dt, 
                       idx->mu_d, idx->Xs, idx->xbar, s);                           // K5
     CKI(cudaGetLastError(), "launch");
     double *hs = static_cast<double *>(t_pinned.p);
-    CKI(cudaMemcpyAsync(hs, idx->stats, ST_COUNT * 8, cudaMemcpyDeviceToHost, s), "D2H stats");
-    CKI(cudaMemcpyAsync(hs + ST_COUNT, flag, 4, cudaMemcpyDeviceToHost, s), "D2H flag");
+    CKI(small_readback(hs, idx->stats, ST_COUNT * 8, s), "D2H stats");
+    CKI(small_readback(hs + ST_COUNT, flag, 4, s), "D2H flag");
     CKI(cudaStreamSynchronize(s), "build");
     memcpy(idx->h_stats, hs, sizeof(idx->h_stats));
     int nonfinite = *reinterpret_cast<int *>(hs + ST_COUNT);
@@ -621,8 +621,8 @@ static snn_status pairs_to_csr(Workspace &ws, cudaStream_t s, int64_t m, int64_t
     launch_pairs_row_count(flag, pq, qperm, P, m, row_count, maxrow, s);
     exclusive_scan_i32_to_i64(row_count, r->offsets, m, scan_tmp, s);
     int64_t *hp = static_cast<int64_t *>(t_pinned.p);
-    if ((e = cudaMemcpyAsync(hp, r->offsets + m, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return bail(e, "D2H");
-    if ((e = cudaMemcpyAsync(hp + 1, maxrow, 4, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return bail(e, "D2H");
+    if ((e = small_readback(hp, r->offsets + m, 8, s)) != cudaSuccess) return bail(e, "D2H");
+    if ((e = small_readback(hp + 1, maxrow, 4, s)) != cudaSuccess) return bail(e, "D2H");
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return bail(e, "recheck");
     const int64_t H = hp[0];
     const int32_t mr = *reinterpret_cast<int32_t *>(hp + 1);
@@ -714,10 +714,10 @@ static snn_status query_tc(snn_index idx, Workspace &ws, cudaStream_t s, int sms
     launch_tc_group_items(blk_lo, blk_hi, nblocks, (int)G, chunk, grp_lo, grp_items, s);
     exclusive_scan_i64(grp_items, grp_start, ngroups, scan_tmp, s);
     int64_t *hp = static_cast<int64_t *>(t_pinned.p);
-    CK(cudaMemcpyAsync(hp, grp_start + ngroups, 8, cudaMemcpyDeviceToHost, s), "D2H items");
-    CK(cudaMemcpyAsync(hp + 1, qflag, 4, cudaMemcpyDeviceToHost, s), "D2H flag");
-    CK(cudaMemcpyAsync(hp + 2, wpairs, 8, cudaMemcpyDeviceToHost, s), "D2H pairs");
-    if (Qd) CK(cudaMemcpyAsync(hp + 3, eq + 1, 8, cudaMemcpyDeviceToHost, s), "D2H query bound");
+    CK(small_readback(hp, grp_start + ngroups, 8, s), "D2H items");
+    CK(small_readback(hp + 1, qflag, 4, s), "D2H flag");
+    CK(small_readback(hp + 2, wpairs, 8, s), "D2H pairs");
+    if (Qd) CK(small_readback(hp + 3, eq + 1, 8, s), "D2H query bound");
     CK(cudaStreamSynchronize(s), "query windows");
     const int64_t total_items = hp[0];
     if (*reinterpret_cast<int *>(hp + 1)) return fail(SNN_ERR_NONFINITE, "Q contains NaN or Inf");
@@ -793,7 +793,7 @@ static snn_status query_tc(snn_index idx, Workspace &ws, cudaStream_t s, int sms
         const int ctok = prof_begin(F_COUNT, s);
         if (!launch_tc_window(Qt, idx->Xt, f16, t, sms, s)) return fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");   // K9
         prof_end(ctok, s, pairs_eval);
-        CK(cudaMemcpyAsync(hp, pcount, 8, cudaMemcpyDeviceToHost, s), "D2H pair count");
+        CK(small_readback(hp, pcount, 8, s), "D2H pair count");
         CK(cudaStreamSynchronize(s), "tc filter");
         np = (int64_t)*reinterpret_cast<unsigned long long *>(hp);
         if (np <= used_cap) break;
@@ -867,10 +867,10 @@ static snn_status query_tcl(snn_index idx, Workspace &ws, cudaStream_t s, int sm
     launch_tcl_items(blk_lo, blk_hi, nblocks, (int)G, chunk, bcount, s);
     exclusive_scan_i64(bcount, bstart, nblocks, scan_tmp, s);
     int64_t *hp = static_cast<int64_t *>(t_pinned.p);
-    CK(cudaMemcpyAsync(hp, bstart + nblocks, 8, cudaMemcpyDeviceToHost, s), "D2H items");
-    CK(cudaMemcpyAsync(hp + 1, qflag, 4, cudaMemcpyDeviceToHost, s), "D2H flag");
-    CK(cudaMemcpyAsync(hp + 2, wpairs, 8, cudaMemcpyDeviceToHost, s), "D2H pairs");
-    if (!self) CK(cudaMemcpyAsync(hp + 3, eq + 1, 8, cudaMemcpyDeviceToHost, s), "D2H query bound");
+    CK(small_readback(hp, bstart + nblocks, 8, s), "D2H items");
+    CK(small_readback(hp + 1, qflag, 4, s), "D2H flag");
+    CK(small_readback(hp + 2, wpairs, 8, s), "D2H pairs");
+    if (!self) CK(small_readback(hp + 3, eq + 1, 8, s), "D2H query bound");
     CK(cudaStreamSynchronize(s), "query windows");
     const int64_t total_items = hp[0];
     if (*reinterpret_cast<int *>(hp + 1)) return fail(SNN_ERR_NONFINITE, "Q contains NaN or Inf");
@@ -953,7 +953,7 @@ static snn_status query_tcl(snn_index idx, Workspace &ws, cudaStream_t s, int sm
     if (ce != cudaSuccess) { delete r; return cuda_fail(ce, "alloc offsets"); }
     r->offsets = static_cast<int64_t *>(pm);
     exclusive_scan_i32_to_i64(row_count, r->offsets, m, scan_tmp, s);
-    if ((ce = cudaMemcpyAsync(hp, r->offsets + m, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+    if ((ce = small_readback(hp, r->offsets + m, 8, s)) != cudaSuccess ||
         (ce = cudaStreamSynchronize(s)) != cudaSuccess) { snn_result_free(r); return cuda_fail(ce, "exact"); }
     const int64_t H = hp[0];
     r->nnz = H;
@@ -1097,10 +1097,10 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
     }
     exclusive_scan_i64(nitems, item_start, nblocks, scan_tmp, s);
     int64_t *hp = static_cast<int64_t *>(t_pinned.p);
-    CK(cudaMemcpyAsync(hp, item_start + nblocks, 8, cudaMemcpyDeviceToHost, s), "D2H items");
-    CK(cudaMemcpyAsync(hp + 1, qflag, 4, cudaMemcpyDeviceToHost, s), "D2H flag");
-    CK(cudaMemcpyAsync(hp + 2, pairs, 8, cudaMemcpyDeviceToHost, s), "D2H pairs");
-    if (own_dev) CK(cudaMemcpyAsync(hp + 3, own_dev, 16, cudaMemcpyDeviceToHost, s), "D2H part range");
+    CK(small_readback(hp, item_start + nblocks, 8, s), "D2H items");
+    CK(small_readback(hp + 1, qflag, 4, s), "D2H flag");
+    CK(small_readback(hp + 2, pairs, 8, s), "D2H pairs");
+    if (own_dev) CK(small_readback(hp + 3, own_dev, 16, s), "D2H part range");
     CK(cudaStreamSynchronize(s), "query windows");
     const int64_t total_items = hp[0];
     const double pairs_eval = (double)*reinterpret_cast<unsigned long long *>(hp + 2);
@@ -1204,10 +1204,10 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
         a.soff = soff;
     }
     {
-        cudaError_t e = cudaMemcpyAsync(hp, r->offsets + m, 8, cudaMemcpyDeviceToHost, s);
+        cudaError_t e = small_readback(hp, r->offsets + m, 8, s);
         if (e == cudaSuccess && a.ovf_count)
-            e = cudaMemcpyAsync(hp + 1, a.ovf_count, 8, cudaMemcpyDeviceToHost, s);
-        if (e == cudaSuccess && maxl) e = cudaMemcpyAsync(hp + 2, maxl, 4, cudaMemcpyDeviceToHost, s);
+            e = small_readback(hp + 1, a.ovf_count, 8, s);
+        if (e == cudaSuccess && maxl) e = small_readback(hp + 2, maxl, 4, s);
         if (e == cudaSuccess) e = cudaStreamSynchronize(s);
         if (e != cudaSuccess) return bail(e, "query count");
     }
@@ -1584,7 +1584,7 @@ snn_status snn_append(snn_index idx, const void *Y, int64_t k, int32_t d, snn_dt
     launch_key_bounds(D, maxabs, idx->mu_d, idx->mu_f, idx->v_d, idx->v_f, stats1, s);
     double *hs = static_cast<double *>(t_pinned.p);
     double h_stats1[ST_COUNT];
-    if ((e = cudaMemcpyAsync(hs, stats1, ST_COUNT * 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return bail(e, "D2H");
+    if ((e = small_readback(hs, stats1, ST_COUNT * 8, s)) != cudaSuccess) return bail(e, "D2H");
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return bail(e, "append");
     memcpy(h_stats1, hs, sizeof(h_stats1));
     if (idx->Xf) {
@@ -1846,16 +1846,23 @@ snn_status snn_result_copy_async(snn_result r, int64_t *offsets, int32_t *indice
     CK(cudaMemcpyAsync(offsets, r->offsets, (size_t)(r->m + 1) * 8, cudaMemcpyDefault, s), "copy offsets");
     if (indices && r->nnz) CK(cudaMemcpyAsync(indices, r->indices, (size_t)r->nnz * 4, cudaMemcpyDefault, s), "copy indices");
     if (distances && r->nnz) CK(cudaMemcpyAsync(distances, r->distances, (size_t)r->nnz * 4, cudaMemcpyDefault, s), "copy distances");
-    r->free_stream = s;   // snn_result_free is ordered after these copies
+    // snn_result_free waits for this event, not for the copy stream: frees ordered on the
+    // copy stream would also wait for later copies queued there, and allocations that reuse
+    // the memory would then serialise the next step behind them
+    if (!r->copy_done) CK(cudaEventCreateWithFlags(&r->copy_done, cudaEventDisableTiming), "event");
+    CK(cudaEventRecord(r->copy_done, s), "event");
     return SNN_OK;
 }
 
 void snn_result_free(snn_result r) {
     if (!r) return;
-    cudaStream_t s = r->free_stream;
-    if (r->offsets) cudaFreeAsync(r->offsets, s);
-    if (r->indices) cudaFreeAsync(r->indices, s);
-    if (r->distances) cudaFreeAsync(r->distances, s);
+    if (r->copy_done) {   // an asynchronous copy may still read the buffers
+        cudaStreamWaitEvent(0, r->copy_done, 0);
+        cudaEventDestroy(r->copy_done);
+    }
+    if (r->offsets) cudaFreeAsync(r->offsets, 0);
+    if (r->indices) cudaFreeAsync(r->indices, 0);
+    if (r->distances) cudaFreeAsync(r->distances, 0);
     delete r;
 }
 

@@ -763,6 +763,31 @@ __global__ void scale_f64_kernel(double *x, int64_t count, double f) {
 }
 }  // namespace
 
+namespace {
+__global__ void set_f64_kernel(double *x, double v) { *x = v; }
+__global__ void readback_kernel(uint8_t *dst, const uint8_t *src, int n) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+}  // namespace
+
+// Small device -> host readbacks (sizes, counts, flags) as kernel stores into mapped pinned
+// memory instead of cudaMemcpyAsync: a copy would queue on the device-to-host copy engine
+// behind any large transfer in flight (e.g. the previous result's copy-out on another
+// stream), stalling the whole call until that transfer ends.
+cudaError_t small_readback(void *host, const void *dev, size_t bytes, cudaStream_t s) {
+    void *dptr = nullptr;
+    if (bytes > 4096 || cudaHostGetDevicePointer(&dptr, host, 0) != cudaSuccess) {
+        cudaGetLastError();
+        return cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, s);
+    }
+    SNN_LAUNCH(readback_kernel, 1, 128, 0, s, static_cast<uint8_t *>(dptr), static_cast<const uint8_t *>(dev), (int)bytes);
+    return cudaGetLastError();
+}
+
+// one device scalar from a host value without a pageable copy (a pageable cudaMemcpyAsync
+// waits behind transfers queued on the copy engines, e.g. a large copy-out on another stream)
+void launch_set_f64(double *x, double v, cudaStream_t s) { SNN_LAUNCH(set_f64_kernel, 1, 1, 0, s, x, v); }
+
 void launch_scale_f64(double *x, int64_t count, double f, cudaStream_t s) {
     if (count == 0) return;
     SNN_LAUNCH(scale_f64_kernel, grid_for(count, kThreads, 148 * 4), kThreads, 0, s, x, count, f);

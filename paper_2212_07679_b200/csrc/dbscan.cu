@@ -20,6 +20,7 @@
 #include "common.cuh"
 #include "index.h"
 #include "query.h"
+#include "internal.h"
 
 namespace snn {
 namespace {
@@ -211,7 +212,7 @@ snn_status dbscan_impl(snn_index idx, double eps, int32_t min_pts, int32_t *labe
     w.blk_lo = blk_lo; w.blk_hi = blk_hi; w.nitems = nitems; w.pairs = pairs;
     launch_block_windows(w, s);
     exclusive_scan_i64(nitems, item_start, nblocks, scan_tmp, s);
-    CKD(cudaMemcpyAsync(hbuf, item_start + nblocks, 8, cudaMemcpyDeviceToHost, s), "D2H");
+    CKD(small_readback(hbuf, item_start + nblocks, 8, s), "D2H");
     CKD(cudaStreamSynchronize(s), "dbscan windows");
     const int64_t total_items = hbuf[0];
 
@@ -221,7 +222,8 @@ snn_status dbscan_impl(snn_index idx, double eps, int32_t min_pts, int32_t *labe
     CKD(ws.alloc(&cnt, (size_t)total_items * B), "alloc");
     CKD(ws.alloc(&count, (size_t)n), "alloc");
     CKD(ws.alloc(&core, (size_t)n), "alloc");
-    CKD(ws.alloc(&parent, (size_t)n), "alloc");
+    CKD(ws.alloc(&parent, (size_t)idx->n_pad), "alloc");   // padding rows: -1 (group-wide parent loads)
+    CKD(cudaMemsetAsync(parent + n, 0xff, (size_t)(idx->n_pad - n) * 4, s), "memset");
     CKD(ws.alloc(&minid, (size_t)n), "alloc");
     CKD(ws.alloc(&best, (size_t)n), "alloc");
     CKD(ws.alloc(&flag, (size_t)n), "alloc");
@@ -267,7 +269,7 @@ snn_status dbscan_impl(snn_index idx, double eps, int32_t min_pts, int32_t *labe
     }
 
     unsigned long long *hp_pairs = reinterpret_cast<unsigned long long *>(hbuf);
-    CKD(cudaMemcpyAsync(hp_pairs, pairs, 8, cudaMemcpyDeviceToHost, s), "D2H");
+    CKD(small_readback(hp_pairs, pairs, 8, s), "D2H");
     CKD(cudaStreamSynchronize(s), "dbscan pairs");
     const double pairs_eval = (double)*hp_pairs;
     const int ctok = prof_begin(F_COUNT, s);
@@ -284,9 +286,9 @@ snn_status dbscan_impl(snn_index idx, double eps, int32_t min_pts, int32_t *labe
         CKD(cudaMemsetAsync(upairs, 0, 8, s), "memset");
         launch_truncate_windows(blk_lo, blk_hi, nblocks, B, chunk, lo2, nit2, n, n, upairs, s);
         exclusive_scan_i64(nit2, st2, nblocks, scan_tmp, s);
-        CKD(cudaMemcpyAsync(hbuf, st2 + nblocks, 8, cudaMemcpyDeviceToHost, s), "D2H");
-        CKD(cudaMemcpyAsync(hbuf + 2, pairs, 8, cudaMemcpyDeviceToHost, s), "D2H");
-        CKD(cudaMemcpyAsync(hbuf + 3, upairs, 8, cudaMemcpyDeviceToHost, s), "D2H");
+        CKD(small_readback(hbuf, st2 + nblocks, 8, s), "D2H");
+        CKD(small_readback(hbuf + 2, pairs, 8, s), "D2H");
+        CKD(small_readback(hbuf + 3, upairs, 8, s), "D2H");
         CKD(cudaStreamSynchronize(s), "dbscan union windows");
         prof_end(ctok, s, (double)*reinterpret_cast<unsigned long long *>(hbuf + 2));   // pairs evaluated
         PassArgs au = a;
@@ -313,7 +315,7 @@ snn_status dbscan_impl(snn_index idx, double eps, int32_t min_pts, int32_t *labe
         CKD(ws.alloc(&npos, (size_t)n + 1), "alloc");
         SNN_LAUNCH(noncore_flags, grid_n(n), 256, 0, s, core, n, flag);
         exclusive_scan_i32_to_i64(flag, npos, n, scan_tmp, s);
-        CKD(cudaMemcpyAsync(hbuf, npos + n, 8, cudaMemcpyDeviceToHost, s), "D2H");
+        CKD(small_readback(hbuf, npos + n, 8, s), "D2H");
         CKD(cudaStreamSynchronize(s), "dbscan non-core");
         const int64_t nb = hbuf[0];
         if (nb > 0) {
@@ -339,7 +341,7 @@ snn_status dbscan_impl(snn_index idx, double eps, int32_t min_pts, int32_t *labe
             w3.blk_lo = lo3; w3.blk_hi = hi3; w3.nitems = nit3; w3.pairs = pairs;
             launch_block_windows(w3, s);
             exclusive_scan_i64(nit3, st3, nb3, scan_tmp, s);
-            CKD(cudaMemcpyAsync(hbuf, st3 + nb3, 8, cudaMemcpyDeviceToHost, s), "D2H");
+            CKD(small_readback(hbuf, st3 + nb3, 8, s), "D2H");
             CKD(cudaStreamSynchronize(s), "dbscan border windows");
             PassArgs ab = a;
             ab.Qs = qb; ab.m = nb; ab.qperm = list;
@@ -353,7 +355,7 @@ snn_status dbscan_impl(snn_index idx, double eps, int32_t min_pts, int32_t *labe
     }
     SNN_LAUNCH(final_labels, grid_n(n), 256, 0, s, lab, core, best, idx->perm, n, out);
     if (!dev_out) CKD(cudaMemcpyAsync(labels, out, (size_t)n * 4, cudaMemcpyDeviceToHost, s), "D2H labels");
-    CKD(cudaMemcpyAsync(hbuf + 1, rank + n, 8, cudaMemcpyDeviceToHost, s), "D2H K");
+    CKD(small_readback(hbuf + 1, rank + n, 8, s), "D2H K");
     CKD(cudaGetLastError(), "launch");
     CKD(cudaStreamSynchronize(s), "dbscan");
     *n_clusters = (int32_t)hbuf[1];
@@ -401,7 +403,7 @@ snn_status dbscan_from_csr(const int64_t *off, const int32_t *nidx, int64_t n, i
     SNN_LAUNCH(csr_border, gw, 256, 0, s, off, nidx, core, lab, n, best);
     SNN_LAUNCH(final_labels, g, 256, 0, s, lab, core, best, iota, n, out);
     if (!dev_out) CKD(cudaMemcpyAsync(labels, out, (size_t)n * 4, cudaMemcpyDeviceToHost, s), "D2H labels");
-    CKD(cudaMemcpyAsync(hbuf, rank + n, 8, cudaMemcpyDeviceToHost, s), "D2H K");
+    CKD(small_readback(hbuf, rank + n, 8, s), "D2H K");
     CKD(cudaGetLastError(), "launch");
     CKD(cudaStreamSynchronize(s), "dbscan");
     *n_clusters = (int32_t)hbuf[0];

@@ -81,7 +81,7 @@ struct snn_index_s {
 
 struct snn_result_s {
     int64_t m = 0, nnz = 0;
-    cudaStream_t free_stream = 0;   // snn_result_copy_async's stream: frees are ordered after the copy
+    cudaEvent_t copy_done = nullptr;   // snn_result_copy_async: frees wait for this event
     int64_t *offsets = nullptr;
     int32_t *indices = nullptr;
     float *distances = nullptr;

@@ -24,6 +24,9 @@ size_t gram_tc_scratch_bytes(int64_t n, int d);
 bool launch_gram_tc(const void *X, bool f64, int64_t n, int d, int64_t rs, const uint32_t *maxabs_bits,
                     double xc_bound, const float *mu_f, double *G, void *scratch, int sm_count, cudaStream_t s);
 void launch_scale_f64(double *x, int64_t count, double f, cudaStream_t s);
+void launch_set_f64(double *x, double v, cudaStream_t s);
+// small device -> host readback into PINNED host memory by a kernel (no copy engine)
+cudaError_t small_readback(void *host, const void *dev, size_t bytes, cudaStream_t s);
 // K2b: power iteration on G (d x d, fp64).  Writes v_d (fp64 unit), v_f (fp32), and
 // stats[]: see enum Stat.  maxabs_bits/mu feed the key error bound E_x.
 enum Stat {

@@ -1307,6 +1307,10 @@ __global__ void part_range_kernel(const int64_t *lo, const int64_t *hi, const in
             atomicMax(&own_blocks[1], (unsigned long long)(b + 1));
         }
 }
+__global__ void part_range_init_kernel(unsigned long long *own_blocks, int64_t nb) {
+    own_blocks[0] = (unsigned long long)nb;
+    own_blocks[1] = 0ull;
+}
 __global__ void restrict_part_sym_kernel(int64_t *lo, int64_t *hi, int64_t *nitems, int64_t nb, int B, int64_t m,
                                          const unsigned long long *own_blocks, int64_t *own) {
     const int64_t b0 = (int64_t)own_blocks[0], b1 = (int64_t)own_blocks[1];
@@ -1329,8 +1333,7 @@ void launch_restrict_part_sym(int64_t *blk_lo, int64_t *blk_hi, int64_t *nitems,
     int64_t g = ceil_div(nblocks, 256);
     if (g > 148 * 16) g = 148 * 16;
     unsigned long long *ob = reinterpret_cast<unsigned long long *>(tmp + 2 * nblocks + 1);
-    const unsigned long long init[2] = {(unsigned long long)nblocks, 0ull};
-    cudaMemcpyAsync(ob, init, sizeof(init), cudaMemcpyHostToDevice, s);
+    SNN_LAUNCH(part_range_init_kernel, 1, 1, 0, s, ob, nblocks);
     SNN_LAUNCH(part_len_kernel, (int)g, 256, 0, s, blk_lo, blk_hi, nblocks, tmp);
     exclusive_scan_i64(tmp, tmp + nblocks, nblocks, scan_tmp, s);
     SNN_LAUNCH(part_range_kernel, (int)g, 256, 0, s, blk_lo, blk_hi, tmp + nblocks, nblocks, part, nparts, ob);
