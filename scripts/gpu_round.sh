@@ -18,6 +18,7 @@ for s in $STAGES; do
     parity_full) rm -f $OUT/full_parity.jsonl; SNN_PARITY_RECORD=$OUT/full_parity.jsonl timeout 1200 python -m pytest tests/test_full_parity.py -m gpu -v > $OUT/pytest_full_parity.txt 2>&1; echo "parity_full rc=$?"; tail -8 $OUT/pytest_full_parity.txt ;;
     benchfast) for c in c2 c3 c4 c5; do timeout 600 python bench.py --config $c --steps 10 --no-cpu-baseline > $OUT/bench_$c.jsonl 2> $OUT/bench_$c.err; echo "bench $c rc=$?"; done ;;
     reference) timeout 600 python bench.py --impl reference --steps 3 > $OUT/bench_reference.jsonl 2> $OUT/bench_reference.err; echo "reference rc=$?" ;;
+    ablation) timeout 900 python scripts/ablation_pruning.py c2 c3 c4 > $OUT/ablation_pruning.jsonl 2> $OUT/ablation.err; echo "ablation rc=$?"; cat $OUT/ablation_pruning.jsonl ;;
     ncu_launch) for c in c2 c3 c4 c5; do
         CMD="python bench.py --config $c --steps 1 --warmup 3 --no-cpu-baseline"
         $CMD > $OUT/plain_$c.log 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$c.csv $CMD > $OUT/ncu_launch_$c.log 2>&1; echo "ncu launch $c rc=$?"; done ;;
