@@ -219,6 +219,10 @@ snn_status snn_result_copy(snn_result r, int64_t *offsets, int32_t *indices,
                            float *distances, void *stream);
 
 void snn_result_free(snn_result r); /* NULL ok */
+/* As snn_result_free, with the device buffers released in `stream`'s order (after any
+ * snn_result_copy_async copy): memory freed on the stream that allocates next is reused
+ * without cross-stream pool dependencies (a compute stream running step after step). */
+void snn_result_free_async(snn_result r, void *stream); /* NULL ok */
 
 /*
  * snn_dbscan -- DBSCAN with SNN as the neighbourhood backend, exact
@@ -236,6 +240,13 @@ snn_status snn_dbscan(snn_index idx, double eps, int32_t min_pts, int32_t *label
                       int32_t *n_clusters, void *stream);
 
 void snn_free(snn_index idx); /* NULL ok */
+/* Grow the device's stream-ordered memory pool (which every call allocates from and which
+ * keeps freed memory) by `bytes` up front, so that later calls do not map new memory
+ * while other streams are busy.  Synchronizes the stream. */
+snn_status snn_pool_reserve(uint64_t bytes, void *stream);
+
+/* As snn_free, with the index's device buffers released in `stream`'s order. */
+void snn_free_async(snn_index idx, void *stream); /* NULL ok */
 
 /* Thread-local message for the last non-OK status of this thread ("" if none). */
 const char *snn_last_error(void);

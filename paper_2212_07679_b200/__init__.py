@@ -32,7 +32,7 @@ STATUS = {0: "SNN_OK", 1: "SNN_ERR_INVALID_ARGUMENT", 2: "SNN_ERR_EMPTY",
 
 EXPORTS = ["snn_build", "snn_build_metric", "snn_append", "snn_save", "snn_load",
            "snn_query_radius_part", "snn_query_self_part", "snn_index_sigma", "snn_query_radius", "snn_query_self", "snn_result_csr",
-           "snn_result_copy", "snn_result_copy_async", "snn_result_free", "snn_dbscan", "snn_free", "snn_last_error",
+           "snn_result_copy", "snn_result_copy_async", "snn_result_free", "snn_result_free_async", "snn_free_async", "snn_pool_reserve", "snn_dbscan", "snn_free", "snn_last_error",
            "snn_index_info", "snn_launch_count", "snn_set_option", "snn_get_option", "snn_profile_enable",
            "snn_profile_read"]
 
@@ -89,6 +89,9 @@ def load_library(path: str = LIB_PATH):
         "snn_result_copy": ([P, P, P, P, P], ctypes.c_int),
         "snn_result_copy_async": ([P, P, P, P, P], ctypes.c_int),
         "snn_result_free": ([P], None),
+        "snn_result_free_async": ([P, P], None),
+        "snn_free_async": ([P, P], None),
+        "snn_pool_reserve": ([ctypes.c_uint64, P], ctypes.c_int),
         "snn_dbscan": ([P, f64, i32, P, ctypes.POINTER(i32), P], ctypes.c_int),
         "snn_free": ([P], None),
         "snn_last_error": ([], ctypes.c_char_p),
@@ -272,6 +275,20 @@ def snn_result_free(result) -> None:
 def snn_free(index) -> None:
     if index:
         load_library().snn_free(index)
+
+
+def snn_result_free_async(result, stream=None) -> None:
+    if result:
+        load_library().snn_result_free_async(result, _stream_ptr(stream))
+
+
+def snn_pool_reserve(nbytes: int, stream=None) -> None:
+    _check(load_library().snn_pool_reserve(int(nbytes), _stream_ptr(stream)))
+
+
+def snn_free_async(index, stream=None) -> None:
+    if index:
+        load_library().snn_free_async(index, _stream_ptr(stream))
 
 
 def snn_append(index, Y, stream=None) -> None:

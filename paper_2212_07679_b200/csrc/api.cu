@@ -564,6 +564,24 @@ static snn_status build_impl(const void *X, int64_t n, int32_t d, snn_dtype dt, 
 
 void snn_free(snn_index idx) { free_index(idx); }
 
+snn_status snn_pool_reserve(uint64_t bytes, void *stream) {
+    int sms = 0;
+    snn_status st = device_check(&sms);   // also keeps freed memory in the pool (release threshold)
+    if (st != SNN_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    void *p = nullptr;
+    CK(cudaMallocAsync(&p, (size_t)bytes, s), "pool reserve");
+    CK(cudaFreeAsync(p, s), "pool reserve");
+    CK(cudaStreamSynchronize(s), "pool reserve");
+    return SNN_OK;
+}
+
+void snn_free_async(snn_index idx, void *stream) {
+    if (!idx) return;
+    for (void *p : idx->owned) cudaFreeAsync(p, static_cast<cudaStream_t>(stream));
+    delete idx;
+}
+
 static void thresholds(double R2, int d, float *T_in, float *T_out) {
     const double u32 = ldexp(1.0, -24), u64 = ldexp(1.0, -53);
     const double g32 = (d + 2) * u32 / (1.0 - (d + 2) * u32);
@@ -1854,17 +1872,20 @@ snn_status snn_result_copy_async(snn_result r, int64_t *offsets, int32_t *indice
     return SNN_OK;
 }
 
-void snn_result_free(snn_result r) {
+void snn_result_free_async(snn_result r, void *stream) {
     if (!r) return;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (r->copy_done) {   // an asynchronous copy may still read the buffers
-        cudaStreamWaitEvent(0, r->copy_done, 0);
+        cudaStreamWaitEvent(s, r->copy_done, 0);
         cudaEventDestroy(r->copy_done);
     }
-    if (r->offsets) cudaFreeAsync(r->offsets, 0);
-    if (r->indices) cudaFreeAsync(r->indices, 0);
-    if (r->distances) cudaFreeAsync(r->distances, 0);
+    if (r->offsets) cudaFreeAsync(r->offsets, s);
+    if (r->indices) cudaFreeAsync(r->indices, s);
+    if (r->distances) cudaFreeAsync(r->distances, s);
     delete r;
 }
+
+void snn_result_free(snn_result r) { snn_result_free_async(r, nullptr); }
 
 snn_status snn_index_sigma(snn_index idx, int32_t k, double *sigma, void *stream) {
     if (!idx || !sigma) return fail(SNN_ERR_INVALID_ARGUMENT, "NULL argument");
