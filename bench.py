@@ -304,6 +304,14 @@ def roofline_block(args, w, prof, times, dev, info):
             "share_of_step": kms / sum(times) if times else None}
 
 
+def step_footprint(w, nnz: int) -> int:
+    """Device memory three overlapping steps may hold (staged input, index copies, result,
+    workspace): what bench.py reserves in the library's pool before a timed loop."""
+    x = w.X.nbytes + (0 if w.Q is None else w.Q.nbytes)
+    res = (w.m + 1) * 8 + 2 * 8 * (nnz or 0)
+    return int(min(3 * (4 * x + 3 * res) + (1 << 30), 48 << 30))
+
+
 # ----------------------------------------------------------------------------- GPU arm
 def run_gpu(args):
     import torch
@@ -399,7 +407,7 @@ def run_gpu(args):
     idx_h = torch.empty(1 if dbscan else max(nnz, 1), dtype=torch.int32).pin_memory()
     dist_h = torch.empty(1 if dbscan else max(nnz, 1), dtype=torch.float32).pin_memory()
     labels_h = torch.empty(w.n, dtype=torch.int32).pin_memory() if dbscan else None
-    snn.snn_pool_reserve(3 * (w.n * 4 if dbscan else 2 * nnz * 8 + (w.m + 1) * 8) + (1 << 30))
+    snn.snn_pool_reserve(step_footprint(w, nnz))
     e2e_times = []
     for i in range(args.warmup + args.steps):
         flush.fill_(1.0)
@@ -438,8 +446,8 @@ def run_gpu(args):
         # the compute behind the copies
         comp = torch.cuda.Stream(device=dev)
         cs = torch.cuda.Stream(device=dev)
-        # room for three steps' results and workspaces in the library's memory pool up front
-        snn.snn_pool_reserve(3 * (2 * nnz * 8 + (w.m + 1) * 8) + (1 << 30), comp)
+        # room for three steps' results, indexes and workspaces in the library's memory pool
+        snn.snn_pool_reserve(step_footprint(w, nnz), comp)
         pending = []
         ev_start = torch.cuda.Event(enable_timing=True)
         tl = [] if os.environ.get("SNN_BENCH_TIMELINE") else None   # diagnostics: per-step stream timeline

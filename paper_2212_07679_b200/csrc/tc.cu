@@ -62,6 +62,19 @@ constexpr uint32_t idesc() {
 }
 template <bool F16> constexpr int k_elems() { return F16 ? 64 : 32; }   // elements per K block
 
+__device__ __forceinline__ unsigned long long f2pack_tc(float x, float y) {
+    float2 v = make_float2(x, y);
+    return *reinterpret_cast<unsigned long long *>(&v);
+}
+// (v0, v1) = (w0, w1) * nc + (v0, v1) with one packed FFMA2 (the same rounding as two FFMAs)
+__device__ __forceinline__ void ffma2_inplace(float &v0, float &v1, float w0, float w1, unsigned long long nc) {
+    unsigned long long acc = f2pack_tc(v0, v1), w = f2pack_tc(w0, w1), r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(w), "l"(nc), "l"(acc));
+    const float2 o = *reinterpret_cast<float2 *>(&r);
+    v0 = o.x;
+    v1 = o.y;
+}
+
 template <bool F16>
 __device__ __forceinline__ void mma_op(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t acc) {
     if constexpr (F16) tc5::mma_f16(tmem_d, adesc, bdesc, idesc<true>(), acc);
@@ -211,6 +224,7 @@ tc_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         const int row = quarter * 32 + lane;
         int32_t *my_hits = s_hits + et * STAGE_CAP;
         const float c1h = a.c1h * a.sc;   // acc is scaled by sc = 2^(a+b) (exact)
+        const unsigned long long nc1h2 = f2pack_tc(-c1h, -c1h);
         uint32_t acc = 0, aphase = 0, aslot = 0, aph = 0;
         unsigned long long wcur = 0, wend = 0;   // this warp's claimed pair-list block
         for (int64_t item = blockIdx.x; item < a.total_items; item += gridDim.x) {
@@ -218,12 +232,12 @@ tc_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             tc_locate(a, item, b, c0, c1);
             const int64_t sp = b * TM + row;
             const float bi = sp < a.m ? fmaf(a.qbar[sp], a.c1h, -a.r2h) * a.sc : INFINITY;
+            int nh = 0;   // staged hits of this row (kept across the item's tiles)
             for (int64_t t0 = c0; t0 < c1; t0 += TN) {
                 const float *av = a_vals + aslot * TN + slice * COLS;
                 mbar_wait_u32(smem_u32(&afull[aslot]), aph);
                 mbar_wait_u32(smem_u32(&tfull[acc]), aphase);
                 tc_fence_after();
-                int nh = 0;
                 const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + acc * TN + slice * COLS;
                 const int nch = a.diag == 1 ? 0 : COLS / 32;   // diag 1: no epilogue work
 #pragma unroll 1
@@ -232,12 +246,10 @@ tc_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     tmem_ld32(taddr + ch * 32, v);
                     const float4 *a4 = reinterpret_cast<const float4 *>(av + ch * 32);
 #pragma unroll
-                    for (int c4 = 0; c4 < 8; ++c4) {   // v = acc - xbar (1 - c1/2)
+                    for (int c4 = 0; c4 < 8; ++c4) {   // v = acc - xbar (1 - c1/2), two columns per FFMA2
                         const float4 w = a4[c4];
-                        v[4 * c4 + 0] = fmaf(-w.x, c1h, v[4 * c4 + 0]);
-                        v[4 * c4 + 1] = fmaf(-w.y, c1h, v[4 * c4 + 1]);
-                        v[4 * c4 + 2] = fmaf(-w.z, c1h, v[4 * c4 + 2]);
-                        v[4 * c4 + 3] = fmaf(-w.w, c1h, v[4 * c4 + 3]);
+                        ffma2_inplace(v[4 * c4 + 0], v[4 * c4 + 1], w.x, w.y, nc1h2);
+                        ffma2_inplace(v[4 * c4 + 2], v[4 * c4 + 3], w.z, w.w, nc1h2);
                     }
                     float m[11];
 #pragma unroll
@@ -275,8 +287,11 @@ tc_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 mbar_arrive(smem_u32(&aempty[aslot]));
                 if (++aslot == ARING) { aslot = 0; aph ^= 1; }
                 // staged hits -> the warp's claimed block of the pair list (one global
-                // atomic per CLAIM slots instead of one per tile); unused slots get q = -1
-                if (__any_sync(0xffffffffu, nh > 0)) {
+                // atomic per CLAIM slots instead of one per tile); unused slots get q = -1.
+                // The stage is flushed when it is half full or at the item's last tile (the
+                // row sp changes with the item), not after every tile.
+                const bool item_end = t0 + TN >= c1;
+                if (__any_sync(0xffffffffu, nh > (item_end ? 0 : STAGE_CAP / 2 - 1))) {
                     int incl = nh;
 #pragma unroll
                     for (int o = 1; o < 32; o <<= 1) {
@@ -302,6 +317,7 @@ tc_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                         }
                     }
                     wcur += (unsigned long long)total;
+                    nh = 0;
                 }
                 acc ^= 1;
                 if (acc == 0) aphase ^= 1;
