@@ -122,6 +122,10 @@ tc_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     uint64_t *qfull = bars + 2 * NST + 4 + 2 * ARING, *qempty = qfull + 2;
     uint32_t *tmem_ptr = reinterpret_cast<uint32_t *>(qfull + 4);
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t hint = a.wait_hint;
+    auto twait = [hint](uint32_t bar, uint32_t ph) {
+        if (hint) mbar_wait_u32_sleep(bar, ph, hint); else mbar_wait_u32(bar, ph);
+    };
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
@@ -151,19 +155,19 @@ tc_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 tc_locate(a, item, b, c0, c1);
                 if (ARES) {
                     if (c1 <= c0) continue;
-                    mbar_wait_u32(smem_u32(&qempty[qs]), qph ^ 1);
+                    twait(smem_u32(&qempty[qs]), qph ^ 1);
                     mbar_arrive_expect_tx(&qfull[qs], A_BYTES);
                     tma_load_2d(qbase + qs * A_BYTES, &tmA, smem_u32(&qfull[qs]), 0, (int)(b * TM));
                     if (++qs == 2) { qs = 0; qph ^= 1; }
                 }
                 for (int64_t t0 = c0; t0 < c1; t0 += TN) {
                     // x-bar slice of this tile -> a-ring slot (read by the epilogue)
-                    mbar_wait_u32(smem_u32(&aempty[aslot]), aph ^ 1);
+                    twait(smem_u32(&aempty[aslot]), aph ^ 1);
                     mbar_arrive_expect_tx(&afull[aslot], TN * 4);
                     bulk_g2s(a_vals + aslot * TN, a.xbar + t0, TN * 4, &afull[aslot]);
                     if (++aslot == ARING) { aslot = 0; aph ^= 1; }
                     for (int kb = 0; kb < a.kblocks; ++kb) {
-                        mbar_wait_u32(smem_u32(&empty[stage]), phase ^ 1);
+                        twait(smem_u32(&empty[stage]), phase ^ 1);
                         const uint32_t sa = base + stage * SB, sb = ARES ? sa : sa + A_BYTES;
                         mbar_arrive_expect_tx(&full[stage], SB);
                         if (!ARES) tma_load_2d(sa, &tmA, smem_u32(&full[stage]), kb * TK, (int)(b * TM));
@@ -183,15 +187,15 @@ tc_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 tc_locate(a, item, b, c0, c1);
                 if (ARES) {
                     if (c1 <= c0) continue;
-                    mbar_wait_u32(smem_u32(&qfull[qs]), qph);
+                    twait(smem_u32(&qfull[qs]), qph);
                     tc_fence_after();
                 }
                 for (int64_t t0 = c0; t0 < c1; t0 += TN) {
-                    mbar_wait_u32(smem_u32(&tempty[acc]), aphase ^ 1);
+                    twait(smem_u32(&tempty[acc]), aphase ^ 1);
                     tc_fence_after();
                     const uint32_t dcol = tmem + acc * TN;
                     for (int kb = 0; kb < a.kblocks; ++kb) {
-                        mbar_wait_u32(smem_u32(&full[stage]), phase);
+                        twait(smem_u32(&full[stage]), phase);
                         tc_fence_after();
                         const uint32_t sa = ARES ? qbase + qs * A_BYTES : base + stage * SB;
                         const uint32_t sb = ARES ? base + stage * SB : sa + A_BYTES;
@@ -235,8 +239,8 @@ tc_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             int nh = 0;   // staged hits of this row (kept across the item's tiles)
             for (int64_t t0 = c0; t0 < c1; t0 += TN) {
                 const float *av = a_vals + aslot * TN + slice * COLS;
-                mbar_wait_u32(smem_u32(&afull[aslot]), aph);
-                mbar_wait_u32(smem_u32(&tfull[acc]), aphase);
+                twait(smem_u32(&afull[aslot]), aph);
+                twait(smem_u32(&tfull[acc]), aphase);
                 tc_fence_after();
                 const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + acc * TN + slice * COLS;
                 const int nch = a.diag == 1 ? 0 : COLS / 32;   // diag 1: no epilogue work

@@ -75,6 +75,22 @@ __device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t phase) {
     }
 }
 
+// try_wait with a suspend-time hint: the waiting thread sleeps until the phase completes
+// (or the hint elapses) instead of re-issuing the probe, leaving issue slots to the
+// other warps of its SM sub-partition
+__device__ __forceinline__ void mbar_wait_u32_sleep(uint32_t bar, uint32_t phase, uint32_t hint_ns) {
+    uint32_t ok = 0;
+    while (!ok) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(bar), "r"(phase), "r"(hint_ns)
+            : "memory");
+    }
+}
+
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
     uint32_t r[32];
     asm volatile(

@@ -30,6 +30,9 @@ for s in $STAGES; do
         CMD="python bench.py --config c5 --steps 1 --warmup 3 --no-cpu-baseline"
         $CMD > $OUT/plaind_c5.log 2>&1 && timeout 1200 ncu --set full --clock-control none --import-source on -k regex:core_count -s 3 -c 1 -o $OUT/core_c5 $CMD > $OUT/ncu_core_c5.log 2>&1; echo "ncu core c5 rc=$?"
         timeout 1200 ncu --set full --clock-control none --import-source on -k regex:window_lowd -s 6 -c 1 -o $OUT/union_c5 $CMD > $OUT/ncu_union_c5.log 2>&1; echo "ncu union c5 rc=$?" ;;
+    ncu_write_c2)
+        CMD="python bench.py --config c2 --steps 1 --warmup 3 --no-cpu-baseline"
+        $CMD > $OUT/plainw_c2.log 2>&1 && timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"compact_lowd_bal|rows_finalize" -s 8 -c 2 -o $OUT/write_c2 $CMD > $OUT/ncu_write_c2.log 2>&1; echo "ncu write c2 rc=$?" ;;
     ncu_gram_c4)
         CMD="python bench.py --config c4 --steps 1 --warmup 3 --no-cpu-baseline"
         $CMD > $OUT/plaing_c4.log 2>&1 && timeout 1200 ncu --set full --clock-control none --import-source on -k regex:gram_tc -s 3 -c 1 -o $OUT/gram_c4 $CMD > $OUT/ncu_gram_c4.log 2>&1; echo "ncu gram c4 rc=$?" ;;
