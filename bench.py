@@ -434,6 +434,7 @@ def run_gpu(args):
             e2e_times.append(e0.elapsed_time(e1))
     e2e_serial_ms = max_over_ranks(sum(e2e_times), world, dev)
     e2e_ms, e2e_mode = e2e_serial_ms, "serial: every step's H2D, build, query and D2H back to back"
+    e2e_pipelined_ms = None
     if not dbscan:
         # pipelined: step k's CSR copy-out (snn_result_copy_async on a copy stream, into one of
         # two pinned host buffer sets) runs under step k+1's H2D + build + query; the timed
@@ -502,9 +503,12 @@ def run_gpu(args):
         for rr, ev in pending:
             ev.synchronize()
             snn.snn_result_free(rr)
-        e2e_ms = max_over_ranks(piped_ms, world, dev)
-        e2e_mode = ("pipelined: step k's D2H copy (snn_result_copy_async, copy stream, double-buffered "
-                    "pinned host CSR) overlaps step k+1's H2D + build + query")
+        piped_ms = max_over_ranks(piped_ms, world, dev)
+        if piped_ms < e2e_ms:   # both schedules copy every step's input and result; report the faster
+            e2e_ms = piped_ms
+            e2e_mode = ("pipelined: step k's D2H copy (snn_result_copy_async, copy stream, double-buffered "
+                        "pinned host CSR) overlaps step k+1's H2D + build + query")
+        e2e_pipelined_ms = piped_ms
     e2e_value = (w.m * args.steps if shard else weak_units(w.m * args.steps, world)) / (e2e_ms / 1e3)
     # bytes per step of the whole job: replicas copy everything on every rank; shards copy
     # X (replicated build) and the offsets on every rank, each entry once (nnz = all parts)
@@ -529,7 +533,8 @@ def run_gpu(args):
             "clocks": clocks, "gpu_launches": launches,
             "e2e": {"value": e2e_value, "unit": unit, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.steps, "mode": e2e_mode,
-                    "serial_ms_per_step": e2e_serial_ms / args.steps},
+                    "serial_ms_per_step": e2e_serial_ms / args.steps,
+                    "pipelined_ms_per_step": None if e2e_pipelined_ms is None else e2e_pipelined_ms / args.steps},
             "roofline": roofline}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, k, dt, threads, sample = oracle_sample_rate(w, args.cpu_seconds)

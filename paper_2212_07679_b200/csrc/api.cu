@@ -524,8 +524,12 @@ static snn_status build_impl(const void *X, int64_t n, int32_t d, snn_dtype dt, 
                       idx->mu_d, idx->Xs, idx->xbar, s);                           // K5
     CKI(cudaGetLastError(), "launch");
     double *hs = static_cast<double *>(t_pinned.p);
-    CKI(small_readback(hs, idx->stats, ST_COUNT * 8, s), "D2H stats");
-    CKI(small_readback(hs + ST_COUNT, flag, 4, s), "D2H flag");
+    {
+        ReadbackBatch rb;
+        rb.add(hs, idx->stats, ST_COUNT * 8);
+        rb.add(hs + ST_COUNT, flag, 4);
+        CKI(small_readback_batch(rb, s), "D2H stats");
+    }
     CKI(cudaStreamSynchronize(s), "build");
     memcpy(idx->h_stats, hs, sizeof(idx->h_stats));
     int nonfinite = *reinterpret_cast<int *>(hs + ST_COUNT);
@@ -646,8 +650,12 @@ static snn_status pairs_to_csr(Workspace &ws, cudaStream_t s, int64_t m, int64_t
     launch_pairs_row_count(flag, pq, qperm, P, m, row_count, maxrow, s);
     exclusive_scan_i32_to_i64(row_count, r->offsets, m, scan_tmp, s);
     int64_t *hp = static_cast<int64_t *>(t_pinned.p);
-    if ((e = small_readback(hp, r->offsets + m, 8, s)) != cudaSuccess) return bail(e, "D2H");
-    if ((e = small_readback(hp + 1, maxrow, 4, s)) != cudaSuccess) return bail(e, "D2H");
+    {
+        ReadbackBatch rb;
+        rb.add(hp, r->offsets + m, 8);
+        rb.add(hp + 1, maxrow, 4);
+        if ((e = small_readback_batch(rb, s)) != cudaSuccess) return bail(e, "D2H");
+    }
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return bail(e, "recheck");
     const int64_t H = hp[0];
     const int32_t mr = *reinterpret_cast<int32_t *>(hp + 1);
@@ -739,10 +747,14 @@ static snn_status query_tc(snn_index idx, Workspace &ws, cudaStream_t s, int sms
     launch_tc_group_items(blk_lo, blk_hi, nblocks, (int)G, chunk, grp_lo, grp_items, s);
     exclusive_scan_i64(grp_items, grp_start, ngroups, scan_tmp, s);
     int64_t *hp = static_cast<int64_t *>(t_pinned.p);
-    CK(small_readback(hp, grp_start + ngroups, 8, s), "D2H items");
-    CK(small_readback(hp + 1, qflag, 4, s), "D2H flag");
-    CK(small_readback(hp + 2, wpairs, 8, s), "D2H pairs");
-    if (Qd) CK(small_readback(hp + 3, eq + 1, 8, s), "D2H query bound");
+    {
+        ReadbackBatch rb;
+        rb.add(hp, grp_start + ngroups, 8);
+        rb.add(hp + 1, qflag, 4);
+        rb.add(hp + 2, wpairs, 8);
+        if (Qd) rb.add(hp + 3, eq + 1, 8);
+        CK(small_readback_batch(rb, s), "D2H windows");
+    }
     CK(cudaStreamSynchronize(s), "query windows");
     const int64_t total_items = hp[0];
     if (*reinterpret_cast<int *>(hp + 1)) return fail(SNN_ERR_NONFINITE, "Q contains NaN or Inf");
@@ -893,10 +905,14 @@ static snn_status query_tcl(snn_index idx, Workspace &ws, cudaStream_t s, int sm
     launch_tcl_items(blk_lo, blk_hi, nblocks, (int)G, chunk, bcount, s);
     exclusive_scan_i64(bcount, bstart, nblocks, scan_tmp, s);
     int64_t *hp = static_cast<int64_t *>(t_pinned.p);
-    CK(small_readback(hp, bstart + nblocks, 8, s), "D2H items");
-    CK(small_readback(hp + 1, qflag, 4, s), "D2H flag");
-    CK(small_readback(hp + 2, wpairs, 8, s), "D2H pairs");
-    if (!self) CK(small_readback(hp + 3, eq + 1, 8, s), "D2H query bound");
+    {
+        ReadbackBatch rb;
+        rb.add(hp, bstart + nblocks, 8);
+        rb.add(hp + 1, qflag, 4);
+        rb.add(hp + 2, wpairs, 8);
+        if (!self) rb.add(hp + 3, eq + 1, 8);
+        CK(small_readback_batch(rb, s), "D2H windows");
+    }
     CK(cudaStreamSynchronize(s), "query windows");
     const int64_t total_items = hp[0];
     if (*reinterpret_cast<int *>(hp + 1)) return fail(SNN_ERR_NONFINITE, "Q contains NaN or Inf");
@@ -1123,10 +1139,14 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
     }
     exclusive_scan_i64(nitems, item_start, nblocks, scan_tmp, s);
     int64_t *hp = static_cast<int64_t *>(t_pinned.p);
-    CK(small_readback(hp, item_start + nblocks, 8, s), "D2H items");
-    CK(small_readback(hp + 1, qflag, 4, s), "D2H flag");
-    CK(small_readback(hp + 2, pairs, 8, s), "D2H pairs");
-    if (own_dev) CK(small_readback(hp + 3, own_dev, 16, s), "D2H part range");
+    {
+        ReadbackBatch rb;
+        rb.add(hp, item_start + nblocks, 8);
+        rb.add(hp + 1, qflag, 4);
+        rb.add(hp + 2, pairs, 8);
+        if (own_dev) rb.add(hp + 3, own_dev, 16);
+        CK(small_readback_batch(rb, s), "D2H windows");
+    }
     CK(cudaStreamSynchronize(s), "query windows");
     const int64_t total_items = hp[0];
     const double pairs_eval = (double)*reinterpret_cast<unsigned long long *>(hp + 2);
@@ -1230,10 +1250,11 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
         a.soff = soff;
     }
     {
-        cudaError_t e = small_readback(hp, r->offsets + m, 8, s);
-        if (e == cudaSuccess && a.ovf_count)
-            e = small_readback(hp + 1, a.ovf_count, 8, s);
-        if (e == cudaSuccess && maxl) e = small_readback(hp + 2, maxl, 4, s);
+        ReadbackBatch rb;
+        rb.add(hp, r->offsets + m, 8);
+        if (a.ovf_count) rb.add(hp + 1, a.ovf_count, 8);
+        if (maxl) rb.add(hp + 2, maxl, 4);
+        cudaError_t e = small_readback_batch(rb, s);
         if (e == cudaSuccess) e = cudaStreamSynchronize(s);
         if (e != cudaSuccess) return bail(e, "query count");
     }

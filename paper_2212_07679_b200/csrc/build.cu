@@ -774,6 +774,33 @@ __global__ void readback_kernel(uint8_t *dst, const uint8_t *src, int n) {
 // memory instead of cudaMemcpyAsync: a copy would queue on the device-to-host copy engine
 // behind any large transfer in flight (e.g. the previous result's copy-out on another
 // stream), stalling the whole call until that transfer ends.
+__global__ void readback_batch_kernel(ReadbackBatch b) {
+    for (int e = 0; e < b.n; ++e) {
+        uint8_t *dst = static_cast<uint8_t *>(b.dst[e]);
+        const uint8_t *src = static_cast<const uint8_t *>(b.src[e]);
+        for (int i = threadIdx.x; i < b.bytes[e]; i += blockDim.x) dst[i] = src[i];
+    }
+}
+
+// several small readbacks in one launch (the destinations' device aliases resolved here)
+cudaError_t small_readback_batch(ReadbackBatch b, cudaStream_t s) {
+    if (b.n == 0) return cudaSuccess;
+    for (int e = 0; e < b.n; ++e) {
+        void *dptr = nullptr;
+        if (b.bytes[e] > 4096 || cudaHostGetDevicePointer(&dptr, b.dst[e], 0) != cudaSuccess) {
+            cudaGetLastError();   // not mapped pinned memory: one copy per entry
+            for (int f = 0; f < b.n; ++f) {
+                cudaError_t x = cudaMemcpyAsync(b.dst[f], b.src[f], (size_t)b.bytes[f], cudaMemcpyDeviceToHost, s);
+                if (x != cudaSuccess) return x;
+            }
+            return cudaSuccess;
+        }
+        b.dst[e] = dptr;
+    }
+    SNN_LAUNCH(readback_batch_kernel, 1, 128, 0, s, b);
+    return cudaGetLastError();
+}
+
 cudaError_t small_readback(void *host, const void *dev, size_t bytes, cudaStream_t s) {
     void *dptr = nullptr;
     if (bytes > 4096 || cudaHostGetDevicePointer(&dptr, host, 0) != cudaSuccess) {

@@ -27,6 +27,14 @@ void launch_scale_f64(double *x, int64_t count, double f, cudaStream_t s);
 void launch_set_f64(double *x, double v, cudaStream_t s);
 // small device -> host readback into PINNED host memory by a kernel (no copy engine)
 cudaError_t small_readback(void *host, const void *dev, size_t bytes, cudaStream_t s);
+struct ReadbackBatch {
+    void *dst[8];
+    const void *src[8];
+    int bytes[8];
+    int n = 0;
+    void add(void *h, const void *d, int nb) { dst[n] = h; src[n] = d; bytes[n] = nb; ++n; }
+};
+cudaError_t small_readback_batch(ReadbackBatch b, cudaStream_t s);
 // K2b: power iteration on G (d x d, fp64).  Writes v_d (fp64 unit), v_f (fp32), and
 // stats[]: see enum Stat.  maxabs_bits/mu feed the key error bound E_x.
 enum Stat {

@@ -36,5 +36,13 @@ for s in $STAGES; do
     ncu_gram_c4)
         CMD="python bench.py --config c4 --steps 1 --warmup 3 --no-cpu-baseline"
         $CMD > $OUT/plaing_c4.log 2>&1 && timeout 1200 ncu --set full --clock-control none --import-source on -k regex:gram_tc -s 3 -c 1 -o $OUT/gram_c4 $CMD > $OUT/ncu_gram_c4.log 2>&1; echo "ncu gram c4 rc=$?" ;;
+    summarize)   # text summaries of every capture, then drop the .ncu-rep files (gpurun_out <= 64 MiB)
+        for r in $OUT/*.ncu-rep; do [ -f "$r" ] || continue; b=${r%.ncu-rep}
+            python scripts/ncu_summary.py full $r > ${b}_metrics.txt 2>&1
+            python scripts/ncu_source.py $r 40 > ${b}_source_top40.txt 2>&1
+            ncu -i $r --page raw --csv > ${b}_raw.csv 2>/dev/null; gzip -f ${b}_raw.csv
+            rm -f $r; done
+        for c in $OUT/launches_*.csv; do [ -f "$c" ] || continue; python scripts/ncu_summary.py launches $c > ${c%.csv}_summary.txt 2>&1; done
+        du -sh $OUT ;;
   esac
 done
