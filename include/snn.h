@@ -298,6 +298,8 @@ snn_status snn_profile_read(const char *family, double *ms, uint64_t *launches, 
  *                    -1 = every row)
  *   "finalize_order" -1 = row assembly walks rows in key order (default: original-id order,
  *                    sequential CSR writes)
+ *   "count_warp"     -1 = DBSCAN core counts by one CTA per query block over whole chunks
+ *                    (default: one warp per point, scanning outward from its position)
  *   "union_load"     DBSCAN union pass: how the parent[j] pre-check is loaded (1 = default
  *                    ld.relaxed.gpu, -1 volatile, 2 ld.global.cg; every value is a valid
  *                    filter; snn_get_option reports 0 volatile / 1 relaxed / 2 cg)

@@ -51,6 +51,7 @@ struct Options {
     int lowd_tc_tiles = 8;     // 256-candidate tiles per work item (low-d tensor-core path)
     int lowd_tc_group = 8;     // query blocks per raster group (low-d tensor-core path)
     int union_load = 1;        // DBSCAN union pass: parent pre-check load (0 volatile, 1 relaxed.gpu, 2 ld.cg)
+    int count_warp = 1;        // DBSCAN core counts: warp per point, outward scan (-1: CTA per block)
     int finalize_order = 1;    // staged rows: rows_finalize walks rows in original-id order (sequential CSR writes)
     int gram_rows = 65536;     // tensor-core Gram of a large build: rows sampled (stride) down to ~this many
     int64_t gram_min_elems = int64_t(1) << 27;   // ... when n*d is at least this
@@ -114,6 +115,7 @@ static void prof_drain() {
 }
 
 bool dbscan_simt_filter() { return g_opt.simt_filter > 0; }
+int dbscan_count_warp() { return g_opt.count_warp; }
 int dbscan_union_load() { return g_opt.union_load; }
 
 snn_status fail(snn_status st, const std::string &msg) {
@@ -306,7 +308,8 @@ snn_status snn_get_option(const char *key, int64_t *value) {
         {"window_all", &Options::window_all}, {"simt_filter", &Options::simt_filter},
         {"lowd_tc", &Options::lowd_tc}, {"lowd_tc_tiles", &Options::lowd_tc_tiles},
         {"lowd_tc_group", &Options::lowd_tc_group}, {"union_load", &Options::union_load},
-        {"finalize_order", &Options::finalize_order}, {"gram_rows", &Options::gram_rows}};
+        {"finalize_order", &Options::finalize_order}, {"gram_rows", &Options::gram_rows},
+        {"count_warp", &Options::count_warp}};
     for (const auto &o : kInt)
         if (strcmp(key, o.name) == 0) { *value = g_opt.*(o.field); return SNN_OK; }
     if (strcmp(key, "ovf_records") == 0) { *value = g_opt.ovf_rec_cap; return SNN_OK; }
@@ -382,6 +385,7 @@ snn_status snn_set_option(const char *key, int64_t value) {
     if (k == "gram_rows") { g_opt.gram_rows = value == 0 ? 65536 : (value < 0 ? 0 : (int)value); return SNN_OK; }
     if (k == "gram_min_elems") { g_opt.gram_min_elems = value == 0 ? (int64_t(1) << 27) : value; return SNN_OK; }
     if (k == "finalize_order") { g_opt.finalize_order = value < 0 ? 0 : 1; return SNN_OK; }
+    if (k == "count_warp") { g_opt.count_warp = value < 0 ? 0 : 1; return SNN_OK; }
     if (k == "union_load") {
         if (value < -1 || value > 2) return fail(SNN_ERR_INVALID_ARGUMENT, "union_load must be -1..2");
         g_opt.union_load = value == -1 ? 0 : (value == 0 ? 1 : (int)value);   // 0: the default (relaxed)

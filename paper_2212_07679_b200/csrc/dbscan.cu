@@ -261,6 +261,7 @@ snn_status dbscan_impl(snn_index idx, double eps, int32_t min_pts, int32_t *labe
     a.cnt = cnt; a.pre = cnt; a.cap = 0; a.variant = 1;
     a.sm_count = idx->sm_count;
     a.core = core; a.parent = parent; a.best = best; a.min_pts = min_pts;
+    a.count_warp = dbscan_count_warp();
     a.n_index = n;
     if (!f64 && idx->Xf && dbscan_simt_filter()) {   // expanded-form SIMT pre-filter (option)
         double c1h = 1.0, r2h = 0.0;

@@ -91,6 +91,7 @@ struct snn_result_s {
 namespace snn {
 bool dbscan_simt_filter();   // option simt_filter (api.cu)
 int dbscan_union_load();     // option union_load (api.cu)
+int dbscan_count_warp();     // option count_warp (api.cu)
 // metric adapters (metric.cu): exact row normalization (flag = 1 on a zero row), radius
 // mapping and in-place distance conversion
 void launch_normalize_rows(const void *X, bool f64, int64_t n, int d, void *out, int *zero_flag, cudaStream_t s);

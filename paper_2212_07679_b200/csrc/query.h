@@ -82,6 +82,7 @@ struct PassArgs {
     int32_t min_pts;        // M_COUNT: counts are only needed up to min_pts (early exit)
     int64_t n_index = 0;    // M_UNION: number of index points (parent array length)
     int uload = 1;          // M_UNION pre-check load of parent[j]: 0 volatile, 1 ld.relaxed.gpu, 2 ld.cg
+    int count_warp = 0;     // DBSCAN core counts: one warp per point scanning outward (core_count_warp_kernel)
     // symmetric self-query (each unordered pair evaluated once): the scan keeps only
     // candidates j > i (U rows) and counts the mirrored hits per candidate; the mirrored
     // entries (L rows) are scattered during compaction and sorted per row afterwards

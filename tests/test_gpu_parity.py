@@ -360,6 +360,25 @@ def test_dbscan_full_parity(snn, n, seed, box, eps, mp, dt):
     assert np.array_equal(lab, ref)
 
 
+@pytest.mark.parametrize("n,box,dt", [(200000, 400.0, np.float32), (60000, 500.0, np.float32),
+                                      (30000, 150.0, np.float64)])
+def test_dbscan_core_count_modes_identical(snn, n, box, dt):
+    """Core counts by one warp per point scanning outward (default) and by one CTA per
+    query block over whole chunks (count_warp = -1): identical labels, equal to the grid
+    oracle's (reading C18)."""
+    import paper_2212_07679_b200 as p
+    X = workloads.c5(n=n, seed=31, box=box).X.astype(dt)
+    ref, Kr, _ = oracle.dbscan(X, 3.0, 5, grid=True)
+    lab1, K1 = _gpu_dbscan(snn, X, 3.0, 5)
+    try:
+        p.snn_set_option("count_warp", -1)
+        lab2, K2 = _gpu_dbscan(snn, X, 3.0, 5)
+    finally:
+        p.snn_set_option("count_warp", 0)
+    assert K1 == K2 == Kr
+    assert np.array_equal(lab1, ref) and np.array_equal(lab2, ref)
+
+
 @pytest.mark.parametrize("d,dt", [(16, np.float32), (40, np.float32), (12, np.float64)])
 def test_dbscan_high_d_parity(snn, d, dt):
     """d > 8: DBSCAN over the exact self-query CSR; labels equal the oracle's."""
