@@ -303,6 +303,20 @@ snn_status snn_profile_read(const char *family, double *ms, uint64_t *launches, 
  *   "union_load"     DBSCAN union pass: how the parent[j] pre-check is loaded (1 = default
  *                    ld.relaxed.gpu, -1 volatile, 2 ld.global.cg; every value is a valid
  *                    filter; snn_get_option reports 0 volatile / 1 relaxed / 2 cg)
+ *                    (applies to the window_lowd union pass, union_snap = -1)
+ *   "union_snap"     DBSCAN union pass for fp32, d <= 8: 1 = default, the staged root-snapshot
+ *                    kernel (a pair reaches the union path only when its staged root differs
+ *                    from the query's); -1 = window_lowd union pass; 2 = the same kernel
+ *                    without the register cap; 3, 4 = diagnostics only (no unions, labels
+ *                    NOT valid)
+ *   "union_behind"   union_snap pass: 1 = default, candidates behind the block (pairs j < i,
+ *                    already settled); -1 = candidates ahead (pairs j > i)
+ *   "union_chunk"    union_snap pass: candidates per work item (default 512; 64..8192)
+ *   "union_phased"   union_snap pass: 1 = one launch per chunk index (chunk k of every block);
+ *                    default off
+ *   "union_stats"    1 = count the union_snap pass's union-path pairs; read back with
+ *                    snn_get_option("last_union_path" / "last_union_hits" / "last_union_links")
+ *   "dbscan_block"   DBSCAN queries per block (default 256; 32..256, multiple of 32)
  *   "simt_filter"    low-d fp32 expanded-form pre-filter: default on for radius queries and
  *                    off for DBSCAN; 1 = on everywhere, -1 = off everywhere
  *   "lowd_tc", "lowd_tc_tiles", "lowd_tc_group"   low-d tcgen05 path (default off)

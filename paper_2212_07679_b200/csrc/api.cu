@@ -52,6 +52,12 @@ struct Options {
     int lowd_tc_group = 8;     // query blocks per raster group (low-d tensor-core path)
     int union_load = 1;        // DBSCAN union pass: parent pre-check load (0 volatile, 1 relaxed.gpu, 2 ld.cg)
     int count_warp = 1;        // DBSCAN core counts: warp per point, outward scan (-1: CTA per block)
+    int union_snap = 1;        // DBSCAN union pass (fp32, d <= 8): staged parent snapshot pre-check (-1: window_lowd)
+    int union_behind = 1;      // DBSCAN union pass (union_snap): candidates behind the block (pairs j < i)
+    int dbscan_block = 256;    // DBSCAN: queries per block (windows, union and border passes)
+    int union_chunk = 512;     // DBSCAN union pass (union_snap): candidates per work item
+    int union_phased = 0;      // DBSCAN union pass (union_snap): chunk k of every block in launch k (near pairs first)
+    int union_stats = 0;       // DBSCAN union pass: count pairs sent to the union path (diagnostics)
     int finalize_order = 1;    // staged rows: rows_finalize walks rows in original-id order (sequential CSR writes)
     int gram_rows = 65536;     // tensor-core Gram of a large build: rows sampled (stride) down to ~this many
     int64_t gram_min_elems = int64_t(1) << 27;   // ... when n*d is at least this
@@ -117,6 +123,16 @@ static void prof_drain() {
 bool dbscan_simt_filter() { return g_opt.simt_filter > 0; }
 int dbscan_count_warp() { return g_opt.count_warp; }
 int dbscan_union_load() { return g_opt.union_load; }
+int dbscan_union_snap() { return g_opt.union_snap; }
+bool dbscan_union_phased() { return g_opt.union_phased > 0; }
+bool dbscan_union_behind() { return g_opt.union_behind > 0; }
+int dbscan_union_chunk() { return g_opt.union_chunk; }
+int dbscan_block() { return g_opt.dbscan_block; }
+static thread_local int64_t g_last_union[3] = {0, 0, 0};
+bool dbscan_union_stats() { return g_opt.union_stats > 0; }
+void dbscan_set_union_stats(const unsigned long long *v) {
+    for (int i = 0; i < 3; ++i) g_last_union[i] = (int64_t)v[i];
+}
 
 snn_status fail(snn_status st, const std::string &msg) {
     t_err = msg;
@@ -309,11 +325,18 @@ snn_status snn_get_option(const char *key, int64_t *value) {
         {"lowd_tc", &Options::lowd_tc}, {"lowd_tc_tiles", &Options::lowd_tc_tiles},
         {"lowd_tc_group", &Options::lowd_tc_group}, {"union_load", &Options::union_load},
         {"finalize_order", &Options::finalize_order}, {"gram_rows", &Options::gram_rows},
-        {"count_warp", &Options::count_warp}};
+        {"count_warp", &Options::count_warp}, {"union_snap", &Options::union_snap},
+        {"union_stats", &Options::union_stats}, {"union_phased", &Options::union_phased},
+        {"union_behind", &Options::union_behind}, {"union_chunk", &Options::union_chunk},
+        {"dbscan_block", &Options::dbscan_block}};
     for (const auto &o : kInt)
         if (strcmp(key, o.name) == 0) { *value = g_opt.*(o.field); return SNN_OK; }
     if (strcmp(key, "ovf_records") == 0) { *value = g_opt.ovf_rec_cap; return SNN_OK; }
     if (strcmp(key, "gram_min_elems") == 0) { *value = g_opt.gram_min_elems; return SNN_OK; }
+    // read-only diagnostics of this thread's last DBSCAN union pass (option union_stats)
+    if (strcmp(key, "last_union_path") == 0) { *value = g_last_union[0]; return SNN_OK; }
+    if (strcmp(key, "last_union_hits") == 0) { *value = g_last_union[1]; return SNN_OK; }
+    if (strcmp(key, "last_union_links") == 0) { *value = g_last_union[2]; return SNN_OK; }
     return fail(SNN_ERR_INVALID_ARGUMENT, std::string("unknown option ") + key);
 }
 
@@ -386,6 +409,26 @@ snn_status snn_set_option(const char *key, int64_t value) {
     if (k == "gram_min_elems") { g_opt.gram_min_elems = value == 0 ? (int64_t(1) << 27) : value; return SNN_OK; }
     if (k == "finalize_order") { g_opt.finalize_order = value < 0 ? 0 : 1; return SNN_OK; }
     if (k == "count_warp") { g_opt.count_warp = value < 0 ? 0 : 1; return SNN_OK; }
+    if (k == "union_snap") {   // 0: default; -1 off; 2: register-capped variant; 3, 4: diagnostics (labels invalid)
+        if (value < -1 || value > 4) return fail(SNN_ERR_INVALID_ARGUMENT, "union_snap must be -1..4");
+        g_opt.union_snap = value < 0 ? 0 : (value == 0 ? 1 : (int)value);
+        return SNN_OK;
+    }
+    if (k == "union_phased") { g_opt.union_phased = value > 0 ? 1 : 0; return SNN_OK; }   // 0: default (off)
+    if (k == "dbscan_block") {
+        if (value == 0) value = 256;
+        if (value < 32 || value > 256 || value % 32) return fail(SNN_ERR_INVALID_ARGUMENT, "dbscan_block must be 32..256, multiple of 32");
+        g_opt.dbscan_block = (int)value;
+        return SNN_OK;
+    }
+    if (k == "union_chunk") {
+        if (value == 0) value = 512;
+        if (value < 64 || value > 8192 || value % 64) return fail(SNN_ERR_INVALID_ARGUMENT, "union_chunk must be 64..8192, multiple of 64");
+        g_opt.union_chunk = (int)value;
+        return SNN_OK;
+    }
+    if (k == "union_behind") { g_opt.union_behind = value < 0 ? 0 : 1; return SNN_OK; }
+    if (k == "union_stats") { g_opt.union_stats = value > 0 ? 1 : 0; return SNN_OK; }
     if (k == "union_load") {
         if (value < -1 || value > 2) return fail(SNN_ERR_INVALID_ARGUMENT, "union_load must be -1..2");
         g_opt.union_load = value == -1 ? 0 : (value == 0 ? 1 : (int)value);   // 0: the default (relaxed)

@@ -182,7 +182,7 @@ snn_status dbscan_impl(snn_index idx, double eps, int32_t min_pts, int32_t *labe
                        int32_t *n_clusters, cudaStream_t s) {
     const int64_t n = idx->n;
     const bool f64 = idx->dt == SNN_F64;
-    const int B = 256, chunk = 2048;
+    const int B = dbscan_block(), chunk = 2048;   // queries per block (option dbscan_block)
     const int64_t nblocks = ceil_div(n, B);
     Workspace ws(s);
 #define CKD(expr, where)                                       \
@@ -277,7 +277,8 @@ snn_status dbscan_impl(snn_index idx, double eps, int32_t min_pts, int32_t *labe
     CKD(cudaMemsetAsync(pairs, 0, 8, s), "memset");
     launch_core_counts(a, count, pairs, s);                                 // counts (to min_pts)
     SNN_LAUNCH(init_core, grid_n(n), 256, 0, s, count, n, min_pts, core, parent, minid, best);
-    {   // unions over the clipped windows (pairs j > i only: block b starts at its first position)
+    {   // unions over the clipped windows (pairs j > i: block b starts at its first position;
+        // or pairs j < i: block b's window ends after its last position)
         int64_t *lo2, *nit2, *st2;
         CKD(ws.alloc(&lo2, (size_t)nblocks), "alloc");
         CKD(ws.alloc(&nit2, (size_t)nblocks), "alloc");
@@ -285,16 +286,30 @@ snn_status dbscan_impl(snn_index idx, double eps, int32_t min_pts, int32_t *labe
         unsigned long long *upairs;
         CKD(ws.alloc(&upairs, 1), "alloc");
         CKD(cudaMemsetAsync(upairs, 0, 8, s), "memset");
-        launch_truncate_windows(blk_lo, blk_hi, nblocks, B, chunk, lo2, nit2, n, n, upairs, s);
+        // staged-snapshot union pass (fp32, d <= 8): candidates behind the block by default
+        const bool snap = dbscan_union_snap() && !f64 && idx->d <= 8;
+        const bool behind = snap && dbscan_union_behind();
+        const int uchunk = snap ? dbscan_union_chunk() : chunk;   // candidates per union work item
+        if (behind)   // lo2 holds the clipped window ends
+            launch_truncate_windows_behind(blk_lo, blk_hi, nblocks, B, uchunk, lo2, nit2, n, n, upairs, s);
+        else
+            launch_truncate_windows(blk_lo, blk_hi, nblocks, B, uchunk, lo2, nit2, n, n, upairs, s);
         exclusive_scan_i64(nit2, st2, nblocks, scan_tmp, s);
         CKD(small_readback(hbuf, st2 + nblocks, 8, s), "D2H");
         CKD(small_readback(hbuf + 2, pairs, 8, s), "D2H");
         CKD(small_readback(hbuf + 3, upairs, 8, s), "D2H");
+        unsigned long long *umax = nullptr;   // most chunks of one block (phased union order)
+        CKD(ws.alloc(&umax, 1), "alloc");
+        CKD(cudaMemsetAsync(umax, 0, 8, s), "memset");
+        launch_max_i64(nit2, nblocks, umax, s);
+        CKD(small_readback(hbuf + 1, umax, 8, s), "D2H");
         CKD(cudaStreamSynchronize(s), "dbscan union windows");
         prof_end(ctok, s, (double)*reinterpret_cast<unsigned long long *>(hbuf + 2));   // pairs evaluated
         PassArgs au = a;
         au.uload = dbscan_union_load();
-        au.blk_lo = lo2; au.item_start = st2; au.total_items = hbuf[0];
+        if (behind) au.blk_hi = lo2; else au.blk_lo = lo2;
+        au.chunk = uchunk;
+        au.item_start = st2; au.total_items = hbuf[0];
         au.item_block = nullptr;
         if (au.total_items > 0 && au.total_items < (int64_t(1) << 31)) {
             int32_t *ib2 = nullptr;
@@ -303,8 +318,21 @@ snn_status dbscan_impl(snn_index idx, double eps, int32_t min_pts, int32_t *labe
             au.item_block = ib2;
         }
         const int utok = prof_begin(F_UNION, s);
-        launch_lowd_mode(3, au, s);                                          // unions
+        unsigned long long *ustats = nullptr;
+        if (dbscan_union_stats()) {
+            CKD(ws.alloc(&ustats, 3), "alloc");
+            CKD(cudaMemsetAsync(ustats, 0, 24, s), "memset");
+        }
+        if (!(snap && launch_union_snap(au, dbscan_union_snap(), nit2, dbscan_union_phased() ? hbuf[1] : 0,
+                                        behind ? 1 : 0, ustats, s)))      // unions
+            launch_lowd_mode(3, au, s);
         prof_end(utok, s, (double)*reinterpret_cast<unsigned long long *>(hbuf + 3));
+        if (ustats) {
+            unsigned long long hs[3];
+            CKD(cudaMemcpyAsync(hs, ustats, 24, cudaMemcpyDeviceToHost, s), "D2H");
+            CKD(cudaStreamSynchronize(s), "union stats");
+            dbscan_set_union_stats(hs);
+        }
     }
     SNN_LAUNCH(flatten, grid_n(n), 256, 0, s, parent, core, idx->perm, n, minid);
     CKD(cudaMemsetAsync(flag, 0, (size_t)n * 4, s), "memset");

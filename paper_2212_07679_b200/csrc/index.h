@@ -92,6 +92,13 @@ namespace snn {
 bool dbscan_simt_filter();   // option simt_filter (api.cu)
 int dbscan_union_load();     // option union_load (api.cu)
 int dbscan_count_warp();     // option count_warp (api.cu)
+int dbscan_union_snap();     // option union_snap (api.cu)
+bool dbscan_union_phased();  // option union_phased (api.cu)
+bool dbscan_union_behind();  // option union_behind (api.cu)
+int dbscan_union_chunk();    // option union_chunk (api.cu)
+int dbscan_block();          // option dbscan_block (api.cu)
+bool dbscan_union_stats();   // option union_stats (api.cu)
+void dbscan_set_union_stats(const unsigned long long *v);   // [path, hits, links] of the last union pass
 // metric adapters (metric.cu): exact row normalization (flag = 1 on a zero row), radius
 // mapping and in-place distance conversion
 void launch_normalize_rows(const void *X, bool f64, int64_t n, int d, void *out, int *zero_flag, cudaStream_t s);

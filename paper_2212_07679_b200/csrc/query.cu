@@ -301,6 +301,19 @@ __device__ __forceinline__ int32_t uf_rep(volatile int32_t *p, int32_t x) {
     }
     return cur;
 }
+// the same union, returning the root of the joined component as seen when it finished
+__device__ __forceinline__ int32_t uf_unite_root(int32_t *p, int32_t a, int32_t b) {
+    volatile int32_t *vp = p;
+    int32_t ra = uf_rep(vp, a), rb = uf_rep(vp, b);
+    while (ra != rb) {
+        if (ra < rb) { const int32_t t = ra; ra = rb; rb = t; }
+        const int32_t old = atomicCAS(&p[ra], ra, rb);
+        if (old == ra) return rb;
+        ra = uf_rep(vp, old);
+        rb = uf_rep(vp, rb);
+    }
+    return ra;
+}
 __device__ __forceinline__ void uf_unite(int32_t *p, int32_t a, int32_t b) {
     SNN_DASSERT(a >= 0 && b >= 0 && p[a] >= 0 && p[b] >= 0);   // both core points
     volatile int32_t *vp = p;
@@ -1541,6 +1554,31 @@ __global__ void truncate_windows_kernel(const int64_t *blk_lo, const int64_t *bl
 }
 }  // namespace
 
+namespace {
+// DBSCAN union pass, candidates behind: block b's window ends after its own last position
+// (rounded up to 4; pairs j < i only)
+__global__ void truncate_windows_behind_kernel(const int64_t *blk_lo, const int64_t *blk_hi, int64_t nblocks, int B,
+                                               int chunk, int64_t *hi2, int64_t *nitems2, int64_t m, int64_t n,
+                                               unsigned long long *pairs) {
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nblocks) return;
+    const int64_t last = min(m, (b + 1) * B);   // one past the block's last position
+    const int64_t lo = blk_lo[b], hi = min(blk_hi[b], round_up(last, 4));
+    hi2[b] = hi;
+    nitems2[b] = hi > lo ? ceil_div(hi - lo, chunk) : 0;
+    const int64_t vh = min(hi, n), nq = min((int64_t)B, m - b * B);
+    if (pairs && vh > lo && nq > 0) atomicAdd(pairs, (unsigned long long)((vh - lo) * nq));
+}
+}  // namespace
+
+void launch_truncate_windows_behind(const int64_t *blk_lo, const int64_t *blk_hi, int64_t nblocks, int B, int chunk,
+                                    int64_t *hi2, int64_t *nitems2, int64_t m, int64_t n, unsigned long long *pairs,
+                                    cudaStream_t s) {
+    if (nblocks == 0) return;
+    SNN_LAUNCH(truncate_windows_behind_kernel, (int)ceil_div(nblocks, 256), 256, 0, s, blk_lo, blk_hi, nblocks, B,
+               chunk, hi2, nitems2, m, n, pairs);
+}
+
 void launch_truncate_windows(const int64_t *blk_lo, const int64_t *blk_hi, int64_t nblocks, int B, int chunk,
                              int64_t *lo2, int64_t *nitems2, int64_t m, int64_t n, unsigned long long *pairs,
                              cudaStream_t s) {
@@ -1787,6 +1825,232 @@ void launch_core_counts(const PassArgs &a, int32_t *count, unsigned long long *e
 #define FN(T, D) run_core_count<T, D>(a, count, evaluated, s)
     SNN_LOWD_DISPATCH(FN)
 #undef FN
+}
+
+}  // namespace snn
+
+namespace snn {
+namespace {
+// K12 union pass with a staged parent snapshot (fp32 AoSoA4 rows, d <= 8).  For every
+// (query block, candidate chunk) item the TMA stages the chunk's rows AND its slice of
+// the union-find parents parent[c0, c1) (sorted positions, so the slice is contiguous).
+// The staged parents are turned into the candidates' current roots (one find each,
+// compressing parent[j] to the root in global memory), and a candidate pair reaches the
+// divergent union path only if it may be a neighbour (fp32 d^2 <= T_out) AND its staged
+// root is a core point's root different from the query's cached root: any ancestor of j
+// ever found stays an ancestor (links only merge components), so equality proves the
+// pair already joined and the exact test is not needed.  The predicated pre-check runs warp-converged; the rare remaining pairs
+// get the exact classification (same rigorous thresholds, oracle-order fp64 in between),
+// a fresh parent[j] check and, if that differs too, the lock-free union; the root joined
+// is written back into the snapshot.
+// ustats (nullable): [0] pairs sent to the union path, [1] exact hits among them,
+// [2] unions attempted (fresh parent differed from the cached root).
+template <int D, int MINB, int DIAG = 0>
+__global__ void __launch_bounds__(256, MINB) union_snap_kernel(PassArgs a, const int64_t *nit, int pass_k,
+                                                              int behind, unsigned long long *ustats) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int tid = threadIdx.x;
+    const float *Xs = static_cast<const float *>(a.Xs);
+    const size_t rows_bytes = (size_t)a.chunk * D * 4;
+    const size_t buf_bytes = rows_bytes + (size_t)a.chunk * 4;
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + 2 * buf_bytes);
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    auto issue = [&](int64_t item, int sidx) {
+        int64_t b, c0, c1;
+        locate(a, item, b, c0, c1);
+        const uint32_t nb = (uint32_t)((c1 - c0) * D * 4), pb = (uint32_t)((c1 - c0) * 4);
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&bar[sidx], nb + pb);
+        bulk_g2s(smem + sidx * buf_bytes, Xs + c0 * D, nb, &bar[sidx]);
+        bulk_g2s(smem + sidx * buf_bytes + rows_bytes, a.parent + c0, pb, &bar[sidx]);
+    };
+    uint32_t phase[2] = {0u, 0u};
+    unsigned long long st_path = 0, st_hit = 0, st_link = 0;
+    // pass_k >= 0: chunk pass_k of every query block (work index = block); else every item
+    const int64_t n_work = pass_k >= 0 ? a.nblocks : a.total_items;
+    auto item_of = [&](int64_t w) -> int64_t {
+        if (pass_k < 0) return w;
+        return nit[w] > pass_k ? a.item_start[w] + pass_k : -1;
+    };
+    int64_t w = blockIdx.x;
+    if (tid == 0 && w < n_work && item_of(w) >= 0) issue(item_of(w), 0);
+    const float T_in = a.T_in, T_out = a.T_out;
+    const double R2 = a.R2;
+    for (int it = 0; w < n_work; w += gridDim.x, ++it) {
+        const int sidx = it & 1;
+        const int64_t wn = w + gridDim.x;
+        if (tid == 0 && wn < n_work && item_of(wn) >= 0) issue(item_of(wn), sidx ^ 1);
+        const int64_t item = item_of(w);
+        if (item < 0) continue;   // CTA-uniform: nothing staged for this work index
+        int64_t b, c0, c1;
+        locate(a, item, b, c0, c1);
+        const int64_t sp = b * a.B + tid;
+        // pairs j > i only (candidates ahead), or j < i only (behind: windows end at the block)
+        const bool active = sp < a.m && a.core[sp] && (behind ? c0 < sp : c1 - 1 > sp);
+        int32_t uroot = active ? uf_rep(a.parent, (int32_t)sp) : -1;
+        float q[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) q[k] = active ? Xs[(sp >> 2) * 4 * D + k * 4 + (sp & 3)] : NAN;   // NaN: no hits
+        mbar_wait(&bar[sidx], phase[sidx]);
+        phase[sidx] ^= 1u;
+        int32_t *spar = reinterpret_cast<int32_t *>(smem + sidx * buf_bytes + rows_bytes);
+        // staged parents -> current roots (path compressed in global memory too: writing an
+        // ancestor into parent[j] of a non-root j is race-benign, links CAS only on roots)
+        // Non-core candidates (parent -1) get NaN coordinates in the staged rows: no pair
+        // with them passes the distance test, so the hot loop needs no core check.
+        float *srows = reinterpret_cast<float *>(smem + sidx * buf_bytes);
+        for (int t = tid; t < (int)(c1 - c0); t += blockDim.x) {
+            const int32_t p = spar[t];
+            if (p >= 0) {
+                const int32_t r = DIAG == 1 ? p : uf_rep(a.parent, p);
+                if (r != p) {
+                    spar[t] = r;
+                    a.parent[c0 + t] = r;
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < D; ++k) srows[(t >> 2) * 4 * D + k * 4 + (t & 3)] = NAN;
+            }
+        }
+        __syncthreads();
+        if (__any_sync(0xffffffffu, active)) {
+            uint64_t nq[D];
+#pragma unroll
+            for (int k = 0; k < D; ++k) nq[k] = f2pack(-q[k], -q[k]);
+            const int ngroups = (int)((c1 - c0) >> 2);
+            uint32_t ra = smem_u32(smem + sidx * buf_bytes);
+            uint32_t pa = ra + (uint32_t)rows_bytes;
+            // the few pairs the snapshot cannot settle: exact test, then the fresh parent[j]
+            // (one relaxed load) against the cached root, union only if they differ; the
+            // root joined is written back into the snapshot
+            auto settle = [&](int g, const float4 (&xv)[D], const float2 dl, const float2 dh, uint32_t nb) {
+                const float dv[4] = {dl.x, dl.y, dh.x, dh.y};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int64_t j = c0 + 4 * g + i;
+                    if (!(nb & (1u << i)) || (behind ? j >= sp : j <= sp)) continue;
+                    ++st_path;
+                    bool hit = dv[i] <= T_in;
+                    if (!hit) {
+                        float x[D];
+#pragma unroll
+                        for (int k = 0; k < D; ++k) x[k] = lane4(xv[k], i);
+                        hit = sqdist_exact(x, q, D) <= R2;
+                    }
+                    if (!hit) continue;
+                    ++st_hit;
+                    const int32_t pj = ld_relaxed_gpu(a.parent + j);
+                    if (pj != uroot) {
+                        uroot = uf_unite_root(a.parent, uroot, pj);   // ancestors of sp and j
+                        ++st_link;
+                        // parent[j] -> the joined root (the smallest position of the component,
+                        // so <= j; j is no root unless it is that root: race-benign)
+                        if (uroot != pj) a.parent[j] = uroot;
+                    }
+                    spar[4 * g + i] = uroot;   // an ancestor of j now: a better filter for the CTA
+                }
+            };
+            // need bits of one group: may be a neighbour (non-core rows are NaN) and the
+            // staged root differs from the cached one
+            auto need4 = [&](const float2 dl, const float2 dh, const float4 pf) -> uint32_t {
+                return (uint32_t)(dl.x <= T_out && __float_as_int(pf.x) != uroot) |
+                       ((uint32_t)(dl.y <= T_out && __float_as_int(pf.y) != uroot) << 1) |
+                       ((uint32_t)(dh.x <= T_out && __float_as_int(pf.z) != uroot) << 2) |
+                       ((uint32_t)(dh.y <= T_out && __float_as_int(pf.w) != uroot) << 3);
+            };
+            int g = 0;
+            for (; g + 1 < ngroups; g += 2, ra += 32u * D, pa += 32u) {   // 2 groups per step
+                float4 xa[D], xb[D];
+#pragma unroll
+                for (int k = 0; k < D; ++k) { xa[k] = lds128(ra + 16u * k); xb[k] = lds128(ra + 16u * (D + k)); }
+                const float4 pfa = lds128(pa), pfb = lds128(pa + 16u);
+                uint64_t la, ha, lb, hb;
+                group_d2<D>(xa, nq, la, ha);
+                group_d2<D>(xb, nq, lb, hb);
+                const float2 dla = f2unpack(la), dha = f2unpack(ha), dlb = f2unpack(lb), dhb = f2unpack(hb);
+                const uint32_t na = need4(dla, dha, pfa), nb = need4(dlb, dhb, pfb);
+                if (DIAG) {   // diagnostics (labels invalid): count the pairs, skip the unions
+                    st_hit += __popc(na) + __popc(nb);
+                } else if (na | nb) {
+                    if (na) settle(g, xa, dla, dha, na);
+                    if (nb) settle(g + 1, xb, dlb, dhb, nb);
+                }
+            }
+            if (g < ngroups) {
+                float4 xa[D];
+#pragma unroll
+                for (int k = 0; k < D; ++k) xa[k] = lds128(ra + 16u * k);
+                const float4 pfa = lds128(pa);
+                uint64_t la, ha;
+                group_d2<D>(xa, nq, la, ha);
+                const float2 dla = f2unpack(la), dha = f2unpack(ha);
+                const uint32_t na = need4(dla, dha, pfa);
+                if (!DIAG && na) settle(g, xa, dla, dha, na);
+            }
+        }
+        __syncthreads();
+    }
+    if (ustats) {
+        if (DIAG) st_path = 1;
+        st_path = warp_sum(st_path);
+        st_hit = warp_sum(st_hit);
+        st_link = warp_sum(st_link);
+        if ((tid & 31) == 0 && st_path) {
+            atomicAdd(&ustats[0], st_path);
+            atomicAdd(&ustats[1], st_hit);
+            atomicAdd(&ustats[2], st_link);
+        }
+    }
+}
+}  // namespace
+
+bool launch_union_snap(const PassArgs &a, int variant, const int64_t *nit, int64_t phases, int behind,
+                       unsigned long long *ustats, cudaStream_t s) {
+    if (a.f64 || a.d < 1 || a.d > 8) return false;
+    if (a.total_items == 0) return true;
+    const size_t smem = (size_t)2 * a.chunk * (a.d + 1) * 4 + 16;
+    switch (a.d) {
+#define CASE(D)                                                                                    \
+    case D: {                                                                                      \
+        auto k = variant == 2 ? union_snap_kernel<D, 1> : variant == 3 ? union_snap_kernel<D, 4, 1>  \
+               : variant == 4 ? union_snap_kernel<D, 4, 2> : union_snap_kernel<D, 4>;              \
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);           \
+        if (phases > 0 && nit) {                                                                   \
+            const int g = persistent_grid(k, a.B, smem, a.nblocks, a.sm_count);                   \
+            for (int64_t ph = 0; ph < phases; ++ph) SNN_LAUNCH(k, g, a.B, smem, s, a, nit, (int)ph, behind, ustats); \
+        } else {                                                                                   \
+            const int g = persistent_grid(k, a.B, smem, a.total_items, a.sm_count);               \
+            SNN_LAUNCH(k, g, a.B, smem, s, a, nit, -1, behind, ustats);                            \
+        }                                                                                          \
+        break;                                                                                     \
+    }
+        CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+#undef CASE
+        default: break;
+    }
+    return true;
+}
+
+namespace {
+__global__ void max_i64_kernel(const int64_t *v, int64_t n, unsigned long long *out) {
+    int64_t m = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        m = max(m, v[i]);
+    m = max(m, (int64_t)__reduce_max_sync(0xffffffffu, (unsigned)m));
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(out, (unsigned long long)m);
+}
+}  // namespace
+
+void launch_max_i64(const int64_t *v, int64_t n, unsigned long long *out, cudaStream_t s) {
+    if (n <= 0) return;
+    const int64_t gb = ceil_div(n, 256);
+    const int g = (int)(gb < 148 * 4 ? gb : 148 * 4);
+    SNN_LAUNCH(max_i64_kernel, g, 256, 0, s, v, n, out);
 }
 
 }  // namespace snn

@@ -129,6 +129,20 @@ void launch_lowd_compact(const PassArgs &a, cudaStream_t s);
 void launch_lowd_fix(const PassArgs &a, cudaStream_t s);
 // DBSCAN passes over the self-query work list: mode 2 = count, 3 = union, 4 = border.
 void launch_lowd_mode(int mode, const PassArgs &a, cudaStream_t s);
+// DBSCAN union pass with the staged parent-snapshot pre-check (fp32, d <= 8; false: not
+// supported for these arguments; variant 2: register cap for 6 CTAs per SM).  phases > 0
+// (nit = items per query block): `phases` launches, launch k processing chunk k of every
+// block (chunk-major order: near pairs first), else one launch over all items.  ustats (nullable, 3 zeroed counters): pairs sent to
+// the union path, exact hits among them, unions that linked two components.
+bool launch_union_snap(const PassArgs &a, int variant, const int64_t *nit, int64_t phases, int behind,
+                       unsigned long long *ustats, cudaStream_t s);
+// DBSCAN union pass, candidates behind (pairs j < i): window of block b clipped to end
+// after its last position (rounded up to 4); lo unchanged
+void launch_truncate_windows_behind(const int64_t *blk_lo, const int64_t *blk_hi, int64_t nblocks, int B, int chunk,
+                                    int64_t *hi2, int64_t *nitems2, int64_t m, int64_t n, unsigned long long *pairs,
+                                    cudaStream_t s);
+// *out = max(*out, max_i v[i]) for non-negative v (out zeroed by the caller)
+void launch_max_i64(const int64_t *v, int64_t n, unsigned long long *out, cudaStream_t s);
 
 // Generic-d path (row-major, any d): count pass + write pass (write recomputes).
 void launch_generic_pass(bool write, const PassArgs &a, cudaStream_t s);

@@ -379,6 +379,32 @@ def test_dbscan_core_count_modes_identical(snn, n, box, dt):
     assert np.array_equal(lab1, ref) and np.array_equal(lab2, ref)
 
 
+@pytest.mark.parametrize("n,box,d", [(200000, 400.0, 2), (60000, 500.0, 2), (40000, 60.0, 3)])
+def test_dbscan_union_variants_identical(snn, n, box, d):
+    """The union pass through the staged root snapshot (default: candidates behind the
+    block, pairs j < i), candidates ahead (j > i), the chunk-major phased order, other
+    chunk sizes and the plain window_lowd union pass: identical labels, equal to the grid
+    oracle's (reading C18)."""
+    import paper_2212_07679_b200 as p
+    X = workloads.c5(n=n, seed=41, box=box).X
+    if d == 3:
+        X = np.concatenate([X, np.random.default_rng(3).uniform(0, 4, (n, 1))], axis=1)
+    X = X.astype(np.float32)
+    ref, Kr, _ = oracle.dbscan(X, 3.0, 5, grid=True)
+    variants = [{}, {"union_behind": -1}, {"union_phased": 1}, {"union_phased": 1, "union_behind": -1},
+                {"union_chunk": 2048}, {"union_chunk": 64}, {"union_snap": 2}, {"union_snap": -1}]
+    for opts in variants:
+        try:
+            for k, v in opts.items():
+                p.snn_set_option(k, v)
+            lab, K = _gpu_dbscan(snn, X, 3.0, 5)
+        finally:
+            for k in opts:
+                p.snn_set_option(k, 0)
+        assert K == Kr, opts
+        assert np.array_equal(lab, ref), opts
+
+
 @pytest.mark.parametrize("d,dt", [(16, np.float32), (40, np.float32), (12, np.float64)])
 def test_dbscan_high_d_parity(snn, d, dt):
     """d > 8: DBSCAN over the exact self-query CSR; labels equal the oracle's."""
