@@ -283,7 +283,10 @@ def roofline_block(args, w, prof, times, dev, info):
     else:
         flop_per_pair = 3 * w.d - 1
         peak = fp32_alu_peak_tflops(sm_max, n_sm)
-        kernel, bound = (f"window_lowd<float,{w.d},union> (K12 DBSCAN union pass)" if fam == "dbscan_union"
+        import paper_2212_07679_b200 as snn
+        snap = snn.snn_get_option("union_snap") > 0 and w.X.dtype == np.float32 and w.d <= 8
+        kernel, bound = ((f"union_snap_kernel<{w.d}> (K12 DBSCAN union pass, staged root snapshot)" if snap
+                          else f"window_lowd<float,{w.d},union> (K12 DBSCAN union pass)") if fam == "dbscan_union"
                          else f"window_lowd<float,{w.d},scan> (K8 scan pass)"), "alu"
         peak_src = f"FP32 FMA issue peak at {sm_max:.0f} MHz x {n_sm} SMs (sm_max_mhz, {src})"
         work = f"{flop_per_pair} flop per evaluated candidate pair (eq:ip1)"

@@ -320,7 +320,9 @@ snn_status snn_profile_read(const char *family, double *ms, uint64_t *launches, 
  *   "simt_filter"    low-d fp32 expanded-form pre-filter: default on for radius queries and
  *                    off for DBSCAN; 1 = on everywhere, -1 = off everywhere
  *   "lowd_tc", "lowd_tc_tiles", "lowd_tc_group"   low-d tcgen05 path (default off)
- *   "tc", "tc_min_d", "tc_tiles", "tc_f16", "tc_group", "tc_diag", "tc_gram_min_d"
+ *   "tc", "tc_min_d", "tc_tiles", "tc_f16", "tc_group", "tc_diag", "tc_gram_min_d",
+ *   "tc_warp_arrive"  (tc_diag 1..4 = diagnostics, results NOT valid: 1 no epilogue work,
+ *                    2 no MMA, 3 no MMA and no hit path, 4 no hit path)
  *                    tensor-core path selection and tiling (tests / sweeps)
  * "force_generic" is read by snn_build (it fixes the sorted copy's layout).
  * Returns SNN_ERR_INVALID_ARGUMENT for an unknown key or bad value. */

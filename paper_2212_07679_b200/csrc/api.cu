@@ -34,11 +34,12 @@ struct Options {
     int tc = 1;          // use the tcgen05 path for d >= tc_min_d
     int tc_min_d = 32;
     int tc_tiles = 8;    // 256-candidate tiles per work item on the tensor-core path
-    int tc_diag = 0;     // diagnostics only (results invalid): 1 = no epilogue work, 2 = no MMA
+    int tc_diag = 0;     // diagnostics only (results invalid): 1 = no epilogue work, 2 = no MMA, 3 = no MMA and no hit path, 4 = no hit path
     int tc_f16 = 1;      // tensor-core operands FP16 (scaled) instead of TF32
     int tc_ares = 1;     // K9: query tile resident per work item when K is one block
     int tc_group = 128;  // query blocks per raster group (upper bound; L2 budget decides)
     int tc_wait_hint = 0;   // K9 mbarrier waits: suspend-time hint in ns (0 = probe loop)
+    int tc_warp_arrive = 1;   // K9 epilogue: one mbarrier arrive per warp (-1: per thread)
     int tc_gram_min_d = 32;    // Gram matrix on the tensor cores for d >= this
     int symmetric = 1;   // low-d self-queries: each unordered pair evaluated once
     int stage_rows = 1;  // low-d: assemble rows in key order, then move each row whole
@@ -318,7 +319,7 @@ snn_status snn_get_option(const char *key, int64_t *value) {
         {"variant", &Options::variant}, {"tc", &Options::tc}, {"tc_min_d", &Options::tc_min_d},
         {"tc_tiles", &Options::tc_tiles}, {"tc_diag", &Options::tc_diag}, {"tc_f16", &Options::tc_f16},
         {"tc_ares", &Options::tc_ares}, {"tc_group", &Options::tc_group},
-        {"tc_wait_hint", &Options::tc_wait_hint},
+        {"tc_wait_hint", &Options::tc_wait_hint}, {"tc_warp_arrive", &Options::tc_warp_arrive},
         {"tc_gram_min_d", &Options::tc_gram_min_d}, {"symmetric", &Options::symmetric},
         {"stage_rows", &Options::stage_rows}, {"balanced_compact", &Options::balanced_compact},
         {"window_all", &Options::window_all}, {"simt_filter", &Options::simt_filter},
@@ -376,7 +377,7 @@ snn_status snn_set_option(const char *key, int64_t value) {
         return SNN_OK;
     }
     if (k == "tc_diag") {   // performance diagnostics only: results are NOT valid
-        if (value < 0 || value > 2) return fail(SNN_ERR_INVALID_ARGUMENT, "tc_diag must be 0..2");
+        if (value < 0 || value > 4) return fail(SNN_ERR_INVALID_ARGUMENT, "tc_diag must be 0..4");
         g_opt.tc_diag = (int)value;
         return SNN_OK;
     }
@@ -434,6 +435,7 @@ snn_status snn_set_option(const char *key, int64_t value) {
         g_opt.union_load = value == -1 ? 0 : (value == 0 ? 1 : (int)value);   // 0: the default (relaxed)
         return SNN_OK;
     }
+    if (k == "tc_warp_arrive") { g_opt.tc_warp_arrive = value < 0 ? 0 : 1; return SNN_OK; }
     if (k == "tc_wait_hint") {
         if (value < 0 || value > 1000000) return fail(SNN_ERR_INVALID_ARGUMENT, "tc_wait_hint must be 0..1e6 ns");
         g_opt.tc_wait_hint = (int)value;
@@ -856,6 +858,7 @@ static snn_status query_tc(snn_index idx, Workspace &ws, cudaStream_t s, int sms
     t.diag = g_opt.tc_diag;
     t.ares = g_opt.tc_ares;
     t.wait_hint = (uint32_t)g_opt.tc_wait_hint;
+    t.warp_arrive = g_opt.tc_warp_arrive;
     {
         const double c1h = 1.0 - c1 / 2;
         const double r2h = (R * R * (1.0 + 1e-12) * (1.0 + ldexp(1.0, -20)) + c0) / 2;

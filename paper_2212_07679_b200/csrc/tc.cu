@@ -129,9 +129,10 @@ tc_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-        for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], EPI); }
+        const uint32_t earr = a.warp_arrive ? EPI / 32 : EPI;   // epilogue arrivals per release
+        for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], earr); }
         for (int s = 0; s < 2; ++s) { mbar_init(&qfull[s], 1); mbar_init(&qempty[s], 1); }
-        for (int s = 0; s < ARING; ++s) { mbar_init(&afull[s], 1); mbar_init(&aempty[s], EPI); }
+        for (int s = 0; s < ARING; ++s) { mbar_init(&afull[s], 1); mbar_init(&aempty[s], earr); }
         fence_mbar_init();
     }
     if (warp == 1) {
@@ -200,7 +201,7 @@ tc_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                         const uint32_t sa = ARES ? qbase + qs * A_BYTES : base + stage * SB;
                         const uint32_t sb = ARES ? base + stage * SB : sa + A_BYTES;
                         const uint64_t da = sw128_desc(sa), db = sw128_desc(sb);
-                        if (a.diag != 2) {
+                        if (a.diag != 2 && a.diag != 3) {
 #pragma unroll
                             for (int kk = 0; kk < 4; ++kk)   // 4 MMAs of 32 bytes of K each
                                 mma_op<F16>(dcol, da + 2 * kk, db + 2 * kk, (kb | kk) != 0);
@@ -262,7 +263,7 @@ tc_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 #pragma unroll
                     for (int c = 0; c < 3; ++c) m[c] = fmaxf(fmaxf(m[3 * c], m[3 * c + 1]), m[3 * c + 2]);
                     const float mx = fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[9] > m[10] ? m[9] : m[10]));
-                    if (mx >= bi) {
+                    if (mx >= bi && a.diag < 3) {
                         // rare (per lane): candidate mask, then one staged entry per set bit
                         uint32_t mask = 0;
 #pragma unroll
@@ -287,8 +288,16 @@ tc_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     }
                 }
                 tc_fence_before();
-                mbar_arrive(smem_u32(&tempty[acc]));
-                mbar_arrive(smem_u32(&aempty[aslot]));
+                if (a.warp_arrive) {   // one arrive per warp once every lane's TMEM loads retired
+                    __syncwarp();
+                    if (lane == 0) {
+                        mbar_arrive(smem_u32(&tempty[acc]));
+                        mbar_arrive(smem_u32(&aempty[aslot]));
+                    }
+                } else {
+                    mbar_arrive(smem_u32(&tempty[acc]));
+                    mbar_arrive(smem_u32(&aempty[aslot]));
+                }
                 if (++aslot == ARING) { aslot = 0; aph ^= 1; }
                 // staged hits -> the warp's claimed block of the pair list (one global
                 // atomic per CLAIM slots instead of one per tile); unused slots get q = -1.
