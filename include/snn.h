@@ -312,6 +312,9 @@ snn_status snn_profile_read(const char *family, double *ms, uint64_t *launches, 
  *   "union_behind"   union_snap pass: 1 = default, candidates behind the block (pairs j < i,
  *                    already settled); -1 = candidates ahead (pairs j > i)
  *   "union_chunk"    union_snap pass: candidates per work item (default 512; 64..8192)
+ *   "union_seed"     union_snap pass (behind): a seed pass first unites every core point
+ *                    with its nearest core neighbour behind it, scanning up to this many
+ *                    steps of 32 positions (default 8; -1 = no seed pass)
  *   "union_phased"   union_snap pass: 1 = one launch per chunk index (chunk k of every block);
  *                    default off
  *   "union_stats"    1 = count the union_snap pass's union-path pairs; read back with

@@ -56,6 +56,7 @@ struct Options {
     int union_snap = 1;        // DBSCAN union pass (fp32, d <= 8): staged parent snapshot pre-check (-1: window_lowd)
     int union_behind = 1;      // DBSCAN union pass (union_snap): candidates behind the block (pairs j < i)
     int dbscan_block = 256;    // DBSCAN: queries per block (windows, union and border passes)
+    int union_seed = 8;        // DBSCAN union pass (union_snap, behind): seed pass uniting each core point with its nearest core neighbour behind (steps of 32 positions; 0 = off)
     int union_chunk = 512;     // DBSCAN union pass (union_snap): candidates per work item
     int union_phased = 0;      // DBSCAN union pass (union_snap): chunk k of every block in launch k (near pairs first)
     int union_stats = 0;       // DBSCAN union pass: count pairs sent to the union path (diagnostics)
@@ -129,6 +130,7 @@ bool dbscan_union_phased() { return g_opt.union_phased > 0; }
 bool dbscan_union_behind() { return g_opt.union_behind > 0; }
 int dbscan_union_chunk() { return g_opt.union_chunk; }
 int dbscan_block() { return g_opt.dbscan_block; }
+int dbscan_union_seed() { return g_opt.union_seed; }
 static thread_local int64_t g_last_union[3] = {0, 0, 0};
 bool dbscan_union_stats() { return g_opt.union_stats > 0; }
 void dbscan_set_union_stats(const unsigned long long *v) {
@@ -329,7 +331,7 @@ snn_status snn_get_option(const char *key, int64_t *value) {
         {"count_warp", &Options::count_warp}, {"union_snap", &Options::union_snap},
         {"union_stats", &Options::union_stats}, {"union_phased", &Options::union_phased},
         {"union_behind", &Options::union_behind}, {"union_chunk", &Options::union_chunk},
-        {"dbscan_block", &Options::dbscan_block}};
+        {"dbscan_block", &Options::dbscan_block}, {"union_seed", &Options::union_seed}};
     for (const auto &o : kInt)
         if (strcmp(key, o.name) == 0) { *value = g_opt.*(o.field); return SNN_OK; }
     if (strcmp(key, "ovf_records") == 0) { *value = g_opt.ovf_rec_cap; return SNN_OK; }
@@ -420,6 +422,11 @@ snn_status snn_set_option(const char *key, int64_t value) {
         if (value == 0) value = 256;
         if (value < 32 || value > 256 || value % 32) return fail(SNN_ERR_INVALID_ARGUMENT, "dbscan_block must be 32..256, multiple of 32");
         g_opt.dbscan_block = (int)value;
+        return SNN_OK;
+    }
+    if (k == "union_seed") {   // 0: default (8 steps); -1 off; else steps of 32 positions
+        if (value > 1 << 20) return fail(SNN_ERR_INVALID_ARGUMENT, "union_seed must be <= 2^20");
+        g_opt.union_seed = value < 0 ? 0 : (value == 0 ? 8 : (int)value);
         return SNN_OK;
     }
     if (k == "union_chunk") {

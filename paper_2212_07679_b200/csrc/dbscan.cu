@@ -318,6 +318,7 @@ snn_status dbscan_impl(snn_index idx, double eps, int32_t min_pts, int32_t *labe
             au.item_block = ib2;
         }
         const int utok = prof_begin(F_UNION, s);
+        if (behind && dbscan_union_seed() > 0) launch_union_seed(a, dbscan_union_seed(), s);   // a: the full windows
         unsigned long long *ustats = nullptr;
         if (dbscan_union_stats()) {
             CKD(ws.alloc(&ustats, 3), "alloc");

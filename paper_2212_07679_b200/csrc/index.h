@@ -97,6 +97,7 @@ bool dbscan_union_phased();  // option union_phased (api.cu)
 bool dbscan_union_behind();  // option union_behind (api.cu)
 int dbscan_union_chunk();    // option union_chunk (api.cu)
 int dbscan_block();          // option dbscan_block (api.cu)
+int dbscan_union_seed();     // option union_seed (api.cu): seed scan steps of 32 positions (0 = off)
 bool dbscan_union_stats();   // option union_stats (api.cu)
 void dbscan_set_union_stats(const unsigned long long *v);   // [path, hits, links] of the last union pass
 // metric adapters (metric.cu): exact row normalization (flag = 1 on a zero row), radius

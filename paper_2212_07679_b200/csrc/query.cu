@@ -1805,6 +1805,55 @@ __global__ void __launch_bounds__(256) core_count_warp_kernel(PassArgs a, int32_
     }
 }
 
+// DBSCAN union seed (before the union pass): one warp per core point scans behind its own
+// key position (pairs j < i, the nearest positions first, 32 per step) and unites it with
+// the first core neighbour found within max_steps x 32 positions (same exact test as the counts).  The seeded forest joins
+// most points to their component before the union pass, whose work items of one query block
+// then start from settled roots instead of singletons.  Stops at the block's window start.
+template <typename T, int D>
+__global__ void __launch_bounds__(256) union_seed_kernel(PassArgs a, int max_steps) {
+    const T *Xs = static_cast<const T *>(a.Xs);
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const float T_in = a.T_in, T_out = a.T_out;
+    const double R2 = a.R2;
+    auto row = [&](int64_t j, T (&x)[D]) {
+#pragma unroll
+        for (int k = 0; k < D; ++k) x[k] = Xs[(j >> 2) * 4 * D + k * 4 + (j & 3)];
+    };
+    for (int64_t sp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; sp < a.m; sp += nw) {
+        if (!a.core[sp]) continue;   // warp-uniform
+        const int64_t lo = a.blk_lo[sp / a.B];
+        T q[D];
+        row(sp, q);
+        for (int64_t off = 1; off <= 32 * max_steps; off += 32) {
+            const int64_t j = sp - off - lane;
+            if (!__any_sync(0xffffffffu, j >= lo)) break;
+            bool h = false;
+            if (j >= lo && a.core[j]) {
+                T x[D];
+                row(j, x);
+                if constexpr (sizeof(T) == 4) {
+                    float d2 = 0.f;
+#pragma unroll
+                    for (int k = 0; k < D; ++k) {
+                        const float t = x[k] - q[k];
+                        d2 = fmaf(t, t, d2);
+                    }
+                    h = d2 <= T_in || (d2 <= T_out && sqdist_exact(x, q, D) <= R2);
+                } else {
+                    h = sqdist_exact(x, q, D) <= R2;
+                }
+            }
+            const uint32_t hb = __ballot_sync(0xffffffffu, h);
+            if (hb) {
+                if (lane == __ffs(hb) - 1) uf_unite(a.parent, (int32_t)sp, (int32_t)j);
+                break;
+            }
+        }
+    }
+}
+
 template <typename T, int D>
 void run_core_count(const PassArgs &a, int32_t *count, unsigned long long *evaluated, cudaStream_t s) {
     const size_t smem = (size_t)2 * a.chunk * D * sizeof(T) + 16;
@@ -1814,6 +1863,13 @@ void run_core_count(const PassArgs &a, int32_t *count, unsigned long long *evalu
     SNN_LAUNCH(k, g, a.B, smem, s, a, count, evaluated);
 }
 }  // namespace
+
+void launch_union_seed(const PassArgs &a, int max_steps, cudaStream_t s) {
+    if (a.nblocks == 0) return;
+#define FN(T, D) SNN_LAUNCH((union_seed_kernel<T, D>), a.sm_count * 8, 256, 0, s, a, max_steps)
+    SNN_LOWD_DISPATCH(FN)
+#undef FN
+}
 
 void launch_core_counts(const PassArgs &a, int32_t *count, unsigned long long *evaluated, cudaStream_t s) {
     if (a.nblocks == 0) return;

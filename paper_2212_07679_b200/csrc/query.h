@@ -109,6 +109,10 @@ struct PassArgs {
 // DBSCAN core counts with early exit: count[sp] = |N_eps| if < min_pts, else some value
 // >= min_pts (one CTA per query block, chunks in order, stop when the block is decided)
 void launch_core_counts(const PassArgs &a, int32_t *count, unsigned long long *evaluated, cudaStream_t s);
+// DBSCAN union seed: every core point united with its nearest core neighbour behind it in
+// key order (within its block's window and max_steps x 32 positions; a.core, a.parent,
+// a.blk_lo set), before the union pass
+void launch_union_seed(const PassArgs &a, int max_steps, cudaStream_t s);
 // DBSCAN union pass work list: window of block b clipped to start at its first position
 // (pairs, nullable, += candidate pairs of the clipped windows for m queries / n points)
 void launch_truncate_windows(const int64_t *blk_lo, const int64_t *blk_hi, int64_t nblocks, int B, int chunk,

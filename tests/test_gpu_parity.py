@@ -381,9 +381,9 @@ def test_dbscan_core_count_modes_identical(snn, n, box, dt):
 
 @pytest.mark.parametrize("n,box,d", [(200000, 400.0, 2), (60000, 500.0, 2), (40000, 60.0, 3)])
 def test_dbscan_union_variants_identical(snn, n, box, d):
-    """The union pass through the staged root snapshot (default: candidates behind the
-    block, pairs j < i), candidates ahead (j > i), the chunk-major phased order, other
-    chunk sizes and the plain window_lowd union pass: identical labels, equal to the grid
+    """The union pass through the staged root snapshot (default: seed pass, then candidates
+    behind the block, pairs j < i), candidates ahead (j > i), the chunk-major phased order,
+    other chunk sizes, no / short / unbounded seed scans and the plain window_lowd union pass: identical labels, equal to the grid
     oracle's (reading C18)."""
     import paper_2212_07679_b200 as p
     X = workloads.c5(n=n, seed=41, box=box).X
@@ -392,7 +392,8 @@ def test_dbscan_union_variants_identical(snn, n, box, d):
     X = X.astype(np.float32)
     ref, Kr, _ = oracle.dbscan(X, 3.0, 5, grid=True)
     variants = [{}, {"union_behind": -1}, {"union_phased": 1}, {"union_phased": 1, "union_behind": -1},
-                {"union_chunk": 2048}, {"union_chunk": 64}, {"union_snap": 2}, {"union_snap": -1}]
+                {"union_chunk": 2048}, {"union_chunk": 64}, {"union_snap": 2}, {"union_snap": -1},
+                {"union_seed": -1}, {"union_seed": 1}, {"union_seed": 1 << 20}]
     for opts in variants:
         try:
             for k, v in opts.items():
