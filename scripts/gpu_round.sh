@@ -23,13 +23,14 @@ for s in $STAGES; do
         CMD="python bench.py --config $c --steps 1 --warmup 3 --no-cpu-baseline"
         $CMD > $OUT/plain_$c.log 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$c.csv $CMD > $OUT/ncu_launch_$c.log 2>&1; echo "ncu launch $c rc=$?"; done ;;
     ncu_full_*) c=${s#ncu_full_}
-        case $c in c2|c5) K='regex:window_lowd';; *) K='regex:tc_window';; esac
+        case $c in c2) K='regex:window_lowd';; c5) K='regex:union_snap';; *) K='regex:tc_window';; esac
         CMD="python bench.py --config $c --steps 1 --warmup 3 --no-cpu-baseline"
         $CMD > $OUT/plainf_$c.log 2>&1 && timeout 1200 ncu --set full --clock-control none --import-source on -k $K -s 6 -c 2 -o $OUT/full_$c $CMD > $OUT/ncu_full_$c.log 2>&1; echo "ncu full $c rc=$?" ;;
     ncu_dbscan_c5)
         CMD="python bench.py --config c5 --steps 1 --warmup 3 --no-cpu-baseline"
         $CMD > $OUT/plaind_c5.log 2>&1 && timeout 1200 ncu --set full --clock-control none --import-source on -k regex:core_count -s 3 -c 1 -o $OUT/core_c5 $CMD > $OUT/ncu_core_c5.log 2>&1; echo "ncu core c5 rc=$?"
-        timeout 1200 ncu --set full --clock-control none --import-source on -k regex:window_lowd -s 6 -c 1 -o $OUT/union_c5 $CMD > $OUT/ncu_union_c5.log 2>&1; echo "ncu union c5 rc=$?" ;;
+        timeout 1200 ncu --set full --clock-control none --import-source on -k regex:union_snap -s 3 -c 1 -o $OUT/union_c5 $CMD > $OUT/ncu_union_c5.log 2>&1; echo "ncu union c5 rc=$?"
+        timeout 1200 ncu --set full --clock-control none --import-source on -k regex:union_seed -s 3 -c 1 -o $OUT/seed_c5 $CMD > $OUT/ncu_seed_c5.log 2>&1; echo "ncu seed c5 rc=$?" ;;
     ncu_write_c2)
         CMD="python bench.py --config c2 --steps 1 --warmup 3 --no-cpu-baseline"
         $CMD > $OUT/plainw_c2.log 2>&1 && timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"compact_lowd_bal|rows_finalize" -s 8 -c 2 -o $OUT/write_c2 $CMD > $OUT/ncu_write_c2.log 2>&1; echo "ncu write c2 rc=$?" ;;
@@ -40,6 +41,7 @@ for s in $STAGES; do
         for r in $OUT/*.ncu-rep; do [ -f "$r" ] || continue; b=${r%.ncu-rep}
             python scripts/ncu_summary.py full $r > ${b}_metrics.txt 2>&1
             python scripts/ncu_source.py $r 40 > ${b}_source_top40.txt 2>&1
+            python scripts/ncu_lines.py $r 30 > ${b}_lines.txt 2>&1
             ncu -i $r --page raw --csv > ${b}_raw.csv 2>/dev/null; gzip -f ${b}_raw.csv
             rm -f $r; done
         for c in $OUT/launches_*.csv; do [ -f "$c" ] || continue; python scripts/ncu_summary.py launches $c > ${c%.csv}_summary.txt 2>&1; done
