@@ -39,7 +39,6 @@ struct Options {
     int tc_ares = 1;     // K9: query tile resident per work item when K is one block
     int tc_group = 128;  // query blocks per raster group (upper bound; L2 budget decides)
     int tc_wait_hint = 0;   // K9 mbarrier waits: suspend-time hint in ns (0 = probe loop)
-    int tc_epi_warps = 16;    // K9 epilogue warps (16 or 32)
     int tc_warp_arrive = 1;   // K9 epilogue: one mbarrier arrive per warp (-1: per thread)
     int tc_gram_min_d = 32;    // Gram matrix on the tensor cores for d >= this
     int symmetric = 1;   // low-d self-queries: each unordered pair evaluated once
@@ -323,7 +322,6 @@ snn_status snn_get_option(const char *key, int64_t *value) {
         {"tc_tiles", &Options::tc_tiles}, {"tc_diag", &Options::tc_diag}, {"tc_f16", &Options::tc_f16},
         {"tc_ares", &Options::tc_ares}, {"tc_group", &Options::tc_group},
         {"tc_wait_hint", &Options::tc_wait_hint}, {"tc_warp_arrive", &Options::tc_warp_arrive},
-        {"tc_epi_warps", &Options::tc_epi_warps},
         {"tc_gram_min_d", &Options::tc_gram_min_d}, {"symmetric", &Options::symmetric},
         {"stage_rows", &Options::stage_rows}, {"balanced_compact", &Options::balanced_compact},
         {"window_all", &Options::window_all}, {"simt_filter", &Options::simt_filter},
@@ -442,12 +440,6 @@ snn_status snn_set_option(const char *key, int64_t value) {
     if (k == "union_load") {
         if (value < -1 || value > 2) return fail(SNN_ERR_INVALID_ARGUMENT, "union_load must be -1..2");
         g_opt.union_load = value == -1 ? 0 : (value == 0 ? 1 : (int)value);   // 0: the default (relaxed)
-        return SNN_OK;
-    }
-    if (k == "tc_epi_warps") {
-        if (value == 0) value = 16;
-        if (value != 16 && value != 32) return fail(SNN_ERR_INVALID_ARGUMENT, "tc_epi_warps must be 16 or 32");
-        g_opt.tc_epi_warps = (int)value;
         return SNN_OK;
     }
     if (k == "tc_warp_arrive") { g_opt.tc_warp_arrive = value < 0 ? 0 : 1; return SNN_OK; }
@@ -874,7 +866,6 @@ static snn_status query_tc(snn_index idx, Workspace &ws, cudaStream_t s, int sms
     t.ares = g_opt.tc_ares;
     t.wait_hint = (uint32_t)g_opt.tc_wait_hint;
     t.warp_arrive = g_opt.tc_warp_arrive;
-    t.epi_warps = g_opt.tc_epi_warps;
     {
         const double c1h = 1.0 - c1 / 2;
         const double r2h = (R * R * (1.0 + 1e-12) * (1.0 + ldexp(1.0, -20)) + c0) / 2;

@@ -42,7 +42,7 @@ using namespace tc5;
 constexpr int TM = 128, TN = 256, STAGES = 4;
 constexpr int KB_BYTES = 128;                      // bytes per operand row per K block (one swizzle atom)
 constexpr int A_BYTES = TM * KB_BYTES, B_BYTES = TN * KB_BYTES, STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int STAGE_CAP = 8;                       // staged hits per epilogue thread per tile (16 warps)
+constexpr int STAGE_CAP = 8;                       // staged hits per epilogue thread per tile
 constexpr int ARING = 8;                           // x-bar slices in flight (decoupled from TMEM)
 constexpr unsigned long long CLAIM = 256;          // pair-list slots claimed per warp atomic
 constexpr int EPI = 512;                           // epilogue threads (16 warps)
@@ -53,14 +53,6 @@ constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + ARING * TN * 4 + EPI * 
 // resident slots; the ring then streams only candidate tiles (a third fewer operand bytes)
 constexpr int STAGES_R = 5;
 constexpr int SMEM_BYTES_R = 1024 + STAGES_R * B_BYTES + 2 * A_BYTES + ARING * TN * 4 + EPI * STAGE_CAP * 4 + 512;
-// epilogue width variants: EPIT epilogue threads (512 = 16 warps, 2 chunks of 32 columns per
-// thread; 1024 = 32 warps, 1 chunk each, half the staged hits per thread)
-template <int EPIT> constexpr int scap() { return EPIT == 512 ? STAGE_CAP : 4; }
-template <int EPIT> constexpr int smem_bytes(bool ares) {
-    return 1024 + (ares ? STAGES_R * B_BYTES + 2 * A_BYTES : STAGES * STAGE_BYTES) + ARING * TN * 4 +
-           EPIT * scap<EPIT>() * 4 + 512;
-}
-static_assert(smem_bytes<1024>(true) <= 227 * 1024 && smem_bytes<1024>(false) <= 227 * 1024, "K9 shared memory");
 // instruction descriptor: D format F32; A, B format F16 (0, kind::f16) or TF32 (2,
 // kind::tf32); both K-major; N >> 3 at bit 17, M >> 4 at bit 24
 template <bool F16>
@@ -109,10 +101,9 @@ __device__ __forceinline__ void tc_locate(const TcArgs &a, int64_t item, int64_t
     if (c1 < c0) c1 = c0;
 }
 
-template <bool F16, bool ARES, int EPIT>
-__global__ void __launch_bounds__(64 + EPIT, 1)
+template <bool F16, bool ARES>
+__global__ void __launch_bounds__(THREADS, 1)
 tc_window_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcArgs a) {
-    constexpr int EPI = EPIT, STAGE_CAP = scap<EPIT>(), COLS = TN / (EPIT / 128);
     constexpr int TK = k_elems<F16>();
     constexpr int NST = ARES ? STAGES_R : STAGES;              // ring stages
     constexpr int SB = ARES ? B_BYTES : STAGE_BYTES;           // bytes per ring stage
@@ -516,7 +507,7 @@ static bool make_map(CUtensorMap *m, const void *ptr, bool f16, int64_t rows, in
 int tc_tile_rows() { return TM; }
 int tc_tile_cols() { return TN; }
 int tc_kpad(int d, bool f16) { return (int)round_up(d, f16 ? 64 : 32); }
-int64_t tc_claim_slack() { return (int64_t)(1024 / 32) * (int64_t)CLAIM; }   // widest epilogue
+int64_t tc_claim_slack() { return (int64_t)(EPI / 32) * (int64_t)CLAIM; }
 
 void launch_gather_tf32(const void *X, bool f64, int64_t rows, int d, const uint32_t *perm, const float *mu_f,
                         float *out, float *half_norm, cudaStream_t s) {
@@ -558,19 +549,13 @@ bool launch_tc_window(const void *Qt, const void *Xt, bool f16, const TcArgs &a,
     if (!make_map(&ma, Qt, f16, a.m, a.kpad, TM) || !make_map(&mb, Xt, f16, a.n, a.kpad, TN)) return false;
     int g = (int)(a.total_items < sm_count ? a.total_items : sm_count);
     const bool ares = a.kblocks == 1 && a.ares;
-#define TCW(F, R, E)                                                                                      \
-    do {                                                                                                  \
-        cudaFuncSetAttribute(tc_window_kernel<F, R, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
-                             smem_bytes<E>(R));                                                           \
-        SNN_LAUNCH((tc_window_kernel<F, R, E>), g, 64 + E, smem_bytes<E>(R), s, ma, mb, a);               \
+#define TCW(F, R, SM)                                                                               \
+    do {                                                                                            \
+        cudaFuncSetAttribute(tc_window_kernel<F, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM); \
+        SNN_LAUNCH((tc_window_kernel<F, R>), g, THREADS, SM, s, ma, mb, a);                          \
     } while (0)
-    if (a.epi_warps == 32) {
-        if (f16) { if (ares) TCW(true, true, 1024); else TCW(true, false, 1024); }
-        else { if (ares) TCW(false, true, 1024); else TCW(false, false, 1024); }
-    } else {
-        if (f16) { if (ares) TCW(true, true, 512); else TCW(true, false, 512); }
-        else { if (ares) TCW(false, true, 512); else TCW(false, false, 512); }
-    }
+    if (f16) { if (ares) TCW(true, true, SMEM_BYTES_R); else TCW(true, false, SMEM_BYTES); }
+    else { if (ares) TCW(false, true, SMEM_BYTES_R); else TCW(false, false, SMEM_BYTES); }
 #undef TCW
     return true;
 }

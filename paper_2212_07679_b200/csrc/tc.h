@@ -24,8 +24,7 @@ struct TcArgs {
     int diag;               // 0; diagnostics: 1 = skip epilogue work, 2 = skip MMAs
     int ares;               // resident query tile per work item when K fits one block
     uint32_t wait_hint;     // mbarrier try_wait suspend-time hint in ns (0: plain probe loop)
-    int warp_arrive = 1;
-    int epi_warps = 16;     // epilogue warps: 16 (2 chunks of 32 columns per thread) or 32 (1 chunk)    // epilogue releases TMEM / x-bar slots with one arrive per warp (else per thread)
+    int warp_arrive = 1;    // epilogue releases TMEM / x-bar slots with one arrive per warp (else per thread)
 };
 
 int tc_tile_rows();   // queries per tile (128)
