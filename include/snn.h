@@ -288,8 +288,8 @@ snn_status snn_profile_read(const char *family, double *ms, uint64_t *launches, 
  *   "variant"        low-d scan loop: 1 = deferred-hit 2-group loop (default), 2 = 8-pair
  *                    direct loop
  *   "symmetric"      -1 = evaluate every pair twice in low-d self-queries (default: once)
- *   "stage_rows"     -1 = compaction writes final rows directly (default: key-order staging
- *                    buffer, then whole-row moves)
+ *   "stage_rows"     1 = the compaction assembles rows in a key-order staging buffer, then
+ *                    moves each row whole; default (0 / -1): it writes the final rows directly
  *   "balanced_compact" -1 = per-entry compaction threads (default for symmetric self-queries:
  *                    one slot record per thread after CTA scans)
  *   "window_all"     1 = brute-force ablation: every query scans all n candidates

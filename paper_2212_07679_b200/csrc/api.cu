@@ -42,7 +42,7 @@ struct Options {
     int tc_warp_arrive = 1;   // K9 epilogue: one mbarrier arrive per warp (-1: per thread)
     int tc_gram_min_d = 32;    // Gram matrix on the tensor cores for d >= this
     int symmetric = 1;   // low-d self-queries: each unordered pair evaluated once
-    int stage_rows = 1;  // low-d: assemble rows in key order, then move each row whole
+    int stage_rows = 0;  // low-d: 1 = assemble rows in key order, then move each row whole (0: direct final rows)
     int balanced_compact = 1;   // low-d compaction: one slot record per thread (CTA scans)
     int window_all = 0;  // ablation "brute force 2": windows = all points
     // low-d fp32 expanded-form SIMT pre-filter: 0 = default (radius queries on: faster on
@@ -390,7 +390,7 @@ snn_status snn_set_option(const char *key, int64_t value) {
         return SNN_OK;
     }
     if (k == "symmetric") { g_opt.symmetric = value < 0 ? 0 : 1; return SNN_OK; }
-    if (k == "stage_rows") { g_opt.stage_rows = value < 0 ? 0 : 1; return SNN_OK; }
+    if (k == "stage_rows") { g_opt.stage_rows = value > 0 ? 1 : 0; return SNN_OK; }   // 0: default (direct)
     if (k == "balanced_compact") { g_opt.balanced_compact = value < 0 ? 0 : 1; return SNN_OK; }
     if (k == "window_all") { g_opt.window_all = value > 0 ? 1 : 0; return SNN_OK; }
     if (k == "simt_filter") { g_opt.simt_filter = value > 0 ? 1 : (value < 0 ? -1 : 0); return SNN_OK; }

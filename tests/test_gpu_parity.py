@@ -1033,7 +1033,7 @@ def test_load_rewrites_padding_sentinels(snn, tmp_path, dt):
 
 @pytest.mark.parametrize("d", [2, 3, 6])
 def test_row_staging_and_symmetry_options_identical(snn, d):
-    """Key-order row staging (default) vs direct final-row writes, symmetric vs two-sided
+    """Direct final-row writes (default) vs key-order row staging, symmetric vs two-sided
     self-queries, expanded filter on/off, balanced vs per-entry compaction: bit-identical
     CSR, equal to the oracle."""
     import paper_2212_07679_b200 as p
@@ -1097,7 +1097,7 @@ def test_query_parts_partition_the_result(snn, d, dt, self_q, nparts):
 
 
 @pytest.mark.parametrize("d,dt,nparts,opts", [(2, np.float32, 8, {}), (3, np.float64, 5, {}),
-                                               (3, np.float32, 4, {"stage_rows": -1}),
+                                               (3, np.float32, 4, {"stage_rows": 1}),
                                                (3, np.float32, 3, {"balanced_compact": -1, "cap": 1, "ovf_records": 50}),
                                                (6, np.float32, 2, {"finalize_order": -1})])
 def test_symmetric_query_parts(snn, d, dt, nparts, opts):
