@@ -31,6 +31,7 @@ struct Options {
     int cap = 64;
     int32_t ovf_rec_cap = 1 << 20;
     int variant = 1;
+    int scan2q = 0;      // fp32 low-d scan with the expanded filter: two queries per thread
     int tc = 1;          // use the tcgen05 path for d >= tc_min_d
     int tc_min_d = 32;
     int tc_tiles = 8;    // 256-candidate tiles per work item on the tensor-core path
@@ -318,7 +319,7 @@ snn_status snn_get_option(const char *key, int64_t *value) {
     static const struct { const char *name; int Options::*field; } kInt[] = {
         {"force_generic", &Options::force_generic}, {"query_block", &Options::query_block},
         {"chunk", &Options::chunk}, {"power_iters", &Options::power_iters}, {"cap", &Options::cap},
-        {"variant", &Options::variant}, {"tc", &Options::tc}, {"tc_min_d", &Options::tc_min_d},
+        {"variant", &Options::variant}, {"scan2q", &Options::scan2q}, {"tc", &Options::tc}, {"tc_min_d", &Options::tc_min_d},
         {"tc_tiles", &Options::tc_tiles}, {"tc_diag", &Options::tc_diag}, {"tc_f16", &Options::tc_f16},
         {"tc_ares", &Options::tc_ares}, {"tc_group", &Options::tc_group},
         {"tc_wait_hint", &Options::tc_wait_hint}, {"tc_warp_arrive", &Options::tc_warp_arrive},
@@ -455,6 +456,7 @@ snn_status snn_set_option(const char *key, int64_t value) {
         g_opt.tc_group = (int)value;
         return SNN_OK;
     }
+    if (k == "scan2q") { g_opt.scan2q = value > 0 ? 1 : 0; return SNN_OK; }
     if (k == "variant") {
         if (value == 0) value = 1;
         if (value < 1 || value > 2) return fail(SNN_ERR_INVALID_ARGUMENT, "variant must be 1 or 2");
@@ -1284,6 +1286,7 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
     a.offsets = r->offsets; a.out_idx = nullptr; a.out_dist = nullptr;
     a.sm_count = sms;
     a.variant = g_opt.variant;
+    a.scan2q = g_opt.scan2q;
     if (!generic && !f64 && idx->Xf && g_opt.simt_filter >= 0) {
         double c1h = 1.0, r2h = 0.0;
         simt_filter_consts(D, R, &c1h, &r2h);

@@ -799,6 +799,244 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
     }
 }
 
+// K8 scan, two queries per thread (fp32 radius queries with the expanded-form filter,
+// B = 256 queries per block on 128 threads: thread t owns queries t and t + 128).  Every
+// staged filter row is read once for both queries, so the shared-memory loads and the loop
+// bookkeeping per pair halve.  Same filter, same deferred FIFO records per query, same
+// warp-cooperative exact drain and the same hit records / counts as window_lowd<G3>.
+template <int D, bool SYM>
+__global__ void __launch_bounds__(128) window_lowd_2q(PassArgs a) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    constexpr int FW = D + 1, NW = 4, GS = 2;
+    __shared__ uint32_t s_drec[NW * 256];
+    __shared__ uint8_t s_dres[NW * 256];
+    __shared__ float s_q[NW * 64 * D];   // per warp: owner o = 2 * lane + s
+    const int tid = threadIdx.x, lane = tid & 31, wq = tid >> 5;
+    const float *Xs = static_cast<const float *>(a.Xs);
+    const float *Qs = static_cast<const float *>(a.Qs);
+    const size_t buf_bytes = (size_t)a.chunk * FW * 4;
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + 2 * buf_bytes);
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    auto issue = [&](int64_t item, int sidx) {
+        int64_t b, c0, c1;
+        locate(a, item, b, c0, c1);
+        const uint32_t fbytes = (uint32_t)((c1 - c0) * FW * 4);
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&bar[sidx], fbytes);
+        bulk_g2s(smem + sidx * buf_bytes, a.Xf + c0 * FW, fbytes, &bar[sidx]);
+    };
+    uint32_t phase[2] = {0u, 0u};
+    int64_t w = blockIdx.x;
+    if (tid == 0 && w < a.total_items) issue(w, 0);
+    const float T_in = a.T_in, T_out = a.T_out;
+    const double R2 = a.R2;
+    const int cap = a.cap;
+    float *dq = s_q + wq * 64 * D;
+    for (int it = 0; w < a.total_items; w += gridDim.x, ++it) {
+        const int sidx = it & 1;
+        const int64_t wn = w + gridDim.x;
+        if (tid == 0 && wn < a.total_items) issue(wn, sidx ^ 1);
+        const int64_t item = w;
+        int64_t b, c0, c1;
+        locate(a, item, b, c0, c1);
+        // per-query state (s = 0, 1: queries tid, tid + 128 of the block)
+        int64_t sp[2], e[2];
+        bool active[2];
+        uint64_t nqc[2][D];
+        float thr[2];
+        uint64_t pend[2] = {0, 0};
+        int npend[2] = {0, 0};
+        int32_t cnt[2] = {0, 0}, rec[2] = {0, 0};
+        bool lost[2] = {false, false};
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+            const int qi = tid + 128 * s;
+            sp[s] = b * a.B + qi;
+            e[s] = item * a.B + qi;
+            active[s] = sp[s] < a.m;
+            double qb = 0.0;
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+                const float qk = active[s] ? Qs[(sp[s] >> 2) * 4 * D + k * 4 + (sp[s] & 3)] : NAN;   // NaN: no hits
+                dq[(2 * lane + s) * D + k] = qk;
+                const float qc = (float)((double)qk - (double)a.mu_f[k]);
+                qb += (double)qc * (double)qc;
+                nqc[s][k] = f2pack(-qc, -qc);
+            }
+            thr[s] = __double2float_ru(a.r2h - 0.5 * qb * a.c1h);
+        }
+        __syncwarp();
+        mbar_wait(&bar[sidx], phase[sidx]);
+        phase[sidx] ^= 1u;
+        const int ngroups = (int)((c1 - c0) >> 2);
+        const float4 *g4 = reinterpret_cast<const float4 *>(Xs) + (c0 >> 2) * D;   // exact rows (global)
+        // hit mask of group gg for owner s -> slot record (symmetric filter, overflow list)
+        auto emit = [&](int s, int gg, uint32_t m) {
+            if constexpr (SYM) {
+                const int64_t jb = c0 + 4 * gg;
+                if (jb + 3 <= sp[s]) return;
+                if (jb <= sp[s]) m &= ~((2u << (sp[s] - jb)) - 1u);
+                uint32_t mm = m;
+                while (mm) {
+                    const int i = __ffs(mm) - 1;
+                    mm &= mm - 1;
+                    if (jb + i < a.own_hi) atomicAdd(&a.lcnt[jb + i], 1);
+                }
+                if (!m) return;
+            }
+            const uint32_t v = ((uint32_t)gg << 4) | m;
+            if (rec[s] < cap) {
+                a.slots[((size_t)item * cap + rec[s]) * a.B + tid + 128 * s] = (uint16_t)v;
+            } else {
+                const int32_t k = atomicAdd(a.ovf_rec_count, 1);
+                if (k < a.ovf_rec_cap) a.ovf_rec[k] = OvfRec{(int32_t)e[s], cnt[s], v};
+                else lost[s] = true;
+            }
+            ++rec[s];
+            cnt[s] += __popc(m);
+        };
+        // warp-cooperative drain: records listed in shared memory, classified one per lane
+        // in the direct form from the global rows, then every owner emits its results in
+        // record order
+        auto drain = [&]() {
+            const int mine = npend[0] + npend[1];
+            int incl = mine;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            const int excl = incl - mine;
+            const int total = __shfl_sync(0xffffffffu, incl, 31);
+            uint32_t *drec = s_drec + wq * 256;
+            uint8_t *dres = s_dres + wq * 256;
+            int pos = excl;
+#pragma unroll
+            for (int s = 0; s < 2; ++s)
+                for (int r = 0; r < npend[s]; ++r)
+                    drec[pos++] = ((uint32_t)(2 * lane + s) << 16) |
+                                  ((uint32_t)(pend[s] >> (16 * (npend[s] - 1 - r))) & 0xffffu);
+            __syncwarp();
+            for (int t = lane; t < total; t += 32) {
+                const uint32_t ev = drec[t];
+                const int o = (int)(ev >> 16);
+                const int g0 = GS * (int)(ev & 0xffffu);
+                float qo[D];
+                uint64_t nqo[D];
+#pragma unroll
+                for (int k = 0; k < D; ++k) {
+                    qo[k] = dq[o * D + k];
+                    nqo[k] = f2pack(-qo[k], -qo[k]);
+                }
+                uint32_t res = 0;
+#pragma unroll
+                for (int h = 0; h < GS; ++h) {
+                    const int gg = g0 + h;
+                    if (gg < ngroups) {
+                        float4 xa[D];
+#pragma unroll
+                        for (int k = 0; k < D; ++k) xa[k] = g4[gg * D + k];
+                        uint64_t la, ha;
+                        group_d2<D>(xa, nqo, la, ha);
+                        const float2 pa = f2unpack(la), qa = f2unpack(ha);
+                        const uint32_t oa = mask4(pa.x, pa.y, qa.x, qa.y, T_out);
+                        if (oa) {
+                            uint32_t ia = mask4(pa.x, pa.y, qa.x, qa.y, T_in);
+                            if (ia ^ oa) ia |= resolve4<D>(oa & ~ia, xa, qo, R2);
+                            res |= ia << (4 * h);
+                        }
+                    }
+                }
+                dres[t] = (uint8_t)res;
+            }
+            __syncwarp();
+            pos = excl;
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+                for (int r = 0; r < npend[s]; ++r, ++pos) {
+                    const uint32_t res = dres[pos];
+                    if (res) {
+                        const int g0 = GS * (int)((uint32_t)(pend[s] >> (16 * (npend[s] - 1 - r))) & 0xffffu);
+                        if (res & 15u) emit(s, g0, res & 15u);
+                        if (res >> 4) emit(s, g0 + 1, res >> 4);
+                    }
+                }
+                pend[s] = 0;
+                npend[s] = 0;
+            }
+            __syncwarp();
+        };
+        int g = 0;
+        uint32_t fa_addr = (uint32_t)__cvta_generic_to_shared(smem + sidx * buf_bytes);
+        for (; g + 1 < ngroups; g += 2, fa_addr += 32u * FW) {
+            float4 fa[FW], fb[FW];
+#pragma unroll
+            for (int k = 0; k < FW; ++k) {
+                fa[k] = lds128(fa_addr + 16u * k);
+                fb[k] = lds128(fa_addr + 16u * (FW + k));
+            }
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+                uint64_t la = f2pack(fa[D].x, fa[D].y), ha = f2pack(fa[D].z, fa[D].w);
+                uint64_t lb = f2pack(fb[D].x, fb[D].y), hb = f2pack(fb[D].z, fb[D].w);
+#pragma unroll
+                for (int k = 0; k < D; ++k) {
+                    la = f2fma(f2pack(fa[k].x, fa[k].y), nqc[s][k], la);
+                    ha = f2fma(f2pack(fa[k].z, fa[k].w), nqc[s][k], ha);
+                    lb = f2fma(f2pack(fb[k].x, fb[k].y), nqc[s][k], lb);
+                    hb = f2fma(f2pack(fb[k].z, fb[k].w), nqc[s][k], hb);
+                }
+                const float2 ea = f2unpack(la), eb = f2unpack(ha), ec = f2unpack(lb), ed = f2unpack(hb);
+                const float m1 = fminf(fminf(ea.x, ea.y), eb.x), m2 = fminf(fminf(eb.y, ec.x), ec.y);
+                const float m3 = fminf(fminf(ed.x, ed.y), m1);
+                if (fminf(m2, m3) <= thr[s]) {
+                    pend[s] = (pend[s] << 16) | (uint32_t)(g >> 1);
+                    ++npend[s];
+                }
+            }
+            if (__any_sync(0xffffffffu, (npend[0] >= 4) | (npend[1] >= 4))) drain();
+        }
+        if (g < ngroups) {   // tail group (odd count): direct form from the global rows, one record
+            float4 xa[D];
+#pragma unroll
+            for (int k = 0; k < D; ++k) xa[k] = g4[g * D + k];
+            bool flag[2];
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+                uint64_t nq[D];
+#pragma unroll
+                for (int k = 0; k < D; ++k) nq[k] = f2pack(-dq[(2 * lane + s) * D + k], -dq[(2 * lane + s) * D + k]);
+                uint64_t la, ha;
+                group_d2<D>(xa, nq, la, ha);
+                const float2 pa = f2unpack(la), qa = f2unpack(ha);
+                flag[s] = fminf(fminf(pa.x, pa.y), fminf(qa.x, qa.y)) <= T_out;
+            }
+            if (__any_sync(0xffffffffu, (flag[0] && npend[0] == 4) | (flag[1] && npend[1] == 4))) drain();
+#pragma unroll
+            for (int s = 0; s < 2; ++s)
+                if (flag[s]) {
+                    pend[s] = (pend[s] << 16) | (uint32_t)(g / GS);
+                    ++npend[s];
+                }
+        }
+        drain();
+        bool anylost = false;
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+            const bool ls = active[s] && lost[s];
+            anylost |= ls;
+            a.cnt[e[s]] = cnt[s] | (ls ? (int32_t)0x80000000 : 0);
+            if (a.nrec) a.nrec[e[s]] = (uint16_t)(rec[s] < cap ? rec[s] : cap);
+        }
+        if (__syncthreads_or(anylost) && tid == 0) a.ovf_items[atomicAdd(a.ovf_count, 1)] = (int32_t)item;
+    }
+}
+
 // Compaction of the recorded hits into the CSR: original ids via pi and distances as
 // (float)sqrt of the oracle-order fp64 squared distance.  One CTA per item; one thread
 // per (item, query) entry expands its slot records (the first `cap` records).
@@ -1254,6 +1492,15 @@ void run_lowd(const PassArgs &a, cudaStream_t s) {
     auto k = exp ? window_lowd<T, D, MODE, 3>
                  : (a.variant == 1 ? window_lowd<T, D, MODE, 1> : window_lowd<T, D, MODE, 2>);
     if (SYMOK && a.sym) k = exp ? window_lowd<T, D, MODE, 3, SYMOK> : window_lowd<T, D, MODE, 1, SYMOK>;
+    if constexpr (MODE == M_SCAN && sizeof(T) == 4) {
+        if (exp && a.scan2q && a.B == 256) {   // two queries per thread (128-thread CTAs)
+            auto k2 = a.sym ? window_lowd_2q<D, true> : window_lowd_2q<D, false>;
+            cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            const int g2 = persistent_grid(k2, 128, smem, a.total_items, a.sm_count);
+            SNN_LAUNCH(k2, g2, 128, smem, s, a);
+            return;
+        }
+    }
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int64_t work = MODE == M_FIX ? a.n_ovf : a.total_items;
     int g = persistent_grid(k, a.B, smem, work, a.sm_count);

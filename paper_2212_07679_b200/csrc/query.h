@@ -74,6 +74,7 @@ struct PassArgs {
     float *out_dist;
     int sm_count;
     int variant;            // low-d inner loop: groups of 4 candidates per iteration (1 or 2)
+    int scan2q = 0;         // fp32 expanded-filter scan: two queries per thread (window_lowd_2q)
     // DBSCAN modes (sorted positions)
     const uint8_t *core;    // core flags
     int32_t *parent;        // union-find parents

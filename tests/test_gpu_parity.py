@@ -448,6 +448,33 @@ def test_dbscan_c5_full_size_sampled(snn):
 
 
 # --------------------------------------------------------------------------- tensor-core path (a9)
+@pytest.mark.parametrize("d,self_q,opts", [(3, True, {}), (2, True, {}), (3, False, {}), (5, True, {"cap": 1}),
+                                           (8, False, {"cap": 2, "ovf_records": 40}), (1, True, {}),
+                                           (3, True, {"chunk": 1024}), (4, True, {"symmetric": -1})])
+def test_scan2q_identical(snn, d, self_q, opts):
+    """K8 scan with two queries per thread (option scan2q) vs one: bit-identical CSR, equal
+    to the oracle; symmetric / two-sided self-queries, separate queries, slot overflow and
+    the overflow-list limit (fix pass)."""
+    import paper_2212_07679_b200 as p
+    rng = np.random.default_rng(900 + d)
+    X = (rng.random((30000, d)) * 10).astype(np.float32)
+    Q = None if self_q else (rng.random((7001, d)) * 10).astype(np.float32)
+    R = {1: 0.002, 2: 0.05, 3: 0.25, 4: 0.6, 5: 1.0, 8: 2.5}[d]
+    outs = []
+    try:
+        for k, v in opts.items():
+            p.snn_set_option(k, v)
+        for v in (0, 1):
+            p.snn_set_option("scan2q", v)
+            outs.append(run(snn, X, Q, R))
+    finally:
+        for k in list(opts) + ["scan2q"]:
+            p.snn_set_option(k, 0)
+    compare(outs[1], oracle.radius_query(X, X if self_q else Q, R))
+    for f in ("offsets", "indices", "distances"):
+        np.testing.assert_array_equal(np.asarray(getattr(outs[1], f)), np.asarray(getattr(outs[0], f)))
+
+
 def test_tc_and_generic_paths_agree_exactly(snn):
     """Same data through the tcgen05 TF32 filter and the SIMT generic kernel."""
     import paper_2212_07679_b200 as p
