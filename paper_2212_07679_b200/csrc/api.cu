@@ -62,6 +62,7 @@ struct Options {
     int union_phased = 0;      // DBSCAN union pass (union_snap): chunk k of every block in launch k (near pairs first)
     int union_stats = 0;       // DBSCAN union pass: count pairs sent to the union path (diagnostics)
     int finalize_order = 1;    // staged rows: rows_finalize walks rows in original-id order (sequential CSR writes)
+    int finalize_pipe = 1;     // symmetric direct rows: 32 rows per warp, software-pipelined (-1: warp per row)
     int gram_rows = 65536;     // tensor-core Gram of a large build: rows sampled (stride) down to ~this many
     int64_t gram_min_elems = int64_t(1) << 27;   // ... when n*d is at least this
 };
@@ -328,7 +329,8 @@ snn_status snn_get_option(const char *key, int64_t *value) {
         {"window_all", &Options::window_all}, {"simt_filter", &Options::simt_filter},
         {"lowd_tc", &Options::lowd_tc}, {"lowd_tc_tiles", &Options::lowd_tc_tiles},
         {"lowd_tc_group", &Options::lowd_tc_group}, {"union_load", &Options::union_load},
-        {"finalize_order", &Options::finalize_order}, {"gram_rows", &Options::gram_rows},
+        {"finalize_order", &Options::finalize_order}, {"finalize_pipe", &Options::finalize_pipe},
+        {"gram_rows", &Options::gram_rows},
         {"count_warp", &Options::count_warp}, {"union_snap", &Options::union_snap},
         {"union_stats", &Options::union_stats}, {"union_phased", &Options::union_phased},
         {"union_behind", &Options::union_behind}, {"union_chunk", &Options::union_chunk},
@@ -412,6 +414,7 @@ snn_status snn_set_option(const char *key, int64_t value) {
     if (k == "gram_rows") { g_opt.gram_rows = value == 0 ? 65536 : (value < 0 ? 0 : (int)value); return SNN_OK; }
     if (k == "gram_min_elems") { g_opt.gram_min_elems = value == 0 ? (int64_t(1) << 27) : value; return SNN_OK; }
     if (k == "finalize_order") { g_opt.finalize_order = value < 0 ? 0 : 1; return SNN_OK; }
+    if (k == "finalize_pipe") { g_opt.finalize_pipe = value < 0 ? 0 : 1; return SNN_OK; }
     if (k == "count_warp") { g_opt.count_warp = value < 0 ? 0 : 1; return SNN_OK; }
     if (k == "union_snap") {   // 0: default; -1 off; 2: register-capped variant; 3, 4: diagnostics (labels invalid)
         if (value < -1 || value > 4) return fail(SNN_ERR_INVALID_ARGUMENT, "union_snap must be -1..4");
@@ -1287,6 +1290,7 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
     a.sm_count = sms;
     a.variant = g_opt.variant;
     a.scan2q = g_opt.scan2q;
+    a.fpipe = g_opt.finalize_pipe;
     if (!generic && !f64 && idx->Xf && g_opt.simt_filter >= 0) {
         double c1h = 1.0, r2h = 0.0;
         simt_filter_consts(D, R, &c1h, &r2h);

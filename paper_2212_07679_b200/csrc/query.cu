@@ -1446,6 +1446,106 @@ __global__ void __launch_bounds__(256) rows_finalize_warp(PassArgs a) {
         __syncwarp();
     }
 }
+// Symmetric self-query with direct rows (no staging): warp per 32 consecutive key
+// positions.  The lanes load the 32 rows' L counts, cursors and self ids together
+// (coalesced), then the warp walks the rows software-pipelined: row k+1's L segment is
+// loaded while row k is ranked, and row k's output stores wait one row for their perm[]
+// load, so the per-row chain of dependent global loads (count -> segment -> perm ->
+// store) overlaps across rows instead of serialising (rows_finalize_warp: one row per warp).
+// Rows with more than 64 L entries take the shared-memory bitonic sort of
+// rows_finalize_warp (<= 512) or rows_lsort_block (more).
+__global__ void __launch_bounds__(256) rows_finalize_pipe(PassArgs a) {
+    __shared__ unsigned long long sbuf[8][kLWarp];
+    const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+    unsigned long long *buf = sbuf[w];
+    const int64_t nw = (int64_t)gridDim.x * 8;
+    for (int64_t r0 = ((int64_t)blockIdx.x * 8 + w) * 32; r0 < a.m; r0 += nw * 32) {
+        const int64_t spl = r0 + lane;
+        const bool own = spl < a.m && spl >= a.own_lo && spl < a.own_hi;
+        const int cl = own ? a.lcnt[spl] : 0;
+        const int64_t bl = own ? (int64_t)a.lpos[spl] - cl : 0;   // L cursor advanced by cl
+        if (own) {   // the point itself, after its L segment
+            SNN_DASSERT(bl + cl < a.offsets[a.m]);
+            a.out_idx[bl + cl] = a.perm[spl];
+            a.out_dist[bl + cl] = 0.f;
+        }
+        auto load = [&](int k, unsigned long long &v0, unsigned long long &v1) {
+            const int c = __shfl_sync(0xffffffffu, cl, k);
+            const int64_t b = __shfl_sync(0xffffffffu, bl, k);
+            v0 = (c <= 64 && lane < c) ? a.tmpL[b + lane] : ~0ull;
+            v1 = (c <= 64 && lane + 32 < c) ? a.tmpL[b + lane + 32] : ~0ull;
+        };
+        unsigned long long v0, v1;
+        load(0, v0, v1);
+        // pending stores of the previous row: id (perm[] load in flight), distance, position
+        int32_t pid0 = 0, pid1 = 0;
+        float pd0 = 0.f, pd1 = 0.f;
+        int64_t pp0 = -1, pp1 = -1;
+        for (int k = 0; k < 32; ++k) {
+            const int c = __shfl_sync(0xffffffffu, cl, k);
+            const int64_t b = __shfl_sync(0xffffffffu, bl, k);
+            unsigned long long n0 = ~0ull, n1 = ~0ull;
+            if (k + 1 < 32) load(k + 1, n0, n1);   // prefetch the next row's segment
+            int64_t q0 = -1, q1 = -1;
+            int32_t id0 = 0, id1 = 0;
+            if (c > 0 && c <= 32) {   // rank sort: positions are unique within a row
+                const uint32_t k0 = (uint32_t)(v0 >> 32);
+                int r0 = 0;
+                for (int j = 0; j < c; j += 4) {   // lanes >= c hold ~0: never "<"
+                    r0 += __shfl_sync(0xffffffffu, k0, j) < k0;
+                    r0 += __shfl_sync(0xffffffffu, k0, j + 1) < k0;
+                    r0 += __shfl_sync(0xffffffffu, k0, j + 2) < k0;
+                    r0 += __shfl_sync(0xffffffffu, k0, j + 3) < k0;
+                }
+                if (lane < c) { q0 = b + r0; id0 = a.perm[k0]; }
+            } else if (c > 32 && c <= 64) {
+                const uint32_t k0 = (uint32_t)(v0 >> 32), k1 = (uint32_t)(v1 >> 32);
+                int r0 = 0, r1 = 0;
+                const int c32 = c < 32 ? c : 32;
+                for (int j = 0; j < c32; ++j) {
+                    const uint32_t kj = __shfl_sync(0xffffffffu, k0, j);
+                    r0 += kj < k0;
+                    r1 += kj < k1;
+                }
+                for (int j = 0; j < c - 32; ++j) {
+                    const uint32_t kj = __shfl_sync(0xffffffffu, k1, j);
+                    r0 += kj < k0;
+                    r1 += kj < k1;
+                }
+                if (lane < c) { q0 = b + r0; id0 = a.perm[k0]; }
+                if (lane + 32 < c) { q1 = b + r1; id1 = a.perm[k1]; }
+            } else if (c > 64 && c <= kLWarp) {   // shared-memory bitonic sort
+                int S = 128;
+                while (S < c) S <<= 1;
+                for (int i = lane; i < S; i += 32) buf[i] = i < c ? a.tmpL[b + i] : ~0ull;
+                __syncwarp();
+                for (int kk = 2; kk <= S; kk <<= 1) {
+                    for (int j = kk >> 1; j > 0; j >>= 1) {
+                        for (int t = lane; t < S / 2; t += 32) {
+                            const int i = 2 * t - (t & (j - 1)), p = i + j;
+                            const unsigned long long x = buf[i], y = buf[p];
+                            if ((x > y) == ((i & kk) == 0)) { buf[i] = y; buf[p] = x; }
+                        }
+                        __syncwarp();
+                    }
+                }
+                for (int i = lane; i < c; i += 32) lemit(a, buf[i], b + i);
+                __syncwarp();
+            }
+            if (pp0 >= 0) { a.out_idx[pp0] = pid0; a.out_dist[pp0] = pd0; }
+            if (pp1 >= 0) { a.out_idx[pp1] = pid1; a.out_dist[pp1] = pd1; }
+            SNN_DASSERT(q0 < 0 || q0 < a.offsets[a.m]);
+            SNN_DASSERT(q1 < 0 || q1 < a.offsets[a.m]);
+            pp0 = q0; pid0 = id0; pd0 = __uint_as_float((uint32_t)v0);
+            pp1 = q1; pid1 = id1; pd1 = __uint_as_float((uint32_t)v1);
+            v0 = n0;
+            v1 = n1;
+        }
+        if (pp0 >= 0) { a.out_idx[pp0] = pid0; a.out_dist[pp0] = pd0; }
+        if (pp1 >= 0) { a.out_idx[pp1] = pid1; a.out_dist[pp1] = pd1; }
+    }
+}
+
 __global__ void __launch_bounds__(1024) rows_lsort_block(PassArgs a) {
     extern __shared__ unsigned long long lbuf[];
     for (int64_t sp = blockIdx.x; sp < a.m; sp += gridDim.x) {
@@ -1729,7 +1829,13 @@ void launch_rows_finalize(const PassArgs &a, int32_t max_l, cudaStream_t s) {
     if (a.m == 0 || (!a.sym && !a.soff)) return;
     int64_t g = ceil_div(a.m * 32, 256);
     if (g > 148 * 16) g = 148 * 16;
-    SNN_LAUNCH(rows_finalize_warp, (int)g, 256, 0, s, a);
+    if (a.sym && !a.soff && a.fpipe) {   // direct rows: 32 rows per warp, pipelined
+        g = ceil_div(a.m, 256);   // 8 warps x 32 rows per CTA
+        if (g > 148 * 8) g = 148 * 8;
+        SNN_LAUNCH(rows_finalize_pipe, (int)g, 256, 0, s, a);
+    } else {
+        SNN_LAUNCH(rows_finalize_warp, (int)g, 256, 0, s, a);
+    }
     if (!a.sym || max_l <= kLWarp) return;
     const size_t smem = (size_t)kLBlock * 8;
     cudaFuncSetAttribute(rows_lsort_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

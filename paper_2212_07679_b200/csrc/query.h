@@ -97,6 +97,7 @@ struct PassArgs {
     const int64_t *soff = nullptr;
     unsigned long long *stage = nullptr;   // staged entries: (fp32 distance bits << 32 | id)
     const int32_t *qinv = nullptr;         // inverse of qperm (original id -> key position): rows_finalize order
+    int fpipe = 1;                         // symmetric direct rows: rows_finalize_pipe (0: rows_finalize_warp)
     // partitioned symmetric self-query: the rows this part owns (key positions); queries
     // before own_lo are ghost queries (mirrored entries only), mirrors into rows >= own_hi
     // are left to their owning part

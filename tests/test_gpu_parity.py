@@ -1061,29 +1061,57 @@ def test_load_rewrites_padding_sentinels(snn, tmp_path, dt):
 @pytest.mark.parametrize("d", [2, 3, 6])
 def test_row_staging_and_symmetry_options_identical(snn, d):
     """Direct final-row writes (default) vs key-order row staging, symmetric vs two-sided
-    self-queries, expanded filter on/off, balanced vs per-entry compaction: bit-identical
-    CSR, equal to the oracle."""
+    self-queries, expanded filter on/off, balanced vs per-entry compaction, pipelined vs
+    warp-per-row L-segment finalize: bit-identical CSR, equal to the oracle."""
     import paper_2212_07679_b200 as p
     rng = np.random.default_rng(1400 + d)
     X = (rng.random((20000, d)) * 20).astype(np.float32)
     R = {2: 0.12, 3: 0.5, 6: 2.5}[d]
     outs = []
     try:
-        for st, sy, sf, bc in [(1, 1, 0, 0), (-1, 1, 0, 0), (1, -1, 0, 0), (-1, -1, -1, 0), (1, 1, -1, 0),
-                               (1, 1, 0, -1), (-1, 1, -1, -1)]:
+        for st, sy, sf, bc, fp in [(1, 1, 0, 0, 0), (-1, 1, 0, 0, 0), (1, -1, 0, 0, 0), (-1, -1, -1, 0, 0),
+                                   (1, 1, -1, 0, 0), (1, 1, 0, -1, 0), (-1, 1, -1, -1, 0), (-1, 1, 0, 0, -1)]:
             p.snn_set_option("stage_rows", st)
             p.snn_set_option("symmetric", sy)
             p.snn_set_option("simt_filter", sf)
             p.snn_set_option("balanced_compact", bc)
+            p.snn_set_option("finalize_pipe", fp)
             outs.append(run(snn, X, None, R))
     finally:
-        for k in ("stage_rows", "symmetric", "simt_filter", "balanced_compact"):
+        for k in ("stage_rows", "symmetric", "simt_filter", "balanced_compact", "finalize_pipe"):
             p.snn_set_option(k, 0)
     compare(outs[0], oracle.radius_query(X, X, R))
     for o in outs[1:]:
         np.testing.assert_array_equal(np.asarray(o.offsets), np.asarray(outs[0].offsets))
         np.testing.assert_array_equal(np.asarray(o.indices), np.asarray(outs[0].indices))
         np.testing.assert_array_equal(np.asarray(o.distances), np.asarray(outs[0].distances))
+
+
+def test_finalize_row_size_classes(snn):
+    """Symmetric self-query L segments of every size class of the finalize (rank sort <= 64
+    entries in the pipelined kernel, shared-memory bitonic <= 512, CTA sort beyond): dense
+    blobs of 20 / 50 / 300 / 3000 points plus scattered points; the pipelined and the
+    warp-per-row finalize give bit-identical CSRs, equal to the oracle."""
+    import paper_2212_07679_b200 as p
+    rng = np.random.default_rng(1451)
+    parts = [rng.random((9000, 3)) * 40.0]
+    for k, c in zip((20, 50, 300, 3000), ((5, 5, 5), (15, 15, 15), (25, 25, 25), (35, 35, 35))):
+        parts.append(np.asarray(c) + rng.standard_normal((k, 3)) * 0.05)
+    X = np.concatenate(parts).astype(np.float32)
+    X = X[rng.permutation(len(X))]
+    R = 0.4
+    outs = []
+    try:
+        for fp in (0, -1):
+            p.snn_set_option("finalize_pipe", fp)
+            outs.append(run(snn, X, None, R))
+    finally:
+        p.snn_set_option("finalize_pipe", 0)
+    assert np.diff(outs[0].offsets).max() >= 3000
+    compare(outs[0], oracle.radius_query(X, X, R))
+    for a, b in zip((outs[1].offsets, outs[1].indices, outs[1].distances),
+                    (outs[0].offsets, outs[0].indices, outs[0].distances)):
+        np.testing.assert_array_equal(np.asarray(a), np.asarray(b))
 
 
 # --------------------------------------------------------------------------- query sharding (§8(e))
