@@ -3,7 +3,7 @@
 set -u
 TAG=$1; shift
 OUT=gpurun_out/$TAG; mkdir -p $OUT
-python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1 || { echo BUILD FAIL; tail -20 $OUT/build.log; exit 1; }
+[ -n "${NOBUILD:-}" ] || python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1 || { echo BUILD FAIL; tail -20 $OUT/build.log; exit 1; }
 for spec in "$@"; do
   IFS=: read cfg steps opts <<< "$spec"
   args=""; name="${cfg}"
