@@ -53,7 +53,7 @@ struct Options {
     int lowd_tc_tiles = 8;     // 256-candidate tiles per work item (low-d tensor-core path)
     int lowd_tc_group = 8;     // query blocks per raster group (low-d tensor-core path)
     int union_load = 1;        // DBSCAN union pass: parent pre-check load (0 volatile, 1 relaxed.gpu, 2 ld.cg)
-    int count_warp = 1;        // DBSCAN core counts: warp per point, outward scan (-1: CTA per block)
+    int count_warp = 2;        // DBSCAN core counts: warp per point, outward scan, next step's rows prefetched (1: no prefetch; -1: CTA per block)
     int union_snap = 1;        // DBSCAN union pass (fp32, d <= 8): staged parent snapshot pre-check (-1: window_lowd)
     int union_behind = 1;      // DBSCAN union pass (union_snap): candidates behind the block (pairs j < i)
     int dbscan_block = 256;    // DBSCAN: queries per block (windows, union and border passes)
@@ -62,6 +62,7 @@ struct Options {
     int union_phased = 0;      // DBSCAN union pass (union_snap): chunk k of every block in launch k (near pairs first)
     int union_stats = 0;       // DBSCAN union pass: count pairs sent to the union path (diagnostics)
     int finalize_order = 1;    // staged rows: rows_finalize walks rows in original-id order (sequential CSR writes)
+    int lkey = 1;              // symmetric direct rows: mirrored entries gathered in key order (-1: at the CSR rows)
     int finalize_pipe = 1;     // symmetric direct rows: 32 rows per warp, software-pipelined (-1: warp per row)
     int gram_rows = 65536;     // tensor-core Gram of a large build: rows sampled (stride) down to ~this many
     int64_t gram_min_elems = int64_t(1) << 27;   // ... when n*d is at least this
@@ -329,7 +330,7 @@ snn_status snn_get_option(const char *key, int64_t *value) {
         {"window_all", &Options::window_all}, {"simt_filter", &Options::simt_filter},
         {"lowd_tc", &Options::lowd_tc}, {"lowd_tc_tiles", &Options::lowd_tc_tiles},
         {"lowd_tc_group", &Options::lowd_tc_group}, {"union_load", &Options::union_load},
-        {"finalize_order", &Options::finalize_order}, {"finalize_pipe", &Options::finalize_pipe},
+        {"finalize_order", &Options::finalize_order}, {"finalize_pipe", &Options::finalize_pipe}, {"lkey", &Options::lkey},
         {"gram_rows", &Options::gram_rows},
         {"count_warp", &Options::count_warp}, {"union_snap", &Options::union_snap},
         {"union_stats", &Options::union_stats}, {"union_phased", &Options::union_phased},
@@ -415,7 +416,8 @@ snn_status snn_set_option(const char *key, int64_t value) {
     if (k == "gram_min_elems") { g_opt.gram_min_elems = value == 0 ? (int64_t(1) << 27) : value; return SNN_OK; }
     if (k == "finalize_order") { g_opt.finalize_order = value < 0 ? 0 : 1; return SNN_OK; }
     if (k == "finalize_pipe") { g_opt.finalize_pipe = value < 0 ? 0 : 1; return SNN_OK; }
-    if (k == "count_warp") { g_opt.count_warp = value < 0 ? 0 : 1; return SNN_OK; }
+    if (k == "lkey") { g_opt.lkey = value < 0 ? 0 : 1; return SNN_OK; }
+    if (k == "count_warp") { g_opt.count_warp = value < 0 ? 0 : (value == 0 || value >= 2 ? 2 : 1); return SNN_OK; }
     if (k == "union_snap") {   // 0: default; -1 off; 2: register-capped variant; 3, 4: diagnostics (labels invalid)
         if (value < -1 || value > 4) return fail(SNN_ERR_INVALID_ARGUMENT, "union_snap must be -1..4");
         g_opt.union_snap = value < 0 ? 0 : (value == 0 ? 1 : (int)value);
@@ -1353,6 +1355,12 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
     }
     if (sym) {
         CKR(ws.alloc(&a.tmpL, (size_t)(r->nnz > 0 ? r->nnz : 1)), "alloc mirrored entries");
+        if (!stage && g_opt.lkey) {   // L segments in key order (sum of lcnt <= nnz)
+            int64_t *loff = nullptr;
+            CKR(ws.alloc(&loff, (size_t)m + 1), "alloc mirrored-entry offsets");
+            exclusive_scan_i32_to_i64(a.lcnt, loff, m, scan_tmp, s);
+            a.loff = loff;
+        }
         launch_sym_lpos_init(a, s);
     }
     if (r->nnz > 0) {

@@ -1381,7 +1381,7 @@ __global__ void __launch_bounds__(256) rows_finalize_warp(PassArgs a) {
         if (sp < a.own_lo || sp >= a.own_hi) continue;   // another part's (empty) row
         const int cnt = a.sym ? a.lcnt[sp] : 0;
         const int64_t src = a.soff ? a.soff[sp] : (int64_t)a.lpos[sp] - cnt;   // L cursor advanced by cnt
-        const int64_t dst = a.soff ? a.offsets[a.qinv ? r : a.qperm[sp]] : src;
+        const int64_t dst = a.soff ? a.offsets[a.qinv ? r : a.qperm[sp]] : (a.loff ? row_base(a, sp) : src);
         if (a.soff) {   // U part (after L and self) or the whole row
             const int64_t k0 = a.sym ? cnt + 1 : 0, len = a.soff[sp + 1] - src;
             SNN_DASSERT(src >= 0 && src + len <= a.offsets[a.m] && dst + len <= a.offsets[a.m]);
@@ -1464,10 +1464,11 @@ __global__ void __launch_bounds__(256) rows_finalize_pipe(PassArgs a) {
         const bool own = spl < a.m && spl >= a.own_lo && spl < a.own_hi;
         const int cl = own ? a.lcnt[spl] : 0;
         const int64_t bl = own ? (int64_t)a.lpos[spl] - cl : 0;   // L cursor advanced by cl
+        const int64_t dl = own && a.loff ? row_base(a, spl) : bl;   // row start in the CSR
         if (own) {   // the point itself, after its L segment
-            SNN_DASSERT(bl + cl < a.offsets[a.m]);
-            a.out_idx[bl + cl] = a.perm[spl];
-            a.out_dist[bl + cl] = 0.f;
+            SNN_DASSERT(dl + cl < a.offsets[a.m]);
+            a.out_idx[dl + cl] = a.perm[spl];
+            a.out_dist[dl + cl] = 0.f;
         }
         auto load = [&](int k, unsigned long long &v0, unsigned long long &v1) {
             const int c = __shfl_sync(0xffffffffu, cl, k);
@@ -1483,7 +1484,8 @@ __global__ void __launch_bounds__(256) rows_finalize_pipe(PassArgs a) {
         int64_t pp0 = -1, pp1 = -1;
         for (int k = 0; k < 32; ++k) {
             const int c = __shfl_sync(0xffffffffu, cl, k);
-            const int64_t b = __shfl_sync(0xffffffffu, bl, k);
+            const int64_t b = __shfl_sync(0xffffffffu, bl, k);    // L segment (tmpL)
+            const int64_t o = __shfl_sync(0xffffffffu, dl, k);    // row start (CSR)
             unsigned long long n0 = ~0ull, n1 = ~0ull;
             if (k + 1 < 32) load(k + 1, n0, n1);   // prefetch the next row's segment
             int64_t q0 = -1, q1 = -1;
@@ -1497,7 +1499,7 @@ __global__ void __launch_bounds__(256) rows_finalize_pipe(PassArgs a) {
                     r0 += __shfl_sync(0xffffffffu, k0, j + 2) < k0;
                     r0 += __shfl_sync(0xffffffffu, k0, j + 3) < k0;
                 }
-                if (lane < c) { q0 = b + r0; id0 = a.perm[k0]; }
+                if (lane < c) { q0 = o + r0; id0 = a.perm[k0]; }
             } else if (c > 32 && c <= 64) {
                 const uint32_t k0 = (uint32_t)(v0 >> 32), k1 = (uint32_t)(v1 >> 32);
                 int r0 = 0, r1 = 0;
@@ -1512,8 +1514,8 @@ __global__ void __launch_bounds__(256) rows_finalize_pipe(PassArgs a) {
                     r0 += kj < k0;
                     r1 += kj < k1;
                 }
-                if (lane < c) { q0 = b + r0; id0 = a.perm[k0]; }
-                if (lane + 32 < c) { q1 = b + r1; id1 = a.perm[k1]; }
+                if (lane < c) { q0 = o + r0; id0 = a.perm[k0]; }
+                if (lane + 32 < c) { q1 = o + r1; id1 = a.perm[k1]; }
             } else if (c > 64 && c <= kLWarp) {   // shared-memory bitonic sort
                 int S = 128;
                 while (S < c) S <<= 1;
@@ -1529,7 +1531,7 @@ __global__ void __launch_bounds__(256) rows_finalize_pipe(PassArgs a) {
                         __syncwarp();
                     }
                 }
-                for (int i = lane; i < c; i += 32) lemit(a, buf[i], b + i);
+                for (int i = lane; i < c; i += 32) lemit(a, buf[i], o + i);
                 __syncwarp();
             }
             if (pp0 >= 0) { a.out_idx[pp0] = pid0; a.out_dist[pp0] = pd0; }
@@ -1552,7 +1554,7 @@ __global__ void __launch_bounds__(1024) rows_lsort_block(PassArgs a) {
         const int cnt = a.lcnt[sp];
         if (cnt <= kLWarp || cnt > kLBlock) continue;
         const int64_t o0 = a.soff ? a.soff[sp] : (int64_t)a.lpos[sp] - cnt;
-        const int64_t dst = a.soff ? a.offsets[a.qperm[sp]] : o0;
+        const int64_t dst = a.soff ? a.offsets[a.qperm[sp]] : (a.loff ? row_base(a, sp) : o0);
         int S = 1024;
         while (S < cnt) S <<= 1;
         for (int i = threadIdx.x; i < S; i += blockDim.x) lbuf[i] = i < cnt ? a.tmpL[o0 + i] : ~0ull;
@@ -1803,7 +1805,7 @@ void launch_row_totals_sym(const int32_t *cnt, int32_t *pre, const int64_t *item
 
 __global__ void sym_lpos_init(PassArgs a) {
     for (int64_t sp = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; sp < a.m; sp += (int64_t)gridDim.x * blockDim.x)
-        a.lpos[sp] = (unsigned long long)row_base(a, sp);
+        a.lpos[sp] = (unsigned long long)(a.loff ? a.loff[sp] : row_base(a, sp));
 }
 
 void launch_sym_lpos_init(const PassArgs &a, cudaStream_t s) {
@@ -2106,7 +2108,10 @@ __global__ void __launch_bounds__(256) core_count_kernel(PassArgs a, int32_t *co
 // barrier held 77% of its stall samples on config 5).  Same exact classification (rigorous
 // fp32 direct-form thresholds, oracle-order fp64 in between).  count = |N_eps| if below
 // min_pts, else some value >= min_pts.
-template <typename T, int D>
+// PF: the next step's rows (32 positions each side) are loaded before this step's test and
+// warp reduction, so a warp keeps two steps of row loads in flight (the loop is bound by
+// the latency of its row loads: the early exit makes every step depend on the last)
+template <typename T, int D, bool PF = true>
 __global__ void __launch_bounds__(256) core_count_warp_kernel(PassArgs a, int32_t *count,
                                                               unsigned long long *evaluated) {
     const T *Xs = static_cast<const T *>(a.Xs);
@@ -2139,16 +2144,38 @@ __global__ void __launch_bounds__(256) core_count_warp_kernel(PassArgs a, int32_
         T q[D];
         row(sp, q);
         int32_t c = 1;   // the point itself
-        for (int64_t off = 1;; off += 32) {
-            const int64_t jr = sp + off + lane, jl = sp - off - lane;
-            const bool vr = jr < hi, vl = jl >= lo;
-            if (!__any_sync(0xffffffffu, vr || vl)) break;
-            int h = 0;
-            if (vr) { T x[D]; row(jr, x); h += hit(x, q); }
-            if (vl) { T x[D]; row(jl, x); h += hit(x, q); }
-            ev += (unsigned long long)(vr + vl);
-            c += __reduce_add_sync(0xffffffffu, h);
-            if (c >= mp) break;
+        if constexpr (PF) {
+            T xr[D], xl[D];
+            int64_t jr = sp + 1 + lane, jl = sp - 1 - lane;
+            bool vr = jr < hi, vl = jl >= lo;
+            if (vr) row(jr, xr);
+            if (vl) row(jl, xl);
+            while (__any_sync(0xffffffffu, vr || vl)) {
+                const int64_t jr2 = jr + 32, jl2 = jl - 32;
+                const bool vr2 = jr2 < hi, vl2 = jl2 >= lo;
+                T nr[D], nl[D];
+                if (vr2) row(jr2, nr);
+                if (vl2) row(jl2, nl);
+                const int h = (vr ? (int)hit(xr, q) : 0) + (vl ? (int)hit(xl, q) : 0);
+                ev += (unsigned long long)(vr + vl);
+                c += __reduce_add_sync(0xffffffffu, h);
+                if (c >= mp) break;
+#pragma unroll
+                for (int k = 0; k < D; ++k) { xr[k] = nr[k]; xl[k] = nl[k]; }
+                jr = jr2; jl = jl2; vr = vr2; vl = vl2;
+            }
+        } else {
+            for (int64_t off = 1;; off += 32) {
+                const int64_t jr = sp + off + lane, jl = sp - off - lane;
+                const bool vr = jr < hi, vl = jl >= lo;
+                if (!__any_sync(0xffffffffu, vr || vl)) break;
+                int h = 0;
+                if (vr) { T x[D]; row(jr, x); h += hit(x, q); }
+                if (vl) { T x[D]; row(jl, x); h += hit(x, q); }
+                ev += (unsigned long long)(vr + vl);
+                c += __reduce_add_sync(0xffffffffu, h);
+                if (c >= mp) break;
+            }
         }
         if (lane == 0) count[sp] = c;
     }
@@ -2227,7 +2254,13 @@ void launch_union_seed(const PassArgs &a, int max_steps, cudaStream_t s) {
 void launch_core_counts(const PassArgs &a, int32_t *count, unsigned long long *evaluated, cudaStream_t s) {
     if (a.nblocks == 0) return;
     if (a.count_warp) {
-#define FN(T, D) SNN_LAUNCH((core_count_warp_kernel<T, D>), a.sm_count * 8, 256, 0, s, a, count, evaluated)
+        if (a.count_warp == 2) {
+#define FN(T, D) SNN_LAUNCH((core_count_warp_kernel<T, D, true>),                                     \
+                          persistent_grid(core_count_warp_kernel<T, D, true>, 256, 0, a.m, a.sm_count), 256, 0, s, a, count, evaluated)
+            SNN_LOWD_DISPATCH(FN)
+#undef FN
+        }
+#define FN(T, D) SNN_LAUNCH((core_count_warp_kernel<T, D, false>), a.sm_count * 8, 256, 0, s, a, count, evaluated)
         SNN_LOWD_DISPATCH(FN)
 #undef FN
     }

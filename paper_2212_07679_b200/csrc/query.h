@@ -97,6 +97,10 @@ struct PassArgs {
     const int64_t *soff = nullptr;
     unsigned long long *stage = nullptr;   // staged entries: (fp32 distance bits << 32 | id)
     const int32_t *qinv = nullptr;         // inverse of qperm (original id -> key position): rows_finalize order
+    // direct rows: the mirrored entries of row sp are collected at loff[sp] (exclusive scan of
+    // lcnt in KEY order, nullptr: at the row's CSR start), so the compaction's scattered 8-byte
+    // stores land in a window of the buffer that follows its sweep through the blocks
+    const int64_t *loff = nullptr;
     int fpipe = 1;                         // symmetric direct rows: rows_finalize_pipe (0: rows_finalize_warp)
     // partitioned symmetric self-query: the rows this part owns (key positions); queries
     // before own_lo are ghost queries (mirrored entries only), mirrors into rows >= own_hi
