@@ -53,7 +53,7 @@ struct Options {
     int lowd_tc_tiles = 8;     // 256-candidate tiles per work item (low-d tensor-core path)
     int lowd_tc_group = 8;     // query blocks per raster group (low-d tensor-core path)
     int union_load = 1;        // DBSCAN union pass: parent pre-check load (0 volatile, 1 relaxed.gpu, 2 ld.cg)
-    int count_warp = 2;        // DBSCAN core counts: warp per point, outward scan, next step's rows prefetched (1: no prefetch; -1: CTA per block)
+    int count_warp = 1;        // DBSCAN core counts: warp per point, outward scan (-1: CTA per block)
     int union_snap = 1;        // DBSCAN union pass (fp32, d <= 8): staged parent snapshot pre-check (-1: window_lowd)
     int union_behind = 1;      // DBSCAN union pass (union_snap): candidates behind the block (pairs j < i)
     int dbscan_block = 256;    // DBSCAN: queries per block (windows, union and border passes)
@@ -417,7 +417,7 @@ snn_status snn_set_option(const char *key, int64_t value) {
     if (k == "finalize_order") { g_opt.finalize_order = value < 0 ? 0 : 1; return SNN_OK; }
     if (k == "finalize_pipe") { g_opt.finalize_pipe = value < 0 ? 0 : 1; return SNN_OK; }
     if (k == "lkey") { g_opt.lkey = value < 0 ? 0 : 1; return SNN_OK; }
-    if (k == "count_warp") { g_opt.count_warp = value < 0 ? 0 : (value == 0 || value >= 2 ? 2 : 1); return SNN_OK; }
+    if (k == "count_warp") { g_opt.count_warp = value < 0 ? 0 : 1; return SNN_OK; }
     if (k == "union_snap") {   // 0: default; -1 off; 2: register-capped variant; 3, 4: diagnostics (labels invalid)
         if (value < -1 || value > 4) return fail(SNN_ERR_INVALID_ARGUMENT, "union_snap must be -1..4");
         g_opt.union_snap = value < 0 ? 0 : (value == 0 ? 1 : (int)value);

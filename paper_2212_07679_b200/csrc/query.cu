@@ -2108,10 +2108,7 @@ __global__ void __launch_bounds__(256) core_count_kernel(PassArgs a, int32_t *co
 // barrier held 77% of its stall samples on config 5).  Same exact classification (rigorous
 // fp32 direct-form thresholds, oracle-order fp64 in between).  count = |N_eps| if below
 // min_pts, else some value >= min_pts.
-// PF: the next step's rows (32 positions each side) are loaded before this step's test and
-// warp reduction, so a warp keeps two steps of row loads in flight (the loop is bound by
-// the latency of its row loads: the early exit makes every step depend on the last)
-template <typename T, int D, bool PF = true>
+template <typename T, int D>
 __global__ void __launch_bounds__(256) core_count_warp_kernel(PassArgs a, int32_t *count,
                                                               unsigned long long *evaluated) {
     const T *Xs = static_cast<const T *>(a.Xs);
@@ -2144,38 +2141,16 @@ __global__ void __launch_bounds__(256) core_count_warp_kernel(PassArgs a, int32_
         T q[D];
         row(sp, q);
         int32_t c = 1;   // the point itself
-        if constexpr (PF) {
-            T xr[D], xl[D];
-            int64_t jr = sp + 1 + lane, jl = sp - 1 - lane;
-            bool vr = jr < hi, vl = jl >= lo;
-            if (vr) row(jr, xr);
-            if (vl) row(jl, xl);
-            while (__any_sync(0xffffffffu, vr || vl)) {
-                const int64_t jr2 = jr + 32, jl2 = jl - 32;
-                const bool vr2 = jr2 < hi, vl2 = jl2 >= lo;
-                T nr[D], nl[D];
-                if (vr2) row(jr2, nr);
-                if (vl2) row(jl2, nl);
-                const int h = (vr ? (int)hit(xr, q) : 0) + (vl ? (int)hit(xl, q) : 0);
-                ev += (unsigned long long)(vr + vl);
-                c += __reduce_add_sync(0xffffffffu, h);
-                if (c >= mp) break;
-#pragma unroll
-                for (int k = 0; k < D; ++k) { xr[k] = nr[k]; xl[k] = nl[k]; }
-                jr = jr2; jl = jl2; vr = vr2; vl = vl2;
-            }
-        } else {
-            for (int64_t off = 1;; off += 32) {
-                const int64_t jr = sp + off + lane, jl = sp - off - lane;
-                const bool vr = jr < hi, vl = jl >= lo;
-                if (!__any_sync(0xffffffffu, vr || vl)) break;
-                int h = 0;
-                if (vr) { T x[D]; row(jr, x); h += hit(x, q); }
-                if (vl) { T x[D]; row(jl, x); h += hit(x, q); }
-                ev += (unsigned long long)(vr + vl);
-                c += __reduce_add_sync(0xffffffffu, h);
-                if (c >= mp) break;
-            }
+        for (int64_t off = 1;; off += 32) {
+            const int64_t jr = sp + off + lane, jl = sp - off - lane;
+            const bool vr = jr < hi, vl = jl >= lo;
+            if (!__any_sync(0xffffffffu, vr || vl)) break;
+            int h = 0;
+            if (vr) { T x[D]; row(jr, x); h += hit(x, q); }
+            if (vl) { T x[D]; row(jl, x); h += hit(x, q); }
+            ev += (unsigned long long)(vr + vl);
+            c += __reduce_add_sync(0xffffffffu, h);
+            if (c >= mp) break;
         }
         if (lane == 0) count[sp] = c;
     }
@@ -2254,13 +2229,7 @@ void launch_union_seed(const PassArgs &a, int max_steps, cudaStream_t s) {
 void launch_core_counts(const PassArgs &a, int32_t *count, unsigned long long *evaluated, cudaStream_t s) {
     if (a.nblocks == 0) return;
     if (a.count_warp) {
-        if (a.count_warp == 2) {
-#define FN(T, D) SNN_LAUNCH((core_count_warp_kernel<T, D, true>),                                     \
-                          persistent_grid(core_count_warp_kernel<T, D, true>, 256, 0, a.m, a.sm_count), 256, 0, s, a, count, evaluated)
-            SNN_LOWD_DISPATCH(FN)
-#undef FN
-        }
-#define FN(T, D) SNN_LAUNCH((core_count_warp_kernel<T, D, false>), a.sm_count * 8, 256, 0, s, a, count, evaluated)
+#define FN(T, D) SNN_LAUNCH((core_count_warp_kernel<T, D>), a.sm_count * 8, 256, 0, s, a, count, evaluated)
         SNN_LOWD_DISPATCH(FN)
 #undef FN
     }
