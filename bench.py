@@ -243,7 +243,7 @@ def roofline_block(args, w, prof, times, dev, info):
     """Roofline of the dominant kernel, from CUDA-event times taken by the library on the
     launching stream (snn_profile_*) during the timed steps.
 
-    d <= 8 : K8 scan pass (window_lowd), FP32-ALU bound: (3d-1) flop per evaluated pair
+    d <= 8 : K8 scan pass (window_lowd / window_lowd_2q), FP32-ALU bound: (3d-1) flop per evaluated pair
              (eq:ip1) vs 148 SMs x 128 lanes x 2 x sm_max_mhz.
     d >= 32: K9 tcgen05 TF32 filter (tc_window_kernel), tensor bound: 2 kpad flop per pair
              (the X(J,:)^T x_q contraction) vs TF32 dense peak = measured
@@ -285,9 +285,12 @@ def roofline_block(args, w, prof, times, dev, info):
         peak = fp32_alu_peak_tflops(sm_max, n_sm)
         import paper_2212_07679_b200 as snn
         snap = snn.snn_get_option("union_snap") > 0 and w.X.dtype == np.float32 and w.d <= 8
+        o2q = snn.snn_get_option("scan2q")   # 0 = auto: on for d = 2, 3 (api.cu query_impl)
+        twoq = w.X.dtype == np.float32 and w.d <= 8 and (o2q > 0 or (o2q == 0 and w.d in (2, 3)))
         kernel, bound = ((f"union_snap_kernel<{w.d}> (K12 DBSCAN union pass, staged root snapshot)" if snap
                           else f"window_lowd<float,{w.d},union> (K12 DBSCAN union pass)") if fam == "dbscan_union"
-                         else f"window_lowd<float,{w.d},scan> (K8 scan pass)"), "alu"
+                         else (f"window_lowd_2q<{w.d}> (K8 scan pass, two queries per thread)" if twoq
+                               else f"window_lowd<float,{w.d},scan> (K8 scan pass)")), "alu"
         peak_src = f"FP32 FMA issue peak at {sm_max:.0f} MHz x {n_sm} SMs (sm_max_mhz, {src})"
         work = f"{flop_per_pair} flop per evaluated candidate pair (eq:ip1)"
     achieved = (flop_per_pair * kunits / klaunch) / (kms / klaunch * 1e-3) / 1e12 if klaunch else 0.0

@@ -288,8 +288,10 @@ snn_status snn_profile_read(const char *family, double *ms, uint64_t *launches, 
  *   "variant"        low-d scan loop: 1 = deferred-hit 2-group loop (default), 2 = 8-pair
  *                    direct loop
  *   "symmetric"      -1 = evaluate every pair twice in low-d self-queries (default: once)
- *   "scan2q"         1 = fp32 low-d scan with two queries per thread (128-thread CTAs;
- *                    measured slower on config 2, default off)
+ *   "scan2q"         fp32 low-d scan with two queries per thread (128-thread CTAs, each staged
+ *                    filter row feeds two queries): 0 = auto (default: on for d = 2, 3),
+ *                    1 = on for every d <= 8, -1 = off
+ *   "chunk2q"        candidates per work item of that scan (default 640, multiple of 64)
  *   "stage_rows"     1 = the compaction assembles rows in a key-order staging buffer, then
  *                    moves each row whole; default (0 / -1): it writes the final rows directly
  *   "balanced_compact" -1 = per-entry compaction threads (default for symmetric self-queries:

@@ -31,7 +31,8 @@ struct Options {
     int cap = 64;
     int32_t ovf_rec_cap = 1 << 20;
     int variant = 1;
-    int scan2q = 0;      // fp32 low-d scan with the expanded filter: two queries per thread
+    int scan2q = 0;      // fp32 low-d scan with the expanded filter, two queries per thread: 0 = auto (d = 2, 3), 1 = on, -1 = off
+    int chunk2q = 640;   // candidates per work item of that scan (128-thread CTAs: smaller chunks keep 7 CTAs per SM)
     int tc = 1;          // use the tcgen05 path for d >= tc_min_d
     int tc_min_d = 32;
     int tc_tiles = 8;    // 256-candidate tiles per work item on the tensor-core path
@@ -321,7 +322,7 @@ snn_status snn_get_option(const char *key, int64_t *value) {
     static const struct { const char *name; int Options::*field; } kInt[] = {
         {"force_generic", &Options::force_generic}, {"query_block", &Options::query_block},
         {"chunk", &Options::chunk}, {"power_iters", &Options::power_iters}, {"cap", &Options::cap},
-        {"variant", &Options::variant}, {"scan2q", &Options::scan2q}, {"tc", &Options::tc}, {"tc_min_d", &Options::tc_min_d},
+        {"variant", &Options::variant}, {"scan2q", &Options::scan2q}, {"chunk2q", &Options::chunk2q}, {"tc", &Options::tc}, {"tc_min_d", &Options::tc_min_d},
         {"tc_tiles", &Options::tc_tiles}, {"tc_diag", &Options::tc_diag}, {"tc_f16", &Options::tc_f16},
         {"tc_ares", &Options::tc_ares}, {"tc_group", &Options::tc_group},
         {"tc_wait_hint", &Options::tc_wait_hint}, {"tc_warp_arrive", &Options::tc_warp_arrive},
@@ -461,7 +462,13 @@ snn_status snn_set_option(const char *key, int64_t value) {
         g_opt.tc_group = (int)value;
         return SNN_OK;
     }
-    if (k == "scan2q") { g_opt.scan2q = value > 0 ? 1 : 0; return SNN_OK; }
+    if (k == "scan2q") { g_opt.scan2q = value > 0 ? 1 : value < 0 ? -1 : 0; return SNN_OK; }
+    if (k == "chunk2q") {
+        if (value == 0) value = 640;
+        if (value < 64 || value > 8192 || value % 64) return fail(SNN_ERR_INVALID_ARGUMENT, "chunk2q must be 64..8192, multiple of 64");
+        g_opt.chunk2q = (int)value;
+        return SNN_OK;
+    }
     if (k == "variant") {
         if (value == 0) value = 1;
         if (value < 1 || value > 2) return fail(SNN_ERR_INVALID_ARGUMENT, "variant must be 1 or 2");
@@ -1162,7 +1169,11 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
     }
     const bool generic = ld != 0;
     const int B = generic ? 64 : g_opt.query_block;
-    const int chunk = generic ? 1024 : g_opt.chunk;
+    // K8 with two queries per thread (fp32 radius queries with the expanded-form filter;
+    // measured faster on d = 2, 3 -- DESIGN.md section 6): smaller work items
+    const bool scan2q = !generic && !f64 && idx->Xf && g_opt.simt_filter >= 0 && B == 256 &&
+                        (g_opt.scan2q > 0 || (g_opt.scan2q == 0 && (D == 2 || D == 3)));
+    const int chunk = generic ? 1024 : scan2q ? g_opt.chunk2q : g_opt.chunk;
     const int64_t nblocks = ceil_div(m, B);
     int64_t *blk_lo = nullptr, *blk_hi = nullptr, *nitems = nullptr, *item_start = nullptr;
     uint8_t *scan_tmp = nullptr;
@@ -1291,7 +1302,7 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
     a.offsets = r->offsets; a.out_idx = nullptr; a.out_dist = nullptr;
     a.sm_count = sms;
     a.variant = g_opt.variant;
-    a.scan2q = g_opt.scan2q;
+    a.scan2q = scan2q ? 1 : 0;
     a.fpipe = g_opt.finalize_pipe;
     if (!generic && !f64 && idx->Xf && g_opt.simt_filter >= 0) {
         double c1h = 1.0, r2h = 0.0;

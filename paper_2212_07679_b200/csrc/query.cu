@@ -804,13 +804,22 @@ __global__ void __launch_bounds__(256) window_lowd(PassArgs a) {
 // staged filter row is read once for both queries, so the shared-memory loads and the loop
 // bookkeeping per pair halve.  Same filter, same deferred FIFO records per query, same
 // warp-cooperative exact drain and the same hit records / counts as window_lowd<G3>.
+#ifdef K2Q_MINB
+#define K2Q_BOUNDS __launch_bounds__(128, K2Q_MINB)
+#else
+#define K2Q_BOUNDS __launch_bounds__(128)
+#endif
 template <int D, bool SYM>
-__global__ void __launch_bounds__(128) window_lowd_2q(PassArgs a) {
+__global__ void K2Q_BOUNDS window_lowd_2q(PassArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     constexpr int FW = D + 1, NW = 4, GS = 2;
     __shared__ uint32_t s_drec[NW * 256];
     __shared__ uint8_t s_dres[NW * 256];
     __shared__ float s_q[NW * 64 * D];   // per warp: owner o = 2 * lane + s
+    // per-query FIFO of deferred records (step indices), 4 slots: slot r of query (s, tid) at
+    // s_fifo[(r * 2 + s) * 128 + tid]; a push is one predicated 16-bit store + pointer bump
+    __shared__ uint16_t s_fifo[4 * 2 * 128];
+    constexpr int FSTR = 2 * 128;   // slot stride (elements)
     const int tid = threadIdx.x, lane = tid & 31, wq = tid >> 5;
     const float *Xs = static_cast<const float *>(a.Xs);
     const float *Qs = static_cast<const float *>(a.Qs);
@@ -849,8 +858,15 @@ __global__ void __launch_bounds__(128) window_lowd_2q(PassArgs a) {
         bool active[2];
         uint64_t nqc[2][D];
         float thr[2];
-        uint64_t pend[2] = {0, 0};
-        int npend[2] = {0, 0};
+        // 32-bit shared addresses (bytes): query s pushes at fp[s], full at flim + 256 * s
+        const uint16_t *const fbase = s_fifo + tid;
+        const uint32_t fb = (uint32_t)__cvta_generic_to_shared(s_fifo + tid);
+        uint32_t fp[2] = {fb, fb + 256u};
+        const uint32_t flim = fb + 4u * 2u * FSTR;
+        auto push = [&](int s, uint32_t v) {
+            asm volatile("st.shared.u16 [%0], %1;" ::"r"(fp[s]), "h"((uint16_t)v) : "memory");
+            fp[s] += 2u * FSTR;
+        };
         int32_t cnt[2] = {0, 0}, rec[2] = {0, 0};
         bool lost[2] = {false, false};
 #pragma unroll
@@ -869,6 +885,10 @@ __global__ void __launch_bounds__(128) window_lowd_2q(PassArgs a) {
                 nqc[s][k] = f2pack(-qc, -qc);
             }
             thr[s] = __double2float_ru(a.r2h - 0.5 * qb * a.c1h);
+            // pin thr to a register: ptxas otherwise rematerialises the fp64 sequence above
+            // inside the step loop (12 fp64 instructions per step in SASS); a shuffle from the
+            // own lane is not rematerialisable
+            thr[s] = __shfl_sync(0xffffffffu, thr[s], lane);
         }
         __syncwarp();
         mbar_wait(&bar[sidx], phase[sidx]);
@@ -876,6 +896,7 @@ __global__ void __launch_bounds__(128) window_lowd_2q(PassArgs a) {
         const int ngroups = (int)((c1 - c0) >> 2);
         const float4 *g4 = reinterpret_cast<const float4 *>(Xs) + (c0 >> 2) * D;   // exact rows (global)
         // hit mask of group gg for owner s -> slot record (symmetric filter, overflow list)
+        uint16_t *const slot0 = a.slots + (size_t)item * cap * a.B + tid;
         auto emit = [&](int s, int gg, uint32_t m) {
             if constexpr (SYM) {
                 const int64_t jb = c0 + 4 * gg;
@@ -891,7 +912,7 @@ __global__ void __launch_bounds__(128) window_lowd_2q(PassArgs a) {
             }
             const uint32_t v = ((uint32_t)gg << 4) | m;
             if (rec[s] < cap) {
-                a.slots[((size_t)item * cap + rec[s]) * a.B + tid + 128 * s] = (uint16_t)v;
+                slot0[(size_t)rec[s] * a.B + 128 * s] = (uint16_t)v;
             } else {
                 const int32_t k = atomicAdd(a.ovf_rec_count, 1);
                 if (k < a.ovf_rec_cap) a.ovf_rec[k] = OvfRec{(int32_t)e[s], cnt[s], v};
@@ -904,6 +925,7 @@ __global__ void __launch_bounds__(128) window_lowd_2q(PassArgs a) {
         // in the direct form from the global rows, then every owner emits its results in
         // record order
         auto drain = [&]() {
+            const int npend[2] = {(int)((fp[0] - fb) / (2u * FSTR)), (int)((fp[1] - fb - 256u) / (2u * FSTR))};
             const int mine = npend[0] + npend[1];
             int incl = mine;
 #pragma unroll
@@ -919,8 +941,7 @@ __global__ void __launch_bounds__(128) window_lowd_2q(PassArgs a) {
 #pragma unroll
             for (int s = 0; s < 2; ++s)
                 for (int r = 0; r < npend[s]; ++r)
-                    drec[pos++] = ((uint32_t)(2 * lane + s) << 16) |
-                                  ((uint32_t)(pend[s] >> (16 * (npend[s] - 1 - r))) & 0xffffu);
+                    drec[pos++] = ((uint32_t)(2 * lane + s) << 16) | fbase[128 * s + FSTR * r];
             __syncwarp();
             for (int t = lane; t < total; t += 32) {
                 const uint32_t ev = drec[t];
@@ -961,13 +982,12 @@ __global__ void __launch_bounds__(128) window_lowd_2q(PassArgs a) {
                 for (int r = 0; r < npend[s]; ++r, ++pos) {
                     const uint32_t res = dres[pos];
                     if (res) {
-                        const int g0 = GS * (int)((uint32_t)(pend[s] >> (16 * (npend[s] - 1 - r))) & 0xffffu);
+                        const int g0 = GS * (int)(drec[pos] & 0xffffu);
                         if (res & 15u) emit(s, g0, res & 15u);
                         if (res >> 4) emit(s, g0 + 1, res >> 4);
                     }
                 }
-                pend[s] = 0;
-                npend[s] = 0;
+                fp[s] = fb + 256u * s;
             }
             __syncwarp();
         };
@@ -994,12 +1014,9 @@ __global__ void __launch_bounds__(128) window_lowd_2q(PassArgs a) {
                 const float2 ea = f2unpack(la), eb = f2unpack(ha), ec = f2unpack(lb), ed = f2unpack(hb);
                 const float m1 = fminf(fminf(ea.x, ea.y), eb.x), m2 = fminf(fminf(eb.y, ec.x), ec.y);
                 const float m3 = fminf(fminf(ed.x, ed.y), m1);
-                if (fminf(m2, m3) <= thr[s]) {
-                    pend[s] = (pend[s] << 16) | (uint32_t)(g >> 1);
-                    ++npend[s];
-                }
+                if (fminf(m2, m3) <= thr[s]) push(s, (uint32_t)g >> 1);
             }
-            if (__any_sync(0xffffffffu, (npend[0] >= 4) | (npend[1] >= 4))) drain();
+            if (__any_sync(0xffffffffu, (fp[0] >= flim) | (fp[1] >= flim + 256u))) drain();
         }
         if (g < ngroups) {   // tail group (odd count): direct form from the global rows, one record
             float4 xa[D];
@@ -1016,13 +1033,10 @@ __global__ void __launch_bounds__(128) window_lowd_2q(PassArgs a) {
                 const float2 pa = f2unpack(la), qa = f2unpack(ha);
                 flag[s] = fminf(fminf(pa.x, pa.y), fminf(qa.x, qa.y)) <= T_out;
             }
-            if (__any_sync(0xffffffffu, (flag[0] && npend[0] == 4) | (flag[1] && npend[1] == 4))) drain();
+            if (__any_sync(0xffffffffu, (flag[0] && fp[0] >= flim) | (flag[1] && fp[1] >= flim + 256u))) drain();
 #pragma unroll
             for (int s = 0; s < 2; ++s)
-                if (flag[s]) {
-                    pend[s] = (pend[s] << 16) | (uint32_t)(g / GS);
-                    ++npend[s];
-                }
+                if (flag[s]) push(s, (uint32_t)(g / GS));
         }
         drain();
         bool anylost = false;

@@ -452,7 +452,7 @@ def test_dbscan_c5_full_size_sampled(snn):
                                            (8, False, {"cap": 2, "ovf_records": 40}), (1, True, {}),
                                            (3, True, {"chunk": 1024}), (4, True, {"symmetric": -1})])
 def test_scan2q_identical(snn, d, self_q, opts):
-    """K8 scan with two queries per thread (option scan2q) vs one: bit-identical CSR, equal
+    """K8 scan with two queries per thread (option scan2q; default for d = 2, 3) vs one: bit-identical CSR, equal
     to the oracle; symmetric / two-sided self-queries, separate queries, slot overflow and
     the overflow-list limit (fix pass)."""
     import paper_2212_07679_b200 as p
@@ -464,15 +464,18 @@ def test_scan2q_identical(snn, d, self_q, opts):
     try:
         for k, v in opts.items():
             p.snn_set_option(k, v)
-        for v in (0, 1):
+        for v in (-1, 1):
             p.snn_set_option("scan2q", v)
             outs.append(run(snn, X, Q, R))
+        p.snn_set_option("chunk2q", 128)   # many items per block, ragged last chunk
+        outs.append(run(snn, X, Q, R))
     finally:
-        for k in list(opts) + ["scan2q"]:
+        for k in list(opts) + ["scan2q", "chunk2q"]:
             p.snn_set_option(k, 0)
     compare(outs[1], oracle.radius_query(X, X if self_q else Q, R))
     for f in ("offsets", "indices", "distances"):
         np.testing.assert_array_equal(np.asarray(getattr(outs[1], f)), np.asarray(getattr(outs[0], f)))
+        np.testing.assert_array_equal(np.asarray(getattr(outs[2], f)), np.asarray(getattr(outs[0], f)))
 
 
 def test_tc_and_generic_paths_agree_exactly(snn):
