@@ -50,6 +50,29 @@ def test_sass_uses_bulk_async_copy(libpath):
     assert "UBLKCP" in sass     # cp.async.bulk (TMA engine) staging of candidate rows
 
 
+def test_k8_two_query_step_loop_has_no_fp64(libpath):
+    """The K8 two-queries-per-thread scan (window_lowd_2q, default for d = 2, 3): ptxas once
+    rematerialised the fp64 filter threshold inside the step loop (12 fp64 instructions per
+    step, DESIGN.md section 6 'the binding resource').  The loop -- from its first LDS.128
+    to the warp vote that closes a step -- must hold packed FP32 FMAs and no fp64."""
+    sass = subprocess.check_output(["/usr/local/cuda/bin/cuobjdump", "-sass", libpath]).decode()
+    fns = re.split(r"\n\s*Function : ", sass)
+    seen = 0
+    for fn in fns:
+        name = fn.split("\n", 1)[0]
+        m = re.search(r"window_lowd_2qILi([23])ELb[01]E", name)
+        if not m:
+            continue
+        ops = [re.sub(r"^@!?U?P\d+\s+", "", x) for x in re.findall(r"/\*[0-9a-f]{4,}\*/\s+(.*?);", fn)]
+        first = next(i for i, o in enumerate(ops) if o.startswith("LDS.128"))
+        vote = next(i for i in range(first, len(ops)) if ops[i].startswith("VOTE.ANY"))
+        loop = ops[first:vote]
+        assert sum(o.startswith("FFMA2") for o in loop) == 8 * int(m.group(1)), name
+        assert not [o for o in loop if re.match(r"D(FMA|MUL|ADD)|F2F", o)], name
+        seen += 1
+    assert seen >= 4
+
+
 def test_binding_names_match_header():
     import paper_2212_07679_b200 as p
     for f in header_functions():
