@@ -813,7 +813,8 @@ template <int D, bool SYM>
 __global__ void K2Q_BOUNDS window_lowd_2q(PassArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     constexpr int FW = D + 1, NW = 4, GS = 2;
-    __shared__ uint32_t s_drec[NW * 256];
+    __shared__ uint16_t s_drec[NW * 256];   // (owner << 10) | step: chunk <= 8192 candidates = 1024 steps
+    __shared__ uint32_t s_own[NW * 64 * 2];  // per owner: (first record | records so far << 16), hits so far (bit 31: lost)
     __shared__ uint8_t s_dres[NW * 256];
     __shared__ float s_q[NW * 64 * D];   // per warp: owner o = 2 * lane + s
     // per-query FIFO of deferred records (step indices), 4 slots: slot r of query (s, tid) at
@@ -895,35 +896,14 @@ __global__ void K2Q_BOUNDS window_lowd_2q(PassArgs a) {
         phase[sidx] ^= 1u;
         const int ngroups = (int)((c1 - c0) >> 2);
         const float4 *g4 = reinterpret_cast<const float4 *>(Xs) + (c0 >> 2) * D;   // exact rows (global)
-        // hit mask of group gg for owner s -> slot record (symmetric filter, overflow list)
-        uint16_t *const slot0 = a.slots + (size_t)item * cap * a.B + tid;
-        auto emit = [&](int s, int gg, uint32_t m) {
-            if constexpr (SYM) {
-                const int64_t jb = c0 + 4 * gg;
-                if (jb + 3 <= sp[s]) return;
-                if (jb <= sp[s]) m &= ~((2u << (sp[s] - jb)) - 1u);
-                uint32_t mm = m;
-                while (mm) {
-                    const int i = __ffs(mm) - 1;
-                    mm &= mm - 1;
-                    if (jb + i < a.own_hi) atomicAdd(&a.lcnt[jb + i], 1);
-                }
-                if (!m) return;
-            }
-            const uint32_t v = ((uint32_t)gg << 4) | m;
-            if (rec[s] < cap) {
-                slot0[(size_t)rec[s] * a.B + 128 * s] = (uint16_t)v;
-            } else {
-                const int32_t k = atomicAdd(a.ovf_rec_count, 1);
-                if (k < a.ovf_rec_cap) a.ovf_rec[k] = OvfRec{(int32_t)e[s], cnt[s], v};
-                else lost[s] = true;
-            }
-            ++rec[s];
-            cnt[s] += __popc(m);
-        };
-        // warp-cooperative drain: records listed in shared memory, classified one per lane
-        // in the direct form from the global rows, then every owner emits its results in
-        // record order
+        // Warp-cooperative drain, lane-parallel throughout: (1) every owner lists its pending
+        // records and its entry's running counts in shared memory; (2) one record per lane is
+        // classified exactly in the direct form from the global rows (symmetric self-query:
+        // only j > i kept, mirrored hits counted); (3) the same lane writes the record's slot
+        // entries -- its slot index is the owner's count plus the entries of the owner's
+        // earlier records in this drain (at most 3, read back from the result list), so slot
+        // order stays record order; (4) owners add up their records' entries and hits.
+        uint16_t *const slot_item = a.slots + (size_t)item * cap * a.B;
         auto drain = [&]() {
             const int npend[2] = {(int)((fp[0] - fb) / (2u * FSTR)), (int)((fp[1] - fb - 256u) / (2u * FSTR))};
             const int mine = npend[0] + npend[1];
@@ -935,18 +915,22 @@ __global__ void K2Q_BOUNDS window_lowd_2q(PassArgs a) {
             }
             const int excl = incl - mine;
             const int total = __shfl_sync(0xffffffffu, incl, 31);
-            uint32_t *drec = s_drec + wq * 256;
+            uint16_t *drec = s_drec + wq * 256;
             uint8_t *dres = s_dres + wq * 256;
+            uint32_t *own = s_own + wq * 128;
             int pos = excl;
 #pragma unroll
-            for (int s = 0; s < 2; ++s)
+            for (int s = 0; s < 2; ++s) {
+                own[2 * (2 * lane + s)] = (uint32_t)pos | ((uint32_t)rec[s] << 16);
+                own[2 * (2 * lane + s) + 1] = (uint32_t)cnt[s];
                 for (int r = 0; r < npend[s]; ++r)
-                    drec[pos++] = ((uint32_t)(2 * lane + s) << 16) | fbase[128 * s + FSTR * r];
+                    drec[pos++] = (uint16_t)(((uint32_t)(2 * lane + s) << 10) | fbase[128 * s + FSTR * r]);
+            }
             __syncwarp();
             for (int t = lane; t < total; t += 32) {
                 const uint32_t ev = drec[t];
-                const int o = (int)(ev >> 16);
-                const int g0 = GS * (int)(ev & 0xffffu);
+                const int o = (int)(ev >> 10);
+                const int g0 = GS * (int)(ev & 0x3ffu);
                 float qo[D];
                 uint64_t nqo[D];
 #pragma unroll
@@ -969,6 +953,18 @@ __global__ void K2Q_BOUNDS window_lowd_2q(PassArgs a) {
                         if (oa) {
                             uint32_t ia = mask4(pa.x, pa.y, qa.x, qa.y, T_in);
                             if (ia ^ oa) ia |= resolve4<D>(oa & ~ia, xa, qo, R2);
+                            if constexpr (SYM) {   // keep j > sp of the owner, count the mirrored hits
+                                const int64_t spo = b * a.B + 32 * wq + (o >> 1) + 128 * (o & 1);
+                                const int64_t jb = c0 + 4 * gg;
+                                if (jb + 3 <= spo) ia = 0;
+                                else if (jb <= spo) ia &= ~((2u << (spo - jb)) - 1u);
+                                uint32_t mm = ia;
+                                while (mm) {
+                                    const int i = __ffs(mm) - 1;
+                                    mm &= mm - 1;
+                                    if (jb + i < a.own_hi) atomicAdd(&a.lcnt[jb + i], 1);   // rows of later parts: theirs
+                                }
+                            }
                             res |= ia << (4 * h);
                         }
                     }
@@ -976,17 +972,49 @@ __global__ void K2Q_BOUNDS window_lowd_2q(PassArgs a) {
                 dres[t] = (uint8_t)res;
             }
             __syncwarp();
+            for (int t = lane; t < total; t += 32) {
+                uint32_t res = dres[t];
+                if (res) {
+                    const uint32_t ev = drec[t];
+                    const int o = (int)(ev >> 10);
+                    const int g0 = GS * (int)(ev & 0x3ffu);
+                    const uint32_t w0 = own[2 * o];
+                    int idx = (int)(w0 >> 16);                          // entries before this record
+                    int hits = (int)(own[2 * o + 1] & 0x7fffffffu);     // hits before this record
+                    for (int u = (int)(w0 & 0xffffu); u < t; ++u) {
+                        const uint32_t x = dres[u];
+                        idx += ((x & 15u) != 0) + ((x >> 4) != 0);
+                        hits += __popc(x);
+                    }
+                    const int qi = 32 * wq + (o >> 1) + 128 * (o & 1);
+#pragma unroll
+                    for (int h = 0; h < GS; ++h) {
+                        const uint32_t m = (res >> (4 * h)) & 15u;
+                        if (m) {
+                            const uint32_t v = ((uint32_t)(g0 + h) << 4) | m;
+                            if (idx < cap) {
+                                slot_item[(uint32_t)idx * (uint32_t)a.B + qi] = (uint16_t)v;
+                            } else {
+                                const int32_t kk = atomicAdd(a.ovf_rec_count, 1);
+                                if (kk < a.ovf_rec_cap) a.ovf_rec[kk] = OvfRec{(int32_t)(item * a.B + qi), hits, v};
+                                else atomicOr(&own[2 * o + 1], 0x80000000u);
+                            }
+                            ++idx;
+                            hits += __popc(m);
+                        }
+                    }
+                }
+            }
+            __syncwarp();
             pos = excl;
 #pragma unroll
             for (int s = 0; s < 2; ++s) {
                 for (int r = 0; r < npend[s]; ++r, ++pos) {
-                    const uint32_t res = dres[pos];
-                    if (res) {
-                        const int g0 = GS * (int)(drec[pos] & 0xffffu);
-                        if (res & 15u) emit(s, g0, res & 15u);
-                        if (res >> 4) emit(s, g0 + 1, res >> 4);
-                    }
+                    const uint32_t x = dres[pos];
+                    rec[s] += ((x & 15u) != 0) + ((x >> 4) != 0);
+                    cnt[s] += __popc(x);
                 }
+                if (own[2 * (2 * lane + s) + 1] >> 31) lost[s] = true;
                 fp[s] = fb + 256u * s;
             }
             __syncwarp();
