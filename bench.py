@@ -285,8 +285,8 @@ def roofline_block(args, w, prof, times, dev, info):
         peak = fp32_alu_peak_tflops(sm_max, n_sm)
         import paper_2212_07679_b200 as snn
         snap = snn.snn_get_option("union_snap") > 0 and w.X.dtype == np.float32 and w.d <= 8
-        o2q = snn.snn_get_option("scan2q")   # 0 = auto: on for d = 2, 3 (api.cu query_impl)
-        twoq = w.X.dtype == np.float32 and w.d <= 8 and (o2q > 0 or (o2q == 0 and w.d in (2, 3)))
+        o2q = snn.snn_get_option("scan2q")   # 0 = auto: on for d >= 2 (api.cu query_impl)
+        twoq = w.X.dtype == np.float32 and w.d <= 8 and (o2q > 0 or (o2q == 0 and w.d >= 2))
         kernel, bound = ((f"union_snap_kernel<{w.d}> (K12 DBSCAN union pass, staged root snapshot)" if snap
                           else f"window_lowd<float,{w.d},union> (K12 DBSCAN union pass)") if fam == "dbscan_union"
                          else (f"window_lowd_2q<{w.d}> (K8 scan pass, two queries per thread)" if twoq

@@ -289,7 +289,7 @@ snn_status snn_profile_read(const char *family, double *ms, uint64_t *launches, 
  *                    direct loop
  *   "symmetric"      -1 = evaluate every pair twice in low-d self-queries (default: once)
  *   "scan2q"         fp32 low-d scan with two queries per thread (128-thread CTAs, each staged
- *                    filter row feeds two queries): 0 = auto (default: on for d = 2, 3),
+ *                    filter row feeds two queries): 0 = auto (default: on for 2 <= d <= 8),
  *                    1 = on for every d <= 8, -1 = off
  *   "chunk2q"        candidates per work item of that scan (default 640, multiple of 64)
  *   "stage_rows"     1 = the compaction assembles rows in a key-order staging buffer, then

@@ -31,7 +31,7 @@ struct Options {
     int cap = 64;
     int32_t ovf_rec_cap = 1 << 20;
     int variant = 1;
-    int scan2q = 0;      // fp32 low-d scan with the expanded filter, two queries per thread: 0 = auto (d = 2, 3), 1 = on, -1 = off
+    int scan2q = 0;      // fp32 low-d scan with the expanded filter, two queries per thread: 0 = auto (d >= 2), 1 = on, -1 = off
     int chunk2q = 640;   // candidates per work item of that scan (128-thread CTAs: smaller chunks keep 7 CTAs per SM)
     int tc = 1;          // use the tcgen05 path for d >= tc_min_d
     int tc_min_d = 32;
@@ -1170,9 +1170,9 @@ static snn_status query_impl(snn_index idx, const void *Q, int64_t m, int32_t d,
     const bool generic = ld != 0;
     const int B = generic ? 64 : g_opt.query_block;
     // K8 with two queries per thread (fp32 radius queries with the expanded-form filter;
-    // measured faster on d = 2, 3 -- DESIGN.md section 6): smaller work items
+    // measured faster for every d = 2..8, scripts/sweep_2q_d.py -- DESIGN.md section 6): smaller work items
     const bool scan2q = !generic && !f64 && idx->Xf && g_opt.simt_filter >= 0 && B == 256 &&
-                        (g_opt.scan2q > 0 || (g_opt.scan2q == 0 && (D == 2 || D == 3)));
+                        (g_opt.scan2q > 0 || (g_opt.scan2q == 0 && D >= 2));
     const int chunk = generic ? 1024 : scan2q ? g_opt.chunk2q : g_opt.chunk;
     const int64_t nblocks = ceil_div(m, B);
     int64_t *blk_lo = nullptr, *blk_hi = nullptr, *nitems = nullptr, *item_start = nullptr;

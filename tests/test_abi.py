@@ -51,7 +51,7 @@ def test_sass_uses_bulk_async_copy(libpath):
 
 
 def test_k8_two_query_step_loop_has_no_fp64(libpath):
-    """The K8 two-queries-per-thread scan (window_lowd_2q, default for d = 2, 3): ptxas once
+    """The K8 two-queries-per-thread scan (window_lowd_2q, default for 2 <= d <= 8): ptxas once
     rematerialised the fp64 filter threshold inside the step loop (12 fp64 instructions per
     step, DESIGN.md section 6 'the binding resource').  The loop -- from its first LDS.128
     to the warp vote that closes a step -- must hold packed FP32 FMAs and no fp64."""

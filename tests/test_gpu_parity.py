@@ -452,7 +452,7 @@ def test_dbscan_c5_full_size_sampled(snn):
                                            (8, False, {"cap": 2, "ovf_records": 40}), (1, True, {}),
                                            (3, True, {"chunk": 1024}), (4, True, {"symmetric": -1})])
 def test_scan2q_identical(snn, d, self_q, opts):
-    """K8 scan with two queries per thread (option scan2q; default for d = 2, 3) vs one: bit-identical CSR, equal
+    """K8 scan with two queries per thread (option scan2q; default for d >= 2) vs one: bit-identical CSR, equal
     to the oracle; symmetric / two-sided self-queries, separate queries, slot overflow and
     the overflow-list limit (fix pass)."""
     import paper_2212_07679_b200 as p
